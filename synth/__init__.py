@@ -1,0 +1,236 @@
+"""synth -- seeded synthetic inputs shared by the oracle tests and the CUDA path.
+
+This module holds NO arithmetic of the Bingo method: it only produces graphs,
+biases, update streams and walker start lists ("Input
+recipe").  Both ``oracle`` (through tests/bench) and ``paper_2504_10233_b200``
+consume its outputs; neither side's code lives here.
+
+Recipe (PAPER.md S6.1 P:656-665):
+* R-MAT (a, b, c, d) = (0.57, 0.19, 0.19, 0.05) on 2^scale ids; self loops and
+  duplicate edges dropped (a simple base graph); random vertex relabelling;
+  symmetrised (each undirected edge -> two arcs); optionally compacted to the
+  non-isolated vertices so that V matches the dataset shape.
+* Biases "based on the degree of vertices": w(u, v) = max(1, deg(v))
+  (reading R-12), optionally clamped (config 1: 1..255); uniform and
+  log-uniform variants exercise every group kind.
+* Update stream: hold out R * BS undirected edges as B, the rest is the
+  initial graph A; each event flips a fair coin (Mixed): delete a
+  uniform live edge of A, or insert a uniform unused edge of B into A.  Each
+  undirected event becomes two arc records {op, src, dst, bias}.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+RMAT_ABCD = (0.57, 0.19, 0.19, 0.05)
+INSERT, DELETE = 0, 1
+
+# name -> recipe.  V / arcs are the targets of BASELINE.json configs; "scale" and
+# "edges" are the generator parameters that land near them.
+CONFIGS = {
+    "c1": dict(desc="tiny power-law 1K V / 16K arcs, biases 1-255", scale=10, edges=11850,
+               compact=False, bias="degree", clamp=(1, 255), batch=500, app="deepwalk"),
+    "c2": dict(desc="LiveJournal-shaped R-MAT (4.8M V, 69M arcs), DeepWalk, 100K-edge batches",
+               scale=24, edges=35_000_000, compact=True, bias="degree", clamp=None, batch=50_000,
+               app="deepwalk"),
+    "c3": dict(desc="Orkut-shaped R-MAT (3.1M V, 234M arcs), node2vec p=2 q=0.5, 1M-edge batches",
+               scale=22, edges=120_000_000, compact=True, bias="degree", clamp=None, batch=1_000_000,
+               app="node2vec"),
+    "c4": dict(desc="Twitter-shaped R-MAT (41.7M V, 1.47B arcs), PPR", scale=26, edges=760_000_000,
+               compact=True, bias="degree", clamp=None, batch=50_000, app="ppr"),
+}
+
+
+def rmat_edges(scale: int, n_edges: int, seed: int, abcd=RMAT_ABCD, chunk: int = 1 << 24):
+    """Raw directed R-MAT endpoint pairs (int64 ids < 2^scale), torch CPU RNG."""
+    import torch
+    g = torch.Generator().manual_seed(seed)
+    a, b, c, _ = abcd
+    src = torch.empty(n_edges, dtype=torch.int64)
+    dst = torch.empty(n_edges, dtype=torch.int64)
+    for lo in range(0, n_edges, chunk):
+        hi = min(n_edges, lo + chunk)
+        m = hi - lo
+        s = torch.zeros(m, dtype=torch.int64)
+        t = torch.zeros(m, dtype=torch.int64)
+        for lvl in range(scale):
+            r = torch.rand(m, generator=g)
+            bit = 1 << (scale - 1 - lvl)
+            # quadrant: [0,a) -> (0,0); [a,a+b) -> (0,1); [a+b,a+b+c) -> (1,0); else (1,1)
+            down = r >= (a + b)
+            right = ((r >= a) & (r < a + b)) | (r >= a + b + c)
+            s += down.to(torch.int64) * bit
+            t += right.to(torch.int64) * bit
+        src[lo:hi] = s
+        dst[lo:hi] = t
+    return src, dst
+
+
+def simple_undirected(scale: int, n_edges: int, seed: int, compact: bool):
+    """Undirected simple edge list (lo < hi pairs, unique) with a random relabelling."""
+    import torch
+    s, t = rmat_edges(scale, n_edges, seed)
+    keep = s != t
+    s, t = s[keep], t[keep]
+    key = torch.unique((torch.minimum(s, t) << 32) | torch.maximum(s, t))
+    lo = key >> 32
+    hi = key & 0xFFFFFFFF
+    n_ids = 1 << scale
+    if compact:
+        used = torch.zeros(n_ids, dtype=torch.bool)
+        used[lo] = True
+        used[hi] = True
+        newid = torch.cumsum(used.to(torch.int64), 0) - 1
+        V = int(used.sum())
+        lo, hi = newid[lo], newid[hi]
+    else:
+        V = n_ids
+    g = torch.Generator().manual_seed(seed + 1000003)
+    perm = torch.randperm(V, generator=g)
+    lo, hi = perm[lo], perm[hi]
+    a = torch.minimum(lo, hi)
+    b = torch.maximum(lo, hi)
+    return V, a.numpy().astype(np.uint32), b.numpy().astype(np.uint32)
+
+
+def csr_from_arcs(V: int, src: np.ndarray, dst: np.ndarray, extra=None):
+    """CSR with arcs ordered by (src, dst); returns row_offsets u64, dst u32 (+ extra permuted)."""
+    import torch
+    key = (torch.from_numpy(src.astype(np.int64)) << 32) | torch.from_numpy(dst.astype(np.int64))
+    order = torch.sort(key, stable=True).indices.numpy()
+    s = src[order]
+    d = dst[order].astype(np.uint32)
+    counts = np.bincount(s, minlength=V).astype(np.uint64)
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    np.cumsum(counts, out=ro[1:])
+    if extra is not None:
+        return ro, d, extra[order]
+    return ro, d
+
+
+def degree_bias_of(deg: np.ndarray, dst: np.ndarray, clamp=None) -> np.ndarray:
+    """w(u, v) = max(1, deg(v)) (reading R-12), optionally clamped."""
+    w = np.maximum(deg[dst].astype(np.int64), 1)
+    if clamp is not None:
+        w = np.clip(w, clamp[0], clamp[1])
+    return w.astype(np.uint32)
+
+
+def make_workload(name: str, rounds: int = 1, **over) -> "Workload":
+    cfg = dict(CONFIGS[name])
+    cfg.update(over)
+    return Workload(cfg["scale"], cfg["edges"], compact=cfg["compact"], bias=cfg["bias"],
+                    clamp=cfg["clamp"], batch=cfg["batch"], rounds=rounds)
+
+
+class Workload:
+    """A seeded graph + update stream following the recipe above."""
+
+    def __init__(self, scale, edges, seed=1, compact=True, bias="degree", clamp=None, batch=1000,
+                 rounds=1, update_seed=2, undirected=True):
+        V, a, b = simple_undirected(scale, edges, seed, compact)
+        self.V = V
+        E = len(a)
+        # full-graph degrees fix every bias, including those of later inserts
+        deg_full = np.bincount(a, minlength=V) + np.bincount(b, minlength=V)
+        rng = np.random.default_rng(update_seed)
+        n_hold = min(E // 2, rounds * batch)
+        perm = rng.permutation(E)
+        held = perm[:n_hold]
+        live = perm[n_hold:]
+        self.batch = batch
+        self.rounds = rounds
+        self.deg_full = deg_full
+        self.bias_kind = bias
+        self.clamp = clamp
+        self._bias_seed = seed + 7
+        # initial graph A
+        src = np.concatenate([a[live], b[live]])
+        dst = np.concatenate([b[live], a[live]])
+        w = self._bias(src, dst)
+        self.row_offsets, self.dst, self.bias = csr_from_arcs(V, src, dst, extra=w)
+        self.num_arcs = int(self.row_offsets[-1])
+        # update stream: coin flip, delete uniform live edge of A,
+        # insert uniform unused edge of B into A
+        self.batches = []
+        live_list = live.copy()
+        n_live = len(live_list)
+        pool = held.copy()
+        rng.shuffle(pool)
+        pool_pos = 0
+        for _ in range(rounds):
+            ops = rng.integers(0, 2, size=batch)
+            uni = rng.random(batch)
+            src_r = np.zeros(batch, dtype=np.int64)
+            dst_r = np.zeros(batch, dtype=np.int64)
+            for i in range(batch):
+                if (ops[i] == 1 and n_live > 0) or pool_pos >= len(pool):
+                    j = int(uni[i] * n_live)
+                    e = live_list[j]
+                    live_list[j] = live_list[n_live - 1]
+                    n_live -= 1
+                else:
+                    ops[i] = 0
+                    e = pool[pool_pos]
+                    pool_pos += 1
+                    if n_live == len(live_list):
+                        live_list = np.concatenate([live_list, np.zeros(max(1024, batch), live_list.dtype)])
+                    live_list[n_live] = e
+                    n_live += 1
+                src_r[i] = a[e]
+                dst_r[i] = b[e]
+            recs = np.zeros((2 * batch, 4), dtype=np.uint32)
+            recs[0::2, 0] = ops
+            recs[1::2, 0] = ops
+            recs[0::2, 1] = src_r
+            recs[0::2, 2] = dst_r
+            recs[1::2, 1] = dst_r
+            recs[1::2, 2] = src_r
+            ins = ops == INSERT
+            recs[0::2, 3] = np.where(ins, self._bias(src_r, dst_r), 0)
+            recs[1::2, 3] = np.where(ins, self._bias(dst_r, src_r), 0)
+            self.batches.append(recs)
+
+    def _bias(self, src, dst):
+        if self.bias_kind == "degree":
+            return degree_bias_of(self.deg_full, dst, self.clamp)
+        lo, hi = self.clamp if self.clamp else (1, 255)
+        # edge-keyed hash so that the same arc always gets the same bias
+        h = (src.astype(np.uint64) * np.uint64(0x9E3779B97F4A7C15) ^
+             (dst.astype(np.uint64) + np.uint64(self._bias_seed)) * np.uint64(0xC2B2AE3D27D4EB4F))
+        h ^= h >> np.uint64(29)
+        h *= np.uint64(0xBF58476D1CE4E5B9)
+        h ^= h >> np.uint64(32)
+        x = (h >> np.uint64(11)).astype(np.float64) / float(1 << 53)
+        if self.bias_kind == "uniform":
+            return (lo + np.floor(x * (hi - lo + 1))).astype(np.uint32)
+        if self.bias_kind == "loguniform":
+            return np.floor(np.exp(np.log(lo) + x * (np.log(hi + 1) - np.log(lo)))).clip(lo, hi).astype(np.uint32)
+        raise ValueError(self.bias_kind)
+
+
+def random_small_graph(rng: np.random.Generator, V: int, max_deg: int, max_bias: int, directed=True):
+    """Tiny random multigraph CSR (duplicates allowed) for property tests."""
+    deg = rng.integers(0, max_deg + 1, size=V)
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, V, size=A).astype(np.uint32)
+    bias = rng.integers(1, max_bias + 1, size=A).astype(np.uint32)
+    return ro, dst, bias
+
+
+def random_batch(rng: np.random.Generator, V: int, n: int, max_bias: int, existing=None, p_delete=0.5):
+    """Random mixed arc batch; deletes target existing arcs (from `existing`
+    = list of (src, dst)) with probability 0.8, else random (possibly missing)."""
+    recs = np.zeros((n, 4), dtype=np.uint32)
+    for i in range(n):
+        if rng.random() < p_delete:
+            if existing and rng.random() < 0.8:
+                s, d = existing[int(rng.integers(0, len(existing)))]
+            else:
+                s, d = int(rng.integers(0, V)), int(rng.integers(0, V))
+            recs[i] = (DELETE, s, d, 0)
+        else:
+            recs[i] = (INSERT, int(rng.integers(0, V)), int(rng.integers(0, V)), int(rng.integers(1, max_bias + 1)))
+    return recs
