@@ -1,0 +1,226 @@
+/*
+ * bingo.h -- C-ABI of the B200-native Bingo hot path (libbingo.so).
+ *
+ * Bingo (arXiv 2504.10233) samples the next hop of a random walk from a
+ * per-vertex radix factorisation of integer edge biases: every bias w_i is
+ * split into its set bits (Eq.3), each set bit k puts the edge in
+ * group k whose weight is W(p_k) = c_k 2^k (Eq.4), a walker picks
+ * a group through an alias table over the group weights (Eq.5) and
+ * then an edge uniformly inside the group (Eq.6).  Groups use the
+ * dense / one-element / sparse / regular layouts of Eq.9.
+ * Batched insert/delete keeps all of it consistent between walk batches
+ * (S5.2).  "P:n" = line n of PAPER.md; "R-n" = reading n of
+ * DESIGN.md section 3 (the canonical semantics where the paper is silent).
+ *
+ * Conventions for every call:
+ *  - Pointers are DEVICE pointers unless the call's flags say HOST.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream).  Work is enqueued on it; calls that must report sizes or
+ *    statistics synchronise that stream before returning (stated per call).
+ *  - Caller-owned buffers must stay valid until the stream passes the call.
+ *  - No exception crosses the ABI; every call returns a bingo_status.
+ *  - After a CUDA error the graph is poisoned: every later call on it
+ *    returns BINGO_E_STATE (bingo_destroy still frees it).
+ *  - Concurrency: one writer or many readers per graph; the caller orders
+ *    bingo_apply_updates against bingo_walk on one stream (P:523 (ii)).
+ */
+#ifndef BINGO_H
+#define BINGO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct bingo_graph bingo_graph; /* opaque; owns all of its HBM */
+
+typedef enum {
+    BINGO_OK = 0,
+    BINGO_E_INVAL = 1,    /* bad argument / invalid batch record (nothing mutated)   */
+    BINGO_E_NOMEM = 2,    /* device memory exhausted (nothing mutated)              */
+    BINGO_E_CUDA = 3,     /* CUDA runtime error (graph poisoned)                    */
+    BINGO_E_OVERFLOW = 4, /* n * T >= 2^64 or degree >= 2^32 - 1 (nothing mutated)  */
+    BINGO_E_STATE = 5     /* graph poisoned by an earlier CUDA error                */
+} bingo_status;
+
+/* Group kinds of Eq.9 as they appear in exports (R-3). */
+enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIND_SPARSE = 3,
+       BINGO_KIND_REGULAR = 4 };
+
+/* ---------------------------------------------------------------------------
+ * bingo_build -- sampling-space construction (S4.1 "Sampling space
+ * construction"; Eq.9 kinds P:436-492; inter-group alias P:292).
+ *
+ * Input is a CSR snapshot in DEVICE memory:
+ *   row_offsets [V+1] u64, non-decreasing, row_offsets[0] = 0;
+ *   dst [A] u32 < V; bias [A] u32 >= 1.  CSR order is the canonical adjacency
+ *   order (R-2); every arc gets epoch 0.
+ * alpha_pct / beta_pct: Eq.9 thresholds (paper: 40 / 10).
+ * flags: BINGO_BUILD_BS_MODE forces the paper's all-regular baseline (
+ *   alpha = 100, beta = 0, no one-element groups).
+ * arc_slack / member_slack: fraction of extra per-vertex capacity reserved
+ *   for growth (Hornet-style dynamic arrays + memory pool);
+ *   pool_reserve: extra fraction of every pool for relocations.
+ * alloc/free/alloc_ctx: optional device allocator (e.g. PyTorch's caching
+ *   allocator); NULL -> cudaMalloc/cudaFree.
+ * Errors: EINVAL (V = 0 with A > 0, dst >= V, bias = 0, bad offsets: checked
+ *   on the device), EOVERFLOW (a vertex with n*T >= 2^64 or d >= 2^32-1),
+ *   NOMEM, CUDA.  Synchronises `stream`.  *out receives the new graph.
+ * ------------------------------------------------------------------------- */
+#define BINGO_BUILD_BS_MODE 1u
+
+typedef void *(*bingo_alloc_fn)(size_t bytes, void *ctx);
+typedef void (*bingo_free_fn)(void *ptr, void *ctx);
+
+typedef struct {
+    uint32_t num_vertices;
+    uint64_t num_arcs;
+    const uint64_t *row_offsets; /* device [V+1] */
+    const uint32_t *dst;         /* device [A]   */
+    const uint32_t *bias;        /* device [A]   */
+    uint32_t alpha_pct, beta_pct;
+    uint32_t flags;
+    double arc_slack;    /* e.g. 0.25 */
+    double member_slack; /* e.g. 0.25 */
+    double pool_reserve; /* e.g. 0.10 */
+    bingo_alloc_fn alloc;
+    bingo_free_fn free;
+    void *alloc_ctx;
+} bingo_build_desc;
+
+bingo_status bingo_build(const bingo_build_desc *desc, void *stream, bingo_graph **out);
+
+/* Frees every device buffer the graph owns.  Safe on NULL. */
+void bingo_destroy(bingo_graph *g);
+
+/* ---------------------------------------------------------------------------
+ * bingo_apply_updates -- batched edge insert/delete (S5.2; single
+ * records are the streaming case of S4.2).
+ *
+ * batch: n arc-level records {op, src, dst, bias}, op 0 = insert (bias >= 1),
+ *   op 1 = delete (bias ignored).  An undirected edge update is two records.
+ *   DEVICE pointer, or HOST pointer with BINGO_UPD_HOST_BATCH (the library
+ *   copies it H2D on `stream`).
+ * Semantics (R-7 .. R-10): epoch e = number of successful calls so far + 1.
+ *   Per touched vertex: all inserts in batch order (append; groups that are
+ *   REGULAR/SPARSE before the batch append the new index), then all deletes
+ *   (each removes the live instance of (src,dst) with the smallest
+ *   (epoch, position) not yet taken; two-phase delete-and-swap,
+ *   P:514-516, on groups and adjacency, renaming moved indices), then one
+ *   rebuild (Eq.9 reclassification, member materialisation on kind change,
+ *   integer Vose alias).  Untouched vertices are not modified.
+ *   A delete with no live instance is counted in missing_deletes, not an
+ *   error (R-8).
+ * Errors (nothing is mutated, epoch unchanged): EINVAL for op > 1, src or
+ *   dst >= V, or an insert with bias 0; EOVERFLOW if for a touched vertex
+ *   (T + inserted bias) * popc(mask | inserted biases) >= 2^64 or
+ *   d + inserts >= 2^32 - 1; NOMEM if the pools cannot grow.
+ * stats_or_null (HOST) receives counts and the 5x5 kind-transition matrix
+ *   [old kind][new kind] over every (touched vertex, k) with a nonempty side
+ *   (cf. Table trans).  Synchronises `stream`.
+ * ------------------------------------------------------------------------- */
+#define BINGO_UPD_HOST_BATCH 1u
+
+typedef struct {
+    uint32_t op, src, dst, bias;
+} bingo_update;
+
+typedef struct {
+    uint64_t inserted, deleted, missing_deletes, touched_vertices;
+    uint64_t kind_transitions[5][5];
+    uint64_t epoch;
+} bingo_update_stats;
+
+bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
+                                 bingo_update_stats *stats_or_null, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * bingo_walk -- the batched walker step (S3 "random walk query", P:215;
+ * Eq.5/Eq.6 two-stage sample; dense rejection P:465; applications S6.1
+ * P:535-536).
+ *
+ * desc->app: BINGO_DEEPWALK: exactly `length` steps (path of length+1
+ *   vertices, R-13);  BINGO_NODE2VEC: second-order walk, first step
+ *   first-order, later steps propose with the first-order sampler and accept
+ *   with f(prev, v) / f_max, f = 1/p, 1, 1/q by distance 0/1/2 (Eq.1,
+ *   P:160-170; KnightKing rejection);  BINGO_PPR: after every step stop
+ *   with probability stop_num/stop_den, `length` caps the steps
+ *   (0xFFFFFFFF = no cap); visit counts (start included) accumulate in the
+ *   graph (read them with bingo_visit_counts).
+ * Walker i (0 <= i < num_walkers) has global id first_walker_id + i and
+ *   starts at starts[i], or at (first_walker_id + i) mod V if starts is NULL
+ *   (one walker per vertex).  Its randomness is Philox4x32-10 keyed by
+ *   seed with counter (walker id, step, (outer << 16) + inner, tag) (R-1), so a
+ *   sharded run (first_walker_id) reproduces the unsharded one bit for bit.
+ * A walker at a vertex of out-degree 0 stops (truncation).
+ * paths_or_null: step-major u32 [(length+1) x num_walkers], entry
+ *   [t * num_walkers + i] = vertex after t steps; 0xFFFFFFFF after truncation.
+ *   Required NULL for PPR without a cap.  lengths_or_null: u32 [num_walkers]
+ *   steps actually taken.  DEVICE pointers, or HOST with
+ *   BINGO_WALK_HOST_OUTPUT (the library stages through device scratch and
+ *   copies D2H on `stream`; `starts` is then HOST too).
+ * Errors: EINVAL (bad app / p, q <= 0 / stop_den == 0 / NULL paths with
+ *   no cap).  Asynchronous unless HOST_OUTPUT (then synchronises `stream`).
+ * ------------------------------------------------------------------------- */
+enum { BINGO_DEEPWALK = 0, BINGO_NODE2VEC = 1, BINGO_PPR = 2 };
+#define BINGO_WALK_HOST_OUTPUT 1u
+#define BINGO_NO_CAP 0xFFFFFFFFu
+
+typedef struct {
+    uint32_t app;
+    uint32_t length;
+    double p, q;                 /* node2vec hyper-parameters (0.5, 2) */
+    uint32_t stop_num, stop_den; /* PPR termination probability (1/80) */
+    uint64_t seed;
+    uint32_t first_walker_id;
+    uint32_t flags;
+} bingo_walk_desc;
+
+bingo_status bingo_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts_or_null,
+                        uint32_t num_walkers, uint32_t *paths_or_null, uint32_t *lengths_or_null,
+                        void *stream);
+
+/* ---------------------------------------------------------------------------
+ * bingo_visit_counts -- PPR visit frequencies ("use the visit frequency
+ * of each vertex"): u64 [V] counts accumulated by BINGO_PPR walks since the
+ * last reset (start vertices included, R-15).  counts: DEVICE [V] (or HOST
+ * with BINGO_COUNTS_HOST; then synchronises).  reset != 0 zeroes the graph's
+ * counters after the copy (counts may be NULL to only reset).
+ * ------------------------------------------------------------------------- */
+#define BINGO_COUNTS_HOST 1u
+bingo_status bingo_visit_counts(bingo_graph *g, uint64_t *counts, int reset, uint32_t flags, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Inspection (parity and reporting; not on the hot path).
+ * bingo_export: canonical dump (R-11) into a HOST buffer: for each vertex u
+ *   ascending: u32 d; d x {u32 dst, u32 bias, u32 epoch}; u32 n; n x {u32 k,
+ *   u32 c, u32 kind, u64 thr, u32 alias, REG/SPARSE: c x u32 member index,
+ *   ONE: u32 member index}; u64 T.  Little-endian, unaligned.  *size_out
+ *   receives the byte count; nothing is written if host_buf is NULL or cap is
+ *   too small.  Synchronises `stream`.
+ * bingo_digests: per-vertex FNV-1a-64 of the same per-vertex bytes, computed
+ *   on the device into DEVICE u64 [V].
+ * bingo_info: sizes and pool usage (HOST struct).
+ * ------------------------------------------------------------------------- */
+bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t cap, size_t *size_out, void *stream);
+bingo_status bingo_digests(bingo_graph *g, uint64_t *digests, void *stream);
+
+typedef struct {
+    uint32_t num_vertices;
+    uint32_t epoch;
+    uint64_t num_arcs;
+    uint64_t arc_pool_used, arc_pool_cap;       /* arcs   */
+    uint64_t bucket_pool_used, bucket_pool_cap; /* 32 B buckets */
+    uint64_t member_pool_used, member_pool_cap; /* 8 B entries */
+    uint64_t device_bytes;
+} bingo_info;
+bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *stream);
+
+const char *bingo_status_str(bingo_status s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BINGO_H */

@@ -1,0 +1,147 @@
+// bingo_internal.cuh -- device data layout and shared device helpers of libbingo.
+//
+// HBM layout.  Everything is structure-of-arrays inside
+// a few pools addressed by OFFSETS (never raw pointers), so a pool can grow by
+// reallocation + one memcpy without fix-ups:
+//
+//  hdr   [V]        VHdr, 32 B, one DRAM sector per vertex: the walker's first
+//                   load.  T = sum of biases (Eq.4 summed), adjacency offset and
+//                   capacity, bucket offset, degree d, group count n.
+//  bkt   pool       Bucket, 32 B, one per nonempty radix group, ascending k.
+//                   Bucket b is both the canonical record of group b (k, kind,
+//                   c, member array) and alias bucket b (thr, alias) -- A-13:
+//                   the alias table is over the nonempty groups, ascending k.
+//                   It also carries a COPY of its alias partner's (k, kind, c,
+//                   ref) so a walker resolves the inter-group sample (Eq.5)
+//                   with one 32 B load whichever side of the bucket it lands.
+//  arc   pool       uint2 {dst, bias} per arc (8 B) + arc_epoch u32 (update
+//                   side only).  Dense groups sample it directly.
+//  mem   pool       uint2 {arc index, dst} member entries of REGULAR/SPARSE
+//                   groups (groups store neighbour INDICES; the dst
+//                   copy saves the walker the dependent adjacency load).
+//                   Group arrays start at 16 B units (u32 unit offsets).
+//
+// A walker step is therefore hdr -> bucket -> member (3 dependent sectors),
+// hdr -> bucket (ONE: dst cached in the bucket), or hdr -> bucket -> arc per
+// dense attempt.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bingo {
+
+enum : uint32_t { K_EMPTY = 0, K_ONE = 1, K_DENSE = 2, K_SPARSE = 3, K_REGULAR = 4 };
+
+struct __align__(32) VHdr {
+    uint64_t T;        // sum of biases = sum_k W(p_k)
+    uint64_t adj_off;  // arc pool index of adj[0]
+    uint32_t bkt_off;  // bucket pool index of bucket 0
+    uint32_t d;        // out-degree (live arcs)
+    uint8_t n;         // nonempty groups (alias buckets)
+    uint8_t ncap;      // bucket capacity at bkt_off
+    uint16_t pad;
+    uint32_t adj_cap;  // arc capacity at adj_off
+};
+static_assert(sizeof(VHdr) == 32, "VHdr must be one sector");
+
+// kk byte: bits 0..4 = k, bits 5..7 = kind
+struct __align__(32) Bucket {
+    uint64_t thr;   // alias threshold in [0, T]: coin < thr -> this group, else alias
+    uint32_t c;     // |G_k|
+    uint32_t ref;   // REG/SPARSE: member array offset (16 B units); ONE: dst of the member
+    uint32_t a_c;   // copy of the alias partner's c
+    uint32_t a_ref; // copy of the alias partner's ref
+    uint8_t kk;     // k | kind << 5
+    uint8_t a_kk;   // alias partner's kk
+    uint8_t alias;  // alias partner bucket
+    uint8_t pad;
+    uint32_t aux;   // REG/SPARSE: member capacity (entries); ONE: the member's arc index
+};
+static_assert(sizeof(Bucket) == 32, "Bucket must be one sector");
+
+__host__ __device__ inline uint32_t kk_k(uint8_t kk) { return kk & 31u; }
+__host__ __device__ inline uint32_t kk_kind(uint8_t kk) { return (uint32_t)kk >> 5; }
+__host__ __device__ inline uint8_t make_kk(uint32_t k, uint32_t kind) { return (uint8_t)(k | (kind << 5)); }
+
+// Eq.9 with the R-3 precedence (one-element first) and strict
+// inequalities (R-3 boundaries).  bs: the all-regular baseline.
+__host__ __device__ inline uint32_t classify(uint32_t c, uint32_t d, uint32_t alpha, uint32_t beta, bool bs) {
+    if (c == 0) return K_EMPTY;
+    if (bs) return K_REGULAR;
+    if (c == 1) return K_ONE;
+    if ((uint64_t)100 * c > (uint64_t)alpha * d) return K_DENSE;
+    if ((uint64_t)100 * c < (uint64_t)beta * d) return K_SPARSE;
+    return K_REGULAR;
+}
+__host__ __device__ inline bool is_list(uint32_t kind) { return kind == K_REGULAR || kind == K_SPARSE; }
+
+// ---------------------------------------------------------------- Philox4x32-10
+// Counter-based generator (R-1).  Written from the Salmon et al. round
+// definition; pinned by the published known-answer vectors in the tests.
+struct P4 { uint32_t x, y, z, w; };
+
+__device__ __forceinline__ P4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+        const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+        const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    return P4{c0, c1, c2, c3};
+}
+
+__device__ __forceinline__ uint64_t join64(uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; }
+
+// ---------------------------------------------------------------- warp helpers
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1u; }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+}  // namespace bingo
+
+// ---------------------------------------------------------------- graph object
+struct bingo_graph {
+    uint32_t V = 0;
+    uint32_t alpha = 40, beta = 10, flags = 0;
+    uint32_t epoch = 0;
+    int poisoned = 0;
+    uint64_t num_arcs = 0;
+
+    // allocator
+    void *(*alloc)(size_t, void *) = nullptr;
+    void (*free_)(void *, void *) = nullptr;
+    void *alloc_ctx = nullptr;
+    double arc_slack = 0.25, member_slack = 0.25, pool_reserve = 0.1;
+
+    bingo::VHdr *hdr = nullptr;        // [V]
+    uint2 *arc = nullptr;              // [arc_cap]
+    uint32_t *arc_epoch = nullptr;     // [arc_cap]
+    uint64_t arc_cap = 0;
+    bingo::Bucket *bkt = nullptr;      // [bkt_cap]
+    uint64_t bkt_cap = 0;
+    uint2 *mem = nullptr;              // [mem_cap] entries
+    uint64_t mem_cap = 0;
+    unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
+    unsigned long long *visit = nullptr;     // [V] PPR visit counts
+    int *dev_flag = nullptr;                 // device error flag
+
+    // update-side scratch (grown on demand)
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    void *hscratch = nullptr;                // pinned host staging
+    size_t hscratch_bytes = 0;
+    void *wscratch = nullptr;                // walk staging for HOST_OUTPUT
+    size_t wscratch_bytes = 0;
+};
+
+// allocation helpers (api.cu)
+void *bingo_dev_alloc(bingo_graph *g, size_t bytes);
+void bingo_dev_free(bingo_graph *g, void *p);

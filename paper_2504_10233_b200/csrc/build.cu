@@ -1,0 +1,292 @@
+// build.cu -- sampling-space construction on the device.
+//
+//  k_build_sizes  (warp per vertex)  validates the CSR, counts the radix groups
+//                 c_k (Eq.3/4) with one ballot per bit per 32 arcs,
+//                 classifies them (Eq.9) and emits the capacity each
+//                 pool needs for the vertex.
+//  scans          exclusive prefix sums -> deterministic pool offsets.
+//  k_build_fill   (warp per vertex)  copies the arcs, materialises REGULAR/SPARSE
+//                 member lists in ascending adjacency order (R-2) by ballot
+//                 compaction, finds one-element members, builds the integer Vose
+//                 alias over the nonempty groups with one lane per bucket (R-4),
+//                 and writes the 32 B buckets and the 32 B vertex header.
+#include <cstdio>
+#include <cstring>
+
+#include "bingo.h"
+#include "bingo_internal.cuh"
+#include "build_common.cuh"
+#include "scan.cuh"
+
+using namespace bingo;
+
+namespace bingo {
+
+__global__ void k_build_sizes(uint32_t V, const uint64_t *__restrict__ ro, const uint32_t *__restrict__ dst,
+                              const uint32_t *__restrict__ bias, uint32_t alpha, uint32_t beta, bool bs,
+                              double arc_slack, double mem_slack, uint64_t *__restrict__ sz_arc,
+                              uint64_t *__restrict__ sz_bkt, uint64_t *__restrict__ sz_mem, int *__restrict__ flag) {
+    const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
+    const uint32_t lane = lane_id();
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+        const uint64_t b0 = ro[u], b1 = ro[u + 1];
+        if (b1 < b0 || b1 - b0 >= 0xFFFFFFFFull) {
+            if (lane == 0) atomicOr(flag, b1 < b0 ? 1 : 4);
+            continue;
+        }
+        const uint32_t d = (uint32_t)(b1 - b0);
+        uint32_t cnt = 0;       // lane k: c_k
+        uint64_t tsum = 0;      // partial sum of biases
+        uint32_t mask = 0;
+        for (uint32_t base = 0; base < d; base += 32) {
+            uint32_t i = base + lane;
+            uint32_t w = 0;
+            if (i < d) {
+                w = bias[b0 + i];
+                uint32_t v = dst[b0 + i];
+                if (w == 0 || v >= V) atomicOr(flag, 1);
+                tsum += w;
+            }
+            mask |= w;
+#pragma unroll
+            for (int k = 0; k < 32; k++) {
+                uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+                if (lane == (uint32_t)k) cnt += __popc(bal);
+            }
+        }
+        const uint64_t T = warp_sum(tsum);
+        mask = __reduce_or_sync(0xffffffffu, mask);
+        const uint32_t n = __popc(mask);
+        if (lane == 0 && __umul64hi(T, (uint64_t)n) != 0) atomicOr(flag, 4);
+        const uint32_t kind = classify(cnt, d, alpha, beta, bs);
+        uint64_t units = is_list(kind) ? member_units(cnt, mem_slack) : 0;
+        units = warp_sum(units);
+        if (lane == 0) {
+            sz_arc[u] = arc_capacity(d, arc_slack);
+            sz_bkt[u] = bucket_capacity(n);
+            sz_mem[u] = units;
+        }
+    }
+}
+
+__global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const uint32_t *__restrict__ dst,
+                             const uint32_t *__restrict__ bias, uint32_t alpha, uint32_t beta, bool bs,
+                             double mem_slack, const uint64_t *__restrict__ off_arc,
+                             const uint64_t *__restrict__ off_bkt, const uint64_t *__restrict__ off_mem,
+                             VHdr *__restrict__ hdr, uint2 *__restrict__ arc, uint32_t *__restrict__ arc_epoch,
+                             Bucket *__restrict__ bkt, uint2 *__restrict__ mem) {
+    const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
+    const uint32_t lane = lane_id();
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+        const uint64_t b0 = ro[u];
+        const uint32_t d = (uint32_t)(ro[u + 1] - b0);
+        const uint64_t aoff = off_arc[u];
+        // pass 1: copy arcs, count groups
+        uint32_t cnt = 0;
+        uint64_t tsum = 0;
+        uint32_t mask = 0;
+        for (uint32_t base = 0; base < d; base += 32) {
+            uint32_t i = base + lane;
+            uint32_t w = 0;
+            if (i < d) {
+                w = bias[b0 + i];
+                arc[aoff + i] = make_uint2(dst[b0 + i], w);
+                arc_epoch[aoff + i] = 0;
+                tsum += w;
+            }
+            mask |= w;
+#pragma unroll
+            for (int k = 0; k < 32; k++) {
+                uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+                if (lane == (uint32_t)k) cnt += __popc(bal);
+            }
+        }
+        const uint64_t T = warp_sum(tsum);
+        mask = __reduce_or_sync(0xffffffffu, mask);
+        const uint32_t n = __popc(mask);
+        const uint32_t kind = classify(cnt, d, alpha, beta, bs);
+        // member array of group k (lane k): offset in 16 B units, capacity in entries
+        const uint32_t units = is_list(kind) ? member_units(cnt, mem_slack) : 0;
+        uint32_t pre = units;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, pre, o);
+            if ((int)lane >= o) pre += y;
+        }
+        pre -= units;
+        const uint64_t my_off = off_mem[u] + pre;   // 16 B units
+        // pass 2: members (ascending adjacency index) and one-element members
+        uint32_t fill = 0;          // lane k: entries written so far
+        uint32_t one_idx = 0, one_dst = 0;
+        const bool any_member_kind = __any_sync(0xffffffffu, is_list(kind) || kind == K_ONE);
+        if (any_member_kind) {
+            for (uint32_t base = 0; base < d; base += 32) {
+                uint32_t i = base + lane;
+                uint32_t w = 0, v = 0;
+                if (i < d) { w = bias[b0 + i]; v = dst[b0 + i]; }
+                uint32_t mk = mask;
+                while (mk) {
+                    const int k = __ffs(mk) - 1;
+                    mk &= mk - 1;
+                    const uint32_t kind_k = __shfl_sync(0xffffffffu, kind, k);
+                    if (!(is_list(kind_k) || kind_k == K_ONE)) continue;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+                    if (!bal) continue;
+                    if (kind_k == K_ONE) {
+                        const int src_lane = __ffs(bal) - 1;
+                        const uint32_t vv = __shfl_sync(0xffffffffu, v, src_lane);
+                        if (lane == (uint32_t)k) { one_idx = base + src_lane; one_dst = vv; }
+                        continue;
+                    }
+                    const uint32_t start = __shfl_sync(0xffffffffu, fill, k);
+                    const uint64_t goff = __shfl_sync(0xffffffffu, my_off, k);
+                    if ((w >> k) & 1u) mem[goff * 2 + start + __popc(bal & lanemask_lt())] = make_uint2(i, v);
+                    if (lane == (uint32_t)k) fill += __popc(bal);
+                }
+            }
+        }
+        // integer Vose over nonempty groups, lane b = bucket b (R-4)
+        const uint32_t kb = (lane < n) ? (uint32_t)__fns(mask, 0, lane + 1) : 0;
+        const uint32_t c_b = __shfl_sync(0xffffffffu, cnt, kb);
+        const uint32_t kind_b = __shfl_sync(0xffffffffu, kind, kb);
+        const uint64_t off_b = __shfl_sync(0xffffffffu, my_off, kb);
+        const uint32_t oi_b = __shfl_sync(0xffffffffu, one_idx, kb);
+        const uint32_t od_b = __shfl_sync(0xffffffffu, one_dst, kb);
+        const uint32_t units_b = __shfl_sync(0xffffffffu, units, kb);
+        uint64_t thr;
+        uint32_t alias;
+        vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
+        const uint64_t bo = off_bkt[u];
+        Bucket B;
+        B.thr = thr;
+        B.c = c_b;
+        B.kk = make_kk(kb, kind_b);
+        B.ref = is_list(kind_b) ? (uint32_t)off_b : (kind_b == K_ONE ? od_b : 0u);
+        B.aux = is_list(kind_b) ? units_b * 2 : (kind_b == K_ONE ? oi_b : 0u);
+        B.alias = (uint8_t)alias;
+        B.pad = 0;
+        const uint32_t a_c = __shfl_sync(0xffffffffu, B.c, alias);
+        const uint32_t a_ref = __shfl_sync(0xffffffffu, B.ref, alias);
+        const uint32_t a_kk = __shfl_sync(0xffffffffu, (uint32_t)B.kk, alias);
+        B.a_c = a_c;
+        B.a_ref = a_ref;
+        B.a_kk = (uint8_t)a_kk;
+        if (lane < n) store_bucket(&bkt[bo + lane], B);
+        if (lane == 0) {
+            VHdr h;
+            h.T = T;
+            h.adj_off = aoff;
+            h.bkt_off = (uint32_t)bo;
+            h.d = d;
+            h.n = (uint8_t)n;
+            h.ncap = (uint8_t)bucket_capacity(n);
+            h.pad = 0;
+            h.adj_cap = (uint32_t)(off_arc[u + 1] - aoff);
+            hdr[u] = h;
+        }
+    }
+}
+
+}  // namespace bingo
+
+// ---------------------------------------------------------------- host side
+static bingo_status fail_cuda(bingo_graph *g, cudaError_t e, const char *where) {
+    fprintf(stderr, "libbingo: CUDA error in %s: %s\n", where, cudaGetErrorString(e));
+    if (g) g->poisoned = 1;
+    return BINGO_E_CUDA;
+}
+#define CK(call)                                                  \
+    do {                                                          \
+        cudaError_t e_ = (call);                                  \
+        if (e_ != cudaSuccess) { st = fail_cuda(g, e_, #call); goto done; } \
+    } while (0)
+
+extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, bingo_graph **out) {
+    if (!desc || !out) return BINGO_E_INVAL;
+    *out = nullptr;
+    const uint32_t V = desc->num_vertices;
+    if (V == 0 && desc->num_arcs) return BINGO_E_INVAL;
+    if (V >= 0x7FFFFFFFu) return BINGO_E_INVAL;
+    if (!desc->row_offsets || (desc->num_arcs && (!desc->dst || !desc->bias))) return BINGO_E_INVAL;
+    if (desc->alpha_pct > 100 || desc->beta_pct > 100) return BINGO_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    bingo_graph *g = new bingo_graph();
+    bingo_status st = BINGO_OK;
+    const bool bs = (desc->flags & BINGO_BUILD_BS_MODE) != 0;
+    g->V = V;
+    g->flags = desc->flags;
+    g->alpha = bs ? 100 : desc->alpha_pct;
+    g->beta = bs ? 0 : desc->beta_pct;
+    g->alloc = desc->alloc;
+    g->free_ = desc->free;
+    g->alloc_ctx = desc->alloc_ctx;
+    g->arc_slack = desc->arc_slack >= 0 ? desc->arc_slack : 0.25;
+    g->member_slack = desc->member_slack >= 0 ? desc->member_slack : 0.25;
+    g->pool_reserve = desc->pool_reserve >= 0 ? desc->pool_reserve : 0.1;
+    g->num_arcs = desc->num_arcs;
+
+    const uint64_t nV = (uint64_t)V;
+    const size_t tmpw = scan_tmp_words(nV);
+    uint64_t *sz = nullptr, *off = nullptr, *tmp = nullptr;
+    uint64_t tot[3] = {0, 0, 0};
+    int hflag = 0;
+    unsigned long long hc[4];
+    const unsigned blocks = (unsigned)std::min<uint64_t>((nV + 7) / 8, 148ull * 64);
+
+    g->counters = (unsigned long long *)bingo_dev_alloc(g, 16 * sizeof(unsigned long long));
+    g->dev_flag = (int *)bingo_dev_alloc(g, sizeof(int) * 4);
+    g->hdr = (VHdr *)bingo_dev_alloc(g, sizeof(VHdr) * std::max<uint64_t>(nV, 1));
+    g->visit = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * std::max<uint64_t>(nV, 1));
+    sz = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (nV + 1));
+    off = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (nV + 1));
+    tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * tmpw);
+    if (!g->counters || !g->dev_flag || !g->hdr || !g->visit || !sz || !off || !tmp) { st = BINGO_E_NOMEM; goto done; }
+    CK(cudaMemsetAsync(g->counters, 0, 16 * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(g->dev_flag, 0, sizeof(int) * 4, s));
+    CK(cudaMemsetAsync(g->visit, 0, sizeof(unsigned long long) * std::max<uint64_t>(nV, 1), s));
+    CK(cudaMemsetAsync(g->hdr, 0, sizeof(VHdr) * std::max<uint64_t>(nV, 1), s));
+    if (V) {
+        k_build_sizes<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
+                                             g->arc_slack, g->member_slack, sz, sz + (nV + 1), sz + 2 * (nV + 1),
+                                             g->dev_flag);
+        CK(cudaGetLastError());
+        for (int p = 0; p < 3; p++) CK(exclusive_scan_u64(sz + p * (nV + 1), off + p * (nV + 1), nV, tmp, s));
+        CK(cudaMemcpyAsync(&hflag, g->dev_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        for (int p = 0; p < 3; p++)
+            CK(cudaMemcpyAsync(&tot[p], off + p * (nV + 1) + nV, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        uint64_t last_ro = 0;
+        CK(cudaMemcpy(&last_ro, desc->row_offsets + V, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+        if (last_ro != desc->num_arcs) hflag |= 1;
+        if (hflag & 1) { st = BINGO_E_INVAL; goto done; }
+        if (hflag & 4) { st = BINGO_E_OVERFLOW; goto done; }
+    }
+    if (tot[1] >= 0xFFFFFFFFull || tot[2] >= 0xFFFFFFFFull) { st = BINGO_E_OVERFLOW; goto done; }
+    g->arc_cap = pool_capacity(tot[0], g->pool_reserve, 1024);
+    g->bkt_cap = std::min<uint64_t>(pool_capacity(tot[1], g->pool_reserve, 1024), 0xFFFFFFF0ull);
+    g->mem_cap = 2 * std::min<uint64_t>(pool_capacity(tot[2], g->pool_reserve, 1024), 0xFFFFFFF0ull);
+    g->arc = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * g->arc_cap);
+    g->arc_epoch = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->arc_cap);
+    g->bkt = (Bucket *)bingo_dev_alloc(g, sizeof(Bucket) * g->bkt_cap);
+    g->mem = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * g->mem_cap);
+    if (!g->arc || !g->arc_epoch || !g->bkt || !g->mem) { st = BINGO_E_NOMEM; goto done; }
+    hc[0] = tot[0]; hc[1] = tot[1]; hc[2] = tot[2]; hc[3] = 0;
+    CK(cudaMemcpyAsync(g->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
+    if (V) {
+        k_build_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
+                                            g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), g->hdr, g->arc,
+                                            g->arc_epoch, g->bkt, g->mem);
+        CK(cudaGetLastError());
+    }
+    CK(cudaStreamSynchronize(s));
+done:
+    bingo_dev_free(g, sz);
+    bingo_dev_free(g, off);
+    bingo_dev_free(g, tmp);
+    if (st != BINGO_OK) {
+        bingo_destroy(g);
+        return st;
+    }
+    *out = g;
+    return BINGO_OK;
+}

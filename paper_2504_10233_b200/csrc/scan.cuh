@@ -1,0 +1,13 @@
+// scan.cuh -- device exclusive prefix sums (u64) used by build and updates.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace bingo {
+
+// Exclusive scan of in[0..n) into out[0..n); out[n] receives the total.
+// `tmp` must hold scan_tmp_words(n) u64.  Asynchronous on `s`.
+size_t scan_tmp_words(uint64_t n);
+cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp, cudaStream_t s);
+
+}  // namespace bingo

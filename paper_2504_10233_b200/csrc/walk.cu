@@ -1,0 +1,200 @@
+// walk.cu -- the batched walker step.
+//
+// One walker per lane, warps of 32 consecutive walkers, a grid-stride loop over
+// walkers with the whole walk kept in registers.  Each step is a chain of
+// dependent 32 B sector loads through the read-only path:
+//   VHdr[u] -> Bucket[bkt_off + b] -> (member | arc per dense attempt)
+// and one coalesced, streaming (evict-first) store of the path column.
+// Randomness: Philox4x32-10 keyed by the seed, counter (walker, step,
+// (outer << 16) + inner, tag) (R-1) -- no RNG state in memory.
+#include <cstdio>
+
+#include "bingo.h"
+#include "bingo_internal.cuh"
+#include "build_common.cuh"
+#include "walk_common.cuh"
+
+using namespace bingo;
+
+namespace bingo {
+
+template <int APP>
+__global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += stride) {
+        const uint32_t w = a.first_walker + i;
+        uint32_t u = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);
+        if (a.paths) __stcs(&a.paths[i], u);
+        if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[u], 1ull);
+        uint32_t steps = 0, prev = 0xFFFFFFFFu;
+        for (uint32_t t = 0; a.L == BINGO_NO_CAP || t < a.L; t++) {
+            const VHdr h = load_hdr(a.hdr + u);
+            if (h.d == 0) break;   // dead end: truncate (R-13)
+            uint32_t next;
+            if (APP == BINGO_NODE2VEC && t >= 1) {
+                // KnightKing rejection: propose first-order, accept with f/f_max
+                for (uint32_t o = 0;; o++) {
+                    next = sample_dst(a, h, w, t, o);
+                    const uint32_t cls = (next == prev) ? 0u : (probe_arc(a, prev, next) ? 1u : 2u);
+                    if (a.n2v_always[cls]) break;
+                    const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
+                    if (join64(r.x, r.y) < a.n2v_thr[cls]) break;
+                }
+            } else {
+                next = sample_dst(a, h, w, t, 0);
+            }
+            steps++;
+            if (a.paths) __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
+            prev = u;
+            u = next;
+            if (APP == BINGO_PPR) {
+                if (a.visit) atomicAdd(&a.visit[u], 1ull);
+                if (a.stop_always) break;
+                const P4 r = philox10(w, t, 0u, 3u, a.k0, a.k1);
+                if (join64(r.x, r.y) < a.stop_thr) break;
+            }
+        }
+        if (a.lengths) a.lengths[i] = steps;
+        if (a.paths && a.L != BINGO_NO_CAP)
+            for (uint32_t t = steps + 1; t <= a.L; t++) __stcs(&a.paths[(size_t)t * a.W + i], 0xFFFFFFFFu);
+    }
+}
+
+}  // namespace bingo
+
+// ---------------------------------------------------------------- host side
+static void n2v_thresholds(double p, double q, unsigned long long thr[3], uint32_t always[3]) {
+    const double f[3] = {1.0 / p, 1.0, 1.0 / q};
+    double fmax = f[0];
+    for (int i = 1; i < 3; i++) fmax = f[i] > fmax ? f[i] : fmax;
+    for (int i = 0; i < 3; i++) {
+        const double r = f[i] / fmax;
+        if (r >= 1.0) {
+            always[i] = 1;
+            thr[i] = 0;
+        } else {
+            // floor(r * 2^64): r < 1 is a double, r * 2^64 is exact, conversion truncates
+            always[i] = 0;
+            thr[i] = (unsigned long long)ldexp(r, 64);
+        }
+    }
+}
+
+static void stop_threshold(uint32_t num, uint32_t den, unsigned long long *thr, uint32_t *always) {
+    if (num >= den) {
+        *always = 1;
+        *thr = 0;
+        return;
+    }
+    *always = 0;
+    *thr = (unsigned long long)(((unsigned __int128)num << 64) / den);   // floor(num 2^64 / den)
+}
+
+static size_t walk_grid(uint32_t W) {
+    size_t blocks = ((size_t)W + 255) / 256;
+    const size_t cap = 148 * 8;
+    return blocks < cap ? (blocks ? blocks : 1) : cap;
+}
+
+bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts, uint32_t W,
+                         uint32_t *paths, uint32_t *lengths, cudaStream_t s) {
+    WalkArgs a;
+    a.hdr = g->hdr;
+    a.bkt = g->bkt;
+    a.arc = g->arc;
+    a.mem = g->mem;
+    a.visit = g->visit;
+    a.starts = starts;
+    a.paths = paths;
+    a.lengths = lengths;
+    a.W = W;
+    a.V = g->V;
+    a.L = desc->length;
+    a.first_walker = desc->first_walker_id;
+    a.k0 = (uint32_t)desc->seed;
+    a.k1 = (uint32_t)(desc->seed >> 32);
+    n2v_thresholds(desc->app == BINGO_NODE2VEC ? desc->p : 1.0, desc->app == BINGO_NODE2VEC ? desc->q : 1.0,
+                   a.n2v_thr, a.n2v_always);
+    stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
+    const unsigned grid = (unsigned)walk_grid(W);
+    switch (desc->app) {
+        case BINGO_DEEPWALK: k_walk<BINGO_DEEPWALK><<<grid, 256, 0, s>>>(a); break;
+        case BINGO_NODE2VEC: k_walk<BINGO_NODE2VEC><<<grid, 256, 0, s>>>(a); break;
+        case BINGO_PPR: k_walk<BINGO_PPR><<<grid, 256, 0, s>>>(a); break;
+        default: return BINGO_E_INVAL;
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        fprintf(stderr, "libbingo: walk launch failed: %s\n", cudaGetErrorString(e));
+        g->poisoned = 1;
+        return BINGO_E_CUDA;
+    }
+    return BINGO_OK;
+}
+
+extern "C" bingo_status bingo_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts_or_null,
+                                   uint32_t num_walkers, uint32_t *paths_or_null, uint32_t *lengths_or_null,
+                                   void *stream) {
+    if (!g || !desc) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    if (desc->app > BINGO_PPR) return BINGO_E_INVAL;
+    if (desc->app == BINGO_NODE2VEC && !(desc->p > 0 && desc->q > 0)) return BINGO_E_INVAL;
+    if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
+    if (desc->length == BINGO_NO_CAP && paths_or_null) return BINGO_E_INVAL;
+    if (desc->length == BINGO_NO_CAP && desc->app != BINGO_PPR) return BINGO_E_INVAL;
+    if (num_walkers == 0) return BINGO_OK;
+    if (g->V == 0) return BINGO_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (!(desc->flags & BINGO_WALK_HOST_OUTPUT))
+        return launch_walk(g, desc, starts_or_null, num_walkers, paths_or_null, lengths_or_null, s);
+    // HOST buffers: stage through device scratch
+    const size_t n_path = paths_or_null ? (size_t)(desc->length + 1) * num_walkers : 0;
+    const size_t need = sizeof(uint32_t) * (n_path + (lengths_or_null ? num_walkers : 0) +
+                                            (starts_or_null ? num_walkers : 0)) + 256;
+    if (g->wscratch_bytes < need) {
+        bingo_dev_free(g, g->wscratch);
+        g->wscratch = bingo_dev_alloc(g, need);
+        g->wscratch_bytes = g->wscratch ? need : 0;
+        if (!g->wscratch) return BINGO_E_NOMEM;
+    }
+    uint32_t *dp = (uint32_t *)g->wscratch;
+    uint32_t *dl = dp + n_path;
+    uint32_t *ds = dl + (lengths_or_null ? num_walkers : 0);
+    cudaError_t e = cudaSuccess;
+    if (starts_or_null)
+        e = cudaMemcpyAsync(ds, starts_or_null, sizeof(uint32_t) * num_walkers, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) {
+        bingo_status st = launch_walk(g, desc, starts_or_null ? ds : nullptr, num_walkers,
+                                      paths_or_null ? dp : nullptr, lengths_or_null ? dl : nullptr, s);
+        if (st != BINGO_OK) return st;
+    }
+    if (e == cudaSuccess && paths_or_null)
+        e = cudaMemcpyAsync(paths_or_null, dp, sizeof(uint32_t) * n_path, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && lengths_or_null)
+        e = cudaMemcpyAsync(lengths_or_null, dl, sizeof(uint32_t) * num_walkers, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "libbingo: walk staging failed: %s\n", cudaGetErrorString(e));
+        g->poisoned = 1;
+        return BINGO_E_CUDA;
+    }
+    return BINGO_OK;
+}
+
+extern "C" bingo_status bingo_visit_counts(bingo_graph *g, uint64_t *counts, int reset, uint32_t flags, void *stream) {
+    if (!g) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    const size_t bytes = sizeof(uint64_t) * g->V;
+    if (counts && g->V)
+        e = cudaMemcpyAsync(counts, g->visit, bytes,
+                            (flags & BINGO_COUNTS_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s);
+    if (e == cudaSuccess && reset && g->V) e = cudaMemsetAsync(g->visit, 0, bytes, s);
+    if (e == cudaSuccess && (flags & BINGO_COUNTS_HOST)) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        g->poisoned = 1;
+        return BINGO_E_CUDA;
+    }
+    return BINGO_OK;
+}
