@@ -29,7 +29,7 @@ void bingo_dev_free(bingo_graph *g, void *p) {
 extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
     void *bufs[] = {g->hdr, g->arc, g->arc_epoch, g->bkt, g->mem, g->counters, g->visit, g->dev_flag,
-                    g->scratch, g->wscratch};
+                    g->scratch, g->wscratch, g->vscratch};
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
     delete g;
@@ -68,7 +68,7 @@ extern "C" bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *s
     info->member_pool_cap = g->mem_cap;
     info->device_bytes = sizeof(VHdr) * (uint64_t)g->V + (sizeof(uint2) + 4) * g->arc_cap +
                          sizeof(Bucket) * g->bkt_cap + sizeof(uint2) * g->mem_cap + 8ull * g->V +
-                         g->scratch_bytes + g->wscratch_bytes;
+                         g->scratch_bytes + g->wscratch_bytes + g->vscratch_bytes;
     return BINGO_OK;
 }
 

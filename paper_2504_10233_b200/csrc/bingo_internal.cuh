@@ -140,6 +140,8 @@ struct bingo_graph {
     size_t hscratch_bytes = 0;
     void *wscratch = nullptr;                // walk staging for HOST_OUTPUT
     size_t wscratch_bytes = 0;
+    void *vscratch = nullptr;                // per-touched-vertex delete scratch
+    size_t vscratch_bytes = 0;
 };
 
 // allocation helpers (api.cu)

@@ -1,9 +1,951 @@
-// update.cu -- batched insert/delete (placeholder until the update pipeline lands)
+// update.cu -- batched edge insert/delete (PAPER S5.2).
+//
+// Pipeline for one batch of n arc records (all on `stream`):
+//   k_upd_validate   record checks (EINVAL) + radix keys (src) / values (index)
+//   radix sort       stable by src -> per-vertex segments in batch order
+//   k_upd_heads + scan + k_upd_segments   touched-vertex segments
+//   k_upd_plan       (warp per touched vertex) overflow checks and the exact
+//                    pool demand of the batch -- nothing is mutated
+//   -- host: one sync; EINVAL / EOVERFLOW / pool growth (NOMEM) decided here --
+//   k_upd_mutate     (block per touched vertex) insert -> delete -> rebuild:
+//                    (1) inserts append to the adjacency and to groups that are
+//                        REGULAR/SPARSE before the batch, in batch order
+//                    (2) deletes: each (u,v) takes the live instance with the
+//                        smallest (epoch, position) (R-8) -- selected by an
+//                        atomicMin over packed (epoch << 32 | position) keys per
+//                        distinct v; then the two-phase parallel delete-and-swap
+//                        (pairing R-6) on every list group and on the
+//                        adjacency, and the rename of moved arcs
+//                    (3) rebuild: Eq.9 reclassification, member materialisation
+//                        on kind change, integer Vose alias (R-4)
+//   k_upd_stats      reduce per-vertex statistics
+// Untouched vertices are never read or written.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
 #include "bingo.h"
 #include "bingo_internal.cuh"
+#include "build_common.cuh"
+#include "scan.cuh"
+#include "sort.cuh"
+
+using namespace bingo;
+
+namespace bingo {
+
+static constexpr uint32_t EMPTY_KEY = 0xFFFFFFFFu;
+static constexpr uint32_t DEL_MARK = 0xFFFFFFFFu;
+static constexpr int MT = 256;   // threads per mutate block
+
+// per-touched-vertex statistics: [0] deleted, [1] missing, [2..26] transitions
+static constexpr int VST = 28;
+
+struct UpdCounters {        // device, zeroed per batch
+    unsigned long long need_arc, need_bkt, need_mem, reserve_mem;
+    unsigned long long scratch_words;
+    int flag;
+    int pad;
+};
+
+__device__ __forceinline__ uint32_t hash_slot(uint32_t x, uint32_t mask) {
+    x ^= x >> 16;
+    x *= 0x7feb352du;
+    x ^= x >> 15;
+    x *= 0x846ca68bu;
+    x ^= x >> 16;
+    return x & mask;
+}
+
+__device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
+    return x <= 1 ? 1u : 1u << (32 - __clz(x - 1));
+}
+
+// ------------------------------------------------------------------ validate
+__global__ void k_upd_validate(const uint4 *__restrict__ recs, uint64_t n, uint32_t V, uint32_t *__restrict__ keys,
+                               uint32_t *__restrict__ vals, UpdCounters *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 r = recs[i];
+        const bool bad = r.x > 1u || r.y >= V || r.z >= V || (r.x == 0u && r.w == 0u);
+        if (bad) atomicOr(&cnt->flag, 1);
+        keys[i] = bad ? 0u : r.y;
+        vals[i] = (uint32_t)i;
+    }
+}
+
+// head flags over the sorted keys
+__global__ void k_upd_heads(const uint32_t *__restrict__ skeys, uint64_t n, uint64_t *__restrict__ head) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        head[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1ull : 0ull;
+}
+
+// segments: touched vertex t covers sorted positions [seg[t], seg[t + 1])
+__global__ void k_upd_segments(const uint64_t *__restrict__ head_ex, const uint32_t *__restrict__ skeys, uint64_t n,
+                               uint32_t *__restrict__ seg, uint32_t *__restrict__ tv) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const bool h = (i == 0 || skeys[i] != skeys[i - 1]);
+        if (h) {
+            const uint64_t t = head_ex[i];
+            seg[t] = (uint32_t)i;
+            tv[t] = skeys[i];
+        }
+        if (i == n - 1) seg[head_ex[n]] = (uint32_t)n;
+    }
+}
+
+// ------------------------------------------------------------------ per-vertex pre-batch view
+struct OldGroups {
+    uint32_t mask;      // nonempty groups (bit k)
+    uint32_t list_mask; // REGULAR/SPARSE groups
+};
+
+// lane b < n loads bucket b; returns (k, kind, c, ref, aux) of lane k's group in lane k
+__device__ __forceinline__ void load_old_groups(const Bucket *bkt, const VHdr &h, uint32_t &kind_k, uint32_t &c_k,
+                                                uint32_t &ref_k, uint32_t &aux_k, OldGroups &og) {
+    const uint32_t lane = lane_id();
+    uint32_t k_b = 0, kind_b = K_EMPTY, c_b = 0, ref_b = 0, aux_b = 0;
+    if (lane < h.n) {
+        const Bucket B = load_bucket(bkt + h.bkt_off + lane);
+        k_b = kk_k(B.kk);
+        kind_b = kk_kind(B.kk);
+        c_b = B.c;
+        ref_b = B.ref;
+        aux_b = B.aux;
+    }
+    const uint32_t m = __reduce_or_sync(0xffffffffu, lane < h.n ? (1u << k_b) : 0u);
+    og.mask = m;
+    og.list_mask = __reduce_or_sync(0xffffffffu, (lane < h.n && is_list(kind_b)) ? (1u << k_b) : 0u);
+    // lane k pulls from lane b = rank of k in mask
+    const uint32_t b = __popc(m & ((1u << lane) - 1u));
+    const bool has = (m >> lane) & 1u;
+    const uint32_t src = has ? b : 0u;
+    const uint32_t kd = __shfl_sync(0xffffffffu, kind_b, src);
+    const uint32_t cc = __shfl_sync(0xffffffffu, c_b, src);
+    const uint32_t rf = __shfl_sync(0xffffffffu, ref_b, src);
+    const uint32_t ax = __shfl_sync(0xffffffffu, aux_b, src);
+    kind_k = has ? kd : K_EMPTY;
+    c_k = has ? cc : 0u;
+    ref_k = has ? rf : 0u;
+    aux_k = has ? ax : 0u;
+}
+
+// ------------------------------------------------------------------ plan (no mutation)
+__global__ void k_upd_plan(const uint4 *__restrict__ recs, const uint32_t *__restrict__ sval,
+                           const uint32_t *__restrict__ seg, const uint32_t *__restrict__ tv, uint32_t ntouch,
+                           const VHdr *__restrict__ hdr, const Bucket *__restrict__ bkt, uint32_t alpha, bool bs,
+                           double arc_slack, double mem_slack, uint64_t *__restrict__ scr_need, UpdCounters *cnt) {
+    const uint32_t lane = lane_id();
+    const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
+    for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntouch; t += warps) {
+        const uint32_t u = tv[t];
+        const uint32_t beg = seg[t], end = seg[t + 1];
+        const VHdr h = hdr[u];
+        uint32_t kind_k, c_k, ref_k, aux_k;
+        OldGroups og;
+        load_old_groups(bkt, h, kind_k, c_k, ref_k, aux_k, og);
+        uint32_t m = 0, q = 0, ins_or = 0, insk = 0;
+        uint64_t ins_sum = 0;
+        for (uint32_t base = beg; base < end; base += 32) {
+            const uint32_t p = base + lane;
+            uint4 r = make_uint4(2u, 0u, 0u, 0u);
+            if (p < end) r = recs[sval[p]];
+            const bool ins = r.x == 0u, del = r.x == 1u;
+            const uint32_t w = ins ? r.w : 0u;
+            m += __popc(__ballot_sync(0xffffffffu, ins));
+            q += __popc(__ballot_sync(0xffffffffu, del));
+            ins_or |= w;
+            ins_sum += w;
+            uint32_t mk = __reduce_or_sync(0xffffffffu, w);
+            while (mk) {
+                const int k = __ffs(mk) - 1;
+                mk &= mk - 1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+                if (lane == (uint32_t)k) insk += __popc(bal);
+            }
+        }
+        ins_or = __reduce_or_sync(0xffffffffu, ins_or);
+        ins_sum = warp_sum(ins_sum);
+        // overflow: (T + inserted) * popc(mask | inserted) < 2^64 and d + m < 2^32 - 1 (R-10)
+        const uint32_t nb = __popc(og.mask | ins_or);
+        const uint64_t Tn = h.T + ins_sum;
+        const bool carry = Tn < h.T;
+        if (lane == 0 && (carry || __umul64hi(Tn, (uint64_t)nb) != 0 || (uint64_t)h.d + m >= 0xFFFFFFFFull))
+            atomicOr(&cnt->flag, 4);
+        const uint32_t L = h.d + m;
+        // pool demand (exact for relocations; a tight upper bound for kind transitions)
+        uint64_t need_mem = 0, reserve = 0;
+        const uint32_t cin = c_k + insk;
+        if (is_list(kind_k)) {
+            if (cin > aux_k) need_mem = member_units(cin, mem_slack);
+        } else if (bs) {
+            if (cin >= 1 && kind_k == K_EMPTY) reserve = member_units(cin, mem_slack);
+        } else if (kind_k == K_EMPTY) {
+            if (insk >= 2) reserve = member_units(cin, mem_slack);
+        } else if (kind_k == K_ONE) {
+            if (insk >= 1) reserve = member_units(cin, mem_slack);
+        } else if (kind_k == K_DENSE) {
+            const uint32_t cmin = c_k > q ? c_k - q : 0u;
+            if ((uint64_t)100 * cmin <= (uint64_t)alpha * L) reserve = member_units(cin, mem_slack);
+        }
+        need_mem = warp_sum(need_mem);
+        reserve = warp_sum(reserve);
+        if (lane == 0) {
+            if (L > h.adj_cap) atomicAdd(&cnt->need_arc, (unsigned long long)arc_capacity(L, arc_slack));
+            if (nb > h.ncap) atomicAdd(&cnt->need_bkt, (unsigned long long)bucket_capacity(nb));
+            if (need_mem) atomicAdd(&cnt->need_mem, (unsigned long long)need_mem);
+            if (reserve) atomicAdd(&cnt->reserve_mem, (unsigned long long)reserve);
+            uint64_t words = 0;
+            if (q) {
+                const uint64_t Hq = next_pow2(2 * q);
+                words = (uint64_t)(L + 31) / 32 + 8 * Hq + 3ull * q + 8;
+                words = (words + 7) & ~7ull;
+            }
+            scr_need[t] = words;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ block helpers
+// block-wide exclusive scan of one u32 per thread; returns prefix, *total via smem
+__device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t *s_tmp /*[MT/32+1]*/, uint32_t &total) {
+    const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) s_tmp[wid] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+        for (int w = 0; w < MT / 32; w++) {
+            const uint32_t t = s_tmp[w];
+            s_tmp[w] = acc;
+            acc += t;
+        }
+        s_tmp[MT / 32] = acc;
+    }
+    __syncthreads();
+    const uint32_t r = x - v + s_tmp[wid];
+    total = s_tmp[MT / 32];
+    __syncthreads();
+    return r;
+}
+
+__device__ __forceinline__ bool bit_test(const uint32_t *bm, uint32_t p) { return (bm[p >> 5] >> (p & 31u)) & 1u; }
+
+// ------------------------------------------------------------------ mutate (block per touched vertex)
+struct MutateArgs {
+    const uint4 *recs;
+    const uint32_t *sval;
+    const uint32_t *seg;
+    const uint32_t *tv;
+    const uint64_t *scr_off;
+    uint32_t *scr;
+    VHdr *hdr;
+    uint2 *arc;
+    uint32_t *arc_epoch;
+    Bucket *bkt;
+    uint2 *mem;
+    unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units
+    uint32_t *vstats;           // [ntouch][VST]
+    uint32_t epoch, alpha, beta;
+    bool bs;
+    double arc_slack, mem_slack;
+};
+
+__global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
+    const uint32_t t = blockIdx.x;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
+    __shared__ uint32_t s_kind0[32], s_c[32], s_insk[32], s_delk[32], s_moff[32], s_cap[32], s_one[32];
+    __shared__ uint32_t s_tmp[MT / 32 + 1];
+    __shared__ uint32_t s_list0, s_m, s_q, s_N, s_missing;
+    __shared__ uint64_t s_adj_off;
+    __shared__ uint32_t s_adj_cap;
+    __shared__ uint32_t s_fill_mask, s_find_mask, s_kind1[32];
+
+    const uint32_t u = a.tv[t];
+    const uint32_t beg = a.seg[t], end = a.seg[t + 1];
+    const VHdr h = a.hdr[u];
+
+    // ---------------- phase 0: pre-batch groups, relocations
+    if (wid == 0) {
+        uint32_t kind_k, c_k, ref_k, aux_k;
+        OldGroups og;
+        load_old_groups(a.bkt, h, kind_k, c_k, ref_k, aux_k, og);
+        // insert counts per bit for capacity decisions
+        uint32_t m = 0, q = 0, insk = 0;
+        for (uint32_t base = beg; base < end; base += 32) {
+            const uint32_t p = base + lane;
+            uint4 r = make_uint4(2u, 0u, 0u, 0u);
+            if (p < end) r = a.recs[a.sval[p]];
+            const uint32_t w = r.x == 0u ? r.w : 0u;
+            m += __popc(__ballot_sync(0xffffffffu, r.x == 0u));
+            q += __popc(__ballot_sync(0xffffffffu, r.x == 1u));
+            uint32_t mk = __reduce_or_sync(0xffffffffu, w);
+            while (mk) {
+                const int k = __ffs(mk) - 1;
+                mk &= mk - 1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+                if (lane == (uint32_t)k) insk += __popc(bal);
+            }
+        }
+        s_kind0[lane] = kind_k;
+        s_c[lane] = c_k;
+        s_insk[lane] = 0;      // filled by the insert phase
+        s_delk[lane] = 0;
+        s_one[lane] = (kind_k == K_ONE) ? aux_k : 0xFFFFFFFFu;
+        uint32_t moff = ref_k, cap = aux_k;
+        const uint32_t cin = c_k + insk;
+        bool grow = is_list(kind_k) && cin > cap;
+        if (grow) {
+            const uint32_t units = member_units(cin, a.mem_slack);
+            moff = (uint32_t)atomicAdd(&a.bump[2], (unsigned long long)units);
+            cap = units * 2;
+        }
+        s_moff[lane] = is_list(kind_k) ? moff : 0u;
+        s_cap[lane] = is_list(kind_k) ? cap : 0u;
+        if (lane == 0) {
+            s_list0 = og.list_mask;
+            s_m = m;
+            s_q = q;
+            s_N = 0;
+            s_missing = 0;
+            const uint32_t L = h.d + m;
+            if (L > h.adj_cap) {
+                const uint64_t cap2 = arc_capacity(L, a.arc_slack);
+                s_adj_off = atomicAdd(&a.bump[0], (unsigned long long)cap2);
+                s_adj_cap = (uint32_t)cap2;
+            } else {
+                s_adj_off = h.adj_off;
+                s_adj_cap = h.adj_cap;
+            }
+        }
+        // copy growing member arrays (warp-cooperative, one group at a time)
+        uint32_t gm = __ballot_sync(0xffffffffu, grow);
+        while (gm) {
+            const int k = __ffs(gm) - 1;
+            gm &= gm - 1;
+            const uint32_t from = __shfl_sync(0xffffffffu, ref_k, k);
+            const uint32_t to = __shfl_sync(0xffffffffu, moff, k);
+            const uint32_t cnt = __shfl_sync(0xffffffffu, c_k, k);
+            for (uint32_t j = lane; j < cnt; j += 32) a.mem[(uint64_t)to * 2 + j] = a.mem[(uint64_t)from * 2 + j];
+        }
+    }
+    __syncthreads();
+    const uint64_t aoff = s_adj_off;
+    const uint32_t m = s_m, q = s_q;
+    const uint32_t L = h.d + m;
+    if (aoff != h.adj_off) {
+        for (uint32_t i = tid; i < h.d; i += MT) {
+            a.arc[aoff + i] = a.arc[h.adj_off + i];
+            a.arc_epoch[aoff + i] = a.arc_epoch[h.adj_off + i];
+        }
+    }
+    __syncthreads();
+
+    // ---------------- phase 1: inserts, batch order
+    if (wid == 0 && m) {
+        uint32_t run = 0;          // inserts so far
+        uint32_t insk = 0;         // lane k: inserts with bit k so far
+        const uint32_t kind_l = s_kind0[lane];
+        const uint32_t c_l = s_c[lane];
+        const uint32_t moff_l = s_moff[lane];
+        for (uint32_t base = beg; base < end; base += 32) {
+            const uint32_t p = base + lane;
+            uint4 r = make_uint4(2u, 0u, 0u, 0u);
+            if (p < end) r = a.recs[a.sval[p]];
+            const bool ins = r.x == 0u;
+            const uint32_t bal_i = __ballot_sync(0xffffffffu, ins);
+            const uint32_t idx = h.d + run + __popc(bal_i & lanemask_lt());
+            const uint32_t w = ins ? r.w : 0u;
+            if (ins) {
+                a.arc[aoff + idx] = make_uint2(r.z, r.w);
+                a.arc_epoch[aoff + idx] = a.epoch;
+            }
+            uint32_t mk = __reduce_or_sync(0xffffffffu, w);
+            while (mk) {
+                const int k = __ffs(mk) - 1;
+                mk &= mk - 1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+                const uint32_t kind_kk = __shfl_sync(0xffffffffu, kind_l, k);
+                const uint32_t start = __shfl_sync(0xffffffffu, c_l + insk, k);
+                const uint32_t mo = __shfl_sync(0xffffffffu, moff_l, k);
+                if (is_list(kind_kk) && ((w >> k) & 1u))
+                    a.mem[(uint64_t)mo * 2 + start + __popc(bal & lanemask_lt())] = make_uint2(idx, r.z);
+                if (lane == (uint32_t)k) insk += __popc(bal);
+            }
+            run += __popc(bal_i);
+        }
+        s_insk[lane] = insk;
+    }
+    __syncthreads();
+
+    // ---------------- phase 2: deletes
+    uint32_t N = 0;
+    uint32_t Lp = L;
+    uint32_t *bm = nullptr, *holes = nullptr, *R = nullptr, *gh = nullptr;
+    if (q) {
+        uint32_t *scr = a.scr + a.scr_off[t];
+        const uint32_t Hq = next_pow2(2 * q), hmask = Hq - 1;
+        const uint32_t bw = (L + 31) / 32;
+        bm = scr;
+        uint32_t *hkey = bm + bw;
+        uint32_t *hk = hkey + Hq;
+        uint32_t *hfound = hk + Hq;
+        uint32_t *hsel = hfound + Hq;
+        unsigned long long *hbest = reinterpret_cast<unsigned long long *>(
+            (reinterpret_cast<uintptr_t>(hsel + Hq) + 7) & ~(uintptr_t)7);
+        unsigned long long *hprev = hbest + Hq;
+        holes = reinterpret_cast<uint32_t *>(hprev + Hq);
+        R = holes + q;
+        gh = R + q;
+        for (uint32_t i = tid; i < bw; i += MT) bm[i] = 0;
+        for (uint32_t i = tid; i < Hq; i += MT) {
+            hkey[i] = EMPTY_KEY;
+            hk[i] = 0;
+            hfound[i] = 0;
+            hsel[i] = 0;
+            hbest[i] = ~0ull;
+            hprev[i] = 0;
+        }
+        __syncthreads();
+        // distinct deleted destinations with multiplicity
+        for (uint32_t p = beg + tid; p < end; p += MT) {
+            const uint4 r = a.recs[a.sval[p]];
+            if (r.x != 1u) continue;
+            uint32_t s = hash_slot(r.z, hmask);
+            for (;;) {
+                const uint32_t old = atomicCAS(&hkey[s], EMPTY_KEY, r.z);
+                if (old == EMPTY_KEY || old == r.z) {
+                    atomicAdd(&hk[s], 1u);
+                    break;
+                }
+                s = (s + 1) & hmask;
+            }
+        }
+        __syncthreads();
+        // selection rounds: round r picks, per distinct v still owed a delete, the
+        // live instance with the smallest (epoch, position) key above the last pick
+        for (uint32_t round = 0;; round++) {
+            for (uint32_t p = tid; p < L; p += MT) {
+                const uint32_t x = a.arc[aoff + p].x;
+                uint32_t s = hash_slot(x, hmask);
+                uint32_t hit = EMPTY_KEY;
+                for (;;) {
+                    const uint32_t kx = hkey[s];
+                    if (kx == x) { hit = s; break; }
+                    if (kx == EMPTY_KEY) break;
+                    s = (s + 1) & hmask;
+                }
+                if (hit == EMPTY_KEY) continue;
+                const unsigned long long key = ((unsigned long long)a.arc_epoch[aoff + p] << 32) | p;
+                if (round == 0) {
+                    atomicAdd(&hfound[hit], 1u);
+                    atomicMin(&hbest[hit], key);
+                } else if (hsel[hit] < hk[hit] && key > hprev[hit]) {
+                    atomicMin(&hbest[hit], key);
+                }
+            }
+            __syncthreads();
+            uint32_t more = 0;
+            for (uint32_t s = tid; s < Hq; s += MT) {
+                if (hkey[s] == EMPTY_KEY || hsel[s] >= hk[s]) continue;
+                const unsigned long long b = hbest[s];
+                if (b == ~0ull) continue;
+                const uint32_t p = (uint32_t)b;
+                atomicOr(&bm[p >> 5], 1u << (p & 31u));
+                hsel[s]++;
+                hprev[s] = b;
+                hbest[s] = ~0ull;
+                atomicAdd(&s_N, 1u);
+                uint32_t w = a.arc[aoff + p].y;
+                while (w) {
+                    const int k = __ffs(w) - 1;
+                    w &= w - 1;
+                    atomicAdd(&s_delk[k], 1u);
+                }
+                if (hsel[s] < hk[s] && hsel[s] < hfound[s]) more = 1;
+            }
+            if (!__syncthreads_or(more)) break;
+        }
+        for (uint32_t s = tid; s < Hq; s += MT)
+            if (hkey[s] != EMPTY_KEY) atomicAdd(&s_missing, hk[s] - hsel[s]);
+        __syncthreads();
+        N = s_N;
+        Lp = L - N;
+        if (N) {
+            // holes = marked positions < L' ascending (rank by block scan over bitmap words)
+            const uint32_t wl = (Lp + 31) / 32;
+            uint32_t carry = 0;
+            for (uint32_t w0 = 0; w0 < wl; w0 += MT) {
+                const uint32_t w = w0 + tid;
+                uint32_t word = 0;
+                if (w < wl) {
+                    word = bm[w];
+                    const uint32_t lim = Lp - w * 32;
+                    if (lim < 32) word &= (1u << lim) - 1u;
+                }
+                uint32_t tot;
+                const uint32_t pre = block_scan_u32(__popc(word), s_tmp, tot);
+                uint32_t r = carry + pre;
+                while (word) {
+                    const int b = __ffs(word) - 1;
+                    word &= word - 1;
+                    holes[r++] = w * 32 + b;
+                }
+                carry += tot;
+            }
+            __syncthreads();
+            // adjacency tail window [L', L): survivors fill holes in rank order
+            uint32_t scarry = 0;
+            for (uint32_t t0 = Lp; t0 < L; t0 += MT) {
+                const uint32_t tt = t0 + tid;
+                const bool in = tt < L;
+                const bool surv = in && !bit_test(bm, tt);
+                uint32_t tot;
+                const uint32_t rank = scarry + block_scan_u32(surv ? 1u : 0u, s_tmp, tot);
+                if (in) {
+                    if (surv) {
+                        const uint32_t dstp = holes[rank];
+                        a.arc[aoff + dstp] = a.arc[aoff + tt];
+                        a.arc_epoch[aoff + dstp] = a.arc_epoch[aoff + tt];
+                        R[tt - Lp] = dstp;
+                    } else {
+                        R[tt - Lp] = DEL_MARK;
+                    }
+                }
+                scarry += tot;
+            }
+            __syncthreads();
+        }
+    }
+    // ---------------- groups: delete-and-swap, rename (lists that existed before the batch)
+    if (N) {
+        uint32_t lm = s_list0;
+        while (lm) {
+            const int k = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const uint32_t cp = s_c[k] + s_insk[k];
+            const uint32_t Nk = s_delk[k];
+            uint2 *M = a.mem + (uint64_t)s_moff[k] * 2;
+            const uint32_t Lk = cp - Nk;
+            if (Nk) {
+                uint32_t carry = 0;
+                for (uint32_t s0 = 0; s0 < Lk; s0 += MT) {
+                    const uint32_t s = s0 + tid;
+                    const bool del = s < Lk && bit_test(bm, M[s].x);
+                    uint32_t tot;
+                    const uint32_t rank = carry + block_scan_u32(del ? 1u : 0u, s_tmp, tot);
+                    if (del) gh[rank] = s;
+                    carry += tot;
+                }
+                __syncthreads();
+                uint32_t scarry = 0;
+                for (uint32_t s0 = Lk; s0 < cp; s0 += MT) {
+                    const uint32_t s = s0 + tid;
+                    const bool surv = s < cp && !bit_test(bm, M[s].x);
+                    uint32_t tot;
+                    const uint32_t rank = scarry + block_scan_u32(surv ? 1u : 0u, s_tmp, tot);
+                    if (surv) M[gh[rank]] = M[s];
+                    scarry += tot;
+                }
+                __syncthreads();
+            }
+            for (uint32_t s = tid; s < Lk; s += MT) {
+                const uint32_t x = M[s].x;
+                if (x >= Lp) M[s].x = R[x - Lp];
+            }
+            __syncthreads();
+        }
+    }
+    // ---------------- phase 3: rebuild
+    const uint32_t dn = Lp;
+    if (wid == 0) {
+        const uint32_t k = lane;
+        const uint32_t kind0 = s_kind0[k];
+        const uint32_t cn = s_c[k] + s_insk[k] - s_delk[k];
+        const uint32_t kind1 = classify(cn, dn, a.alpha, a.beta, a.bs);
+        s_kind1[k] = kind1;
+        s_c[k] = cn;
+        bool fill = false, find = false;
+        uint32_t one = 0xFFFFFFFFu;
+        if (is_list(kind1) && !is_list(kind0)) {
+            const uint32_t units = member_units(cn, a.mem_slack);
+            s_moff[k] = (uint32_t)atomicAdd(&a.bump[2], (unsigned long long)units);
+            s_cap[k] = units * 2;
+            fill = true;
+        } else if (kind1 == K_ONE) {
+            if (is_list(kind0)) {
+                one = a.mem[(uint64_t)s_moff[k] * 2].x;
+            } else if (kind0 == K_ONE) {
+                const uint32_t mo = s_one[k];
+                if (q && N && bit_test(bm, mo)) find = true;
+                else one = (N && mo >= Lp) ? R[mo - Lp] : mo;
+                if (!find && one == DEL_MARK) find = true;
+            } else {
+                find = true;
+            }
+        }
+        s_one[k] = one;
+        const uint32_t fm = __ballot_sync(0xffffffffu, fill);
+        const uint32_t fd = __ballot_sync(0xffffffffu, find);
+        if (lane == 0) {
+            s_fill_mask = fm;
+            s_find_mask = fd;
+        }
+        // stats: transitions
+        uint32_t *vs = a.vstats + (uint64_t)t * VST;
+        if (lane < 25) vs[2 + lane] = 0;
+        __syncwarp();
+        if (kind0 != K_EMPTY || kind1 != K_EMPTY) atomicAdd(&vs[2 + 5 * kind0 + kind1], 1u);
+        if (lane == 0) {
+            vs[0] = N;
+            vs[1] = s_missing;
+        }
+    }
+    __syncthreads();
+    if (wid == 0 && (s_fill_mask | s_find_mask)) {
+        // one ascending pass over the post-batch adjacency materialises new lists
+        // (scan order = ascending index, R-2) and finds the unique member of ONE groups
+        const uint32_t fm = s_fill_mask, fd = s_find_mask;
+        uint32_t fillc = 0;     // lane k: entries written
+        uint32_t onev = s_one[lane];
+        for (uint32_t base = 0; base < dn; base += 32) {
+            const uint32_t i = base + lane;
+            uint2 e = make_uint2(0u, 0u);
+            if (i < dn) e = a.arc[aoff + i];
+            uint32_t mk = (fm | fd) & __reduce_or_sync(0xffffffffu, e.y);
+            while (mk) {
+                const int k = __ffs(mk) - 1;
+                mk &= mk - 1;
+                const uint32_t bal = __ballot_sync(0xffffffffu, (e.y >> k) & 1u);
+                if ((fd >> k) & 1u) {
+                    if (lane == (uint32_t)k) onev = base + __ffs(bal) - 1;
+                    continue;
+                }
+                const uint32_t start = __shfl_sync(0xffffffffu, fillc, k);
+                const uint32_t mo = s_moff[k];
+                if ((e.y >> k) & 1u) a.mem[(uint64_t)mo * 2 + start + __popc(bal & lanemask_lt())] = make_uint2(i, e.x);
+                if (lane == (uint32_t)k) fillc += __popc(bal);
+            }
+        }
+        s_one[lane] = onev;
+    }
+    __syncthreads();
+    if (wid == 0) {
+        const uint32_t k = lane;
+        const uint32_t kind1 = s_kind1[k];
+        const uint32_t cn = s_c[k];
+        uint32_t onedst = 0;
+        if (kind1 == K_ONE) onedst = a.arc[aoff + s_one[k]].x;
+        const uint32_t mask = __ballot_sync(0xffffffffu, cn != 0);
+        const uint32_t n = __popc(mask);
+        uint64_t Tp = cn ? ((uint64_t)cn << k) : 0ull;
+        const uint64_t T = warp_sum(Tp);
+        // bucket b <- group k_b
+        const uint32_t kb = (lane < n) ? (uint32_t)__fns(mask, 0, lane + 1) : 0u;
+        const uint32_t c_b = __shfl_sync(0xffffffffu, cn, kb);
+        const uint32_t kind_b = __shfl_sync(0xffffffffu, kind1, kb);
+        const uint32_t moff_b = __shfl_sync(0xffffffffu, s_moff[k], kb);
+        const uint32_t cap_b = __shfl_sync(0xffffffffu, s_cap[k], kb);
+        const uint32_t one_b = __shfl_sync(0xffffffffu, s_one[k], kb);
+        const uint32_t od_b = __shfl_sync(0xffffffffu, onedst, kb);
+        uint64_t thr;
+        uint32_t alias;
+        vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
+        Bucket B;
+        B.thr = thr;
+        B.c = c_b;
+        B.kk = make_kk(kb, kind_b);
+        B.ref = is_list(kind_b) ? moff_b : (kind_b == K_ONE ? od_b : 0u);
+        B.aux = is_list(kind_b) ? cap_b : (kind_b == K_ONE ? one_b : 0u);
+        B.alias = (uint8_t)alias;
+        B.pad = 0;
+        B.a_c = __shfl_sync(0xffffffffu, B.c, alias);
+        B.a_ref = __shfl_sync(0xffffffffu, B.ref, alias);
+        B.a_kk = (uint8_t)__shfl_sync(0xffffffffu, (uint32_t)B.kk, alias);
+        uint32_t bo = h.bkt_off, ncap = h.ncap;
+        if (n > h.ncap) {
+            // plan reserved bucket_capacity(popc(mask | inserted)) >= n
+            if (lane == 0) bo = (uint32_t)atomicAdd(&a.bump[1], (unsigned long long)bucket_capacity(n));
+            bo = __shfl_sync(0xffffffffu, bo, 0);
+            ncap = bucket_capacity(n);
+        }
+        if (lane < n) store_bucket(&a.bkt[(uint64_t)bo + lane], B);
+        if (lane == 0) {
+            VHdr nh;
+            nh.T = T;
+            nh.adj_off = aoff;
+            nh.bkt_off = bo;
+            nh.d = dn;
+            nh.n = (uint8_t)n;
+            nh.ncap = (uint8_t)ncap;
+            nh.pad = 0;
+            nh.adj_cap = s_adj_cap;
+            a.hdr[u] = nh;
+        }
+    }
+}
+
+__global__ void k_upd_stats(const uint32_t *__restrict__ vstats, uint32_t ntouch, unsigned long long *__restrict__ out) {
+    __shared__ unsigned long long acc[VST];
+    if (threadIdx.x < VST) acc[threadIdx.x] = 0;
+    __syncthreads();
+    unsigned long long loc[VST];
+    for (int j = 0; j < VST; j++) loc[j] = 0;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntouch; t += gridDim.x * blockDim.x)
+        for (int j = 0; j < 27; j++) loc[j] += vstats[(uint64_t)t * VST + j];
+    for (int j = 0; j < 27; j++) {
+        unsigned long long v = loc[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31u) == 0 && v) atomicAdd(&acc[j], v);
+    }
+    __syncthreads();
+    if (threadIdx.x < 27 && acc[threadIdx.x]) atomicAdd(&out[threadIdx.x], acc[threadIdx.x]);
+}
+
+}  // namespace bingo
+
+// ------------------------------------------------------------------ host side
+namespace {
+
+struct Carve {
+    char *base;
+    size_t pos;
+    template <typename T>
+    T *take(size_t count) {
+        pos = (pos + 255) & ~(size_t)255;
+        T *p = reinterpret_cast<T *>(base + pos);
+        pos += sizeof(T) * count;
+        return p;
+    }
+};
+
+size_t batch_scratch_bytes(uint64_t n) {
+    size_t b = 0;
+    auto add = [&](size_t x) { b = ((b + 255) & ~(size_t)255) + x; };
+    add(16 * n);                                   // recs copy
+    add(4 * n); add(4 * n); add(4 * n); add(4 * n); // keys/vals ping-pong
+    add(8 * radix_tmp_words(n));
+    add(8 * (n + 1)); add(8 * (n + 2));            // head, head_ex
+    add(8 * scan_tmp_words(n + 1));
+    add(4 * (n + 1)); add(4 * n);                  // seg, tv
+    add(8 * (n + 1)); add(8 * (n + 2));            // scr_need, scr_off
+    add(4 * VST * n);                              // vstats
+    add(sizeof(UpdCounters) + 8 * 32);             // counters, stats
+    return b + 4096;
+}
+
+bingo_status grow_pool(bingo_graph *g, int which, uint64_t need_total, cudaStream_t s) {
+    // which: 0 arcs, 1 buckets, 2 members (units)
+    if (which == 0) {
+        uint64_t cap = std::max<uint64_t>(need_total + need_total / 4, g->arc_cap + g->arc_cap / 4);
+        uint2 *na = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * cap);
+        uint32_t *ne = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * cap);
+        if (!na || !ne) { bingo_dev_free(g, na); bingo_dev_free(g, ne); return BINGO_E_NOMEM; }
+        if (cudaMemcpyAsync(na, g->arc, sizeof(uint2) * g->arc_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(ne, g->arc_epoch, 4 * g->arc_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return BINGO_E_CUDA;
+        bingo_dev_free(g, g->arc);
+        bingo_dev_free(g, g->arc_epoch);
+        g->arc = na; g->arc_epoch = ne; g->arc_cap = cap;
+    } else if (which == 1) {
+        uint64_t cap = std::min<uint64_t>(std::max<uint64_t>(need_total + need_total / 4, g->bkt_cap + g->bkt_cap / 4),
+                                          0xFFFFFFF0ull);
+        if (cap < need_total) return BINGO_E_NOMEM;
+        Bucket *nb = (Bucket *)bingo_dev_alloc(g, sizeof(Bucket) * cap);
+        if (!nb) return BINGO_E_NOMEM;
+        if (cudaMemcpyAsync(nb, g->bkt, sizeof(Bucket) * g->bkt_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return BINGO_E_CUDA;
+        bingo_dev_free(g, g->bkt);
+        g->bkt = nb; g->bkt_cap = cap;
+    } else {
+        uint64_t units = std::min<uint64_t>(std::max<uint64_t>(need_total + need_total / 4, g->mem_cap / 2 + g->mem_cap / 8),
+                                            0xFFFFFFF0ull);
+        if (units < need_total) return BINGO_E_NOMEM;
+        uint2 *nm = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * 2 * units);
+        if (!nm) return BINGO_E_NOMEM;
+        if (cudaMemcpyAsync(nm, g->mem, sizeof(uint2) * g->mem_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return BINGO_E_CUDA;
+        bingo_dev_free(g, g->mem);
+        g->mem = nm; g->mem_cap = 2 * units;
+    }
+    return BINGO_OK;
+}
+
+int key_bits_for(uint32_t V) {
+    int b = 0;
+    while (b < 32 && (V - 1) >> b) b++;
+    return b ? b : 1;
+}
+
+}  // namespace
+
+static bingo_status upd_cuda_fail(bingo_graph *g, cudaError_t e, const char *w) {
+    fprintf(stderr, "libbingo: CUDA error in %s: %s\n", w, cudaGetErrorString(e));
+    g->poisoned = 1;
+    return BINGO_E_CUDA;
+}
+#define UCK(call)                                                   \
+    do {                                                            \
+        cudaError_t e_ = (call);                                    \
+        if (e_ != cudaSuccess) return upd_cuda_fail(g, e_, #call);  \
+    } while (0)
+
 extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
                                             bingo_update_stats *stats, void *stream) {
-    (void)batch; (void)n; (void)flags; (void)stats; (void)stream;
     if (!g) return BINGO_E_INVAL;
-    return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    if (n && !batch) return BINGO_E_INVAL;
+    if (n >= 0xFFFFFFFFull) return BINGO_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (n == 0) {
+        g->epoch++;
+        if (stats) stats->epoch = g->epoch;
+        return BINGO_OK;
+    }
+    // ---- scratch
+    const size_t need = batch_scratch_bytes(n);
+    if (g->scratch_bytes < need) {
+        bingo_dev_free(g, g->scratch);
+        g->scratch = bingo_dev_alloc(g, need);
+        g->scratch_bytes = g->scratch ? need : 0;
+        if (!g->scratch) return BINGO_E_NOMEM;
+    }
+    const size_t hneed = sizeof(UpdCounters) + 8 * 32;
+    if (g->hscratch_bytes < hneed) {
+        if (g->hscratch) cudaFreeHost(g->hscratch);
+        g->hscratch = nullptr;
+        g->hscratch_bytes = 0;
+        UCK(cudaMallocHost(&g->hscratch, hneed));
+        g->hscratch_bytes = hneed;
+    }
+    Carve cv{(char *)g->scratch, 0};
+    uint4 *drec = cv.take<uint4>(n);
+    uint32_t *k0 = cv.take<uint32_t>(n), *v0 = cv.take<uint32_t>(n), *k1 = cv.take<uint32_t>(n),
+             *v1 = cv.take<uint32_t>(n);
+    uint64_t *rtmp = cv.take<uint64_t>(radix_tmp_words(n));
+    uint64_t *head = cv.take<uint64_t>(n + 1), *head_ex = cv.take<uint64_t>(n + 2);
+    uint64_t *stmp = cv.take<uint64_t>(scan_tmp_words(n + 1));
+    uint32_t *seg = cv.take<uint32_t>(n + 1), *tv = cv.take<uint32_t>(n);
+    uint64_t *scr_need = cv.take<uint64_t>(n + 1), *scr_off = cv.take<uint64_t>(n + 2);
+    uint32_t *vstats = cv.take<uint32_t>((size_t)VST * n);
+    UpdCounters *dc = cv.take<UpdCounters>(1);
+    unsigned long long *dstats = cv.take<unsigned long long>(32);
+
+    const uint4 *recs = reinterpret_cast<const uint4 *>(batch);
+    if (flags & BINGO_UPD_HOST_BATCH) {
+        UCK(cudaMemcpyAsync(drec, batch, 16 * n, cudaMemcpyHostToDevice, s));
+        recs = drec;
+    }
+    UCK(cudaMemsetAsync(dc, 0, sizeof(UpdCounters), s));
+    UCK(cudaMemsetAsync(dstats, 0, 8 * 32, s));
+    const unsigned gb = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    k_upd_validate<<<gb, 256, 0, s>>>(recs, n, g->V, k0, v0, dc);
+    UCK(cudaGetLastError());
+    bool in1 = false;
+    UCK(radix_sort_pairs(k0, v0, k1, v1, n, key_bits_for(g->V), rtmp, s, &in1));
+    const uint32_t *sk = in1 ? k1 : k0;
+    const uint32_t *sv = in1 ? v1 : v0;
+    k_upd_heads<<<gb, 256, 0, s>>>(sk, n, head);
+    UCK(cudaGetLastError());
+    UCK(exclusive_scan_u64(head, head_ex, n, stmp, s));   // head_ex[n] = #touched
+    k_upd_segments<<<gb, 256, 0, s>>>(head_ex, sk, n, seg, tv);
+    UCK(cudaGetLastError());
+    uint64_t ntouch = 0;
+    UCK(cudaMemcpyAsync(&ntouch, head_ex + n, 8, cudaMemcpyDeviceToHost, s));
+    UCK(cudaStreamSynchronize(s));
+    const bool bs = (g->flags & BINGO_BUILD_BS_MODE) != 0;
+    const unsigned gp = (unsigned)std::min<uint64_t>((ntouch + 7) / 8, 148 * 32);
+    k_upd_plan<<<gp ? gp : 1, 256, 0, s>>>(recs, sv, seg, tv, (uint32_t)ntouch, g->hdr, g->bkt, g->alpha, bs,
+                                          g->arc_slack, g->member_slack, scr_need, dc);
+    UCK(cudaGetLastError());
+    UCK(exclusive_scan_u64(scr_need, scr_off, ntouch, stmp, s));
+    UpdCounters hc;
+    unsigned long long bump[3];
+    uint64_t scr_total = 0;
+    UCK(cudaMemcpyAsync(&hc, dc, sizeof(hc), cudaMemcpyDeviceToHost, s));
+    UCK(cudaMemcpyAsync(bump, g->counters, sizeof(bump), cudaMemcpyDeviceToHost, s));
+    UCK(cudaMemcpyAsync(&scr_total, scr_off + ntouch, 8, cudaMemcpyDeviceToHost, s));
+    UCK(cudaStreamSynchronize(s));
+    if (hc.flag & 1) return BINGO_E_INVAL;
+    if (hc.flag & 4) return BINGO_E_OVERFLOW;
+    // ---- capacity (grow pools before any mutation; NOMEM leaves the graph untouched)
+    bingo_status st;
+    if (bump[0] + hc.need_arc > g->arc_cap && (st = grow_pool(g, 0, bump[0] + hc.need_arc, s)) != BINGO_OK)
+        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
+    if (bump[1] + hc.need_bkt > g->bkt_cap && (st = grow_pool(g, 1, bump[1] + hc.need_bkt, s)) != BINGO_OK)
+        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
+    const uint64_t mem_units_need = bump[2] + hc.need_mem + hc.reserve_mem;
+    if (mem_units_need > g->mem_cap / 2 && (st = grow_pool(g, 2, mem_units_need, s)) != BINGO_OK)
+        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
+    // per-vertex delete scratch
+    uint32_t *vscr = nullptr;
+    const size_t vbytes = 4 * (scr_total + 64);
+    if (scr_total) {
+        if (g->vscratch_bytes < vbytes) {
+            bingo_dev_free(g, g->vscratch);
+            g->vscratch = bingo_dev_alloc(g, vbytes);
+            g->vscratch_bytes = g->vscratch ? vbytes : 0;
+            if (!g->vscratch) return BINGO_E_NOMEM;
+        }
+        vscr = (uint32_t *)g->vscratch;
+    }
+    // ---- mutate (from here on the batch is applied)
+    const uint32_t e = g->epoch + 1;
+    MutateArgs ma;
+    ma.recs = recs;
+    ma.sval = sv;
+    ma.seg = seg;
+    ma.tv = tv;
+    ma.scr_off = scr_off;
+    ma.scr = vscr;
+    ma.hdr = g->hdr;
+    ma.arc = g->arc;
+    ma.arc_epoch = g->arc_epoch;
+    ma.bkt = g->bkt;
+    ma.mem = g->mem;
+    ma.bump = g->counters;
+    ma.vstats = vstats;
+    ma.epoch = e;
+    ma.alpha = g->alpha;
+    ma.beta = g->beta;
+    ma.bs = bs;
+    ma.arc_slack = g->arc_slack;
+    ma.mem_slack = g->member_slack;
+    if (ntouch) {
+        k_upd_mutate<<<(unsigned)ntouch, MT, 0, s>>>(ma);
+        UCK(cudaGetLastError());
+        k_upd_stats<<<(unsigned)std::min<uint64_t>((ntouch + 255) / 256, 148), 256, 0, s>>>(vstats, (uint32_t)ntouch,
+                                                                                            dstats);
+        UCK(cudaGetLastError());
+    }
+    unsigned long long hs[32];
+    UCK(cudaMemcpyAsync(hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    UCK(cudaStreamSynchronize(s));
+    g->epoch = e;
+    // inserted = number of insert records (validated batch)
+    uint64_t inserted = 0;
+    {
+        // count inserts on the host side cheaply from the stats: deleted + missing = #delete records
+        const uint64_t dels = hs[0] + hs[1];
+        inserted = n - dels;
+    }
+    g->num_arcs = g->num_arcs + inserted - hs[0];
+    if (stats) {
+        stats->inserted = inserted;
+        stats->deleted = hs[0];
+        stats->missing_deletes = hs[1];
+        stats->touched_vertices = ntouch;
+        for (int i = 0; i < 25; i++) stats->kind_transitions[i / 5][i % 5] = hs[2 + i];
+        stats->epoch = e;
+    }
+    return BINGO_OK;
 }

@@ -1,0 +1,176 @@
+"""-m gpu: batched insert/delete on the device vs the CPU oracle, bit-exact after every batch
+(canonical dumps, digests, statistics), plus walks on the updated structures."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.conftest import gpu_available
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not gpu_available(), reason="needs a CUDA device")]
+
+
+def _pb():
+    import paper_2504_10233_b200 as pb
+    return pb
+
+
+def u32(t):
+    return t.cpu().numpy().view(np.uint32)
+
+
+def _pair(ro, dst, bias, bs_mode=False, **kw):
+    pb = _pb()
+    g = pb.Graph(ro, dst, bias, bs_mode=bs_mode, **kw)
+    o = oracle.OracleGraph(ro, dst, bias, flags=oracle.FLAG_BS_MODE if bs_mode else 0)
+    return g, o
+
+
+def _same(g, o, V, ctx=""):
+    a, b = g.export(), o.dump()
+    if a != b:
+        pa, pb_ = oracle.parse_dump(a, V), oracle.parse_dump(b, V)
+        for u in range(V):
+            assert pa[u] == pb_[u], f"{ctx} vertex {u}:\n gpu    {pa[u]}\n oracle {pb_[u]}"
+    assert a == b
+    assert np.array_equal(g.digests().cpu().numpy().view(np.uint64), o.digests())
+
+
+def _same_stats(sg, so):
+    for k in ("inserted", "deleted", "missing_deletes", "touched_vertices", "epoch"):
+        assert sg[k] == so[k], (k, sg[k], so[k])
+    assert np.array_equal(sg["kind_transitions"], so["kind_transitions"])
+
+
+def test_paper_examples_bs_mode():
+    """P:317 insertion then P:336 deletion on the running example, explicit lists (BS mode)."""
+    ro = np.array([0, 0, 0, 3, 3, 3, 3], dtype=np.uint64)
+    g, o = _pair(ro, [1, 4, 5], [5, 4, 3], bs_mode=True)
+    for batch in ([[0, 2, 3, 3]], [[1, 2, 1, 0]]):
+        _same_stats(g.apply_updates(np.array(batch, dtype=np.uint32)), o.apply_updates(batch))
+        _same(g, o, 6)
+
+
+def test_c1_stream_batches():
+    w = synth.make_workload("c1", rounds=4)
+    g, o = _pair(w.row_offsets, w.dst, w.bias)
+    for i, b in enumerate(w.batches):
+        _same_stats(g.apply_updates(b), o.apply_updates(b))
+        _same(g, o, w.V, f"batch {i}")
+        out = g.walk(length=80, seed=100 + i)
+        ref = o.walk(length=80, seed=100 + i)
+        assert np.array_equal(u32(out["paths"]), ref["paths"])
+
+
+def _bias_of(u, v, e, hi):
+    return 1 + ((u * 2654435761 + v * 40503 + e * 97) % hi)
+
+
+@pytest.mark.parametrize("seed,bs_mode,hi", [(0, False, 200), (1, False, 1 << 20), (2, True, 200),
+                                             (3, False, 7), (4, False, 255), (5, True, 1 << 31)])
+def test_random_multigraph_batches(seed, bs_mode, hi):
+    """Random multigraphs with duplicates, hubs (multi-chunk scans), missing deletes, repeated
+    deletes of one pair, mixed biases forcing kind transitions in every direction."""
+    rng = np.random.default_rng(1000 + seed)
+    V = int(rng.integers(5, 60))
+    deg = rng.integers(0, 30, size=V)
+    deg[0] = 700                               # a hub spanning many 32-arc chunks
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, V, size=A).astype(np.uint32)
+    src = np.repeat(np.arange(V), deg)
+    bias = np.array([_bias_of(int(s), int(d), 0, hi) for s, d in zip(src, dst)], dtype=np.uint32)
+    g, o = _pair(ro, dst, bias, bs_mode=bs_mode, arc_slack=0.0, member_slack=0.0, pool_reserve=0.0)
+    live = {u: list(dst[int(ro[u]):int(ro[u + 1])]) for u in range(V)}
+    for e in range(1, 13):
+        n = int(rng.integers(0, 400))
+        recs = np.zeros((n, 4), dtype=np.uint32)
+        for i in range(n):
+            u = 0 if rng.random() < 0.3 else int(rng.integers(0, V))
+            if rng.random() < 0.5:
+                if live[u] and rng.random() < 0.85:
+                    v = int(live[u][int(rng.integers(0, len(live[u])))])
+                else:
+                    v = int(rng.integers(0, V))
+                recs[i] = (1, u, v, 0)
+            else:
+                v = int(rng.integers(0, V))
+                recs[i] = (0, u, v, _bias_of(u, v, e, hi) if rng.random() < 0.7 else int(rng.integers(1, hi + 1)))
+                live[u].append(v)
+        _same_stats(g.apply_updates(recs), o.apply_updates(recs))
+        _same(g, o, V, f"seed {seed} batch {e}")
+        d = oracle.parse_dump(o.dump(), V)
+        live = {u: [a[0] for a in d[u]["adj"]] for u in range(V)}
+    out = g.walk(length=30, seed=5)
+    ref = o.walk(length=30, seed=5)
+    assert np.array_equal(u32(out["paths"]), ref["paths"])
+
+
+def test_delete_everything_and_regrow():
+    rng = np.random.default_rng(7)
+    ro, dst, bias = synth.random_small_graph(rng, 20, 40, 1000)
+    g, o = _pair(ro, dst, bias)
+    recs = []
+    for u in range(20):
+        for i in range(int(ro[u]), int(ro[u + 1])):
+            recs.append((1, u, int(dst[i]), 0))
+    recs = np.array(recs, dtype=np.uint32)
+    _same_stats(g.apply_updates(recs), o.apply_updates(recs))
+    _same(g, o, 20, "all deleted")
+    ins = np.array([(0, u, (u * 7 + j) % 20, 1 + (u * 31 + j) % 900) for u in range(20) for j in range(25)], dtype=np.uint32)
+    _same_stats(g.apply_updates(ins), o.apply_updates(ins))
+    _same(g, o, 20, "regrown")
+
+
+def test_invalid_batch_and_empty_batch():
+    pb = _pb()
+    w = synth.make_workload("c1")
+    g, o = _pair(w.row_offsets, w.dst, w.bias)
+    before = g.export()
+    for bad in ([[0, 0, w.V, 1]], [[0, w.V, 0, 1]], [[0, 1, 2, 0]], [[3, 1, 2, 3]]):
+        assert g.try_apply_updates(np.array(bad, dtype=np.uint32)) == pb.bingo.E_INVAL
+        assert g.export() == before
+    st = g.apply_updates(np.zeros((0, 4), dtype=np.uint32))
+    assert st["epoch"] == 1 and st["touched_vertices"] == 0
+    o.apply_updates(np.zeros((0, 4), dtype=np.uint32))
+    b = w.batches[0]
+    _same_stats(g.apply_updates(b), o.apply_updates(b))
+    _same(g, o, w.V)
+
+
+def test_device_batch_equals_host_batch():
+    import torch
+    w = synth.make_workload("c1", rounds=2)
+    g1, o = _pair(w.row_offsets, w.dst, w.bias)
+    g2, _ = _pair(w.row_offsets, w.dst, w.bias)
+    for b in w.batches:
+        g1.apply_updates(b)
+        g2.apply_updates(torch.from_numpy(b.view(np.int32)).cuda())
+        o.apply_updates(b)
+    assert g1.export() == g2.export() == o.dump()
+
+
+def test_streaming_single_records():
+    """a11: the same stream applied one record per call (streaming updates, S4.2)."""
+    w = synth.make_workload("c1")
+    g, o = _pair(w.row_offsets, w.dst, w.bias)
+    for r in w.batches[0][:300]:
+        _same_stats(g.apply_updates(r[None, :]), o.apply_updates(r[None, :]))
+    _same(g, o, w.V)
+
+
+def test_larger_graph_batches_digests():
+    """scale-16 R-MAT, unclamped degree biases, 3 batches of 20K arc records: per-vertex
+    digests after each batch, then sampled walks."""
+    w = synth.Workload(16, 600_000, compact=True, batch=10_000, rounds=3)
+    g, o = _pair(w.row_offsets, w.dst, w.bias)
+    for b in w.batches:
+        _same_stats(g.apply_updates(b), o.apply_updates(b))
+        assert np.array_equal(g.digests().cpu().numpy().view(np.uint64), o.digests())
+    starts = (np.arange(50_000, dtype=np.uint64) * 2654435761 % w.V).astype(np.uint32)
+    out = g.walk(length=80, seed=3, starts=starts)
+    ref = o.walk(length=80, seed=3, starts=starts)
+    assert np.array_equal(u32(out["paths"]), ref["paths"])
