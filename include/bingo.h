@@ -215,8 +215,20 @@ typedef struct {
     uint64_t bucket_pool_used, bucket_pool_cap; /* 32 B buckets */
     uint64_t member_pool_used, member_pool_cap; /* 8 B entries */
     uint64_t device_bytes;
+    uint64_t kernel_launches;  /* process-wide count of libbingo kernel launches so far */
 } bingo_info;
 bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *stream);
+
+/* bingo_walk_profile: bingo_walk (DEVICE buffers only) that also counts, into
+ * counters_host[8] (HOST u64), the records every walker step loaded:
+ * [0] steps taken, [1] vertex headers, [2] alias buckets, [3] group members,
+ * [4] adjacency arcs (dense attempts), [5] node2vec probe sectors, [6] PPR
+ * visit-count increments, [7] walkers.  Same walks as bingo_walk (bit for
+ * bit).  Used to compute the algorithmic bytes behind the roofline.
+ * Synchronises `stream`. */
+bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts_or_null,
+                                uint32_t num_walkers, uint32_t *paths_or_null, uint32_t *lengths_or_null,
+                                uint64_t *counters_host, void *stream);
 
 const char *bingo_status_str(bingo_status s);
 

@@ -28,7 +28,7 @@ NO_CAP = 0xFFFFFFFF
 
 # every symbol include/bingo.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("bingo_build", "bingo_destroy", "bingo_apply_updates", "bingo_walk", "bingo_visit_counts",
-               "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str")
+               "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str", "bingo_walk_profile")
 
 
 class BingoError(RuntimeError):
@@ -68,7 +68,7 @@ class Info(ctypes.Structure):
                 ("arc_pool_used", ctypes.c_uint64), ("arc_pool_cap", ctypes.c_uint64),
                 ("bucket_pool_used", ctypes.c_uint64), ("bucket_pool_cap", ctypes.c_uint64),
                 ("member_pool_used", ctypes.c_uint64), ("member_pool_cap", ctypes.c_uint64),
-                ("device_bytes", ctypes.c_uint64)]
+                ("device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64)]
 
 
 _LIB = None
@@ -99,6 +99,8 @@ def _lib():
         L.bingo_digests.restype = ctypes.c_int
         L.bingo_get_info.argtypes = [P, ctypes.POINTER(Info), P]
         L.bingo_get_info.restype = ctypes.c_int
+        L.bingo_walk_profile.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, P, P]
+        L.bingo_walk_profile.restype = ctypes.c_int
         L.bingo_status_str.argtypes = [ctypes.c_int]
         L.bingo_status_str.restype = ctypes.c_char_p
         _LIB = L
@@ -286,6 +288,28 @@ class Graph:
             _check(_lib().bingo_walk(self._h, ctypes.byref(d), ptr(starts), W, ptr(paths), ptr(lengths),
                                      _stream_ptr(stream)), "bingo_walk")
         return {"paths": paths, "lengths": lengths}
+
+    def walk_profile(self, app: int = DEEPWALK, length: int = 80, seed: int = 0, first_walker: int = 0, starts=None,
+                     num_walkers: Optional[int] = None, p: float = 1.0, q: float = 1.0, stop=(1, 80), paths=True,
+                     stream=None) -> dict:
+        """bingo_walk that also counts the records each step loaded (see bingo.h)."""
+        torch = _torch()
+        W = num_walkers if num_walkers is not None else (len(starts) if starts is not None else self.V)
+        st = _dev_u32(starts, torch, self.device) if starts is not None else None
+        pa = torch.empty((length + 1, W), dtype=torch.int32, device=self.device) if paths else None
+        ln = torch.empty(W, dtype=torch.int32, device=self.device)
+        d = WalkDesc(app=app, length=length, p=p, q=q, stop_num=stop[0], stop_den=stop[1], seed=seed,
+                     first_walker_id=first_walker, flags=0)
+        c = np.zeros(8, dtype=np.uint64)
+        with torch.cuda.device(self.device):
+            _check(_lib().bingo_walk_profile(self._h, ctypes.byref(d), st.data_ptr() if st is not None else None, W,
+                                             pa.data_ptr() if pa is not None else None, ln.data_ptr(), c.ctypes.data,
+                                             _stream_ptr(stream)), "bingo_walk_profile")
+        names = ("steps", "hdr", "bkt", "mem", "arc", "probe", "visit", "walkers")
+        out = {k: int(v) for k, v in zip(names, c)}
+        out["paths"] = pa
+        out["lengths"] = ln
+        return out
 
     def visit_counts(self, reset: bool = False, stream=None):
         torch = _torch()

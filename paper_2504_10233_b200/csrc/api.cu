@@ -9,6 +9,10 @@
 
 using namespace bingo;
 
+#include <atomic>
+static std::atomic<unsigned long long> g_launch_count{0};
+void bingo_count_launch(unsigned n) { g_launch_count += n; }
+
 void *bingo_dev_alloc(bingo_graph *g, size_t bytes) {
     if (bytes == 0) bytes = 16;
     if (g && g->alloc) return g->alloc(bytes, g->alloc_ctx);
@@ -66,6 +70,7 @@ extern "C" bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *s
     info->bucket_pool_cap = g->bkt_cap;
     info->member_pool_used = 2 * c[2];
     info->member_pool_cap = g->mem_cap;
+    info->kernel_launches = g_launch_count.load();
     info->device_bytes = sizeof(VHdr) * (uint64_t)g->V + (sizeof(uint2) + 4) * g->arc_cap +
                          sizeof(Bucket) * g->bkt_cap + sizeof(uint2) * g->mem_cap + 8ull * g->V +
                          g->scratch_bytes + g->wscratch_bytes + g->vscratch_bytes;
@@ -193,6 +198,7 @@ extern "C" bingo_status bingo_digests(bingo_graph *g, uint64_t *digests, void *s
     cudaStream_t s = (cudaStream_t)stream;
     unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)g->V + 255) / 256, 148ull * 16);
     k_digests<<<blocks, 256, 0, s>>>(g->V, g->hdr, g->arc, g->arc_epoch, g->bkt, g->mem, digests);
+    bingo_count_launch();
     if (cudaGetLastError() != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     return BINGO_OK;
 }

@@ -144,6 +144,9 @@ struct bingo_graph {
     size_t vscratch_bytes = 0;
 };
 
+// process-wide count of kernel launches issued by libbingo (api.cu)
+void bingo_count_launch(unsigned n = 1);
+
 // allocation helpers (api.cu)
 void *bingo_dev_alloc(bingo_graph *g, size_t bytes);
 void bingo_dev_free(bingo_graph *g, void *p);

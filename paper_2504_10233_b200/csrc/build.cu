@@ -249,6 +249,7 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
         k_build_sizes<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
                                              g->arc_slack, g->member_slack, sz, sz + (nV + 1), sz + 2 * (nV + 1),
                                              g->dev_flag);
+        bingo_count_launch();
         CK(cudaGetLastError());
         for (int p = 0; p < 3; p++) CK(exclusive_scan_u64(sz + p * (nV + 1), off + p * (nV + 1), nV, tmp, s));
         CK(cudaMemcpyAsync(&hflag, g->dev_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -276,6 +277,7 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
         k_build_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
                                             g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), g->hdr, g->arc,
                                             g->arc_epoch, g->bkt, g->mem);
+        bingo_count_launch();
         CK(cudaGetLastError());
     }
     CK(cudaStreamSynchronize(s));

@@ -1,6 +1,7 @@
 // scan.cu -- three-phase exclusive scan over u64 (tile reduce, scan of tile
 // sums, tile scan + carry).  Tiles of 2048 elements (256 threads x 8).
 #include "scan.cuh"
+#include "bingo_internal.cuh"
 
 namespace bingo {
 
@@ -85,15 +86,18 @@ cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, ui
     uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (tiles == 1) {
         k_tile_scan<<<1, SCAN_THREADS, 0, s>>>(in, out, n, nullptr);
+        bingo_count_launch();
         return cudaGetLastError();
     }
     uint64_t *sums = tmp;               // [tiles]
     uint64_t *sums_scan = tmp + tiles + 1; // [tiles + 1]
     uint64_t *rest = sums_scan + tiles + 1;
     k_tile_reduce<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, sums);
+    bingo_count_launch();
     cudaError_t e = exclusive_scan_u64(sums, sums_scan, tiles, rest, s);
     if (e != cudaSuccess) return e;
     k_tile_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, sums_scan);
+    bingo_count_launch();
     return cudaGetLastError();
 }
 

@@ -9,6 +9,7 @@
 // processed round-major (item = base + r * 256 + thread) so rank order is
 // input order.
 #include "scan.cuh"
+#include "bingo_internal.cuh"
 #include "sort.cuh"
 
 namespace bingo {
@@ -98,9 +99,11 @@ cudaError_t radix_sort_pairs(uint32_t *k0, uint32_t *v0, uint32_t *k1, uint32_t 
     uint32_t *ki = k0, *vi = v0, *ko = k1, *vo = v1;
     for (int shift = 0; shift < key_bits; shift += 8) {
         k_radix_hist<<<tiles, RT, 0, s>>>(ki, n, shift, hist, tiles);
+        bingo_count_launch();
         cudaError_t e = exclusive_scan_u64(hist, off, 256ull * tiles, stmp, s);
         if (e != cudaSuccess) return e;
         k_radix_scatter<<<tiles, RT, 0, s>>>(ki, vi, ko, vo, n, shift, off, tiles);
+        bingo_count_launch();
         e = cudaGetLastError();
         if (e != cudaSuccess) return e;
         uint32_t *t = ki; ki = ko; ko = t;

@@ -849,15 +849,18 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     UCK(cudaMemsetAsync(dstats, 0, 8 * 32, s));
     const unsigned gb = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
     k_upd_validate<<<gb, 256, 0, s>>>(recs, n, g->V, k0, v0, dc);
+    bingo_count_launch();
     UCK(cudaGetLastError());
     bool in1 = false;
     UCK(radix_sort_pairs(k0, v0, k1, v1, n, key_bits_for(g->V), rtmp, s, &in1));
     const uint32_t *sk = in1 ? k1 : k0;
     const uint32_t *sv = in1 ? v1 : v0;
     k_upd_heads<<<gb, 256, 0, s>>>(sk, n, head);
+    bingo_count_launch();
     UCK(cudaGetLastError());
     UCK(exclusive_scan_u64(head, head_ex, n, stmp, s));   // head_ex[n] = #touched
     k_upd_segments<<<gb, 256, 0, s>>>(head_ex, sk, n, seg, tv);
+    bingo_count_launch();
     UCK(cudaGetLastError());
     uint64_t ntouch = 0;
     UCK(cudaMemcpyAsync(&ntouch, head_ex + n, 8, cudaMemcpyDeviceToHost, s));
@@ -866,6 +869,7 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     const unsigned gp = (unsigned)std::min<uint64_t>((ntouch + 7) / 8, 148 * 32);
     k_upd_plan<<<gp ? gp : 1, 256, 0, s>>>(recs, sv, seg, tv, (uint32_t)ntouch, g->hdr, g->bkt, g->alpha, bs,
                                           g->arc_slack, g->member_slack, scr_need, dc);
+    bingo_count_launch();
     UCK(cudaGetLastError());
     UCK(exclusive_scan_u64(scr_need, scr_off, ntouch, stmp, s));
     UpdCounters hc;
@@ -922,9 +926,11 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     ma.mem_slack = g->member_slack;
     if (ntouch) {
         k_upd_mutate<<<(unsigned)ntouch, MT, 0, s>>>(ma);
+        bingo_count_launch();
         UCK(cudaGetLastError());
         k_upd_stats<<<(unsigned)std::min<uint64_t>((ntouch + 255) / 256, 148), 256, 0, s>>>(vstats, (uint32_t)ntouch,
                                                                                             dstats);
+        bingo_count_launch();
         UCK(cudaGetLastError());
     }
     unsigned long long hs[32];

@@ -18,9 +18,10 @@ using namespace bingo;
 
 namespace bingo {
 
-template <int APP>
+template <int APP, bool PROF>
 __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
     const uint32_t stride = gridDim.x * blockDim.x;
+    WalkProf prof;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += stride) {
         const uint32_t w = a.first_walker + i;
         uint32_t u = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);
@@ -29,35 +30,40 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
         uint32_t steps = 0, prev = 0xFFFFFFFFu;
         for (uint32_t t = 0; a.L == BINGO_NO_CAP || t < a.L; t++) {
             const VHdr h = load_hdr(a.hdr + u);
+            if (PROF) prof.hdr++;
             if (h.d == 0) break;   // dead end: truncate (R-13)
             uint32_t next;
             if (APP == BINGO_NODE2VEC && t >= 1) {
                 // KnightKing rejection: propose first-order, accept with f/f_max
                 for (uint32_t o = 0;; o++) {
-                    next = sample_dst(a, h, w, t, o);
-                    const uint32_t cls = (next == prev) ? 0u : (probe_arc(a, prev, next) ? 1u : 2u);
+                    next = sample_dst<PROF>(a, h, w, t, o, prof);
+                    const uint32_t cls = (next == prev) ? 0u : (probe_arc<PROF>(a, prev, next, prof) ? 1u : 2u);
                     if (a.n2v_always[cls]) break;
                     const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
                     if (join64(r.x, r.y) < a.n2v_thr[cls]) break;
                 }
             } else {
-                next = sample_dst(a, h, w, t, 0);
+                next = sample_dst<PROF>(a, h, w, t, 0, prof);
             }
             steps++;
+            if (PROF) prof.steps++;
             if (a.paths) __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
             prev = u;
             u = next;
             if (APP == BINGO_PPR) {
                 if (a.visit) atomicAdd(&a.visit[u], 1ull);
+                if (PROF) prof.visit++;
                 if (a.stop_always) break;
                 const P4 r = philox10(w, t, 0u, 3u, a.k0, a.k1);
                 if (join64(r.x, r.y) < a.stop_thr) break;
             }
         }
+        if (PROF) prof.walkers++;
         if (a.lengths) a.lengths[i] = steps;
         if (a.paths && a.L != BINGO_NO_CAP)
             for (uint32_t t = steps + 1; t <= a.L; t++) __stcs(&a.paths[(size_t)t * a.W + i], 0xFFFFFFFFu);
     }
+    if (PROF) prof.flush(a.prof);
 }
 
 }  // namespace bingo
@@ -97,7 +103,7 @@ static size_t walk_grid(uint32_t W) {
 }
 
 bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts, uint32_t W,
-                         uint32_t *paths, uint32_t *lengths, cudaStream_t s) {
+                         uint32_t *paths, uint32_t *lengths, cudaStream_t s, unsigned long long *prof = nullptr) {
     WalkArgs a;
     a.hdr = g->hdr;
     a.bkt = g->bkt;
@@ -116,13 +122,24 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     n2v_thresholds(desc->app == BINGO_NODE2VEC ? desc->p : 1.0, desc->app == BINGO_NODE2VEC ? desc->q : 1.0,
                    a.n2v_thr, a.n2v_always);
     stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
+    a.prof = prof;
     const unsigned grid = (unsigned)walk_grid(W);
-    switch (desc->app) {
-        case BINGO_DEEPWALK: k_walk<BINGO_DEEPWALK><<<grid, 256, 0, s>>>(a); break;
-        case BINGO_NODE2VEC: k_walk<BINGO_NODE2VEC><<<grid, 256, 0, s>>>(a); break;
-        case BINGO_PPR: k_walk<BINGO_PPR><<<grid, 256, 0, s>>>(a); break;
-        default: return BINGO_E_INVAL;
+    if (prof) {
+        switch (desc->app) {
+            case BINGO_DEEPWALK: k_walk<BINGO_DEEPWALK, true><<<grid, 256, 0, s>>>(a); break;
+            case BINGO_NODE2VEC: k_walk<BINGO_NODE2VEC, true><<<grid, 256, 0, s>>>(a); break;
+            case BINGO_PPR: k_walk<BINGO_PPR, true><<<grid, 256, 0, s>>>(a); break;
+            default: return BINGO_E_INVAL;
+        }
+    } else {
+        switch (desc->app) {
+            case BINGO_DEEPWALK: k_walk<BINGO_DEEPWALK, false><<<grid, 256, 0, s>>>(a); break;
+            case BINGO_NODE2VEC: k_walk<BINGO_NODE2VEC, false><<<grid, 256, 0, s>>>(a); break;
+            case BINGO_PPR: k_walk<BINGO_PPR, false><<<grid, 256, 0, s>>>(a); break;
+            default: return BINGO_E_INVAL;
+        }
     }
+    bingo_count_launch();
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fprintf(stderr, "libbingo: walk launch failed: %s\n", cudaGetErrorString(e));
@@ -179,6 +196,31 @@ extern "C" bingo_status bingo_walk(bingo_graph *g, const bingo_walk_desc *desc, 
         return BINGO_E_CUDA;
     }
     return BINGO_OK;
+}
+
+extern "C" bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts_or_null,
+                                           uint32_t num_walkers, uint32_t *paths_or_null, uint32_t *lengths_or_null,
+                                           uint64_t *counters_host, void *stream) {
+    if (!g || !desc || !counters_host) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    if (desc->app > BINGO_PPR || (desc->flags & BINGO_WALK_HOST_OUTPUT)) return BINGO_E_INVAL;
+    if (desc->app == BINGO_NODE2VEC && !(desc->p > 0 && desc->q > 0)) return BINGO_E_INVAL;
+    if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
+    if (desc->length == BINGO_NO_CAP && (paths_or_null || desc->app != BINGO_PPR)) return BINGO_E_INVAL;
+    if (g->V == 0) return BINGO_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *dprof = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * BINGO_PROF_N);
+    if (!dprof) return BINGO_E_NOMEM;
+    cudaError_t e = cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * BINGO_PROF_N, s);
+    bingo_status st = BINGO_OK;
+    if (e == cudaSuccess)
+        st = launch_walk(g, desc, starts_or_null, num_walkers, paths_or_null, lengths_or_null, s, dprof);
+    if (st == BINGO_OK && e == cudaSuccess)
+        e = cudaMemcpyAsync(counters_host, dprof, sizeof(unsigned long long) * BINGO_PROF_N, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    bingo_dev_free(g, dprof);
+    if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
+    return st;
 }
 
 extern "C" bingo_status bingo_visit_counts(bingo_graph *g, uint64_t *counts, int reset, uint32_t flags, void *stream) {
