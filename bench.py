@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-walkers", type=int, default=1 << 18)
+    ap.add_argument("--layout", default="walker", choices=["walker", "step"],
+                    help="path layout written by the walk (walker-major: one contiguous walk per walker)")
     return ap.parse_args()
 
 
@@ -221,7 +223,8 @@ def main():
     # inputs resident in HBM before the timed region (rank 0 holds the stream; others receive it)
     dev_batches = [b.to(dev) for b in batches[:W + K]]
     first = rank * V            # weak scaling: every rank walks one walker per vertex
-    paths = torch.empty((L + 1, V), dtype=torch.int32, device=dev)
+    wmajor = args.layout == "walker"
+    paths = torch.empty((V, L + 1) if wmajor else (L + 1, V), dtype=torch.int32, device=dev)
     lens = [torch.empty(V, dtype=torch.int32, device=dev) for _ in range(K)]
     scratch_len = torch.empty(V, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
@@ -236,7 +239,7 @@ def main():
         if ev is not None:
             ev[1].record(stream)
         g.walk(app=pb.DEEPWALK, length=L, seed=1000 + i, first_walker=first, num_walkers=V, paths=paths,
-               lengths=out_len)
+               lengths=out_len, walker_major=wmajor)
         if ev is not None:
             ev[2].record(stream)
 
@@ -336,7 +339,8 @@ def main():
             "value": value, "unit": "steps/s", "n_gpus": ws, "steps": K, "warmup": W,
             "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": config_block(args, w, {"parallelism": f"replicated graph x{ws}, walkers sharded by id"}),
+            "config": config_block(args, w, {"parallelism": f"replicated graph x{ws}, walkers sharded by id",
+                                             "path_layout": "walker-major" if wmajor else "step-major"}),
             "walk_steps_per_s": steps_total / ws / K / walk_avg_s * ws,
             "update_edges_per_s": nrec / upd_avg,
             "update_ms": upd_avg * 1e3, "walk_ms": walk_avg_s * 1e3,
@@ -348,6 +352,7 @@ def main():
                                           "+ 4 B x path entries + 4 B x lengths, exact counts from bingo_walk_profile",
                          "load_counts": {k: prof[k] for k in ("steps", "hdr", "bkt", "mem", "arc")},
                          "gather_roofline": gather},
+            "l2_plan": {k: g.info()[k] for k in ("l2_persist_bytes", "hot_degree")},
             "clocks": clk, "gpu_launches": int(launches),
             "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -157,6 +157,8 @@ bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint
  * A walker at a vertex of out-degree 0 stops (truncation).
  * paths_or_null: step-major u32 [(length+1) x num_walkers], entry
  *   [t * num_walkers + i] = vertex after t steps; 0xFFFFFFFF after truncation.
+ *   With BINGO_WALK_WALKER_MAJOR the layout is [num_walkers x (length+1)],
+ *   entry [i * (length+1) + t] (one contiguous walk per walker).
  *   Required NULL for PPR without a cap.  lengths_or_null: u32 [num_walkers]
  *   steps actually taken.  DEVICE pointers, or HOST with
  *   BINGO_WALK_HOST_OUTPUT (the library stages through device scratch and
@@ -166,6 +168,7 @@ bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint
  * ------------------------------------------------------------------------- */
 enum { BINGO_DEEPWALK = 0, BINGO_NODE2VEC = 1, BINGO_PPR = 2 };
 #define BINGO_WALK_HOST_OUTPUT 1u
+#define BINGO_WALK_WALKER_MAJOR 2u /* paths walker-major: entry [i * (length+1) + t] */
 #define BINGO_NO_CAP 0xFFFFFFFFu
 
 typedef struct {
@@ -216,6 +219,8 @@ typedef struct {
     uint64_t member_pool_used, member_pool_cap; /* 8 B entries */
     uint64_t device_bytes;
     uint64_t kernel_launches;  /* process-wide count of libbingo kernel launches so far */
+    uint64_t l2_persist_bytes; /* L2 persisting set-aside in effect (walker hot set) */
+    uint64_t hot_degree;       /* low 32 bits: degree from which buckets are L2 evict_last; high 32: member arrays */
 } bingo_info;
 bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *stream);
 

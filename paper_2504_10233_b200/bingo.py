@@ -15,7 +15,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libbingo.so")
+LIB_PATH = os.environ.get("BINGO_LIB_OVERRIDE") or os.path.join(HERE, "libbingo.so")   # override: A/B experiments only
 
 OK, E_INVAL, E_NOMEM, E_CUDA, E_OVERFLOW, E_STATE = 0, 1, 2, 3, 4, 5
 EMPTY, ONE, DENSE, SPARSE, REGULAR = 0, 1, 2, 3, 4
@@ -23,6 +23,7 @@ DEEPWALK, NODE2VEC, PPR = 0, 1, 2
 BUILD_BS_MODE = 1
 UPD_HOST_BATCH = 1
 WALK_HOST_OUTPUT = 1
+WALK_WALKER_MAJOR = 2
 COUNTS_HOST = 1
 NO_CAP = 0xFFFFFFFF
 
@@ -68,7 +69,8 @@ class Info(ctypes.Structure):
                 ("arc_pool_used", ctypes.c_uint64), ("arc_pool_cap", ctypes.c_uint64),
                 ("bucket_pool_used", ctypes.c_uint64), ("bucket_pool_cap", ctypes.c_uint64),
                 ("member_pool_used", ctypes.c_uint64), ("member_pool_cap", ctypes.c_uint64),
-                ("device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64)]
+                ("device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
+                ("l2_persist_bytes", ctypes.c_uint64), ("hot_degree", ctypes.c_uint64)]
 
 
 _LIB = None
@@ -245,15 +247,17 @@ class Graph:
     # ---------------------------------------------------------- walks
     def walk(self, app: int = DEEPWALK, length: int = 80, seed: int = 0, first_walker: int = 0, starts=None,
              num_walkers: Optional[int] = None, p: float = 1.0, q: float = 1.0, stop=(1, 80), paths=True,
-             lengths=True, stream=None):
+             lengths=True, walker_major: bool = False, stream=None):
         """Launch ``num_walkers`` walkers (default: one per vertex).  Returns device tensors
-        {"paths": int32 [(length+1), W] or None, "lengths": int32 [W] or None}."""
+        {"paths": int32 [(length+1), W] (or [W, length+1] walker-major) or None,
+         "lengths": int32 [W] or None}."""
         torch = _torch()
         W = num_walkers if num_walkers is not None else (len(starts) if starts is not None else self.V)
         st = _dev_u32(starts, torch, self.device) if starts is not None else None
         pa = None
         if paths is True:
-            pa = torch.empty((length + 1, W), dtype=torch.int32, device=self.device)
+            shape = (W, length + 1) if walker_major else (length + 1, W)
+            pa = torch.empty(shape, dtype=torch.int32, device=self.device)
         elif paths is not None and paths is not False:
             pa = paths
         ln = None
@@ -262,7 +266,7 @@ class Graph:
         elif lengths is not None and lengths is not False:
             ln = lengths
         d = WalkDesc(app=app, length=length, p=p, q=q, stop_num=stop[0], stop_den=stop[1], seed=seed,
-                     first_walker_id=first_walker, flags=0)
+                     first_walker_id=first_walker, flags=WALK_WALKER_MAJOR if walker_major else 0)
         with torch.cuda.device(self.device):
             _check(_lib().bingo_walk(self._h, ctypes.byref(d), st.data_ptr() if st is not None else None, W,
                                      pa.data_ptr() if pa is not None else None,

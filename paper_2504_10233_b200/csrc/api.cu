@@ -32,7 +32,7 @@ void bingo_dev_free(bingo_graph *g, void *p) {
 
 extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
-    void *bufs[] = {g->hdr, g->arc, g->arc_epoch, g->bkt, g->mem, g->counters, g->visit, g->dev_flag,
+    void *bufs[] = {g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->bkt, g->mdst, g->midx, g->counters, g->visit, g->dev_flag,
                     g->scratch, g->wscratch, g->vscratch};
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
@@ -68,11 +68,13 @@ extern "C" bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *s
     info->arc_pool_cap = g->arc_cap;
     info->bucket_pool_used = c[1];
     info->bucket_pool_cap = g->bkt_cap;
-    info->member_pool_used = 2 * c[2];
+    info->member_pool_used = 4 * c[2];
     info->member_pool_cap = g->mem_cap;
     info->kernel_launches = g_launch_count.load();
-    info->device_bytes = sizeof(VHdr) * (uint64_t)g->V + (sizeof(uint2) + 4) * g->arc_cap +
-                         sizeof(Bucket) * g->bkt_cap + sizeof(uint2) * g->mem_cap + 8ull * g->V +
+    info->l2_persist_bytes = g->persist_bytes;
+    info->hot_degree = ((uint64_t)g->hot_mem_degree << 32) | g->hot_bkt_degree;
+    info->device_bytes = (sizeof(VHdr) + sizeof(ThinHdr)) * (uint64_t)g->V + (sizeof(uint2) + 4) * g->arc_cap +
+                         (sizeof(Bucket) + sizeof(GCan)) * g->bkt_cap + 8ull * g->mem_cap + 8ull * g->V +
                          g->scratch_bytes + g->wscratch_bytes + g->vscratch_bytes;
     return BINGO_OK;
 }
@@ -107,11 +109,13 @@ extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t c
     std::vector<uint2> arc(c[0]);
     std::vector<uint32_t> ep(c[0]);
     std::vector<Bucket> bkt(c[1]);
-    std::vector<uint2> mem(2 * c[2]);
+    std::vector<GCan> gc(c[1]);
+    std::vector<uint32_t> mem(4 * c[2]);
     if (c[0]) e = cudaMemcpyAsync(arc.data(), g->arc, sizeof(uint2) * c[0], cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && c[0]) e = cudaMemcpyAsync(ep.data(), g->arc_epoch, 4 * c[0], cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && c[1]) e = cudaMemcpyAsync(bkt.data(), g->bkt, sizeof(Bucket) * c[1], cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess && c[2]) e = cudaMemcpyAsync(mem.data(), g->mem, sizeof(uint2) * 2 * c[2], cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && c[1]) e = cudaMemcpyAsync(gc.data(), g->gcan, sizeof(GCan) * c[1], cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && c[2]) e = cudaMemcpyAsync(mem.data(), g->midx, sizeof(uint32_t) * 4 * c[2], cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     Out o{(host_buf && cap) ? host_buf : nullptr, cap, 0};
@@ -126,16 +130,17 @@ extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t c
         o.u32(h.n);
         for (uint32_t b = 0; b < h.n; b++) {
             const Bucket &B = bkt[(size_t)h.bkt_off + b];
+            const GCan &G = gc[(size_t)h.bkt_off + b];
             const uint32_t kind = kk_kind(B.kk);
             o.u32(kk_k(B.kk));
-            o.u32(B.c);
+            o.u32(G.c);
             o.u32(kind);
-            o.u64(B.thr);
+            o.u64(G.thr);
             o.u32(B.alias);
             if (is_list(kind))
-                for (uint32_t j = 0; j < B.c; j++) o.u32(mem[(size_t)B.ref * 2 + j].x);
+                for (uint32_t j = 0; j < G.c; j++) o.u32(mem[(size_t)B.py * 4 + j]);
             else if (kind == K_ONE)
-                o.u32(B.aux);
+                o.u32(G.aux);
         }
         o.u64(h.T);
     }
@@ -161,7 +166,7 @@ __device__ __forceinline__ uint64_t fnv64(uint64_t h, uint64_t v) {
 
 __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 *__restrict__ arc,
                           const uint32_t *__restrict__ ep, const Bucket *__restrict__ bkt,
-                          const uint2 *__restrict__ mem, uint64_t *__restrict__ out) {
+                          const GCan *__restrict__ gcan, const uint32_t *__restrict__ midx, uint64_t *__restrict__ out) {
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
         const VHdr h = hdr[u];
         uint64_t x = 0xcbf29ce484222325ull;
@@ -175,16 +180,17 @@ __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 
         x = fnv32(x, h.n);
         for (uint32_t b = 0; b < h.n; b++) {
             const Bucket B = load_bucket(bkt + h.bkt_off + b);
+            const GCan G = load_gcan(gcan + h.bkt_off + b);
             const uint32_t kind = kk_kind(B.kk);
             x = fnv32(x, kk_k(B.kk));
-            x = fnv32(x, B.c);
+            x = fnv32(x, G.c);
             x = fnv32(x, kind);
-            x = fnv64(x, B.thr);
+            x = fnv64(x, G.thr);
             x = fnv32(x, B.alias);
             if (is_list(kind))
-                for (uint32_t j = 0; j < B.c; j++) x = fnv32(x, mem[(uint64_t)B.ref * 2 + j].x);
+                for (uint32_t j = 0; j < G.c; j++) x = fnv32(x, midx[(uint64_t)B.py * 4 + j]);
             else if (kind == K_ONE)
-                x = fnv32(x, B.aux);
+                x = fnv32(x, G.aux);
         }
         out[u] = fnv64(x, h.T);
     }
@@ -197,7 +203,7 @@ extern "C" bingo_status bingo_digests(bingo_graph *g, uint64_t *digests, void *s
     if (!g->V) return BINGO_OK;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)g->V + 255) / 256, 148ull * 16);
-    k_digests<<<blocks, 256, 0, s>>>(g->V, g->hdr, g->arc, g->arc_epoch, g->bkt, g->mem, digests);
+    k_digests<<<blocks, 256, 0, s>>>(g->V, g->hdr, g->arc, g->arc_epoch, g->bkt, g->gcan, g->midx, digests);
     bingo_count_launch();
     if (cudaGetLastError() != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     return BINGO_OK;

@@ -2,28 +2,36 @@
 //
 // HBM layout.  Everything is structure-of-arrays inside
 // a few pools addressed by OFFSETS (never raw pointers), so a pool can grow by
-// reallocation + one memcpy without fix-ups:
+// reallocation + one memcpy without fix-ups.
 //
-//  hdr   [V]        VHdr, 32 B, one DRAM sector per vertex: the walker's first
-//                   load.  T = sum of biases (Eq.4 summed), adjacency offset and
-//                   capacity, bucket offset, degree d, group count n.
-//  bkt   pool       Bucket, 32 B, one per nonempty radix group, ascending k.
-//                   Bucket b is both the canonical record of group b (k, kind,
-//                   c, member array) and alias bucket b (thr, alias) -- A-13:
-//                   the alias table is over the nonempty groups, ascending k.
-//                   It also carries a COPY of its alias partner's (k, kind, c,
-//                   ref) so a walker resolves the inter-group sample (Eq.5)
-//                   with one 32 B load whichever side of the bucket it lands.
-//  arc   pool       uint2 {dst, bias} per arc (8 B) + arc_epoch u32 (update
-//                   side only).  Dense groups sample it directly.
-//  mem   pool       uint2 {arc index, dst} member entries of REGULAR/SPARSE
-//                   groups (groups store neighbour INDICES; the dst
-//                   copy saves the walker the dependent adjacency load).
-//                   Group arrays start at 16 B units (u32 unit offsets).
+// Walker-facing (read by every step):
+//  thdr  [V]        ThinHdr, 8 B: bucket offset + group count n.  38 MB at
+//                   4.7M vertices -> L2-resident (pinned with an access-policy
+//                   window), so a step's first load is not a DRAM access.
+//  bkt   pool       Bucket, 32 B (one 256-bit load), one per nonempty radix
+//                   group in ascending k: alias bucket b = group b (A-13).  It
+//                   holds lim = ceil(thr * 2^64 / T), the alias threshold
+//                   rescaled so the walker's coin test needs no T (R-4'), the
+//                   sampling view (kind, k, count/degree, member or adjacency
+//                   base, or the one-element dst) of group b AND of its alias
+//                   partner, so the inter-group stage (Eq.5) is one load.
+//  mdst  pool       u32 dst of every member of a REGULAR/SPARSE group (the
+//                   walker reads only this 4 B array: twice the entries per
+//                   byte of L2 than an {index, dst} pair).  Group arrays start
+//                   at 16 B units of 4 entries (u32 unit offsets).
+//  arc   pool       uint2 {dst, bias} per arc; dense groups sample it directly
+//                   (P:465).  Adjacency blocks are 4-arc (32 B) aligned.
+// Update-side (canonical state, not read by walkers):
+//  hdr   [V]        VHdr, 32 B: T, adjacency offset/capacity, bucket offset and
+//                   capacity, degree d, n.
+//  gcan  pool       GCan, 16 B per bucket: integer Vose threshold thr, |G_k|,
+//                   member capacity or the one-element member's arc index.
+//  midx  pool       u32 adjacency INDEX of every member (groups store
+//                   neighbour indices), parallel to mdst.
+//  arc_epoch pool   u32 epoch per arc (R-9).
 //
-// A walker step is therefore hdr -> bucket -> member (3 dependent sectors),
-// hdr -> bucket (ONE: dst cached in the bucket), or hdr -> bucket -> arc per
-// dense attempt.
+// A walker step is thdr (L2) -> Bucket -> member (REGULAR/SPARSE), thdr ->
+// Bucket (ONE), or thdr -> Bucket -> arc per dense attempt.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -44,20 +52,35 @@ struct __align__(32) VHdr {
 };
 static_assert(sizeof(VHdr) == 32, "VHdr must be one sector");
 
-// kk byte: bits 0..4 = k, bits 5..7 = kind
+struct __align__(8) ThinHdr {
+    uint32_t bkt_off;  // bucket pool index of bucket 0
+    uint8_t n;         // nonempty groups (0: dead end)
+    uint8_t flags;     // bit 0: hot buckets, bit 1: hot member arrays (L2 evict_last)
+    uint16_t pad1;
+};
+static_assert(sizeof(ThinHdr) == 8, "ThinHdr is 8 B");
+
+// kk byte: bits 0..4 = k, bits 5..7 = kind.
+// Group view (x, y): REGULAR/SPARSE (c, member offset in 16 B units);
+// ONE (unused, dst of the member); DENSE (d, adjacency offset / 4).
 struct __align__(32) Bucket {
-    uint64_t thr;   // alias threshold in [0, T]: coin < thr -> this group, else alias
-    uint32_t c;     // |G_k|
-    uint32_t ref;   // REG/SPARSE: member array offset (16 B units); ONE: dst of the member
-    uint32_t a_c;   // copy of the alias partner's c
-    uint32_t a_ref; // copy of the alias partner's ref
-    uint8_t kk;     // k | kind << 5
-    uint8_t a_kk;   // alias partner's kk
-    uint8_t alias;  // alias partner bucket
+    uint64_t lim;   // coin R (64-bit) < lim -> this group, else the alias partner
+    uint32_t px, py;
+    uint32_t ax, ay;
+    uint8_t kk;     // this group
+    uint8_t a_kk;   // alias partner
+    uint8_t alias;  // alias partner bucket index
     uint8_t pad;
-    uint32_t aux;   // REG/SPARSE: member capacity (entries); ONE: the member's arc index
+    uint32_t spare;
 };
 static_assert(sizeof(Bucket) == 32, "Bucket must be one sector");
+
+struct __align__(16) GCan {
+    uint64_t thr;   // integer Vose threshold in [0, T] (canonical, R-4)
+    uint32_t c;     // |G_k|
+    uint32_t aux;   // REGULAR/SPARSE: member capacity (entries); ONE: the member's arc index
+};
+static_assert(sizeof(GCan) == 16, "GCan is 16 B");
 
 __host__ __device__ inline uint32_t kk_k(uint8_t kk) { return kk & 31u; }
 __host__ __device__ inline uint32_t kk_kind(uint8_t kk) { return (uint32_t)kk >> 5; }
@@ -125,10 +148,16 @@ struct bingo_graph {
     uint2 *arc = nullptr;              // [arc_cap]
     uint32_t *arc_epoch = nullptr;     // [arc_cap]
     uint64_t arc_cap = 0;
+    bingo::ThinHdr *thdr = nullptr;    // [V]
     bingo::Bucket *bkt = nullptr;      // [bkt_cap]
+    bingo::GCan *gcan = nullptr;       // [bkt_cap]
     uint64_t bkt_cap = 0;
-    uint2 *mem = nullptr;              // [mem_cap] entries
-    uint64_t mem_cap = 0;
+    size_t persist_bytes = 0;          // L2 persisting set-aside granted to this process
+    uint32_t hot_bkt_degree = 0xFFFFFFFFu; // d >= this: buckets loaded evict_last
+    uint32_t hot_mem_degree = 0xFFFFFFFFu; // d >= this: member dsts loaded evict_last
+    uint32_t *mdst = nullptr;          // [mem_cap] member dst (walker side)
+    uint32_t *midx = nullptr;          // [mem_cap] member adjacency index (canonical)
+    uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
     unsigned long long *visit = nullptr;     // [V] PPR visit counts
     int *dev_flag = nullptr;                 // device error flag

@@ -10,7 +10,9 @@
 //                 compaction, finds one-element members, builds the integer Vose
 //                 alias over the nonempty groups with one lane per bucket (R-4),
 //                 and writes the 32 B buckets and the 32 B vertex header.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "bingo.h"
@@ -25,7 +27,11 @@ namespace bingo {
 __global__ void k_build_sizes(uint32_t V, const uint64_t *__restrict__ ro, const uint32_t *__restrict__ dst,
                               const uint32_t *__restrict__ bias, uint32_t alpha, uint32_t beta, bool bs,
                               double arc_slack, double mem_slack, uint64_t *__restrict__ sz_arc,
-                              uint64_t *__restrict__ sz_bkt, uint64_t *__restrict__ sz_mem, int *__restrict__ flag) {
+                              uint64_t *__restrict__ sz_bkt, uint64_t *__restrict__ sz_mem, int *__restrict__ flag,
+                              unsigned long long *__restrict__ hot_hist) {
+    __shared__ unsigned long long s_hist[2 * HOT_BINS];
+    for (int i = threadIdx.x; i < 2 * HOT_BINS; i += blockDim.x) s_hist[i] = 0;
+    __syncthreads();
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     const uint32_t lane = lane_id();
     for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
@@ -65,16 +71,24 @@ __global__ void k_build_sizes(uint32_t V, const uint64_t *__restrict__ ro, const
             sz_arc[u] = arc_capacity(d, arc_slack);
             sz_bkt[u] = bucket_capacity(n);
             sz_mem[u] = units;
+            // walker-read bytes of this vertex by degree bin: buckets, member dsts
+            atomicAdd(&s_hist[hot_bin(d)], (unsigned long long)(32ull * n));
+            atomicAdd(&s_hist[HOT_BINS + hot_bin(d)], (unsigned long long)(16ull * units));
         }
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2 * HOT_BINS; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(&hot_hist[i], s_hist[i]);
 }
 
 __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const uint32_t *__restrict__ dst,
                              const uint32_t *__restrict__ bias, uint32_t alpha, uint32_t beta, bool bs,
                              double mem_slack, const uint64_t *__restrict__ off_arc,
                              const uint64_t *__restrict__ off_bkt, const uint64_t *__restrict__ off_mem,
-                             VHdr *__restrict__ hdr, uint2 *__restrict__ arc, uint32_t *__restrict__ arc_epoch,
-                             Bucket *__restrict__ bkt, uint2 *__restrict__ mem) {
+                             VHdr *__restrict__ hdr, ThinHdr *__restrict__ thdr, uint2 *__restrict__ arc,
+                             uint32_t *__restrict__ arc_epoch, Bucket *__restrict__ bkt, GCan *__restrict__ gcan,
+                             uint32_t *__restrict__ mdst, uint32_t *__restrict__ midx, uint32_t hot_b,
+                             uint32_t hot_m) {
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     const uint32_t lane = lane_id();
     for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
@@ -140,7 +154,11 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
                     }
                     const uint32_t start = __shfl_sync(0xffffffffu, fill, k);
                     const uint64_t goff = __shfl_sync(0xffffffffu, my_off, k);
-                    if ((w >> k) & 1u) mem[goff * 2 + start + __popc(bal & lanemask_lt())] = make_uint2(i, v);
+                    if ((w >> k) & 1u) {
+                        const uint64_t e = goff * 4 + start + __popc(bal & lanemask_lt());
+                        mdst[e] = v;
+                        midx[e] = i;
+                    }
                     if (lane == (uint32_t)k) fill += __popc(bal);
                 }
             }
@@ -157,21 +175,10 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
         uint32_t alias;
         vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
         const uint64_t bo = off_bkt[u];
-        Bucket B;
-        B.thr = thr;
-        B.c = c_b;
-        B.kk = make_kk(kb, kind_b);
-        B.ref = is_list(kind_b) ? (uint32_t)off_b : (kind_b == K_ONE ? od_b : 0u);
-        B.aux = is_list(kind_b) ? units_b * 2 : (kind_b == K_ONE ? oi_b : 0u);
-        B.alias = (uint8_t)alias;
-        B.pad = 0;
-        const uint32_t a_c = __shfl_sync(0xffffffffu, B.c, alias);
-        const uint32_t a_ref = __shfl_sync(0xffffffffu, B.ref, alias);
-        const uint32_t a_kk = __shfl_sync(0xffffffffu, (uint32_t)B.kk, alias);
-        B.a_c = a_c;
-        B.a_ref = a_ref;
-        B.a_kk = (uint8_t)a_kk;
-        if (lane < n) store_bucket(&bkt[bo + lane], B);
+        uint32_t x_b, y_b;
+        group_view(kind_b, c_b, (uint32_t)off_b, od_b, d, aoff, x_b, y_b);
+        const uint32_t aux_b = is_list(kind_b) ? units_b * 4 : (kind_b == K_ONE ? oi_b : 0u);
+        write_buckets(bkt, gcan, bo, n, lane, kb, kind_b, c_b, x_b, y_b, aux_b, thr, alias, T);
         if (lane == 0) {
             VHdr h;
             h.T = T;
@@ -183,6 +190,12 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
             h.pad = 0;
             h.adj_cap = (uint32_t)(off_arc[u + 1] - aoff);
             hdr[u] = h;
+            ThinHdr th;
+            th.bkt_off = (uint32_t)bo;
+            th.n = (uint8_t)n;
+            th.flags = (d >= hot_b ? 1 : 0) | (d >= hot_m ? 2 : 0);
+            th.pad1 = 0;
+            thdr[u] = th;
         }
     }
 }
@@ -190,6 +203,46 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
 }  // namespace bingo
 
 // ---------------------------------------------------------------- host side
+// L2 residency plan: the walker loads every thin header with an
+// evict_last policy, and the buckets / member arrays of "hot" vertices too; the
+// hot set is the highest-degree vertices whose walker bytes fit in the
+// persisting set-aside left after the thin headers.  Walk visits are
+// degree-skewed, so this set serves most bucket and member reads.
+static uint32_t degree_for_budget(const unsigned long long *hist, double budget) {
+    if (budget <= 0) return 0xFFFFFFFFu;
+    double acc = 0;
+    int b = HOT_BINS - 1;
+    for (; b >= 0; b--) {
+        if (acc + (double)hist[b] > budget) break;
+        acc += (double)hist[b];
+    }
+    return hot_bin_floor(b + 1);
+}
+
+static void choose_hot_degrees(bingo_graph *g, const unsigned long long *hist, uint64_t nV) {
+    g->hot_bkt_degree = g->hot_mem_degree = 0xFFFFFFFFu;
+    int dev = 0, max_persist = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+        max_persist <= 0) {
+        cudaGetLastError();
+        g->persist_bytes = 0;
+        return;
+    }
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    if (cur < (size_t)max_persist) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    cudaGetLastError();
+    g->persist_bytes = cur;
+    const double thdr_bytes = (double)sizeof(ThinHdr) * (double)nV;
+    const double budget = 0.9 * (double)cur - thdr_bytes;
+    double share = 0.35;   // bucket share of the hot budget (buckets are read ~d/n times per byte more)
+    if (const char *e = getenv("BINGO_L2_BUCKET_SHARE")) share = atof(e);
+    g->hot_bkt_degree = degree_for_budget(hist, budget * share);
+    g->hot_mem_degree = degree_for_budget(hist + HOT_BINS, budget * (1.0 - share));
+}
+
 static bingo_status fail_cuda(bingo_graph *g, cudaError_t e, const char *where) {
     fprintf(stderr, "libbingo: CUDA error in %s: %s\n", where, cudaGetErrorString(e));
     if (g) g->poisoned = 1;
@@ -231,31 +284,42 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     uint64_t tot[3] = {0, 0, 0};
     int hflag = 0;
     unsigned long long hc[4];
+    unsigned long long *dhist = nullptr;
+    unsigned long long hhist[2 * HOT_BINS];
     const unsigned blocks = (unsigned)std::min<uint64_t>((nV + 7) / 8, 148ull * 64);
 
     g->counters = (unsigned long long *)bingo_dev_alloc(g, 16 * sizeof(unsigned long long));
     g->dev_flag = (int *)bingo_dev_alloc(g, sizeof(int) * 4);
     g->hdr = (VHdr *)bingo_dev_alloc(g, sizeof(VHdr) * std::max<uint64_t>(nV, 1));
+    g->thdr = (ThinHdr *)bingo_dev_alloc(g, sizeof(ThinHdr) * std::max<uint64_t>(nV, 1));
     g->visit = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * std::max<uint64_t>(nV, 1));
     sz = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (nV + 1));
     off = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (nV + 1));
     tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * tmpw);
-    if (!g->counters || !g->dev_flag || !g->hdr || !g->visit || !sz || !off || !tmp) { st = BINGO_E_NOMEM; goto done; }
+    dhist = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * 2 * HOT_BINS);
+    if (!g->counters || !g->dev_flag || !g->hdr || !g->thdr || !g->visit || !sz || !off || !tmp || !dhist) {
+        st = BINGO_E_NOMEM;
+        goto done;
+    }
+    CK(cudaMemsetAsync(dhist, 0, sizeof(unsigned long long) * 2 * HOT_BINS, s));
     CK(cudaMemsetAsync(g->counters, 0, 16 * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(g->dev_flag, 0, sizeof(int) * 4, s));
     CK(cudaMemsetAsync(g->visit, 0, sizeof(unsigned long long) * std::max<uint64_t>(nV, 1), s));
     CK(cudaMemsetAsync(g->hdr, 0, sizeof(VHdr) * std::max<uint64_t>(nV, 1), s));
+    CK(cudaMemsetAsync(g->thdr, 0, sizeof(ThinHdr) * std::max<uint64_t>(nV, 1), s));
     if (V) {
         k_build_sizes<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
                                              g->arc_slack, g->member_slack, sz, sz + (nV + 1), sz + 2 * (nV + 1),
-                                             g->dev_flag);
+                                             g->dev_flag, dhist);
         bingo_count_launch();
         CK(cudaGetLastError());
         for (int p = 0; p < 3; p++) CK(exclusive_scan_u64(sz + p * (nV + 1), off + p * (nV + 1), nV, tmp, s));
         CK(cudaMemcpyAsync(&hflag, g->dev_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         for (int p = 0; p < 3; p++)
             CK(cudaMemcpyAsync(&tot[p], off + p * (nV + 1) + nV, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(hhist, dhist, sizeof(hhist), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        choose_hot_degrees(g, hhist, nV);
         uint64_t last_ro = 0;
         CK(cudaMemcpy(&last_ro, desc->row_offsets + V, sizeof(uint64_t), cudaMemcpyDeviceToHost));
         if (last_ro != desc->num_arcs) hflag |= 1;
@@ -265,18 +329,21 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     if (tot[1] >= 0xFFFFFFFFull || tot[2] >= 0xFFFFFFFFull) { st = BINGO_E_OVERFLOW; goto done; }
     g->arc_cap = pool_capacity(tot[0], g->pool_reserve, 1024);
     g->bkt_cap = std::min<uint64_t>(pool_capacity(tot[1], g->pool_reserve, 1024), 0xFFFFFFF0ull);
-    g->mem_cap = 2 * std::min<uint64_t>(pool_capacity(tot[2], g->pool_reserve, 1024), 0xFFFFFFF0ull);
+    g->mem_cap = 4 * std::min<uint64_t>(pool_capacity(tot[2], g->pool_reserve, 1024), 0xFFFFFFF0ull);
     g->arc = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * g->arc_cap);
     g->arc_epoch = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->arc_cap);
     g->bkt = (Bucket *)bingo_dev_alloc(g, sizeof(Bucket) * g->bkt_cap);
-    g->mem = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * g->mem_cap);
-    if (!g->arc || !g->arc_epoch || !g->bkt || !g->mem) { st = BINGO_E_NOMEM; goto done; }
+    g->gcan = (GCan *)bingo_dev_alloc(g, sizeof(GCan) * g->bkt_cap);
+    g->mdst = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->mem_cap);
+    g->midx = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->mem_cap);
+    if (!g->arc || !g->arc_epoch || !g->bkt || !g->gcan || !g->mdst || !g->midx) { st = BINGO_E_NOMEM; goto done; }
     hc[0] = tot[0]; hc[1] = tot[1]; hc[2] = tot[2]; hc[3] = 0;
     CK(cudaMemcpyAsync(g->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
     if (V) {
         k_build_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
-                                            g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), g->hdr, g->arc,
-                                            g->arc_epoch, g->bkt, g->mem);
+                                            g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), g->hdr, g->thdr,
+                                            g->arc, g->arc_epoch, g->bkt, g->gcan, g->mdst, g->midx,
+                                            g->hot_bkt_degree, g->hot_mem_degree);
         bingo_count_launch();
         CK(cudaGetLastError());
     }
@@ -285,6 +352,7 @@ done:
     bingo_dev_free(g, sz);
     bingo_dev_free(g, off);
     bingo_dev_free(g, tmp);
+    bingo_dev_free(g, dhist);
     if (st != BINGO_OK) {
         bingo_destroy(g);
         return st;

@@ -99,18 +99,20 @@ struct OldGroups {
     uint32_t list_mask; // REGULAR/SPARSE groups
 };
 
-// lane b < n loads bucket b; returns (k, kind, c, ref, aux) of lane k's group in lane k
-__device__ __forceinline__ void load_old_groups(const Bucket *bkt, const VHdr &h, uint32_t &kind_k, uint32_t &c_k,
-                                                uint32_t &ref_k, uint32_t &aux_k, OldGroups &og) {
+// lane b < n loads bucket b; returns (kind, c, ref, aux) of lane k's group in lane k
+// (ref: REGULAR/SPARSE member offset; aux: member capacity or the ONE arc index)
+__device__ __forceinline__ void load_old_groups(const Bucket *bkt, const GCan *gcan, const VHdr &h, uint32_t &kind_k,
+                                                uint32_t &c_k, uint32_t &ref_k, uint32_t &aux_k, OldGroups &og) {
     const uint32_t lane = lane_id();
     uint32_t k_b = 0, kind_b = K_EMPTY, c_b = 0, ref_b = 0, aux_b = 0;
     if (lane < h.n) {
         const Bucket B = load_bucket(bkt + h.bkt_off + lane);
+        const GCan G = load_gcan(gcan + h.bkt_off + lane);
         k_b = kk_k(B.kk);
         kind_b = kk_kind(B.kk);
-        c_b = B.c;
-        ref_b = B.ref;
-        aux_b = B.aux;
+        c_b = G.c;
+        ref_b = B.py;
+        aux_b = G.aux;
     }
     const uint32_t m = __reduce_or_sync(0xffffffffu, lane < h.n ? (1u << k_b) : 0u);
     og.mask = m;
@@ -132,7 +134,8 @@ __device__ __forceinline__ void load_old_groups(const Bucket *bkt, const VHdr &h
 // ------------------------------------------------------------------ plan (no mutation)
 __global__ void k_upd_plan(const uint4 *__restrict__ recs, const uint32_t *__restrict__ sval,
                            const uint32_t *__restrict__ seg, const uint32_t *__restrict__ tv, uint32_t ntouch,
-                           const VHdr *__restrict__ hdr, const Bucket *__restrict__ bkt, uint32_t alpha, bool bs,
+                           const VHdr *__restrict__ hdr, const Bucket *__restrict__ bkt,
+                           const GCan *__restrict__ gcan, uint32_t alpha, bool bs,
                            double arc_slack, double mem_slack, uint64_t *__restrict__ scr_need, UpdCounters *cnt) {
     const uint32_t lane = lane_id();
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
@@ -142,7 +145,7 @@ __global__ void k_upd_plan(const uint4 *__restrict__ recs, const uint32_t *__res
         const VHdr h = hdr[u];
         uint32_t kind_k, c_k, ref_k, aux_k;
         OldGroups og;
-        load_old_groups(bkt, h, kind_k, c_k, ref_k, aux_k, og);
+        load_old_groups(bkt, gcan, h, kind_k, c_k, ref_k, aux_k, og);
         uint32_t m = 0, q = 0, ins_or = 0, insk = 0;
         uint64_t ins_sum = 0;
         for (uint32_t base = beg; base < end; base += 32) {
@@ -244,13 +247,15 @@ struct MutateArgs {
     const uint64_t *scr_off;
     uint32_t *scr;
     VHdr *hdr;
+    ThinHdr *thdr;
     uint2 *arc;
     uint32_t *arc_epoch;
     Bucket *bkt;
-    uint2 *mem;
+    GCan *gcan;
+    uint32_t *mdst, *midx;
     unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units
     uint32_t *vstats;           // [ntouch][VST]
-    uint32_t epoch, alpha, beta;
+    uint32_t epoch, alpha, beta, hot_b, hot_m;
     bool bs;
     double arc_slack, mem_slack;
 };
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
     if (wid == 0) {
         uint32_t kind_k, c_k, ref_k, aux_k;
         OldGroups og;
-        load_old_groups(a.bkt, h, kind_k, c_k, ref_k, aux_k, og);
+        load_old_groups(a.bkt, a.gcan, h, kind_k, c_k, ref_k, aux_k, og);
         // insert counts per bit for capacity decisions
         uint32_t m = 0, q = 0, insk = 0;
         for (uint32_t base = beg; base < end; base += 32) {
@@ -302,7 +307,7 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
         if (grow) {
             const uint32_t units = member_units(cin, a.mem_slack);
             moff = (uint32_t)atomicAdd(&a.bump[2], (unsigned long long)units);
-            cap = units * 2;
+            cap = units * 4;
         }
         s_moff[lane] = is_list(kind_k) ? moff : 0u;
         s_cap[lane] = is_list(kind_k) ? cap : 0u;
@@ -330,7 +335,10 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             const uint32_t from = __shfl_sync(0xffffffffu, ref_k, k);
             const uint32_t to = __shfl_sync(0xffffffffu, moff, k);
             const uint32_t cnt = __shfl_sync(0xffffffffu, c_k, k);
-            for (uint32_t j = lane; j < cnt; j += 32) a.mem[(uint64_t)to * 2 + j] = a.mem[(uint64_t)from * 2 + j];
+            for (uint32_t j = lane; j < cnt; j += 32) {
+                a.mdst[(uint64_t)to * 4 + j] = a.mdst[(uint64_t)from * 4 + j];
+                a.midx[(uint64_t)to * 4 + j] = a.midx[(uint64_t)from * 4 + j];
+            }
         }
     }
     __syncthreads();
@@ -372,8 +380,11 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                 const uint32_t kind_kk = __shfl_sync(0xffffffffu, kind_l, k);
                 const uint32_t start = __shfl_sync(0xffffffffu, c_l + insk, k);
                 const uint32_t mo = __shfl_sync(0xffffffffu, moff_l, k);
-                if (is_list(kind_kk) && ((w >> k) & 1u))
-                    a.mem[(uint64_t)mo * 2 + start + __popc(bal & lanemask_lt())] = make_uint2(idx, r.z);
+                if (is_list(kind_kk) && ((w >> k) & 1u)) {
+                    const uint64_t e = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
+                    a.mdst[e] = r.z;
+                    a.midx[e] = idx;
+                }
                 if (lane == (uint32_t)k) insk += __popc(bal);
             }
             run += __popc(bal_i);
@@ -529,13 +540,14 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             lm &= lm - 1;
             const uint32_t cp = s_c[k] + s_insk[k];
             const uint32_t Nk = s_delk[k];
-            uint2 *M = a.mem + (uint64_t)s_moff[k] * 2;
+            uint32_t *Md = a.mdst + (uint64_t)s_moff[k] * 4;
+            uint32_t *Mi = a.midx + (uint64_t)s_moff[k] * 4;
             const uint32_t Lk = cp - Nk;
             if (Nk) {
                 uint32_t carry = 0;
                 for (uint32_t s0 = 0; s0 < Lk; s0 += MT) {
                     const uint32_t s = s0 + tid;
-                    const bool del = s < Lk && bit_test(bm, M[s].x);
+                    const bool del = s < Lk && bit_test(bm, Mi[s]);
                     uint32_t tot;
                     const uint32_t rank = carry + block_scan_u32(del ? 1u : 0u, s_tmp, tot);
                     if (del) gh[rank] = s;
@@ -545,17 +557,20 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                 uint32_t scarry = 0;
                 for (uint32_t s0 = Lk; s0 < cp; s0 += MT) {
                     const uint32_t s = s0 + tid;
-                    const bool surv = s < cp && !bit_test(bm, M[s].x);
+                    const bool surv = s < cp && !bit_test(bm, Mi[s]);
                     uint32_t tot;
                     const uint32_t rank = scarry + block_scan_u32(surv ? 1u : 0u, s_tmp, tot);
-                    if (surv) M[gh[rank]] = M[s];
+                    if (surv) {
+                        Md[gh[rank]] = Md[s];
+                        Mi[gh[rank]] = Mi[s];
+                    }
                     scarry += tot;
                 }
                 __syncthreads();
             }
             for (uint32_t s = tid; s < Lk; s += MT) {
-                const uint32_t x = M[s].x;
-                if (x >= Lp) M[s].x = R[x - Lp];
+                const uint32_t x = Mi[s];
+                if (x >= Lp) Mi[s] = R[x - Lp];
             }
             __syncthreads();
         }
@@ -574,11 +589,11 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
         if (is_list(kind1) && !is_list(kind0)) {
             const uint32_t units = member_units(cn, a.mem_slack);
             s_moff[k] = (uint32_t)atomicAdd(&a.bump[2], (unsigned long long)units);
-            s_cap[k] = units * 2;
+            s_cap[k] = units * 4;
             fill = true;
         } else if (kind1 == K_ONE) {
             if (is_list(kind0)) {
-                one = a.mem[(uint64_t)s_moff[k] * 2].x;
+                one = a.midx[(uint64_t)s_moff[k] * 4];
             } else if (kind0 == K_ONE) {
                 const uint32_t mo = s_one[k];
                 if (q && N && bit_test(bm, mo)) find = true;
@@ -627,7 +642,11 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                 }
                 const uint32_t start = __shfl_sync(0xffffffffu, fillc, k);
                 const uint32_t mo = s_moff[k];
-                if ((e.y >> k) & 1u) a.mem[(uint64_t)mo * 2 + start + __popc(bal & lanemask_lt())] = make_uint2(i, e.x);
+                if ((e.y >> k) & 1u) {
+                    const uint64_t q = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
+                    a.mdst[q] = e.x;
+                    a.midx[q] = i;
+                }
                 if (lane == (uint32_t)k) fillc += __popc(bal);
             }
         }
@@ -655,17 +674,6 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
         uint64_t thr;
         uint32_t alias;
         vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
-        Bucket B;
-        B.thr = thr;
-        B.c = c_b;
-        B.kk = make_kk(kb, kind_b);
-        B.ref = is_list(kind_b) ? moff_b : (kind_b == K_ONE ? od_b : 0u);
-        B.aux = is_list(kind_b) ? cap_b : (kind_b == K_ONE ? one_b : 0u);
-        B.alias = (uint8_t)alias;
-        B.pad = 0;
-        B.a_c = __shfl_sync(0xffffffffu, B.c, alias);
-        B.a_ref = __shfl_sync(0xffffffffu, B.ref, alias);
-        B.a_kk = (uint8_t)__shfl_sync(0xffffffffu, (uint32_t)B.kk, alias);
         uint32_t bo = h.bkt_off, ncap = h.ncap;
         if (n > h.ncap) {
             // plan reserved bucket_capacity(popc(mask | inserted)) >= n
@@ -673,7 +681,10 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             bo = __shfl_sync(0xffffffffu, bo, 0);
             ncap = bucket_capacity(n);
         }
-        if (lane < n) store_bucket(&a.bkt[(uint64_t)bo + lane], B);
+        uint32_t x_b, y_b;
+        group_view(kind_b, c_b, moff_b, od_b, dn, aoff, x_b, y_b);
+        const uint32_t aux_b = is_list(kind_b) ? cap_b : (kind_b == K_ONE ? one_b : 0u);
+        write_buckets(a.bkt, a.gcan, bo, n, lane, kb, kind_b, c_b, x_b, y_b, aux_b, thr, alias, T);
         if (lane == 0) {
             VHdr nh;
             nh.T = T;
@@ -685,6 +696,12 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             nh.pad = 0;
             nh.adj_cap = s_adj_cap;
             a.hdr[u] = nh;
+            ThinHdr th;
+            th.bkt_off = bo;
+            th.n = (uint8_t)n;
+            th.flags = (dn >= a.hot_b ? 1 : 0) | (dn >= a.hot_m ? 2 : 0);
+            th.pad1 = 0;
+            a.thdr[u] = th;
         }
     }
 }
@@ -758,23 +775,29 @@ bingo_status grow_pool(bingo_graph *g, int which, uint64_t need_total, cudaStrea
                                           0xFFFFFFF0ull);
         if (cap < need_total) return BINGO_E_NOMEM;
         Bucket *nb = (Bucket *)bingo_dev_alloc(g, sizeof(Bucket) * cap);
-        if (!nb) return BINGO_E_NOMEM;
+        GCan *ng = (GCan *)bingo_dev_alloc(g, sizeof(GCan) * cap);
+        if (!nb || !ng) { bingo_dev_free(g, nb); bingo_dev_free(g, ng); return BINGO_E_NOMEM; }
         if (cudaMemcpyAsync(nb, g->bkt, sizeof(Bucket) * g->bkt_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(ng, g->gcan, sizeof(GCan) * g->bkt_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess)
             return BINGO_E_CUDA;
         bingo_dev_free(g, g->bkt);
-        g->bkt = nb; g->bkt_cap = cap;
+        bingo_dev_free(g, g->gcan);
+        g->bkt = nb; g->gcan = ng; g->bkt_cap = cap;
     } else {
-        uint64_t units = std::min<uint64_t>(std::max<uint64_t>(need_total + need_total / 4, g->mem_cap / 2 + g->mem_cap / 8),
+        uint64_t units = std::min<uint64_t>(std::max<uint64_t>(need_total + need_total / 4, g->mem_cap / 4 + g->mem_cap / 16),
                                             0xFFFFFFF0ull);
         if (units < need_total) return BINGO_E_NOMEM;
-        uint2 *nm = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * 2 * units);
-        if (!nm) return BINGO_E_NOMEM;
-        if (cudaMemcpyAsync(nm, g->mem, sizeof(uint2) * g->mem_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+        uint32_t *nd = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * units);
+        uint32_t *ni = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * units);
+        if (!nd || !ni) { bingo_dev_free(g, nd); bingo_dev_free(g, ni); return BINGO_E_NOMEM; }
+        if (cudaMemcpyAsync(nd, g->mdst, sizeof(uint32_t) * g->mem_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(ni, g->midx, sizeof(uint32_t) * g->mem_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess)
             return BINGO_E_CUDA;
-        bingo_dev_free(g, g->mem);
-        g->mem = nm; g->mem_cap = 2 * units;
+        bingo_dev_free(g, g->mdst);
+        bingo_dev_free(g, g->midx);
+        g->mdst = nd; g->midx = ni; g->mem_cap = 4 * units;
     }
     return BINGO_OK;
 }
@@ -867,7 +890,7 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     UCK(cudaStreamSynchronize(s));
     const bool bs = (g->flags & BINGO_BUILD_BS_MODE) != 0;
     const unsigned gp = (unsigned)std::min<uint64_t>((ntouch + 7) / 8, 148 * 32);
-    k_upd_plan<<<gp ? gp : 1, 256, 0, s>>>(recs, sv, seg, tv, (uint32_t)ntouch, g->hdr, g->bkt, g->alpha, bs,
+    k_upd_plan<<<gp ? gp : 1, 256, 0, s>>>(recs, sv, seg, tv, (uint32_t)ntouch, g->hdr, g->bkt, g->gcan, g->alpha, bs,
                                           g->arc_slack, g->member_slack, scr_need, dc);
     bingo_count_launch();
     UCK(cudaGetLastError());
@@ -888,7 +911,7 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     if (bump[1] + hc.need_bkt > g->bkt_cap && (st = grow_pool(g, 1, bump[1] + hc.need_bkt, s)) != BINGO_OK)
         return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
     const uint64_t mem_units_need = bump[2] + hc.need_mem + hc.reserve_mem;
-    if (mem_units_need > g->mem_cap / 2 && (st = grow_pool(g, 2, mem_units_need, s)) != BINGO_OK)
+    if (mem_units_need > g->mem_cap / 4 && (st = grow_pool(g, 2, mem_units_need, s)) != BINGO_OK)
         return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
     // per-vertex delete scratch
     uint32_t *vscr = nullptr;
@@ -912,15 +935,20 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     ma.scr_off = scr_off;
     ma.scr = vscr;
     ma.hdr = g->hdr;
+    ma.thdr = g->thdr;
     ma.arc = g->arc;
     ma.arc_epoch = g->arc_epoch;
     ma.bkt = g->bkt;
-    ma.mem = g->mem;
+    ma.gcan = g->gcan;
+    ma.mdst = g->mdst;
+    ma.midx = g->midx;
     ma.bump = g->counters;
     ma.vstats = vstats;
     ma.epoch = e;
     ma.alpha = g->alpha;
     ma.beta = g->beta;
+    ma.hot_b = g->hot_bkt_degree;
+    ma.hot_m = g->hot_mem_degree;
     ma.bs = bs;
     ma.arc_slack = g->arc_slack;
     ma.mem_slack = g->member_slack;

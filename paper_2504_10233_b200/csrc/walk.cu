@@ -7,7 +7,9 @@
 // and one coalesced, streaming (evict-first) store of the path column.
 // Randomness: Philox4x32-10 keyed by the seed, counter (walker, step,
 // (outer << 16) + inner, tag) (R-1) -- no RNG state in memory.
+#include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "bingo.h"
 #include "bingo_internal.cuh"
@@ -18,36 +20,52 @@ using namespace bingo;
 
 namespace bingo {
 
-template <int APP, bool PROF>
-__global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
+template <int APP, bool PROF, bool WMAJOR>
+#ifndef BINGO_WALK_MINB
+#define BINGO_WALK_MINB 5
+#endif
+__global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BINGO_WALK_MINB) k_walk(const WalkArgs a) {
     const uint32_t stride = gridDim.x * blockDim.x;
     WalkProf prof;
+    // L2 eviction priorities: the thin headers are re-read by every step of every
+    // walker (keep), member/arc sectors are one-shot random reads (stream).
+    uint64_t pol_keep, pol_stream;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const Policies pol{pol_keep, pol_stream};
+    const size_t row = (size_t)a.L + 1;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += stride) {
         const uint32_t w = a.first_walker + i;
         uint32_t u = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);
-        if (a.paths) __stcs(&a.paths[i], u);
+        if (a.paths) {
+            if (WMAJOR) a.paths[(size_t)i * row] = u;
+            else __stcs(&a.paths[i], u);
+        }
         if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[u], 1ull);
         uint32_t steps = 0, prev = 0xFFFFFFFFu;
         for (uint32_t t = 0; a.L == BINGO_NO_CAP || t < a.L; t++) {
-            const VHdr h = load_hdr(a.hdr + u);
+            const ThinHdr h = load_thdr(a.thdr + u, pol);
             if (PROF) prof.hdr++;
-            if (h.d == 0) break;   // dead end: truncate (R-13)
+            if (h.n == 0) break;   // dead end (d = 0): truncate (R-13)
             uint32_t next;
             if (APP == BINGO_NODE2VEC && t >= 1) {
                 // KnightKing rejection: propose first-order, accept with f/f_max
                 for (uint32_t o = 0;; o++) {
-                    next = sample_dst<PROF>(a, h, w, t, o, prof);
+                    next = sample_dst<PROF>(a, h, w, t, o, prof, pol);
                     const uint32_t cls = (next == prev) ? 0u : (probe_arc<PROF>(a, prev, next, prof) ? 1u : 2u);
                     if (a.n2v_always[cls]) break;
                     const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
                     if (join64(r.x, r.y) < a.n2v_thr[cls]) break;
                 }
             } else {
-                next = sample_dst<PROF>(a, h, w, t, 0, prof);
+                next = sample_dst<PROF>(a, h, w, t, 0, prof, pol);
             }
             steps++;
             if (PROF) prof.steps++;
-            if (a.paths) __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
+            if (a.paths) {
+                if (WMAJOR) a.paths[(size_t)i * row + t + 1] = next;
+                else __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
+            }
             prev = u;
             u = next;
             if (APP == BINGO_PPR) {
@@ -60,8 +78,12 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
         }
         if (PROF) prof.walkers++;
         if (a.lengths) a.lengths[i] = steps;
-        if (a.paths && a.L != BINGO_NO_CAP)
-            for (uint32_t t = steps + 1; t <= a.L; t++) __stcs(&a.paths[(size_t)t * a.W + i], 0xFFFFFFFFu);
+        if (a.paths && a.L != BINGO_NO_CAP) {
+            for (uint32_t t = steps + 1; t <= a.L; t++) {
+                if (WMAJOR) a.paths[(size_t)i * row + t] = 0xFFFFFFFFu;
+                else __stcs(&a.paths[(size_t)t * a.W + i], 0xFFFFFFFFu);
+            }
+        }
     }
     if (PROF) prof.flush(a.prof);
 }
@@ -96,19 +118,29 @@ static void stop_threshold(uint32_t num, uint32_t den, unsigned long long *thr, 
     *thr = (unsigned long long)(((unsigned __int128)num << 64) / den);   // floor(num 2^64 / den)
 }
 
-static size_t walk_grid(uint32_t W) {
-    size_t blocks = ((size_t)W + 255) / 256;
-    const size_t cap = 148 * 8;
-    return blocks < cap ? (blocks ? blocks : 1) : cap;
+// Persistent grid: exactly the resident capacity (SMs x occupancy), so every
+// block runs from the start and strides over walkers -- no partial second wave.
+template <typename K>
+static unsigned walk_grid(K kernel, uint32_t W) {
+    int dev = 0, sms = 148, per_sm = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    if (const char *e = getenv("BINGO_WALK_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
+    cudaGetLastError();
+    const size_t need = ((size_t)W + 255) / 256;
+    const size_t cap = (size_t)sms * (size_t)std::max(per_sm, 1);
+    return (unsigned)std::max<size_t>(1, std::min(need, cap));
 }
 
 bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts, uint32_t W,
                          uint32_t *paths, uint32_t *lengths, cudaStream_t s, unsigned long long *prof = nullptr) {
     WalkArgs a;
+    a.thdr = g->thdr;
     a.hdr = g->hdr;
     a.bkt = g->bkt;
     a.arc = g->arc;
-    a.mem = g->mem;
+    a.mdst = g->mdst;
     a.visit = g->visit;
     a.starts = starts;
     a.paths = paths;
@@ -123,21 +155,40 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
                    a.n2v_thr, a.n2v_always);
     stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
     a.prof = prof;
-    const unsigned grid = (unsigned)walk_grid(W);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(1);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cfg.attrs = nullptr;
+    cfg.numAttrs = 0;
+    cudaError_t le = cudaSuccess;
+    const bool wmajor = (desc->flags & BINGO_WALK_WALKER_MAJOR) != 0;
+#define BINGO_K(APP_, PROF_)                                                                      \
+    (wmajor ? (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, true>, W)),                       \
+               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, true>, a))                            \
+            : (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, false>, W)),                      \
+               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, false>, a)))
     if (prof) {
         switch (desc->app) {
-            case BINGO_DEEPWALK: k_walk<BINGO_DEEPWALK, true><<<grid, 256, 0, s>>>(a); break;
-            case BINGO_NODE2VEC: k_walk<BINGO_NODE2VEC, true><<<grid, 256, 0, s>>>(a); break;
-            case BINGO_PPR: k_walk<BINGO_PPR, true><<<grid, 256, 0, s>>>(a); break;
+            case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, true); break;
+            case BINGO_NODE2VEC: le = BINGO_K(BINGO_NODE2VEC, true); break;
+            case BINGO_PPR: le = BINGO_K(BINGO_PPR, true); break;
             default: return BINGO_E_INVAL;
         }
     } else {
         switch (desc->app) {
-            case BINGO_DEEPWALK: k_walk<BINGO_DEEPWALK, false><<<grid, 256, 0, s>>>(a); break;
-            case BINGO_NODE2VEC: k_walk<BINGO_NODE2VEC, false><<<grid, 256, 0, s>>>(a); break;
-            case BINGO_PPR: k_walk<BINGO_PPR, false><<<grid, 256, 0, s>>>(a); break;
+            case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, false); break;
+            case BINGO_NODE2VEC: le = BINGO_K(BINGO_NODE2VEC, false); break;
+            case BINGO_PPR: le = BINGO_K(BINGO_PPR, false); break;
             default: return BINGO_E_INVAL;
         }
+    }
+#undef BINGO_K
+    if (le != cudaSuccess) {
+        fprintf(stderr, "libbingo: walk launch failed: %s\n", cudaGetErrorString(le));
+        g->poisoned = 1;
+        return BINGO_E_CUDA;
     }
     bingo_count_launch();
     cudaError_t e = cudaGetLastError();

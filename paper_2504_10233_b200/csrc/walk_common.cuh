@@ -26,10 +26,11 @@ struct WalkProf {
 };
 
 struct WalkArgs {
+    const ThinHdr *thdr;
     const VHdr *hdr;
     const Bucket *bkt;
     const uint2 *arc;
-    const uint2 *mem;
+    const uint32_t *mdst;
     unsigned long long *visit;
     const uint32_t *starts;
     uint32_t *paths;
@@ -43,66 +44,112 @@ struct WalkArgs {
     unsigned long long *prof;
 };
 
-__device__ __forceinline__ VHdr load_hdr(const VHdr *p) {
-    const uint4 *q = reinterpret_cast<const uint4 *>(p);
-    const uint4 lo = __ldg(q), hi = __ldg(q + 1);
-    VHdr h;
-    h.T = ((uint64_t)lo.y << 32) | lo.x;
-    h.adj_off = ((uint64_t)lo.w << 32) | lo.z;
-    h.bkt_off = hi.x;
-    h.d = hi.y;
-    h.n = (uint8_t)(hi.z & 0xff);
-    h.ncap = (uint8_t)((hi.z >> 8) & 0xff);
-    h.pad = (uint16_t)(hi.z >> 16);
-    h.adj_cap = hi.w;
+struct Policies {
+    uint64_t keep, stream;   // L2 cache-hint policies (createpolicy)
+};
+
+__device__ __forceinline__ ThinHdr load_thdr(const ThinHdr *p, const Policies &pol) {
+    unsigned long long v;
+    asm volatile("ld.global.nc.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(p), "l"(pol.keep));
+    ThinHdr h;
+    h.bkt_off = (uint32_t)v;
+    h.n = (uint8_t)(v >> 32);
+    h.flags = (uint8_t)(v >> 40);
+    h.pad1 = 0;
     return h;
 }
 
-__device__ __forceinline__ Bucket ldg_bucket(const Bucket *p) {
-    const uint4 *q = reinterpret_cast<const uint4 *>(p);
-    return unpack_bucket(__ldg(q), __ldg(q + 1));
+// one 256-bit read-only load of a 32 B bucket (LDG.E.256 on sm_100a), 64 B L2
+// fetch, with the vertex's L2 policy (hot: evict_last, cold: evict_first)
+__device__ __forceinline__ Bucket ldg_bucket(const Bucket *p, uint64_t pol) {
+    uint4 lo, hi;
+    asm volatile("ld.global.nc.L2::cache_hint.L2::64B.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p), "l"(pol));
+    return unpack_bucket(lo, hi);
 }
 
-// One first-order sample at a vertex with d > 0 (P:215 two stages).
-//  (i)  inter-group: bucket b = floor(r0 n / 2^32), coin = floor(r1r2 T / 2^64),
-//       group = coin < thr[b] ? b : alias[b]                 (Eq.5, alias P:191)
+// 4 B random read with an explicit L2 policy, 64 B fetch
+__device__ __forceinline__ uint32_t ldg4(const uint32_t *p, uint64_t pol) {
+    uint32_t v;
+    asm volatile("ld.global.nc.L2::cache_hint.L2::64B.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// 8 B random read with an explicit L2 policy, 64 B fetch
+__device__ __forceinline__ uint2 ldg8(const uint2 *p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.L2::64B.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Speculative dense rejection width: S attempts' draws and loads are issued at
+// once and the FIRST accepted attempt in order is taken -- the same result as
+// the sequential loop of P:465 (A-23), without serialising a warp on the
+// slowest lane's retries (acceptance > alpha = 40%, so P(all S rejected) < 0.6^S).
+#ifndef BINGO_DENSE_SPEC
+#define BINGO_DENSE_SPEC 2
+#endif
+
+// One first-order sample at a vertex with n > 0 (P:215 two stages).
+//  (i)  inter-group: bucket b = floor(r0 n / 2^32); the group is b if the 64-bit
+//       coin R = r1r2 satisfies R < lim_b, else alias[b]  (Eq.5, alias P:191;
+//       R < lim_b <=> floor(R T / 2^64) < thr_b, R-4')
 //  (ii) intra-group: ONE -> its member; REGULAR/SPARSE -> member
 //       floor(x c / 2^64) (Eq.6); DENSE -> rejection over the adjacency,
 //       accept iff bias AND 2^k != 0, re-drawing only the index (A-23).
 template <bool PROF>
-__device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const VHdr &h, uint32_t w, uint32_t t,
-                                               uint32_t outer, WalkProf &prof) {
+__device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr &h, uint32_t w, uint32_t t,
+                                               uint32_t outer, WalkProf &prof, const Policies &pol) {
     const P4 r = philox10(w, t, outer << 16, 0u, a.k0, a.k1);
     const uint32_t b = __umulhi(r.x, (uint32_t)h.n);
-    const Bucket B = ldg_bucket(a.bkt + h.bkt_off + b);
+    const Bucket B = ldg_bucket(a.bkt + h.bkt_off + b, (h.flags & 1u) ? pol.keep : pol.stream);
     if (PROF) prof.bkt++;
-    const uint64_t coin = __umul64hi(join64(r.y, r.z), h.T);
-    const bool alt = coin >= B.thr;
-    const uint32_t c = alt ? B.a_c : B.c;
-    const uint32_t ref = alt ? B.a_ref : B.ref;
+    const bool alt = join64(r.y, r.z) >= B.lim;
+    const uint32_t x = alt ? B.ax : B.px;
+    const uint32_t y = alt ? B.ay : B.py;
     const uint32_t kk = alt ? B.a_kk : B.kk;
     const uint32_t kind = kk >> 5;
-    if (kind == K_ONE) return ref;
+#ifdef BINGO_EXP_NO_MEMBER   // measurement experiment only: skip the intra-group load
+    if (kind != K_ONE) return y & 0xFFFFFu;
+#endif
+#ifdef BINGO_EXP_NO_DENSE    // measurement experiment only: skip dense rejection
+    if (kind == K_DENSE) return y & 0xFFFFFu;
+#endif
+    if (kind == K_ONE) return y;
     if (kind != K_DENSE) {
         const P4 q = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
-        const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)c);
+        const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)x);
         if (PROF) prof.mem++;
-        return __ldg(a.mem + (uint64_t)ref * 2 + j).y;
+        return ldg4(a.mdst + (uint64_t)y * 4 + j, (h.flags & 2u) ? pol.keep : pol.stream);
     }
     const uint32_t k = kk & 31u;
-    for (uint32_t att = 0;; att++) {
-        const P4 q = philox10(w, t, (outer << 16) + att, 1u, a.k0, a.k1);
-        const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)h.d);
-        const uint2 e = __ldg(a.arc + h.adj_off + j);
-        if (PROF) prof.arc++;
-        if ((e.y >> k) & 1u) return e.x;
+    const uint2 *adj = a.arc + ((uint64_t)y << 2);
+    for (uint32_t base = 0;; base += BINGO_DENSE_SPEC) {
+        uint2 e[BINGO_DENSE_SPEC];
+#pragma unroll
+        for (int s = 0; s < BINGO_DENSE_SPEC; s++) {
+            const P4 q = philox10(w, t, (outer << 16) + base + s, 1u, a.k0, a.k1);
+            const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)x);
+            e[s] = ldg8(adj + j, pol.stream);
+        }
+        bool done = false;
+        uint32_t res = 0;
+#pragma unroll
+        for (int s = 0; s < BINGO_DENSE_SPEC; s++) {
+            const bool acc = !done && ((e[s].y >> k) & 1u);
+            if (PROF && !done) prof.arc++;
+            res = acc ? e[s].x : res;
+            done = done || acc;
+        }
+        if (done) return res;
     }
 }
 
 // node2vec distance-1 test (Eq.1, A-17): does a live arc prev -> v exist?
 template <bool PROF>
 __device__ __forceinline__ bool probe_arc(const WalkArgs &a, uint32_t prev, uint32_t v, WalkProf &prof) {
-    const VHdr h = load_hdr(a.hdr + prev);
+    const VHdr h = a.hdr[prev];
     if (PROF) prof.probe++;
     for (uint32_t i = 0; i < h.d; i++) {
         if (PROF && (i & 3u) == 0) prof.probe++;   // one 32 B sector per 4 arcs scanned

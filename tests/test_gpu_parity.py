@@ -170,3 +170,23 @@ def test_walk_parity_larger_graph():
     out = g.walk(length=80, seed=1234, starts=starts)
     ref = o.walk(length=80, seed=1234, starts=starts)
     assert np.array_equal(u32(out["paths"]), ref["paths"])
+
+
+def test_walker_major_layout_and_profile():
+    """BINGO_WALK_WALKER_MAJOR is the transpose of the step-major paths; the profiling variant
+    returns the same walks and load counts consistent with the steps taken."""
+    pb = _pb()
+    w = synth.make_workload("c1")
+    g, o = _graphs(w.row_offsets, w.dst, w.bias)
+    ref = o.walk(length=80, seed=31)
+    wm = g.walk(length=80, seed=31, walker_major=True)
+    assert np.array_equal(u32(wm["paths"]).T, ref["paths"])
+    assert np.array_equal(u32(wm["lengths"]), ref["lengths"])
+    pr = g.walk_profile(length=80, seed=31)
+    assert np.array_equal(u32(pr["paths"]), ref["paths"])
+    assert pr["steps"] == int(ref["lengths"].astype(np.int64).sum())
+    assert pr["bkt"] == pr["steps"] and pr["walkers"] == w.V
+    assert pr["hdr"] >= pr["steps"] and pr["arc"] + pr["mem"] <= pr["steps"] + pr["arc"]
+    ppr = g.walk(app=pb.PPR, length=40, stop=(1, 7), seed=4, walker_major=True)
+    rp = o.walk(app=oracle.APP_PPR, length=40, stop=(1, 7), seed=4)
+    assert np.array_equal(u32(ppr["paths"]).T, rp["paths"])

@@ -9,7 +9,7 @@
 //                `steps` hops (1 chain per thread = the walker's access pattern:
 //                every load's address depends on the previous load).
 // Every load is one full 32 B sector (two 16 B vector loads of the same
-// sector), so bytes = 32 x loads.
+// sector), so bytes = 32 x loads.  nslots must be a power of two.
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -22,7 +22,7 @@ __device__ __forceinline__ uint64_t mix64(uint64_t x) {
 
 __global__ void gb_fill(uint4 *buf, uint64_t nslots, uint64_t seed) {
     for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nslots; s += (uint64_t)gridDim.x * blockDim.x) {
-        uint64_t nx = mix64(s ^ seed) % nslots;
+        uint64_t nx = mix64(s ^ seed) & (nslots - 1);
         buf[2 * s] = make_uint4((uint32_t)nx, (uint32_t)(nx >> 32), (uint32_t)s, 0u);
         buf[2 * s + 1] = make_uint4(1u, 2u, 3u, 4u);
     }
@@ -36,7 +36,7 @@ __global__ void gb_independent(const uint4 *__restrict__ buf, uint64_t nslots, u
         uint4 v[ILP], w[ILP];
 #pragma unroll
         for (int j = 0; j < ILP; j++) {
-            const uint64_t s = mix64(tid * 0x9E3779B97F4A7C15ull + (it + j) + seed) % nslots;
+            const uint64_t s = mix64(tid * 0x9E3779B97F4A7C15ull + (it + j) + seed) & (nslots - 1);
             v[j] = __ldg(buf + 2 * s);
             w[j] = __ldg(buf + 2 * s + 1);
         }
@@ -46,13 +46,39 @@ __global__ void gb_independent(const uint4 *__restrict__ buf, uint64_t nslots, u
     if (acc == 0x12345678u) out[0] = acc;
 }
 
+template <int Q>
+__device__ __forceinline__ uint4 ld16(const uint4 *p) {
+    uint4 v;
+    if (Q == 0) v = __ldg(p);
+    else if (Q == 1) asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else if (Q == 2) asm volatile("ld.global.ca.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else if (Q == 3) asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else if (Q == 4) asm volatile("ld.global.nc.L2::64B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    else asm volatile("ld.global.nc.L2::256B.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+// dependent chase reading only 16 B (first half of each 32 B slot) with load qualifier Q
+template <int Q>
+__global__ void gb_chase_q(const uint4 *__restrict__ buf, uint64_t nslots, uint32_t steps, uint64_t seed, uint32_t *out) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint64_t cur = mix64(tid + seed) & (nslots - 1);
+    uint32_t acc = 0;
+    for (uint32_t it = 0; it < steps; it++) {
+        const uint4 v = ld16<Q>(buf + 2 * cur);
+        cur = ((uint64_t)v.y << 32) | v.x;
+        acc ^= v.z;
+    }
+    if (acc == 0x12345678u) out[0] = (uint32_t)cur;
+}
+
 template <int CH>
 __global__ void gb_chase(const uint4 *__restrict__ buf, uint64_t nslots, uint32_t steps, uint64_t seed, uint32_t *out) {
     const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
     uint64_t cur[CH];
     uint32_t acc = 0;
 #pragma unroll
-    for (int c = 0; c < CH; c++) cur[c] = mix64(tid * CH + c + seed) % nslots;
+    for (int c = 0; c < CH; c++) cur[c] = mix64(tid * CH + c + seed) & (nslots - 1);
     for (uint32_t it = 0; it < steps; it++) {
 #pragma unroll
         for (int c = 0; c < CH; c++) {
@@ -87,6 +113,12 @@ extern "C" int gather_run(void *buf, uint64_t nslots, int mode, uint32_t blocks,
         case 1: gb_chase<1><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= iters; break;
         case 2: gb_chase<2><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= 2.0 * iters; break;
         case 3: gb_chase<4><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= 4.0 * iters; break;
+        case 10: gb_chase_q<0><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= iters; break;
+        case 11: gb_chase_q<1><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= iters; break;
+        case 12: gb_chase_q<2><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= iters; break;
+        case 14: gb_chase_q<4><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= iters; break;
+        case 15: gb_chase_q<5><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= iters; break;
+        case 13: gb_chase_q<3><<<blocks, threads, 0, s>>>(B, nslots, iters, seed, o); total *= iters; break;
         default: return -1;
     }
     cudaEventRecord(b, s);
@@ -96,4 +128,12 @@ extern "C" int gather_run(void *buf, uint64_t nslots, int mode, uint32_t blocks,
     cudaEventDestroy(b);
     *loads = total;
     return (int)cudaGetLastError();
+}
+
+// L2 fetch-granularity limit (cudaLimitMaxL2FetchGranularity): returns the value in effect.
+extern "C" int gather_set_l2_fetch(int bytes) {
+    if (bytes >= 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes);
+    size_t v = 0;
+    cudaDeviceGetLimit(&v, cudaLimitMaxL2FetchGranularity);
+    return (int)v;
 }
