@@ -59,7 +59,10 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
  *   order (R-2); every arc gets epoch 0.
  * alpha_pct / beta_pct: Eq.9 thresholds (paper: 40 / 10).
  * flags: BINGO_BUILD_BS_MODE forces the paper's all-regular baseline (
- *   alpha = 100, beta = 0, no one-element groups).
+ *   alpha = 100, beta = 0, no one-element groups).  BINGO_BUILD_NEIGHBOR_INDEX
+ *   keeps a per-vertex hash set of destination ids (derived state, rebuilt for
+ *   touched vertices by every update) so node2vec's "arc prev -> v exists?"
+ *   test (Eq.1, A-17) is one probe instead of a scan of adj(prev).
  * arc_slack / member_slack: fraction of extra per-vertex capacity reserved
  *   for growth (Hornet-style dynamic arrays + memory pool);
  *   pool_reserve: extra fraction of every pool for relocations.
@@ -70,6 +73,7 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
  *   NOMEM, CUDA.  Synchronises `stream`.  *out receives the new graph.
  * ------------------------------------------------------------------------- */
 #define BINGO_BUILD_BS_MODE 1u
+#define BINGO_BUILD_NEIGHBOR_INDEX 2u /* keep per-vertex neighbour hash sets: O(1) node2vec distance test */
 
 typedef void *(*bingo_alloc_fn)(size_t bytes, void *ctx);
 typedef void (*bingo_free_fn)(void *ptr, void *ctx);

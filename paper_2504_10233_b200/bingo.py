@@ -21,6 +21,7 @@ OK, E_INVAL, E_NOMEM, E_CUDA, E_OVERFLOW, E_STATE = 0, 1, 2, 3, 4, 5
 EMPTY, ONE, DENSE, SPARSE, REGULAR = 0, 1, 2, 3, 4
 DEEPWALK, NODE2VEC, PPR = 0, 1, 2
 BUILD_BS_MODE = 1
+BUILD_NEIGHBOR_INDEX = 2
 UPD_HOST_BATCH = 1
 WALK_HOST_OUTPUT = 1
 WALK_WALKER_MAJOR = 2
@@ -175,7 +176,7 @@ class Graph:
 
     def __init__(self, row_offsets, dst, bias, alpha: int = 40, beta: int = 10, bs_mode: bool = False,
                  arc_slack: float = 0.25, member_slack: float = 0.25, pool_reserve: float = 0.1,
-                 device=None, stream=None, torch_alloc: bool = True):
+                 neighbor_index: bool = False, device=None, stream=None, torch_alloc: bool = True):
         torch = _torch()
         L = _lib()
         self.device = torch.device(device if device is not None else "cuda")
@@ -187,7 +188,8 @@ class Graph:
         self.V = ro.numel() - 1
         self._alloc = _TorchAllocator(self.device) if torch_alloc else None
         d = BuildDesc(num_vertices=self.V, num_arcs=ds.numel(), row_offsets=ro.data_ptr(), dst=ds.data_ptr(),
-                      bias=bs.data_ptr(), alpha_pct=alpha, beta_pct=beta, flags=BUILD_BS_MODE if bs_mode else 0,
+                      bias=bs.data_ptr(), alpha_pct=alpha, beta_pct=beta,
+                      flags=(BUILD_BS_MODE if bs_mode else 0) | (BUILD_NEIGHBOR_INDEX if neighbor_index else 0),
                       arc_slack=arc_slack, member_slack=member_slack, pool_reserve=pool_reserve,
                       alloc=self._alloc.alloc if self._alloc else ALLOC_FN(), free=self._alloc.free if self._alloc else FREE_FN(),
                       alloc_ctx=None)

@@ -157,6 +157,8 @@ struct bingo_graph {
     uint32_t hot_mem_degree = 0xFFFFFFFFu; // d >= this: member dsts loaded evict_last
     uint32_t *mdst = nullptr;          // [mem_cap] member dst (walker side)
     uint32_t *midx = nullptr;          // [mem_cap] member adjacency index (canonical)
+    uint32_t *nbt = nullptr;           // [4 * arc_cap] neighbour hash sets (node2vec), optional
+    uint64_t *nbo = nullptr;           // [V] hash-set base | log2 size << 48
     uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
     unsigned long long *visit = nullptr;     // [V] PPR visit counts

@@ -18,6 +18,7 @@
 #include "bingo.h"
 #include "bingo_internal.cuh"
 #include "build_common.cuh"
+#include "nbr_index.cuh"
 #include "scan.cuh"
 
 using namespace bingo;
@@ -200,6 +201,23 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
     }
 }
 
+// neighbour hash sets (node2vec distance test), warp per vertex
+__global__ void k_build_nbt(uint32_t V, const VHdr *__restrict__ hdr, const uint2 *__restrict__ arc,
+                            uint32_t *__restrict__ nbt, uint64_t *__restrict__ nbo) {
+    const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
+    const uint32_t lane = lane_id();
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+        const VHdr h = hdr[u];
+        const uint32_t lg = nb_log2size(h.d);
+        const uint64_t base = 4 * h.adj_off;
+        uint32_t *tbl = nbt + base;
+        for (uint32_t j = lane; j < (1u << lg); j += 32) tbl[j] = NB_EMPTY;
+        __syncwarp();
+        for (uint32_t i = lane; i < h.d; i += 32) nb_insert(tbl, (1u << lg) - 1, arc[h.adj_off + i].x);
+        if (lane == 0) nbo[u] = nb_pack(base, lg);
+    }
+}
+
 }  // namespace bingo
 
 // ---------------------------------------------------------------- host side
@@ -346,6 +364,16 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
                                             g->hot_bkt_degree, g->hot_mem_degree);
         bingo_count_launch();
         CK(cudaGetLastError());
+    }
+    if (desc->flags & BINGO_BUILD_NEIGHBOR_INDEX) {
+        g->nbt = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * g->arc_cap);
+        g->nbo = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * std::max<uint64_t>(nV, 1));
+        if (!g->nbt || !g->nbo) { st = BINGO_E_NOMEM; goto done; }
+        if (V) {
+            k_build_nbt<<<blocks, 256, 0, s>>>(V, g->hdr, g->arc, g->nbt, g->nbo);
+            bingo_count_launch();
+            CK(cudaGetLastError());
+        }
     }
     CK(cudaStreamSynchronize(s));
 done:

@@ -27,6 +27,7 @@
 #include "bingo.h"
 #include "bingo_internal.cuh"
 #include "build_common.cuh"
+#include "nbr_index.cuh"
 #include "scan.cuh"
 #include "sort.cuh"
 
@@ -253,6 +254,8 @@ struct MutateArgs {
     Bucket *bkt;
     GCan *gcan;
     uint32_t *mdst, *midx;
+    uint32_t *nbt;
+    uint64_t *nbo;
     unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units
     uint32_t *vstats;           // [ntouch][VST]
     uint32_t epoch, alpha, beta, hot_b, hot_m;
@@ -704,6 +707,15 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             a.thdr[u] = th;
         }
     }
+    if (a.nbt) {
+        // neighbour hash set of the post-batch adjacency (node2vec distance test)
+        const uint32_t lg = nb_log2size(dn);
+        uint32_t *tbl = a.nbt + 4 * aoff;
+        for (uint32_t j = tid; j < (1u << lg); j += MT) tbl[j] = NB_EMPTY;
+        __syncthreads();
+        for (uint32_t i = tid; i < dn; i += MT) nb_insert(tbl, (1u << lg) - 1, a.arc[aoff + i].x);
+        if (tid == 0) a.nbo[u] = nb_pack(4 * aoff, lg);
+    }
 }
 
 __global__ void k_upd_stats(const uint32_t *__restrict__ vstats, uint32_t ntouch, unsigned long long *__restrict__ out) {
@@ -767,6 +779,15 @@ bingo_status grow_pool(bingo_graph *g, int which, uint64_t need_total, cudaStrea
             cudaMemcpyAsync(ne, g->arc_epoch, 4 * g->arc_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess)
             return BINGO_E_CUDA;
+        if (g->nbt) {
+            uint32_t *nt = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * cap);
+            if (!nt) { bingo_dev_free(g, na); bingo_dev_free(g, ne); return BINGO_E_NOMEM; }
+            if (cudaMemcpyAsync(nt, g->nbt, sizeof(uint32_t) * 4 * g->arc_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                return BINGO_E_CUDA;
+            bingo_dev_free(g, g->nbt);
+            g->nbt = nt;
+        }
         bingo_dev_free(g, g->arc);
         bingo_dev_free(g, g->arc_epoch);
         g->arc = na; g->arc_epoch = ne; g->arc_cap = cap;
@@ -942,6 +963,8 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     ma.gcan = g->gcan;
     ma.mdst = g->mdst;
     ma.midx = g->midx;
+    ma.nbt = g->nbt;
+    ma.nbo = g->nbo;
     ma.bump = g->counters;
     ma.vstats = vstats;
     ma.epoch = e;

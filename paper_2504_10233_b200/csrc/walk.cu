@@ -43,8 +43,10 @@ __global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BIN
         }
         if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[u], 1ull);
         uint32_t steps = 0, prev = 0xFFFFFFFFu;
+        uint64_t prev_nbo = 0, cur_nbo = 0;
         for (uint32_t t = 0; a.L == BINGO_NO_CAP || t < a.L; t++) {
             const ThinHdr h = load_thdr(a.thdr + u, pol);
+            if (APP == BINGO_NODE2VEC && a.nbo) cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
             if (PROF) prof.hdr++;
             if (h.n == 0) break;   // dead end (d = 0): truncate (R-13)
             uint32_t next;
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BIN
                 // KnightKing rejection: propose first-order, accept with f/f_max
                 for (uint32_t o = 0;; o++) {
                     next = sample_dst<PROF>(a, h, w, t, o, prof, pol);
-                    const uint32_t cls = (next == prev) ? 0u : (probe_arc<PROF>(a, prev, next, prof) ? 1u : 2u);
+                    const uint32_t cls = (next == prev) ? 0u : (probe_arc<PROF>(a, prev, prev_nbo, next, prof) ? 1u : 2u);
                     if (a.n2v_always[cls]) break;
                     const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
                     if (join64(r.x, r.y) < a.n2v_thr[cls]) break;
@@ -67,6 +69,7 @@ __global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BIN
                 else __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
             }
             prev = u;
+            prev_nbo = cur_nbo;
             u = next;
             if (APP == BINGO_PPR) {
                 if (a.visit) atomicAdd(&a.visit[u], 1ull);
@@ -141,6 +144,8 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     a.bkt = g->bkt;
     a.arc = g->arc;
     a.mdst = g->mdst;
+    a.nbt = g->nbt;
+    a.nbo = g->nbo;
     a.visit = g->visit;
     a.starts = starts;
     a.paths = paths;

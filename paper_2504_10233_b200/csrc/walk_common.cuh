@@ -4,6 +4,7 @@
 
 #include "bingo_internal.cuh"
 #include "build_common.cuh"
+#include "nbr_index.cuh"
 
 namespace bingo {
 
@@ -31,6 +32,8 @@ struct WalkArgs {
     const Bucket *bkt;
     const uint2 *arc;
     const uint32_t *mdst;
+    const uint32_t *nbt;
+    const uint64_t *nbo;
     unsigned long long *visit;
     const uint32_t *starts;
     uint32_t *paths;
@@ -147,8 +150,15 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
 }
 
 // node2vec distance-1 test (Eq.1, A-17): does a live arc prev -> v exist?
+// With the neighbour index: one hash-set probe (prev's table base/mask were
+// loaded while the walker stood at prev).  Without: a scan of adj(prev).
 template <bool PROF>
-__device__ __forceinline__ bool probe_arc(const WalkArgs &a, uint32_t prev, uint32_t v, WalkProf &prof) {
+__device__ __forceinline__ bool probe_arc(const WalkArgs &a, uint32_t prev, uint64_t prev_nbo, uint32_t v,
+                                          WalkProf &prof) {
+    if (a.nbt) {
+        if (PROF) prof.probe++;
+        return nb_contains(a.nbt + nb_base(prev_nbo), nb_mask(prev_nbo), v);
+    }
     const VHdr h = a.hdr[prev];
     if (PROF) prof.probe++;
     for (uint32_t i = 0; i < h.d; i++) {

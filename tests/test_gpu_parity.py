@@ -131,13 +131,21 @@ def test_walk_edge_cases():
         assert np.array_equal(u32(out["lengths"]), ref["lengths"])
 
 
-@pytest.mark.parametrize("p,q", [(2.0, 0.5), (0.5, 2.0), (1.0, 1.0)])
-def test_node2vec_parity(p, q):
+@pytest.mark.parametrize("p,q,index", [(2.0, 0.5, True), (0.5, 2.0, True), (1.0, 1.0, True), (2.0, 0.5, False)])
+def test_node2vec_parity(p, q, index):
     pb = _pb()
     w = synth.make_workload("c1")
-    g, o = _graphs(w.row_offsets, w.dst, w.bias)
+    g = pb.Graph(w.row_offsets, w.dst, w.bias, neighbor_index=index)
+    o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
     out = g.walk(app=pb.NODE2VEC, length=40, p=p, q=q, seed=21)
     ref = o.walk(app=oracle.APP_NODE2VEC, length=40, p=p, q=q, seed=21)
+    assert np.array_equal(u32(out["paths"]), ref["paths"])
+    # the neighbour index follows updates
+    for b in synth.make_workload("c1", rounds=2).batches:
+        g.apply_updates(b)
+        o.apply_updates(b)
+    out = g.walk(app=pb.NODE2VEC, length=40, p=p, q=q, seed=22)
+    ref = o.walk(app=oracle.APP_NODE2VEC, length=40, p=p, q=q, seed=22)
     assert np.array_equal(u32(out["paths"]), ref["paths"])
 
 
