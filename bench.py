@@ -221,25 +221,27 @@ def main():
     batches = [torch.from_numpy(b.view(np.int32)) for b in w.batches]
     nrec = batches[0].shape[0]
     # inputs resident in HBM before the timed region (rank 0 holds the stream; others receive it)
-    dev_batches = [b.to(dev) for b in batches[:W + K]]
-    first = rank * V            # weak scaling: every rank walks one walker per vertex
+    dev_batches = [b.to(dev) for b in batches[:W + K]] if rank == 0 else [None] * (W + K)
+    first = rank * V            # this rank's first walker id (weak scaling: V walkers per rank)
     wmajor = args.layout == "walker"
     paths = torch.empty((V, L + 1) if wmajor else (L + 1, V), dtype=torch.int32, device=dev)
     lens = [torch.empty(V, dtype=torch.int32, device=dev) for _ in range(K)]
     scratch_len = torch.empty(V, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream()
 
+    from paper_2504_10233_b200.distributed import ReplicatedBingo
+    rb = ReplicatedBingo(g, device=dev)
+
     def step(i, out_len, ev=None):
-        b = dev_batches[i]
-        if dist is not None:
-            dist.broadcast(b, 0)          # rank 0's batch reaches every replica over NVLink
         if ev is not None:
             ev[0].record(stream)
-        g.apply_updates(b)
+        # rank 0's batch is broadcast to every replica inside the step (NCCL over NVLink)
+        rb.apply_updates(dev_batches[i] if rank == 0 else None)
         if ev is not None:
             ev[1].record(stream)
-        g.walk(app=pb.DEEPWALK, length=L, seed=1000 + i, first_walker=first, num_walkers=V, paths=paths,
-               lengths=out_len, walker_major=wmajor)
+        # walker ids [rank*V, (rank+1)*V): one walker per vertex per rank (weak scaling)
+        rb.walk(num_walkers=V * ws, app=pb.DEEPWALK, length=L, seed=1000 + i, paths=paths, lengths=out_len,
+                walker_major=wmajor)
         if ev is not None:
             ev[2].record(stream)
 

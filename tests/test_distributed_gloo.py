@@ -1,0 +1,114 @@
+"""-m "not gpu": the multi-GPU driver's host logic (paper_2504_10233_b200.distributed) on
+world_size 2 with the gloo backend on CPU.  The engine under the driver is the CPU
+oracle wrapped in the Graph interface (test infrastructure only): sharded walks must
+reproduce the unsharded run, replicas must stay identical after broadcast batches,
+and all-reduced PPR counts must equal the single-process counts."""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+class OracleEngine:
+    """Graph-like adapter over the oracle (tests only)."""
+
+    def __init__(self, w):
+        import oracle
+        self.o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
+        self.V = w.V
+        self.device = torch.device("cpu")
+        self._counts = np.zeros(self.V, dtype=np.uint64)
+
+    def apply_updates(self, batch):
+        return self.o.apply_updates(batch.numpy().view(np.uint32))
+
+    def walk(self, app=0, length=80, seed=0, first_walker=0, num_walkers=None, stop=(1, 80), **kw):
+        import oracle
+        counts = app == oracle.APP_PPR
+        r = self.o.walk(app=app, length=length, seed=seed, first_walker=first_walker, num_walkers=num_walkers,
+                        stop=stop, paths=length != oracle.NONE, counts=counts, threads=1)
+        if counts:
+            self._counts += r["counts"]
+        out = {"lengths": torch.from_numpy(r["lengths"].view(np.int32).copy())}
+        out["paths"] = torch.from_numpy(r["paths"].view(np.int32).copy()) if r["paths"] is not None else None
+        return out
+
+    def visit_counts(self, reset=False):
+        c = torch.from_numpy(self._counts.view(np.int64).copy())
+        if reset:
+            self._counts[:] = 0
+        return c
+
+    def digests(self):
+        return torch.from_numpy(self.o.digests().view(np.int64).copy())
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, outdir):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import synth
+    from paper_2504_10233_b200.distributed import ReplicatedBingo, shard_range
+    w = synth.make_workload("c1", rounds=3)
+    rb = ReplicatedBingo(OracleEngine(w))
+    for b in w.batches:
+        st = rb.apply_updates(torch.from_numpy(b.view(np.int32)) if rank == 0 else None)
+        assert st["epoch"] >= 1
+    assert rb.replicas_identical()
+    out = rb.walk(num_walkers=w.V, length=20, seed=3)
+    first, count = out["shard"]
+    assert (first, count) == shard_range(w.V, rank, world)
+    rb.walk(num_walkers=3 * w.V, length=oracle.NONE, app=oracle.APP_PPR, seed=4)
+    counts = rb.visit_counts()
+    np.save(os.path.join(outdir, f"paths{rank}.npy"), out["paths"].numpy())
+    np.save(os.path.join(outdir, f"counts{rank}.npy"), counts.numpy())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_shard_range_partitions():
+    from paper_2504_10233_b200.distributed import shard_range
+    for total in (0, 1, 7, 1000, 1001):
+        for world in (1, 2, 3, 8):
+            spans = [shard_range(total, r, world) for r in range(world)]
+            assert spans[0][0] == 0 and sum(c for _, c in spans) == total
+            for (f0, c0), (f1, _) in zip(spans, spans[1:]):
+                assert f0 + c0 == f1
+            assert max(c for _, c in spans) - min(c for _, c in spans) <= 1
+
+
+def test_two_rank_gloo_driver(tmp_path):
+    import oracle
+    import synth
+    world = 2
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    # single-process reference on the same stream
+    w = synth.make_workload("c1", rounds=3)
+    o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
+    for b in w.batches:
+        o.apply_updates(b)
+    full = o.walk(length=20, seed=3, num_walkers=w.V)["paths"]
+    parts = [np.load(tmp_path / f"paths{r}.npy").view(np.uint32) for r in range(world)]
+    assert np.array_equal(np.concatenate(parts, axis=1), full)
+    ref = o.walk(app=oracle.APP_PPR, length=oracle.NONE, seed=4, num_walkers=3 * w.V, paths=False, counts=True)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"counts{r}.npy").view(np.uint64), ref["counts"])
