@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-walkers", type=int, default=1 << 18)
-    ap.add_argument("--layout", default="walker", choices=["walker", "step"],
+    ap.add_argument("--layout", default="step", choices=["walker", "step"],
                     help="path layout written by the walk (walker-major: one contiguous walk per walker)")
     return ap.parse_args()
 

@@ -152,6 +152,7 @@ class _TorchAllocator:
         import torch
         self.device = torch.device(device)
         self.live = {}
+        release = torch.cuda.caching_allocator_delete     # bound now: callbacks may run at interpreter exit
 
         def _alloc(nbytes, ctx):
             try:
@@ -165,7 +166,10 @@ class _TorchAllocator:
         def _free(ptr, ctx):
             if ptr:
                 self.live.pop(ptr, None)
-                torch.cuda.caching_allocator_delete(ptr)
+                try:
+                    release(ptr)
+                except Exception:
+                    pass
 
         self.alloc = ALLOC_FN(_alloc)
         self.free = FREE_FN(_free)

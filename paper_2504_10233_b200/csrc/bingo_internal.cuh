@@ -173,6 +173,9 @@ struct bingo_graph {
     size_t wscratch_bytes = 0;
     void *vscratch = nullptr;                // per-touched-vertex delete scratch
     size_t vscratch_bytes = 0;
+    uint32_t *fast_scr = nullptr;            // small-batch fast path scratch (device)
+    void *fast_out_host = nullptr;           // mapped pinned status/stats of the fast path
+    void *fast_out_dev = nullptr;
 };
 
 // process-wide count of kernel launches issued by libbingo (api.cu)

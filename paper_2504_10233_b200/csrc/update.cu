@@ -22,6 +22,7 @@
 // Untouched vertices are never read or written.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "bingo.h"
@@ -37,7 +38,8 @@ namespace bingo {
 
 static constexpr uint32_t EMPTY_KEY = 0xFFFFFFFFu;
 static constexpr uint32_t DEL_MARK = 0xFFFFFFFFu;
-static constexpr int MT = 256;   // threads per mutate block
+static constexpr int MT = 256;   // threads per block (warp-per-vertex mutate, other kernels)
+static constexpr int LT = 1024;  // threads per block for large (hub) vertices
 
 // per-touched-vertex statistics: [0] deleted, [1] missing, [2..26] transitions
 static constexpr int VST = 28;
@@ -46,8 +48,14 @@ struct UpdCounters {        // device, zeroed per batch
     unsigned long long need_arc, need_bkt, need_mem, reserve_mem;
     unsigned long long scratch_words;
     int flag;
+    unsigned n_small, n_large;
     int pad;
 };
+
+// touched vertices whose post-insert adjacency or delete count exceed these go
+// to the block-per-vertex kernel; the rest are handled by one warp each
+// (BINGO_UPD_SMALL_L overrides the first, e.g. 0 to route everything to blocks in tests)
+static constexpr uint32_t SMALL_L = 2048, SMALL_Q = 128;
 
 __device__ __forceinline__ uint32_t hash_slot(uint32_t x, uint32_t mask) {
     x ^= x >> 16;
@@ -133,85 +141,123 @@ __device__ __forceinline__ void load_old_groups(const Bucket *bkt, const GCan *g
 }
 
 // ------------------------------------------------------------------ plan (no mutation)
+// Per touched vertex (one warp): overflow check (R-10) and the exact pool demand
+// of the batch -- relocations are exact, kind transitions a tight upper bound.
+struct PlanOut {
+    bool overflow;
+    uint32_t L, q;
+    unsigned long long arc, bkt, mem, res, words;
+};
+
+__device__ __forceinline__ PlanOut plan_vertex(const uint4 *__restrict__ recs, const uint32_t *__restrict__ sval,
+                                               uint32_t beg, uint32_t end, const VHdr &h,
+                                               const Bucket *__restrict__ bkt, const GCan *__restrict__ gcan,
+                                               uint32_t alpha, bool bs, double arc_slack, double mem_slack) {
+    const uint32_t lane = lane_id();
+    uint32_t kind_k, c_k, ref_k, aux_k;
+    OldGroups og;
+    load_old_groups(bkt, gcan, h, kind_k, c_k, ref_k, aux_k, og);
+    uint32_t m = 0, q = 0, ins_or = 0, insk = 0;
+    uint64_t ins_sum = 0;
+    for (uint32_t base = beg; base < end; base += 32) {
+        const uint32_t p = base + lane;
+        uint4 r = make_uint4(2u, 0u, 0u, 0u);
+        if (p < end) r = recs[sval[p]];
+        const bool ins = r.x == 0u, del = r.x == 1u;
+        const uint32_t w = ins ? r.w : 0u;
+        m += __popc(__ballot_sync(0xffffffffu, ins));
+        q += __popc(__ballot_sync(0xffffffffu, del));
+        ins_or |= w;
+        ins_sum += w;
+        uint32_t mk = __reduce_or_sync(0xffffffffu, w);
+        while (mk) {
+            const int k = __ffs(mk) - 1;
+            mk &= mk - 1;
+            const uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+            if (lane == (uint32_t)k) insk += __popc(bal);
+        }
+    }
+    ins_or = __reduce_or_sync(0xffffffffu, ins_or);
+    ins_sum = warp_sum(ins_sum);
+    PlanOut o;
+    // overflow: (T + inserted) * popc(mask | inserted) < 2^64 and d + m < 2^32 - 1 (R-10)
+    const uint32_t nb = __popc(og.mask | ins_or);
+    const uint64_t Tn = h.T + ins_sum;
+    o.overflow = Tn < h.T || __umul64hi(Tn, (uint64_t)nb) != 0 || (uint64_t)h.d + m >= 0xFFFFFFFFull;
+    const uint32_t L = h.d + m;
+    uint64_t need_mem = 0, reserve = 0;
+    const uint32_t cin = c_k + insk;
+    if (is_list(kind_k)) {
+        if (cin > aux_k) need_mem = member_units(cin, mem_slack);
+    } else if (bs) {
+        if (cin >= 1 && kind_k == K_EMPTY) reserve = member_units(cin, mem_slack);
+    } else if (kind_k == K_EMPTY) {
+        if (insk >= 2) reserve = member_units(cin, mem_slack);
+    } else if (kind_k == K_ONE) {
+        if (insk >= 1) reserve = member_units(cin, mem_slack);
+    } else if (kind_k == K_DENSE) {
+        const uint32_t cmin = c_k > q ? c_k - q : 0u;
+        if ((uint64_t)100 * cmin <= (uint64_t)alpha * L) reserve = member_units(cin, mem_slack);
+    }
+    o.mem = warp_sum(need_mem);
+    o.res = warp_sum(reserve);
+    o.arc = L > h.adj_cap ? arc_capacity(L, arc_slack) : 0;
+    o.bkt = nb > h.ncap ? bucket_capacity(nb) : 0;
+    uint64_t words = 0;
+    if (q) {
+        const uint64_t Hq = next_pow2(2 * q);
+        words = (uint64_t)(L + 31) / 32 + 8 * Hq + 3ull * q + 8;
+        words = (words + 7) & ~7ull;
+    }
+    o.words = words;
+    o.L = L;
+    o.q = q;
+    return o;
+}
+
 __global__ void k_upd_plan(const uint4 *__restrict__ recs, const uint32_t *__restrict__ sval,
                            const uint32_t *__restrict__ seg, const uint32_t *__restrict__ tv, uint32_t ntouch,
                            const VHdr *__restrict__ hdr, const Bucket *__restrict__ bkt,
                            const GCan *__restrict__ gcan, uint32_t alpha, bool bs,
-                           double arc_slack, double mem_slack, uint64_t *__restrict__ scr_need, UpdCounters *cnt) {
+                           double arc_slack, double mem_slack, uint64_t *__restrict__ scr_need, UpdCounters *cnt,
+                           uint8_t *__restrict__ route, uint32_t *__restrict__ large_list, uint32_t small_L) {
+    // demand counters are aggregated per block in shared memory (one global atomic per
+    // block and counter instead of one per touched vertex)
+    __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res;
+    __shared__ int b_flag;
+    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = 0; b_flag = 0; }
+    __syncthreads();
     const uint32_t lane = lane_id();
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < ntouch; t += warps) {
-        const uint32_t u = tv[t];
-        const uint32_t beg = seg[t], end = seg[t + 1];
-        const VHdr h = hdr[u];
-        uint32_t kind_k, c_k, ref_k, aux_k;
-        OldGroups og;
-        load_old_groups(bkt, gcan, h, kind_k, c_k, ref_k, aux_k, og);
-        uint32_t m = 0, q = 0, ins_or = 0, insk = 0;
-        uint64_t ins_sum = 0;
-        for (uint32_t base = beg; base < end; base += 32) {
-            const uint32_t p = base + lane;
-            uint4 r = make_uint4(2u, 0u, 0u, 0u);
-            if (p < end) r = recs[sval[p]];
-            const bool ins = r.x == 0u, del = r.x == 1u;
-            const uint32_t w = ins ? r.w : 0u;
-            m += __popc(__ballot_sync(0xffffffffu, ins));
-            q += __popc(__ballot_sync(0xffffffffu, del));
-            ins_or |= w;
-            ins_sum += w;
-            uint32_t mk = __reduce_or_sync(0xffffffffu, w);
-            while (mk) {
-                const int k = __ffs(mk) - 1;
-                mk &= mk - 1;
-                const uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
-                if (lane == (uint32_t)k) insk += __popc(bal);
-            }
-        }
-        ins_or = __reduce_or_sync(0xffffffffu, ins_or);
-        ins_sum = warp_sum(ins_sum);
-        // overflow: (T + inserted) * popc(mask | inserted) < 2^64 and d + m < 2^32 - 1 (R-10)
-        const uint32_t nb = __popc(og.mask | ins_or);
-        const uint64_t Tn = h.T + ins_sum;
-        const bool carry = Tn < h.T;
-        if (lane == 0 && (carry || __umul64hi(Tn, (uint64_t)nb) != 0 || (uint64_t)h.d + m >= 0xFFFFFFFFull))
-            atomicOr(&cnt->flag, 4);
-        const uint32_t L = h.d + m;
-        // pool demand (exact for relocations; a tight upper bound for kind transitions)
-        uint64_t need_mem = 0, reserve = 0;
-        const uint32_t cin = c_k + insk;
-        if (is_list(kind_k)) {
-            if (cin > aux_k) need_mem = member_units(cin, mem_slack);
-        } else if (bs) {
-            if (cin >= 1 && kind_k == K_EMPTY) reserve = member_units(cin, mem_slack);
-        } else if (kind_k == K_EMPTY) {
-            if (insk >= 2) reserve = member_units(cin, mem_slack);
-        } else if (kind_k == K_ONE) {
-            if (insk >= 1) reserve = member_units(cin, mem_slack);
-        } else if (kind_k == K_DENSE) {
-            const uint32_t cmin = c_k > q ? c_k - q : 0u;
-            if ((uint64_t)100 * cmin <= (uint64_t)alpha * L) reserve = member_units(cin, mem_slack);
-        }
-        need_mem = warp_sum(need_mem);
-        reserve = warp_sum(reserve);
+        const VHdr h = hdr[tv[t]];
+        const PlanOut o = plan_vertex(recs, sval, seg[t], seg[t + 1], h, bkt, gcan, alpha, bs, arc_slack, mem_slack);
         if (lane == 0) {
-            if (L > h.adj_cap) atomicAdd(&cnt->need_arc, (unsigned long long)arc_capacity(L, arc_slack));
-            if (nb > h.ncap) atomicAdd(&cnt->need_bkt, (unsigned long long)bucket_capacity(nb));
-            if (need_mem) atomicAdd(&cnt->need_mem, (unsigned long long)need_mem);
-            if (reserve) atomicAdd(&cnt->reserve_mem, (unsigned long long)reserve);
-            uint64_t words = 0;
-            if (q) {
-                const uint64_t Hq = next_pow2(2 * q);
-                words = (uint64_t)(L + 31) / 32 + 8 * Hq + 3ull * q + 8;
-                words = (words + 7) & ~7ull;
-            }
-            scr_need[t] = words;
+            if (o.overflow) atomicOr(&b_flag, 4);
+            if (o.arc) atomicAdd(&b_arc, o.arc);
+            if (o.bkt) atomicAdd(&b_bkt, o.bkt);
+            if (o.mem) atomicAdd(&b_mem, o.mem);
+            if (o.res) atomicAdd(&b_res, o.res);
+            scr_need[t] = o.words;
+            const bool large = !(o.L <= small_L && o.q <= SMALL_Q);
+            route[t] = large ? 1 : 0;
+            if (large) large_list[atomicAdd(&cnt->n_large, 1u)] = t;   // hubs: few, so little contention
         }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (b_arc) atomicAdd(&cnt->need_arc, b_arc);
+        if (b_bkt) atomicAdd(&cnt->need_bkt, b_bkt);
+        if (b_mem) atomicAdd(&cnt->need_mem, b_mem);
+        if (b_res) atomicAdd(&cnt->reserve_mem, b_res);
+        if (b_flag) atomicOr(&cnt->flag, b_flag);
     }
 }
 
 // ------------------------------------------------------------------ block helpers
 // block-wide exclusive scan of one u32 per thread; returns prefix, *total via smem
-__device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t *s_tmp /*[MT/32+1]*/, uint32_t &total) {
+template <int NT>
+__device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t *s_tmp /*[NT/32+1]*/, uint32_t &total) {
     const uint32_t lane = threadIdx.x & 31u, wid = threadIdx.x >> 5;
     uint32_t x = v;
 #pragma unroll
@@ -223,16 +269,16 @@ __device__ __forceinline__ uint32_t block_scan_u32(uint32_t v, uint32_t *s_tmp /
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t acc = 0;
-        for (int w = 0; w < MT / 32; w++) {
+        for (int w = 0; w < NT / 32; w++) {
             const uint32_t t = s_tmp[w];
             s_tmp[w] = acc;
             acc += t;
         }
-        s_tmp[MT / 32] = acc;
+        s_tmp[NT / 32] = acc;
     }
     __syncthreads();
     const uint32_t r = x - v + s_tmp[wid];
-    total = s_tmp[MT / 32];
+    total = s_tmp[NT / 32];
     __syncthreads();
     return r;
 }
@@ -263,15 +309,55 @@ struct MutateArgs {
     double arc_slack, mem_slack;
 };
 
-__global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
-    const uint32_t t = blockIdx.x;
-    const uint32_t tid = threadIdx.x, lane = tid & 31u, wid = tid >> 5;
-    __shared__ uint32_t s_kind0[32], s_c[32], s_insk[32], s_delk[32], s_moff[32], s_cap[32], s_one[32];
-    __shared__ uint32_t s_tmp[MT / 32 + 1];
-    __shared__ uint32_t s_list0, s_m, s_q, s_N, s_missing;
-    __shared__ uint64_t s_adj_off;
-    __shared__ uint32_t s_adj_cap;
-    __shared__ uint32_t s_fill_mask, s_find_mask, s_kind1[32];
+struct MutSmem {
+    uint32_t kind0[32], c[32], insk[32], delk[32], moff[32], cap[32], one[32], kind1[32];
+    uint32_t tmp[LT / 32 + 1];
+    uint32_t list0, m, q, N, missing, fill_mask, find_mask, adj_cap;
+    uint64_t adj_off;
+};
+
+template <int GT>
+struct Grp;
+template <>
+struct Grp<32> {
+    static __device__ __forceinline__ uint32_t rank() { return threadIdx.x & 31u; }
+    static __device__ __forceinline__ void sync() { __syncwarp(); }
+    static __device__ __forceinline__ bool any(bool p) { return __any_sync(0xffffffffu, p); }
+    static __device__ __forceinline__ uint32_t scan(uint32_t v, uint32_t *, uint32_t &total) {
+        const uint32_t lane = threadIdx.x & 31u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        total = __shfl_sync(0xffffffffu, x, 31);
+        return x - v;
+    }
+};
+template <>
+struct Grp<LT> {
+    static __device__ __forceinline__ uint32_t rank() { return threadIdx.x; }
+    static __device__ __forceinline__ void sync() { __syncthreads(); }
+    static __device__ __forceinline__ bool any(bool p) { return __syncthreads_or(p) != 0; }
+    static __device__ __forceinline__ uint32_t scan(uint32_t v, uint32_t *tmp, uint32_t &total) {
+        return block_scan_u32<LT>(v, tmp, total);
+    }
+};
+
+// Per-vertex insert -> delete -> rebuild, executed by a group of GT threads:
+// one warp (GT = 32, small vertices, 8 per block) or a whole block (GT = MT,
+// large vertices).  Lanes 0..31 of the group own radix bit k = lane.
+template <int GT>
+__device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_t t, MutSmem &sm) {
+    using G = Grp<GT>;
+    const uint32_t tid = G::rank(), lane = tid & 31u, wid = tid >> 5;
+    uint32_t *s_kind0 = sm.kind0, *s_c = sm.c, *s_insk = sm.insk, *s_delk = sm.delk, *s_moff = sm.moff,
+             *s_cap = sm.cap, *s_one = sm.one, *s_kind1 = sm.kind1, *s_tmp = sm.tmp;
+    uint32_t &s_list0 = sm.list0, &s_m = sm.m, &s_q = sm.q, &s_N = sm.N, &s_missing = sm.missing;
+    uint32_t &s_fill_mask = sm.fill_mask, &s_find_mask = sm.find_mask, &s_adj_cap = sm.adj_cap;
+    uint64_t &s_adj_off = sm.adj_off;
+    G::sync();   // the group's shared slot may still be read by its previous vertex
 
     const uint32_t u = a.tv[t];
     const uint32_t beg = a.seg[t], end = a.seg[t + 1];
@@ -344,17 +430,17 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             }
         }
     }
-    __syncthreads();
+    G::sync();
     const uint64_t aoff = s_adj_off;
     const uint32_t m = s_m, q = s_q;
     const uint32_t L = h.d + m;
     if (aoff != h.adj_off) {
-        for (uint32_t i = tid; i < h.d; i += MT) {
+        for (uint32_t i = tid; i < h.d; i += GT) {
             a.arc[aoff + i] = a.arc[h.adj_off + i];
             a.arc_epoch[aoff + i] = a.arc_epoch[h.adj_off + i];
         }
     }
-    __syncthreads();
+    G::sync();
 
     // ---------------- phase 1: inserts, batch order
     if (wid == 0 && m) {
@@ -394,7 +480,7 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
         }
         s_insk[lane] = insk;
     }
-    __syncthreads();
+    G::sync();
 
     // ---------------- phase 2: deletes
     uint32_t N = 0;
@@ -415,8 +501,8 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
         holes = reinterpret_cast<uint32_t *>(hprev + Hq);
         R = holes + q;
         gh = R + q;
-        for (uint32_t i = tid; i < bw; i += MT) bm[i] = 0;
-        for (uint32_t i = tid; i < Hq; i += MT) {
+        for (uint32_t i = tid; i < bw; i += GT) bm[i] = 0;
+        for (uint32_t i = tid; i < Hq; i += GT) {
             hkey[i] = EMPTY_KEY;
             hk[i] = 0;
             hfound[i] = 0;
@@ -424,9 +510,9 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             hbest[i] = ~0ull;
             hprev[i] = 0;
         }
-        __syncthreads();
+        G::sync();
         // distinct deleted destinations with multiplicity
-        for (uint32_t p = beg + tid; p < end; p += MT) {
+        for (uint32_t p = beg + tid; p < end; p += GT) {
             const uint4 r = a.recs[a.sval[p]];
             if (r.x != 1u) continue;
             uint32_t s = hash_slot(r.z, hmask);
@@ -439,12 +525,13 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                 s = (s + 1) & hmask;
             }
         }
-        __syncthreads();
+        G::sync();
         // selection rounds: round r picks, per distinct v still owed a delete, the
         // live instance with the smallest (epoch, position) key above the last pick
         for (uint32_t round = 0;; round++) {
-            for (uint32_t p = tid; p < L; p += MT) {
-                const uint32_t x = a.arc[aoff + p].x;
+#pragma unroll 4
+            for (uint32_t p = tid; p < L; p += GT) {
+                const uint32_t x = __ldg(&a.arc[aoff + p].x);
                 uint32_t s = hash_slot(x, hmask);
                 uint32_t hit = EMPTY_KEY;
                 for (;;) {
@@ -462,9 +549,9 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                     atomicMin(&hbest[hit], key);
                 }
             }
-            __syncthreads();
+            G::sync();
             uint32_t more = 0;
-            for (uint32_t s = tid; s < Hq; s += MT) {
+            for (uint32_t s = tid; s < Hq; s += GT) {
                 if (hkey[s] == EMPTY_KEY || hsel[s] >= hk[s]) continue;
                 const unsigned long long b = hbest[s];
                 if (b == ~0ull) continue;
@@ -482,18 +569,18 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                 }
                 if (hsel[s] < hk[s] && hsel[s] < hfound[s]) more = 1;
             }
-            if (!__syncthreads_or(more)) break;
+            if (!G::any(more != 0)) break;
         }
-        for (uint32_t s = tid; s < Hq; s += MT)
+        for (uint32_t s = tid; s < Hq; s += GT)
             if (hkey[s] != EMPTY_KEY) atomicAdd(&s_missing, hk[s] - hsel[s]);
-        __syncthreads();
+        G::sync();
         N = s_N;
         Lp = L - N;
         if (N) {
             // holes = marked positions < L' ascending (rank by block scan over bitmap words)
             const uint32_t wl = (Lp + 31) / 32;
             uint32_t carry = 0;
-            for (uint32_t w0 = 0; w0 < wl; w0 += MT) {
+            for (uint32_t w0 = 0; w0 < wl; w0 += GT) {
                 const uint32_t w = w0 + tid;
                 uint32_t word = 0;
                 if (w < wl) {
@@ -502,7 +589,7 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                     if (lim < 32) word &= (1u << lim) - 1u;
                 }
                 uint32_t tot;
-                const uint32_t pre = block_scan_u32(__popc(word), s_tmp, tot);
+                const uint32_t pre = G::scan(__popc(word), s_tmp, tot);
                 uint32_t r = carry + pre;
                 while (word) {
                     const int b = __ffs(word) - 1;
@@ -511,15 +598,15 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                 }
                 carry += tot;
             }
-            __syncthreads();
+            G::sync();
             // adjacency tail window [L', L): survivors fill holes in rank order
             uint32_t scarry = 0;
-            for (uint32_t t0 = Lp; t0 < L; t0 += MT) {
+            for (uint32_t t0 = Lp; t0 < L; t0 += GT) {
                 const uint32_t tt = t0 + tid;
                 const bool in = tt < L;
                 const bool surv = in && !bit_test(bm, tt);
                 uint32_t tot;
-                const uint32_t rank = scarry + block_scan_u32(surv ? 1u : 0u, s_tmp, tot);
+                const uint32_t rank = scarry + G::scan(surv ? 1u : 0u, s_tmp, tot);
                 if (in) {
                     if (surv) {
                         const uint32_t dstp = holes[rank];
@@ -532,7 +619,7 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
                 }
                 scarry += tot;
             }
-            __syncthreads();
+            G::sync();
         }
     }
     // ---------------- groups: delete-and-swap, rename (lists that existed before the batch)
@@ -546,36 +633,39 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             uint32_t *Md = a.mdst + (uint64_t)s_moff[k] * 4;
             uint32_t *Mi = a.midx + (uint64_t)s_moff[k] * 4;
             const uint32_t Lk = cp - Nk;
-            if (Nk) {
-                uint32_t carry = 0;
-                for (uint32_t s0 = 0; s0 < Lk; s0 += MT) {
-                    const uint32_t s = s0 + tid;
-                    const bool del = s < Lk && bit_test(bm, Mi[s]);
-                    uint32_t tot;
-                    const uint32_t rank = carry + block_scan_u32(del ? 1u : 0u, s_tmp, tot);
-                    if (del) gh[rank] = s;
-                    carry += tot;
+            // pass 1 over the front [0, L_k'): deleted slots become holes (ranked in slot
+            // order); surviving entries that point into the adjacency tail are renamed
+            // in place.  pass 2 over the tail window [L_k', c'): survivors, renamed,
+            // fill the holes in rank order (R-6).
+            uint32_t carry = 0;
+            for (uint32_t s0 = 0; s0 < Lk; s0 += GT) {
+                const uint32_t s = s0 + tid;
+                bool del = false;
+                if (s < Lk) {
+                    const uint32_t x = Mi[s];
+                    del = bit_test(bm, x);
+                    if (!del && x >= Lp) Mi[s] = R[x - Lp];
                 }
-                __syncthreads();
-                uint32_t scarry = 0;
-                for (uint32_t s0 = Lk; s0 < cp; s0 += MT) {
-                    const uint32_t s = s0 + tid;
-                    const bool surv = s < cp && !bit_test(bm, Mi[s]);
-                    uint32_t tot;
-                    const uint32_t rank = scarry + block_scan_u32(surv ? 1u : 0u, s_tmp, tot);
-                    if (surv) {
-                        Md[gh[rank]] = Md[s];
-                        Mi[gh[rank]] = Mi[s];
-                    }
-                    scarry += tot;
+                uint32_t tot = 0;
+                const uint32_t rank = Nk ? carry + G::scan(del ? 1u : 0u, s_tmp, tot) : 0u;
+                if (del) gh[rank] = s;
+                carry += tot;
+            }
+            G::sync();
+            uint32_t scarry = 0;
+            for (uint32_t s0 = Lk; s0 < cp; s0 += GT) {
+                const uint32_t s = s0 + tid;
+                uint32_t x = 0;
+                const bool surv = s < cp && !bit_test(bm, (x = Mi[s]));
+                uint32_t tot;
+                const uint32_t rank = scarry + G::scan(surv ? 1u : 0u, s_tmp, tot);
+                if (surv) {
+                    Md[gh[rank]] = Md[s];
+                    Mi[gh[rank]] = x >= Lp ? R[x - Lp] : x;
                 }
-                __syncthreads();
+                scarry += tot;
             }
-            for (uint32_t s = tid; s < Lk; s += MT) {
-                const uint32_t x = Mi[s];
-                if (x >= Lp) Mi[s] = R[x - Lp];
-            }
-            __syncthreads();
+            G::sync();
         }
     }
     // ---------------- phase 3: rebuild
@@ -623,7 +713,7 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
             vs[1] = s_missing;
         }
     }
-    __syncthreads();
+    G::sync();
     if (wid == 0 && (s_fill_mask | s_find_mask)) {
         // one ascending pass over the post-batch adjacency materialises new lists
         // (scan order = ascending index, R-2) and finds the unique member of ONE groups
@@ -655,7 +745,7 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
         }
         s_one[lane] = onev;
     }
-    __syncthreads();
+    G::sync();
     if (wid == 0) {
         const uint32_t k = lane;
         const uint32_t kind1 = s_kind1[k];
@@ -711,10 +801,30 @@ __global__ void __launch_bounds__(MT) k_upd_mutate(const MutateArgs a) {
         // neighbour hash set of the post-batch adjacency (node2vec distance test)
         const uint32_t lg = nb_log2size(dn);
         uint32_t *tbl = a.nbt + 4 * aoff;
-        for (uint32_t j = tid; j < (1u << lg); j += MT) tbl[j] = NB_EMPTY;
-        __syncthreads();
-        for (uint32_t i = tid; i < dn; i += MT) nb_insert(tbl, (1u << lg) - 1, a.arc[aoff + i].x);
+        for (uint32_t j = tid; j < (1u << lg); j += GT) tbl[j] = NB_EMPTY;
+        G::sync();
+        for (uint32_t i = tid; i < dn; i += GT) nb_insert(tbl, (1u << lg) - 1, a.arc[aoff + i].x);
         if (tid == 0) a.nbo[u] = nb_pack(4 * aoff, lg);
+    }
+}
+
+// small touched vertices: one warp each, 8 per block (grid-stride over all touched
+// vertices, skipping those routed to the block kernel)
+__global__ void __launch_bounds__(MT) k_upd_mutate_warp(const MutateArgs a, const uint8_t *__restrict__ route,
+                                                        uint32_t count) {
+    __shared__ MutSmem sm[MT / 32];
+    const uint32_t w = threadIdx.x >> 5;
+    for (uint32_t i = blockIdx.x * (MT / 32) + w; i < count; i += gridDim.x * (MT / 32))
+        if (!route[i]) mutate_vertex<32>(a, i, sm[w]);
+}
+
+// large touched vertices (hubs): one 1024-thread block each
+__global__ void __launch_bounds__(LT) k_upd_mutate_block(const MutateArgs a, const uint32_t *__restrict__ list,
+                                                         uint32_t count) {
+    __shared__ MutSmem sm;
+    for (uint32_t i = blockIdx.x; i < count; i += gridDim.x) {
+        mutate_vertex<LT>(a, list[i], sm);
+        __syncthreads();
     }
 }
 
@@ -734,6 +844,150 @@ __global__ void k_upd_stats(const uint32_t *__restrict__ vstats, uint32_t ntouch
     }
     __syncthreads();
     if (threadIdx.x < 27 && acc[threadIdx.x]) atomicAdd(&out[threadIdx.x], acc[threadIdx.x]);
+}
+
+// ------------------------------------------------------------------ small-batch fast path (a11)
+// Streaming updates (S4.2; BJ.c5): for n <= FAST_N records a single
+// 1024-thread block validates, groups by source (stable rank sort in shared
+// memory), runs the same per-vertex plan and, when everything fits, the same
+// per-vertex mutate (one warp per touched vertex) -- one launch, no host round
+// trips before the mutation.  Status and statistics land in mapped pinned host
+// memory.  If a vertex is too large for the preallocated scratch or a pool would
+// have to grow, nothing is mutated and the host runs the general pipeline.
+static constexpr uint32_t FAST_N = 64;
+static constexpr uint32_t FAST_MAXL = 1u << 16;
+enum : uint32_t { FAST_OK = 0, FAST_INVAL = 1, FAST_OVERFLOW = 4, FAST_SLOW = 8 };
+
+struct FastOut {
+    uint32_t status, ntouch;
+    unsigned long long stats[27];
+    unsigned long long inserted;
+};
+
+struct FastArgs {
+    MutateArgs m;                     // graph, allocator and policy fields (pointers set in-kernel)
+    uint4 recs[FAST_N];               // the batch, inline (host batches need no copy)
+    const uint4 *drecs;               // or a device batch
+    uint32_t n, V;
+    unsigned long long arc_cap, bkt_cap, mem_units_cap;
+    uint32_t *scr;                    // FAST_N * fast_words() words
+    unsigned long long scr_cap;
+    uint32_t *vstats;                 // FAST_N * VST
+    FastOut *out;                     // mapped pinned host memory
+};
+
+__host__ __device__ inline unsigned long long fast_words_per_vertex() {
+    return (FAST_MAXL + 31) / 32 + 8ull * (2 * FAST_N) + 3ull * FAST_N + 16;
+}
+
+__global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
+    __shared__ uint4 recs[FAST_N];
+    __shared__ uint32_t sval[FAST_N], seg[FAST_N + 1], tv[FAST_N];
+    __shared__ unsigned long long scr_off[FAST_N + 1];
+    __shared__ MutSmem sm[32];
+    __shared__ unsigned long long need_arc, need_bkt, need_mem;
+    __shared__ uint32_t flag, ntouch, go;
+    const uint32_t tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
+    const uint32_t n = fa.n;
+    if (tid == 0) { need_arc = need_bkt = need_mem = 0; flag = 0; }
+    if (tid < n) recs[tid] = fa.drecs ? fa.drecs[tid] : fa.recs[tid];
+    __syncthreads();
+    // validation (whole batch, before anything else)
+    if (tid < n) {
+        const uint4 r = recs[tid];
+        if (r.x > 1u || r.y >= fa.V || r.z >= fa.V || (r.x == 0u && r.w == 0u)) atomicOr(&flag, FAST_INVAL);
+    }
+    // stable grouping by src: rank = #{j : src_j < src_i, or src_j == src_i and j < i}
+    if (tid < n) {
+        const uint32_t si = recs[tid].y;
+        uint32_t rank = 0;
+        for (uint32_t j = 0; j < n; j++) {
+            const uint32_t sj = recs[j].y;
+            rank += (sj < si || (sj == si && j < tid)) ? 1u : 0u;
+        }
+        sval[rank] = tid;
+    }
+    __syncthreads();
+    if (w == 0) {
+        uint32_t cntv = 0;
+        for (uint32_t base = 0; base < FAST_N; base += 32) {
+            const uint32_t p = base + lane;
+            const bool head = p < n && (p == 0 || recs[sval[p]].y != recs[sval[p - 1]].y);
+            const uint32_t bal = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                const uint32_t t = cntv + __popc(bal & lanemask_lt());
+                seg[t] = p;
+                tv[t] = recs[sval[p]].y;
+            }
+            cntv += __popc(bal);
+        }
+        if (lane == 0) {
+            ntouch = cntv;
+            seg[cntv] = n;
+        }
+    }
+    __syncthreads();
+    const uint32_t nt = ntouch;
+    // plan, one warp per touched vertex
+    for (uint32_t t = w; t < nt; t += 32) {
+        const VHdr h = fa.m.hdr[tv[t]];
+        const PlanOut o = plan_vertex(recs, sval, seg[t], seg[t + 1], h, fa.m.bkt, fa.m.gcan, fa.m.alpha, fa.m.bs,
+                                      fa.m.arc_slack, fa.m.mem_slack);
+        if (lane == 0) {
+            if (o.overflow) atomicOr(&flag, FAST_OVERFLOW);
+            if (o.L > FAST_MAXL || o.q > FAST_N) atomicOr(&flag, FAST_SLOW);
+            atomicAdd(&need_arc, o.arc);
+            atomicAdd(&need_bkt, o.bkt);
+            atomicAdd(&need_mem, o.mem + o.res);
+            scr_off[t] = o.words;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long acc = 0;
+        for (uint32_t t = 0; t < nt; t++) {
+            const unsigned long long x = scr_off[t];
+            scr_off[t] = acc;
+            acc += x;
+        }
+        scr_off[nt] = acc;
+        uint32_t f = flag;
+        if (!(f & (FAST_INVAL | FAST_OVERFLOW))) {
+            const unsigned long long *c = fa.m.bump;
+            if (c[0] + need_arc > fa.arc_cap || c[1] + need_bkt > fa.bkt_cap || c[2] + need_mem > fa.mem_units_cap ||
+                acc > fa.scr_cap)
+                f |= FAST_SLOW;
+        }
+        flag = f;
+        go = f == 0 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (go) {
+        MutateArgs a = fa.m;
+        a.recs = recs;
+        a.sval = sval;
+        a.seg = seg;
+        a.tv = tv;
+        a.scr_off = reinterpret_cast<const uint64_t *>(scr_off);
+        a.scr = fa.scr;
+        a.vstats = fa.vstats;
+        for (uint32_t t = w; t < nt; t += 32) mutate_vertex<32>(a, t, sm[w]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        FastOut *o = fa.out;
+        const uint32_t f = flag;
+        o->status = (f & FAST_INVAL) ? FAST_INVAL : (f & FAST_OVERFLOW) ? FAST_OVERFLOW : (f & FAST_SLOW) ? FAST_SLOW : FAST_OK;
+        o->ntouch = nt;
+        unsigned long long ins = 0;
+        for (uint32_t i = 0; i < n; i++) ins += recs[i].x == 0u ? 1ull : 0ull;
+        o->inserted = ins;
+    }
+    if (go && tid < 27) {
+        unsigned long long acc = 0;
+        for (uint32_t t = 0; t < nt; t++) acc += fa.vstats[(uint64_t)t * VST + tid];
+        fa.out->stats[tid] = acc;
+    }
 }
 
 }  // namespace bingo
@@ -764,6 +1018,7 @@ size_t batch_scratch_bytes(uint64_t n) {
     add(4 * (n + 1)); add(4 * n);                  // seg, tv
     add(8 * (n + 1)); add(8 * (n + 2));            // scr_need, scr_off
     add(4 * VST * n);                              // vstats
+    add(4 * n); add(4 * n);                        // small / large touched lists
     add(sizeof(UpdCounters) + 8 * 32);             // counters, stats
     return b + 4096;
 }
@@ -842,6 +1097,95 @@ static bingo_status upd_cuda_fail(bingo_graph *g, cudaError_t e, const char *w) 
         if (e_ != cudaSuccess) return upd_cuda_fail(g, e_, #call);  \
     } while (0)
 
+static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
+    const bool bs = (g->flags & BINGO_BUILD_BS_MODE) != 0;
+    ma.hdr = g->hdr;
+    ma.thdr = g->thdr;
+    ma.arc = g->arc;
+    ma.arc_epoch = g->arc_epoch;
+    ma.bkt = g->bkt;
+    ma.gcan = g->gcan;
+    ma.mdst = g->mdst;
+    ma.midx = g->midx;
+    ma.nbt = g->nbt;
+    ma.nbo = g->nbo;
+    ma.bump = g->counters;
+    ma.epoch = e;
+    ma.alpha = g->alpha;
+    ma.beta = g->beta;
+    ma.hot_b = g->hot_bkt_degree;
+    ma.hot_m = g->hot_mem_degree;
+    ma.bs = bs;
+    ma.arc_slack = g->arc_slack;
+    ma.mem_slack = g->member_slack;
+}
+
+// returns true when the fast path decided the call (OK / EINVAL / EOVERFLOW / CUDA)
+static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
+                          bingo_update_stats *stats, cudaStream_t s, bingo_status *out) {
+    if (!g->fast_scr) {
+        const size_t words = (size_t)(FAST_N * fast_words_per_vertex());
+        g->fast_scr = (uint32_t *)bingo_dev_alloc(g, 4 * words + 4 * FAST_N * VST + 64);
+        if (!g->fast_scr) return false;
+        void *h = nullptr;
+        if (cudaHostAlloc(&h, sizeof(FastOut), cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+        g->fast_out_host = h;
+        if (cudaHostGetDevicePointer(&g->fast_out_dev, h, 0) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+    }
+    FastArgs fa;
+    memset(&fa, 0, sizeof(fa));
+    fill_mutate_common(g, fa.m, g->epoch + 1);
+    if (flags & BINGO_UPD_HOST_BATCH) {
+        memcpy(fa.recs, batch, 16 * n);
+        fa.drecs = nullptr;
+    } else {
+        fa.drecs = reinterpret_cast<const uint4 *>(batch);
+    }
+    fa.n = (uint32_t)n;
+    fa.V = g->V;
+    fa.arc_cap = g->arc_cap;
+    fa.bkt_cap = g->bkt_cap;
+    fa.mem_units_cap = g->mem_cap / 4;
+    fa.scr = g->fast_scr;
+    fa.scr_cap = FAST_N * fast_words_per_vertex();
+    fa.vstats = g->fast_scr + fa.scr_cap;
+    fa.out = (FastOut *)g->fast_out_dev;
+    FastOut *ho = (FastOut *)g->fast_out_host;
+    ho->status = 0xFFFFFFFFu;
+    k_upd_fast<<<1, 1024, 0, s>>>(fa);
+    bingo_count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) {
+        *out = upd_cuda_fail(g, e, "k_upd_fast");
+        return true;
+    }
+    const uint32_t st = ho->status;
+    if (st == FAST_SLOW) return false;
+    if (st == FAST_INVAL) { *out = BINGO_E_INVAL; return true; }
+    if (st == FAST_OVERFLOW) { *out = BINGO_E_OVERFLOW; return true; }
+    if (st != FAST_OK) { *out = upd_cuda_fail(g, cudaErrorUnknown, "k_upd_fast status"); return true; }
+    g->epoch++;
+    const uint64_t deleted = ho->stats[0];
+    g->num_arcs = g->num_arcs + ho->inserted - deleted;
+    if (stats) {
+        stats->inserted = ho->inserted;
+        stats->deleted = deleted;
+        stats->missing_deletes = ho->stats[1];
+        stats->touched_vertices = ho->ntouch;
+        for (int i = 0; i < 25; i++) stats->kind_transitions[i / 5][i % 5] = ho->stats[2 + i];
+        stats->epoch = g->epoch;
+    }
+    *out = BINGO_OK;
+    return true;
+}
+
 extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
                                             bingo_update_stats *stats, void *stream) {
     if (!g) return BINGO_E_INVAL;
@@ -854,6 +1198,11 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
         g->epoch++;
         if (stats) stats->epoch = g->epoch;
         return BINGO_OK;
+    }
+    // ---- small batches: single-launch fast path (falls through when it reports SLOW)
+    if (n <= FAST_N) {
+        bingo_status fst;
+        if (try_fast_path(g, batch, n, flags, stats, s, &fst)) return fst;
     }
     // ---- scratch
     const size_t need = batch_scratch_bytes(n);
@@ -881,6 +1230,8 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     uint32_t *seg = cv.take<uint32_t>(n + 1), *tv = cv.take<uint32_t>(n);
     uint64_t *scr_need = cv.take<uint64_t>(n + 1), *scr_off = cv.take<uint64_t>(n + 2);
     uint32_t *vstats = cv.take<uint32_t>((size_t)VST * n);
+    uint8_t *route = cv.take<uint8_t>(n);
+    uint32_t *large_list = cv.take<uint32_t>(n);
     UpdCounters *dc = cv.take<UpdCounters>(1);
     unsigned long long *dstats = cv.take<unsigned long long>(32);
 
@@ -910,9 +1261,12 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     UCK(cudaMemcpyAsync(&ntouch, head_ex + n, 8, cudaMemcpyDeviceToHost, s));
     UCK(cudaStreamSynchronize(s));
     const bool bs = (g->flags & BINGO_BUILD_BS_MODE) != 0;
+    uint32_t small_L = SMALL_L;
+    if (const char *ev = getenv("BINGO_UPD_SMALL_L")) small_L = (uint32_t)strtoul(ev, nullptr, 10);
     const unsigned gp = (unsigned)std::min<uint64_t>((ntouch + 7) / 8, 148 * 32);
     k_upd_plan<<<gp ? gp : 1, 256, 0, s>>>(recs, sv, seg, tv, (uint32_t)ntouch, g->hdr, g->bkt, g->gcan, g->alpha, bs,
-                                          g->arc_slack, g->member_slack, scr_need, dc);
+                                          g->arc_slack, g->member_slack, scr_need, dc, route, large_list,
+                                          small_L);
     bingo_count_launch();
     UCK(cudaGetLastError());
     UCK(exclusive_scan_u64(scr_need, scr_off, ntouch, stmp, s));
@@ -976,9 +1330,18 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     ma.arc_slack = g->arc_slack;
     ma.mem_slack = g->member_slack;
     if (ntouch) {
-        k_upd_mutate<<<(unsigned)ntouch, MT, 0, s>>>(ma);
-        bingo_count_launch();
-        UCK(cudaGetLastError());
+        if (hc.n_large < ntouch) {
+            const unsigned gs = (unsigned)std::min<uint64_t>((ntouch + MT / 32 - 1) / (MT / 32), 148ull * 8);
+            k_upd_mutate_warp<<<gs, MT, 0, s>>>(ma, route, (uint32_t)ntouch);
+            bingo_count_launch();
+            UCK(cudaGetLastError());
+        }
+        if (hc.n_large) {
+            k_upd_mutate_block<<<(unsigned)std::min<uint64_t>(hc.n_large, 148ull * 2), LT, 0, s>>>(ma, large_list,
+                                                                                               hc.n_large);
+            bingo_count_launch();
+            UCK(cudaGetLastError());
+        }
         k_upd_stats<<<(unsigned)std::min<uint64_t>((ntouch + 255) / 256, 148), 256, 0, s>>>(vstats, (uint32_t)ntouch,
                                                                                             dstats);
         bingo_count_launch();

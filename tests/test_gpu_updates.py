@@ -68,9 +68,14 @@ def _bias_of(u, v, e, hi):
     return 1 + ((u * 2654435761 + v * 40503 + e * 97) % hi)
 
 
-@pytest.mark.parametrize("seed,bs_mode,hi", [(0, False, 200), (1, False, 1 << 20), (2, True, 200),
-                                             (3, False, 7), (4, False, 255), (5, True, 1 << 31)])
-def test_random_multigraph_batches(seed, bs_mode, hi):
+@pytest.mark.parametrize("seed,bs_mode,hi,route", [(0, False, 200, "auto"), (1, False, 1 << 20, "auto"),
+                                                   (2, True, 200, "auto"), (3, False, 7, "auto"),
+                                                   (4, False, 255, "auto"), (5, True, 1 << 31, "auto"),
+                                                   (0, False, 200, "block"), (3, False, 7, "block"),
+                                                   (6, False, 1 << 20, "block")])
+def test_random_multigraph_batches(seed, bs_mode, hi, route, monkeypatch):
+    if route == "block":       # every touched vertex through the block-per-vertex kernel
+        monkeypatch.setenv("BINGO_UPD_SMALL_L", "0")
     """Random multigraphs with duplicates, hubs (multi-chunk scans), missing deletes, repeated
     deletes of one pair, mixed biases forcing kind transitions in every direction."""
     rng = np.random.default_rng(1000 + seed)
@@ -174,3 +179,25 @@ def test_larger_graph_batches_digests():
     out = g.walk(length=80, seed=3, starts=starts)
     ref = o.walk(length=80, seed=3, starts=starts)
     assert np.array_equal(u32(out["paths"]), ref["paths"])
+
+
+def test_small_batches_fast_path():
+    """a11: batches of 1..64 records take the single-launch path; the state after each equals
+    the oracle's, including when a batch needs pool growth (the fast path hands over to the
+    general pipeline without mutating)."""
+    rng = np.random.default_rng(17)
+    w = synth.make_workload("c1", rounds=3)
+    g, o = _pair(w.row_offsets, w.dst, w.bias, arc_slack=0.0, member_slack=0.0, pool_reserve=0.0)
+    stream = np.concatenate(w.batches)
+    pos = 0
+    while pos < len(stream):
+        k = int(rng.integers(1, 65))
+        b = stream[pos:pos + k]
+        pos += k
+        _same_stats(g.apply_updates(b), o.apply_updates(b))
+    _same(g, o, w.V, "after the small-batch stream")
+    # a hub gaining many arcs in small batches forces relocations (SLOW -> general path)
+    for i in range(20):
+        b = np.array([(0, 5, (7 * i + j) % w.V, 1 + (i * 64 + j) % 300) for j in range(64)], dtype=np.uint32)
+        _same_stats(g.apply_updates(b), o.apply_updates(b))
+    _same(g, o, w.V, "after hub growth")
