@@ -330,6 +330,27 @@ def main():
                "d2h_bytes_per_step": int(4 * V * (L + 2)), "steps": e2e_steps,
                "note": "bingo_apply_updates(HOST batch) + bingo_walk(HOST_OUTPUT paths+lengths), pinned"}
 
+    # ---- a11: streaming single-record updates (synchronous C-ABI calls, host batch)
+    streaming = None
+    if rank == 0:
+        recs = w.batches[-1][:300]
+        lat_host, lat_dev = [], []
+        for r in recs:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(stream)
+            g.apply_updates(r[None, :])
+            e1.record(stream)
+            t1 = time.perf_counter()
+            torch.cuda.synchronize()
+            lat_host.append(1e6 * (t1 - t0))
+            lat_dev.append(1e3 * e0.elapsed_time(e1))
+        streaming = {"records": len(recs), "call_us_p50": float(np.percentile(lat_host, 50)),
+                     "call_us_p99": float(np.percentile(lat_host, 99)),
+                     "device_us_p50": float(np.percentile(lat_dev, 50)),
+                     "device_us_p99": float(np.percentile(lat_dev, 99)),
+                     "note": "one bingo_apply_updates call per arc record (epoch per record), c2 graph"}
+
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args, w, w.batches[0])
@@ -355,6 +376,7 @@ def main():
                          "load_counts": {k: prof[k] for k in ("steps", "hdr", "bkt", "mem", "arc")},
                          "gather_roofline": gather},
             "l2_plan": {k: g.info()[k] for k in ("l2_persist_bytes", "hot_degree")},
+            "streaming_update": streaming,
             "clocks": clk, "gpu_launches": int(launches),
             "e2e": e2e, "cpu_baseline": cpu,
         }

@@ -37,6 +37,9 @@ extern "C" void bingo_destroy(bingo_graph *g) {
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
     if (g->fast_out_host) cudaFreeHost(g->fast_out_host);
+    if (g->aux_stream) cudaStreamDestroy(g->aux_stream);
+    if (g->ev_fork) cudaEventDestroy(g->ev_fork);
+    if (g->ev_join) cudaEventDestroy(g->ev_join);
     delete g;
 }
 

@@ -174,6 +174,8 @@ struct bingo_graph {
     void *vscratch = nullptr;                // per-touched-vertex delete scratch
     size_t vscratch_bytes = 0;
     uint32_t *fast_scr = nullptr;            // small-batch fast path scratch (device)
+    cudaStream_t aux_stream = nullptr;       // side stream for hub mutations
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     void *fast_out_host = nullptr;           // mapped pinned status/stats of the fast path
     void *fast_out_dev = nullptr;
 };

@@ -1330,17 +1330,34 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     ma.arc_slack = g->arc_slack;
     ma.mem_slack = g->member_slack;
     if (ntouch) {
+        // hubs (block kernel, side stream) overlap the small vertices (warp kernel): the two
+        // sets are disjoint and only share the bump counters (atomics)
+        const bool both = hc.n_large && hc.n_large < ntouch;
+        if (both && !g->aux_stream) {
+            UCK(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
+            UCK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+            UCK(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+        }
+        cudaStream_t sl = both ? g->aux_stream : s;
+        if (both) {
+            UCK(cudaEventRecord(g->ev_fork, s));
+            UCK(cudaStreamWaitEvent(sl, g->ev_fork, 0));
+        }
+        if (hc.n_large) {
+            k_upd_mutate_block<<<(unsigned)std::min<uint64_t>(hc.n_large, 148ull * 2), LT, 0, sl>>>(ma, large_list,
+                                                                                                hc.n_large);
+            bingo_count_launch();
+            UCK(cudaGetLastError());
+        }
         if (hc.n_large < ntouch) {
             const unsigned gs = (unsigned)std::min<uint64_t>((ntouch + MT / 32 - 1) / (MT / 32), 148ull * 8);
             k_upd_mutate_warp<<<gs, MT, 0, s>>>(ma, route, (uint32_t)ntouch);
             bingo_count_launch();
             UCK(cudaGetLastError());
         }
-        if (hc.n_large) {
-            k_upd_mutate_block<<<(unsigned)std::min<uint64_t>(hc.n_large, 148ull * 2), LT, 0, s>>>(ma, large_list,
-                                                                                               hc.n_large);
-            bingo_count_launch();
-            UCK(cudaGetLastError());
+        if (both) {
+            UCK(cudaEventRecord(g->ev_join, sl));
+            UCK(cudaStreamWaitEvent(s, g->ev_join, 0));
         }
         k_upd_stats<<<(unsigned)std::min<uint64_t>((ntouch + 255) / 256, 148), 256, 0, s>>>(vstats, (uint32_t)ntouch,
                                                                                             dstats);
