@@ -55,6 +55,8 @@ def lib():
             L.ora_alias_build.argtypes = [u32, P, P, P]
             L.ora_build.argtypes = [u32, P, P, P, u32, u32, u32, ctypes.POINTER(P)]
             L.ora_build.restype = ctypes.c_int
+            L.ora_build_float.argtypes = [u32, P, P, P, u32, u32, u32, ctypes.POINTER(P)]
+            L.ora_build_float.restype = ctypes.c_int
             L.ora_free.argtypes = [P]
             L.ora_epoch.argtypes = [P]
             L.ora_epoch.restype = u32
@@ -133,14 +135,19 @@ def stop_threshold(num: int, den: int):
 class OracleGraph:
     """One oracle graph instance (host memory)."""
 
-    def __init__(self, row_offsets, dst, bias, alpha=40, beta=10, flags=0):
+    def __init__(self, row_offsets, dst, bias, alpha=40, beta=10, flags=0, float_bias=False):
         L = lib()
         self.V = len(row_offsets) - 1
+        self.float_mode = bool(float_bias)
         ro = np.ascontiguousarray(row_offsets, dtype=np.uint64)
         ds = np.ascontiguousarray(dst, dtype=np.uint32)
-        bs = np.ascontiguousarray(bias, dtype=np.uint32)
         h = ctypes.c_void_p()
-        rc = L.ora_build(self.V, _p(ro), _p(ds), _p(bs), alpha, beta, flags, ctypes.byref(h))
+        if float_bias:
+            bf = np.ascontiguousarray(bias, dtype=np.float64)
+            rc = L.ora_build_float(self.V, _p(ro), _p(ds), _p(bf), alpha, beta, flags, ctypes.byref(h))
+        else:
+            bs = np.ascontiguousarray(bias, dtype=np.uint32)
+            rc = L.ora_build(self.V, _p(ro), _p(ds), _p(bs), alpha, beta, flags, ctypes.byref(h))
         if rc != 0:
             raise ValueError(f"ora_build failed with status {rc}")
         self._h = h
@@ -198,7 +205,7 @@ class OracleGraph:
         return d
 
 
-def parse_dump(buf: bytes, V: int) -> list:
+def parse_dump(buf: bytes, V: int, float_mode: bool = False) -> list:
     """Parse the canonical dump (R-11) into per-vertex dicts (test helper)."""
     mv = memoryview(buf)
     pos = 0
@@ -231,6 +238,11 @@ def parse_dump(buf: bytes, V: int) -> list:
                 one = u32()
             groups.append({"k": k, "c": c, "kind": kind, "thr": thr, "alias": al, "mem": mem, "one": one})
         T = u64()
-        out.append({"d": d, "adj": adj, "groups": groups, "T": T})
+        v = {"d": d, "adj": adj, "groups": groups, "T": T}
+        if float_mode:
+            v["lam"], v["fflags"], v["dmax"], v["thrD"] = u32(), u32(), u64(), u64()
+            dc = u32()
+            v["dec"] = [(u32(), u64()) for _ in range(dc)]
+        out.append(v)
     assert pos == len(buf), (pos, len(buf))
     return out

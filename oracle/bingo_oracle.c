@@ -29,6 +29,7 @@
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <math.h>
 #ifdef _OPENMP
 #include <omp.h>
 #endif
@@ -106,10 +107,19 @@ typedef struct {
     uint32_t n;        /* number of nonempty groups */
     o_group *grp;      /* n groups, ascending k     */
     uint64_t T;        /* sum_k W(p_k) = sum_i w_i  */
+    /* floating-point bias mode (S4.3; reading R-15) */
+    uint32_t lam;      /* lambda = 10^lam                                   */
+    uint32_t fflags;   /* bit 0: constraint unmet, bit 1: integer part empty */
+    uint32_t dcnt;     /* decimal group: arcs with a nonzero decimal part   */
+    uint32_t *didx;    /* their adjacency indices, ascending                */
+    uint64_t *dval;    /* D_i = floor(frac(w_i lambda) 2^52)                */
+    uint64_t dmax;
+    uint64_t thrD;     /* decimal iff 64-bit draw < thrD                    */
 } o_vertex;
 
 typedef struct ora_graph {
     uint32_t V;
+    int float_mode;
     uint32_t alpha, beta, flags;
     uint32_t epoch;
     o_vertex *v;
@@ -279,6 +289,136 @@ int ora_build(uint32_t V, const uint64_t *row_offsets, const uint32_t *dst, cons
     return O_OK;
 }
 
+void ora_free(ora_graph *G);
+
+/* ------------------------------------------------------------------ */
+/* Floating-point biases (S4.3 P:344-363, S4.4 P:368-377; R-15).       */
+/* For lambda = 10^j, j = 0..9: s_i = fl(w_i lambda) (IEEE binary64),  */
+/* I_i = floor(s_i) must be < 2^32, D_i = floor((s_i - I_i) 2^52).      */
+/* W_I = sum I_i, W_D = sum D_i (units of 2^-52).  lambda = the        */
+/* smallest with W_D / (W_I 2^52 + W_D) < 1/d, i.e. (d-1) W_D < W_I 2^52;*/
+/* none -> the largest valid j, flag "constraint unmet".  Integer radix */
+/* groups are built over I_i (Eq.3-4, Eq.9); the decimal group holds    */
+/* the arcs with D_i > 0.  Inter-group: decimal with            */
+/* probability W_D / (W_I 2^52 + W_D) (64-bit threshold), else the      */
+/* integer alias.  Decimal intra-group: rejection with bound max D_i.   */
+/* ------------------------------------------------------------------ */
+static const double POW10[10] = {1e0, 1e1, 1e2, 1e3, 1e4, 1e5, 1e6, 1e7, 1e8, 1e9};
+
+static int scale_one(double w, int j, uint32_t *I, uint64_t *D)
+{
+    double s = w * POW10[j];
+    if (!(s < 4294967296.0)) return 0;
+    double fl = floor(s);
+    *I = (uint32_t)fl;
+    *D = (uint64_t)floor((s - fl) * 4503599627370496.0);   /* 2^52, exact scaling */
+    return 1;
+}
+
+/* floor(a * 2^64 / b) for a < b (binary long division, exact) */
+static uint64_t frac64(unsigned __int128 a, unsigned __int128 b)
+{
+    uint64_t q = 0;
+    for (int i = 0; i < 64; i++) {
+        a <<= 1;
+        q <<= 1;
+        if (a >= b) { a -= b; q |= 1; }
+    }
+    return q;
+}
+
+static int build_float_vertex(const ora_graph *G, o_vertex *x, const double *w)
+{
+    int chosen = -1, last_valid = -1;
+    for (int j = 0; j < 10; j++) {
+        unsigned __int128 WI = 0, WD = 0;
+        int valid = 1;
+        for (uint32_t i = 0; i < x->d; i++) {
+            uint32_t I;
+            uint64_t D;
+            if (!scale_one(w[i], j, &I, &D)) { valid = 0; break; }
+            WI += I;
+            WD += D;
+        }
+        if (!valid) break;             /* larger lambda only grows s_i */
+        last_valid = j;
+        if ((unsigned __int128)(x->d ? x->d - 1 : 0) * WD < (WI << 52)) { chosen = j; break; }
+    }
+    if (last_valid < 0 && x->d > 0) return O_EOVERFLOW;
+    x->fflags = 0;
+    if (chosen < 0) { chosen = last_valid < 0 ? 0 : last_valid; if (x->d) x->fflags |= 1u; }
+    x->lam = (uint32_t)chosen;
+    unsigned __int128 WI = 0, WD = 0;
+    x->dcnt = 0;
+    x->dmax = 0;
+    x->didx = (uint32_t *)malloc(sizeof(uint32_t) * (x->d ? x->d : 1));
+    x->dval = (uint64_t *)malloc(sizeof(uint64_t) * (x->d ? x->d : 1));
+    for (uint32_t i = 0; i < x->d; i++) {
+        uint32_t I;
+        uint64_t D;
+        scale_one(w[i], chosen, &I, &D);
+        x->adj[i].bias = I;            /* the integer part is the radix-decomposed bias */
+        WI += I;
+        WD += D;
+        if (D) {
+            x->didx[x->dcnt] = i;
+            x->dval[x->dcnt] = D;
+            x->dcnt++;
+            if (D > x->dmax) x->dmax = D;
+        }
+    }
+    if (WI == 0 && x->d) x->fflags |= 2u;
+    if (WD == 0) x->thrD = 0;
+    else if (WI == 0) x->thrD = ~0ull;                 /* always decimal (flag bit 1) */
+    else x->thrD = frac64(WD, (WI << 52) + WD);
+    (void)G;
+    return O_OK;
+}
+
+int ora_build_float(uint32_t V, const uint64_t *row_offsets, const uint32_t *dst, const double *wf,
+                    uint32_t alpha, uint32_t beta, uint32_t flags, ora_graph **out)
+{
+    *out = NULL;
+    for (uint32_t u = 0; u < V; u++)
+        if (row_offsets[u + 1] < row_offsets[u] || row_offsets[u + 1] - row_offsets[u] >= 0xFFFFFFFFull)
+            return O_EINVAL;
+    uint64_t A = row_offsets[V];
+    for (uint64_t a = 0; a < A; a++)
+        if (dst[a] >= V || !(wf[a] > 0.0) || wf[a] != wf[a] || wf[a] > 1e300) return O_EINVAL;
+    ora_graph *G = (ora_graph *)calloc(1, sizeof(ora_graph));
+    G->V = V;
+    G->float_mode = 1;
+    G->alpha = (flags & O_FLAG_BS_MODE) ? 100 : alpha;
+    G->beta = (flags & O_FLAG_BS_MODE) ? 0 : beta;
+    G->flags = flags;
+    G->v = (o_vertex *)calloc(V ? V : 1, sizeof(o_vertex));
+    for (uint32_t u = 0; u < V; u++) {
+        o_vertex *x = &G->v[u];
+        x->d = (uint32_t)(row_offsets[u + 1] - row_offsets[u]);
+        x->cap = x->d;
+        x->adj = (o_arc *)xrealloc(NULL, sizeof(o_arc) * (x->cap ? x->cap : 1));
+        for (uint32_t i = 0; i < x->d; i++) {
+            x->adj[i].dst = dst[row_offsets[u] + i];
+            x->adj[i].epoch = 0;
+        }
+        int rc = build_float_vertex(G, x, wf + row_offsets[u]);
+        if (rc == O_OK) {
+            unsigned __int128 T = 0;
+            uint32_t mask = 0;
+            for (uint32_t i = 0; i < x->d; i++) { T += x->adj[i].bias; mask |= x->adj[i].bias; }
+            if (T * (unsigned __int128)__builtin_popcount(mask) >= ((unsigned __int128)1 << 64)) rc = O_EOVERFLOW;
+        }
+        if (rc != O_OK) {
+            G->V = u + 1;
+            ora_free(G);
+            return rc;
+        }
+        build_vertex(G, x);
+    }
+    *out = G;
+    return O_OK;
+}
+
 void ora_free(ora_graph *G)
 {
     if (!G) return;
@@ -287,6 +427,8 @@ void ora_free(ora_graph *G)
         for (uint32_t b = 0; b < x->n; b++) free(x->grp[b].mem);
         free(x->grp);
         free(x->adj);
+        free(x->didx);
+        free(x->dval);
     }
     free(G->v);
     free(G);
@@ -483,6 +625,7 @@ int ora_apply_updates(ora_graph *G, const uint32_t *recs, uint64_t n, uint64_t *
 {
     uint64_t st[30];
     memset(st, 0, sizeof(st));
+    if (G->float_mode) return O_EINVAL;   /* float-bias updates: not defined in this round */
     for (uint64_t r = 0; r < n; r++) {
         const uint32_t *rec = recs + 4 * r;
         if (rec[0] > 1 || rec[1] >= G->V || rec[2] >= G->V) return O_EINVAL;
@@ -547,13 +690,28 @@ static uint32_t sample_arc(const o_vertex *x, uint64_t seed, uint32_t w, uint32_
                            uint32_t *attempts)
 {
     uint32_t r[4];
+    *attempts = 0;
+    if (x->thrD) {
+        /* float mode (R-15): the decimal group with probability thrD / 2^64 */
+        int dec = 1;
+        if (!(x->fflags & 2u)) {
+            draw(seed, w, t, outer << 16, 5, r);
+            dec = (((uint64_t)r[0] << 32) | r[1]) < x->thrD;
+        }
+        if (dec) {
+            for (uint32_t a = 0;; a++) {
+                draw(seed, w, t, (outer << 16) + a, 4, r);
+                uint64_t j = mulhi64(((uint64_t)r[0] << 32) | r[1], x->dcnt);
+                if (mulhi64(((uint64_t)r[2] << 32) | r[3], x->dmax) < x->dval[j]) return x->didx[j];
+            }
+        }
+    }
     draw(seed, w, t, outer << 16, 0, r);
     /* stage (i): inter-group alias */
     uint32_t b = (uint32_t)(((uint64_t)r[0] * x->n) >> 32);
     uint64_t coin = mulhi64(((uint64_t)r[1] << 32) | r[2], x->T);
     uint32_t gsel = (coin < x->grp[b].thr) ? b : x->grp[b].alias;
     const o_group *g = &x->grp[gsel];
-    *attempts = 0;
     /* stage (ii): intra-group */
     if (g->kind == O_ONE) return g->one;
     if (g->kind == O_REGULAR || g->kind == O_SPARSE) {
@@ -678,6 +836,8 @@ static void put64(o_out *o, uint64_t v)
     o->pos += 8;
 }
 
+static int g_dump_float = 0;
+
 static void dump_vertex(const o_vertex *x, o_out *o)
 {
     put32(o, x->d);
@@ -700,10 +860,22 @@ static void dump_vertex(const o_vertex *x, o_out *o)
             put32(o, g->one);
     }
     put64(o, x->T);
+    if (g_dump_float) {
+        put32(o, x->lam);
+        put32(o, x->fflags);
+        put64(o, x->dmax);
+        put64(o, x->thrD);
+        put32(o, x->dcnt);
+        for (uint32_t j = 0; j < x->dcnt; j++) {
+            put32(o, x->didx[j]);
+            put64(o, x->dval[j]);
+        }
+    }
 }
 
 size_t ora_dump(const ora_graph *G, uint8_t *buf, size_t cap)
 {
+    g_dump_float = G->float_mode;
     o_out o = {buf, cap, 0};
     for (uint32_t u = 0; u < G->V; u++) dump_vertex(&G->v[u], &o);
     return o.pos;
@@ -712,6 +884,7 @@ size_t ora_dump(const ora_graph *G, uint8_t *buf, size_t cap)
 /* Per-vertex FNV-1a 64 digest of the vertex's canonical dump bytes. */
 void ora_digests(const ora_graph *G, uint64_t *dig)
 {
+    g_dump_float = G->float_mode;
 #ifdef _OPENMP
 #pragma omp parallel for schedule(dynamic, 1024)
 #endif
