@@ -63,6 +63,13 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
  *   keeps a per-vertex hash set of destination ids (derived state, rebuilt for
  *   touched vertices by every update) so node2vec's "arc prev -> v exists?"
  *   test (Eq.1, A-17) is one probe instead of a scan of adj(prev).
+ *   BINGO_BUILD_FLOAT_BIAS takes real biases from bias_f64 (S4.3):
+ *   per vertex lambda = the smallest 10^j (j <= 9) with W_D/(W_I+W_D) < 1/d
+ *   (P:377), integer parts floor(w lambda) form the radix groups, fractional
+ *   parts (fixed point, 2^-52) form the decimal group sampled by rejection;
+ *   sampled probabilities are within 1e-6 relative of w/sum(w) (R-15).
+ *   Float-mode graphs are static in this version: bingo_apply_updates returns
+ *   BINGO_E_INVAL.  Exports append a per-vertex decimal trailer (R-11).
  * arc_slack / member_slack: fraction of extra per-vertex capacity reserved
  *   for growth (Hornet-style dynamic arrays + memory pool);
  *   pool_reserve: extra fraction of every pool for relocations.
@@ -74,6 +81,7 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
  * ------------------------------------------------------------------------- */
 #define BINGO_BUILD_BS_MODE 1u
 #define BINGO_BUILD_NEIGHBOR_INDEX 2u /* keep per-vertex neighbour hash sets: O(1) node2vec distance test */
+#define BINGO_BUILD_FLOAT_BIAS 4u     /* biases come from bias_f64 (S4.3 floating-point extension, R-15) */
 
 typedef void *(*bingo_alloc_fn)(size_t bytes, void *ctx);
 typedef void (*bingo_free_fn)(void *ptr, void *ctx);
@@ -92,6 +100,7 @@ typedef struct {
     bingo_alloc_fn alloc;
     bingo_free_fn free;
     void *alloc_ctx;
+    const double *bias_f64; /* device [A], > 0 and finite; used with BINGO_BUILD_FLOAT_BIAS */
 } bingo_build_desc;
 
 bingo_status bingo_build(const bingo_build_desc *desc, void *stream, bingo_graph **out);

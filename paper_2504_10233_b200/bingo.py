@@ -22,6 +22,7 @@ EMPTY, ONE, DENSE, SPARSE, REGULAR = 0, 1, 2, 3, 4
 DEEPWALK, NODE2VEC, PPR = 0, 1, 2
 BUILD_BS_MODE = 1
 BUILD_NEIGHBOR_INDEX = 2
+BUILD_FLOAT_BIAS = 4
 UPD_HOST_BATCH = 1
 WALK_HOST_OUTPUT = 1
 WALK_WALKER_MAJOR = 2
@@ -50,7 +51,7 @@ class BuildDesc(ctypes.Structure):
                 ("alpha_pct", ctypes.c_uint32), ("beta_pct", ctypes.c_uint32), ("flags", ctypes.c_uint32),
                 ("arc_slack", ctypes.c_double), ("member_slack", ctypes.c_double),
                 ("pool_reserve", ctypes.c_double), ("alloc", ALLOC_FN), ("free", FREE_FN),
-                ("alloc_ctx", ctypes.c_void_p)]
+                ("alloc_ctx", ctypes.c_void_p), ("bias_f64", ctypes.c_void_p)]
 
 
 class UpdateStats(ctypes.Structure):
@@ -180,7 +181,8 @@ class Graph:
 
     def __init__(self, row_offsets, dst, bias, alpha: int = 40, beta: int = 10, bs_mode: bool = False,
                  arc_slack: float = 0.25, member_slack: float = 0.25, pool_reserve: float = 0.1,
-                 neighbor_index: bool = False, device=None, stream=None, torch_alloc: bool = True):
+                 neighbor_index: bool = False, float_bias: bool = False, device=None, stream=None,
+                 torch_alloc: bool = True):
         torch = _torch()
         L = _lib()
         self.device = torch.device(device if device is not None else "cuda")
@@ -188,15 +190,23 @@ class Graph:
             self.device = torch.device("cuda", torch.cuda.current_device())
         ro = _dev_u64(row_offsets, torch, self.device)
         ds = _dev_u32(dst, torch, self.device)
-        bs = _dev_u32(bias, torch, self.device)
+        self.float_mode = bool(float_bias)
+        if float_bias:
+            bf = (bias.to(self.device, torch.float64) if isinstance(bias, torch.Tensor)
+                  else torch.from_numpy(np.ascontiguousarray(bias, dtype=np.float64)).to(self.device))
+            bs = torch.zeros(1, dtype=torch.int32, device=self.device)
+        else:
+            bf = None
+            bs = _dev_u32(bias, torch, self.device)
         self.V = ro.numel() - 1
         self._alloc = _TorchAllocator(self.device) if torch_alloc else None
         d = BuildDesc(num_vertices=self.V, num_arcs=ds.numel(), row_offsets=ro.data_ptr(), dst=ds.data_ptr(),
                       bias=bs.data_ptr(), alpha_pct=alpha, beta_pct=beta,
-                      flags=(BUILD_BS_MODE if bs_mode else 0) | (BUILD_NEIGHBOR_INDEX if neighbor_index else 0),
+                      flags=(BUILD_BS_MODE if bs_mode else 0) | (BUILD_NEIGHBOR_INDEX if neighbor_index else 0)
+                      | (BUILD_FLOAT_BIAS if float_bias else 0),
                       arc_slack=arc_slack, member_slack=member_slack, pool_reserve=pool_reserve,
                       alloc=self._alloc.alloc if self._alloc else ALLOC_FN(), free=self._alloc.free if self._alloc else FREE_FN(),
-                      alloc_ctx=None)
+                      alloc_ctx=None, bias_f64=bf.data_ptr() if bf is not None else None)
         h = ctypes.c_void_p()
         with torch.cuda.device(self.device):
             _check(L.bingo_build(ctypes.byref(d), _stream_ptr(stream), ctypes.byref(h)), "bingo_build")

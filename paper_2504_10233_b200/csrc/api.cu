@@ -32,7 +32,7 @@ void bingo_dev_free(bingo_graph *g, void *p) {
 
 extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
-    void *bufs[] = {g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->counters, g->visit, g->dev_flag,
+    void *bufs[] = {g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->dec, g->dmem, g->counters, g->visit, g->dev_flag,
                     g->scratch, g->wscratch, g->vscratch, g->fast_scr};
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
@@ -115,11 +115,17 @@ extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t c
     std::vector<Bucket> bkt(c[1]);
     std::vector<GCan> gc(c[1]);
     std::vector<uint32_t> mem(4 * c[2]);
+    std::vector<DecRec> dec(g->float_mode ? g->V : 0);
+    std::vector<uint4> dmem(g->float_mode ? g->dmem_cap : 0);
     if (c[0]) e = cudaMemcpyAsync(arc.data(), g->arc, sizeof(uint2) * c[0], cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && c[0]) e = cudaMemcpyAsync(ep.data(), g->arc_epoch, 4 * c[0], cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && c[1]) e = cudaMemcpyAsync(bkt.data(), g->bkt, sizeof(Bucket) * c[1], cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && c[1]) e = cudaMemcpyAsync(gc.data(), g->gcan, sizeof(GCan) * c[1], cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && c[2]) e = cudaMemcpyAsync(mem.data(), g->midx, sizeof(uint32_t) * 4 * c[2], cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && g->float_mode && g->V)
+        e = cudaMemcpyAsync(dec.data(), g->dec, sizeof(DecRec) * g->V, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && g->float_mode)
+        e = cudaMemcpyAsync(dmem.data(), g->dmem, sizeof(uint4) * g->dmem_cap, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     Out o{(host_buf && cap) ? host_buf : nullptr, cap, 0};
@@ -147,6 +153,19 @@ extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t c
                 o.u32(G.aux);
         }
         o.u64(h.T);
+        if (g->float_mode) {
+            const DecRec &r = dec[u];
+            o.u32(r.lam);
+            o.u32(r.flags);
+            o.u64(r.dmax);
+            o.u64(r.thrD);
+            o.u32(r.dcnt);
+            for (uint32_t j = 0; j < r.dcnt; j++) {
+                const uint4 &m = dmem[(size_t)r.doff + j];
+                o.u32(m.x);
+                o.u64(((uint64_t)m.w << 32) | m.z);
+            }
+        }
     }
     *size_out = o.pos;
     if (host_buf && o.pos > cap) return BINGO_E_INVAL;
@@ -170,7 +189,8 @@ __device__ __forceinline__ uint64_t fnv64(uint64_t h, uint64_t v) {
 
 __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 *__restrict__ arc,
                           const uint32_t *__restrict__ ep, const Bucket *__restrict__ bkt,
-                          const GCan *__restrict__ gcan, const uint32_t *__restrict__ midx, uint64_t *__restrict__ out) {
+                          const GCan *__restrict__ gcan, const uint32_t *__restrict__ midx,
+                          const DecRec *__restrict__ dec, const uint4 *__restrict__ dmem, uint64_t *__restrict__ out) {
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
         const VHdr h = hdr[u];
         uint64_t x = 0xcbf29ce484222325ull;
@@ -196,7 +216,21 @@ __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 
             else if (kind == K_ONE)
                 x = fnv32(x, G.aux);
         }
-        out[u] = fnv64(x, h.T);
+        x = fnv64(x, h.T);
+        if (dec) {
+            const DecRec r = dec[u];
+            x = fnv32(x, r.lam);
+            x = fnv32(x, r.flags);
+            x = fnv64(x, r.dmax);
+            x = fnv64(x, r.thrD);
+            x = fnv32(x, r.dcnt);
+            for (uint32_t j = 0; j < r.dcnt; j++) {
+                const uint4 m = dmem[(uint64_t)r.doff + j];
+                x = fnv32(x, m.x);
+                x = fnv64(x, ((uint64_t)m.w << 32) | m.z);
+            }
+        }
+        out[u] = x;
     }
 }
 }  // namespace bingo
@@ -207,7 +241,8 @@ extern "C" bingo_status bingo_digests(bingo_graph *g, uint64_t *digests, void *s
     if (!g->V) return BINGO_OK;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)g->V + 255) / 256, 148ull * 16);
-    k_digests<<<blocks, 256, 0, s>>>(g->V, g->hdr, g->arc, g->arc_epoch, g->bkt, g->gcan, g->midx, digests);
+    k_digests<<<blocks, 256, 0, s>>>(g->V, g->hdr, g->arc, g->arc_epoch, g->bkt, g->gcan, g->midx,
+                                                 g->float_mode ? g->dec : nullptr, g->dmem, digests);
     bingo_count_launch();
     if (cudaGetLastError() != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     return BINGO_OK;

@@ -36,6 +36,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "float_bias.cuh"
+
 namespace bingo {
 
 enum : uint32_t { K_EMPTY = 0, K_ONE = 1, K_DENSE = 2, K_SPARSE = 3, K_REGULAR = 4 };
@@ -157,6 +159,10 @@ struct bingo_graph {
     uint32_t hot_mem_degree = 0xFFFFFFFFu; // d >= this: member dsts loaded evict_last
     uint32_t *mdst = nullptr;          // [mem_cap] member dst (walker side)
     uint32_t *midx = nullptr;          // [mem_cap] member adjacency index (canonical)
+    bool float_mode = false;
+    bingo::DecRec *dec = nullptr;      // [V] decimal-group records (float mode)
+    uint4 *dmem = nullptr;             // decimal members {idx, dst, D lo, D hi}
+    uint64_t dmem_cap = 0;
     uint32_t *nbt = nullptr;           // [4 * arc_cap] neighbour hash sets (node2vec), optional
     uint64_t *nbo = nullptr;           // [V] hash-set base | log2 size << 48
     uint64_t mem_cap = 0;              // entries

@@ -29,7 +29,7 @@ __global__ void k_build_sizes(uint32_t V, const uint64_t *__restrict__ ro, const
                               const uint32_t *__restrict__ bias, uint32_t alpha, uint32_t beta, bool bs,
                               double arc_slack, double mem_slack, uint64_t *__restrict__ sz_arc,
                               uint64_t *__restrict__ sz_bkt, uint64_t *__restrict__ sz_mem, int *__restrict__ flag,
-                              unsigned long long *__restrict__ hot_hist) {
+                              unsigned long long *__restrict__ hot_hist, bool allow_zero) {
     __shared__ unsigned long long s_hist[2 * HOT_BINS];
     for (int i = threadIdx.x; i < 2 * HOT_BINS; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
@@ -51,7 +51,7 @@ __global__ void k_build_sizes(uint32_t V, const uint64_t *__restrict__ ro, const
             if (i < d) {
                 w = bias[b0 + i];
                 uint32_t v = dst[b0 + i];
-                if (w == 0 || v >= V) atomicOr(flag, 1);
+                if ((w == 0 && !allow_zero) || v >= V) atomicOr(flag, 1);
                 tsum += w;
             }
             mask |= w;
@@ -272,6 +272,10 @@ static bingo_status fail_cuda(bingo_graph *g, cudaError_t e, const char *where) 
         if (e_ != cudaSuccess) { st = fail_cuda(g, e_, #call); goto done; } \
     } while (0)
 
+bingo_status float_prepare(bingo_graph *g, const bingo_build_desc *desc, uint32_t *ibias, uint64_t *dcnt,
+                           uint64_t *dscan, uint64_t *tmp, cudaStream_t s, uint64_t *total_dec);
+bingo_status float_fill(bingo_graph *g, const bingo_build_desc *desc, const uint64_t *dscan, cudaStream_t s);
+
 extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, bingo_graph **out) {
     if (!desc || !out) return BINGO_E_INVAL;
     *out = nullptr;
@@ -304,6 +308,10 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     unsigned long long hc[4];
     unsigned long long *dhist = nullptr;
     unsigned long long hhist[2 * HOT_BINS];
+    const bool fm = (desc->flags & BINGO_BUILD_FLOAT_BIAS) != 0;
+    bingo_build_desc idesc = *desc;      // the integer build's view (float mode: integer parts)
+    uint32_t *ibias = nullptr;
+    uint64_t *dcnt = nullptr, *dscan = nullptr, total_dec = 0;
     const unsigned blocks = (unsigned)std::min<uint64_t>((nV + 7) / 8, 148ull * 64);
 
     g->counters = (unsigned long long *)bingo_dev_alloc(g, 16 * sizeof(unsigned long long));
@@ -320,15 +328,30 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
         goto done;
     }
     CK(cudaMemsetAsync(dhist, 0, sizeof(unsigned long long) * 2 * HOT_BINS, s));
+    if (fm) {
+        g->float_mode = true;
+        if (desc->num_arcs && !desc->bias_f64) { st = BINGO_E_INVAL; goto done; }
+        g->dec = (DecRec *)bingo_dev_alloc(g, sizeof(DecRec) * std::max<uint64_t>(nV, 1));
+        ibias = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * std::max<uint64_t>(desc->num_arcs, 1));
+        dcnt = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (nV + 1));
+        dscan = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (nV + 1));
+        if (!g->dec || !ibias || !dcnt || !dscan) { st = BINGO_E_NOMEM; goto done; }
+        CK(cudaMemsetAsync(g->dec, 0, sizeof(DecRec) * std::max<uint64_t>(nV, 1), s));
+        if (V) {
+            st = float_prepare(g, desc, ibias, dcnt, dscan, tmp, s, &total_dec);
+            if (st != BINGO_OK) { if (st == BINGO_E_CUDA) g->poisoned = 1; goto done; }
+        }
+        idesc.bias = ibias;
+    }
     CK(cudaMemsetAsync(g->counters, 0, 16 * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(g->dev_flag, 0, sizeof(int) * 4, s));
     CK(cudaMemsetAsync(g->visit, 0, sizeof(unsigned long long) * std::max<uint64_t>(nV, 1), s));
     CK(cudaMemsetAsync(g->hdr, 0, sizeof(VHdr) * std::max<uint64_t>(nV, 1), s));
     CK(cudaMemsetAsync(g->thdr, 0, sizeof(ThinHdr) * std::max<uint64_t>(nV, 1), s));
     if (V) {
-        k_build_sizes<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
+        k_build_sizes<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, idesc.bias, g->alpha, g->beta, bs,
                                              g->arc_slack, g->member_slack, sz, sz + (nV + 1), sz + 2 * (nV + 1),
-                                             g->dev_flag, dhist);
+                                             g->dev_flag, dhist, fm);
         bingo_count_launch();
         CK(cudaGetLastError());
         for (int p = 0; p < 3; p++) CK(exclusive_scan_u64(sz + p * (nV + 1), off + p * (nV + 1), nV, tmp, s));
@@ -358,12 +381,21 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     hc[0] = tot[0]; hc[1] = tot[1]; hc[2] = tot[2]; hc[3] = 0;
     CK(cudaMemcpyAsync(g->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
     if (V) {
-        k_build_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, g->alpha, g->beta, bs,
+        k_build_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, idesc.bias, g->alpha, g->beta, bs,
                                             g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), g->hdr, g->thdr,
                                             g->arc, g->arc_epoch, g->bkt, g->gcan, g->mdst, g->midx,
                                             g->hot_bkt_degree, g->hot_mem_degree);
         bingo_count_launch();
         CK(cudaGetLastError());
+    }
+    if (fm) {
+        g->dmem_cap = std::max<uint64_t>(total_dec, 1);
+        g->dmem = (uint4 *)bingo_dev_alloc(g, sizeof(uint4) * g->dmem_cap);
+        if (!g->dmem) { st = BINGO_E_NOMEM; goto done; }
+        if (V) {
+            st = float_fill(g, desc, dscan, s);
+            if (st != BINGO_OK) { g->poisoned = 1; goto done; }
+        }
     }
     if (desc->flags & BINGO_BUILD_NEIGHBOR_INDEX) {
         g->nbt = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * g->arc_cap);
@@ -381,6 +413,9 @@ done:
     bingo_dev_free(g, off);
     bingo_dev_free(g, tmp);
     bingo_dev_free(g, dhist);
+    bingo_dev_free(g, ibias);
+    bingo_dev_free(g, dcnt);
+    bingo_dev_free(g, dscan);
     if (st != BINGO_OK) {
         bingo_destroy(g);
         return st;

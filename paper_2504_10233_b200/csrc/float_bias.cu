@@ -1,0 +1,189 @@
+// float_bias.cu -- floating-point biases (S4.3 P:344-363, S4.4 P:368-377; R-15), build side.
+//
+// Per vertex (warp): for lambda = 10^j, j = 0..9, s_i = fl(w_i lambda) (IEEE binary64,
+// round-to-nearest, no contraction), I_i = floor(s_i) < 2^32, D_i = floor((s_i - I_i) 2^52)
+// (exact), W_I = sum I_i, W_D = sum D_i (u128).  lambda = the smallest j with
+// (d - 1) W_D < W_I 2^52 (W_D / (W_I + W_D) < 1/d in real units); none -> the largest
+// valid j and flag "constraint unmet".  The integer parts I_i become the arcs' radix-
+// decomposed biases (the integer build then runs unchanged); the decimal group is the
+// arcs with D_i > 0, ascending; thrD = floor(W_D 2^64 / (W_I 2^52 + W_D)).
+#include <cstdio>
+
+#include "bingo.h"
+#include "bingo_internal.cuh"
+#include "build_common.cuh"
+#include "float_bias.cuh"
+#include "scan.cuh"
+
+namespace bingo {
+
+__device__ __forceinline__ bool scale_one(double w, int j, uint32_t &I, uint64_t &D) {
+    const double s = __dmul_rn(w, pow10_exact(j));
+    if (!(s < 4294967296.0)) return false;
+    const double fl = floor(s);
+    I = (uint32_t)fl;
+    D = (uint64_t)floor(__dmul_rn(__dsub_rn(s, fl), 4503599627370496.0));   // 2^52
+    return true;
+}
+
+__device__ __forceinline__ unsigned __int128 warp_sum128(unsigned __int128 v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t lo = __shfl_xor_sync(0xffffffffu, (uint64_t)v, o);
+        const uint64_t hi = __shfl_xor_sync(0xffffffffu, (uint64_t)(v >> 64), o);
+        v += ((unsigned __int128)hi << 64) | lo;
+    }
+    return v;
+}
+
+// floor(a 2^64 / b) for a < b, binary long division (exact)
+__device__ __forceinline__ uint64_t frac64(unsigned __int128 a, unsigned __int128 b) {
+    uint64_t q = 0;
+    for (int i = 0; i < 64; i++) {
+        a <<= 1;
+        q <<= 1;
+        if (a >= b) { a -= b; q |= 1; }
+    }
+    return q;
+}
+
+__global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, const double *__restrict__ wf,
+                               uint32_t *__restrict__ ibias, DecRec *__restrict__ dec, uint64_t *__restrict__ dcnt_out,
+                               int *__restrict__ flag) {
+    const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
+    const uint32_t lane = lane_id();
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+        const uint64_t b0 = ro[u];
+        const uint32_t d = (uint32_t)(ro[u + 1] - b0);
+        // input validation: w > 0, finite, <= 1e300
+        bool bad = false;
+        for (uint32_t i = lane; i < d; i += 32) {
+            const double w = wf[b0 + i];
+            if (!(w > 0.0) || !(w <= 1e300)) bad = true;
+        }
+        if (__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) atomicOr(flag, 1);
+            continue;
+        }
+        int chosen = -1, last_valid = -1;
+        for (int j = 0; j < 10 && chosen < 0; j++) {
+            unsigned __int128 wi = 0, wd = 0;
+            bool valid = true;
+            for (uint32_t i = lane; i < d; i += 32) {
+                uint32_t I;
+                uint64_t D;
+                if (!scale_one(wf[b0 + i], j, I, D)) { valid = false; break; }
+                wi += I;
+                wd += D;
+            }
+            if (!__all_sync(0xffffffffu, valid)) break;     // larger lambda only grows s_i
+            wi = warp_sum128(wi);
+            wd = warp_sum128(wd);
+            last_valid = j;
+            if ((unsigned __int128)(d ? d - 1 : 0) * wd < (wi << 52)) chosen = j;
+        }
+        if (last_valid < 0 && d > 0) {
+            if (lane == 0) atomicOr(flag, 4);
+            continue;
+        }
+        uint32_t fl = 0;
+        if (chosen < 0) {
+            chosen = last_valid < 0 ? 0 : last_valid;
+            if (d) fl |= 1u;
+        }
+        unsigned __int128 wi = 0, wd = 0;
+        uint64_t dmax = 0;
+        uint32_t cnt = 0;
+        for (uint32_t i = lane; i < d; i += 32) {
+            uint32_t I;
+            uint64_t D;
+            scale_one(wf[b0 + i], chosen, I, D);
+            ibias[b0 + i] = I;
+            wi += I;
+            wd += D;
+            dmax = D > dmax ? D : dmax;
+            cnt += D ? 1u : 0u;
+        }
+        wi = warp_sum128(wi);
+        wd = warp_sum128(wd);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t m = __shfl_xor_sync(0xffffffffu, dmax, o);
+            dmax = m > dmax ? m : dmax;
+            cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        }
+        if (lane == 0) {
+            if (wi == 0 && d) fl |= 2u;
+            DecRec r;
+            r.thrD = wd == 0 ? 0ull : (wi == 0 ? ~0ull : frac64(wd, (wi << 52) + wd));
+            r.dmax = dmax;
+            r.doff = 0;
+            r.dcnt = cnt;
+            r.lam = (uint8_t)chosen;
+            r.flags = (uint8_t)fl;
+            r.pad = 0;
+            r.pad2 = 0;
+            dec[u] = r;
+            dcnt_out[u] = cnt;
+        }
+    }
+}
+
+// decimal members (ascending adjacency index), after the integer build placed the arcs
+__global__ void k_float_fill(uint32_t V, const uint64_t *__restrict__ ro, const uint32_t *__restrict__ dst,
+                             const double *__restrict__ wf, const uint64_t *__restrict__ doff,
+                             DecRec *__restrict__ dec, uint4 *__restrict__ dmem) {
+    const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
+    const uint32_t lane = lane_id();
+    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+        const uint64_t b0 = ro[u];
+        const uint32_t d = (uint32_t)(ro[u + 1] - b0);
+        const int lam = dec[u].lam;
+        const uint64_t base = doff[u];
+        uint32_t run = 0;
+        for (uint32_t c0 = 0; c0 < d; c0 += 32) {
+            const uint32_t i = c0 + lane;
+            uint32_t I = 0;
+            uint64_t D = 0;
+            if (i < d) scale_one(wf[b0 + i], lam, I, D);
+            const uint32_t bal = __ballot_sync(0xffffffffu, D != 0);
+            if (D) dmem[base + run + __popc(bal & lanemask_lt())] = make_uint4(i, dst[b0 + i], (uint32_t)D, (uint32_t)(D >> 32));
+            run += __popc(bal);
+        }
+        if (lane == 0) dec[u].doff = (uint32_t)base;
+    }
+}
+
+}  // namespace bingo
+
+using namespace bingo;
+
+// Called by bingo_build in float mode: validates, picks lambda, writes the integer parts
+// into `ibias` (device [A]) and the decimal records; the caller runs the integer build on
+// ibias and then float_fill().
+bingo_status float_prepare(bingo_graph *g, const bingo_build_desc *desc, uint32_t *ibias, uint64_t *dcnt,
+                           uint64_t *dscan, uint64_t *tmp, cudaStream_t s, uint64_t *total_dec) {
+    const uint32_t V = desc->num_vertices;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)V + 7) / 8, 148ull * 64);
+    int hflag = 0;
+    if (cudaMemsetAsync(g->dev_flag, 0, sizeof(int), s) != cudaSuccess) return BINGO_E_CUDA;
+    k_float_lambda<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->bias_f64, ibias, g->dec, dcnt, g->dev_flag);
+    bingo_count_launch();
+    if (cudaGetLastError() != cudaSuccess) return BINGO_E_CUDA;
+    if (exclusive_scan_u64(dcnt, dscan, V, tmp, s) != cudaSuccess) return BINGO_E_CUDA;
+    if (cudaMemcpyAsync(&hflag, g->dev_flag, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaMemcpyAsync(total_dec, dscan + V, sizeof(uint64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return BINGO_E_CUDA;
+    if (hflag & 1) return BINGO_E_INVAL;
+    if (hflag & 4) return BINGO_E_OVERFLOW;
+    return BINGO_OK;
+}
+
+bingo_status float_fill(bingo_graph *g, const bingo_build_desc *desc, const uint64_t *dscan, cudaStream_t s) {
+    const uint32_t V = desc->num_vertices;
+    const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)V + 7) / 8, 148ull * 64);
+    k_float_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias_f64, dscan, g->dec, g->dmem);
+    bingo_count_launch();
+    return cudaGetLastError() == cudaSuccess ? BINGO_OK : BINGO_E_CUDA;
+}

@@ -1191,6 +1191,7 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     if (!g) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     if (n && !batch) return BINGO_E_INVAL;
+    if (g->float_mode) return BINGO_E_INVAL;   // float-bias graphs are static in this version
     if (n >= 0xFFFFFFFFull) return BINGO_E_INVAL;
     cudaStream_t s = (cudaStream_t)stream;
     if (stats) memset(stats, 0, sizeof(*stats));

@@ -47,20 +47,25 @@ __global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BIN
         for (uint32_t t = 0; a.L == BINGO_NO_CAP || t < a.L; t++) {
             const ThinHdr h = load_thdr(a.thdr + u, pol);
             if (APP == BINGO_NODE2VEC && a.nbo) cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
+            DecRec dr;
+            dr.dcnt = 0;
+            if (a.dec) dr = load_dec(a.dec + u);
             if (PROF) prof.hdr++;
-            if (h.n == 0) break;   // dead end (d = 0): truncate (R-13)
+            if (h.n == 0 && dr.dcnt == 0) break;   // dead end (d = 0): truncate (R-13)
             uint32_t next;
             if (APP == BINGO_NODE2VEC && t >= 1) {
                 // KnightKing rejection: propose first-order, accept with f/f_max
                 for (uint32_t o = 0;; o++) {
-                    next = sample_dst<PROF>(a, h, w, t, o, prof, pol);
+                    next = a.dec ? sample_dst_f<PROF>(a, h, dr, w, t, o, prof, pol)
+                                 : sample_dst<PROF>(a, h, w, t, o, prof, pol);
                     const uint32_t cls = (next == prev) ? 0u : (probe_arc<PROF>(a, prev, prev_nbo, next, prof) ? 1u : 2u);
                     if (a.n2v_always[cls]) break;
                     const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
                     if (join64(r.x, r.y) < a.n2v_thr[cls]) break;
                 }
             } else {
-                next = sample_dst<PROF>(a, h, w, t, 0, prof, pol);
+                next = a.dec ? sample_dst_f<PROF>(a, h, dr, w, t, 0, prof, pol)
+                             : sample_dst<PROF>(a, h, w, t, 0, prof, pol);
             }
             steps++;
             if (PROF) prof.steps++;
@@ -146,6 +151,8 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     a.mdst = g->mdst;
     a.nbt = g->nbt;
     a.nbo = g->nbo;
+    a.dec = g->float_mode ? g->dec : nullptr;
+    a.dmem = g->dmem;
     a.visit = g->visit;
     a.starts = starts;
     a.paths = paths;

@@ -34,6 +34,8 @@ struct WalkArgs {
     const uint32_t *mdst;
     const uint32_t *nbt;
     const uint64_t *nbo;
+    const DecRec *dec;      // float mode (R-15) or null
+    const uint4 *dmem;
     unsigned long long *visit;
     const uint32_t *starts;
     uint32_t *paths;
@@ -147,6 +149,48 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
         }
         if (done) return res;
     }
+}
+
+__device__ __forceinline__ DecRec load_dec(const DecRec *p) {
+    uint4 lo, hi;
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
+                 : "l"(p));
+    DecRec r;
+    r.thrD = ((uint64_t)lo.y << 32) | lo.x;
+    r.dmax = ((uint64_t)lo.w << 32) | lo.z;
+    r.doff = hi.x;
+    r.dcnt = hi.y;
+    r.lam = (uint8_t)(hi.z & 0xff);
+    r.flags = (uint8_t)((hi.z >> 8) & 0xff);
+    r.pad = 0;
+    r.pad2 = 0;
+    return r;
+}
+
+// Float mode (R-15): the decimal group with probability thrD / 2^64 (tag 5), sampled by
+// rejection (tag 4: index floor(x |D| / 2^64), accept iff floor(y Dmax / 2^64) < D_j);
+// otherwise the integer two-stage sample over the radix groups of floor(w lambda).
+template <bool PROF>
+__device__ __forceinline__ uint32_t sample_dst_f(const WalkArgs &a, const ThinHdr &h, const DecRec &dr, uint32_t w,
+                                                 uint32_t t, uint32_t outer, WalkProf &prof, const Policies &pol) {
+    if (dr.thrD) {
+        bool decimal = true;
+        if (!(dr.flags & 2u)) {
+            const P4 r = philox10(w, t, outer << 16, 5u, a.k0, a.k1);
+            decimal = join64(r.x, r.y) < dr.thrD;
+        }
+        if (decimal) {
+            for (uint32_t att = 0;; att++) {
+                const P4 q = philox10(w, t, (outer << 16) + att, 4u, a.k0, a.k1);
+                const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)dr.dcnt);
+                const uint4 e = __ldg(a.dmem + dr.doff + j);
+                if (PROF) prof.arc++;
+                if (__umul64hi(join64(q.z, q.w), dr.dmax) < (((uint64_t)e.w << 32) | e.z)) return e.y;
+            }
+        }
+    }
+    return sample_dst<PROF>(a, h, w, t, outer, prof, pol);
 }
 
 // node2vec distance-1 test (Eq.1, A-17): does a live arc prev -> v exist?
