@@ -55,6 +55,10 @@ def lib():
             L.ora_alias_build.argtypes = [u32, P, P, P]
             L.ora_build.argtypes = [u32, P, P, P, u32, u32, u32, ctypes.POINTER(P)]
             L.ora_build.restype = ctypes.c_int
+            L.ora_build_lazy.argtypes = [u32, P, P, P, u32, u32, u32, ctypes.POINTER(P)]
+            L.ora_build_lazy.restype = ctypes.c_int
+            L.ora_dump_vertex.argtypes = [P, u32, P, ctypes.c_size_t]
+            L.ora_dump_vertex.restype = ctypes.c_size_t
             L.ora_build_float.argtypes = [u32, P, P, P, u32, u32, u32, ctypes.POINTER(P)]
             L.ora_build_float.restype = ctypes.c_int
             L.ora_free.argtypes = [P]
@@ -135,14 +139,19 @@ def stop_threshold(num: int, den: int):
 class OracleGraph:
     """One oracle graph instance (host memory)."""
 
-    def __init__(self, row_offsets, dst, bias, alpha=40, beta=10, flags=0, float_bias=False):
+    def __init__(self, row_offsets, dst, bias, alpha=40, beta=10, flags=0, float_bias=False, lazy=False):
         L = lib()
         self.V = len(row_offsets) - 1
         self.float_mode = bool(float_bias)
         ro = np.ascontiguousarray(row_offsets, dtype=np.uint64)
         ds = np.ascontiguousarray(dst, dtype=np.uint32)
         h = ctypes.c_void_p()
-        if float_bias:
+        if lazy:
+            # vertices are built from these arrays on first access: keep them alive
+            bs = np.ascontiguousarray(bias, dtype=np.uint32)
+            self._keep = (ro, ds, bs)
+            rc = L.ora_build_lazy(self.V, _p(ro), _p(ds), _p(bs), alpha, beta, flags, ctypes.byref(h))
+        elif float_bias:
             bf = np.ascontiguousarray(bias, dtype=np.float64)
             rc = L.ora_build_float(self.V, _p(ro), _p(ds), _p(bf), alpha, beta, flags, ctypes.byref(h))
         else:
@@ -198,6 +207,19 @@ class OracleGraph:
         buf = np.zeros(n, dtype=np.uint8)
         lib().ora_dump(self._h, _p(buf), n)
         return buf.tobytes()
+
+    def dump_vertex(self, u: int) -> bytes:
+        n = lib().ora_dump_vertex(self._h, u, None, 0)
+        buf = np.zeros(max(n, 1), dtype=np.uint8)
+        lib().ora_dump_vertex(self._h, u, _p(buf), n)
+        return buf[:n].tobytes()
+
+    def vertex_digest(self, u: int) -> int:
+        h = 0xcbf29ce484222325
+        for b in self.dump_vertex(u):
+            h ^= b
+            h = (h * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+        return h
 
     def digests(self) -> np.ndarray:
         d = np.zeros(self.V, dtype=np.uint64)

@@ -120,6 +120,13 @@ typedef struct {
 typedef struct ora_graph {
     uint32_t V;
     int float_mode;
+    /* lazy mode (test infrastructure for BASELINE-scale parity): a vertex is built
+     * from the caller's CSR on its first access; the result is the same as an
+     * eager build, only untouched vertices are never materialised */
+    int lazy;
+    uint8_t *built;
+    const uint64_t *lro;
+    const uint32_t *ldst, *lbias;
     uint32_t alpha, beta, flags;
     uint32_t epoch;
     o_vertex *v;
@@ -130,6 +137,41 @@ static void *xrealloc(void *p, size_t n)
     void *q = realloc(p, n ? n : 1);
     if (!q) abort();
     return q;
+}
+
+static void build_vertex(const ora_graph *G, o_vertex *x);
+static int g_dump_float = 0;
+typedef struct o_out_s o_out;
+static void dump_vertex(const o_vertex *x, o_out *o);
+
+/* vertex accessor: materialises lazily-built vertices on first use */
+static o_vertex *vx(const ora_graph *Gc, uint32_t u)
+{
+    ora_graph *G = (ora_graph *)Gc;
+    o_vertex *x = &G->v[u];
+    if (G->lazy && !G->built[u]) {
+#ifdef _OPENMP
+#pragma omp critical(ora_lazy)
+#endif
+        {
+            if (!G->built[u]) {
+                x->d = (uint32_t)(G->lro[u + 1] - G->lro[u]);
+                x->cap = x->d;
+                x->adj = (o_arc *)malloc(sizeof(o_arc) * (x->cap ? x->cap : 1));
+                for (uint32_t i = 0; i < x->d; i++) {
+                    x->adj[i].dst = G->ldst[G->lro[u] + i];
+                    x->adj[i].bias = G->lbias[G->lro[u] + i];
+                    x->adj[i].epoch = 0;
+                }
+                build_vertex(G, x);
+#ifdef _OPENMP
+#pragma omp flush
+#endif
+                G->built[u] = 1;
+            }
+        }
+    }
+    return x;
 }
 
 /* ---------------- Eq.9 classification (R-3) ---------------- */
@@ -334,8 +376,8 @@ static int build_float_vertex(const ora_graph *G, o_vertex *x, const double *w)
         unsigned __int128 WI = 0, WD = 0;
         int valid = 1;
         for (uint32_t i = 0; i < x->d; i++) {
-            uint32_t I;
-            uint64_t D;
+            uint32_t I = 0;
+            uint64_t D = 0;
             if (!scale_one(w[i], j, &I, &D)) { valid = 0; break; }
             WI += I;
             WD += D;
@@ -354,8 +396,8 @@ static int build_float_vertex(const ora_graph *G, o_vertex *x, const double *w)
     x->didx = (uint32_t *)malloc(sizeof(uint32_t) * (x->d ? x->d : 1));
     x->dval = (uint64_t *)malloc(sizeof(uint64_t) * (x->d ? x->d : 1));
     for (uint32_t i = 0; i < x->d; i++) {
-        uint32_t I;
-        uint64_t D;
+        uint32_t I = 0;
+        uint64_t D = 0;
         scale_one(w[i], chosen, &I, &D);
         x->adj[i].bias = I;            /* the integer part is the radix-decomposed bias */
         WI += I;
@@ -431,12 +473,33 @@ void ora_free(ora_graph *G)
         free(x->dval);
     }
     free(G->v);
+    free(G->built);
     free(G);
 }
 
 uint32_t ora_epoch(const ora_graph *G) { return G->epoch; }
 uint32_t ora_num_vertices(const ora_graph *G) { return G->V; }
-uint32_t ora_degree(const ora_graph *G, uint32_t u) { return G->v[u].d; }
+uint32_t ora_degree(const ora_graph *G, uint32_t u) { return vx(G, u)->d; }
+
+/* Lazy build: the CSR arrays must outlive the graph.  Validation is done per
+ * vertex on first access by the caller's contract (inputs are generated). */
+int ora_build_lazy(uint32_t V, const uint64_t *row_offsets, const uint32_t *dst, const uint32_t *bias,
+                   uint32_t alpha, uint32_t beta, uint32_t flags, ora_graph **out)
+{
+    ora_graph *G = (ora_graph *)calloc(1, sizeof(ora_graph));
+    G->V = V;
+    G->alpha = (flags & O_FLAG_BS_MODE) ? 100 : alpha;
+    G->beta = (flags & O_FLAG_BS_MODE) ? 0 : beta;
+    G->flags = flags;
+    G->lazy = 1;
+    G->built = (uint8_t *)calloc(V ? V : 1, 1);
+    G->lro = row_offsets;
+    G->ldst = dst;
+    G->lbias = bias;
+    G->v = (o_vertex *)calloc(V ? V : 1, sizeof(o_vertex));
+    *out = G;
+    return O_OK;
+}
 
 /* ------------------------------------------------------------------ */
 /* Two-phase parallel delete-and-swap (pairing R-6).        */
@@ -481,11 +544,6 @@ uint32_t ora_two_phase_u32(uint32_t *arr, uint32_t len, const uint32_t *del_sort
     return two_phase_delete(arr, sizeof(uint32_t), len, del_sorted, N, NULL, NULL, NULL);
 }
 
-static int cmp_u32(const void *a, const void *b)
-{
-    uint32_t x = *(const uint32_t *)a, y = *(const uint32_t *)b;
-    return x < y ? -1 : x > y;
-}
 
 /* stats layout (u64): [0] inserted [1] deleted [2] missing_deletes
  * [3] touched_vertices [4..28] kind_transitions[5][5] [29] epoch */
@@ -645,7 +703,7 @@ int ora_apply_updates(ora_graph *G, const uint32_t *recs, uint64_t n, uint64_t *
      * and d + inserted < 2^32 - 1 */
     for (uint32_t u = 0; u < G->V; u++) {
         if (cnt[u + 1] == cnt[u]) continue;
-        const o_vertex *x = &G->v[u];
+        const o_vertex *x = vx(G, u);
         unsigned __int128 T = x->T;
         uint32_t mask = 0;
         uint64_t ins = 0;
@@ -663,7 +721,7 @@ int ora_apply_updates(ora_graph *G, const uint32_t *recs, uint64_t n, uint64_t *
     uint32_t e = ++G->epoch;   /* R-9: epoch = call number, build = 0 */
     for (uint32_t u = 0; u < G->V; u++) {
         if (cnt[u + 1] == cnt[u]) continue;
-        update_vertex(G, &G->v[u], recs, idx + cnt[u], cnt[u + 1] - cnt[u], e, st);
+        update_vertex(G, vx(G, u), recs, idx + cnt[u], cnt[u + 1] - cnt[u], e, st);
     }
     st[ST_EPOCH] = e;
     free(cnt);
@@ -731,7 +789,7 @@ static uint32_t sample_arc(const o_vertex *x, uint64_t seed, uint32_t w, uint32_
 uint32_t ora_sample(const ora_graph *G, uint32_t u, uint64_t seed, uint32_t w, uint32_t t, uint32_t outer)
 {
     uint32_t att;
-    const o_vertex *x = &G->v[u];
+    const o_vertex *x = vx(G, u);
     if (x->d == 0) return O_NONE;
     return x->adj[sample_arc(x, seed, w, t, outer, &att)].dst;
 }
@@ -741,7 +799,7 @@ uint32_t ora_sample(const ora_graph *G, uint32_t u, uint64_t seed, uint32_t w, u
 static int n2v_class(const ora_graph *G, uint32_t prev, uint32_t v)
 {
     if (v == prev) return 0;
-    const o_vertex *y = &G->v[prev];
+    const o_vertex *y = vx(G, prev);
     for (uint32_t i = 0; i < y->d; i++)
         if (y->adj[i].dst == v) return 1;
     return 2;
@@ -773,7 +831,7 @@ void ora_walk(const ora_graph *G, uint32_t app, uint32_t L, uint64_t seed, uint3
             counts[u]++;
         }
         for (uint32_t t = 0; L == 0xFFFFFFFFu || t < L; t++) {
-            const o_vertex *x = &G->v[u];
+            const o_vertex *x = vx(G, u);
             if (x->d == 0) break;                       /* dead end: truncate */
             uint32_t att, next;
             if (app == 1 && t >= 1) {
@@ -823,7 +881,7 @@ void ora_walk(const ora_graph *G, uint32_t app, uint32_t L, uint64_t seed, uint3
 /*        REG/SPARSE: c x u32 member; ONE: u32 member}; u64 T.         */
 /* little-endian.  Returns the byte count; writes only if cap allows.  */
 /* ------------------------------------------------------------------ */
-typedef struct { uint8_t *buf; size_t cap, pos; } o_out;
+struct o_out_s { uint8_t *buf; size_t cap, pos; };
 
 static void put32(o_out *o, uint32_t v)
 {
@@ -835,8 +893,6 @@ static void put64(o_out *o, uint64_t v)
     if (o->buf && o->pos + 8 <= o->cap) memcpy(o->buf + o->pos, &v, 8);
     o->pos += 8;
 }
-
-static int g_dump_float = 0;
 
 static void dump_vertex(const o_vertex *x, o_out *o)
 {
@@ -877,7 +933,7 @@ size_t ora_dump(const ora_graph *G, uint8_t *buf, size_t cap)
 {
     g_dump_float = G->float_mode;
     o_out o = {buf, cap, 0};
-    for (uint32_t u = 0; u < G->V; u++) dump_vertex(&G->v[u], &o);
+    for (uint32_t u = 0; u < G->V; u++) dump_vertex(vx(G, u), &o);
     return o.pos;
 }
 
@@ -890,13 +946,22 @@ void ora_digests(const ora_graph *G, uint64_t *dig)
 #endif
     for (int64_t u = 0; u < (int64_t)G->V; u++) {
         o_out o = {NULL, 0, 0};
-        dump_vertex(&G->v[u], &o);
+        dump_vertex(vx(G, (uint32_t)u), &o);
         uint8_t *tmp = (uint8_t *)malloc(o.pos);
         o_out o2 = {tmp, o.pos, 0};
-        dump_vertex(&G->v[u], &o2);
+        dump_vertex(vx(G, (uint32_t)u), &o2);
         uint64_t h = 0xcbf29ce484222325ull;
         for (size_t i = 0; i < o.pos; i++) { h ^= tmp[i]; h *= 0x100000001b3ull; }
         dig[u] = h;
         free(tmp);
     }
+}
+
+/* Per-vertex canonical dump bytes of one vertex (for sampled parity at scale). */
+size_t ora_dump_vertex(const ora_graph *G, uint32_t u, uint8_t *buf, size_t cap)
+{
+    o_out o = {buf, cap, 0};
+    g_dump_float = G->float_mode;
+    dump_vertex(vx(G, u), &o);
+    return o.pos;
 }

@@ -34,27 +34,31 @@ CONFIGS = {
                scale=24, edges=35_000_000, compact=True, bias="degree", clamp=None, batch=50_000,
                app="deepwalk"),
     "c3": dict(desc="Orkut-shaped R-MAT (3.1M V, 234M arcs), node2vec p=2 q=0.5, 1M-edge batches",
-               scale=22, edges=120_000_000, compact=True, bias="degree", clamp=None, batch=1_000_000,
+               scale=22, edges=125_000_000, compact=True, bias="degree", clamp=None, batch=1_000_000,
                app="node2vec"),
-    "c4": dict(desc="Twitter-shaped R-MAT (41.7M V, 1.47B arcs), PPR", scale=26, edges=760_000_000,
+    "c4": dict(desc="Twitter-shaped R-MAT (41.7M V, 1.47B arcs), PPR", scale=27, edges=740_000_000,
                compact=True, bias="degree", clamp=None, batch=50_000, app="ppr"),
+    "c5": dict(desc="Friendster-shaped R-MAT (65.6M V, 3.6B arcs), streaming updates + DeepWalk batches",
+               scale=27, edges=1_830_000_000, compact=True, bias="degree", clamp=None, batch=1,
+               app="deepwalk"),
 }
 
 
-def rmat_edges(scale: int, n_edges: int, seed: int, abcd=RMAT_ABCD, chunk: int = 1 << 24):
-    """Raw directed R-MAT endpoint pairs (int64 ids < 2^scale), torch CPU RNG."""
+def rmat_edges(scale: int, n_edges: int, seed: int, abcd=RMAT_ABCD, chunk: int = 1 << 24, device="cpu"):
+    """Raw directed R-MAT endpoint pairs (int64 ids < 2^scale), torch RNG on `device`
+    (the CPU and CUDA streams differ; each is deterministic for a given seed)."""
     import torch
-    g = torch.Generator().manual_seed(seed)
+    g = torch.Generator(device=device).manual_seed(seed)
     a, b, c, _ = abcd
-    src = torch.empty(n_edges, dtype=torch.int64)
-    dst = torch.empty(n_edges, dtype=torch.int64)
+    src = torch.empty(n_edges, dtype=torch.int64, device=device)
+    dst = torch.empty(n_edges, dtype=torch.int64, device=device)
     for lo in range(0, n_edges, chunk):
         hi = min(n_edges, lo + chunk)
         m = hi - lo
-        s = torch.zeros(m, dtype=torch.int64)
-        t = torch.zeros(m, dtype=torch.int64)
+        s = torch.zeros(m, dtype=torch.int64, device=device)
+        t = torch.zeros(m, dtype=torch.int64, device=device)
         for lvl in range(scale):
-            r = torch.rand(m, generator=g)
+            r = torch.rand(m, generator=g, device=device)
             bit = 1 << (scale - 1 - lvl)
             # quadrant: [0,a) -> (0,0); [a,a+b) -> (0,1); [a+b,a+b+c) -> (1,0); else (1,1)
             down = r >= (a + b)
@@ -66,18 +70,19 @@ def rmat_edges(scale: int, n_edges: int, seed: int, abcd=RMAT_ABCD, chunk: int =
     return src, dst
 
 
-def simple_undirected(scale: int, n_edges: int, seed: int, compact: bool):
+def simple_undirected(scale: int, n_edges: int, seed: int, compact: bool, device="cpu"):
     """Undirected simple edge list (lo < hi pairs, unique) with a random relabelling."""
     import torch
-    s, t = rmat_edges(scale, n_edges, seed)
+    s, t = rmat_edges(scale, n_edges, seed, device=device)
     keep = s != t
     s, t = s[keep], t[keep]
     key = torch.unique((torch.minimum(s, t) << 32) | torch.maximum(s, t))
+    del s, t
     lo = key >> 32
     hi = key & 0xFFFFFFFF
     n_ids = 1 << scale
     if compact:
-        used = torch.zeros(n_ids, dtype=torch.bool)
+        used = torch.zeros(n_ids, dtype=torch.bool, device=device)
         used[lo] = True
         used[hi] = True
         newid = torch.cumsum(used.to(torch.int64), 0) - 1
@@ -85,24 +90,47 @@ def simple_undirected(scale: int, n_edges: int, seed: int, compact: bool):
         lo, hi = newid[lo], newid[hi]
     else:
         V = n_ids
-    g = torch.Generator().manual_seed(seed + 1000003)
-    perm = torch.randperm(V, generator=g)
+    g = torch.Generator(device=device).manual_seed(seed + 1000003)
+    perm = torch.randperm(V, generator=g, device=device)
     lo, hi = perm[lo], perm[hi]
-    a = torch.minimum(lo, hi)
-    b = torch.maximum(lo, hi)
-    return V, a.numpy().astype(np.uint32), b.numpy().astype(np.uint32)
+    a = torch.minimum(lo, hi).to(torch.int32)
+    b = torch.maximum(lo, hi).to(torch.int32)
+    del lo, hi, perm
+    return V, a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32)
 
 
-def csr_from_arcs(V: int, src: np.ndarray, dst: np.ndarray, extra=None):
-    """CSR with arcs ordered by (src, dst); returns row_offsets u64, dst u32 (+ extra permuted)."""
+def csr_from_arcs(V: int, src: np.ndarray, dst: np.ndarray, extra=None, device="cpu", lim: int = 1 << 30):
+    """CSR with arcs ordered by (src, dst); returns row_offsets u64, dst u32 (+ extra permuted).
+    Large inputs are sorted in source-vertex ranges of < 2^30 arcs (torch.sort's limit)."""
     import torch
-    key = (torch.from_numpy(src.astype(np.int64)) << 32) | torch.from_numpy(dst.astype(np.int64))
-    order = torch.sort(key, stable=True).indices.numpy()
-    s = src[order]
-    d = dst[order].astype(np.uint32)
-    counts = np.bincount(s, minlength=V).astype(np.uint64)
+    counts = np.bincount(src, minlength=V).astype(np.uint64)
     ro = np.zeros(V + 1, dtype=np.uint64)
     np.cumsum(counts, out=ro[1:])
+    n = len(src)
+    LIM = lim
+    if n <= LIM:
+        key = (torch.from_numpy(src.astype(np.int64)).to(device) << 32) | torch.from_numpy(dst.astype(np.int64)).to(device)
+        order = torch.sort(key, stable=True).indices.cpu().numpy()
+        del key
+    else:
+        s_t = torch.from_numpy(src.view(np.int32)).to(device)
+        d_t = torch.from_numpy(dst.view(np.int32)).to(device)
+        order = np.empty(n, dtype=np.int64)
+        v0 = 0
+        while v0 < V:
+            # the largest v1 with ro[v1] - ro[v0] <= LIM (at least one vertex)
+            v1 = int(np.searchsorted(ro, ro[v0] + LIM, side="right")) - 1
+            v1 = max(v1, v0 + 1)
+            m = (s_t >= v0) & (s_t < v1)
+            idx = m.nonzero().squeeze(1)
+            del m
+            key = (s_t[idx].to(torch.int64) << 32) | d_t[idx].to(torch.int64)
+            o = torch.sort(key, stable=True).indices
+            order[int(ro[v0]):int(ro[v1])] = idx[o].cpu().numpy()
+            del idx, key, o
+            v0 = v1
+        del s_t, d_t
+    d = dst[order].astype(np.uint32)
     if extra is not None:
         return ro, d, extra[order]
     return ro, d
@@ -116,19 +144,19 @@ def degree_bias_of(deg: np.ndarray, dst: np.ndarray, clamp=None) -> np.ndarray:
     return w.astype(np.uint32)
 
 
-def make_workload(name: str, rounds: int = 1, **over) -> "Workload":
+def make_workload(name: str, rounds: int = 1, device="cpu", **over) -> "Workload":
     cfg = dict(CONFIGS[name])
     cfg.update(over)
     return Workload(cfg["scale"], cfg["edges"], compact=cfg["compact"], bias=cfg["bias"],
-                    clamp=cfg["clamp"], batch=cfg["batch"], rounds=rounds)
+                    clamp=cfg["clamp"], batch=cfg["batch"], rounds=rounds, device=device)
 
 
 class Workload:
     """A seeded graph + update stream following the recipe above."""
 
     def __init__(self, scale, edges, seed=1, compact=True, bias="degree", clamp=None, batch=1000,
-                 rounds=1, update_seed=2, undirected=True):
-        V, a, b = simple_undirected(scale, edges, seed, compact)
+                 rounds=1, update_seed=2, undirected=True, device="cpu"):
+        V, a, b = simple_undirected(scale, edges, seed, compact, device=device)
         self.V = V
         E = len(a)
         # full-graph degrees fix every bias, including those of later inserts
@@ -148,7 +176,8 @@ class Workload:
         src = np.concatenate([a[live], b[live]])
         dst = np.concatenate([b[live], a[live]])
         w = self._bias(src, dst)
-        self.row_offsets, self.dst, self.bias = csr_from_arcs(V, src, dst, extra=w)
+        self.row_offsets, self.dst, self.bias = csr_from_arcs(V, src, dst, extra=w, device=device)
+        del src, dst, w
         self.num_arcs = int(self.row_offsets[-1])
         # update stream: coin flip, delete uniform live edge of A,
         # insert uniform unused edge of B into A

@@ -1,0 +1,134 @@
+"""Full-size parity + throughput on a BASELINE config (c2 .. c5).
+
+The CUDA path runs exactly as bench.py runs it (full graph, all walkers of the
+config in one launch, update batches through the C-ABI); the CPU oracle (lazy:
+builds only the vertices the comparison touches) replays the same batches and
+recomputes sampled outputs one by one:
+  * per-vertex canonical digests of every touched vertex of the last batch plus a
+    random sample of vertices,
+  * walks of contiguous walker-id ranges sliced out of the full launch.
+Prints one JSON line.  Test infrastructure (imports the oracle)."""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import synth  # noqa: E402
+import paper_2504_10233_b200 as pb  # noqa: E402
+
+APP = {"deepwalk": pb.DEEPWALK, "node2vec": pb.NODE2VEC, "ppr": pb.PPR}
+OAPP = {"deepwalk": oracle.APP_DEEPWALK, "node2vec": oracle.APP_NODE2VEC, "ppr": oracle.APP_PPR}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--rounds", type=int, default=2)
+    ap.add_argument("--ranges", type=int, default=6, help="walker-id ranges compared")
+    ap.add_argument("--range-len", type=int, default=512)
+    ap.add_argument("--vertices", type=int, default=3000, help="random vertices whose digests are compared")
+    ap.add_argument("--walkers", type=int, default=0, help="walkers in the launch (default: one per vertex)")
+    ap.add_argument("--ppr-cap", type=int, default=400)
+    ap.add_argument("--slack", type=float, default=0.25)
+    ap.add_argument("--out", default="")
+    a = ap.parse_args()
+    cfg = synth.CONFIGS[a.config]
+    app = cfg["app"]
+    t0 = time.time()
+    w = synth.make_workload(a.config, rounds=a.rounds, device="cuda")
+    torch.cuda.empty_cache()
+    t_gen = time.time() - t0
+    rec = {"config": a.config, "V": int(w.V), "arcs": int(w.num_arcs), "app": app, "gen_s": round(t_gen, 1)}
+    t0 = time.time()
+    g = pb.Graph(w.row_offsets, w.dst, w.bias, neighbor_index=(app == "node2vec"), arc_slack=a.slack,
+                 member_slack=a.slack)
+    torch.cuda.synchronize()
+    rec["gpu_build_s"] = round(time.time() - t0, 2)
+    o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias, lazy=True)
+    # ---- updates, timed on the device, replayed by the oracle
+    upd_ms = []
+    touched = set()
+    for b in w.batches:
+        db = torch.from_numpy(b.view(np.int32)).cuda()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sg = g.apply_updates(db)
+        e1.record()
+        torch.cuda.synchronize()
+        upd_ms.append(e0.elapsed_time(e1))
+        so = o.apply_updates(b)
+        for k in ("inserted", "deleted", "missing_deletes", "touched_vertices"):
+            assert sg[k] == so[k], (k, sg[k], so[k])
+        assert np.array_equal(sg["kind_transitions"], so["kind_transitions"])
+        touched.update(np.unique(b[:, 1]).tolist())
+    rec["update_ms"] = [round(x, 3) for x in upd_ms]
+    rec["update_arcs_per_s"] = float(len(w.batches[0]) / (np.mean(upd_ms) / 1e3))
+    # ---- digests: touched vertices + a random sample
+    rng = np.random.default_rng(11)
+    tv = np.array(sorted(touched), dtype=np.int64)
+    sample = np.unique(np.concatenate([rng.choice(tv, size=min(len(tv), a.vertices), replace=False),
+                                       rng.integers(0, w.V, size=a.vertices)]))
+    dg = g.digests().cpu().numpy().view(np.uint64)
+    bad = [int(u) for u in sample if int(dg[u]) != o.vertex_digest(int(u))]
+    assert not bad, f"digest mismatch at vertices {bad[:10]}"
+    rec["digests_compared"] = int(len(sample))
+    # ---- the full launch, as bench.py runs it
+    W = a.walkers or w.V
+    L = 80 if app != "ppr" else pb.NO_CAP       # PPR: geometric lengths, visit counts, no paths
+    kw = dict(app=APP[app], length=L, seed=4242, num_walkers=W)
+    if app == "node2vec":
+        kw.update(p=2.0, q=0.5)
+    if app == "ppr":
+        kw.update(stop=(1, 80), paths=None)
+        g.reset_visit_counts()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    out = g.walk(**kw)
+    e1.record()
+    torch.cuda.synchronize()
+    walk_ms = e0.elapsed_time(e1)
+    lens = out["lengths"].cpu().numpy().view(np.uint32)
+    steps = int(lens.astype(np.int64).sum())
+    rec["walk_ms"] = round(walk_ms, 2)
+    rec["walk_steps_per_s"] = steps / (walk_ms / 1e3)
+    rec["steps"] = steps
+    P = out["paths"]
+    if app == "ppr":
+        counts = g.visit_counts().cpu().numpy().view(np.uint64)
+        assert int(counts.astype(np.uint64).sum()) == steps + W, "PPR: sum of visit counts = sum(lengths + 1)"
+        rec["ppr_mean_length"] = steps / W
+    # ---- sampled walker ranges vs the oracle
+    starts = rng.integers(0, max(1, W - a.range_len), size=a.ranges)
+    okw = dict(app=OAPP[app], length=L, seed=4242, stop=(1, 80), threads=os.cpu_count())
+    if app == "node2vec":
+        okw.update(p=2.0, q=0.5)
+    t0 = time.time()
+    for s0 in starts.tolist():
+        ref = o.walk(first_walker=s0, num_walkers=a.range_len, paths=(app != "ppr"), **okw)
+        if P is not None:
+            gp = P[:, s0:s0 + a.range_len].cpu().numpy().view(np.uint32)
+            assert np.array_equal(gp, ref["paths"]), f"walk mismatch in walker range [{s0}, {s0 + a.range_len})"
+        assert np.array_equal(lens[s0:s0 + a.range_len], ref["lengths"])
+    rec["walkers_compared"] = int(a.ranges * a.range_len)
+    rec["oracle_walk_s"] = round(time.time() - t0, 2)
+    rec["parity"] = "bit-exact"
+    print(json.dumps(rec), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(rec, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
