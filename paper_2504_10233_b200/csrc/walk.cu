@@ -30,8 +30,13 @@ __global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BIN
     // L2 eviction priorities: the thin headers are re-read by every step of every
     // walker (keep), member/arc sectors are one-shot random reads (stream).
     uint64_t pol_keep, pol_stream;
+#ifdef BINGO_NO_L2_POLICY         // A/B experiment switch: plain evict_normal everywhere
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_keep));
+    pol_stream = pol_keep;
+#else
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+#endif
     const Policies pol{pol_keep, pol_stream};
     const size_t row = (size_t)a.L + 1;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += stride) {
