@@ -293,12 +293,13 @@ class Graph:
     def walk_host(self, app: int = DEEPWALK, length: int = 80, seed: int = 0, first_walker: int = 0,
                   starts: Optional[np.ndarray] = None, num_walkers: Optional[int] = None, p: float = 1.0,
                   q: float = 1.0, stop=(1, 80), paths: Optional[np.ndarray] = None,
-                  lengths: Optional[np.ndarray] = None, stream=None):
+                  lengths: Optional[np.ndarray] = None, walker_major: bool = False, stream=None):
         """Same walk with HOST (ideally pinned) buffers: the library stages H2D/D2H itself."""
         torch = _torch()
         W = num_walkers if num_walkers is not None else (len(starts) if starts is not None else self.V)
         d = WalkDesc(app=app, length=length, p=p, q=q, stop_num=stop[0], stop_den=stop[1], seed=seed,
-                     first_walker_id=first_walker, flags=WALK_HOST_OUTPUT)
+                     first_walker_id=first_walker,
+                     flags=WALK_HOST_OUTPUT | (WALK_WALKER_MAJOR if walker_major else 0))
 
         def ptr(a):
             if a is None:

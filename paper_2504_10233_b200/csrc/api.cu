@@ -38,6 +38,11 @@ extern "C" void bingo_destroy(bingo_graph *g) {
     if (g->hscratch) cudaFreeHost(g->hscratch);
     if (g->fast_out_host) cudaFreeHost(g->fast_out_host);
     if (g->aux_stream) cudaStreamDestroy(g->aux_stream);
+    if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
+    for (int i = 0; i < 2; i++) {
+        if (g->ev_walk[i]) cudaEventDestroy(g->ev_walk[i]);
+        if (g->ev_copy[i]) cudaEventDestroy(g->ev_copy[i]);
+    }
     if (g->ev_fork) cudaEventDestroy(g->ev_fork);
     if (g->ev_join) cudaEventDestroy(g->ev_join);
     delete g;

@@ -181,6 +181,8 @@ struct bingo_graph {
     size_t vscratch_bytes = 0;
     uint32_t *fast_scr = nullptr;            // small-batch fast path scratch (device)
     cudaStream_t aux_stream = nullptr;       // side stream for hub mutations
+    cudaStream_t copy_stream = nullptr;      // D2H of walk chunks (HOST_OUTPUT)
+    cudaEvent_t ev_walk[2] = {nullptr, nullptr}, ev_copy[2] = {nullptr, nullptr};
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     void *fast_out_host = nullptr;           // mapped pinned status/stats of the fast path
     void *fast_out_dev = nullptr;

@@ -232,32 +232,67 @@ extern "C" bingo_status bingo_walk(bingo_graph *g, const bingo_walk_desc *desc, 
     cudaStream_t s = (cudaStream_t)stream;
     if (!(desc->flags & BINGO_WALK_HOST_OUTPUT))
         return launch_walk(g, desc, starts_or_null, num_walkers, paths_or_null, lengths_or_null, s);
-    // HOST buffers: stage through device scratch
-    const size_t n_path = paths_or_null ? (size_t)(desc->length + 1) * num_walkers : 0;
-    const size_t need = sizeof(uint32_t) * (n_path + (lengths_or_null ? num_walkers : 0) +
-                                            (starts_or_null ? num_walkers : 0)) + 256;
+    // HOST buffers: the walkers run in chunks whose paths are staged in two device
+    // buffers; each chunk's D2H copy (a strided 2-D copy for step-major paths) runs on
+    // a side stream while the next chunk walks, so the PCIe transfer of the paths
+    // overlaps the walk instead of following it.
+    const uint64_t W = num_walkers;
+    const uint64_t row = (uint64_t)desc->length + 1;
+    const bool wmajor = (desc->flags & BINGO_WALK_WALKER_MAJOR) != 0;
+    uint64_t Wc = W;
+    if (paths_or_null) {
+        Wc = std::max<uint64_t>(1 << 18, (W + 7) / 8);
+        Wc = std::min<uint64_t>(Wc, W);
+    }
+    const uint64_t nchunks = (W + Wc - 1) / Wc;
+    const size_t slot_words = paths_or_null ? (size_t)(row * Wc) : 0;
+    const size_t need = sizeof(uint32_t) * (2 * slot_words + (lengths_or_null ? W : 0) + (starts_or_null ? W : 0)) + 256;
     if (g->wscratch_bytes < need) {
         bingo_dev_free(g, g->wscratch);
         g->wscratch = bingo_dev_alloc(g, need);
         g->wscratch_bytes = g->wscratch ? need : 0;
         if (!g->wscratch) return BINGO_E_NOMEM;
     }
-    uint32_t *dp = (uint32_t *)g->wscratch;
-    uint32_t *dl = dp + n_path;
-    uint32_t *ds = dl + (lengths_or_null ? num_walkers : 0);
+    uint32_t *slots[2] = {(uint32_t *)g->wscratch, (uint32_t *)g->wscratch + slot_words};
+    uint32_t *dl = (uint32_t *)g->wscratch + 2 * slot_words;
+    uint32_t *ds = dl + (lengths_or_null ? W : 0);
     cudaError_t e = cudaSuccess;
-    if (starts_or_null)
-        e = cudaMemcpyAsync(ds, starts_or_null, sizeof(uint32_t) * num_walkers, cudaMemcpyHostToDevice, s);
-    if (e == cudaSuccess) {
-        bingo_status st = launch_walk(g, desc, starts_or_null ? ds : nullptr, num_walkers,
-                                      paths_or_null ? dp : nullptr, lengths_or_null ? dl : nullptr, s);
-        if (st != BINGO_OK) return st;
+    if (!g->copy_stream) {
+        e = cudaStreamCreateWithFlags(&g->copy_stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 2 && e == cudaSuccess; i++) {
+            e = cudaEventCreateWithFlags(&g->ev_walk[i], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&g->ev_copy[i], cudaEventDisableTiming);
+        }
     }
-    if (e == cudaSuccess && paths_or_null)
-        e = cudaMemcpyAsync(paths_or_null, dp, sizeof(uint32_t) * n_path, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && starts_or_null)
+        e = cudaMemcpyAsync(ds, starts_or_null, sizeof(uint32_t) * W, cudaMemcpyHostToDevice, s);
+    for (uint64_t c = 0; c < nchunks && e == cudaSuccess; c++) {
+        const uint64_t c0 = c * Wc, wn = std::min<uint64_t>(Wc, W - c0);
+        const int sl = (int)(c & 1);
+        if (c >= 2 && paths_or_null) e = cudaStreamWaitEvent(s, g->ev_copy[sl], 0);
+        if (e != cudaSuccess) break;
+        bingo_walk_desc dc = *desc;
+        dc.first_walker_id = desc->first_walker_id + (uint32_t)c0;
+        bingo_status st = launch_walk(g, &dc, starts_or_null ? ds + c0 : nullptr, (uint32_t)wn,
+                                      paths_or_null ? slots[sl] : nullptr, lengths_or_null ? dl + c0 : nullptr, s);
+        if (st != BINGO_OK) return st;
+        if (!paths_or_null) continue;
+        e = cudaEventRecord(g->ev_walk[sl], s);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(g->copy_stream, g->ev_walk[sl], 0);
+        if (e == cudaSuccess) {
+            if (wmajor)
+                e = cudaMemcpyAsync(paths_or_null + c0 * row, slots[sl], sizeof(uint32_t) * wn * row,
+                                    cudaMemcpyDeviceToHost, g->copy_stream);
+            else
+                e = cudaMemcpy2DAsync(paths_or_null + c0, sizeof(uint32_t) * W, slots[sl], sizeof(uint32_t) * wn,
+                                      sizeof(uint32_t) * wn, row, cudaMemcpyDeviceToHost, g->copy_stream);
+        }
+        if (e == cudaSuccess) e = cudaEventRecord(g->ev_copy[sl], g->copy_stream);
+    }
     if (e == cudaSuccess && lengths_or_null)
-        e = cudaMemcpyAsync(lengths_or_null, dl, sizeof(uint32_t) * num_walkers, cudaMemcpyDeviceToHost, s);
+        e = cudaMemcpyAsync(lengths_or_null, dl, sizeof(uint32_t) * W, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess && g->copy_stream) e = cudaStreamSynchronize(g->copy_stream);
     if (e != cudaSuccess) {
         fprintf(stderr, "libbingo: walk staging failed: %s\n", cudaGetErrorString(e));
         g->poisoned = 1;

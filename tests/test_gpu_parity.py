@@ -110,6 +110,17 @@ def test_deepwalk_parity_starts_shards_and_host_path():
     g.walk_host(length=33, seed=77, first_walker=1000, starts=starts, paths=hp, lengths=hl)
     assert np.array_equal(hp.numpy().view(np.uint32), ref["paths"])
     assert np.array_equal(hl.numpy().view(np.uint32), ref["lengths"])
+    # chunked host-output pipeline (several chunks: > 2^18 walkers), step- and walker-major
+    big = rng.integers(0, w.V, size=700_001).astype(np.uint32)
+    refb = o.walk(length=12, seed=5, first_walker=3, starts=big)
+    hp2 = torch.empty((13, len(big)), dtype=torch.int32).pin_memory()
+    hl2 = torch.empty(len(big), dtype=torch.int32).pin_memory()
+    g.walk_host(length=12, seed=5, first_walker=3, starts=big, paths=hp2, lengths=hl2)
+    assert np.array_equal(hp2.numpy().view(np.uint32), refb["paths"])
+    assert np.array_equal(hl2.numpy().view(np.uint32), refb["lengths"])
+    hp3 = torch.empty((len(big), 13), dtype=torch.int32).pin_memory()
+    g.walk_host(length=12, seed=5, first_walker=3, starts=big, paths=hp3, lengths=hl2, walker_major=True)
+    assert np.array_equal(hp3.numpy().view(np.uint32).T, refb["paths"])
     # sharding by first_walker_id reproduces the unsharded run (P-invariance)
     a = g.walk(length=33, seed=77, first_walker=1000, starts=starts[:1234])
     b = g.walk(length=33, seed=77, first_walker=1000 + 1234, starts=starts[1234:])
