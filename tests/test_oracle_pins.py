@@ -498,3 +498,17 @@ def test_ppr_lengths_and_counts():
     assert abs(out["lengths"].mean() - 80.0) < 0.5
     assert int(out["counts"].sum()) == int(out["lengths"].astype(np.int64).sum()) + n
     assert oracle.stop_threshold(1, 80)[0] == 230584300921369395       # floor(2^64 / 80)
+
+
+def test_lazy_oracle_equals_eager():
+    """The lazy oracle (used for BASELINE-scale parity) is the eager oracle, vertex for vertex."""
+    w = synth.make_workload("c1", rounds=3)
+    a = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
+    b = oracle.OracleGraph(w.row_offsets, w.dst, w.bias, lazy=True)
+    for bt in w.batches:
+        assert a.apply_updates(bt)["deleted"] == b.apply_updates(bt)["deleted"]
+    assert np.array_equal(a.walk(length=30, seed=3)["paths"], b.walk(length=30, seed=3)["paths"])
+    assert a.dump() == b.dump()
+    d = a.digests()
+    for u in range(0, w.V, 37):
+        assert b.vertex_digest(u) == int(d[u])
