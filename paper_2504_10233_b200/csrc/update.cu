@@ -349,7 +349,8 @@ struct Grp<LT> {
 // one warp (GT = 32, small vertices, 8 per block) or a whole block (GT = MT,
 // large vertices).  Lanes 0..31 of the group own radix bit k = lane.
 template <int GT>
-__device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_t t, MutSmem &sm) {
+__device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_t t, MutSmem &sm,
+                                              uint32_t *local_scr = nullptr, uint32_t local_words = 0) {
     using G = Grp<GT>;
     const uint32_t tid = G::rank(), lane = tid & 31u, wid = tid >> 5;
     uint32_t *s_kind0 = sm.kind0, *s_c = sm.c, *s_insk = sm.insk, *s_delk = sm.delk, *s_moff = sm.moff,
@@ -487,7 +488,9 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
     uint32_t Lp = L;
     uint32_t *bm = nullptr, *holes = nullptr, *R = nullptr, *gh = nullptr;
     if (q) {
-        uint32_t *scr = a.scr + a.scr_off[t];
+        // delete scratch: the caller's shared-memory slice when it fits, else global
+        const uint64_t so = a.scr_off[t], words = a.scr_off[t + 1] - so;
+        uint32_t *scr = (local_scr && words <= local_words) ? local_scr : a.scr + so;
         const uint32_t Hq = next_pow2(2 * q), hmask = Hq - 1;
         const uint32_t bw = (L + 31) / 32;
         bm = scr;
@@ -809,13 +812,17 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
 }
 
 // small touched vertices: one warp each, 8 per block (grid-stride over all touched
-// vertices, skipping those routed to the block kernel)
+// vertices, skipping those routed to the block kernel); each warp keeps its delete
+// scratch (bitmap, hash of deleted destinations, holes, rename table) in a 4 KB
+// shared-memory slice when it fits
+static constexpr uint32_t WARP_SCR_WORDS = 1024;
 __global__ void __launch_bounds__(MT) k_upd_mutate_warp(const MutateArgs a, const uint8_t *__restrict__ route,
                                                         uint32_t count) {
     __shared__ MutSmem sm[MT / 32];
+    __shared__ __align__(16) uint32_t wscr[MT / 32][WARP_SCR_WORDS];
     const uint32_t w = threadIdx.x >> 5;
     for (uint32_t i = blockIdx.x * (MT / 32) + w; i < count; i += gridDim.x * (MT / 32))
-        if (!route[i]) mutate_vertex<32>(a, i, sm[w]);
+        if (!route[i]) mutate_vertex<32>(a, i, sm[w], wscr[w], WARP_SCR_WORDS);
 }
 
 // large touched vertices (hubs): one 1024-thread block each
