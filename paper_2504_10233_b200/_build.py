@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libbingo.so")
-TOOLS_SRC = os.path.join(ROOT, "tools", "gather_bench.cu")
+TOOLS_SRC = [os.path.join(ROOT, "tools", "gather_bench.cu"), os.path.join(ROOT, "tools", "unit_kernels.cu")]
 TOOLS_LIB = os.path.join(HERE, "libbingo_tools.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -47,10 +47,11 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
         cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
         subprocess.check_call(cmd)
         os.replace(tmp, LIB)
-    if force or not os.path.exists(TOOLS_LIB) or os.path.getmtime(TOOLS_LIB) < os.path.getmtime(TOOLS_SRC):
+    tmax = max(max(os.path.getmtime(t) for t in TOOLS_SRC), hmax)
+    if force or not os.path.exists(TOOLS_LIB) or os.path.getmtime(TOOLS_LIB) < tmax:
         tmp = TOOLS_LIB + f".{os.getpid()}.tmp"
-        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-shared", "-o", tmp,
-                               TOOLS_SRC, "-lcudart"])
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+                               "-I", INCLUDE, "-I", CSRC, "-o", tmp, *TOOLS_SRC, "-lcudart"])
         os.replace(tmp, TOOLS_LIB)
     return LIB
 

@@ -33,7 +33,7 @@ void bingo_dev_free(bingo_graph *g, void *p) {
 extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
     void *bufs[] = {g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->dec, g->dmem, g->counters, g->visit, g->dev_flag,
-                    g->scratch, g->wscratch, g->vscratch, g->fast_scr};
+                    g->scratch, g->wscratch, g->vscratch, g->bscratch, g->iscratch, g->fast_scr};
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
     if (g->fast_out_host) cudaFreeHost(g->fast_out_host);
@@ -84,7 +84,8 @@ extern "C" bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *s
     info->hot_degree = ((uint64_t)g->hot_mem_degree << 32) | g->hot_bkt_degree;
     info->device_bytes = (sizeof(VHdr) + sizeof(ThinHdr)) * (uint64_t)g->V + (sizeof(uint2) + 4) * g->arc_cap +
                          (sizeof(Bucket) + sizeof(GCan)) * g->bkt_cap + 8ull * g->mem_cap + 8ull * g->V +
-                         g->scratch_bytes + g->wscratch_bytes + g->vscratch_bytes;
+                         g->scratch_bytes + g->wscratch_bytes + g->vscratch_bytes + g->bscratch_bytes +
+                         g->iscratch_bytes;
     return BINGO_OK;
 }
 

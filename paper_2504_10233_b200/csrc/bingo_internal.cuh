@@ -179,6 +179,10 @@ struct bingo_graph {
     size_t wscratch_bytes = 0;
     void *vscratch = nullptr;                // per-touched-vertex delete scratch
     size_t vscratch_bytes = 0;
+    void *bscratch = nullptr;                // bulk-synchronous update: per-vertex state + chunk items
+    size_t bscratch_bytes = 0;
+    void *iscratch = nullptr;                // bulk-synchronous update: per-chunk-item counts
+    size_t iscratch_bytes = 0;
     uint32_t *fast_scr = nullptr;            // small-batch fast path scratch (device)
     cudaStream_t aux_stream = nullptr;       // side stream for hub mutations
     cudaStream_t copy_stream = nullptr;      // D2H of walk chunks (HOST_OUTPUT)

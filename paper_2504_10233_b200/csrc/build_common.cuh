@@ -98,12 +98,43 @@ __device__ __forceinline__ GCan load_gcan(const GCan *p) {
 // walker's test R < lim takes exactly the decision of the canonical coin
 // mulhi64(R, T) < thr.  Saturation only hits thr = T, i.e. an unassigned bucket
 // whose alias is itself, where both branches pick the same group.
+//
+// The quotient floor(thr 2^64 / T) is computed without a 128-bit division: a
+// double-precision estimate (off by at most ~2^13), one exact 128-bit remainder,
+// a second double estimate of the correction (off by at most 1), and exact
+// integer fix-ups until 0 <= remainder < T.  thr < T, so the quotient is below
+// 2^64 - 1 and the ceiling cannot overflow.
+__device__ __forceinline__ void rem128(uint64_t thr, uint64_t q, uint64_t T, int64_t &rh, uint64_t &rl) {
+    // r = thr * 2^64 - q * T as a signed 128-bit (rh, rl); |r| < 2^126
+    const uint64_t pl = q * T, ph = __umul64hi(q, T);
+    rl = 0ull - pl;
+    rh = (int64_t)(thr - ph - (pl != 0ull ? 1ull : 0ull));
+}
 __device__ __forceinline__ uint64_t alias_lim(uint64_t thr, uint64_t T) {
     if (thr >= T) return ~0ull;
-    const unsigned __int128 num = (unsigned __int128)thr << 64;
-    const unsigned __int128 q = num / T;
-    const bool exact = (q * T) == num;
-    return (uint64_t)q + (exact ? 0ull : 1ull);
+    if (thr == 0) return 0ull;
+    const double Td = (double)T;
+    double qd = (double)thr / Td * 18446744073709551616.0;
+    uint64_t q = qd >= 18446744073709549568.0 ? 18446744073709549568ull : (uint64_t)qd;
+    int64_t rh;
+    uint64_t rl;
+    rem128(thr, q, T, rh, rl);
+    const double cd = floor(((double)rh * 18446744073709551616.0 + (double)rl) / Td);
+    q += (uint64_t)(int64_t)cd;
+    rem128(thr, q, T, rh, rl);
+    while (rh < 0) {                          // r < 0: q too large
+        q--;
+        const uint64_t o = rl;
+        rl += T;
+        rh += (rl < o) ? 1 : 0;
+    }
+    while (rh > 0 || rl >= T) {               // r >= T: q too small
+        q++;
+        const uint64_t o = rl;
+        rl -= T;
+        rh -= (rl > o) ? 1 : 0;
+    }
+    return q + ((rh != 0 || rl != 0) ? 1ull : 0ull);
 }
 
 // Walker view of group (k, kind): (x, y) as documented on Bucket.

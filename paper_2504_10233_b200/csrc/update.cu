@@ -148,11 +148,16 @@ struct PlanOut {
     uint32_t L, q;
     unsigned long long arc, bkt, mem, res, words;
 };
+// per-lane (lane = radix bit k) pre-batch view of group k, for the bulk-synchronous path
+struct PlanLane {
+    uint32_t kind, c, ref, aux, insk, list0;
+};
 
 __device__ __forceinline__ PlanOut plan_vertex(const uint4 *__restrict__ recs, const uint32_t *__restrict__ sval,
                                                uint32_t beg, uint32_t end, const VHdr &h,
                                                const Bucket *__restrict__ bkt, const GCan *__restrict__ gcan,
-                                               uint32_t alpha, bool bs, double arc_slack, double mem_slack) {
+                                               uint32_t alpha, bool bs, double arc_slack, double mem_slack,
+                                               PlanLane *pl = nullptr) {
     const uint32_t lane = lane_id();
     uint32_t kind_k, c_k, ref_k, aux_k;
     OldGroups og;
@@ -212,6 +217,14 @@ __device__ __forceinline__ PlanOut plan_vertex(const uint4 *__restrict__ recs, c
     o.words = words;
     o.L = L;
     o.q = q;
+    if (pl) {
+        pl->kind = kind_k;
+        pl->c = c_k;
+        pl->ref = ref_k;
+        pl->aux = aux_k;
+        pl->insk = insk;
+        pl->list0 = og.list_mask;
+    }
     return o;
 }
 
@@ -999,6 +1012,8 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
 
 }  // namespace bingo
 
+#include "update_bsp.cuh"
+
 // ------------------------------------------------------------------ host side
 namespace {
 
@@ -1193,6 +1208,218 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
     return true;
 }
 
+// grow-on-demand device buffer owned by the graph
+static bool ensure_buf(bingo_graph *g, void *&buf, size_t &have, size_t need) {
+    if (have >= need) return true;
+    bingo_dev_free(g, buf);
+    buf = bingo_dev_alloc(g, need);
+    have = buf ? need : 0;
+    return buf != nullptr;
+}
+
+// pool growth for the batch's demand; nothing is mutated when this fails
+static bingo_status check_capacity(bingo_graph *g, const UpdCounters &hc, const unsigned long long *bump,
+                                   cudaStream_t s) {
+    if (hc.flag & 1) return BINGO_E_INVAL;
+    if (hc.flag & 4) return BINGO_E_OVERFLOW;
+    bingo_status st;
+    if (bump[0] + hc.need_arc > g->arc_cap && (st = grow_pool(g, 0, bump[0] + hc.need_arc, s)) != BINGO_OK)
+        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
+    if (bump[1] + hc.need_bkt > g->bkt_cap && (st = grow_pool(g, 1, bump[1] + hc.need_bkt, s)) != BINGO_OK)
+        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
+    const uint64_t mem_units_need = bump[2] + hc.need_mem + hc.reserve_mem;
+    if (mem_units_need > g->mem_cap / 4 && (st = grow_pool(g, 2, mem_units_need, s)) != BINGO_OK)
+        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
+    return BINGO_OK;
+}
+
+static inline unsigned warp_grid(uint64_t units, unsigned cap) {
+    const uint64_t b = (units + MT / 32 - 1) / (MT / 32);
+    return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, cap));
+}
+
+// Bulk-synchronous batch (update_bsp.cuh) over the touched vertices of a sorted,
+// segmented batch.  Touched vertices are processed in sub-batches of at most
+// BSP_MAXT (vertices are independent, all sub-batches use epoch e); the pool
+// demand of the whole batch is reserved before anything is mutated.
+static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t *sv, const uint32_t *seg,
+                              const uint32_t *tv, uint64_t ntouch, uint32_t e, UpdCounters *dc,
+                              unsigned long long *dstats, cudaStream_t s) {
+    uint64_t maxt = BSP_MAXT;   // BINGO_BSP_MAXT: smaller sub-batches (tests)
+    if (const char *ev = getenv("BINGO_BSP_MAXT")) maxt = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
+    const uint64_t ntmax = std::min<uint64_t>(ntouch, maxt);
+    size_t vb = 0;
+    {
+        auto add = [&](size_t x) { vb = ((vb + 255) & ~(size_t)255) + x; };
+        for (int j = 0; j < 7; j++) add(4 * ntmax);
+        add(8 * ntmax);
+        add(4ull * GK_N * 32 * ntmax);
+        for (int j = 0; j < 4; j++) add(8 * (ntmax + 1));
+        for (int j = 0; j < 4; j++) add(8 * (ntmax + 2));
+        add(8 * (ntmax + 1));
+        add(8 * (ntmax + 2));
+        add(4ull * VST * ntmax);
+        add(8 * scan_tmp_words(ntmax + 1));
+        add(sizeof(BspTotals));
+        add(4 * ntmax);
+        add(64);
+        vb += 4096;
+    }
+    if (!ensure_buf(g, g->bscratch, g->bscratch_bytes, vb)) return BINGO_E_NOMEM;
+    if (g->hscratch_bytes < sizeof(BspTotals)) {
+        if (g->hscratch) cudaFreeHost(g->hscratch);
+        g->hscratch = nullptr;
+        g->hscratch_bytes = 0;
+        UCK(cudaMallocHost(&g->hscratch, sizeof(BspTotals)));
+        g->hscratch_bytes = sizeof(BspTotals);
+    }
+    BspTotals *ht = (BspTotals *)g->hscratch;
+    Carve cv{(char *)g->bscratch, 0};
+    BspArgs a;
+    memset(&a, 0, sizeof(a));
+    a.vL = cv.take<uint32_t>(ntmax);
+    a.vq = cv.take<uint32_t>(ntmax);
+    a.vm = cv.take<uint32_t>(ntmax);
+    a.vN = cv.take<uint32_t>(ntmax);
+    a.vmiss = cv.take<uint32_t>(ntmax);
+    a.vlist0 = cv.take<uint32_t>(ntmax);
+    a.vacap = cv.take<uint32_t>(ntmax);
+    a.vaoff = cv.take<uint64_t>(ntmax);
+    a.gk = cv.take<uint32_t>((size_t)GK_N * 32 * ntmax);
+    a.cc_copy = cv.take<uint64_t>(ntmax + 1);
+    a.cc_sel = cv.take<uint64_t>(ntmax + 1);
+    a.cc_grp = cv.take<uint64_t>(ntmax + 1);
+    a.cc_all = cv.take<uint64_t>(ntmax + 1);
+    uint64_t *p_copy = cv.take<uint64_t>(ntmax + 2), *p_sel = cv.take<uint64_t>(ntmax + 2),
+             *p_grp = cv.take<uint64_t>(ntmax + 2), *p_all = cv.take<uint64_t>(ntmax + 2);
+    a.p_copy = p_copy;
+    a.p_sel = p_sel;
+    a.p_grp = p_grp;
+    a.p_all = p_all;
+    uint64_t *scr_need = cv.take<uint64_t>(ntmax + 1), *scr_off = cv.take<uint64_t>(ntmax + 2);
+    uint32_t *vstats = cv.take<uint32_t>((size_t)VST * ntmax);
+    uint64_t *stmp = cv.take<uint64_t>(scan_tmp_words(ntmax + 1));
+    BspTotals *dt = cv.take<BspTotals>(1);
+    a.hubs = cv.take<uint32_t>(ntmax);
+    a.nhubs = cv.take<uint32_t>(16);
+    auto refresh = [&]() {
+        fill_mutate_common(g, a.g, e);
+        a.g.recs = recs;
+        a.g.sval = sv;
+        a.g.seg = seg;
+        a.g.tv = tv;
+        a.g.scr_off = scr_off;
+        a.g.vstats = vstats;
+    };
+    refresh();
+    const bool multi = ntouch > maxt;
+    const unsigned WG = 148 * 16, IG = 148 * 32;
+    if (multi) {
+        // demand of the whole batch first (read-only pass)
+        a.t0 = 0;
+        a.nt = (uint32_t)ntouch;
+        k_bsp_plan<<<warp_grid(ntouch, WG), MT, 0, s>>>(a, scr_need, dc, true, false);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        UCK(cudaMemcpyAsync(&ht->c, dc, sizeof(UpdCounters), cudaMemcpyDeviceToHost, s));
+        UCK(cudaMemcpyAsync(ht->bump, g->counters, sizeof(ht->bump), cudaMemcpyDeviceToHost, s));
+        UCK(cudaStreamSynchronize(s));
+        const bingo_status st = check_capacity(g, ht->c, ht->bump, s);
+        if (st != BINGO_OK) return st;
+        refresh();
+    }
+    for (uint64_t t0 = 0; t0 < ntouch; t0 += maxt) {
+        a.t0 = (uint32_t)t0;
+        a.nt = (uint32_t)std::min<uint64_t>(maxt, ntouch - t0);
+        const uint32_t nt = a.nt;
+        UCK(cudaMemsetAsync(a.nhubs, 0, 4, s));
+        k_bsp_plan<<<warp_grid(nt, WG), MT, 0, s>>>(a, scr_need, dc, !multi, true);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        UCK(exclusive_scan_u64(scr_need, scr_off, nt, stmp, s));
+        UCK(exclusive_scan_u64(a.cc_copy, p_copy, nt, stmp, s));
+        UCK(exclusive_scan_u64(a.cc_sel, p_sel, nt, stmp, s));
+        UCK(exclusive_scan_u64(a.cc_grp, p_grp, nt, stmp, s));
+        if (g->nbt) UCK(exclusive_scan_u64(a.cc_all, p_all, nt, stmp, s));
+        else UCK(cudaMemsetAsync(p_all + nt, 0, 8, s));
+        k_bsp_totals<<<1, 32, 0, s>>>(a, dc, scr_off, dt);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        UCK(cudaMemcpyAsync(ht, dt, sizeof(BspTotals), cudaMemcpyDeviceToHost, s));
+        UCK(cudaStreamSynchronize(s));
+        if (!multi) {
+            const bingo_status st = check_capacity(g, ht->c, ht->bump, s);
+            if (st != BINGO_OK) return st;
+            refresh();
+        }
+        // ---- from here on the (sub-)batch is applied
+        const uint64_t sel = ht->sel, grp = ht->grp, copy = ht->copy, all = ht->all;
+        if (ht->scr) {
+            if (!ensure_buf(g, g->vscratch, g->vscratch_bytes, 4 * (ht->scr + 64))) return BINGO_E_NOMEM;
+            a.g.scr = (uint32_t *)g->vscratch;
+        }
+        uint64_t *itmp = nullptr;
+        if (sel || grp) {
+            size_t ib = 0;
+            auto add = [&](size_t x) { ib = ((ib + 255) & ~(size_t)255) + x; };
+            add(8 * (sel + 1)); add(8 * (sel + 2)); add(8 * (grp + 1)); add(8 * (grp + 2));
+            add(8 * scan_tmp_words(std::max(sel, grp) + 1));
+            ib += 1024;
+            if (!ensure_buf(g, g->iscratch, g->iscratch_bytes, ib)) return BINGO_E_NOMEM;
+            Carve ic{(char *)g->iscratch, 0};
+            a.icnt = ic.take<uint64_t>(sel + 1);
+            uint64_t *ipref = ic.take<uint64_t>(sel + 2);
+            a.gcnt = ic.take<uint64_t>(grp + 1);
+            uint64_t *gpref = ic.take<uint64_t>(grp + 2);
+            a.ipref = ipref;
+            a.gpref = gpref;
+            itmp = ic.take<uint64_t>(scan_tmp_words(std::max(sel, grp) + 1));
+        }
+#define BSP_LAUNCH(kern, grid, ...)                                  \
+        do {                                                         \
+            kern<<<(grid), MT, 0, s>>>(__VA_ARGS__);                 \
+            bingo_count_launch();                                    \
+            UCK(cudaGetLastError());                                 \
+        } while (0)
+        BSP_LAUNCH(k_bsp_alloc_insert, warp_grid(nt, WG), a);
+        if (copy) BSP_LAUNCH(k_bsp_copy, warp_grid(copy, IG), a, copy);
+        if (ht->scr) {   // some touched vertex has deletes
+            if (sel) BSP_LAUNCH(k_bsp_select, warp_grid(sel, IG), a, sel);
+            BSP_LAUNCH(k_bsp_finalize, warp_grid(nt, WG), a);
+        }
+        if (sel) {       // large vertices with deletes
+            BSP_LAUNCH(k_bsp_hole_count, warp_grid(sel, IG), a, sel);
+            UCK(exclusive_scan_u64(a.icnt, const_cast<uint64_t *>(a.ipref), sel, itmp, s));
+            BSP_LAUNCH(k_bsp_hole_write, warp_grid(sel, IG), a, sel);
+            BSP_LAUNCH(k_bsp_tail, warp_grid(ht->hubs, WG), a);
+            if (grp) {
+                BSP_LAUNCH(k_bsp_grp_count, warp_grid(grp, IG), a, grp);
+                UCK(exclusive_scan_u64(a.gcnt, const_cast<uint64_t *>(a.gpref), grp, itmp, s));
+                BSP_LAUNCH(k_bsp_grp_write, warp_grid(grp, IG), a, grp);
+                BSP_LAUNCH(k_bsp_grp_tail, warp_grid(ht->hubs, WG), a);
+            }
+        }
+        BSP_LAUNCH(k_bsp_rebuild, warp_grid(nt, WG), a);
+        if (g->nbt && all) {
+            BSP_LAUNCH(k_bsp_nb_clear, warp_grid(all, IG), a, all);
+            BSP_LAUNCH(k_bsp_nb_fill, warp_grid(all, IG), a, all);
+        }
+#undef BSP_LAUNCH
+        k_upd_stats<<<(unsigned)std::min<uint64_t>((nt + 255) / 256, 148), 256, 0, s>>>(vstats, nt, dstats);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+    }
+    return BINGO_OK;
+}
+
+static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
+                                 const unsigned long long *dstats, bingo_update_stats *stats, cudaStream_t s);
+
+static bool use_legacy_mutate() {
+    const char *ev = getenv("BINGO_UPD_LEGACY");
+    return ev && ev[0] == '1';
+}
+
 extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
                                             bingo_update_stats *stats, void *stream) {
     if (!g) return BINGO_E_INVAL;
@@ -1268,6 +1495,12 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     uint64_t ntouch = 0;
     UCK(cudaMemcpyAsync(&ntouch, head_ex + n, 8, cudaMemcpyDeviceToHost, s));
     UCK(cudaStreamSynchronize(s));
+    const uint32_t e = g->epoch + 1;
+    if (!use_legacy_mutate()) {
+        const bingo_status st = apply_bsp(g, recs, sv, seg, tv, ntouch, e, dc, dstats, s);
+        if (st != BINGO_OK) return st;
+        return finish_batch(g, n, ntouch, e, dstats, stats, s);
+    }
     const bool bs = (g->flags & BINGO_BUILD_BS_MODE) != 0;
     uint32_t small_L = SMALL_L;
     if (const char *ev = getenv("BINGO_UPD_SMALL_L")) small_L = (uint32_t)strtoul(ev, nullptr, 10);
@@ -1285,17 +1518,11 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     UCK(cudaMemcpyAsync(bump, g->counters, sizeof(bump), cudaMemcpyDeviceToHost, s));
     UCK(cudaMemcpyAsync(&scr_total, scr_off + ntouch, 8, cudaMemcpyDeviceToHost, s));
     UCK(cudaStreamSynchronize(s));
-    if (hc.flag & 1) return BINGO_E_INVAL;
-    if (hc.flag & 4) return BINGO_E_OVERFLOW;
     // ---- capacity (grow pools before any mutation; NOMEM leaves the graph untouched)
-    bingo_status st;
-    if (bump[0] + hc.need_arc > g->arc_cap && (st = grow_pool(g, 0, bump[0] + hc.need_arc, s)) != BINGO_OK)
-        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
-    if (bump[1] + hc.need_bkt > g->bkt_cap && (st = grow_pool(g, 1, bump[1] + hc.need_bkt, s)) != BINGO_OK)
-        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
-    const uint64_t mem_units_need = bump[2] + hc.need_mem + hc.reserve_mem;
-    if (mem_units_need > g->mem_cap / 4 && (st = grow_pool(g, 2, mem_units_need, s)) != BINGO_OK)
-        return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
+    {
+        const bingo_status st = check_capacity(g, hc, bump, s);
+        if (st != BINGO_OK) return st;
+    }
     // per-vertex delete scratch
     uint32_t *vscr = nullptr;
     const size_t vbytes = 4 * (scr_total + 64);
@@ -1309,7 +1536,6 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
         vscr = (uint32_t *)g->vscratch;
     }
     // ---- mutate (from here on the batch is applied)
-    const uint32_t e = g->epoch + 1;
     MutateArgs ma;
     ma.recs = recs;
     ma.sval = sv;
@@ -1372,6 +1598,11 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
         bingo_count_launch();
         UCK(cudaGetLastError());
     }
+    return finish_batch(g, n, ntouch, e, dstats, stats, s);
+}
+
+static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
+                                 const unsigned long long *dstats, bingo_update_stats *stats, cudaStream_t s) {
     unsigned long long hs[32];
     UCK(cudaMemcpyAsync(hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, s));
     UCK(cudaStreamSynchronize(s));

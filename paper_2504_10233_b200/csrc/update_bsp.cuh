@@ -1,0 +1,874 @@
+// update_bsp.cuh -- the bulk-synchronous batched update (included by update.cu).
+//
+// Same semantics as mutate_vertex (insert -> delete -> rebuild per touched
+// vertex, readings R-6/R-8), restructured for the GPU: every phase is
+// ONE wide kernel over all touched vertices of the batch, with the per-vertex
+// state held in global structure-of-arrays between phases, and every O(degree)
+// scan split into chunk ITEMS of CH adjacency positions (or member slots) that
+// are spread over the whole GPU, one warp per item.  A hub's delete scan
+// therefore runs on hundreds of SMs instead of one block, and a small vertex's
+// ~25 dependent round trips are paid once per phase for the whole batch instead
+// of once per vertex-wave.
+//
+//   plan          (warp / vertex)  pre-batch groups, demand, chunk-item counts
+//   alloc_insert  (warp / vertex)  relocations, member growth, inserts (batch
+//                                  order), delete-scratch init
+//   copy          (warp / item)    adjacency relocation copies
+//   select        (warp / item)    round 0 of the (epoch, position) selection
+//   finalize      (warp / vertex)  picks, further rounds for repeated deletes,
+//                                  per-group delete counts
+//   hole_count / scan / hole_write (warp / item)   holes = marked positions
+//                                  < L' in ascending order
+//   tail          (warp / vertex)  adjacency tail window fills the holes (R-6)
+//   grp_count / scan / grp_write (warp / item)     group fronts: holes in slot
+//                                  order + renames of moved arcs
+//   grp_tail      (warp / vertex)  group tail windows fill the holes (R-6)
+//   rebuild       (warp / vertex)  Eq.9 reclassification, member
+//                                  materialisation, integer Vose (R-4)
+//   nb_clear / nb_fill (warp / item)   node2vec neighbour sets (optional)
+#pragma once
+
+namespace bingo {
+
+static constexpr uint32_t CH = 1024;   // adjacency positions / member slots per chunk item (32 per lane)
+static constexpr uint32_t BSP_MAXT = 1u << 21;   // touched vertices per sub-batch (state ~1.1 KB each)
+enum : uint32_t { GK_KIND0 = 0, GK_C, GK_INSK, GK_DELK, GK_MOFF, GK_CAP, GK_ONE, GK_GHO, GK_N };
+
+struct BspArgs {
+    MutateArgs g;                  // graph, batch (global touched index), delete scratch, vstats (local)
+    uint32_t t0, nt;               // this sub-batch: touched vertices [t0, t0 + nt); local i = t - t0
+    uint32_t *vL, *vq, *vm, *vN, *vmiss, *vlist0, *vacap;
+    uint64_t *vaoff;
+    uint32_t *gk;                  // [GK_N][nt][32]: lane k = radix group k
+    uint64_t *cc_copy, *cc_sel, *cc_grp, *cc_all;          // chunk items per vertex (plan)
+    const uint64_t *p_copy, *p_sel, *p_grp, *p_all;        // their exclusive prefixes [nt + 1]
+    uint64_t *icnt;                // per select item: holes in its chunk
+    const uint64_t *ipref;
+    uint64_t *gcnt;                // per group item: deleted slots in its chunk
+    const uint64_t *gpref;
+    uint32_t *hubs, *nhubs;        // large vertices (L > CH) with deletes, any order
+};
+
+__device__ __forceinline__ uint32_t *gkp(const BspArgs &a, uint32_t f, uint32_t i) {
+    return a.gk + ((uint64_t)f * a.nt + i) * 32;
+}
+
+// per-vertex delete scratch (words from plan: bsp_scr_words)
+struct DelScr {
+    uint32_t *bm, *hkey, *hk, *hfound, *hsel, *holes, *R, *gh;
+    unsigned long long *hbest, *hprev;
+    uint32_t Hq;
+};
+__host__ __device__ inline uint64_t bsp_scr_words(uint32_t L, uint32_t q, uint32_t nlist) {
+    if (!q) return 0;
+    uint64_t Hq = 1;
+    while (Hq < 2ull * q) Hq <<= 1;
+    uint64_t w = (uint64_t)(L + 31) / 32 + 8 * Hq + (2ull + nlist) * q + 8;
+    return (w + 7) & ~7ull;
+}
+__device__ __forceinline__ DelScr del_scr(uint32_t *base, uint32_t L, uint32_t q) {
+    DelScr s;
+    s.Hq = next_pow2(2 * q);
+    s.bm = base;
+    s.hkey = base + (L + 31) / 32;
+    s.hk = s.hkey + s.Hq;
+    s.hfound = s.hk + s.Hq;
+    s.hsel = s.hfound + s.Hq;
+    s.hbest = reinterpret_cast<unsigned long long *>((reinterpret_cast<uintptr_t>(s.hsel + s.Hq) + 7) & ~(uintptr_t)7);
+    s.hprev = s.hbest + s.Hq;
+    s.holes = reinterpret_cast<uint32_t *>(s.hprev + s.Hq);
+    s.R = s.holes + q;
+    s.gh = s.R + q;
+    return s;
+}
+
+// largest i in [0, n) with pref[i] <= x  (pref nondecreasing, pref[0] = 0, x < pref[n])
+__device__ __forceinline__ uint32_t owner_of(const uint64_t *pref, uint32_t n, uint64_t x) {
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (__ldg(pref + mid) <= x) lo = mid;
+        else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t hash_find(const uint32_t *hkey, uint32_t hmask, uint32_t x) {
+    uint32_t s = hash_slot(x, hmask);
+    for (;;) {
+        const uint32_t kx = hkey[s];
+        if (kx == x) return s;
+        if (kx == EMPTY_KEY) return EMPTY_KEY;
+        s = (s + 1) & hmask;
+    }
+}
+
+#define BSP_WARP_LOOP(i, n)                                                                     \
+    for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < (n);                    \
+         i += (gridDim.x * blockDim.x) >> 5)
+#define BSP_ITEM_LOOP(it, total)                                                                \
+    for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < (total);    \
+         it += ((uint64_t)gridDim.x * blockDim.x) >> 5)
+
+// ------------------------------------------------------------------ plan
+// count: add the batch's pool demand to cnt; state: write the per-vertex state
+__global__ void __launch_bounds__(MT) k_bsp_plan(const BspArgs a, uint64_t *__restrict__ scr_need, UpdCounters *cnt,
+                                                 bool count, bool state) {
+    __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res;
+    __shared__ int b_flag;
+    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = 0; b_flag = 0; }
+    __syncthreads();
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(i, a.nt) {
+        const uint32_t t = a.t0 + i;
+        const VHdr h = g.hdr[g.tv[t]];
+        PlanLane pl;
+        const PlanOut o = plan_vertex(g.recs, g.sval, g.seg[t], g.seg[t + 1], h, g.bkt, g.gcan, g.alpha, g.bs,
+                                      g.arc_slack, g.mem_slack, &pl);
+        if (count && lane == 0) {
+            if (o.overflow) atomicOr(&b_flag, 4);
+            if (o.arc) atomicAdd(&b_arc, o.arc);
+            if (o.bkt) atomicAdd(&b_bkt, o.bkt);
+            if (o.mem) atomicAdd(&b_mem, o.mem);
+            if (o.res) atomicAdd(&b_res, o.res);
+        }
+        if (!state) continue;
+        const bool lst = is_list(pl.kind);
+        gkp(a, GK_KIND0, i)[lane] = pl.kind;
+        gkp(a, GK_C, i)[lane] = pl.c;
+        gkp(a, GK_INSK, i)[lane] = pl.insk;
+        gkp(a, GK_MOFF, i)[lane] = lst ? pl.ref : 0u;
+        gkp(a, GK_CAP, i)[lane] = lst ? pl.aux : 0u;
+        gkp(a, GK_ONE, i)[lane] = pl.kind == K_ONE ? pl.aux : 0xFFFFFFFFu;
+        const uint32_t gch = warp_sum(lst ? (pl.c + pl.insk + CH - 1) / CH : 0u);
+        if (lane == 0) {
+            a.vL[i] = o.L;
+            a.vq[i] = o.q;
+            a.vm[i] = o.L - h.d;
+            a.vlist0[i] = pl.list0;
+            scr_need[i] = bsp_scr_words(o.L, o.q, __popc(pl.list0));
+            // chunk items only for LARGE vertices (L > CH); a small vertex's scans are
+            // done by its own warp inside alloc_insert / finalize
+            const bool large = o.L > CH;
+            a.cc_copy[i] = (o.L > h.adj_cap && h.d > CH) ? (h.d + CH - 1) / CH : 0;
+            a.cc_sel[i] = (o.q && large) ? (o.L + CH - 1) / CH : 0;
+            a.cc_grp[i] = (o.q && large) ? gch : 0;
+            if (o.q && large) a.hubs[atomicAdd(a.nhubs, 1u)] = i;
+            a.cc_all[i] = o.L ? (o.L + CH - 1) / CH : 1;
+        }
+    }
+    if (!count) return;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (b_arc) atomicAdd(&cnt->need_arc, b_arc);
+        if (b_bkt) atomicAdd(&cnt->need_bkt, b_bkt);
+        if (b_mem) atomicAdd(&cnt->need_mem, b_mem);
+        if (b_res) atomicAdd(&cnt->reserve_mem, b_res);
+        if (b_flag) atomicOr(&cnt->flag, b_flag);
+    }
+}
+
+// host-visible totals after the plan (one D2H copy, one sync)
+struct BspTotals {
+    UpdCounters c;
+    unsigned long long bump[3];
+    unsigned long long scr, copy, sel, grp, all, hubs;
+};
+__global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint64_t *scr_off, BspTotals *out) {
+    if (threadIdx.x != 0) return;
+    out->c = *cnt;
+    for (int j = 0; j < 3; j++) out->bump[j] = a.g.bump[j];
+    out->scr = scr_off[a.nt];
+    out->copy = a.p_copy[a.nt];
+    out->sel = a.p_sel[a.nt];
+    out->grp = a.p_grp[a.nt];
+    out->all = a.p_all[a.nt];
+    out->hubs = *a.nhubs;
+}
+
+// ------------------------------------------------------------------ relocations, inserts, scratch init
+__global__ void __launch_bounds__(MT) k_bsp_alloc_insert(const BspArgs a) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(i, a.nt) {
+        const uint32_t t = a.t0 + i;
+        const uint32_t beg = g.seg[t], end = g.seg[t + 1];
+        const VHdr h = g.hdr[g.tv[t]];
+        const uint32_t L = a.vL[i], q = a.vq[i], m = a.vm[i];
+        // adjacency relocation (the copy of the d live arcs is the chunked k_bsp_copy)
+        uint64_t aoff = h.adj_off;
+        uint32_t acap = h.adj_cap;
+        if (L > h.adj_cap) {
+            const uint64_t cap2 = arc_capacity(L, g.arc_slack);
+            unsigned long long o = 0;
+            if (lane == 0) o = atomicAdd(&g.bump[0], (unsigned long long)cap2);
+            aoff = __shfl_sync(0xffffffffu, o, 0);
+            acap = (uint32_t)cap2;
+        }
+        if (lane == 0) {
+            a.vaoff[i] = aoff;
+            a.vacap[i] = acap;
+            a.vN[i] = 0;
+            a.vmiss[i] = 0;
+        }
+        if (aoff != h.adj_off && h.d <= CH) {
+            // small relocation: copied here (larger ones by k_bsp_copy items)
+            for (uint32_t p = lane; p < h.d; p += 32) {
+                g.arc[aoff + p] = g.arc[h.adj_off + p];
+                g.arc_epoch[aoff + p] = g.arc_epoch[h.adj_off + p];
+            }
+        }
+        // member arrays that overflow their capacity (lists before the batch)
+        const uint32_t kind = gkp(a, GK_KIND0, i)[lane];
+        const uint32_t c = gkp(a, GK_C, i)[lane];
+        const uint32_t insk_tot = gkp(a, GK_INSK, i)[lane];
+        const uint32_t ref = gkp(a, GK_MOFF, i)[lane];
+        uint32_t moff = ref, cap = gkp(a, GK_CAP, i)[lane];
+        const bool grow = is_list(kind) && c + insk_tot > cap;
+        if (grow) {
+            const uint32_t units = member_units(c + insk_tot, g.mem_slack);
+            moff = (uint32_t)atomicAdd(&g.bump[2], (unsigned long long)units);
+            cap = units * 4;
+            gkp(a, GK_MOFF, i)[lane] = moff;
+            gkp(a, GK_CAP, i)[lane] = cap;
+        }
+        gkp(a, GK_DELK, i)[lane] = 0;
+        uint32_t gm = __ballot_sync(0xffffffffu, grow);
+        while (gm) {
+            const int k = __ffs(gm) - 1;
+            gm &= gm - 1;
+            const uint32_t from = __shfl_sync(0xffffffffu, ref, k);
+            const uint32_t to = __shfl_sync(0xffffffffu, moff, k);
+            const uint32_t cnt = __shfl_sync(0xffffffffu, c, k);
+#pragma unroll 4
+            for (uint32_t j = lane; j < cnt; j += 32) {
+                g.mdst[(uint64_t)to * 4 + j] = g.mdst[(uint64_t)from * 4 + j];
+                g.midx[(uint64_t)to * 4 + j] = g.midx[(uint64_t)from * 4 + j];
+            }
+        }
+        // inserts in batch order: adjacency appends at d + rank,
+        // member appends to groups that are REGULAR/SPARSE before the batch
+        if (m) {
+            uint32_t run = 0, insk = 0;
+            for (uint32_t base = beg; base < end; base += 32) {
+                const uint32_t p = base + lane;
+                uint4 r = make_uint4(2u, 0u, 0u, 0u);
+                if (p < end) r = g.recs[g.sval[p]];
+                const bool ins = r.x == 0u;
+                const uint32_t bal_i = __ballot_sync(0xffffffffu, ins);
+                const uint32_t idx = h.d + run + __popc(bal_i & lanemask_lt());
+                const uint32_t w = ins ? r.w : 0u;
+                if (ins) {
+                    g.arc[aoff + idx] = make_uint2(r.z, r.w);
+                    g.arc_epoch[aoff + idx] = g.epoch;
+                }
+                uint32_t mk = __reduce_or_sync(0xffffffffu, w);
+                while (mk) {
+                    const int k = __ffs(mk) - 1;
+                    mk &= mk - 1;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, (w >> k) & 1u);
+                    const uint32_t kind_kk = __shfl_sync(0xffffffffu, kind, k);
+                    const uint32_t start = __shfl_sync(0xffffffffu, c + insk, k);
+                    const uint32_t mo = __shfl_sync(0xffffffffu, moff, k);
+                    if (is_list(kind_kk) && ((w >> k) & 1u)) {
+                        const uint64_t e = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
+                        g.mdst[e] = r.z;
+                        g.midx[e] = idx;
+                    }
+                    if (lane == (uint32_t)k) insk += __popc(bal);
+                }
+                run += __popc(bal_i);
+            }
+        }
+        // delete scratch: bitmap, hash of the distinct deleted destinations
+        if (q) {
+            const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
+            const uint32_t bw = (L + 31) / 32;
+            for (uint32_t j = lane; j < bw; j += 32) s.bm[j] = 0;
+            for (uint32_t j = lane; j < s.Hq; j += 32) {
+                s.hkey[j] = EMPTY_KEY;
+                s.hk[j] = 0;
+                s.hfound[j] = 0;
+                s.hsel[j] = 0;
+                s.hbest[j] = ~0ull;
+                s.hprev[j] = 0;
+            }
+            __syncwarp();
+            const uint32_t hmask = s.Hq - 1;
+            for (uint32_t p = beg + lane; p < end; p += 32) {
+                const uint4 r = g.recs[g.sval[p]];
+                if (r.x != 1u) continue;
+                uint32_t sl = hash_slot(r.z, hmask);
+                for (;;) {
+                    const uint32_t old = atomicCAS(&s.hkey[sl], EMPTY_KEY, r.z);
+                    if (old == EMPTY_KEY || old == r.z) {
+                        atomicAdd(&s.hk[sl], 1u);
+                        break;
+                    }
+                    sl = (sl + 1) & hmask;
+                }
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------------ adjacency relocation copies
+__global__ void __launch_bounds__(MT) k_bsp_copy(const BspArgs a, uint64_t total) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_ITEM_LOOP(it, total) {
+        const uint32_t i = owner_of(a.p_copy, a.nt, it);
+        const uint32_t c = (uint32_t)(it - a.p_copy[i]);
+        const VHdr h = g.hdr[g.tv[a.t0 + i]];
+        const uint64_t to = a.vaoff[i];
+        const uint32_t e = min(h.d, (c + 1) * CH);
+#pragma unroll 4
+        for (uint32_t p = c * CH + lane; p < e; p += 32) {
+            g.arc[to + p] = g.arc[h.adj_off + p];
+            g.arc_epoch[to + p] = g.arc_epoch[h.adj_off + p];
+        }
+    }
+}
+
+// ------------------------------------------------------------------ delete selection, round 0 (R-8)
+// every live instance of a deleted destination: count it, and atomicMin its
+// packed (epoch << 32 | position) key
+__global__ void __launch_bounds__(MT) k_bsp_select(const BspArgs a, uint64_t total) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_ITEM_LOOP(it, total) {
+        const uint32_t i = owner_of(a.p_sel, a.nt, it);
+        const uint32_t c = (uint32_t)(it - a.p_sel[i]);
+        const uint32_t L = a.vL[i], q = a.vq[i];
+        const uint64_t aoff = a.vaoff[i];
+        const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
+        const uint32_t hmask = s.Hq - 1;
+        const uint32_t e = min(L, (c + 1) * CH);
+#pragma unroll 4
+        for (uint32_t p = c * CH + lane; p < e; p += 32) {
+            const uint32_t x = __ldg(&g.arc[aoff + p].x);
+            const uint32_t hit = hash_find(s.hkey, hmask, x);
+            if (hit == EMPTY_KEY) continue;
+            const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
+            atomicAdd(&s.hfound[hit], 1u);
+            atomicMin(&s.hbest[hit], key);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ delete-and-swap pieces (warp-wide)
+// adjacency tail window [L', L): survivors fill the holes in rank order (R-6),
+// R maps tail position -> new position (or DEL_MARK)
+__device__ __forceinline__ void tail_window(const MutateArgs &g, const DelScr &s, uint64_t aoff, uint32_t L,
+                                            uint32_t Lp) {
+    const uint32_t lane = lane_id();
+    uint32_t carry = 0;
+    for (uint32_t t0 = Lp; t0 < L; t0 += 32) {
+        const uint32_t tt = t0 + lane;
+        const bool in = tt < L;
+        const bool surv = in && !bit_test(s.bm, tt);
+        const uint32_t bal = __ballot_sync(0xffffffffu, surv);
+        if (in) {
+            if (surv) {
+                const uint32_t dstp = s.holes[carry + __popc(bal & lanemask_lt())];
+                g.arc[aoff + dstp] = g.arc[aoff + tt];
+                g.arc_epoch[aoff + dstp] = g.arc_epoch[aoff + tt];
+                s.R[tt - Lp] = dstp;
+            } else {
+                s.R[tt - Lp] = DEL_MARK;
+            }
+        }
+        carry += __popc(bal);
+    }
+}
+
+// group front, slots [sb, se) of [0, L_k'): deleted slots are recorded as holes
+// gh[r0 + rank] in slot order; surviving members pointing into the adjacency tail
+// are renamed in place
+__device__ __forceinline__ void group_front(const MutateArgs &g, const DelScr &s, uint32_t *Mi, uint32_t *gh,
+                                            uint32_t sb, uint32_t se, uint32_t r0, uint32_t Lp) {
+    const uint32_t lane = lane_id();
+    uint32_t r = r0;
+    for (uint32_t s0 = sb; s0 < se; s0 += 32) {
+        const uint32_t sl = s0 + lane;
+        bool del = false;
+        if (sl < se) {
+            const uint32_t x = Mi[sl];
+            del = bit_test(s.bm, x);
+            if (!del && x >= Lp) Mi[sl] = s.R[x - Lp];
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, del);
+        if (del) gh[r + __popc(bal & lanemask_lt())] = sl;
+        r += __popc(bal);
+    }
+}
+
+// group tail window [L_k', c'): survivors, renamed, fill the holes in rank order (R-6)
+__device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s, uint32_t *Md, uint32_t *Mi,
+                                           const uint32_t *gh, uint32_t cp, uint32_t Nk, uint32_t Lp) {
+    const uint32_t lane = lane_id();
+    uint32_t carry = 0;
+    for (uint32_t s0 = cp - Nk; s0 < cp; s0 += 32) {
+        const uint32_t sl = s0 + lane;
+        uint32_t x = 0;
+        const bool surv = sl < cp && !bit_test(s.bm, (x = Mi[sl]));
+        const uint32_t bal = __ballot_sync(0xffffffffu, surv);
+        if (surv) {
+            const uint32_t hslot = gh[carry + __popc(bal & lanemask_lt())];
+            Md[hslot] = Md[sl];
+            Mi[hslot] = x >= Lp ? s.R[x - Lp] : x;
+        }
+        carry += __popc(bal);
+    }
+}
+
+// ------------------------------------------------------------------ picks, further rounds, per-group counts
+__global__ void __launch_bounds__(MT) k_bsp_finalize(const BspArgs a) {
+    __shared__ uint32_t s_delk[MT / 32][32];
+    const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(i, a.nt) {
+        const uint32_t q = a.vq[i];
+        if (!q) continue;
+        const uint32_t L = a.vL[i];
+        const uint64_t aoff = a.vaoff[i];
+        const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
+        const uint32_t hmask = s.Hq - 1;
+        s_delk[w][lane] = 0;
+        const bool small = L <= CH;
+        if (small) {
+            // round 0 of a small vertex (large ones: k_bsp_select items)
+            for (uint32_t p = lane; p < L; p += 32) {
+                const uint32_t hit = hash_find(s.hkey, hmask, g.arc[aoff + p].x);
+                if (hit == EMPTY_KEY) continue;
+                const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
+                atomicAdd(&s.hfound[hit], 1u);
+                atomicMin(&s.hbest[hit], key);
+            }
+        }
+        __syncwarp();
+        uint32_t N = 0;
+        for (uint32_t round = 0;; round++) {
+            if (round) {
+                // round r > 0: per destination still owed a delete, the smallest key
+                // above the previous pick (repeated deletes of one (u, v), R-8)
+                for (uint32_t p = lane; p < L; p += 32) {
+                    const uint32_t hit = hash_find(s.hkey, hmask, g.arc[aoff + p].x);
+                    if (hit == EMPTY_KEY) continue;
+                    const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
+                    if (s.hsel[hit] < s.hk[hit] && key > s.hprev[hit]) atomicMin(&s.hbest[hit], key);
+                }
+                __syncwarp();
+            }
+            bool more = false;
+            for (uint32_t sl = lane; sl < s.Hq; sl += 32) {
+                if (s.hkey[sl] == EMPTY_KEY || s.hsel[sl] >= s.hk[sl]) continue;
+                const unsigned long long b = s.hbest[sl];
+                if (b == ~0ull) continue;
+                const uint32_t p = (uint32_t)b;
+                atomicOr(&s.bm[p >> 5], 1u << (p & 31u));
+                const uint32_t hs = ++s.hsel[sl];
+                s.hprev[sl] = b;
+                s.hbest[sl] = ~0ull;
+                N++;
+                uint32_t bits = g.arc[aoff + p].y;
+                while (bits) {
+                    const int k = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    atomicAdd(&s_delk[w][k], 1u);
+                }
+                if (hs < s.hk[sl] && hs < s.hfound[sl]) more = true;
+            }
+            __syncwarp();
+            if (!__any_sync(0xffffffffu, more)) break;
+        }
+        uint32_t miss = 0;
+        for (uint32_t sl = lane; sl < s.Hq; sl += 32)
+            if (s.hkey[sl] != EMPTY_KEY) miss += s.hk[sl] - s.hsel[sl];
+        N = warp_sum(N);
+        miss = warp_sum(miss);
+        __syncwarp();
+        const uint32_t delk = s_delk[w][lane];
+        const uint32_t list0 = a.vlist0[i];
+        // gh offsets: the deleted-slot lists of the list groups, packed in k order
+        const uint32_t v = ((list0 >> lane) & 1u) ? delk : 0u;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        gkp(a, GK_DELK, i)[lane] = delk;
+        gkp(a, GK_GHO, i)[lane] = x - v;
+        if (lane == 0) {
+            a.vN[i] = N;
+            a.vmiss[i] = miss;
+        }
+        __syncwarp();
+        if (!small || !N) continue;
+        // ---- small vertex: the whole delete-and-swap here (L <= CH: one bitmap word per lane)
+        const uint32_t Lp = L - N;
+        {
+            uint32_t word = 0;
+            if (lane * 32 < Lp) {
+                word = s.bm[lane];
+                const uint32_t lim = Lp - lane * 32;
+                if (lim < 32) word &= (1u << lim) - 1u;
+            }
+            const uint32_t pc = __popc(word);
+            uint32_t y = pc;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= (uint32_t)o) y += z;
+            }
+            uint32_t r = y - pc;
+            while (word) {
+                const int b = __ffs(word) - 1;
+                word &= word - 1;
+                s.holes[r++] = lane * 32 + b;
+            }
+        }
+        __syncwarp();
+        tail_window(g, s, aoff, L, Lp);
+        __syncwarp();
+        const uint32_t cp_l = gkp(a, GK_C, i)[lane] + gkp(a, GK_INSK, i)[lane];
+        const uint32_t mo_l = gkp(a, GK_MOFF, i)[lane];
+        uint32_t lm = list0;
+        while (lm) {
+            const int k = __ffs(lm) - 1;
+            lm &= lm - 1;
+            const uint32_t cp = __shfl_sync(0xffffffffu, cp_l, k);
+            const uint32_t Nk = __shfl_sync(0xffffffffu, delk, k);
+            const uint32_t mo = __shfl_sync(0xffffffffu, mo_l, k);
+            const uint32_t gho = __shfl_sync(0xffffffffu, x - v, k);
+            uint32_t *Md = g.mdst + (uint64_t)mo * 4;
+            uint32_t *Mi = g.midx + (uint64_t)mo * 4;
+            group_front(g, s, Mi, s.gh + gho, 0, cp - Nk, 0, Lp);
+            __syncwarp();
+            if (Nk) group_tail(g, s, Md, Mi, s.gh + gho, cp, Nk, Lp);
+            __syncwarp();
+        }
+    }
+}
+
+// ------------------------------------------------------------------ holes: marked positions < L', ascending
+__device__ __forceinline__ uint32_t hole_word(const BspArgs &a, uint32_t i, uint32_t c, uint32_t &wi, DelScr &s) {
+    const uint32_t L = a.vL[i], q = a.vq[i], N = a.vN[i];
+    if (!N) return 0;
+    const uint32_t Lp = L - N;
+    s = del_scr(a.g.scr + a.g.scr_off[i], L, q);
+    wi = c * 32 + lane_id();
+    if (wi * 32 >= Lp) return 0;
+    uint32_t word = s.bm[wi];
+    const uint32_t lim = Lp - wi * 32;
+    if (lim < 32) word &= (1u << lim) - 1u;
+    return word;
+}
+
+__global__ void __launch_bounds__(MT) k_bsp_hole_count(const BspArgs a, uint64_t total) {
+    BSP_ITEM_LOOP(it, total) {
+        const uint32_t i = owner_of(a.p_sel, a.nt, it);
+        const uint32_t c = (uint32_t)(it - a.p_sel[i]);
+        uint32_t wi;
+        DelScr s;
+        const uint32_t n = warp_sum((uint32_t)__popc(hole_word(a, i, c, wi, s)));
+        if (lane_id() == 0) a.icnt[it] = n;
+    }
+}
+
+__global__ void __launch_bounds__(MT) k_bsp_hole_write(const BspArgs a, uint64_t total) {
+    const uint32_t lane = lane_id();
+    BSP_ITEM_LOOP(it, total) {
+        const uint32_t i = owner_of(a.p_sel, a.nt, it);
+        if (!a.vN[i]) continue;
+        const uint32_t c = (uint32_t)(it - a.p_sel[i]);
+        uint32_t wi = 0;
+        DelScr s;
+        uint32_t word = hole_word(a, i, c, wi, s);
+        const uint32_t n = __popc(word);
+        uint32_t x = n;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        uint32_t r = (uint32_t)(a.ipref[it] - a.ipref[a.p_sel[i]]) + x - n;
+        while (word) {
+            const int b = __ffs(word) - 1;
+            word &= word - 1;
+            s.holes[r++] = wi * 32 + b;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ adjacency tail window [L', L) (R-6)
+__global__ void __launch_bounds__(MT) k_bsp_tail(const BspArgs a) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(h, *a.nhubs) {
+        const uint32_t i = a.hubs[h];
+        const uint32_t N = a.vN[i], L = a.vL[i];
+        if (!N) continue;
+        const uint32_t q = a.vq[i];
+        const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
+        tail_window(g, s, a.vaoff[i], L, L - N);
+    }
+}
+
+// ------------------------------------------------------------------ group fronts
+// group item -> (vertex i, group k, chunk j of the slots [0, c + ins_k)); every
+// lane computes the same answer
+struct GrpItem {
+    uint32_t i, k, j, first;   // first: item index of chunk 0 of (i, k)
+    uint32_t cp, Nk, moff, gho;
+};
+__device__ __forceinline__ GrpItem grp_item(const BspArgs &a, uint64_t it) {
+    const uint32_t lane = lane_id();
+    GrpItem gi;
+    gi.i = owner_of(a.p_grp, a.nt, it);
+    const uint32_t c = (uint32_t)(it - a.p_grp[gi.i]);
+    const uint32_t list0 = a.vlist0[gi.i];
+    const bool lst = (list0 >> lane) & 1u;
+    const uint32_t cp = lst ? gkp(a, GK_C, gi.i)[lane] + gkp(a, GK_INSK, gi.i)[lane] : 0u;
+    const uint32_t nch = (cp + CH - 1) / CH;
+    uint32_t x = nch;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    const uint32_t pre = x - nch;
+    const uint32_t own = __ballot_sync(0xffffffffu, nch && pre <= c && c < pre + nch);
+    gi.k = __ffs(own) - 1;
+    gi.j = c - __shfl_sync(0xffffffffu, pre, gi.k);
+    gi.first = (uint32_t)(it - gi.j);
+    gi.cp = __shfl_sync(0xffffffffu, cp, gi.k);
+    gi.Nk = gkp(a, GK_DELK, gi.i)[gi.k];
+    gi.moff = gkp(a, GK_MOFF, gi.i)[gi.k];
+    gi.gho = gkp(a, GK_GHO, gi.i)[gi.k];
+    return gi;
+}
+
+__global__ void __launch_bounds__(MT) k_bsp_grp_count(const BspArgs a, uint64_t total) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_ITEM_LOOP(it, total) {
+        const GrpItem gi = grp_item(a, it);
+        uint32_t n = 0;
+        if (gi.Nk) {
+            const uint32_t L = a.vL[gi.i], q = a.vq[gi.i];
+            const DelScr s = del_scr(g.scr + g.scr_off[gi.i], L, q);
+            const uint32_t *Mi = g.midx + (uint64_t)gi.moff * 4;
+            const uint32_t e = min(gi.cp - gi.Nk, (gi.j + 1) * CH);
+#pragma unroll 4
+            for (uint32_t sl = gi.j * CH + lane; sl < e; sl += 32) n += bit_test(s.bm, Mi[sl]) ? 1u : 0u;
+            n = warp_sum(n);
+        }
+        if (lane == 0) a.gcnt[it] = n;
+    }
+}
+
+// pass 1 over the front [0, L_k'): deleted slots become holes ranked in slot
+// order; survivors pointing into the adjacency tail are renamed in place
+__global__ void __launch_bounds__(MT) k_bsp_grp_write(const BspArgs a, uint64_t total) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_ITEM_LOOP(it, total) {
+        const GrpItem gi = grp_item(a, it);
+        const uint32_t N = a.vN[gi.i];
+        if (!N) continue;
+        const uint32_t L = a.vL[gi.i], q = a.vq[gi.i], Lp = L - N;
+        const DelScr s = del_scr(g.scr + g.scr_off[gi.i], L, q);
+        uint32_t *Mi = g.midx + (uint64_t)gi.moff * 4;
+        const uint32_t Lk = gi.cp - gi.Nk;
+        const uint32_t r0 = gi.Nk ? (uint32_t)(a.gpref[it] - a.gpref[gi.first]) : 0u;
+        group_front(g, s, Mi, s.gh + gi.gho, gi.j * CH, min(Lk, (gi.j + 1) * CH), r0, Lp);
+    }
+}
+
+// pass 2 over each group's tail window [L_k', c'): survivors, renamed, fill the
+// holes in rank order (R-6)
+__global__ void __launch_bounds__(MT) k_bsp_grp_tail(const BspArgs a) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(h, *a.nhubs) {
+        const uint32_t i = a.hubs[h];
+        const uint32_t N = a.vN[i], L = a.vL[i];
+        if (!N) continue;
+        const uint32_t q = a.vq[i], Lp = L - N;
+        const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
+        const uint32_t Nk_l = gkp(a, GK_DELK, i)[lane];
+        uint32_t gm = __ballot_sync(0xffffffffu, ((a.vlist0[i] >> lane) & 1u) && Nk_l);
+        const uint32_t cp_l = gkp(a, GK_C, i)[lane] + gkp(a, GK_INSK, i)[lane];
+        const uint32_t mo_l = gkp(a, GK_MOFF, i)[lane];
+        const uint32_t gho_l = gkp(a, GK_GHO, i)[lane];
+        while (gm) {
+            const int k = __ffs(gm) - 1;
+            gm &= gm - 1;
+            const uint32_t cp = __shfl_sync(0xffffffffu, cp_l, k);
+            const uint32_t Nk = __shfl_sync(0xffffffffu, Nk_l, k);
+            const uint32_t mo = __shfl_sync(0xffffffffu, mo_l, k);
+            const uint32_t gho = __shfl_sync(0xffffffffu, gho_l, k);
+            group_tail(g, s, g.mdst + (uint64_t)mo * 4, g.midx + (uint64_t)mo * 4, s.gh + gho, cp, Nk, Lp);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ rebuild
+__global__ void __launch_bounds__(MT) k_bsp_rebuild(const BspArgs a) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(i, a.nt) {
+        const uint32_t t = a.t0 + i;
+        const uint32_t u = g.tv[t];
+        const VHdr h = g.hdr[u];
+        const uint32_t L = a.vL[i], q = a.vq[i], N = a.vN[i], dn = L - N, Lp = dn;
+        const uint64_t aoff = a.vaoff[i];
+        DelScr s;
+        if (q) s = del_scr(g.scr + g.scr_off[i], L, q);
+        const uint32_t k = lane;
+        const uint32_t kind0 = gkp(a, GK_KIND0, i)[k];
+        const uint32_t cn = gkp(a, GK_C, i)[k] + gkp(a, GK_INSK, i)[k] - gkp(a, GK_DELK, i)[k];
+        const uint32_t kind1 = classify(cn, dn, g.alpha, g.beta, g.bs);
+        uint32_t moff = gkp(a, GK_MOFF, i)[k], cap = gkp(a, GK_CAP, i)[k];
+        bool fill = false, find = false;
+        uint32_t one = 0xFFFFFFFFu;
+        if (is_list(kind1) && !is_list(kind0)) {
+            const uint32_t units = member_units(cn, g.mem_slack);
+            moff = (uint32_t)atomicAdd(&g.bump[2], (unsigned long long)units);
+            cap = units * 4;
+            fill = true;
+        } else if (kind1 == K_ONE) {
+            if (is_list(kind0)) {
+                one = g.midx[(uint64_t)moff * 4];
+            } else if (kind0 == K_ONE) {
+                const uint32_t mo = gkp(a, GK_ONE, i)[k];
+                if (q && N && bit_test(s.bm, mo)) find = true;
+                else one = (N && mo >= Lp) ? s.R[mo - Lp] : mo;
+                if (!find && one == DEL_MARK) find = true;
+            } else {
+                find = true;
+            }
+        }
+        // statistics: deletes, missing deletes, kind transitions
+        uint32_t *vs = g.vstats + (uint64_t)i * VST;
+        if (lane < 25) vs[2 + lane] = 0;
+        __syncwarp();
+        if (kind0 != K_EMPTY || kind1 != K_EMPTY) atomicAdd(&vs[2 + 5 * kind0 + kind1], 1u);
+        if (lane == 0) {
+            vs[0] = N;
+            vs[1] = a.vmiss[i];
+        }
+        const uint32_t fm = __ballot_sync(0xffffffffu, fill);
+        const uint32_t fd = __ballot_sync(0xffffffffu, find);
+        if (fm | fd) {
+            // one ascending pass over the post-batch adjacency materialises new lists
+            // (scan order = ascending index, R-2) and finds the member of ONE groups
+            uint32_t fillc = 0;
+            for (uint32_t base = 0; base < dn; base += 32) {
+                const uint32_t p = base + lane;
+                uint2 e = make_uint2(0u, 0u);
+                if (p < dn) e = g.arc[aoff + p];
+                uint32_t mk = (fm | fd) & __reduce_or_sync(0xffffffffu, e.y);
+                while (mk) {
+                    const int kb = __ffs(mk) - 1;
+                    mk &= mk - 1;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, (e.y >> kb) & 1u);
+                    if ((fd >> kb) & 1u) {
+                        if (lane == (uint32_t)kb) one = base + __ffs(bal) - 1;
+                        continue;
+                    }
+                    const uint32_t start = __shfl_sync(0xffffffffu, fillc, kb);
+                    const uint32_t mo = __shfl_sync(0xffffffffu, moff, kb);
+                    if ((e.y >> kb) & 1u) {
+                        const uint64_t qq = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
+                        g.mdst[qq] = e.x;
+                        g.midx[qq] = p;
+                    }
+                    if (lane == (uint32_t)kb) fillc += __popc(bal);
+                }
+            }
+            // a ONE group found by the scan: its first member in ascending order
+            // (find lanes were written by the lowest set lane of the first hit)
+        }
+        uint32_t onedst = 0;
+        if (kind1 == K_ONE) onedst = g.arc[aoff + one].x;
+        const uint32_t mask = __ballot_sync(0xffffffffu, cn != 0);
+        const uint32_t n = __popc(mask);
+        const uint64_t T = warp_sum(cn ? ((uint64_t)cn << k) : 0ull);
+        const uint32_t kb = (lane < n) ? (uint32_t)__fns(mask, 0, lane + 1) : 0u;
+        const uint32_t c_b = __shfl_sync(0xffffffffu, cn, kb);
+        const uint32_t kind_b = __shfl_sync(0xffffffffu, kind1, kb);
+        const uint32_t moff_b = __shfl_sync(0xffffffffu, moff, kb);
+        const uint32_t cap_b = __shfl_sync(0xffffffffu, cap, kb);
+        const uint32_t one_b = __shfl_sync(0xffffffffu, one, kb);
+        const uint32_t od_b = __shfl_sync(0xffffffffu, onedst, kb);
+        uint64_t thr;
+        uint32_t alias;
+        vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
+        uint32_t bo = h.bkt_off, ncap = h.ncap;
+        if (n > h.ncap) {
+            unsigned long long o = 0;
+            if (lane == 0) o = atomicAdd(&g.bump[1], (unsigned long long)bucket_capacity(n));
+            bo = (uint32_t)__shfl_sync(0xffffffffu, o, 0);
+            ncap = bucket_capacity(n);
+        }
+        uint32_t x_b, y_b;
+        group_view(kind_b, c_b, moff_b, od_b, dn, aoff, x_b, y_b);
+        const uint32_t aux_b = is_list(kind_b) ? cap_b : (kind_b == K_ONE ? one_b : 0u);
+        write_buckets(g.bkt, g.gcan, bo, n, lane, kb, kind_b, c_b, x_b, y_b, aux_b, thr, alias, T);
+        if (lane == 0) {
+            VHdr nh;
+            nh.T = T;
+            nh.adj_off = aoff;
+            nh.bkt_off = bo;
+            nh.d = dn;
+            nh.n = (uint8_t)n;
+            nh.ncap = (uint8_t)ncap;
+            nh.pad = 0;
+            nh.adj_cap = a.vacap[i];
+            g.hdr[u] = nh;
+            ThinHdr th;
+            th.bkt_off = bo;
+            th.n = (uint8_t)n;
+            th.flags = (dn >= g.hot_b ? 1 : 0) | (dn >= g.hot_m ? 2 : 0);
+            th.pad1 = 0;
+            g.thdr[u] = th;
+            if (g.nbt) g.nbo[u] = nb_pack(4 * aoff, nb_log2size(dn));
+        }
+    }
+}
+
+// ------------------------------------------------------------------ node2vec neighbour sets of touched vertices
+__global__ void __launch_bounds__(MT) k_bsp_nb_clear(const BspArgs a, uint64_t total) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_ITEM_LOOP(it, total) {
+        const uint32_t i = owner_of(a.p_all, a.nt, it);
+        const uint32_t c = (uint32_t)(it - a.p_all[i]);
+        const uint32_t dn = a.vL[i] - a.vN[i];
+        const uint32_t size = 1u << nb_log2size(dn);
+        uint32_t *tbl = g.nbt + 4 * a.vaoff[i];
+        const uint32_t e = min(size, (c + 1) * 4 * CH);
+        for (uint32_t j = c * 4 * CH + lane; j < e; j += 32) tbl[j] = NB_EMPTY;
+    }
+}
+
+__global__ void __launch_bounds__(MT) k_bsp_nb_fill(const BspArgs a, uint64_t total) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_ITEM_LOOP(it, total) {
+        const uint32_t i = owner_of(a.p_all, a.nt, it);
+        const uint32_t c = (uint32_t)(it - a.p_all[i]);
+        const uint32_t dn = a.vL[i] - a.vN[i];
+        const uint32_t mask = (1u << nb_log2size(dn)) - 1;
+        const uint64_t aoff = a.vaoff[i];
+        uint32_t *tbl = g.nbt + 4 * aoff;
+        const uint32_t e = min(dn, (c + 1) * CH);
+        for (uint32_t p = c * CH + lane; p < e; p += 32) nb_insert(tbl, mask, g.arc[aoff + p].x);
+    }
+}
+
+}  // namespace bingo

@@ -68,20 +68,32 @@ def _bias_of(u, v, e, hi):
     return 1 + ((u * 2654435761 + v * 40503 + e * 97) % hi)
 
 
-@pytest.mark.parametrize("seed,bs_mode,hi,route", [(0, False, 200, "auto"), (1, False, 1 << 20, "auto"),
-                                                   (2, True, 200, "auto"), (3, False, 7, "auto"),
-                                                   (4, False, 255, "auto"), (5, True, 1 << 31, "auto"),
-                                                   (0, False, 200, "block"), (3, False, 7, "block"),
-                                                   (6, False, 1 << 20, "block")])
-def test_random_multigraph_batches(seed, bs_mode, hi, route, monkeypatch):
-    if route == "block":       # every touched vertex through the block-per-vertex kernel
-        monkeypatch.setenv("BINGO_UPD_SMALL_L", "0")
-    """Random multigraphs with duplicates, hubs (multi-chunk scans), missing deletes, repeated
-    deletes of one pair, mixed biases forcing kind transitions in every direction."""
+ROUTES = {
+    "bsp": {},                                                  # bulk-synchronous pipeline (default)
+    "bsp-sub": {"BINGO_BSP_MAXT": "7"},                         # ... in sub-batches of 7 touched vertices
+    "legacy": {"BINGO_UPD_LEGACY": "1"},                        # per-vertex mutate kernels (warp / block)
+    "legacy-block": {"BINGO_UPD_LEGACY": "1", "BINGO_UPD_SMALL_L": "0"},   # ... every vertex on a block
+}
+
+
+@pytest.mark.parametrize("seed,bs_mode,hi,route,hub", [
+    (0, False, 200, "bsp", 700), (1, False, 1 << 20, "bsp", 700), (2, True, 200, "bsp", 700),
+    (3, False, 7, "bsp", 700), (4, False, 255, "bsp", 700), (5, True, 1 << 31, "bsp", 700),
+    (7, False, 200, "bsp", 3500), (8, False, 7, "bsp", 5000), (9, True, 255, "bsp", 3000),
+    (0, False, 200, "bsp-sub", 700), (8, False, 7, "bsp-sub", 5000),
+    (0, False, 200, "legacy", 700), (3, False, 7, "legacy", 700), (7, False, 200, "legacy", 3500),
+    (0, False, 200, "legacy-block", 700), (3, False, 7, "legacy-block", 700),
+    (6, False, 1 << 20, "legacy-block", 700)])
+def test_random_multigraph_batches(seed, bs_mode, hi, route, hub, monkeypatch):
+    """Random multigraphs with duplicates, hubs (multi-chunk scans: 32-arc warp chunks and
+    1024-position chunk items), missing deletes, repeated deletes of one pair, mixed biases
+    forcing kind transitions in every direction -- through every update route."""
+    for k, v in ROUTES[route].items():
+        monkeypatch.setenv(k, v)
     rng = np.random.default_rng(1000 + seed)
     V = int(rng.integers(5, 60))
     deg = rng.integers(0, 30, size=V)
-    deg[0] = 700                               # a hub spanning many 32-arc chunks
+    deg[0] = hub                               # a hub spanning many chunks
     ro = np.zeros(V + 1, dtype=np.uint64)
     ro[1:] = np.cumsum(deg)
     A = int(ro[-1])
