@@ -1251,7 +1251,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     size_t vb = 0;
     {
         auto add = [&](size_t x) { vb = ((vb + 255) & ~(size_t)255) + x; };
-        for (int j = 0; j < 7; j++) add(4 * ntmax);
+        for (int j = 0; j < 8; j++) add(4 * ntmax);
         add(8 * ntmax);
         add(4ull * GK_N * 32 * ntmax);
         for (int j = 0; j < 4; j++) add(8 * (ntmax + 1));
@@ -1261,6 +1261,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         add(4ull * VST * ntmax);
         add(8 * scan_tmp_words(ntmax + 1));
         add(sizeof(BspTotals));
+        add(4 * ntmax);
         add(4 * ntmax);
         add(64);
         vb += 4096;
@@ -1284,6 +1285,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     a.vmiss = cv.take<uint32_t>(ntmax);
     a.vlist0 = cv.take<uint32_t>(ntmax);
     a.vacap = cv.take<uint32_t>(ntmax);
+    a.vmoved = cv.take<uint32_t>(ntmax);
     a.vaoff = cv.take<uint64_t>(ntmax);
     a.gk = cv.take<uint32_t>((size_t)GK_N * 32 * ntmax);
     a.cc_copy = cv.take<uint64_t>(ntmax + 1);
@@ -1301,7 +1303,9 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     uint64_t *stmp = cv.take<uint64_t>(scan_tmp_words(ntmax + 1));
     BspTotals *dt = cv.take<BspTotals>(1);
     a.hubs = cv.take<uint32_t>(ntmax);
+    a.bigs = cv.take<uint32_t>(ntmax);
     a.nhubs = cv.take<uint32_t>(16);
+    a.nbigs = a.nhubs + 1;
     auto refresh = [&]() {
         fill_mutate_common(g, a.g, e);
         a.g.recs = recs;
@@ -1332,7 +1336,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         a.t0 = (uint32_t)t0;
         a.nt = (uint32_t)std::min<uint64_t>(maxt, ntouch - t0);
         const uint32_t nt = a.nt;
-        UCK(cudaMemsetAsync(a.nhubs, 0, 4, s));
+        UCK(cudaMemsetAsync(a.nhubs, 0, 8, s));
         k_bsp_plan<<<warp_grid(nt, WG), MT, 0, s>>>(a, scr_need, dc, !multi, true);
         bingo_count_launch();
         UCK(cudaGetLastError());
@@ -1375,34 +1379,57 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             a.gpref = gpref;
             itmp = ic.take<uint64_t>(scan_tmp_words(std::max(sel, grp) + 1));
         }
-#define BSP_LAUNCH(kern, grid, ...)                                  \
+#define BSP_LAUNCH(kern, grid, strm, ...)                            \
         do {                                                         \
-            kern<<<(grid), MT, 0, s>>>(__VA_ARGS__);                 \
+            kern<<<(grid), MT, 0, (strm)>>>(__VA_ARGS__);            \
             bingo_count_launch();                                    \
             UCK(cudaGetLastError());                                 \
         } while (0)
-        BSP_LAUNCH(k_bsp_alloc_insert, warp_grid(nt, WG), a);
-        if (copy) BSP_LAUNCH(k_bsp_copy, warp_grid(copy, IG), a, copy);
-        if (ht->scr) {   // some touched vertex has deletes
-            if (sel) BSP_LAUNCH(k_bsp_select, warp_grid(sel, IG), a, sel);
-            BSP_LAUNCH(k_bsp_finalize, warp_grid(nt, WG), a);
+        BSP_LAUNCH(k_bsp_alloc_insert, warp_grid(nt, WG), s, a);
+        // two independent chains over disjoint vertex sets (shared state: bump
+        // counters, atomics only): small vertices on `s`, large ones on the side stream
+        const bool side = ht->bigs != 0;
+        if (side && !g->aux_stream) {
+            UCK(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
+            UCK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
+            UCK(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
         }
-        if (sel) {       // large vertices with deletes
-            BSP_LAUNCH(k_bsp_hole_count, warp_grid(sel, IG), a, sel);
-            UCK(exclusive_scan_u64(a.icnt, const_cast<uint64_t *>(a.ipref), sel, itmp, s));
-            BSP_LAUNCH(k_bsp_hole_write, warp_grid(sel, IG), a, sel);
-            BSP_LAUNCH(k_bsp_tail, warp_grid(ht->hubs, WG), a);
+        cudaStream_t sh = side ? g->aux_stream : s;
+        if (side) {
+            UCK(cudaEventRecord(g->ev_fork, s));
+            UCK(cudaStreamWaitEvent(sh, g->ev_fork, 0));
+        }
+        // -- large vertices
+        if (copy) BSP_LAUNCH(k_bsp_copy, warp_grid(copy, IG), sh, a, copy);
+        if (sel) {
+            BSP_LAUNCH(k_bsp_select, warp_grid(sel, IG), sh, a, sel);
+            BSP_LAUNCH(k_bsp_finalize, warp_grid(ht->hubs, WG), sh, a, true);
+            BSP_LAUNCH(k_bsp_hole_count, warp_grid(sel, IG), sh, a, sel);
+            UCK(exclusive_scan_u64(a.icnt, const_cast<uint64_t *>(a.ipref), sel, itmp, sh));
+            BSP_LAUNCH(k_bsp_hole_write, warp_grid(sel, IG), sh, a, sel);
+            BSP_LAUNCH(k_bsp_tail, warp_grid(ht->hubs, WG), sh, a);
             if (grp) {
-                BSP_LAUNCH(k_bsp_grp_count, warp_grid(grp, IG), a, grp);
-                UCK(exclusive_scan_u64(a.gcnt, const_cast<uint64_t *>(a.gpref), grp, itmp, s));
-                BSP_LAUNCH(k_bsp_grp_write, warp_grid(grp, IG), a, grp);
-                BSP_LAUNCH(k_bsp_grp_tail, warp_grid(ht->hubs, WG), a);
+                BSP_LAUNCH(k_bsp_grp_count, warp_grid(grp, IG), sh, a, grp);
+                UCK(exclusive_scan_u64(a.gcnt, const_cast<uint64_t *>(a.gpref), grp, itmp, sh));
+                BSP_LAUNCH(k_bsp_grp_write, warp_grid(grp, IG), sh, a, grp);
+                BSP_LAUNCH(k_bsp_grp_tail, warp_grid(ht->hubs, WG), sh, a);
             }
         }
-        BSP_LAUNCH(k_bsp_rebuild, warp_grid(nt, WG), a);
+        if (ht->bigs) {
+            k_bsp_rebuild_big<<<(unsigned)std::min<uint64_t>(ht->bigs, 148 * 2), LT, 0, sh>>>(a);
+            bingo_count_launch();
+            UCK(cudaGetLastError());
+        }
+        // -- small vertices
+        if (ht->scr) BSP_LAUNCH(k_bsp_finalize, warp_grid(nt, WG), s, a, false);
+        BSP_LAUNCH(k_bsp_rebuild, warp_grid(nt, WG), s, a);
+        if (side) {
+            UCK(cudaEventRecord(g->ev_join, sh));
+            UCK(cudaStreamWaitEvent(s, g->ev_join, 0));
+        }
         if (g->nbt && all) {
-            BSP_LAUNCH(k_bsp_nb_clear, warp_grid(all, IG), a, all);
-            BSP_LAUNCH(k_bsp_nb_fill, warp_grid(all, IG), a, all);
+            BSP_LAUNCH(k_bsp_nb_clear, warp_grid(all, IG), s, a, all);
+            BSP_LAUNCH(k_bsp_nb_fill, warp_grid(all, IG), s, a, all);
         }
 #undef BSP_LAUNCH
         k_upd_stats<<<(unsigned)std::min<uint64_t>((nt + 255) / 256, 148), 256, 0, s>>>(vstats, nt, dstats);

@@ -37,7 +37,7 @@ enum : uint32_t { GK_KIND0 = 0, GK_C, GK_INSK, GK_DELK, GK_MOFF, GK_CAP, GK_ONE,
 struct BspArgs {
     MutateArgs g;                  // graph, batch (global touched index), delete scratch, vstats (local)
     uint32_t t0, nt;               // this sub-batch: touched vertices [t0, t0 + nt); local i = t - t0
-    uint32_t *vL, *vq, *vm, *vN, *vmiss, *vlist0, *vacap;
+    uint32_t *vL, *vq, *vm, *vN, *vmiss, *vlist0, *vacap, *vmoved;
     uint64_t *vaoff;
     uint32_t *gk;                  // [GK_N][nt][32]: lane k = radix group k
     uint64_t *cc_copy, *cc_sel, *cc_grp, *cc_all;          // chunk items per vertex (plan)
@@ -47,6 +47,7 @@ struct BspArgs {
     uint64_t *gcnt;                // per group item: deleted slots in its chunk
     const uint64_t *gpref;
     uint32_t *hubs, *nhubs;        // large vertices (L > CH) with deletes, any order
+    uint32_t *bigs, *nbigs;        // all large vertices, any order
 };
 
 __device__ __forceinline__ uint32_t *gkp(const BspArgs &a, uint32_t f, uint32_t i) {
@@ -155,6 +156,7 @@ __global__ void __launch_bounds__(MT) k_bsp_plan(const BspArgs a, uint64_t *__re
             a.cc_sel[i] = (o.q && large) ? (o.L + CH - 1) / CH : 0;
             a.cc_grp[i] = (o.q && large) ? gch : 0;
             if (o.q && large) a.hubs[atomicAdd(a.nhubs, 1u)] = i;
+            if (large) a.bigs[atomicAdd(a.nbigs, 1u)] = i;
             a.cc_all[i] = o.L ? (o.L + CH - 1) / CH : 1;
         }
     }
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(MT) k_bsp_plan(const BspArgs a, uint64_t *__re
 struct BspTotals {
     UpdCounters c;
     unsigned long long bump[3];
-    unsigned long long scr, copy, sel, grp, all, hubs;
+    unsigned long long scr, copy, sel, grp, all, hubs, bigs;
 };
 __global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint64_t *scr_off, BspTotals *out) {
     if (threadIdx.x != 0) return;
@@ -185,6 +187,7 @@ __global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint
     out->grp = a.p_grp[a.nt];
     out->all = a.p_all[a.nt];
     out->hubs = *a.nhubs;
+    out->bigs = *a.nbigs;
 }
 
 // ------------------------------------------------------------------ relocations, inserts, scratch init
@@ -360,10 +363,10 @@ __global__ void __launch_bounds__(MT) k_bsp_select(const BspArgs a, uint64_t tot
 // ------------------------------------------------------------------ delete-and-swap pieces (warp-wide)
 // adjacency tail window [L', L): survivors fill the holes in rank order (R-6),
 // R maps tail position -> new position (or DEL_MARK)
-__device__ __forceinline__ void tail_window(const MutateArgs &g, const DelScr &s, uint64_t aoff, uint32_t L,
-                                            uint32_t Lp) {
+__device__ __forceinline__ uint32_t tail_window(const MutateArgs &g, const DelScr &s, uint64_t aoff, uint32_t L,
+                                                uint32_t Lp) {
     const uint32_t lane = lane_id();
-    uint32_t carry = 0;
+    uint32_t carry = 0, moved = 0;   // moved: OR of the biases of the arcs that move (their groups need renames)
     for (uint32_t t0 = Lp; t0 < L; t0 += 32) {
         const uint32_t tt = t0 + lane;
         const bool in = tt < L;
@@ -372,7 +375,9 @@ __device__ __forceinline__ void tail_window(const MutateArgs &g, const DelScr &s
         if (in) {
             if (surv) {
                 const uint32_t dstp = s.holes[carry + __popc(bal & lanemask_lt())];
-                g.arc[aoff + dstp] = g.arc[aoff + tt];
+                const uint2 e = g.arc[aoff + tt];
+                moved |= e.y;
+                g.arc[aoff + dstp] = e;
                 g.arc_epoch[aoff + dstp] = g.arc_epoch[aoff + tt];
                 s.R[tt - Lp] = dstp;
             } else {
@@ -381,6 +386,7 @@ __device__ __forceinline__ void tail_window(const MutateArgs &g, const DelScr &s
         }
         carry += __popc(bal);
     }
+    return __reduce_or_sync(0xffffffffu, moved);
 }
 
 // group front, slots [sb, se) of [0, L_k'): deleted slots are recorded as holes
@@ -424,19 +430,24 @@ __device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s,
 }
 
 // ------------------------------------------------------------------ picks, further rounds, per-group counts
-__global__ void __launch_bounds__(MT) k_bsp_finalize(const BspArgs a) {
+// hubs = false: small vertices (all of their delete path here); hubs = true: the
+// large vertices with deletes (picks only; the rest by the chunk-item kernels)
+__global__ void __launch_bounds__(MT) k_bsp_finalize(const BspArgs a, bool hubs) {
     __shared__ uint32_t s_delk[MT / 32][32];
+    // small vertices: bitmap, holes, rename table and group holes in shared memory
+    __shared__ uint32_t s_bm[MT / 32][32], s_hol[MT / 32][32], s_R[MT / 32][32], s_gh[MT / 32][64];
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
     const MutateArgs &g = a.g;
-    BSP_WARP_LOOP(i, a.nt) {
+    BSP_WARP_LOOP(j, hubs ? *a.nhubs : a.nt) {
+        const uint32_t i = hubs ? a.hubs[j] : j;
         const uint32_t q = a.vq[i];
-        if (!q) continue;
         const uint32_t L = a.vL[i];
+        const bool small = L <= CH;
+        if (!q || small == hubs) continue;
         const uint64_t aoff = a.vaoff[i];
         const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
         const uint32_t hmask = s.Hq - 1;
         s_delk[w][lane] = 0;
-        const bool small = L <= CH;
         if (small) {
             // round 0 of a small vertex (large ones: k_bsp_select items)
             for (uint32_t p = lane; p < L; p += 32) {
@@ -509,10 +520,19 @@ __global__ void __launch_bounds__(MT) k_bsp_finalize(const BspArgs a) {
         if (!small || !N) continue;
         // ---- small vertex: the whole delete-and-swap here (L <= CH: one bitmap word per lane)
         const uint32_t Lp = L - N;
+        DelScr ls = s;
+        ls.bm = s_bm[w];
+        s_bm[w][lane] = lane < (L + 31) / 32 ? s.bm[lane] : 0u;
+        if (N <= 32) {
+            ls.holes = s_hol[w];
+            ls.R = s_R[w];
+        }
+        if (__shfl_sync(0xffffffffu, x, 31) <= 64) ls.gh = s_gh[w];
+        __syncwarp();
         {
             uint32_t word = 0;
             if (lane * 32 < Lp) {
-                word = s.bm[lane];
+                word = ls.bm[lane];
                 const uint32_t lim = Lp - lane * 32;
                 if (lim < 32) word &= (1u << lim) - 1u;
             }
@@ -527,15 +547,17 @@ __global__ void __launch_bounds__(MT) k_bsp_finalize(const BspArgs a) {
             while (word) {
                 const int b = __ffs(word) - 1;
                 word &= word - 1;
-                s.holes[r++] = lane * 32 + b;
+                ls.holes[r++] = lane * 32 + b;
             }
         }
         __syncwarp();
-        tail_window(g, s, aoff, L, Lp);
+        const uint32_t moved = tail_window(g, ls, aoff, L, Lp);
         __syncwarp();
+        if (N <= 32 && lane < N) s.R[lane] = ls.R[lane];   // rebuild reads R (ONE groups)
         const uint32_t cp_l = gkp(a, GK_C, i)[lane] + gkp(a, GK_INSK, i)[lane];
         const uint32_t mo_l = gkp(a, GK_MOFF, i)[lane];
-        uint32_t lm = list0;
+        // only groups that lost a member or hold an arc that moved change
+        uint32_t lm = list0 & (__ballot_sync(0xffffffffu, delk != 0) | moved);
         while (lm) {
             const int k = __ffs(lm) - 1;
             lm &= lm - 1;
@@ -545,9 +567,9 @@ __global__ void __launch_bounds__(MT) k_bsp_finalize(const BspArgs a) {
             const uint32_t gho = __shfl_sync(0xffffffffu, x - v, k);
             uint32_t *Md = g.mdst + (uint64_t)mo * 4;
             uint32_t *Mi = g.midx + (uint64_t)mo * 4;
-            group_front(g, s, Mi, s.gh + gho, 0, cp - Nk, 0, Lp);
+            group_front(g, ls, Mi, ls.gh + gho, 0, cp - Nk, 0, Lp);
             __syncwarp();
-            if (Nk) group_tail(g, s, Md, Mi, s.gh + gho, cp, Nk, Lp);
+            if (Nk) group_tail(g, ls, Md, Mi, ls.gh + gho, cp, Nk, Lp);
             __syncwarp();
         }
     }
@@ -613,7 +635,8 @@ __global__ void __launch_bounds__(MT) k_bsp_tail(const BspArgs a) {
         if (!N) continue;
         const uint32_t q = a.vq[i];
         const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
-        tail_window(g, s, a.vaoff[i], L, L - N);
+        const uint32_t moved = tail_window(g, s, a.vaoff[i], L, L - N);
+        if (lane_id() == 0) a.vmoved[i] = moved;
     }
 }
 
@@ -678,7 +701,7 @@ __global__ void __launch_bounds__(MT) k_bsp_grp_write(const BspArgs a, uint64_t 
     BSP_ITEM_LOOP(it, total) {
         const GrpItem gi = grp_item(a, it);
         const uint32_t N = a.vN[gi.i];
-        if (!N) continue;
+        if (!N || (!gi.Nk && !((a.vmoved[gi.i] >> gi.k) & 1u))) continue;   // group unchanged
         const uint32_t L = a.vL[gi.i], q = a.vq[gi.i], Lp = L - N;
         const DelScr s = del_scr(g.scr + g.scr_off[gi.i], L, q);
         uint32_t *Mi = g.midx + (uint64_t)gi.moff * 4;
@@ -717,127 +740,216 @@ __global__ void __launch_bounds__(MT) k_bsp_grp_tail(const BspArgs a) {
 }
 
 // ------------------------------------------------------------------ rebuild
-__global__ void __launch_bounds__(MT) k_bsp_rebuild(const BspArgs a) {
-    const uint32_t lane = lane_id();
+// lane k = radix group k of the vertex being rebuilt
+struct RbLane {
+    uint32_t kind1, cn, moff, cap, one;
+};
+
+// stage A (one warp): Eq.9 reclassification, member-array allocation for groups
+// that become lists, the ONE member when it is known without a scan, statistics.
+// Returns the (fill, find) masks of groups that need the adjacency scan.
+__device__ __forceinline__ void rebuild_classify(const BspArgs &a, uint32_t i, RbLane &r, uint32_t &fm, uint32_t &fd) {
+    const uint32_t lane = lane_id(), k = lane;
     const MutateArgs &g = a.g;
-    BSP_WARP_LOOP(i, a.nt) {
-        const uint32_t t = a.t0 + i;
-        const uint32_t u = g.tv[t];
-        const VHdr h = g.hdr[u];
-        const uint32_t L = a.vL[i], q = a.vq[i], N = a.vN[i], dn = L - N, Lp = dn;
-        const uint64_t aoff = a.vaoff[i];
-        DelScr s;
-        if (q) s = del_scr(g.scr + g.scr_off[i], L, q);
-        const uint32_t k = lane;
-        const uint32_t kind0 = gkp(a, GK_KIND0, i)[k];
-        const uint32_t cn = gkp(a, GK_C, i)[k] + gkp(a, GK_INSK, i)[k] - gkp(a, GK_DELK, i)[k];
-        const uint32_t kind1 = classify(cn, dn, g.alpha, g.beta, g.bs);
-        uint32_t moff = gkp(a, GK_MOFF, i)[k], cap = gkp(a, GK_CAP, i)[k];
-        bool fill = false, find = false;
-        uint32_t one = 0xFFFFFFFFu;
-        if (is_list(kind1) && !is_list(kind0)) {
-            const uint32_t units = member_units(cn, g.mem_slack);
-            moff = (uint32_t)atomicAdd(&g.bump[2], (unsigned long long)units);
-            cap = units * 4;
-            fill = true;
-        } else if (kind1 == K_ONE) {
-            if (is_list(kind0)) {
-                one = g.midx[(uint64_t)moff * 4];
-            } else if (kind0 == K_ONE) {
-                const uint32_t mo = gkp(a, GK_ONE, i)[k];
-                if (q && N && bit_test(s.bm, mo)) find = true;
-                else one = (N && mo >= Lp) ? s.R[mo - Lp] : mo;
-                if (!find && one == DEL_MARK) find = true;
-            } else {
-                find = true;
+    const uint32_t L = a.vL[i], q = a.vq[i], N = a.vN[i], dn = L - N, Lp = dn;
+    DelScr s;
+    if (q) s = del_scr(g.scr + g.scr_off[i], L, q);
+    const uint32_t kind0 = gkp(a, GK_KIND0, i)[k];
+    r.cn = gkp(a, GK_C, i)[k] + gkp(a, GK_INSK, i)[k] - gkp(a, GK_DELK, i)[k];
+    r.kind1 = classify(r.cn, dn, g.alpha, g.beta, g.bs);
+    r.moff = gkp(a, GK_MOFF, i)[k];
+    r.cap = gkp(a, GK_CAP, i)[k];
+    r.one = 0xFFFFFFFFu;
+    bool fill = false, find = false;
+    if (is_list(r.kind1) && !is_list(kind0)) {
+        const uint32_t units = member_units(r.cn, g.mem_slack);
+        r.moff = (uint32_t)atomicAdd(&g.bump[2], (unsigned long long)units);
+        r.cap = units * 4;
+        fill = true;
+    } else if (r.kind1 == K_ONE) {
+        if (is_list(kind0)) {
+            r.one = g.midx[(uint64_t)r.moff * 4];
+        } else if (kind0 == K_ONE) {
+            const uint32_t mo = gkp(a, GK_ONE, i)[k];
+            if (q && N && bit_test(s.bm, mo)) find = true;
+            else r.one = (N && mo >= Lp) ? s.R[mo - Lp] : mo;
+            if (!find && r.one == DEL_MARK) find = true;
+        } else {
+            find = true;
+        }
+    }
+    // statistics: deletes, missing deletes, kind transitions
+    uint32_t *vs = g.vstats + (uint64_t)i * VST;
+    if (lane < 25) vs[2 + lane] = 0;
+    __syncwarp();
+    if (kind0 != K_EMPTY || r.kind1 != K_EMPTY) atomicAdd(&vs[2 + 5 * kind0 + r.kind1], 1u);
+    if (lane == 0) {
+        vs[0] = N;
+        vs[1] = a.vmiss[i];
+    }
+    fm = __ballot_sync(0xffffffffu, fill);
+    fd = __ballot_sync(0xffffffffu, find);
+}
+
+// adjacency positions [pb, pe), one warp, ascending: lane k counts (count_only) or
+// writes its fill-group members starting at slot base_k (R-2: ascending index), and
+// records the first position of each find group in first_k
+__device__ __forceinline__ void fill_scan(const MutateArgs &g, uint64_t aoff, uint32_t pb, uint32_t pe, uint32_t fm,
+                                          uint32_t fd, uint32_t moff_l, bool count_only, uint32_t &cnt_l,
+                                          uint32_t &first_l) {
+    const uint32_t lane = lane_id();
+    for (uint32_t base = pb; base < pe; base += 32) {
+        const uint32_t p = base + lane;
+        uint2 e = make_uint2(0u, 0u);
+        if (p < pe) e = g.arc[aoff + p];
+        uint32_t mk = (fm | fd) & __reduce_or_sync(0xffffffffu, e.y);
+        while (mk) {
+            const int kb = __ffs(mk) - 1;
+            mk &= mk - 1;
+            const uint32_t bal = __ballot_sync(0xffffffffu, (e.y >> kb) & 1u);
+            if ((fd >> kb) & 1u) {
+                if (lane == (uint32_t)kb && first_l == 0xFFFFFFFFu) first_l = base + __ffs(bal) - 1;
+                continue;
             }
-        }
-        // statistics: deletes, missing deletes, kind transitions
-        uint32_t *vs = g.vstats + (uint64_t)i * VST;
-        if (lane < 25) vs[2 + lane] = 0;
-        __syncwarp();
-        if (kind0 != K_EMPTY || kind1 != K_EMPTY) atomicAdd(&vs[2 + 5 * kind0 + kind1], 1u);
-        if (lane == 0) {
-            vs[0] = N;
-            vs[1] = a.vmiss[i];
-        }
-        const uint32_t fm = __ballot_sync(0xffffffffu, fill);
-        const uint32_t fd = __ballot_sync(0xffffffffu, find);
-        if (fm | fd) {
-            // one ascending pass over the post-batch adjacency materialises new lists
-            // (scan order = ascending index, R-2) and finds the member of ONE groups
-            uint32_t fillc = 0;
-            for (uint32_t base = 0; base < dn; base += 32) {
-                const uint32_t p = base + lane;
-                uint2 e = make_uint2(0u, 0u);
-                if (p < dn) e = g.arc[aoff + p];
-                uint32_t mk = (fm | fd) & __reduce_or_sync(0xffffffffu, e.y);
-                while (mk) {
-                    const int kb = __ffs(mk) - 1;
-                    mk &= mk - 1;
-                    const uint32_t bal = __ballot_sync(0xffffffffu, (e.y >> kb) & 1u);
-                    if ((fd >> kb) & 1u) {
-                        if (lane == (uint32_t)kb) one = base + __ffs(bal) - 1;
-                        continue;
-                    }
-                    const uint32_t start = __shfl_sync(0xffffffffu, fillc, kb);
-                    const uint32_t mo = __shfl_sync(0xffffffffu, moff, kb);
-                    if ((e.y >> kb) & 1u) {
-                        const uint64_t qq = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
-                        g.mdst[qq] = e.x;
-                        g.midx[qq] = p;
-                    }
-                    if (lane == (uint32_t)kb) fillc += __popc(bal);
+            if (!count_only) {
+                const uint32_t start = __shfl_sync(0xffffffffu, cnt_l, kb);
+                const uint32_t mo = __shfl_sync(0xffffffffu, moff_l, kb);
+                if ((e.y >> kb) & 1u) {
+                    const uint64_t qq = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
+                    g.mdst[qq] = e.x;
+                    g.midx[qq] = p;
                 }
             }
-            // a ONE group found by the scan: its first member in ascending order
-            // (find lanes were written by the lowest set lane of the first hit)
+            if (lane == (uint32_t)kb) cnt_l += __popc(bal);
         }
-        uint32_t onedst = 0;
-        if (kind1 == K_ONE) onedst = g.arc[aoff + one].x;
-        const uint32_t mask = __ballot_sync(0xffffffffu, cn != 0);
-        const uint32_t n = __popc(mask);
-        const uint64_t T = warp_sum(cn ? ((uint64_t)cn << k) : 0ull);
-        const uint32_t kb = (lane < n) ? (uint32_t)__fns(mask, 0, lane + 1) : 0u;
-        const uint32_t c_b = __shfl_sync(0xffffffffu, cn, kb);
-        const uint32_t kind_b = __shfl_sync(0xffffffffu, kind1, kb);
-        const uint32_t moff_b = __shfl_sync(0xffffffffu, moff, kb);
-        const uint32_t cap_b = __shfl_sync(0xffffffffu, cap, kb);
-        const uint32_t one_b = __shfl_sync(0xffffffffu, one, kb);
-        const uint32_t od_b = __shfl_sync(0xffffffffu, onedst, kb);
-        uint64_t thr;
-        uint32_t alias;
-        vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
-        uint32_t bo = h.bkt_off, ncap = h.ncap;
-        if (n > h.ncap) {
-            unsigned long long o = 0;
-            if (lane == 0) o = atomicAdd(&g.bump[1], (unsigned long long)bucket_capacity(n));
-            bo = (uint32_t)__shfl_sync(0xffffffffu, o, 0);
-            ncap = bucket_capacity(n);
+    }
+}
+
+// stage C (one warp): integer Vose (R-4), buckets, headers
+__device__ __forceinline__ void rebuild_write(const BspArgs &a, uint32_t i, const RbLane &r) {
+    const uint32_t lane = lane_id(), k = lane;
+    const MutateArgs &g = a.g;
+    const uint32_t u = g.tv[a.t0 + i];
+    const VHdr h = g.hdr[u];
+    const uint32_t dn = a.vL[i] - a.vN[i];
+    const uint64_t aoff = a.vaoff[i];
+    uint32_t onedst = 0;
+    if (r.kind1 == K_ONE) onedst = g.arc[aoff + r.one].x;
+    const uint32_t mask = __ballot_sync(0xffffffffu, r.cn != 0);
+    const uint32_t n = __popc(mask);
+    const uint64_t T = warp_sum(r.cn ? ((uint64_t)r.cn << k) : 0ull);
+    const uint32_t kb = (lane < n) ? (uint32_t)__fns(mask, 0, lane + 1) : 0u;
+    const uint32_t c_b = __shfl_sync(0xffffffffu, r.cn, kb);
+    const uint32_t kind_b = __shfl_sync(0xffffffffu, r.kind1, kb);
+    const uint32_t moff_b = __shfl_sync(0xffffffffu, r.moff, kb);
+    const uint32_t cap_b = __shfl_sync(0xffffffffu, r.cap, kb);
+    const uint32_t one_b = __shfl_sync(0xffffffffu, r.one, kb);
+    const uint32_t od_b = __shfl_sync(0xffffffffu, onedst, kb);
+    uint64_t thr;
+    uint32_t alias;
+    vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
+    uint32_t bo = h.bkt_off, ncap = h.ncap;
+    if (n > h.ncap) {
+        unsigned long long o = 0;
+        if (lane == 0) o = atomicAdd(&g.bump[1], (unsigned long long)bucket_capacity(n));
+        bo = (uint32_t)__shfl_sync(0xffffffffu, o, 0);
+        ncap = bucket_capacity(n);
+    }
+    uint32_t x_b, y_b;
+    group_view(kind_b, c_b, moff_b, od_b, dn, aoff, x_b, y_b);
+    const uint32_t aux_b = is_list(kind_b) ? cap_b : (kind_b == K_ONE ? one_b : 0u);
+    write_buckets(g.bkt, g.gcan, bo, n, lane, kb, kind_b, c_b, x_b, y_b, aux_b, thr, alias, T);
+    if (lane == 0) {
+        VHdr nh;
+        nh.T = T;
+        nh.adj_off = aoff;
+        nh.bkt_off = bo;
+        nh.d = dn;
+        nh.n = (uint8_t)n;
+        nh.ncap = (uint8_t)ncap;
+        nh.pad = 0;
+        nh.adj_cap = a.vacap[i];
+        g.hdr[u] = nh;
+        ThinHdr th;
+        th.bkt_off = bo;
+        th.n = (uint8_t)n;
+        th.flags = (dn >= g.hot_b ? 1 : 0) | (dn >= g.hot_m ? 2 : 0);
+        th.pad1 = 0;
+        g.thdr[u] = th;
+        if (g.nbt) g.nbo[u] = nb_pack(4 * aoff, nb_log2size(dn));
+    }
+}
+
+// small vertices (L <= CH): one warp each
+__global__ void __launch_bounds__(MT) k_bsp_rebuild(const BspArgs a) {
+    BSP_WARP_LOOP(i, a.nt) {
+        if (a.vL[i] > CH) continue;
+        RbLane r;
+        uint32_t fm, fd;
+        rebuild_classify(a, i, r, fm, fd);
+        if (fm | fd) {
+            // one ascending pass over the post-batch adjacency materialises new lists
+            // and finds the member of ONE groups
+            uint32_t cnt = 0, first = 0xFFFFFFFFu;
+            fill_scan(a.g, a.vaoff[i], 0, a.vL[i] - a.vN[i], fm, fd, r.moff, false, cnt, first);
+            if ((fd >> lane_id()) & 1u) r.one = first;
         }
-        uint32_t x_b, y_b;
-        group_view(kind_b, c_b, moff_b, od_b, dn, aoff, x_b, y_b);
-        const uint32_t aux_b = is_list(kind_b) ? cap_b : (kind_b == K_ONE ? one_b : 0u);
-        write_buckets(g.bkt, g.gcan, bo, n, lane, kb, kind_b, c_b, x_b, y_b, aux_b, thr, alias, T);
-        if (lane == 0) {
-            VHdr nh;
-            nh.T = T;
-            nh.adj_off = aoff;
-            nh.bkt_off = bo;
-            nh.d = dn;
-            nh.n = (uint8_t)n;
-            nh.ncap = (uint8_t)ncap;
-            nh.pad = 0;
-            nh.adj_cap = a.vacap[i];
-            g.hdr[u] = nh;
-            ThinHdr th;
-            th.bkt_off = bo;
-            th.n = (uint8_t)n;
-            th.flags = (dn >= g.hot_b ? 1 : 0) | (dn >= g.hot_m ? 2 : 0);
-            th.pad1 = 0;
-            g.thdr[u] = th;
-            if (g.nbt) g.nbo[u] = nb_pack(4 * aoff, nb_log2size(dn));
+        rebuild_write(a, i, r);
+    }
+}
+
+// large vertices (L > CH): one 1024-thread block each; the fill/find scan is split
+// over the 32 warps (count pass, per-group scan over warps, write pass)
+__global__ void __launch_bounds__(LT) k_bsp_rebuild_big(const BspArgs a) {
+    __shared__ RbLane s_r[32];
+    __shared__ uint32_t s_fm, s_fd;
+    __shared__ uint32_t s_cnt[32][33];     // [warp][group], then exclusive prefixes
+    __shared__ uint32_t s_first[32][33];
+    const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
+    for (uint32_t h = blockIdx.x; h < *a.nbigs; h += gridDim.x) {
+        const uint32_t i = a.bigs[h];
+        if (w == 0) {
+            RbLane r;
+            uint32_t fm, fd;
+            rebuild_classify(a, i, r, fm, fd);
+            s_r[lane] = r;
+            if (lane == 0) { s_fm = fm; s_fd = fd; }
         }
+        __syncthreads();
+        const uint32_t fm = s_fm, fd = s_fd;
+        if (fm | fd) {
+            const uint32_t dn = a.vL[i] - a.vN[i];
+            const uint64_t aoff = a.vaoff[i];
+            const uint32_t seg = ((dn + 32 * 32 - 1) / (32 * 32)) * 32;   // positions per warp, multiple of 32
+            const uint32_t pb = min(dn, w * seg), pe = min(dn, pb + seg);
+            const uint32_t moff_l = s_r[lane].moff;
+            uint32_t cnt = 0, first = 0xFFFFFFFFu;
+            fill_scan(a.g, aoff, pb, pe, fm, 0u, moff_l, true, cnt, first);
+            s_cnt[w][lane] = cnt;
+            __syncthreads();
+            if (w == 0) {
+                uint32_t acc = 0;
+                for (uint32_t j = 0; j < 32; j++) {
+                    const uint32_t c = s_cnt[j][lane];
+                    s_cnt[j][lane] = acc;
+                    acc += c;
+                }
+            }
+            __syncthreads();
+            cnt = s_cnt[w][lane];
+            first = 0xFFFFFFFFu;
+            fill_scan(a.g, aoff, pb, pe, fm, fd, moff_l, false, cnt, first);
+            s_first[w][lane] = first;
+            __syncthreads();
+            if (w == 0 && ((fd >> lane) & 1u)) {
+                uint32_t f = 0xFFFFFFFFu;
+                for (uint32_t j = 0; j < 32; j++) f = min(f, s_first[j][lane]);
+                s_r[lane].one = f;
+            }
+            __syncthreads();
+        }
+        if (w == 0) rebuild_write(a, i, s_r[lane]);
+        __syncthreads();
     }
 }
 
