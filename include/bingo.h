@@ -70,6 +70,9 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
  *   sampled probabilities are within 1e-6 relative of w/sum(w) (R-15).
  *   Float-mode graphs are static in this version: bingo_apply_updates returns
  *   BINGO_E_INVAL.  Exports append a per-vertex decimal trailer (R-11).
+ *   BINGO_BUILD_ID_LAYOUT lays the pools out in vertex-id order instead of the
+ *   default hot-first order (descending out-degree): a performance choice
+ *   only, invisible in every result and export.
  * arc_slack / member_slack: fraction of extra per-vertex capacity reserved
  *   for growth (Hornet-style dynamic arrays + memory pool);
  *   pool_reserve: extra fraction of every pool for relocations.
@@ -82,6 +85,7 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
 #define BINGO_BUILD_BS_MODE 1u
 #define BINGO_BUILD_NEIGHBOR_INDEX 2u /* keep per-vertex neighbour hash sets: O(1) node2vec distance test */
 #define BINGO_BUILD_FLOAT_BIAS 4u     /* biases come from bias_f64 (S4.3 floating-point extension, R-15) */
+#define BINGO_BUILD_ID_LAYOUT 8u      /* pools in vertex-id order (default: hot-first) */
 
 typedef void *(*bingo_alloc_fn)(size_t bytes, void *ctx);
 typedef void (*bingo_free_fn)(void *ptr, void *ctx);

@@ -132,6 +132,10 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 }  // namespace bingo
 
+// walker-claim counters: each walk launch takes the next of these slots (zeroed on its
+// stream), so up to BINGO_WALK_SLOTS launches may run concurrently on one graph.
+#define BINGO_WALK_SLOTS 64
+
 // ---------------------------------------------------------------- graph object
 struct bingo_graph {
     uint32_t V = 0;
@@ -168,6 +172,8 @@ struct bingo_graph {
     uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
     unsigned long long *visit = nullptr;     // [V] PPR visit counts
+    unsigned long long *walk_ctr = nullptr;  // [BINGO_WALK_SLOTS] walker-claim counters (counters + 16)
+    uint32_t walk_slot = 0;                  // next claim-counter slot (host, atomic increment)
     int *dev_flag = nullptr;                 // device error flag
 
     // update-side scratch (grown on demand)

@@ -20,6 +20,7 @@
 #include "build_common.cuh"
 #include "nbr_index.cuh"
 #include "scan.cuh"
+#include "sort.cuh"
 
 using namespace bingo;
 
@@ -86,7 +87,7 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
                              const uint32_t *__restrict__ bias, uint32_t alpha, uint32_t beta, bool bs,
                              double mem_slack, const uint64_t *__restrict__ off_arc,
                              const uint64_t *__restrict__ off_bkt, const uint64_t *__restrict__ off_mem,
-                             VHdr *__restrict__ hdr, ThinHdr *__restrict__ thdr, uint2 *__restrict__ arc,
+                             const uint64_t *__restrict__ sz_arc, VHdr *__restrict__ hdr, ThinHdr *__restrict__ thdr, uint2 *__restrict__ arc,
                              uint32_t *__restrict__ arc_epoch, Bucket *__restrict__ bkt, GCan *__restrict__ gcan,
                              uint32_t *__restrict__ mdst, uint32_t *__restrict__ midx, uint32_t hot_b,
                              uint32_t hot_m) {
@@ -189,7 +190,7 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
             h.n = (uint8_t)n;
             h.ncap = (uint8_t)bucket_capacity(n);
             h.pad = 0;
-            h.adj_cap = (uint32_t)(off_arc[u + 1] - aoff);
+            h.adj_cap = (uint32_t)sz_arc[u];
             hdr[u] = h;
             ThinHdr th;
             th.bkt_off = (uint32_t)bo;
@@ -199,6 +200,29 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
             thdr[u] = th;
         }
     }
+}
+
+// Hot-first pool layout: vertices in descending out-degree (ties by id, a stable
+// sort) get the lowest offsets of every pool.  Walk visits are degree-skewed, so
+// the buckets, member lists and arcs that serve most steps share a few 2 MB pages:
+// random access on B200 is bound by address translation once a footprint outgrows
+// the TLB reach (~128-256 MB, profiles/r01_tlb_sweep.json), and this keeps the hot
+// part of the graph inside it.  Offsets are internal; every export is canonical.
+__global__ void k_hot_keys(uint32_t V, const uint64_t *__restrict__ ro, uint32_t *__restrict__ key,
+                           uint32_t *__restrict__ val) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
+        key[u] = ~(uint32_t)(ro[u + 1] - ro[u]);
+        val[u] = u;
+    }
+}
+__global__ void k_perm_gather(uint32_t V, const uint32_t *__restrict__ perm, const uint64_t *__restrict__ in,
+                              uint64_t *__restrict__ out) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < V; j += gridDim.x * blockDim.x) out[j] = in[perm[j]];
+}
+__global__ void k_perm_scatter(uint32_t V, const uint32_t *__restrict__ perm, const uint64_t *__restrict__ in,
+                               uint64_t *__restrict__ out) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j <= V; j += gridDim.x * blockDim.x)
+        out[j < V ? perm[j] : V] = in[j];
 }
 
 // neighbour hash sets (node2vec distance test), warp per vertex
@@ -313,8 +337,14 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     uint32_t *ibias = nullptr;
     uint64_t *dcnt = nullptr, *dscan = nullptr, total_dec = 0;
     const unsigned blocks = (unsigned)std::min<uint64_t>((nV + 7) / 8, 148ull * 64);
+    // pool layout: hot-first (default) or vertex-id order (BINGO_BUILD_ID_LAYOUT / env BINGO_LAYOUT=id, A/B)
+    const char *lay = getenv("BINGO_LAYOUT");
+    const bool hot_layout = !(desc->flags & BINGO_BUILD_ID_LAYOUT) && !(lay && strcmp(lay, "id") == 0);
+    uint32_t *pk = nullptr;
+    uint64_t *rtmp = nullptr, *pbuf = nullptr;
 
-    g->counters = (unsigned long long *)bingo_dev_alloc(g, 16 * sizeof(unsigned long long));
+    g->counters = (unsigned long long *)bingo_dev_alloc(g, (16 + BINGO_WALK_SLOTS) * sizeof(unsigned long long));
+    g->walk_ctr = g->counters ? g->counters + 16 : nullptr;
     g->dev_flag = (int *)bingo_dev_alloc(g, sizeof(int) * 4);
     g->hdr = (VHdr *)bingo_dev_alloc(g, sizeof(VHdr) * std::max<uint64_t>(nV, 1));
     g->thdr = (ThinHdr *)bingo_dev_alloc(g, sizeof(ThinHdr) * std::max<uint64_t>(nV, 1));
@@ -323,6 +353,12 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     off = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (nV + 1));
     tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * tmpw);
     dhist = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * 2 * HOT_BINS);
+    if (hot_layout && nV) {
+        pk = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * nV);
+        rtmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * radix_tmp_words(nV));
+        pbuf = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 2 * (nV + 1));
+        if (!pk || !rtmp || !pbuf) { st = BINGO_E_NOMEM; goto done; }
+    }
     if (!g->counters || !g->dev_flag || !g->hdr || !g->thdr || !g->visit || !sz || !off || !tmp || !dhist) {
         st = BINGO_E_NOMEM;
         goto done;
@@ -354,7 +390,26 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
                                              g->dev_flag, dhist, fm);
         bingo_count_launch();
         CK(cudaGetLastError());
-        for (int p = 0; p < 3; p++) CK(exclusive_scan_u64(sz + p * (nV + 1), off + p * (nV + 1), nV, tmp, s));
+        if (hot_layout) {
+            const unsigned eg = (unsigned)std::min<uint64_t>((nV + 255) / 256, 148ull * 16);
+            k_hot_keys<<<eg, 256, 0, s>>>(V, desc->row_offsets, pk, pk + nV);
+            bingo_count_launch();
+            CK(cudaGetLastError());
+            bool in1 = false;
+            CK(radix_sort_pairs(pk, pk + nV, pk + 2 * nV, pk + 3 * nV, nV, 32, rtmp, s, &in1));
+            const uint32_t *perm = in1 ? pk + 3 * nV : pk + nV;
+            for (int p = 0; p < 3; p++) {
+                k_perm_gather<<<eg, 256, 0, s>>>(V, perm, sz + p * (nV + 1), pbuf);
+                bingo_count_launch();
+                CK(cudaGetLastError());
+                CK(exclusive_scan_u64(pbuf, pbuf + (nV + 1), nV, tmp, s));
+                k_perm_scatter<<<eg, 256, 0, s>>>(V, perm, pbuf + (nV + 1), off + p * (nV + 1));
+                bingo_count_launch();
+                CK(cudaGetLastError());
+            }
+        } else {
+            for (int p = 0; p < 3; p++) CK(exclusive_scan_u64(sz + p * (nV + 1), off + p * (nV + 1), nV, tmp, s));
+        }
         CK(cudaMemcpyAsync(&hflag, g->dev_flag, sizeof(int), cudaMemcpyDeviceToHost, s));
         for (int p = 0; p < 3; p++)
             CK(cudaMemcpyAsync(&tot[p], off + p * (nV + 1) + nV, sizeof(uint64_t), cudaMemcpyDeviceToHost, s));
@@ -382,7 +437,7 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     CK(cudaMemcpyAsync(g->counters, hc, sizeof(hc), cudaMemcpyHostToDevice, s));
     if (V) {
         k_build_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, idesc.bias, g->alpha, g->beta, bs,
-                                            g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), g->hdr, g->thdr,
+                                            g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), sz, g->hdr, g->thdr,
                                             g->arc, g->arc_epoch, g->bkt, g->gcan, g->mdst, g->midx,
                                             g->hot_bkt_degree, g->hot_mem_degree);
         bingo_count_launch();
@@ -413,6 +468,9 @@ done:
     bingo_dev_free(g, off);
     bingo_dev_free(g, tmp);
     bingo_dev_free(g, dhist);
+    bingo_dev_free(g, pk);
+    bingo_dev_free(g, rtmp);
+    bingo_dev_free(g, pbuf);
     bingo_dev_free(g, ibias);
     bingo_dev_free(g, dcnt);
     bingo_dev_free(g, dscan);

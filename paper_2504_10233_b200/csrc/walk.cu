@@ -1,7 +1,7 @@
 // walk.cu -- the batched walker step.
 //
-// One walker per lane, warps of 32 consecutive walkers, a grid-stride loop over
-// walkers with the whole walk kept in registers.  Each step is a chain of
+// One walker per lane at a time, a persistent grid whose lanes claim walker ids
+// dynamically (k_walk below), the whole walk kept in registers.  Each step is a chain of
 // dependent 32 B sector loads through the read-only path:
 //   VHdr[u] -> Bucket[bkt_off + b] -> (member | arc per dense attempt)
 // and one coalesced, streaming (evict-first) store of the path column.
@@ -21,11 +21,32 @@ using namespace bingo;
 namespace bingo {
 
 template <int APP, bool PROF, bool WMAJOR>
+__device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint32_t &w, uint32_t &u) {
+    w = a.first_walker + (uint32_t)i;
+    u = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);
+    if (a.paths) {
+        if (WMAJOR) a.paths[i * ((size_t)a.L + 1)] = u;
+        else __stcs(&a.paths[i], u);
+    }
+    if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[u], 1ull);
+}
+
 #ifndef BINGO_WALK_MINB
 #define BINGO_WALK_MINB 5
 #endif
-__global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BINGO_WALK_MINB) k_walk(const WalkArgs a) {
-    const uint32_t stride = gridDim.x * blockDim.x;
+// Each lane owns one walker at a time and every loop iteration advances every
+// active lane by one step (node2vec: one proposal).  A lane whose walker ends
+// (length reached, dead end, PPR stop) claims the next walker id at once from a
+// per-launch counter (one warp-aggregated atomic per iteration in which some lane
+// finished), so lanes never wait for the longest walk of their warp (PPR's
+// geometric lengths, node2vec rejections, dead ends) and no SM idles while others
+// still hold walkers (the static walker-to-thread split left ~20% of SM cycles
+// idle at the tail).  DeepWalk lanes finish together, so a warp claims 32
+// consecutive ids and the step-major path stores stay coalesced.  Results depend
+// only on the walker id (R-1), never on which lane ran it.
+template <int APP, bool PROF, bool WMAJOR>
+__global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BINGO_WALK_MINB)
+    k_walk(const WalkArgs a, unsigned long long *__restrict__ claim) {
     WalkProf prof;
     // L2 eviction priorities: the thin headers are re-read by every step of every
     // walker (keep), member/arc sectors are one-shot random reads (stream).
@@ -39,64 +60,101 @@ __global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BIN
 #endif
     const Policies pol{pol_keep, pol_stream};
     const size_t row = (size_t)a.L + 1;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < a.W; i += stride) {
-        const uint32_t w = a.first_walker + i;
-        uint32_t u = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);
-        if (a.paths) {
-            if (WMAJOR) a.paths[(size_t)i * row] = u;
-            else __stcs(&a.paths[i], u);
-        }
-        if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[u], 1ull);
-        uint32_t steps = 0, prev = 0xFFFFFFFFu;
-        uint64_t prev_nbo = 0, cur_nbo = 0;
-        for (uint32_t t = 0; a.L == BINGO_NO_CAP || t < a.L; t++) {
-            const ThinHdr h = load_thdr(a.thdr + u, pol);
-            if (APP == BINGO_NODE2VEC && a.nbo) cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
-            DecRec dr;
-            dr.dcnt = 0;
-            if (a.dec) dr = load_dec(a.dec + u);
-            if (PROF) prof.hdr++;
-            if (h.n == 0 && dr.dcnt == 0) break;   // dead end (d = 0): truncate (R-13)
-            uint32_t next;
-            if (APP == BINGO_NODE2VEC && t >= 1) {
-                // KnightKing rejection: propose first-order, accept with f/f_max
-                for (uint32_t o = 0;; o++) {
-                    next = a.dec ? sample_dst_f<PROF>(a, h, dr, w, t, o, prof, pol)
-                                 : sample_dst<PROF>(a, h, w, t, o, prof, pol);
-                    const uint32_t cls = (next == prev) ? 0u : (probe_arc<PROF>(a, prev, prev_nbo, next, prof) ? 1u : 2u);
-                    if (a.n2v_always[cls]) break;
-                    const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
-                    if (join64(r.x, r.y) < a.n2v_thr[cls]) break;
-                }
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
+    uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;   // first walker: static
+    bool active = i < a.W;
+    uint32_t w = 0, u = 0, t = 0, o = 0, prev = 0xFFFFFFFFu;
+    uint64_t prev_nbo = 0, cur_nbo = 0;
+    ThinHdr h;
+    DecRec dr;
+    dr.dcnt = 0;
+    if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u);
+    for (;;) {
+        bool fin = false;
+        if (active) {
+            if (a.L != BINGO_NO_CAP && t >= a.L) {
+                fin = true;                                   // L = 0
             } else {
-                next = a.dec ? sample_dst_f<PROF>(a, h, dr, w, t, 0, prof, pol)
-                             : sample_dst<PROF>(a, h, w, t, 0, prof, pol);
+                if (APP != BINGO_NODE2VEC || o == 0) {        // node2vec keeps u's header across proposals
+                    h = load_thdr(a.thdr + u, pol);
+                    if (APP == BINGO_NODE2VEC && a.nbo)
+                        cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
+                    if (a.dec) dr = load_dec(a.dec + u);
+                    if (PROF) prof.hdr++;
+                }
+                if (h.n == 0 && dr.dcnt == 0) {
+                    fin = true;                               // dead end (d = 0): truncate (R-13)
+                } else {
+                    const uint32_t next = a.dec ? sample_dst_f<PROF>(a, h, dr, w, t, o, prof, pol)
+                                                : sample_dst<PROF>(a, h, w, t, o, prof, pol);
+                    bool accept = true;
+                    if (APP == BINGO_NODE2VEC && t >= 1) {
+                        // KnightKing rejection: propose first-order, accept with f/f_max;
+                        // a rejected proposal re-draws everything under outer attempt o + 1 (R-14)
+                        const uint32_t cls =
+                            (next == prev) ? 0u : (probe_arc<PROF>(a, prev, prev_nbo, next, prof) ? 1u : 2u);
+                        if (!a.n2v_always[cls]) {
+                            const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
+                            accept = join64(r.x, r.y) < a.n2v_thr[cls];
+                        }
+                    }
+                    if (!accept) {
+                        o++;
+                    } else {
+                        if (PROF) prof.steps++;
+                        if (a.paths) {
+                            if (WMAJOR) a.paths[i * row + t + 1] = next;
+                            else __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
+                        }
+                        prev = u;
+                        prev_nbo = cur_nbo;
+                        u = next;
+                        o = 0;
+                        if (APP == BINGO_PPR) {
+                            if (a.visit) atomicAdd(&a.visit[u], 1ull);
+                            if (PROF) prof.visit++;
+                            if (a.stop_always) {
+                                fin = true;
+                            } else {
+                                const P4 r = philox10(w, t, 0u, 3u, a.k0, a.k1);
+                                fin = join64(r.x, r.y) < a.stop_thr;
+                            }
+                        }
+                        t++;
+                        if (a.L != BINGO_NO_CAP && t >= a.L) fin = true;
+                    }
+                }
             }
-            steps++;
-            if (PROF) prof.steps++;
-            if (a.paths) {
-                if (WMAJOR) a.paths[(size_t)i * row + t + 1] = next;
-                else __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
-            }
-            prev = u;
-            prev_nbo = cur_nbo;
-            u = next;
-            if (APP == BINGO_PPR) {
-                if (a.visit) atomicAdd(&a.visit[u], 1ull);
-                if (PROF) prof.visit++;
-                if (a.stop_always) break;
-                const P4 r = philox10(w, t, 0u, 3u, a.k0, a.k1);
-                if (join64(r.x, r.y) < a.stop_thr) break;
+            if (fin) {
+                if (PROF) prof.walkers++;
+                if (a.lengths) a.lengths[i] = t;
+                if (a.paths && a.L != BINGO_NO_CAP) {
+                    for (uint32_t s = t + 1; s <= a.L; s++) {
+                        if (WMAJOR) a.paths[i * row + s] = 0xFFFFFFFFu;
+                        else __stcs(&a.paths[(size_t)s * a.W + i], 0xFFFFFFFFu);
+                    }
+                }
             }
         }
-        if (PROF) prof.walkers++;
-        if (a.lengths) a.lengths[i] = steps;
-        if (a.paths && a.L != BINGO_NO_CAP) {
-            for (uint32_t t = steps + 1; t <= a.L; t++) {
-                if (WMAJOR) a.paths[(size_t)i * row + t] = 0xFFFFFFFFu;
-                else __stcs(&a.paths[(size_t)t * a.W + i], 0xFFFFFFFFu);
+        // refill: the lanes that finished claim consecutive walker ids in lane order
+        const unsigned fmask = __ballot_sync(0xffffffffu, fin);
+        if (fmask) {
+            const uint32_t leader = __ffs(fmask) - 1;
+            unsigned long long base = 0;
+            if (lane == leader) base = atomicAdd(claim, (unsigned long long)__popc(fmask));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (fin) {
+                i = nthreads + base + __popc(fmask & ((1u << lane) - 1u));
+                active = i < a.W;
+                t = 0;
+                o = 0;
+                prev = 0xFFFFFFFFu;
+                prev_nbo = cur_nbo = 0;
+                if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u);
             }
         }
+        if (!__any_sync(0xffffffffu, active)) break;
     }
     if (PROF) prof.flush(a.prof);
 }
@@ -172,6 +230,12 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
                    a.n2v_thr, a.n2v_always);
     stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
     a.prof = prof;
+    if (!g->walk_ctr) return BINGO_E_STATE;
+    unsigned long long *claim = g->walk_ctr + (__atomic_fetch_add(&g->walk_slot, 1u, __ATOMIC_RELAXED) % BINGO_WALK_SLOTS);
+    if (cudaMemsetAsync(claim, 0, sizeof(unsigned long long), s) != cudaSuccess) {
+        g->poisoned = 1;
+        return BINGO_E_CUDA;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(1);
     cfg.blockDim = dim3(256);
@@ -183,9 +247,9 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     const bool wmajor = (desc->flags & BINGO_WALK_WALKER_MAJOR) != 0;
 #define BINGO_K(APP_, PROF_)                                                                      \
     (wmajor ? (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, true>, W)),                       \
-               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, true>, a))                            \
+               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, true>, a, claim))                            \
             : (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, false>, W)),                      \
-               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, false>, a)))
+               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, false>, a, claim)))
     if (prof) {
         switch (desc->app) {
             case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, true); break;

@@ -130,6 +130,52 @@ extern "C" int gather_run(void *buf, uint64_t nslots, int mode, uint32_t blocks,
     return (int)cudaGetLastError();
 }
 
+
+// TLB-reach experiment: nslots logical 32 B slots, slot s placed at 128 B line
+// s * spread_lines + (hash(s) mod spread_lines) of a buffer of nslots * spread_lines
+// lines.  The set of touched lines (and so the L2 footprint) is the same for every
+// spread; only the number of 2 MB pages they are scattered over changes.
+__device__ __forceinline__ uint64_t spread_line(uint64_t s, uint64_t spread) {
+    return s * spread + (spread > 1 ? (mix64(s * 0x2545F4914F6CDD1Dull) % spread) : 0);
+}
+__global__ void gb_fill_spread(uint4 *buf, uint64_t nslots, uint64_t spread, uint64_t seed) {
+    for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s < nslots; s += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t nx = mix64(s ^ seed) & (nslots - 1);
+        const uint64_t ln = spread_line(nx, spread);
+        const uint64_t me = spread_line(s, spread);
+        buf[8 * me] = make_uint4((uint32_t)ln, (uint32_t)(ln >> 32), (uint32_t)s, 0u);
+    }
+}
+__global__ void gb_chase_spread(const uint4 *__restrict__ buf, uint64_t nslots, uint64_t spread, uint32_t steps,
+                                uint64_t seed, uint32_t *out) {
+    const uint64_t tid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+    uint64_t cur = spread_line(mix64(tid + seed) & (nslots - 1), spread);
+    uint32_t acc = 0;
+    for (uint32_t it = 0; it < steps; it++) {
+        const uint4 v = __ldg(buf + 8 * cur);
+        cur = ((uint64_t)v.y << 32) | v.x;
+        acc ^= v.z;
+    }
+    if (acc == 0x12345678u) out[0] = (uint32_t)cur;
+}
+extern "C" int gather_spread(void *buf, uint64_t nslots, uint64_t spread, uint32_t blocks, uint32_t threads,
+                             uint32_t iters, uint64_t seed, void *scratch, float *ms, void *stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    gb_fill_spread<<<148 * 8, 256, 0, s>>>((uint4 *)buf, nslots, spread, 12345);
+    gb_chase_spread<<<blocks, threads, 0, s>>>((const uint4 *)buf, nslots, spread, iters, seed + 1, (uint32_t *)scratch);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, s);
+    gb_chase_spread<<<blocks, threads, 0, s>>>((const uint4 *)buf, nslots, spread, iters, seed, (uint32_t *)scratch);
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return (int)cudaGetLastError();
+}
+
 // L2 fetch-granularity limit (cudaLimitMaxL2FetchGranularity): returns the value in effect.
 extern "C" int gather_set_l2_fetch(int bytes) {
     if (bytes >= 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)bytes);
