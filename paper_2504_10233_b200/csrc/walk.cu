@@ -32,7 +32,10 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
 }
 
 #ifndef BINGO_WALK_MINB
-#define BINGO_WALK_MINB 5
+#define BINGO_WALK_MINB 2
+#endif
+#ifndef BINGO_N2V_MINB
+#define BINGO_N2V_MINB 2
 #endif
 // Each lane owns one walker at a time and every loop iteration advances every
 // active lane by one step (node2vec: one proposal).  A lane whose walker ends
@@ -45,7 +48,7 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
 // consecutive ids and the step-major path stores stay coalesced.  Results depend
 // only on the walker id (R-1), never on which lane ran it.
 template <int APP, bool PROF, bool WMAJOR>
-__global__ void __launch_bounds__(256, (APP == BINGO_NODE2VEC || PROF) ? 4 : BINGO_WALK_MINB)
+__global__ void __launch_bounds__(256, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO_N2V_MINB : BINGO_WALK_MINB))
     k_walk(const WalkArgs a, unsigned long long *__restrict__ claim) {
     WalkProf prof;
     // L2 eviction priorities: the thin headers are re-read by every step of every

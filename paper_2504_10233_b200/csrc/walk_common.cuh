@@ -128,21 +128,42 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
     if (kind == K_DENSE) return y & 0xFFFFFu;
 #endif
     if (kind == K_ONE) return y;
+    // the first intra-group draw (tag 1, inner 0) is the same for list and dense
+    // groups: computed once, before the branch, so a warp whose lanes hold both
+    // kinds does not run it twice
+#ifdef BINGO_NO_HOIST            // A/B experiment switch: the draw inside each branch
     if (kind != K_DENSE) {
-        const P4 q = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
-        const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)x);
+        const P4 q0 = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
+        const uint64_t j0 = __umul64hi(join64(q0.x, q0.y), (uint64_t)x);
         if (PROF) prof.mem++;
-        return ldg4(a.mdst + (uint64_t)y * 4 + j, (h.flags & 2u) ? pol.keep : pol.stream);
+        return ldg4(a.mdst + (uint64_t)y * 4 + j0, (h.flags & 2u) ? pol.keep : pol.stream);
     }
+    const P4 q0 = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
+    const uint64_t j0 = __umul64hi(join64(q0.x, q0.y), (uint64_t)x);
+#else
+    const P4 q0 = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
+    const uint64_t j0 = __umul64hi(join64(q0.x, q0.y), (uint64_t)x);
+    if (kind != K_DENSE) {
+        if (PROF) prof.mem++;
+        return ldg4(a.mdst + (uint64_t)y * 4 + j0, (h.flags & 2u) ? pol.keep : pol.stream);
+    }
+#endif
     const uint32_t k = kk & 31u;
     const uint2 *adj = a.arc + ((uint64_t)y << 2);
     for (uint32_t base = 0;; base += BINGO_DENSE_SPEC) {
         uint2 e[BINGO_DENSE_SPEC];
 #pragma unroll
         for (int s = 0; s < BINGO_DENSE_SPEC; s++) {
-            const P4 q = philox10(w, t, (outer << 16) + base + s, 1u, a.k0, a.k1);
-            const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)x);
+            uint64_t j = j0;
+            if (base + s) {
+                const P4 q = philox10(w, t, (outer << 16) + base + s, 1u, a.k0, a.k1);
+                j = __umul64hi(join64(q.x, q.y), (uint64_t)x);
+            }
+            #ifdef BINGO_ARC_STREAM          // A/B experiment switch: dense arc reads always evict_first
             e[s] = ldg8(adj + j, pol.stream);
+#else
+            e[s] = ldg8(adj + j, (h.flags & 2u) ? pol.keep : pol.stream);
+#endif
         }
         bool done = false;
         uint32_t res = 0;
