@@ -169,6 +169,7 @@ struct bingo_graph {
     uint64_t dmem_cap = 0;
     uint32_t *nbt = nullptr;           // [4 * arc_cap] neighbour hash sets (node2vec), optional
     uint64_t *nbo = nullptr;           // [V] hash-set base | log2 size << 48
+    uint32_t *nbtomb = nullptr;        // [V] tombstones in each hash set (incremental updates)
     uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
     unsigned long long *visit = nullptr;     // [V] PPR visit counts

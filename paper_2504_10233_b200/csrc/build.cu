@@ -455,7 +455,9 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     if (desc->flags & BINGO_BUILD_NEIGHBOR_INDEX) {
         g->nbt = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * g->arc_cap);
         g->nbo = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * std::max<uint64_t>(nV, 1));
-        if (!g->nbt || !g->nbo) { st = BINGO_E_NOMEM; goto done; }
+        g->nbtomb = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * std::max<uint64_t>(nV, 1));
+        if (!g->nbt || !g->nbo || !g->nbtomb) { st = BINGO_E_NOMEM; goto done; }
+        CK(cudaMemsetAsync(g->nbtomb, 0, sizeof(uint32_t) * std::max<uint64_t>(nV, 1), s));
         if (V) {
             k_build_nbt<<<blocks, 256, 0, s>>>(V, g->hdr, g->arc, g->nbt, g->nbo);
             bingo_count_launch();

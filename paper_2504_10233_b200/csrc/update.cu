@@ -315,6 +315,7 @@ struct MutateArgs {
     uint32_t *mdst, *midx;
     uint32_t *nbt;
     uint64_t *nbo;
+    uint32_t *nbtomb;
     unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units
     uint32_t *vstats;           // [ntouch][VST]
     uint32_t epoch, alpha, beta, hot_b, hot_m;
@@ -820,7 +821,10 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
         for (uint32_t j = tid; j < (1u << lg); j += GT) tbl[j] = NB_EMPTY;
         G::sync();
         for (uint32_t i = tid; i < dn; i += GT) nb_insert(tbl, (1u << lg) - 1, a.arc[aoff + i].x);
-        if (tid == 0) a.nbo[u] = nb_pack(4 * aoff, lg);
+        if (tid == 0) {
+            a.nbo[u] = nb_pack(4 * aoff, lg);
+            a.nbtomb[u] = 0;
+        }
     }
 }
 
@@ -1131,6 +1135,7 @@ static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
     ma.midx = g->midx;
     ma.nbt = g->nbt;
     ma.nbo = g->nbo;
+    ma.nbtomb = g->nbtomb;
     ma.bump = g->counters;
     ma.epoch = e;
     ma.alpha = g->alpha;
@@ -1263,6 +1268,8 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         add(sizeof(BspTotals));
         add(4 * ntmax);
         add(4 * ntmax);
+        add(8 * ntmax);
+        add(4 * ntmax);
         add(64);
         vb += 4096;
     }
@@ -1304,6 +1311,8 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     BspTotals *dt = cv.take<BspTotals>(1);
     a.hubs = cv.take<uint32_t>(ntmax);
     a.bigs = cv.take<uint32_t>(ntmax);
+    a.vnbo = cv.take<uint64_t>(ntmax);
+    a.vnbfull = cv.take<uint32_t>(ntmax);
     a.nhubs = cv.take<uint32_t>(16);
     a.nbigs = a.nhubs + 1;
     auto refresh = [&]() {
@@ -1427,6 +1436,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             UCK(cudaEventRecord(g->ev_join, sh));
             UCK(cudaStreamWaitEvent(s, g->ev_join, 0));
         }
+        if (g->nbt) BSP_LAUNCH(k_bsp_nb_incr, warp_grid(nt, WG), s, a);
         if (g->nbt && all) {
             BSP_LAUNCH(k_bsp_nb_clear, warp_grid(all, IG), s, a, all);
             BSP_LAUNCH(k_bsp_nb_fill, warp_grid(all, IG), s, a, all);
@@ -1580,6 +1590,7 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     ma.midx = g->midx;
     ma.nbt = g->nbt;
     ma.nbo = g->nbo;
+    ma.nbtomb = g->nbtomb;
     ma.bump = g->counters;
     ma.vstats = vstats;
     ma.epoch = e;

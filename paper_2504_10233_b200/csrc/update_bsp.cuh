@@ -48,6 +48,8 @@ struct BspArgs {
     const uint64_t *gpref;
     uint32_t *hubs, *nhubs;        // large vertices (L > CH) with deletes, any order
     uint32_t *bigs, *nbigs;        // all large vertices, any order
+    uint64_t *vnbo;                // pre-batch nbo[u] (node2vec neighbour sets)
+    uint32_t *vnbfull;             // 1: the vertex's neighbour set is rebuilt from its adjacency
 };
 
 __device__ __forceinline__ uint32_t *gkp(const BspArgs &a, uint32_t f, uint32_t i) {
@@ -214,6 +216,7 @@ __global__ void __launch_bounds__(MT) k_bsp_alloc_insert(const BspArgs a) {
             a.vacap[i] = acap;
             a.vN[i] = 0;
             a.vmiss[i] = 0;
+            if (g.nbt) a.vnbo[i] = g.nbo[g.tv[t]];
         }
         if (aoff != h.adj_off && h.d <= CH) {
             // small relocation: copied here (larger ones by k_bsp_copy items)
@@ -954,11 +957,62 @@ __global__ void __launch_bounds__(LT) k_bsp_rebuild_big(const BspArgs a) {
 }
 
 // ------------------------------------------------------------------ node2vec neighbour sets of touched vertices
+// Incremental when the set keeps its base and size (no relocation, same
+// log2 size) and its tombstones stay <= size / 4: inserted destinations are
+// added, a destination whose every live instance this batch deleted (all found
+// instances selected, hsel = hfound > 0) is tombstoned.  Otherwise the vertex is
+// flagged for the full rebuild by the chunk items below.
+__global__ void __launch_bounds__(MT) k_bsp_nb_incr(const BspArgs a) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(i, a.nt) {
+        const uint32_t t = a.t0 + i;
+        const uint32_t u = g.tv[t];
+        const uint32_t L = a.vL[i], q = a.vq[i];
+        const uint32_t dn = L - a.vN[i];
+        const uint32_t lg = nb_log2size(dn);
+        const uint64_t base = 4 * a.vaoff[i];
+        const uint64_t old = a.vnbo[i];
+        uint32_t tomb = g.nbtomb[u];
+        bool full = nb_base(old) != base || (uint32_t)(old >> 48) != lg;
+        DelScr s;
+        uint32_t rem = 0;
+        if (!full && q) {
+            s = del_scr(g.scr + g.scr_off[i], L, q);
+            for (uint32_t sl = lane; sl < s.Hq; sl += 32)
+                if (s.hkey[sl] != EMPTY_KEY && s.hfound[sl] && s.hsel[sl] == s.hfound[sl]) rem++;
+            rem = warp_sum(rem);
+            if (tomb + rem > (1u << lg) / 4) full = true;
+        }
+        if (lane == 0) a.vnbfull[i] = full ? 1u : 0u;
+        if (full) {
+            if (lane == 0) g.nbtomb[u] = 0;
+            continue;
+        }
+        uint32_t *tbl = g.nbt + base;
+        const uint32_t mask = (1u << lg) - 1;
+        for (uint32_t p = g.seg[t] + lane; p < g.seg[t + 1]; p += 32) {
+            const uint4 r = g.recs[g.sval[p]];
+            if (r.x == 0u) nb_insert(tbl, mask, r.z);
+        }
+        __syncwarp();
+        __threadfence_block();
+        uint32_t gone = 0;
+        if (q)
+            for (uint32_t sl = lane; sl < s.Hq; sl += 32)
+                if (s.hkey[sl] != EMPTY_KEY && s.hfound[sl] && s.hsel[sl] == s.hfound[sl])
+                    gone += nb_remove(tbl, mask, s.hkey[sl]) ? 1u : 0u;
+        gone = warp_sum(gone);
+        if (lane == 0) g.nbtomb[u] = tomb + gone;
+    }
+}
+
 __global__ void __launch_bounds__(MT) k_bsp_nb_clear(const BspArgs a, uint64_t total) {
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_ITEM_LOOP(it, total) {
         const uint32_t i = owner_of(a.p_all, a.nt, it);
+        if (!a.vnbfull[i]) continue;
         const uint32_t c = (uint32_t)(it - a.p_all[i]);
         const uint32_t dn = a.vL[i] - a.vN[i];
         const uint32_t size = 1u << nb_log2size(dn);
@@ -973,6 +1027,7 @@ __global__ void __launch_bounds__(MT) k_bsp_nb_fill(const BspArgs a, uint64_t to
     const MutateArgs &g = a.g;
     BSP_ITEM_LOOP(it, total) {
         const uint32_t i = owner_of(a.p_all, a.nt, it);
+        if (!a.vnbfull[i]) continue;
         const uint32_t c = (uint32_t)(it - a.p_all[i]);
         const uint32_t dn = a.vL[i] - a.vN[i];
         const uint32_t mask = (1u << nb_log2size(dn)) - 1;

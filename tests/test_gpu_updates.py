@@ -213,3 +213,52 @@ def test_small_batches_fast_path():
         b = np.array([(0, 5, (7 * i + j) % w.V, 1 + (i * 64 + j) % 300) for j in range(64)], dtype=np.uint32)
         _same_stats(g.apply_updates(b), o.apply_updates(b))
     _same(g, o, w.V, "after hub growth")
+
+
+@pytest.mark.parametrize("route", ["bsp", "bsp-sub", "legacy"])
+def test_node2vec_neighbour_index_across_batches(route, monkeypatch):
+    """The node2vec distance test (Eq.1, A-17) reads per-vertex neighbour sets that updates
+    maintain in place (inserted destinations added, a destination whose last live instance
+    is deleted tombstoned, rebuilt on relocation / size change / too many tombstones).
+    Multigraph with duplicate arcs and a hub; batches delete every copy of some
+    destinations, some copies of others, and re-insert removed ones.  Walks with the index
+    must equal the oracle's (which scans the adjacency) after every batch."""
+    for k, v in ROUTES[route].items():
+        monkeypatch.setenv(k, v)
+    rng = np.random.default_rng(77)
+    V = 300
+    deg = rng.integers(1, 12, size=V)
+    deg[0] = 900                               # hub: duplicates of ~300 destinations
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, V, size=A).astype(np.uint32)
+    bias = rng.integers(1, 300, size=A).astype(np.uint32)
+    g, o = _pair(ro, dst, bias, neighbor_index=True)
+    live = {u: list(dst[int(ro[u]):int(ro[u + 1])]) for u in range(V)}
+    removed = {u: [] for u in range(V)}
+    for e in range(1, 25):
+        recs = []
+        for _ in range(int(rng.integers(5, 40))):
+            u = 0 if rng.random() < 0.5 else int(rng.integers(0, V))
+            r = rng.random()
+            if r < 0.4 and live[u]:            # delete every copy of one destination
+                v = int(live[u][int(rng.integers(0, len(live[u])))])
+                recs += [(1, u, v, 0)] * live[u].count(v)
+                removed[u].append(v)
+            elif r < 0.6 and live[u]:          # delete one copy
+                recs.append((1, u, int(live[u][int(rng.integers(0, len(live[u])))]), 0))
+            elif r < 0.8 and removed[u]:       # re-insert a removed destination
+                recs.append((0, u, int(removed[u][int(rng.integers(0, len(removed[u])))]), int(rng.integers(1, 300))))
+            else:
+                recs.append((0, u, int(rng.integers(0, V)), int(rng.integers(1, 300))))
+        recs = np.array(recs, dtype=np.uint32)
+        _same_stats(g.apply_updates(recs), o.apply_updates(recs))
+        d = oracle.parse_dump(o.dump(), V)
+        live = {u: [a[0] for a in d[u]["adj"]] for u in range(V)}
+        if e % 4 == 0:
+            _same(g, o, V, f"batch {e}")
+        for p, q in ((2.0, 0.5), (0.5, 2.0)):
+            out = g.walk(app=_pb().NODE2VEC, length=20, p=p, q=q, seed=e)
+            ref = o.walk(app=oracle.APP_NODE2VEC, length=20, p=p, q=q, seed=e)
+            assert np.array_equal(u32(out["paths"]), ref["paths"]), f"{route} batch {e} p={p} q={q}"
