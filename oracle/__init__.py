@@ -70,6 +70,8 @@ def lib():
             L.ora_two_phase_u32.restype = u32
             L.ora_apply_updates.argtypes = [P, P, u64, P]
             L.ora_apply_updates.restype = ctypes.c_int
+            L.ora_apply_updates_f.argtypes = [P, P, P, u64, P]
+            L.ora_apply_updates_f.restype = ctypes.c_int
             L.ora_sample.argtypes = [P, u32, u64, u32, u32, u32]
             L.ora_sample.restype = u32
             L.ora_walk.argtypes = [P, u32, u32, u64, u32, P, u32, P, P, P, P, P, u64, u32,
@@ -171,19 +173,27 @@ class OracleGraph:
     def epoch(self) -> int:
         return int(lib().ora_epoch(self._h))
 
-    def apply_updates(self, recs) -> dict:
+    def apply_updates(self, recs, bias_f64=None) -> dict:
+        """Apply one batch; float-mode graphs take the inserted biases from bias_f64 (R-16)."""
         r = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 4)
         st = np.zeros(30, dtype=np.uint64)
-        rc = lib().ora_apply_updates(self._h, _p(r) if len(r) else None, len(r), _p(st))
+        rc = self._apply(r, bias_f64, st)
         if rc != 0:
             raise ValueError(f"ora_apply_updates failed with status {rc}")
         return {"inserted": int(st[0]), "deleted": int(st[1]), "missing_deletes": int(st[2]),
                 "touched_vertices": int(st[3]), "kind_transitions": st[4:29].reshape(5, 5).copy(),
                 "epoch": int(st[29])}
 
-    def try_apply_updates(self, recs) -> int:
+    def _apply(self, r, bias_f64, st):
+        if bias_f64 is None:
+            return int(lib().ora_apply_updates(self._h, _p(r) if len(r) else None, len(r), _p(st)))
+        wf = np.ascontiguousarray(bias_f64, dtype=np.float64)
+        return int(lib().ora_apply_updates_f(self._h, _p(r) if len(r) else None, _p(wf) if len(wf) else None,
+                                             len(r), _p(st)))
+
+    def try_apply_updates(self, recs, bias_f64=None) -> int:
         r = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 4)
-        return int(lib().ora_apply_updates(self._h, _p(r) if len(r) else None, len(r), None))
+        return self._apply(r, bias_f64, None)
 
     def sample(self, u, seed, w, t, outer=0) -> int:
         return int(lib().ora_sample(self._h, u, seed, w, t, outer))

@@ -88,6 +88,7 @@ static uint64_t mulhi64(uint64_t a, uint64_t b)
 /* ------------------------------------------------------------------ */
 typedef struct {
     uint32_t dst, bias, epoch;
+    uint64_t dval;     /* float mode: D = floor(frac(w lambda) 2^52) of this arc (R-15); 0 otherwise */
 } o_arc;
 
 typedef struct {
@@ -162,6 +163,7 @@ static o_vertex *vx(const ora_graph *Gc, uint32_t u)
                     x->adj[i].dst = G->ldst[G->lro[u] + i];
                     x->adj[i].bias = G->lbias[G->lro[u] + i];
                     x->adj[i].epoch = 0;
+                    x->adj[i].dval = 0;
                 }
                 build_vertex(G, x);
 #ifdef _OPENMP
@@ -324,6 +326,7 @@ int ora_build(uint32_t V, const uint64_t *row_offsets, const uint32_t *dst, cons
             x->adj[i].dst = dst[row_offsets[u] + i];
             x->adj[i].bias = bias[row_offsets[u] + i];
             x->adj[i].epoch = 0;
+            x->adj[i].dval = 0;
         }
         build_vertex(G, x);
     }
@@ -369,6 +372,40 @@ static uint64_t frac64(unsigned __int128 a, unsigned __int128 b)
     return q;
 }
 
+/* The decimal group of a float-mode vertex from its arcs (R-15): the arcs with
+ * D_i > 0 in ascending adjacency index, W_I = sum I_i (= T), W_D = sum D_i,
+ * thrD = floor(W_D 2^64 / (W_I 2^52 + W_D)) (always decimal when W_I = 0),
+ * flag bit 0 = the lambda constraint (d - 1) W_D < W_I 2^52 does not
+ * hold, bit 1 = the integer part is empty.  Used by the build and, with the
+ * vertex's lambda fixed, after every batch that touches the vertex. */
+static void decimal_group(o_vertex *x)
+{
+    unsigned __int128 WI = 0, WD = 0;
+    free(x->didx);
+    free(x->dval);
+    x->dcnt = 0;
+    x->dmax = 0;
+    x->didx = (uint32_t *)malloc(sizeof(uint32_t) * (x->d ? x->d : 1));
+    x->dval = (uint64_t *)malloc(sizeof(uint64_t) * (x->d ? x->d : 1));
+    for (uint32_t i = 0; i < x->d; i++) {
+        const uint64_t D = x->adj[i].dval;
+        WI += x->adj[i].bias;
+        WD += D;
+        if (D) {
+            x->didx[x->dcnt] = i;
+            x->dval[x->dcnt] = D;
+            x->dcnt++;
+            if (D > x->dmax) x->dmax = D;
+        }
+    }
+    x->fflags = 0;
+    if (x->d && !((unsigned __int128)(x->d - 1) * WD < (WI << 52))) x->fflags |= 1u;
+    if (WI == 0 && x->d) x->fflags |= 2u;
+    if (WD == 0) x->thrD = 0;
+    else if (WI == 0) x->thrD = ~0ull;                 /* always decimal (flag bit 1) */
+    else x->thrD = frac64(WD, (WI << 52) + WD);
+}
+
 static int build_float_vertex(const ora_graph *G, o_vertex *x, const double *w)
 {
     int chosen = -1, last_valid = -1;
@@ -387,32 +424,17 @@ static int build_float_vertex(const ora_graph *G, o_vertex *x, const double *w)
         if ((unsigned __int128)(x->d ? x->d - 1 : 0) * WD < (WI << 52)) { chosen = j; break; }
     }
     if (last_valid < 0 && x->d > 0) return O_EOVERFLOW;
-    x->fflags = 0;
-    if (chosen < 0) { chosen = last_valid < 0 ? 0 : last_valid; if (x->d) x->fflags |= 1u; }
+    if (chosen < 0) chosen = last_valid < 0 ? 0 : last_valid;   /* constraint unmet: flagged below */
+    if (x->d == 0) chosen = 0;   /* R-15: P:377's constraint is vacuous for d = 0 -> the smallest lambda */
     x->lam = (uint32_t)chosen;
-    unsigned __int128 WI = 0, WD = 0;
-    x->dcnt = 0;
-    x->dmax = 0;
-    x->didx = (uint32_t *)malloc(sizeof(uint32_t) * (x->d ? x->d : 1));
-    x->dval = (uint64_t *)malloc(sizeof(uint64_t) * (x->d ? x->d : 1));
     for (uint32_t i = 0; i < x->d; i++) {
         uint32_t I = 0;
         uint64_t D = 0;
         scale_one(w[i], chosen, &I, &D);
         x->adj[i].bias = I;            /* the integer part is the radix-decomposed bias */
-        WI += I;
-        WD += D;
-        if (D) {
-            x->didx[x->dcnt] = i;
-            x->dval[x->dcnt] = D;
-            x->dcnt++;
-            if (D > x->dmax) x->dmax = D;
-        }
+        x->adj[i].dval = D;
     }
-    if (WI == 0 && x->d) x->fflags |= 2u;
-    if (WD == 0) x->thrD = 0;
-    else if (WI == 0) x->thrD = ~0ull;                 /* always decimal (flag bit 1) */
-    else x->thrD = frac64(WD, (WI << 52) + WD);
+    decimal_group(x);
     (void)G;
     return O_OK;
 }
@@ -442,6 +464,7 @@ int ora_build_float(uint32_t V, const uint64_t *row_offsets, const uint32_t *dst
         for (uint32_t i = 0; i < x->d; i++) {
             x->adj[i].dst = dst[row_offsets[u] + i];
             x->adj[i].epoch = 0;
+            x->adj[i].dval = 0;
         }
         int rc = build_float_vertex(G, x, wf + row_offsets[u]);
         if (rc == O_OK) {
@@ -555,8 +578,8 @@ uint32_t ora_two_phase_u32(uint32_t *arr, uint32_t len, const uint32_t *del_sort
 #define ST_EPOCH 29
 
 /* Batched update of one vertex: insert -> delete -> rebuild. */
-static void update_vertex(ora_graph *G, o_vertex *x, const uint32_t *recs, const uint64_t *idx, uint64_t m,
-                          uint32_t e, uint64_t *st)
+static void update_vertex(ora_graph *G, o_vertex *x, const uint32_t *recs, const uint64_t *dv, const uint64_t *idx,
+                          uint64_t m, uint32_t e, uint64_t *st)
 {
     /* expand the pre-batch groups into per-k working arrays */
     uint32_t kind0[32] = {0}, c[32] = {0}, len[32] = {0}, mcap[32] = {0}, one[32];
@@ -589,6 +612,7 @@ static void update_vertex(ora_graph *G, o_vertex *x, const uint32_t *recs, const
         x->adj[i].dst = rec[2];
         x->adj[i].bias = rec[3];
         x->adj[i].epoch = e;
+        x->adj[i].dval = dv ? dv[idx[r]] : 0;   /* float mode: the inserted arc's decimal part */
         for (int k = 0; k < 32; k++) {
             if (!((rec[3] >> k) & 1u)) continue;
             c[k]++;
@@ -674,21 +698,61 @@ static void update_vertex(ora_graph *G, o_vertex *x, const uint32_t *recs, const
         one[k] = (kind1[k] == O_ONE) ? find_one(x, k) : O_NONE;
     }
     install_groups(x, c, kind1, mem, mcap, one);
+    if (G->float_mode) decimal_group(x);   /* R-16: lambda fixed, decimal group from the live arcs */
     st[ST_TOUCH]++;
 }
 
 /* Batched updates.  recs: n records of 4 x u32 {op, src, dst, bias},
- * op 0 = insert, 1 = delete.  Whole-batch validation before any mutation. */
-int ora_apply_updates(ora_graph *G, const uint32_t *recs, uint64_t n, uint64_t *stats)
+ * op 0 = insert, 1 = delete.  Whole-batch validation before any mutation.
+ * Float-mode graphs (R-16) take the inserted biases from wf[n] (the records'
+ * bias fields are ignored): with the source vertex's lambda fixed at build
+ * (S:229), s = fl(w lambda), the arc's integer bias I = floor(s) (must be
+ * < 2^32, else EOVERFLOW; I = 0 is allowed: the arc joins no radix group) and
+ * its decimal part D = floor((s - I) 2^52). */
+static int apply_updates_int(ora_graph *G, const uint32_t *recs, const uint64_t *dv, uint64_t n, uint64_t *st);
+
+int ora_apply_updates_f(ora_graph *G, const uint32_t *recs, const double *wf, uint64_t n, uint64_t *stats)
 {
     uint64_t st[30];
     memset(st, 0, sizeof(st));
-    if (G->float_mode) return O_EINVAL;   /* float-bias updates: not defined in this round */
+    if (G->float_mode != (wf != NULL) && n) return O_EINVAL;
     for (uint64_t r = 0; r < n; r++) {
         const uint32_t *rec = recs + 4 * r;
         if (rec[0] > 1 || rec[1] >= G->V || rec[2] >= G->V) return O_EINVAL;
-        if (rec[0] == 0 && rec[3] == 0) return O_EINVAL;
+        if (!G->float_mode && rec[0] == 0 && rec[3] == 0) return O_EINVAL;
+        if (G->float_mode && rec[0] == 0 && (!(wf[r] > 0.0) || wf[r] != wf[r] || wf[r] > 1e300)) return O_EINVAL;
     }
+    uint32_t *frecs = NULL;
+    uint64_t *dv = NULL;
+    if (G->float_mode && n) {
+        frecs = (uint32_t *)malloc(sizeof(uint32_t) * 4 * n);
+        dv = (uint64_t *)calloc(n, sizeof(uint64_t));
+        memcpy(frecs, recs, sizeof(uint32_t) * 4 * n);
+        for (uint64_t r = 0; r < n; r++) {
+            if (frecs[4 * r] != 0) { frecs[4 * r + 3] = 0; continue; }
+            uint32_t I = 0;
+            if (!scale_one(wf[r], (int)vx(G, frecs[4 * r + 1])->lam, &I, &dv[r])) {
+                free(frecs); free(dv);
+                return O_EOVERFLOW;
+            }
+            frecs[4 * r + 3] = I;
+        }
+        recs = frecs;
+    }
+    int rc = apply_updates_int(G, recs, dv, n, st);
+    free(frecs);
+    free(dv);
+    if (rc == O_OK && stats) memcpy(stats, st, sizeof(st));
+    return rc;
+}
+
+int ora_apply_updates(ora_graph *G, const uint32_t *recs, uint64_t n, uint64_t *stats)
+{
+    return ora_apply_updates_f(G, recs, NULL, n, stats);
+}
+
+static int apply_updates_int(ora_graph *G, const uint32_t *recs, const uint64_t *dv, uint64_t n, uint64_t *st)
+{
     /* stable partition of the batch by src ("put the graph updates of
      * the same vertex together") -- a counting sort keeps batch order */
     uint64_t *cnt = (uint64_t *)calloc((size_t)G->V + 1, sizeof(uint64_t));
@@ -721,12 +785,11 @@ int ora_apply_updates(ora_graph *G, const uint32_t *recs, uint64_t n, uint64_t *
     uint32_t e = ++G->epoch;   /* R-9: epoch = call number, build = 0 */
     for (uint32_t u = 0; u < G->V; u++) {
         if (cnt[u + 1] == cnt[u]) continue;
-        update_vertex(G, vx(G, u), recs, idx + cnt[u], cnt[u + 1] - cnt[u], e, st);
+        update_vertex(G, vx(G, u), recs, dv, idx + cnt[u], cnt[u + 1] - cnt[u], e, st);
     }
     st[ST_EPOCH] = e;
     free(cnt);
     free(idx);
-    if (stats) memcpy(stats, st, sizeof(st));
     return O_OK;
 }
 

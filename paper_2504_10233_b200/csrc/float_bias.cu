@@ -91,6 +91,7 @@ __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, cons
             chosen = last_valid < 0 ? 0 : last_valid;
             if (d) fl |= 1u;
         }
+        if (d == 0) chosen = 0;   // R-15: the constraint is vacuous for d = 0 -> the smallest lambda
         unsigned __int128 wi = 0, wd = 0;
         uint64_t dmax = 0;
         uint32_t cnt = 0;

@@ -111,6 +111,84 @@ def test_float_sampling_chi_square():
     assert chi2_stat(list(counts), list(p), n) < chi2_crit(len(p) - 1)
 
 
-def test_float_updates_refused():
+def test_float_updates_need_real_biases():
+    """Float-mode graphs take inserted biases as doubles (R-16); an integer-only batch is refused."""
     g, V = _star([0.5, 1.5])
     assert g.try_apply_updates([[0, 0, 1, 3]]) == 1
+    assert g.try_apply_updates([[0, 0, 1, 3]], bias_f64=[0.25]) == 0
+    assert g.try_apply_updates([[0, 0, 1, 0]], bias_f64=[-1.0]) == 1          # w <= 0: EINVAL
+    assert g.try_apply_updates([[0, 0, 1, 0]], bias_f64=[float("nan")]) == 1
+    lam = 10 ** _vertex(g, V)["lam"]
+    before = g.dump()
+    assert g.try_apply_updates([[0, 0, 2, 0], [0, 0, 1, 0]], bias_f64=[1.0, 2.0 ** 33 / lam]) == 4   # I >= 2^32
+    assert g.dump() == before                                                      # whole batch refused
+
+
+def _real_dist(ws):
+    tot = sum(Fraction(float(x)) for x in ws)
+    return [Fraction(float(x)) / tot for x in ws]
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_float_updates_keep_distribution_within_1e6(seed):
+    """R-16: with each vertex's lambda fixed at build, inserts split the real bias into
+    I = floor(fl(w lambda)) (radix groups, Eq.3-9) and D (decimal group); after every batch the
+    structure's exact induced distribution is within 1e-6 relative of w / sum w over the live arcs
+    (BASELINE north_star), the integer part satisfies every invariant (Eq.4, Eq.9, exact alias),
+    lambda never changes and flag bit 0 is exactly the P:377 constraint check."""
+    from tests.helpers import check_vertex_invariants
+    rng = np.random.default_rng(100 + seed)
+    V = 12
+    live = {u: {} for u in range(V)}                     # u -> {dst: real bias}; unique dst per vertex
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    dst, wf = [], []
+    for u in range(V):
+        d = int(rng.integers(0, 9)) if u else 0         # vertex 0 starts isolated (lambda = 1)
+        ds = rng.choice(np.arange(V, 4 * V), size=d, replace=False) % (4 * V)
+        for v in ds:
+            w = float(rng.uniform(0.05, 20.0))
+            live[u][int(v) % V + 0] = live[u].get(int(v) % V, 0) or w
+        ro[u + 1] = ro[u] + len(live[u])
+        for v, w in live[u].items():
+            dst.append(v)
+            wf.append(w)
+    g = oracle.OracleGraph(ro, np.array(dst, dtype=np.uint32), np.array(wf), float_bias=True)
+    lam0 = [v["lam"] for v in oracle.parse_dump(g.dump(), V, float_mode=True)]
+    for e in range(1, 15):
+        recs, ws = [], []
+        for _ in range(int(rng.integers(1, 12))):
+            u = int(rng.integers(0, V))
+            if live[u] and rng.random() < 0.45:
+                v = int(rng.choice(list(live[u])))
+                recs.append((1, u, v, 0))
+                ws.append(0.0)
+                del live[u][v]
+            else:
+                free = [v for v in range(V) if v not in live[u]]
+                if not free:
+                    continue
+                v = int(rng.choice(free))
+                w = float(rng.uniform(0.05, 20.0)) if rng.random() < 0.8 else float(rng.uniform(0.001, 0.05))
+                recs.append((0, u, v, 0))
+                ws.append(w)
+                live[u][v] = w
+        st = g.apply_updates(np.array(recs, dtype=np.uint32).reshape(-1, 4), bias_f64=np.array(ws))
+        assert st["epoch"] == e
+        dump = oracle.parse_dump(g.dump(), V, float_mode=True)
+        for u in range(V):
+            v = dump[u]
+            assert v["lam"] == lam0[u]
+            assert sorted(a[0] for a in v["adj"]) == sorted(live[u])
+            if not v["d"]:
+                continue
+            if v["T"]:                                   # integer part nonempty (else flag bit 1)
+                check_vertex_invariants(v)
+            dist = induced_float(v)
+            ref = _real_dist([live[u][a[0]] for a in v["adj"]])
+            for i in range(v["d"]):
+                assert abs(dist[i] - ref[i]) / ref[i] <= Fraction(1, 10 ** 6), (u, i, float(dist[i]), float(ref[i]))
+            WI = sum(a[1] for a in v["adj"])
+            WD = sum(D for _, D in v["dec"])
+            assert bool(v["fflags"] & 1) == (not ((v["d"] - 1) * WD < (WI << 52)))
+            assert bool(v["fflags"] & 2) == (WI == 0)
+            assert [i for i, _ in v["dec"]] == sorted(i for i, _ in v["dec"])
