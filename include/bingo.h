@@ -68,8 +68,9 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
  *   (P:377), integer parts floor(w lambda) form the radix groups, fractional
  *   parts (fixed point, 2^-52) form the decimal group sampled by rejection;
  *   sampled probabilities are within 1e-6 relative of w/sum(w) (R-15).
- *   Float-mode graphs are static in this version: bingo_apply_updates returns
- *   BINGO_E_INVAL.  Exports append a per-vertex decimal trailer (R-11).
+ *   lambda stays fixed per vertex after the build; updates of float
+ *   graphs go through bingo_apply_updates_f64 (R-16).  Exports append a
+ *   per-vertex decimal trailer (R-11).
  *   BINGO_BUILD_ID_LAYOUT lays the pools out in vertex-id order instead of the
  *   default hot-first order (descending out-degree): a performance choice
  *   only, invisible in every result and export.
@@ -131,7 +132,8 @@ void bingo_destroy(bingo_graph *g);
  *   A delete with no live instance is counted in missing_deletes, not an
  *   error (R-8).
  * Errors (nothing is mutated, epoch unchanged): EINVAL for op > 1, src or
- *   dst >= V, or an insert with bias 0; EOVERFLOW if for a touched vertex
+ *   dst >= V, an insert with bias 0, or a float-bias graph (use
+ *   bingo_apply_updates_f64); EOVERFLOW if for a touched vertex
  *   (T + inserted bias) * popc(mask | inserted biases) >= 2^64 or
  *   d + inserts >= 2^32 - 1; NOMEM if the pools cannot grow.
  * stats_or_null (HOST) receives counts and the 5x5 kind-transition matrix
@@ -152,6 +154,29 @@ typedef struct {
 
 bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
                                  bingo_update_stats *stats_or_null, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * bingo_apply_updates_f64 -- the same batched update for a graph built with
+ * BINGO_BUILD_FLOAT_BIAS (floating-point biases, S4.3-4.4 P:344-377; R-16).
+ *
+ * batch: as for bingo_apply_updates; the records' bias fields are ignored.
+ * bias_f64: n doubles, same memory space as batch (HOST with
+ *   BINGO_UPD_HOST_BATCH, else DEVICE); entry i is the real bias of insert
+ *   record i (> 0, finite, <= 1e300), ignored for deletes.
+ * Semantics: each vertex keeps the lambda chosen at its build.  An
+ *   insert (u, v, w) computes s = fl(w * lambda_u) (IEEE binary64), appends an
+ *   arc with radix bias I = floor(s) (I = 0 is allowed: the arc joins no radix
+ *   group) and decimal part D = floor((s - I) * 2^52); inserts, deletes and the
+ *   radix rebuild are those of bingo_apply_updates; then every touched
+ *   vertex's decimal group is rebuilt from its live arcs (ascending index),
+ *   with thrD = floor(W_D 2^64 / (W_I 2^52 + W_D)) and flag bit 0 set iff the
+ *   P:377 constraint (d-1) W_D < W_I 2^52 no longer holds.
+ * Errors (nothing mutated): EINVAL as bingo_apply_updates, for a non-float
+ *   graph, or a bias that is not > 0 and finite; EOVERFLOW if some s >= 2^32
+ *   or as bingo_apply_updates; NOMEM.  Synchronises `stream`.
+ * ------------------------------------------------------------------------- */
+bingo_status bingo_apply_updates_f64(bingo_graph *g, const bingo_update *batch, const double *bias_f64, uint64_t n,
+                                     uint32_t flags, bingo_update_stats *stats_or_null, void *stream);
 
 /* ---------------------------------------------------------------------------
  * bingo_walk -- the batched walker step (S3 "random walk query", P:215;

@@ -30,7 +30,8 @@ COUNTS_HOST = 1
 NO_CAP = 0xFFFFFFFF
 
 # every symbol include/bingo.h declares (checked by tests/test_abi.py)
-ABI_SYMBOLS = ("bingo_build", "bingo_destroy", "bingo_apply_updates", "bingo_walk", "bingo_visit_counts",
+ABI_SYMBOLS = ("bingo_build", "bingo_destroy", "bingo_apply_updates", "bingo_apply_updates_f64", "bingo_walk",
+               "bingo_visit_counts",
                "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str", "bingo_walk_profile")
 
 
@@ -93,6 +94,8 @@ def _lib():
         L.bingo_destroy.restype = None
         L.bingo_apply_updates.argtypes = [P, P, u64, u32, ctypes.POINTER(UpdateStats), P]
         L.bingo_apply_updates.restype = ctypes.c_int
+        L.bingo_apply_updates_f64.argtypes = [P, P, P, u64, u32, ctypes.POINTER(UpdateStats), P]
+        L.bingo_apply_updates_f64.restype = ctypes.c_int
         L.bingo_walk.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, P]
         L.bingo_walk.restype = ctypes.c_int
         L.bingo_visit_counts.argtypes = [P, P, ctypes.c_int, u32, P]
@@ -229,33 +232,45 @@ class Graph:
         return self._h
 
     # ---------------------------------------------------------- updates
-    def apply_updates(self, batch, stream=None) -> dict:
+    def apply_updates(self, batch, stream=None, bias_f64=None) -> dict:
         """Batched insert/delete; ``batch`` is an (n, 4) u32 {op, src, dst, bias} array:
-        a CUDA tensor (device path) or a numpy array (host path, H2D inside the call)."""
+        a CUDA tensor (device path) or a numpy array (host path, H2D inside the call).
+        Float-bias graphs take the inserted biases from ``bias_f64`` ([n] float64, same
+        memory space as ``batch``; bingo_apply_updates_f64, R-16)."""
         torch = _torch()
         st = UpdateStats()
         flags = 0
+        wf = None
         if isinstance(batch, torch.Tensor) and batch.is_cuda:
             b = batch.contiguous()
             n = b.numel() // 4
             ptr = b.data_ptr() if n else None
+            if bias_f64 is not None:
+                wf = torch.as_tensor(bias_f64, dtype=torch.float64, device=b.device).contiguous()
         else:
             arr = np.ascontiguousarray(batch, dtype=np.uint32).reshape(-1, 4)
             n = arr.shape[0]
             ptr = arr.ctypes.data if n else None
             flags = UPD_HOST_BATCH
             b = arr
+            if bias_f64 is not None:
+                wf = np.ascontiguousarray(bias_f64, dtype=np.float64)
         with torch.cuda.device(self.device):
-            _check(_lib().bingo_apply_updates(self._h, ptr, n, flags, ctypes.byref(st), _stream_ptr(stream)),
-                   "bingo_apply_updates")
+            if wf is None:
+                rc = _lib().bingo_apply_updates(self._h, ptr, n, flags, ctypes.byref(st), _stream_ptr(stream))
+            else:
+                wptr = (wf.data_ptr() if isinstance(wf, torch.Tensor) else wf.ctypes.data) if n else None
+                rc = _lib().bingo_apply_updates_f64(self._h, ptr, wptr, n, flags, ctypes.byref(st),
+                                                    _stream_ptr(stream))
+            _check(rc, "bingo_apply_updates")
         return {"inserted": st.inserted, "deleted": st.deleted, "missing_deletes": st.missing_deletes,
                 "touched_vertices": st.touched_vertices,
                 "kind_transitions": np.array(st.kind_transitions, dtype=np.uint64).reshape(5, 5),
                 "epoch": st.epoch}
 
-    def try_apply_updates(self, batch, stream=None) -> int:
+    def try_apply_updates(self, batch, stream=None, bias_f64=None) -> int:
         try:
-            self.apply_updates(batch, stream)
+            self.apply_updates(batch, stream, bias_f64=bias_f64)
             return OK
         except BingoError as e:
             return e.status

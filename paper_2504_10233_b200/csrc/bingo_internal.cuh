@@ -153,6 +153,8 @@ struct bingo_graph {
     bingo::VHdr *hdr = nullptr;        // [V]
     uint2 *arc = nullptr;              // [arc_cap]
     uint32_t *arc_epoch = nullptr;     // [arc_cap]
+    uint64_t *arc_dval = nullptr;      // [arc_cap] float mode: decimal part D of each arc (R-15/R-16)
+    const uint64_t *cur_dins = nullptr; // float mode, during bingo_apply_updates_f64: D of each record
     uint64_t arc_cap = 0;
     bingo::ThinHdr *thdr = nullptr;    // [V]
     bingo::Bucket *bkt = nullptr;      // [bkt_cap]

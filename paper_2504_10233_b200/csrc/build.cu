@@ -444,9 +444,16 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
         CK(cudaGetLastError());
     }
     if (fm) {
-        g->dmem_cap = std::max<uint64_t>(total_dec, 1);
+        g->dmem_cap = std::max<uint64_t>(total_dec + total_dec / 8, 1024);
         g->dmem = (uint4 *)bingo_dev_alloc(g, sizeof(uint4) * g->dmem_cap);
-        if (!g->dmem) { st = BINGO_E_NOMEM; goto done; }
+        g->arc_dval = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * g->arc_cap);
+        if (!g->dmem || !g->arc_dval) { st = BINGO_E_NOMEM; goto done; }
+        CK(cudaMemsetAsync(g->arc_dval, 0, sizeof(uint64_t) * g->arc_cap, s));
+        {
+            const unsigned long long used = total_dec;   // decimal-member bump pointer (counters[3])
+            CK(cudaMemcpyAsync(g->counters + 3, &used, sizeof(used), cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+        }
         if (V) {
             st = float_fill(g, desc, dscan, s);
             if (st != BINGO_OK) { g->poisoned = 1; goto done; }

@@ -17,36 +17,6 @@
 
 namespace bingo {
 
-__device__ __forceinline__ bool scale_one(double w, int j, uint32_t &I, uint64_t &D) {
-    const double s = __dmul_rn(w, pow10_exact(j));
-    if (!(s < 4294967296.0)) return false;
-    const double fl = floor(s);
-    I = (uint32_t)fl;
-    D = (uint64_t)floor(__dmul_rn(__dsub_rn(s, fl), 4503599627370496.0));   // 2^52
-    return true;
-}
-
-__device__ __forceinline__ unsigned __int128 warp_sum128(unsigned __int128 v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        const uint64_t lo = __shfl_xor_sync(0xffffffffu, (uint64_t)v, o);
-        const uint64_t hi = __shfl_xor_sync(0xffffffffu, (uint64_t)(v >> 64), o);
-        v += ((unsigned __int128)hi << 64) | lo;
-    }
-    return v;
-}
-
-// floor(a 2^64 / b) for a < b, binary long division (exact)
-__device__ __forceinline__ uint64_t frac64(unsigned __int128 a, unsigned __int128 b) {
-    uint64_t q = 0;
-    for (int i = 0; i < 64; i++) {
-        a <<= 1;
-        q <<= 1;
-        if (a >= b) { a -= b; q |= 1; }
-    }
-    return q;
-}
-
 __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, const double *__restrict__ wf,
                                uint32_t *__restrict__ ibias, DecRec *__restrict__ dec, uint64_t *__restrict__ dcnt_out,
                                int *__restrict__ flag) {
@@ -123,9 +93,9 @@ __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, cons
             r.lam = (uint8_t)chosen;
             r.flags = (uint8_t)fl;
             r.pad = 0;
-            r.pad2 = 0;
+            r.pad2 = dec_capacity(cnt);   // decimal-member capacity (updates, R-16)
             dec[u] = r;
-            dcnt_out[u] = cnt;
+            dcnt_out[u] = dec_capacity(cnt);
         }
     }
 }
@@ -133,7 +103,8 @@ __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, cons
 // decimal members (ascending adjacency index), after the integer build placed the arcs
 __global__ void k_float_fill(uint32_t V, const uint64_t *__restrict__ ro, const uint32_t *__restrict__ dst,
                              const double *__restrict__ wf, const uint64_t *__restrict__ doff,
-                             DecRec *__restrict__ dec, uint4 *__restrict__ dmem) {
+                             DecRec *__restrict__ dec, uint4 *__restrict__ dmem, const VHdr *__restrict__ hdr,
+                             uint64_t *__restrict__ arc_dval) {
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     const uint32_t lane = lane_id();
     for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
@@ -141,12 +112,16 @@ __global__ void k_float_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
         const uint32_t d = (uint32_t)(ro[u + 1] - b0);
         const int lam = dec[u].lam;
         const uint64_t base = doff[u];
+        const uint64_t aoff = hdr[u].adj_off;   // the arc's D travels with it in updates (R-16)
         uint32_t run = 0;
         for (uint32_t c0 = 0; c0 < d; c0 += 32) {
             const uint32_t i = c0 + lane;
             uint32_t I = 0;
             uint64_t D = 0;
-            if (i < d) scale_one(wf[b0 + i], lam, I, D);
+            if (i < d) {
+                scale_one(wf[b0 + i], lam, I, D);
+                arc_dval[aoff + i] = D;
+            }
             const uint32_t bal = __ballot_sync(0xffffffffu, D != 0);
             if (D) dmem[base + run + __popc(bal & lanemask_lt())] = make_uint4(i, dst[b0 + i], (uint32_t)D, (uint32_t)(D >> 32));
             run += __popc(bal);
@@ -184,7 +159,8 @@ bingo_status float_prepare(bingo_graph *g, const bingo_build_desc *desc, uint32_
 bingo_status float_fill(bingo_graph *g, const bingo_build_desc *desc, const uint64_t *dscan, cudaStream_t s) {
     const uint32_t V = desc->num_vertices;
     const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)V + 7) / 8, 148ull * 64);
-    k_float_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias_f64, dscan, g->dec, g->dmem);
+    k_float_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias_f64, dscan, g->dec, g->dmem,
+                                        g->hdr, g->arc_dval);
     bingo_count_launch();
     return cudaGetLastError() == cudaSuccess ? BINGO_OK : BINGO_E_CUDA;
 }

@@ -72,10 +72,11 @@ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
 
 // ------------------------------------------------------------------ validate
 __global__ void k_upd_validate(const uint4 *__restrict__ recs, uint64_t n, uint32_t V, uint32_t *__restrict__ keys,
-                               uint32_t *__restrict__ vals, UpdCounters *cnt) {
+                               uint32_t *__restrict__ vals, UpdCounters *cnt, bool allow_zero) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
         const uint4 r = recs[i];
-        const bool bad = r.x > 1u || r.y >= V || r.z >= V || (r.x == 0u && r.w == 0u);
+        // float mode (R-16): the integer part of an inserted bias may be 0
+        const bool bad = r.x > 1u || r.y >= V || r.z >= V || (r.x == 0u && r.w == 0u && !allow_zero);
         if (bad) atomicOr(&cnt->flag, 1);
         keys[i] = bad ? 0u : r.y;
         vals[i] = (uint32_t)i;
@@ -310,6 +311,8 @@ struct MutateArgs {
     ThinHdr *thdr;
     uint2 *arc;
     uint32_t *arc_epoch;
+    uint64_t *arc_dval;         // float mode: D per arc, moves with the arc (R-16); else null
+    const uint64_t *dins;       // float mode: D of each record (batch order); else null
     Bucket *bkt;
     GCan *gcan;
     uint32_t *mdst, *midx;
@@ -453,6 +456,7 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
         for (uint32_t i = tid; i < h.d; i += GT) {
             a.arc[aoff + i] = a.arc[h.adj_off + i];
             a.arc_epoch[aoff + i] = a.arc_epoch[h.adj_off + i];
+            if (a.arc_dval) a.arc_dval[aoff + i] = a.arc_dval[h.adj_off + i];
         }
     }
     G::sync();
@@ -475,6 +479,7 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
             if (ins) {
                 a.arc[aoff + idx] = make_uint2(r.z, r.w);
                 a.arc_epoch[aoff + idx] = a.epoch;
+                if (a.arc_dval) a.arc_dval[aoff + idx] = a.dins[a.sval[p]];
             }
             uint32_t mk = __reduce_or_sync(0xffffffffu, w);
             while (mk) {
@@ -629,6 +634,7 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
                         const uint32_t dstp = holes[rank];
                         a.arc[aoff + dstp] = a.arc[aoff + tt];
                         a.arc_epoch[aoff + dstp] = a.arc_epoch[aoff + tt];
+                        if (a.arc_dval) a.arc_dval[aoff + dstp] = a.arc_dval[aoff + tt];
                         R[tt - Lp] = dstp;
                     } else {
                         R[tt - Lp] = DEL_MARK;
@@ -880,6 +886,10 @@ __global__ void k_upd_stats(const uint32_t *__restrict__ vstats, uint32_t ntouch
 // have to grow, nothing is mutated and the host runs the general pipeline.
 static constexpr uint32_t FAST_N = 64;
 static constexpr uint32_t FAST_MAXL = 1u << 16;
+// a touched vertex above this many (post-insert) arcs hands the batch to the bulk-synchronous
+// pipeline, whose chunk items spread the vertex's scans over the GPU (one block here walks
+// them alone: c5 batches of 16 records took 0.9 ms on the fast path, profiles/r01_streaming_c5)
+static constexpr uint32_t FAST_HANDOFF_L = 8192;
 enum : uint32_t { FAST_OK = 0, FAST_INVAL = 1, FAST_OVERFLOW = 4, FAST_SLOW = 8 };
 
 struct FastOut {
@@ -959,7 +969,7 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
                                       fa.m.arc_slack, fa.m.mem_slack);
         if (lane == 0) {
             if (o.overflow) atomicOr(&flag, FAST_OVERFLOW);
-            if (o.L > FAST_MAXL || o.q > FAST_N) atomicOr(&flag, FAST_SLOW);
+            if (o.L > FAST_HANDOFF_L || o.q > FAST_N) atomicOr(&flag, FAST_SLOW);
             atomicAdd(&need_arc, o.arc);
             atomicAdd(&need_bkt, o.bkt);
             atomicAdd(&need_mem, o.mem + o.res);
@@ -1017,6 +1027,7 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
 }  // namespace bingo
 
 #include "update_bsp.cuh"
+#include "float_update.cuh"
 
 // ------------------------------------------------------------------ host side
 namespace {
@@ -1046,6 +1057,8 @@ size_t batch_scratch_bytes(uint64_t n) {
     add(4 * VST * n);                              // vstats
     add(4 * n); add(4 * n);                        // small / large touched lists
     add(sizeof(UpdCounters) + 8 * 32);             // counters, stats
+    add(8 * n); add(8 * n);                        // float mode: dins, device copy of the real biases
+    add(4 * n); add(4 * n);                        // float mode: decimal-member offsets / capacities
     return b + 4096;
 }
 
@@ -1056,6 +1069,15 @@ bingo_status grow_pool(bingo_graph *g, int which, uint64_t need_total, cudaStrea
         uint2 *na = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * cap);
         uint32_t *ne = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * cap);
         if (!na || !ne) { bingo_dev_free(g, na); bingo_dev_free(g, ne); return BINGO_E_NOMEM; }
+        if (g->arc_dval) {
+            uint64_t *nv = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * cap);
+            if (!nv) { bingo_dev_free(g, na); bingo_dev_free(g, ne); return BINGO_E_NOMEM; }
+            if (cudaMemcpyAsync(nv, g->arc_dval, 8 * g->arc_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+                cudaStreamSynchronize(s) != cudaSuccess)
+                return BINGO_E_CUDA;
+            bingo_dev_free(g, g->arc_dval);
+            g->arc_dval = nv;
+        }
         if (cudaMemcpyAsync(na, g->arc, sizeof(uint2) * g->arc_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
             cudaMemcpyAsync(ne, g->arc_epoch, 4 * g->arc_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
             cudaStreamSynchronize(s) != cudaSuccess)
@@ -1129,6 +1151,8 @@ static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
     ma.thdr = g->thdr;
     ma.arc = g->arc;
     ma.arc_epoch = g->arc_epoch;
+    ma.arc_dval = g->arc_dval;
+    ma.dins = g->cur_dins;
     ma.bkt = g->bkt;
     ma.gcan = g->gcan;
     ma.mdst = g->mdst;
@@ -1452,18 +1476,49 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
 static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
                                  const unsigned long long *dstats, bingo_update_stats *stats, cudaStream_t s);
 
+static cudaError_t float_fixup(bingo_graph *g, const uint32_t *tv, uint64_t ntouch, const uint32_t *fdoff,
+                               const uint32_t *fdcap, cudaStream_t s) {
+    if (!ntouch) return cudaSuccess;
+    k_float_fixup<<<(unsigned)std::min<uint64_t>((ntouch + 7) / 8, 148 * 16), 256, 0, s>>>(
+        tv, ntouch, g->hdr, g->arc, g->arc_dval, fdoff, fdcap, g->dec, g->dmem);
+    bingo_count_launch();
+    return cudaGetLastError();
+}
+
 static bool use_legacy_mutate() {
     const char *ev = getenv("BINGO_UPD_LEGACY");
     return ev && ev[0] == '1';
 }
 
+static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const double *wf, uint64_t n,
+                               uint32_t flags, bingo_update_stats *stats, void *stream);
+
 extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
                                             bingo_update_stats *stats, void *stream) {
+    return apply_impl(g, batch, nullptr, n, flags, stats, stream);
+}
+
+extern "C" bingo_status bingo_apply_updates_f64(bingo_graph *g, const bingo_update *batch, const double *bias_f64,
+                                                uint64_t n, uint32_t flags, bingo_update_stats *stats, void *stream) {
+    if (n && !bias_f64) return BINGO_E_INVAL;
+    return apply_impl(g, batch, bias_f64, n, flags, stats, stream);
+}
+
+// restores g->cur_dins on every exit path of a float-mode batch
+struct DinsGuard {
+    bingo_graph *g;
+    ~DinsGuard() { g->cur_dins = nullptr; }
+};
+
+static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const double *wf, uint64_t n,
+                               uint32_t flags, bingo_update_stats *stats, void *stream) {
     if (!g) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     if (n && !batch) return BINGO_E_INVAL;
-    if (g->float_mode) return BINGO_E_INVAL;   // float-bias graphs are static in this version
+    // float-bias graphs take real biases (bingo_apply_updates_f64, R-16); integer graphs do not
+    if (n && g->float_mode != (wf != nullptr)) return BINGO_E_INVAL;
     if (n >= 0xFFFFFFFFull) return BINGO_E_INVAL;
+    const bool fm = g->float_mode;
     cudaStream_t s = (cudaStream_t)stream;
     if (stats) memset(stats, 0, sizeof(*stats));
     if (n == 0) {
@@ -1472,7 +1527,7 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
         return BINGO_OK;
     }
     // ---- small batches: single-launch fast path (falls through when it reports SLOW)
-    if (n <= FAST_N) {
+    if (n <= FAST_N && !fm) {
         bingo_status fst;
         if (try_fast_path(g, batch, n, flags, stats, s, &fst)) return fst;
     }
@@ -1506,16 +1561,34 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     uint32_t *large_list = cv.take<uint32_t>(n);
     UpdCounters *dc = cv.take<UpdCounters>(1);
     unsigned long long *dstats = cv.take<unsigned long long>(32);
+    uint64_t *dins = cv.take<uint64_t>(n);
+    double *dwf = cv.take<double>(n);
+    uint32_t *fdoff = cv.take<uint32_t>(n), *fdcap = cv.take<uint32_t>(n);
 
     const uint4 *recs = reinterpret_cast<const uint4 *>(batch);
     if (flags & BINGO_UPD_HOST_BATCH) {
         UCK(cudaMemcpyAsync(drec, batch, 16 * n, cudaMemcpyHostToDevice, s));
         recs = drec;
+    } else if (fm) {   // float mode rewrites the bias fields: work on a copy
+        UCK(cudaMemcpyAsync(drec, batch, 16 * n, cudaMemcpyDeviceToDevice, s));
+        recs = drec;
     }
     UCK(cudaMemsetAsync(dc, 0, sizeof(UpdCounters), s));
     UCK(cudaMemsetAsync(dstats, 0, 8 * 32, s));
     const unsigned gb = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
-    k_upd_validate<<<gb, 256, 0, s>>>(recs, n, g->V, k0, v0, dc);
+    DinsGuard dguard{g};
+    if (fm) {
+        const double *w = wf;
+        if (flags & BINGO_UPD_HOST_BATCH) {
+            UCK(cudaMemcpyAsync(dwf, wf, 8 * n, cudaMemcpyHostToDevice, s));
+            w = dwf;
+        }
+        k_float_scale<<<gb, 256, 0, s>>>(drec, w, n, g->V, g->dec, dins, dc);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        g->cur_dins = dins;
+    }
+    k_upd_validate<<<gb, 256, 0, s>>>(recs, n, g->V, k0, v0, dc, fm);
     bingo_count_launch();
     UCK(cudaGetLastError());
     bool in1 = false;
@@ -1533,9 +1606,34 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     UCK(cudaMemcpyAsync(&ntouch, head_ex + n, 8, cudaMemcpyDeviceToHost, s));
     UCK(cudaStreamSynchronize(s));
     const uint32_t e = g->epoch + 1;
+    if (fm && ntouch) {
+        // decimal-member regions for the batch; validation errors and pool growth before any mutation
+        k_float_plan<<<(unsigned)std::min<uint64_t>((ntouch + 255) / 256, 148 * 16), 256, 0, s>>>(
+            recs, sv, seg, tv, ntouch, dins, g->dec, g->counters, fdoff, fdcap);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        unsigned long long used = 0;
+        int fl = 0;
+        UCK(cudaMemcpyAsync(&used, g->counters + 3, 8, cudaMemcpyDeviceToHost, s));
+        UCK(cudaMemcpyAsync(&fl, &dc->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UCK(cudaStreamSynchronize(s));
+        if (fl & 1) return BINGO_E_INVAL;
+        if (fl & 4) return BINGO_E_OVERFLOW;
+        if (used > g->dmem_cap) {
+            const uint64_t cap = std::max<uint64_t>(used + used / 4, g->dmem_cap + g->dmem_cap / 4);
+            uint4 *nd = (uint4 *)bingo_dev_alloc(g, sizeof(uint4) * cap);
+            if (!nd) return BINGO_E_NOMEM;
+            UCK(cudaMemcpyAsync(nd, g->dmem, sizeof(uint4) * g->dmem_cap, cudaMemcpyDeviceToDevice, s));
+            UCK(cudaStreamSynchronize(s));
+            bingo_dev_free(g, g->dmem);
+            g->dmem = nd;
+            g->dmem_cap = cap;
+        }
+    }
     if (!use_legacy_mutate()) {
         const bingo_status st = apply_bsp(g, recs, sv, seg, tv, ntouch, e, dc, dstats, s);
         if (st != BINGO_OK) return st;
+        if (fm) UCK(float_fixup(g, tv, ntouch, fdoff, fdcap, s));
         return finish_batch(g, n, ntouch, e, dstats, stats, s);
     }
     const bool bs = (g->flags & BINGO_BUILD_BS_MODE) != 0;
@@ -1584,6 +1682,8 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
     ma.thdr = g->thdr;
     ma.arc = g->arc;
     ma.arc_epoch = g->arc_epoch;
+    ma.arc_dval = g->arc_dval;
+    ma.dins = g->cur_dins;
     ma.bkt = g->bkt;
     ma.gcan = g->gcan;
     ma.mdst = g->mdst;
@@ -1636,6 +1736,7 @@ extern "C" bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *
         bingo_count_launch();
         UCK(cudaGetLastError());
     }
+    if (fm) UCK(float_fixup(g, tv, ntouch, fdoff, fdcap, s));
     return finish_batch(g, n, ntouch, e, dstats, stats, s);
 }
 

@@ -223,6 +223,7 @@ __global__ void __launch_bounds__(MT) k_bsp_alloc_insert(const BspArgs a) {
             for (uint32_t p = lane; p < h.d; p += 32) {
                 g.arc[aoff + p] = g.arc[h.adj_off + p];
                 g.arc_epoch[aoff + p] = g.arc_epoch[h.adj_off + p];
+                if (g.arc_dval) g.arc_dval[aoff + p] = g.arc_dval[h.adj_off + p];
             }
         }
         // member arrays that overflow their capacity (lists before the batch)
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(MT) k_bsp_alloc_insert(const BspArgs a) {
                 if (ins) {
                     g.arc[aoff + idx] = make_uint2(r.z, r.w);
                     g.arc_epoch[aoff + idx] = g.epoch;
+                    if (g.arc_dval) g.arc_dval[aoff + idx] = g.dins[g.sval[p]];
                 }
                 uint32_t mk = __reduce_or_sync(0xffffffffu, w);
                 while (mk) {
@@ -333,6 +335,7 @@ __global__ void __launch_bounds__(MT) k_bsp_copy(const BspArgs a, uint64_t total
         for (uint32_t p = c * CH + lane; p < e; p += 32) {
             g.arc[to + p] = g.arc[h.adj_off + p];
             g.arc_epoch[to + p] = g.arc_epoch[h.adj_off + p];
+            if (g.arc_dval) g.arc_dval[to + p] = g.arc_dval[h.adj_off + p];
         }
     }
 }
@@ -382,6 +385,7 @@ __device__ __forceinline__ uint32_t tail_window(const MutateArgs &g, const DelSc
                 moved |= e.y;
                 g.arc[aoff + dstp] = e;
                 g.arc_epoch[aoff + dstp] = g.arc_epoch[aoff + tt];
+                if (g.arc_dval) g.arc_dval[aoff + dstp] = g.arc_dval[aoff + tt];
                 s.R[tt - Lp] = dstp;
             } else {
                 s.R[tt - Lp] = DEL_MARK;

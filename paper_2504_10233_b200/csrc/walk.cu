@@ -115,7 +115,9 @@ __global__ void __launch_bounds__(256, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO
                         u = next;
                         o = 0;
                         if (APP == BINGO_PPR) {
+#ifndef BINGO_EXP_NO_VISIT       // measurement experiment only: skip the visit counts
                             if (a.visit) atomicAdd(&a.visit[u], 1ull);
+#endif
                             if (PROF) prof.visit++;
                             if (a.stop_always) {
                                 fin = true;

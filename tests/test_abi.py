@@ -12,7 +12,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 def declared_symbols():
     src = open(os.path.join(ROOT, "include", "bingo.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(bingo_[a-z_]+)\s*\(", src)) - {"bingo_alloc_fn", "bingo_free_fn"})
+    return sorted(set(re.findall(r"\b(bingo_[a-z0-9_]+)\s*\(", src)) - {"bingo_alloc_fn", "bingo_free_fn"})
 
 
 def test_header_symbols_exported():

@@ -21,22 +21,25 @@ ap.add_argument("--gen", default="cpu", help="workload generator device (cuda: m
 a = ap.parse_args()
 w = synth.make_workload(a.config, rounds=2, device=a.gen)
 torch.cuda.empty_cache()
-g = pb.Graph(w.row_offsets, w.dst, w.bias, neighbor_index=(a.app == "node2vec"))
+g = pb.Graph(w.row_offsets, w.dst, w.bias, neighbor_index=("node2vec" in a.app))
 for b in w.batches:
     g.apply_updates(b)
-app = {"deepwalk": pb.DEEPWALK, "node2vec": pb.NODE2VEC, "ppr": pb.PPR}[a.app]
-paths = None if a.app == "ppr" else torch.empty((81, w.V), dtype=torch.int32, device="cuda")
 lens = torch.empty(w.V, dtype=torch.int32, device="cuda")
-for i in range(a.walks):
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    if app == pb.PPR:
-        g.walk(app=app, length=pb.NO_CAP, seed=i, paths=None, lengths=lens)
-    else:
-        g.walk(app=app, length=80, seed=i, paths=paths, lengths=lens, p=2.0, q=0.5)
-    e1.record()
-    torch.cuda.synchronize()
-    steps = int(lens.to(torch.int64).sum())
-    ms = e0.elapsed_time(e1)
-    print(f"walk {i}: {ms:.2f} ms, {steps} steps, {steps / ms / 1e6:.2f} G steps/s", flush=True)
+paths = None
+for name in a.app.split(","):
+    app = {"deepwalk": pb.DEEPWALK, "node2vec": pb.NODE2VEC, "ppr": pb.PPR}[name]
+    if app != pb.PPR and paths is None:
+        paths = torch.empty((81, w.V), dtype=torch.int32, device="cuda")
+    for i in range(a.walks):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        if app == pb.PPR:
+            g.walk(app=app, length=pb.NO_CAP, seed=i, paths=None, lengths=lens)
+        else:
+            g.walk(app=app, length=80, seed=i, paths=paths, lengths=lens, p=2.0, q=0.5)
+        e1.record()
+        torch.cuda.synchronize()
+        steps = int(lens.to(torch.int64).sum())
+        ms = e0.elapsed_time(e1)
+        print(f"{name} walk {i}: {ms:.2f} ms, {steps} steps, {steps / ms / 1e6:.2f} G steps/s", flush=True)
 print("done", w.V, w.num_arcs)
