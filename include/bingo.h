@@ -71,9 +71,11 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
  *   lambda stays fixed per vertex after the build; updates of float
  *   graphs go through bingo_apply_updates_f64 (R-16).  Exports append a
  *   per-vertex decimal trailer (R-11).
- *   BINGO_BUILD_ID_LAYOUT lays the pools out in vertex-id order instead of the
- *   default hot-first order (descending out-degree): a performance choice
- *   only, invisible in every result and export.
+ *   Layout (a performance choice only, invisible in every result and export):
+ *   by default the pools are laid out hot-first (descending out-degree) and,
+ *   for V >= 2^23, the vertices are also relabelled internally by that order
+ *   (BINGO_BUILD_RELABEL forces it); BINGO_BUILD_ID_LAYOUT keeps vertex-id
+ *   order for everything.
  * arc_slack / member_slack: fraction of extra per-vertex capacity reserved
  *   for growth (Hornet-style dynamic arrays + memory pool);
  *   pool_reserve: extra fraction of every pool for relocations.
@@ -87,6 +89,7 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
 #define BINGO_BUILD_NEIGHBOR_INDEX 2u /* keep per-vertex neighbour hash sets: O(1) node2vec distance test */
 #define BINGO_BUILD_FLOAT_BIAS 4u     /* biases come from bias_f64 (S4.3 floating-point extension, R-15) */
 #define BINGO_BUILD_ID_LAYOUT 8u      /* pools in vertex-id order (default: hot-first) */
+#define BINGO_BUILD_RELABEL 16u       /* relabel vertices hot-first internally at any V (default: V >= 2^23) */
 
 typedef void *(*bingo_alloc_fn)(size_t bytes, void *ctx);
 typedef void (*bingo_free_fn)(void *ptr, void *ctx);

@@ -355,6 +355,15 @@ class Graph:
                    "bingo_visit_counts")
         return out
 
+    def visit_counts_host(self, reset: bool = False, stream=None) -> np.ndarray:
+        """The same counts copied to a host array by the library (BINGO_COUNTS_HOST)."""
+        torch = _torch()
+        out = np.empty(self.V, dtype=np.uint64)
+        with torch.cuda.device(self.device):
+            _check(_lib().bingo_visit_counts(self._h, out.ctypes.data if self.V else None, int(reset), COUNTS_HOST,
+                                             _stream_ptr(stream)), "bingo_visit_counts")
+        return out
+
     def reset_visit_counts(self, stream=None):
         torch = _torch()
         with torch.cuda.device(self.device):

@@ -32,7 +32,7 @@ void bingo_dev_free(bingo_graph *g, void *p) {
 
 extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
-    void *bufs[] = {g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->arc_dval, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->nbtomb, g->dec, g->dmem, g->counters, g->visit, g->dev_flag,
+    void *bufs[] = {g->perm, g->inv, g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->arc_dval, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->nbtomb, g->dec, g->dmem, g->counters, g->visit, g->dev_flag,
                     g->scratch, g->wscratch, g->vscratch, g->bscratch, g->iscratch, g->fast_scr};
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
@@ -111,9 +111,15 @@ extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t c
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long c[4];
     std::vector<VHdr> hdr(g->V);
+    std::vector<uint32_t> perm(g->V), inv(g->V);   // dumps are in external ids and order (R-11)
     cudaError_t e = cudaMemcpyAsync(c, g->counters, sizeof(c), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess && g->V)
         e = cudaMemcpyAsync(hdr.data(), g->hdr, sizeof(VHdr) * g->V, cudaMemcpyDeviceToHost, s);
+    for (uint32_t x = 0; x < g->V; x++) perm[x] = inv[x] = x;   // identity unless relabelled
+    if (e == cudaSuccess && g->V && g->perm)
+        e = cudaMemcpyAsync(perm.data(), g->perm, sizeof(uint32_t) * g->V, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess && g->V && g->inv)
+        e = cudaMemcpyAsync(inv.data(), g->inv, sizeof(uint32_t) * g->V, cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     std::vector<uint2> arc(c[0]);
@@ -135,11 +141,12 @@ extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t c
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     Out o{(host_buf && cap) ? host_buf : nullptr, cap, 0};
-    for (uint32_t u = 0; u < g->V; u++) {
+    for (uint32_t x = 0; x < g->V; x++) {
+        const uint32_t u = inv[x];
         const VHdr &h = hdr[u];
         o.u32(h.d);
         for (uint32_t i = 0; i < h.d; i++) {
-            o.u32(arc[h.adj_off + i].x);
+            o.u32(perm[arc[h.adj_off + i].x]);
             o.u32(arc[h.adj_off + i].y);
             o.u32(ep[h.adj_off + i]);
         }
@@ -196,14 +203,16 @@ __device__ __forceinline__ uint64_t fnv64(uint64_t h, uint64_t v) {
 __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 *__restrict__ arc,
                           const uint32_t *__restrict__ ep, const Bucket *__restrict__ bkt,
                           const GCan *__restrict__ gcan, const uint32_t *__restrict__ midx,
-                          const DecRec *__restrict__ dec, const uint4 *__restrict__ dmem, uint64_t *__restrict__ out) {
-    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
+                          const DecRec *__restrict__ dec, const uint4 *__restrict__ dmem, const uint32_t *__restrict__ perm,
+                          const uint32_t *__restrict__ inv, uint64_t *__restrict__ out) {
+    for (uint32_t xu = blockIdx.x * blockDim.x + threadIdx.x; xu < V; xu += gridDim.x * blockDim.x) {
+        const uint32_t u = inv ? inv[xu] : xu;   // digest of external vertex xu over its canonical (external-id) bytes
         const VHdr h = hdr[u];
         uint64_t x = 0xcbf29ce484222325ull;
         x = fnv32(x, h.d);
         for (uint32_t i = 0; i < h.d; i++) {
             const uint2 a = arc[h.adj_off + i];
-            x = fnv32(x, a.x);
+            x = fnv32(x, perm ? perm[a.x] : a.x);
             x = fnv32(x, a.y);
             x = fnv32(x, ep[h.adj_off + i]);
         }
@@ -236,7 +245,7 @@ __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 
                 x = fnv64(x, ((uint64_t)m.w << 32) | m.z);
             }
         }
-        out[u] = x;
+        out[xu] = x;
     }
 }
 }  // namespace bingo
@@ -248,7 +257,7 @@ extern "C" bingo_status bingo_digests(bingo_graph *g, uint64_t *digests, void *s
     cudaStream_t s = (cudaStream_t)stream;
     unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)g->V + 255) / 256, 148ull * 16);
     k_digests<<<blocks, 256, 0, s>>>(g->V, g->hdr, g->arc, g->arc_epoch, g->bkt, g->gcan, g->midx,
-                                                 g->float_mode ? g->dec : nullptr, g->dmem, digests);
+                                                 g->float_mode ? g->dec : nullptr, g->dmem, g->perm, g->inv, digests);
     bingo_count_launch();
     if (cudaGetLastError() != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     return BINGO_OK;

@@ -132,6 +132,26 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 }  // namespace bingo
 
+// PPR visit counters, indexed by internal id: the hottest VISIT_PAD vertices (ids
+// 0..VISIT_PAD-1 after the hot-first relabelling) get a 256 B slot each so their
+// atomics spread over the L2 slices (packed, the top hubs' counters shared a few
+// lines and serialised in one slice: c4 PPR 403 ms packed, 164 ms padded); the
+// rest are packed u64 (hot-first, so within the TLB reach; padding 2^18 vertices
+// was slower again, 252 ms).
+// graphs with at least this many vertices are relabelled hot-first
+#ifndef BINGO_RELABEL_MIN_V
+#define BINGO_RELABEL_MIN_V (1u << 23)
+#endif
+#ifndef BINGO_VISIT_PAD
+#define BINGO_VISIT_PAD 4096u
+#endif
+#define BINGO_VISIT_STRIDE 32u
+__host__ __device__ inline uint64_t visit_slot(uint32_t j) {
+    return j < BINGO_VISIT_PAD ? (uint64_t)j * BINGO_VISIT_STRIDE
+                               : (uint64_t)BINGO_VISIT_PAD * BINGO_VISIT_STRIDE + (j - BINGO_VISIT_PAD);
+}
+__host__ __device__ inline uint64_t visit_words(uint32_t V) { return visit_slot(V); }
+
 // walker-claim counters: each walk launch takes the next of these slots (zeroed on its
 // stream), so up to BINGO_WALK_SLOTS launches may run concurrently on one graph.
 #define BINGO_WALK_SLOTS 64
@@ -150,7 +170,9 @@ struct bingo_graph {
     void *alloc_ctx = nullptr;
     double arc_slack = 0.25, member_slack = 0.25, pool_reserve = 0.1;
 
-    bingo::VHdr *hdr = nullptr;        // [V]
+    uint32_t *perm = nullptr;          // [V] internal id -> external id (hot-first relabelling), or
+    uint32_t *inv = nullptr;           // [V] external id -> internal id; both null: ids are external
+    bingo::VHdr *hdr = nullptr;        // [V] indexed by internal id, like every per-vertex array
     uint2 *arc = nullptr;              // [arc_cap]
     uint32_t *arc_epoch = nullptr;     // [arc_cap]
     uint64_t *arc_dval = nullptr;      // [arc_cap] float mode: decimal part D of each arc (R-15/R-16)

@@ -30,13 +30,15 @@ __global__ void k_build_sizes(uint32_t V, const uint64_t *__restrict__ ro, const
                               const uint32_t *__restrict__ bias, uint32_t alpha, uint32_t beta, bool bs,
                               double arc_slack, double mem_slack, uint64_t *__restrict__ sz_arc,
                               uint64_t *__restrict__ sz_bkt, uint64_t *__restrict__ sz_mem, int *__restrict__ flag,
-                              unsigned long long *__restrict__ hot_hist, bool allow_zero) {
+                              unsigned long long *__restrict__ hot_hist, bool allow_zero,
+                              const uint32_t *__restrict__ perm) {
     __shared__ unsigned long long s_hist[2 * HOT_BINS];
     for (int i = threadIdx.x; i < 2 * HOT_BINS; i += blockDim.x) s_hist[i] = 0;
     __syncthreads();
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     const uint32_t lane = lane_id();
-    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < V; j += warps) {
+        const uint32_t u = perm ? perm[j] : j;   // internal id j = hot rank of external vertex u
         const uint64_t b0 = ro[u], b1 = ro[u + 1];
         if (b1 < b0 || b1 - b0 >= 0xFFFFFFFFull) {
             if (lane == 0) atomicOr(flag, b1 < b0 ? 1 : 4);
@@ -70,9 +72,9 @@ __global__ void k_build_sizes(uint32_t V, const uint64_t *__restrict__ ro, const
         uint64_t units = is_list(kind) ? member_units(cnt, mem_slack) : 0;
         units = warp_sum(units);
         if (lane == 0) {
-            sz_arc[u] = arc_capacity(d, arc_slack);
-            sz_bkt[u] = bucket_capacity(n);
-            sz_mem[u] = units;
+            sz_arc[j] = arc_capacity(d, arc_slack);
+            sz_bkt[j] = bucket_capacity(n);
+            sz_mem[j] = units;
             // walker-read bytes of this vertex by degree bin: buckets, member dsts
             atomicAdd(&s_hist[hot_bin(d)], (unsigned long long)(32ull * n));
             atomicAdd(&s_hist[HOT_BINS + hot_bin(d)], (unsigned long long)(16ull * units));
@@ -90,13 +92,14 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
                              const uint64_t *__restrict__ sz_arc, VHdr *__restrict__ hdr, ThinHdr *__restrict__ thdr, uint2 *__restrict__ arc,
                              uint32_t *__restrict__ arc_epoch, Bucket *__restrict__ bkt, GCan *__restrict__ gcan,
                              uint32_t *__restrict__ mdst, uint32_t *__restrict__ midx, uint32_t hot_b,
-                             uint32_t hot_m) {
+                             uint32_t hot_m, const uint32_t *__restrict__ perm, const uint32_t *__restrict__ inv) {
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     const uint32_t lane = lane_id();
-    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < V; j += warps) {
+        const uint32_t u = perm ? perm[j] : j;   // external row; everything stored uses internal ids
         const uint64_t b0 = ro[u];
         const uint32_t d = (uint32_t)(ro[u + 1] - b0);
-        const uint64_t aoff = off_arc[u];
+        const uint64_t aoff = off_arc[j];
         // pass 1: copy arcs, count groups
         uint32_t cnt = 0;
         uint64_t tsum = 0;
@@ -106,7 +109,7 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
             uint32_t w = 0;
             if (i < d) {
                 w = bias[b0 + i];
-                arc[aoff + i] = make_uint2(dst[b0 + i], w);
+                arc[aoff + i] = make_uint2(inv ? inv[dst[b0 + i]] : dst[b0 + i], w);
                 arc_epoch[aoff + i] = 0;
                 tsum += w;
             }
@@ -130,7 +133,7 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
             if ((int)lane >= o) pre += y;
         }
         pre -= units;
-        const uint64_t my_off = off_mem[u] + pre;   // 16 B units
+        const uint64_t my_off = off_mem[j] + pre;   // 16 B units
         // pass 2: members (ascending adjacency index) and one-element members
         uint32_t fill = 0;          // lane k: entries written so far
         uint32_t one_idx = 0, one_dst = 0;
@@ -139,7 +142,7 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
             for (uint32_t base = 0; base < d; base += 32) {
                 uint32_t i = base + lane;
                 uint32_t w = 0, v = 0;
-                if (i < d) { w = bias[b0 + i]; v = dst[b0 + i]; }
+                if (i < d) { w = bias[b0 + i]; v = inv ? inv[dst[b0 + i]] : dst[b0 + i]; }
                 uint32_t mk = mask;
                 while (mk) {
                     const int k = __ffs(mk) - 1;
@@ -176,7 +179,7 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
         uint64_t thr;
         uint32_t alias;
         vose_warp(lane < n, n, (uint64_t)c_b << kb, T, thr, alias);
-        const uint64_t bo = off_bkt[u];
+        const uint64_t bo = off_bkt[j];
         uint32_t x_b, y_b;
         group_view(kind_b, c_b, (uint32_t)off_b, od_b, d, aoff, x_b, y_b);
         const uint32_t aux_b = is_list(kind_b) ? units_b * 4 : (kind_b == K_ONE ? oi_b : 0u);
@@ -190,31 +193,39 @@ __global__ void k_build_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
             h.n = (uint8_t)n;
             h.ncap = (uint8_t)bucket_capacity(n);
             h.pad = 0;
-            h.adj_cap = (uint32_t)sz_arc[u];
-            hdr[u] = h;
+            h.adj_cap = (uint32_t)sz_arc[j];
+            hdr[j] = h;
             ThinHdr th;
             th.bkt_off = (uint32_t)bo;
             th.n = (uint8_t)n;
             th.flags = (d >= hot_b ? 1 : 0) | (d >= hot_m ? 2 : 0);
             th.pad1 = 0;
-            thdr[u] = th;
+            thdr[j] = th;
         }
     }
 }
 
-// Hot-first pool layout: vertices in descending out-degree (ties by id, a stable
-// sort) get the lowest offsets of every pool.  Walk visits are degree-skewed, so
-// the buckets, member lists and arcs that serve most steps share a few 2 MB pages:
+// Hot-first vertex relabelling: internal id j = rank of the vertex in descending
+// out-degree (ties by id, a stable sort); perm[j] = external id, inv[u] = internal
+// id.  Every per-vertex array (headers, visit counts, neighbour-set offsets, decimal
+// records) is indexed by j and every stored destination is internal, so pool
+// offsets (plain scans in j order) and the per-vertex arrays both put the vertices
+// that serve most walk steps (walk visits are degree-skewed) into a few 2 MB pages:
 // random access on B200 is bound by address translation once a footprint outgrows
-// the TLB reach (~128-256 MB, profiles/r01_tlb_sweep.json), and this keeps the hot
-// part of the graph inside it.  Offsets are internal; every export is canonical.
+// the TLB reach (~128-256 MB, profiles/r01_tlb_sweep.json).  The boundary
+// translates: starts, update records and exports in, paths, counts and dumps out.
 __global__ void k_hot_keys(uint32_t V, const uint64_t *__restrict__ ro, uint32_t *__restrict__ key,
-                           uint32_t *__restrict__ val) {
+                           uint32_t *__restrict__ val, bool hot) {
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
-        key[u] = ~(uint32_t)(ro[u + 1] - ro[u]);
+        key[u] = hot ? ~(uint32_t)(ro[u + 1] - ro[u]) : 0u;
         val[u] = u;
     }
 }
+__global__ void k_inverse(uint32_t V, const uint32_t *__restrict__ perm, uint32_t *__restrict__ inv) {
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < V; j += gridDim.x * blockDim.x) inv[perm[j]] = j;
+}
+// Hot-first pools without relabelling (graphs whose per-vertex arrays already fit
+// the TLB reach): ids stay external, only the pool offsets follow the hot order.
 __global__ void k_perm_gather(uint32_t V, const uint32_t *__restrict__ perm, const uint64_t *__restrict__ in,
                               uint64_t *__restrict__ out) {
     for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < V; j += gridDim.x * blockDim.x) out[j] = in[perm[j]];
@@ -337,10 +348,16 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     uint32_t *ibias = nullptr;
     uint64_t *dcnt = nullptr, *dscan = nullptr, total_dec = 0;
     const unsigned blocks = (unsigned)std::min<uint64_t>((nV + 7) / 8, 148ull * 64);
-    // pool layout: hot-first (default) or vertex-id order (BINGO_BUILD_ID_LAYOUT / env BINGO_LAYOUT=id, A/B)
-    const char *lay = getenv("BINGO_LAYOUT");
-    const bool hot_layout = !(desc->flags & BINGO_BUILD_ID_LAYOUT) && !(lay && strcmp(lay, "id") == 0);
-    uint32_t *pk = nullptr;
+    // layout: 0 = vertex-id order; 1 = hot-first pools, external ids; 2 = hot-first
+    // relabelling (internal ids = hot rank).  Default: 2 for V >= BINGO_RELABEL_MIN_V (the
+    // per-vertex arrays outgrow the TLB reach), else 1.  BINGO_BUILD_ID_LAYOUT / BINGO_BUILD_RELABEL
+    // force 0 / 2; env BINGO_LAYOUT=id|hot|relabel overrides (A/B).
+    int layout = (desc->flags & BINGO_BUILD_ID_LAYOUT) ? 0
+                 : (desc->flags & BINGO_BUILD_RELABEL) ? 2
+                 : (V >= BINGO_RELABEL_MIN_V ? 2 : 1);
+    if (const char *lay = getenv("BINGO_LAYOUT"))
+        layout = strcmp(lay, "id") == 0 ? 0 : strcmp(lay, "hot") == 0 ? 1 : strcmp(lay, "relabel") == 0 ? 2 : layout;
+    uint32_t *pk = nullptr, *hperm = nullptr;
     uint64_t *rtmp = nullptr, *pbuf = nullptr;
 
     g->counters = (unsigned long long *)bingo_dev_alloc(g, (16 + BINGO_WALK_SLOTS) * sizeof(unsigned long long));
@@ -348,16 +365,34 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     g->dev_flag = (int *)bingo_dev_alloc(g, sizeof(int) * 4);
     g->hdr = (VHdr *)bingo_dev_alloc(g, sizeof(VHdr) * std::max<uint64_t>(nV, 1));
     g->thdr = (ThinHdr *)bingo_dev_alloc(g, sizeof(ThinHdr) * std::max<uint64_t>(nV, 1));
-    g->visit = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * std::max<uint64_t>(nV, 1));
+    g->visit = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * std::max<uint64_t>(visit_words(V), 1));
     sz = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (nV + 1));
     off = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (nV + 1));
     tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * tmpw);
     dhist = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * 2 * HOT_BINS);
-    if (hot_layout && nV) {
+    if (nV && layout > 0) {
         pk = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * 4 * nV);
         rtmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * radix_tmp_words(nV));
-        pbuf = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 2 * (nV + 1));
-        if (!pk || !rtmp || !pbuf) { st = BINGO_E_NOMEM; goto done; }
+        if (!pk || !rtmp) { st = BINGO_E_NOMEM; goto done; }
+        const unsigned eg = (unsigned)std::min<uint64_t>((nV + 255) / 256, 148ull * 16);
+        k_hot_keys<<<eg, 256, 0, s>>>(V, desc->row_offsets, pk, pk + nV, true);
+        bingo_count_launch();
+        CK(cudaGetLastError());
+        bool in1 = false;
+        CK(radix_sort_pairs(pk, pk + nV, pk + 2 * nV, pk + 3 * nV, nV, 32, rtmp, s, &in1));
+        hperm = in1 ? pk + 3 * nV : pk + nV;
+        if (layout == 2) {
+            g->perm = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * nV);
+            g->inv = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * nV);
+            if (!g->perm || !g->inv) { st = BINGO_E_NOMEM; goto done; }
+            CK(cudaMemcpyAsync(g->perm, hperm, sizeof(uint32_t) * nV, cudaMemcpyDeviceToDevice, s));
+            k_inverse<<<eg, 256, 0, s>>>(V, g->perm, g->inv);
+            bingo_count_launch();
+            CK(cudaGetLastError());
+        } else {
+            pbuf = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 2 * (nV + 1));
+            if (!pbuf) { st = BINGO_E_NOMEM; goto done; }
+        }
     }
     if (!g->counters || !g->dev_flag || !g->hdr || !g->thdr || !g->visit || !sz || !off || !tmp || !dhist) {
         st = BINGO_E_NOMEM;
@@ -381,29 +416,23 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     }
     CK(cudaMemsetAsync(g->counters, 0, 16 * sizeof(unsigned long long), s));
     CK(cudaMemsetAsync(g->dev_flag, 0, sizeof(int) * 4, s));
-    CK(cudaMemsetAsync(g->visit, 0, sizeof(unsigned long long) * std::max<uint64_t>(nV, 1), s));
+    CK(cudaMemsetAsync(g->visit, 0, sizeof(unsigned long long) * std::max<uint64_t>(visit_words(V), 1), s));
     CK(cudaMemsetAsync(g->hdr, 0, sizeof(VHdr) * std::max<uint64_t>(nV, 1), s));
     CK(cudaMemsetAsync(g->thdr, 0, sizeof(ThinHdr) * std::max<uint64_t>(nV, 1), s));
     if (V) {
         k_build_sizes<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, idesc.bias, g->alpha, g->beta, bs,
                                              g->arc_slack, g->member_slack, sz, sz + (nV + 1), sz + 2 * (nV + 1),
-                                             g->dev_flag, dhist, fm);
+                                             g->dev_flag, dhist, fm, g->perm);
         bingo_count_launch();
         CK(cudaGetLastError());
-        if (hot_layout) {
+        if (layout == 1) {   // sizes are in external order; offsets follow the hot order
             const unsigned eg = (unsigned)std::min<uint64_t>((nV + 255) / 256, 148ull * 16);
-            k_hot_keys<<<eg, 256, 0, s>>>(V, desc->row_offsets, pk, pk + nV);
-            bingo_count_launch();
-            CK(cudaGetLastError());
-            bool in1 = false;
-            CK(radix_sort_pairs(pk, pk + nV, pk + 2 * nV, pk + 3 * nV, nV, 32, rtmp, s, &in1));
-            const uint32_t *perm = in1 ? pk + 3 * nV : pk + nV;
             for (int p = 0; p < 3; p++) {
-                k_perm_gather<<<eg, 256, 0, s>>>(V, perm, sz + p * (nV + 1), pbuf);
+                k_perm_gather<<<eg, 256, 0, s>>>(V, hperm, sz + p * (nV + 1), pbuf);
                 bingo_count_launch();
                 CK(cudaGetLastError());
                 CK(exclusive_scan_u64(pbuf, pbuf + (nV + 1), nV, tmp, s));
-                k_perm_scatter<<<eg, 256, 0, s>>>(V, perm, pbuf + (nV + 1), off + p * (nV + 1));
+                k_perm_scatter<<<eg, 256, 0, s>>>(V, hperm, pbuf + (nV + 1), off + p * (nV + 1));
                 bingo_count_launch();
                 CK(cudaGetLastError());
             }
@@ -439,7 +468,7 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
         k_build_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, idesc.bias, g->alpha, g->beta, bs,
                                             g->member_slack, off, off + (nV + 1), off + 2 * (nV + 1), sz, g->hdr, g->thdr,
                                             g->arc, g->arc_epoch, g->bkt, g->gcan, g->mdst, g->midx,
-                                            g->hot_bkt_degree, g->hot_mem_degree);
+                                            g->hot_bkt_degree, g->hot_mem_degree, g->perm, g->inv);
         bingo_count_launch();
         CK(cudaGetLastError());
     }

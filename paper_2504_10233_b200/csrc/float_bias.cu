@@ -19,10 +19,11 @@ namespace bingo {
 
 __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, const double *__restrict__ wf,
                                uint32_t *__restrict__ ibias, DecRec *__restrict__ dec, uint64_t *__restrict__ dcnt_out,
-                               int *__restrict__ flag) {
+                               int *__restrict__ flag, const uint32_t *__restrict__ perm) {
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     const uint32_t lane = lane_id();
-    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < V; j += warps) {
+        const uint32_t u = perm ? perm[j] : j;   // external CSR row of internal vertex j
         const uint64_t b0 = ro[u];
         const uint32_t d = (uint32_t)(ro[u + 1] - b0);
         // input validation: w > 0, finite, <= 1e300
@@ -36,21 +37,21 @@ __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, cons
             continue;
         }
         int chosen = -1, last_valid = -1;
-        for (int j = 0; j < 10 && chosen < 0; j++) {
+        for (int lj = 0; lj < 10 && chosen < 0; lj++) {
             unsigned __int128 wi = 0, wd = 0;
             bool valid = true;
             for (uint32_t i = lane; i < d; i += 32) {
                 uint32_t I;
                 uint64_t D;
-                if (!scale_one(wf[b0 + i], j, I, D)) { valid = false; break; }
+                if (!scale_one(wf[b0 + i], lj, I, D)) { valid = false; break; }
                 wi += I;
                 wd += D;
             }
             if (!__all_sync(0xffffffffu, valid)) break;     // larger lambda only grows s_i
             wi = warp_sum128(wi);
             wd = warp_sum128(wd);
-            last_valid = j;
-            if ((unsigned __int128)(d ? d - 1 : 0) * wd < (wi << 52)) chosen = j;
+            last_valid = lj;
+            if ((unsigned __int128)(d ? d - 1 : 0) * wd < (wi << 52)) chosen = lj;
         }
         if (last_valid < 0 && d > 0) {
             if (lane == 0) atomicOr(flag, 4);
@@ -94,8 +95,8 @@ __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, cons
             r.flags = (uint8_t)fl;
             r.pad = 0;
             r.pad2 = dec_capacity(cnt);   // decimal-member capacity (updates, R-16)
-            dec[u] = r;
-            dcnt_out[u] = dec_capacity(cnt);
+            dec[j] = r;
+            dcnt_out[j] = dec_capacity(cnt);
         }
     }
 }
@@ -104,15 +105,17 @@ __global__ void k_float_lambda(uint32_t V, const uint64_t *__restrict__ ro, cons
 __global__ void k_float_fill(uint32_t V, const uint64_t *__restrict__ ro, const uint32_t *__restrict__ dst,
                              const double *__restrict__ wf, const uint64_t *__restrict__ doff,
                              DecRec *__restrict__ dec, uint4 *__restrict__ dmem, const VHdr *__restrict__ hdr,
-                             uint64_t *__restrict__ arc_dval) {
+                             uint64_t *__restrict__ arc_dval, const uint32_t *__restrict__ perm,
+                             const uint32_t *__restrict__ inv) {
     const uint32_t warps = (blockDim.x >> 5) * gridDim.x;
     const uint32_t lane = lane_id();
-    for (uint32_t u = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < V; u += warps) {
+    for (uint32_t j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; j < V; j += warps) {
+        const uint32_t u = perm ? perm[j] : j;
         const uint64_t b0 = ro[u];
         const uint32_t d = (uint32_t)(ro[u + 1] - b0);
-        const int lam = dec[u].lam;
-        const uint64_t base = doff[u];
-        const uint64_t aoff = hdr[u].adj_off;   // the arc's D travels with it in updates (R-16)
+        const int lam = dec[j].lam;
+        const uint64_t base = doff[j];
+        const uint64_t aoff = hdr[j].adj_off;   // the arc's D travels with it in updates (R-16)
         uint32_t run = 0;
         for (uint32_t c0 = 0; c0 < d; c0 += 32) {
             const uint32_t i = c0 + lane;
@@ -123,10 +126,10 @@ __global__ void k_float_fill(uint32_t V, const uint64_t *__restrict__ ro, const 
                 arc_dval[aoff + i] = D;
             }
             const uint32_t bal = __ballot_sync(0xffffffffu, D != 0);
-            if (D) dmem[base + run + __popc(bal & lanemask_lt())] = make_uint4(i, dst[b0 + i], (uint32_t)D, (uint32_t)(D >> 32));
+            if (D) dmem[base + run + __popc(bal & lanemask_lt())] = make_uint4(i, inv ? inv[dst[b0 + i]] : dst[b0 + i], (uint32_t)D, (uint32_t)(D >> 32));
             run += __popc(bal);
         }
-        if (lane == 0) dec[u].doff = (uint32_t)base;
+        if (lane == 0) dec[j].doff = (uint32_t)base;
     }
 }
 
@@ -143,7 +146,8 @@ bingo_status float_prepare(bingo_graph *g, const bingo_build_desc *desc, uint32_
     const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)V + 7) / 8, 148ull * 64);
     int hflag = 0;
     if (cudaMemsetAsync(g->dev_flag, 0, sizeof(int), s) != cudaSuccess) return BINGO_E_CUDA;
-    k_float_lambda<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->bias_f64, ibias, g->dec, dcnt, g->dev_flag);
+    k_float_lambda<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->bias_f64, ibias, g->dec, dcnt, g->dev_flag,
+                                          g->perm);
     bingo_count_launch();
     if (cudaGetLastError() != cudaSuccess) return BINGO_E_CUDA;
     if (exclusive_scan_u64(dcnt, dscan, V, tmp, s) != cudaSuccess) return BINGO_E_CUDA;
@@ -160,7 +164,7 @@ bingo_status float_fill(bingo_graph *g, const bingo_build_desc *desc, const uint
     const uint32_t V = desc->num_vertices;
     const unsigned blocks = (unsigned)std::min<uint64_t>(((uint64_t)V + 7) / 8, 148ull * 64);
     k_float_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias_f64, dscan, g->dec, g->dmem,
-                                        g->hdr, g->arc_dval);
+                                        g->hdr, g->arc_dval, g->perm, g->inv);
     bingo_count_launch();
     return cudaGetLastError() == cudaSuccess ? BINGO_OK : BINGO_E_CUDA;
 }

@@ -71,13 +71,24 @@ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
 }
 
 // ------------------------------------------------------------------ validate
-__global__ void k_upd_validate(const uint4 *__restrict__ recs, uint64_t n, uint32_t V, uint32_t *__restrict__ keys,
-                               uint32_t *__restrict__ vals, UpdCounters *cnt, bool allow_zero) {
+// validates every record and writes it to `out` with src/dst translated to internal ids
+// (hot-first relabelling; in == out is allowed)
+__global__ void k_upd_validate(const uint4 *in, uint4 *out, uint64_t n, uint32_t V, const uint32_t *__restrict__ inv,
+                               uint32_t *__restrict__ keys, uint32_t *__restrict__ vals, UpdCounters *cnt,
+                               bool allow_zero) {
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint4 r = recs[i];
-        // float mode (R-16): the integer part of an inserted bias may be 0
+        uint4 r = in[i];
+        // float mode (R-16): the integer part of an inserted bias is set later and may be 0
         const bool bad = r.x > 1u || r.y >= V || r.z >= V || (r.x == 0u && r.w == 0u && !allow_zero);
-        if (bad) atomicOr(&cnt->flag, 1);
+        if (bad) {
+            atomicOr(&cnt->flag, 1);
+        } else {
+            if (inv) {
+                r.y = __ldg(inv + r.y);
+                r.z = __ldg(inv + r.z);
+            }
+        }
+        out[i] = r;
         keys[i] = bad ? 0u : r.y;
         vals[i] = (uint32_t)i;
     }
@@ -902,6 +913,7 @@ struct FastArgs {
     MutateArgs m;                     // graph, allocator and policy fields (pointers set in-kernel)
     uint4 recs[FAST_N];               // the batch, inline (host batches need no copy)
     const uint4 *drecs;               // or a device batch
+    const uint32_t *inv;              // external -> internal vertex ids
     uint32_t n, V;
     unsigned long long arc_cap, bkt_cap, mem_units_cap;
     uint32_t *scr;                    // FAST_N * fast_words() words
@@ -928,9 +940,16 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
     __syncthreads();
     // validation (whole batch, before anything else)
     if (tid < n) {
-        const uint4 r = recs[tid];
-        if (r.x > 1u || r.y >= fa.V || r.z >= fa.V || (r.x == 0u && r.w == 0u)) atomicOr(&flag, FAST_INVAL);
+        uint4 r = recs[tid];
+        if (r.x > 1u || r.y >= fa.V || r.z >= fa.V || (r.x == 0u && r.w == 0u)) {
+            atomicOr(&flag, FAST_INVAL);
+        } else if (fa.inv) {   // internal vertex ids from here on
+            r.y = fa.inv[r.y];
+            r.z = fa.inv[r.z];
+            recs[tid] = r;
+        }
     }
+    __syncthreads();
     // stable grouping by src: rank = #{j : src_j < src_i, or src_j == src_i and j < i}
     if (tid < n) {
         const uint32_t si = recs[tid].y;
@@ -1200,6 +1219,7 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
     }
     fa.n = (uint32_t)n;
     fa.V = g->V;
+    fa.inv = g->inv;
     fa.arc_cap = g->arc_cap;
     fa.bkt_cap = g->bkt_cap;
     fa.mem_units_cap = g->mem_cap / 4;
@@ -1565,17 +1585,19 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     double *dwf = cv.take<double>(n);
     uint32_t *fdoff = cv.take<uint32_t>(n), *fdcap = cv.take<uint32_t>(n);
 
-    const uint4 *recs = reinterpret_cast<const uint4 *>(batch);
+    // records are validated into drec with internal vertex ids (the caller's batch is never written)
+    const uint4 *src_recs = reinterpret_cast<const uint4 *>(batch);
     if (flags & BINGO_UPD_HOST_BATCH) {
         UCK(cudaMemcpyAsync(drec, batch, 16 * n, cudaMemcpyHostToDevice, s));
-        recs = drec;
-    } else if (fm) {   // float mode rewrites the bias fields: work on a copy
-        UCK(cudaMemcpyAsync(drec, batch, 16 * n, cudaMemcpyDeviceToDevice, s));
-        recs = drec;
+        src_recs = drec;
     }
+    const uint4 *recs = drec;
     UCK(cudaMemsetAsync(dc, 0, sizeof(UpdCounters), s));
     UCK(cudaMemsetAsync(dstats, 0, 8 * 32, s));
     const unsigned gb = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
+    k_upd_validate<<<gb, 256, 0, s>>>(src_recs, drec, n, g->V, g->inv, k0, v0, dc, fm);
+    bingo_count_launch();
+    UCK(cudaGetLastError());
     DinsGuard dguard{g};
     if (fm) {
         const double *w = wf;
@@ -1588,9 +1610,6 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
         UCK(cudaGetLastError());
         g->cur_dins = dins;
     }
-    k_upd_validate<<<gb, 256, 0, s>>>(recs, n, g->V, k0, v0, dc, fm);
-    bingo_count_launch();
-    UCK(cudaGetLastError());
     bool in1 = false;
     UCK(radix_sort_pairs(k0, v0, k1, v1, n, key_bits_for(g->V), rtmp, s, &in1));
     const uint32_t *sk = in1 ? k1 : k0;

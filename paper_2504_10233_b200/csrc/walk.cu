@@ -23,12 +23,13 @@ namespace bingo {
 template <int APP, bool PROF, bool WMAJOR>
 __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint32_t &w, uint32_t &u) {
     w = a.first_walker + (uint32_t)i;
-    u = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);
+    const uint32_t u0 = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);   // external
+    u = a.inv ? __ldg(a.inv + u0) : u0;
     if (a.paths) {
-        if (WMAJOR) a.paths[i * ((size_t)a.L + 1)] = u;
-        else __stcs(&a.paths[i], u);
+        if (WMAJOR) a.paths[i * ((size_t)a.L + 1)] = u0;
+        else __stcs(&a.paths[i], u0);
     }
-    if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[u], 1ull);
+    if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
 }
 
 #ifndef BINGO_WALK_MINB
@@ -106,9 +107,10 @@ __global__ void __launch_bounds__(256, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO
                         o++;
                     } else {
                         if (PROF) prof.steps++;
-                        if (a.paths) {
-                            if (WMAJOR) a.paths[i * row + t + 1] = next;
-                            else __stcs(&a.paths[(size_t)(t + 1) * a.W + i], next);
+                        if (a.paths) {   // paths hold external ids
+                            const uint32_t xn = a.perm ? __ldg(a.perm + next) : next;
+                            if (WMAJOR) a.paths[i * row + t + 1] = xn;
+                            else __stcs(&a.paths[(size_t)(t + 1) * a.W + i], xn);
                         }
                         prev = u;
                         prev_nbo = cur_nbo;
@@ -116,7 +118,16 @@ __global__ void __launch_bounds__(256, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO
                         o = 0;
                         if (APP == BINGO_PPR) {
 #ifndef BINGO_EXP_NO_VISIT       // measurement experiment only: skip the visit counts
-                            if (a.visit) atomicAdd(&a.visit[u], 1ull);
+#ifndef BINGO_VISIT_PLAIN          // one atomic per distinct vertex per warp iteration (A/B: plain)
+                            if (a.visit) {
+                                const unsigned act = __activemask();
+                                const unsigned same = __match_any_sync(act, u);
+                                if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u))
+                                    atomicAdd(&a.visit[visit_slot(u)], (unsigned long long)__popc(same));
+                            }
+#else
+                            if (a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
+#endif
 #endif
                             if (PROF) prof.visit++;
                             if (a.stop_always) {
@@ -223,6 +234,8 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     a.dmem = g->dmem;
     a.visit = g->visit;
     a.starts = starts;
+    a.perm = g->perm;
+    a.inv = g->inv;
     a.paths = paths;
     a.lengths = lengths;
     a.W = W;
@@ -395,16 +408,37 @@ extern "C" bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc
     return st;
 }
 
+// counts in external vertex order: out[u] = visit[inv[u]]
+__global__ void k_visit_gather(uint32_t V, const uint32_t *__restrict__ inv, const unsigned long long *__restrict__ visit,
+                               unsigned long long *__restrict__ out) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) out[u] = visit[visit_slot(inv ? inv[u] : u)];
+}
+
 extern "C" bingo_status bingo_visit_counts(bingo_graph *g, uint64_t *counts, int reset, uint32_t flags, void *stream) {
     if (!g) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
     const size_t bytes = sizeof(uint64_t) * g->V;
-    if (counts && g->V)
-        e = cudaMemcpyAsync(counts, g->visit, bytes,
-                            (flags & BINGO_COUNTS_HOST) ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, s);
-    if (e == cudaSuccess && reset && g->V) e = cudaMemsetAsync(g->visit, 0, bytes, s);
+    if (counts && g->V) {
+        unsigned long long *dst = reinterpret_cast<unsigned long long *>(counts);
+        if (flags & BINGO_COUNTS_HOST) {   // gather into the walk staging buffer, then D2H
+            if (g->wscratch_bytes < bytes) {
+                bingo_dev_free(g, g->wscratch);
+                g->wscratch = bingo_dev_alloc(g, bytes);
+                g->wscratch_bytes = g->wscratch ? bytes : 0;
+                if (!g->wscratch) return BINGO_E_NOMEM;
+            }
+            dst = (unsigned long long *)g->wscratch;
+        }
+        k_visit_gather<<<(unsigned)std::min<uint64_t>((g->V + 255) / 256, 148ull * 16), 256, 0, s>>>(g->V, g->inv,
+                                                                                                   g->visit, dst);
+        bingo_count_launch();
+        e = cudaGetLastError();
+        if (e == cudaSuccess && (flags & BINGO_COUNTS_HOST))
+            e = cudaMemcpyAsync(counts, dst, bytes, cudaMemcpyDeviceToHost, s);
+    }
+    if (e == cudaSuccess && reset && g->V) e = cudaMemsetAsync(g->visit, 0, 8 * visit_words(g->V), s);
     if (e == cudaSuccess && (flags & BINGO_COUNTS_HOST)) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) {
         g->poisoned = 1;

@@ -38,6 +38,7 @@ struct WalkArgs {
     const uint4 *dmem;
     unsigned long long *visit;
     const uint32_t *starts;
+    const uint32_t *perm, *inv;   // internal <-> external vertex ids (paths and starts are external)
     uint32_t *paths;
     uint32_t *lengths;
     uint32_t W, V, L, first_walker;
