@@ -345,11 +345,28 @@ def main():
             torch.cuda.synchronize()
             lat_host.append(1e6 * (t1 - t0))
             lat_dev.append(1e3 * e0.elapsed_time(e1))
+        # the same C-ABI call without the Python wrapper (ctypes directly on pre-packed records):
+        # the library's own per-record latency, host call to completion
+        from paper_2504_10233_b200 import bingo as bb
+        packed = np.ascontiguousarray(w.batches[-2][:300], dtype=np.uint32)
+        lib, h, sp = bb._lib(), g.handle, stream.cuda_stream
+        base = packed.ctypes.data
+        lat_c = []
+        for i in range(len(packed)):
+            t0 = time.perf_counter()
+            rc = lib.bingo_apply_updates(h, base + 16 * i, 1, bb.UPD_HOST_BATCH, None, sp)
+            lat_c.append(1e6 * (time.perf_counter() - t0))
+            assert rc == 0, rc
         streaming = {"records": len(recs), "call_us_p50": float(np.percentile(lat_host, 50)),
                      "call_us_p99": float(np.percentile(lat_host, 99)),
                      "device_us_p50": float(np.percentile(lat_dev, 50)),
                      "device_us_p99": float(np.percentile(lat_dev, 99)),
-                     "note": "one bingo_apply_updates call per arc record (epoch per record), c2 graph"}
+                     "abi_call_us_p50": float(np.percentile(lat_c, 50)),
+                     "abi_call_us_p99": float(np.percentile(lat_c, 99)),
+                     "abi_updates_per_s": float(len(lat_c) / (1e-6 * sum(lat_c))),
+                     "note": "one bingo_apply_updates call per arc record (epoch per record), c2 graph; call_us: "
+                             "through the Python binding; abi_call_us: the C-ABI call via ctypes, host to "
+                             "completion (the library synchronises)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

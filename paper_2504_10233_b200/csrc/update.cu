@@ -982,7 +982,8 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
     __syncthreads();
     const uint32_t nt = ntouch;
     // plan, one warp per touched vertex
-    for (uint32_t t = w; t < nt; t += 32) {
+    const uint32_t nw = blockDim.x >> 5;   // launched with 32 * clamp(n, 2, 32) threads
+    for (uint32_t t = w; t < nt; t += nw) {
         const VHdr h = fa.m.hdr[tv[t]];
         const PlanOut o = plan_vertex(recs, sval, seg[t], seg[t + 1], h, fa.m.bkt, fa.m.gcan, fa.m.alpha, fa.m.bs,
                                       fa.m.arc_slack, fa.m.mem_slack);
@@ -1024,7 +1025,7 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
         a.scr_off = reinterpret_cast<const uint64_t *>(scr_off);
         a.scr = fa.scr;
         a.vstats = fa.vstats;
-        for (uint32_t t = w; t < nt; t += 32) mutate_vertex<32>(a, t, sm[w]);
+        for (uint32_t t = w; t < nt; t += nw) mutate_vertex<32>(a, t, sm[w]);
     }
     __syncthreads();
     if (tid == 0) {
@@ -1229,7 +1230,9 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
     fa.out = (FastOut *)g->fast_out_dev;
     FastOut *ho = (FastOut *)g->fast_out_host;
     ho->status = 0xFFFFFFFFu;
-    k_upd_fast<<<1, 1024, 0, s>>>(fa);
+    // one warp per touched vertex at most (a vertex's records go to one warp): small
+    // blocks keep the block-wide barriers of the single-record case cheap
+    k_upd_fast<<<1, 32 * (unsigned)std::min<uint64_t>(32, std::max<uint64_t>(2, n)), 0, s>>>(fa);
     bingo_count_launch();
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
