@@ -43,6 +43,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-walkers", type=int, default=1 << 18)
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N > 1 (gloo: test the multi-rank path without NVLink)")
+    ap.add_argument("--share-device", action="store_true",
+                    help="test only: every rank on cuda:0 (exercise the N > 1 code path on a 1-GPU box)")
     ap.add_argument("--layout", default="step", choices=["walker", "step"],
                     help="path layout written by the walk (walker-major: one contiguous walk per walker)")
     return ap.parse_args()
@@ -205,10 +209,15 @@ def main():
         return
     import torch
     ws, rank, local, dist = dist_setup(args)
+    if args.share_device:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if dist is not None:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     import paper_2504_10233_b200 as pb
     from paper_2504_10233_b200 import bingo
 
