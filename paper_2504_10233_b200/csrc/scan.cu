@@ -1,5 +1,5 @@
-// scan.cu -- three-phase exclusive scan over u64 (tile reduce, scan of tile
-// sums, tile scan + carry).  Tiles of 2048 elements (256 threads x 8).
+// scan.cu -- single-pass exclusive scan over u64 (decoupled look-back).
+// Tiles of 2048 elements (256 threads x 8).
 #include "scan.cuh"
 #include "bingo_internal.cuh"
 
@@ -10,9 +10,8 @@ static constexpr int SCAN_ITEMS = 8;
 static constexpr uint64_t SCAN_TILE = SCAN_THREADS * SCAN_ITEMS;
 
 size_t scan_tmp_words(uint64_t n) {
-    uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (tiles <= 1) return 1;
-    return (size_t)(tiles + (tiles + 1)) + scan_tmp_words(tiles);
+    const uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    return (size_t)(tiles + 2);   // look-back status per tile + the tile counter
 }
 
 __device__ __forceinline__ uint64_t block_exclusive(uint64_t v, uint64_t *total) {
@@ -43,19 +42,6 @@ __device__ __forceinline__ uint64_t block_exclusive(uint64_t v, uint64_t *total)
     return r;
 }
 
-__global__ void k_tile_reduce(const uint64_t *__restrict__ in, uint64_t n, uint64_t *__restrict__ sums) {
-    uint64_t base = (uint64_t)blockIdx.x * SCAN_TILE;
-    uint64_t acc = 0;
-#pragma unroll
-    for (int j = 0; j < SCAN_ITEMS; j++) {
-        uint64_t i = base + (uint64_t)threadIdx.x * SCAN_ITEMS + j;
-        if (i < n) acc += in[i];
-    }
-    __shared__ uint64_t tot;
-    block_exclusive(acc, &tot);
-    if (threadIdx.x == 0) sums[blockIdx.x] = tot;
-}
-
 // tile scan with optional carry-in array (per tile) ; writes total at out[n]
 __global__ void k_tile_scan(const uint64_t *__restrict__ in, uint64_t *__restrict__ out, uint64_t n,
                             const uint64_t *__restrict__ carry) {
@@ -79,24 +65,83 @@ __global__ void k_tile_scan(const uint64_t *__restrict__ in, uint64_t *__restric
     if (blockIdx.x == gridDim.x - 1 && threadIdx.x == SCAN_THREADS - 1) out[n] = pre;
 }
 
+// Single-pass exclusive scan (decoupled look-back): tiles take ids from an atomic
+// counter in launch order, publish their aggregate, then their inclusive prefix once
+// the look-back over predecessors is resolved.  One kernel instead of three.
+// Status word: bits 63..62 = flag (1 aggregate, 2 inclusive prefix), 61..0 = value
+// (every scanned quantity here is < 2^62).  tmp: [tiles] status words + counter.
+static constexpr uint64_t ST_A = 1ull << 62, ST_P = 2ull << 62, ST_V = (1ull << 62) - 1;
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const uint64_t *__restrict__ in,
+                                                                uint64_t *__restrict__ out, uint64_t n,
+                                                                unsigned long long *status, unsigned *counter) {
+    __shared__ unsigned s_tile;
+    __shared__ uint64_t s_excl, tot;
+    if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
+    __syncthreads();
+    const uint64_t tile = s_tile;
+    const uint64_t base = tile * SCAN_TILE;
+    uint64_t v[SCAN_ITEMS];
+    uint64_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; j++) {
+        const uint64_t i = base + (uint64_t)threadIdx.x * SCAN_ITEMS + j;
+        v[j] = i < n ? in[i] : 0;
+        acc += v[j];
+    }
+    uint64_t pre = block_exclusive(acc, &tot);
+    if (threadIdx.x == 0) {
+        volatile unsigned long long *st = status;
+        uint64_t excl = 0;
+        if (tile == 0) {
+            st[0] = ST_P | (tot & ST_V);
+        } else {
+            st[tile] = ST_A | (tot & ST_V);
+            __threadfence();
+            uint64_t j = tile - 1;
+            unsigned spins = 0;
+            for (;;) {
+                const unsigned long long w = st[j];
+                const unsigned long long f = w & ~ST_V;
+                if (f == 0) {   // predecessor not published yet (it started earlier: it will)
+                    if (++spins > (1u << 28)) __trap();   // never hang the device silently
+                    continue;
+                }
+                excl += w & ST_V;
+                if (f == ST_P || j == 0) break;
+                j--;
+            }
+            __threadfence();
+            st[tile] = ST_P | ((excl + tot) & ST_V);
+        }
+        s_excl = excl;
+    }
+    __syncthreads();
+    pre += s_excl;
+#pragma unroll
+    for (int j = 0; j < SCAN_ITEMS; j++) {
+        const uint64_t i = base + (uint64_t)threadIdx.x * SCAN_ITEMS + j;
+        if (i < n) out[i] = pre;
+        pre += v[j];
+    }
+    if (base + SCAN_TILE >= n && threadIdx.x == SCAN_THREADS - 1) out[n] = pre;   // the last tile: the total
+}
+
 cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp, cudaStream_t s) {
     if (n == 0) {
         return cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
     }
-    uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    const uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (tiles == 1) {
         k_tile_scan<<<1, SCAN_THREADS, 0, s>>>(in, out, n, nullptr);
         bingo_count_launch();
         return cudaGetLastError();
     }
-    uint64_t *sums = tmp;               // [tiles]
-    uint64_t *sums_scan = tmp + tiles + 1; // [tiles + 1]
-    uint64_t *rest = sums_scan + tiles + 1;
-    k_tile_reduce<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, sums);
-    bingo_count_launch();
-    cudaError_t e = exclusive_scan_u64(sums, sums_scan, tiles, rest, s);
+    unsigned long long *status = reinterpret_cast<unsigned long long *>(tmp);
+    unsigned *counter = reinterpret_cast<unsigned *>(tmp + tiles);
+    cudaError_t e = cudaMemsetAsync(tmp, 0, sizeof(uint64_t) * (tiles + 1), s);
     if (e != cudaSuccess) return e;
-    k_tile_scan<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, sums_scan);
+    k_scan_lookback<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, status, counter);
     bingo_count_launch();
     return cudaGetLastError();
 }

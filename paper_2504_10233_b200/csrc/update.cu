@@ -24,6 +24,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
 
 #include "bingo.h"
 #include "bingo_internal.cuh"
@@ -1165,6 +1166,37 @@ static bingo_status upd_cuda_fail(bingo_graph *g, cudaError_t e, const char *w) 
         if (e_ != cudaSuccess) return upd_cuda_fail(g, e_, #call);  \
     } while (0)
 
+// BINGO_UPD_TRACE=1: device (CUDA events) and host timestamps at the phase boundaries of
+// one bingo_apply_updates call, printed to stderr (measurement only)
+struct UpdTrace {
+    bool on = false;
+    int n = 0;
+    const char *tag[24];
+    cudaEvent_t ev[24];
+    std::chrono::steady_clock::time_point ht[24];
+    void mark(const char *t, cudaStream_t s) {
+        if (!on || n >= 24) return;
+        tag[n] = t;
+        cudaEventCreate(&ev[n]);
+        cudaEventRecord(ev[n], s);
+        ht[n] = std::chrono::steady_clock::now();
+        n++;
+    }
+    void dump() {
+        if (!on || !n) return;
+        cudaEventSynchronize(ev[n - 1]);
+        for (int i = 1; i < n; i++) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            const double hus = std::chrono::duration<double, std::micro>(ht[i] - ht[i - 1]).count();
+            fprintf(stderr, "upd-trace %-24s device %8.1f us  host %8.1f us\n", tag[i], 1e3 * ms, hus);
+        }
+        for (int i = 0; i < n; i++) cudaEventDestroy(ev[i]);
+        n = 0;
+    }
+};
+static UpdTrace g_trace;
+
 static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
     const bool bs = (g->flags & BINGO_BUILD_BS_MODE) != 0;
     ma.hdr = g->hdr;
@@ -1405,8 +1437,10 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         k_bsp_totals<<<1, 32, 0, s>>>(a, dc, scr_off, dt);
         bingo_count_launch();
         UCK(cudaGetLastError());
+        g_trace.mark("plan+scans", s);
         UCK(cudaMemcpyAsync(ht, dt, sizeof(BspTotals), cudaMemcpyDeviceToHost, s));
         UCK(cudaStreamSynchronize(s));
+        g_trace.mark("sync plan totals", s);
         if (!multi) {
             const bingo_status st = check_capacity(g, ht->c, ht->bump, s);
             if (st != BINGO_OK) return st;
@@ -1442,6 +1476,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             UCK(cudaGetLastError());                                 \
         } while (0)
         BSP_LAUNCH(k_bsp_alloc_insert, warp_grid(nt, WG), s, a);
+        g_trace.mark("alloc_insert", s);
         // two independent chains over disjoint vertex sets (shared state: bump
         // counters, atomics only): small vertices on `s`, large ones on the side stream
         const bool side = ht->bigs != 0;
@@ -1479,10 +1514,12 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         // -- small vertices
         if (ht->scr) BSP_LAUNCH(k_bsp_finalize, warp_grid(nt, WG), s, a, false);
         BSP_LAUNCH(k_bsp_rebuild, warp_grid(nt, WG), s, a);
+        g_trace.mark("small-vertex chain", s);
         if (side) {
             UCK(cudaEventRecord(g->ev_join, sh));
             UCK(cudaStreamWaitEvent(s, g->ev_join, 0));
         }
+        g_trace.mark("join hub chain", s);
         if (g->nbt) BSP_LAUNCH(k_bsp_nb_incr, warp_grid(nt, WG), s, a);
         if (g->nbt && all) {
             BSP_LAUNCH(k_bsp_nb_clear, warp_grid(all, IG), s, a, all);
@@ -1542,6 +1579,8 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     if (n && g->float_mode != (wf != nullptr)) return BINGO_E_INVAL;
     if (n >= 0xFFFFFFFFull) return BINGO_E_INVAL;
     const bool fm = g->float_mode;
+    g_trace.on = getenv("BINGO_UPD_TRACE") != nullptr;
+    g_trace.mark("start", (cudaStream_t)stream);
     cudaStream_t s = (cudaStream_t)stream;
     if (stats) memset(stats, 0, sizeof(*stats));
     if (n == 0) {
@@ -1625,8 +1664,10 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     bingo_count_launch();
     UCK(cudaGetLastError());
     uint64_t ntouch = 0;
+    g_trace.mark("front (validate+sort+seg)", s);
     UCK(cudaMemcpyAsync(&ntouch, head_ex + n, 8, cudaMemcpyDeviceToHost, s));
     UCK(cudaStreamSynchronize(s));
+    g_trace.mark("sync #touched", s);
     const uint32_t e = g->epoch + 1;
     if (fm && ntouch) {
         // decimal-member regions for the batch; validation errors and pool growth before any mutation
@@ -1765,8 +1806,11 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
 static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
                                  const unsigned long long *dstats, bingo_update_stats *stats, cudaStream_t s) {
     unsigned long long hs[32];
+    g_trace.mark("tail (nb, stats)", s);
     UCK(cudaMemcpyAsync(hs, dstats, sizeof(hs), cudaMemcpyDeviceToHost, s));
     UCK(cudaStreamSynchronize(s));
+    g_trace.mark("sync stats", s);
+    g_trace.dump();
     g->epoch = e;
     // inserted = number of insert records (validated batch)
     uint64_t inserted = 0;
