@@ -8,6 +8,7 @@ entry point raises.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 from typing import Optional
@@ -119,17 +120,24 @@ def _check(st: int, where: str):
         raise BingoError(st, where)
 
 
+_TORCH = None
+
+
 def _torch():
-    import torch
-    if not torch.cuda.is_available():
-        raise RuntimeError("paper_2504_10233_b200 needs a CUDA device (B200); there is no CPU fallback")
-    return torch
+    global _TORCH
+    if _TORCH is None:
+        import torch
+        if not torch.cuda.is_available():
+            raise RuntimeError("paper_2504_10233_b200 needs a CUDA device (B200); there is no CPU fallback")
+        _TORCH = torch
+    return _TORCH
 
 
 def _stream_ptr(stream) -> Optional[int]:
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+    if stream is None:   # the current stream's raw handle without building a Stream object
+        return torch._C._cuda_getCurrentRawStream(torch.cuda.current_device())
+    return stream.cuda_stream
 
 
 def _dev_u32(x, torch, device):
@@ -255,7 +263,8 @@ class Graph:
             b = arr
             if bias_f64 is not None:
                 wf = np.ascontiguousarray(bias_f64, dtype=np.float64)
-        with torch.cuda.device(self.device):
+        same = self.device.index is None or torch.cuda.current_device() == self.device.index
+        with contextlib.nullcontext() if same else torch.cuda.device(self.device):
             if wf is None:
                 rc = _lib().bingo_apply_updates(self._h, ptr, n, flags, ctypes.byref(st), _stream_ptr(stream))
             else:
