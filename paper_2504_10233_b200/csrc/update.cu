@@ -1186,10 +1186,12 @@ struct UpdTrace {
         if (!on || !n) return;
         cudaEventSynchronize(ev[n - 1]);
         for (int i = 1; i < n; i++) {
-            float ms = 0;
+            float ms = 0, at = 0;
             cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+            cudaEventElapsedTime(&at, ev[0], ev[i]);
             const double hus = std::chrono::duration<double, std::micro>(ht[i] - ht[i - 1]).count();
-            fprintf(stderr, "upd-trace %-24s device %8.1f us  host %8.1f us\n", tag[i], 1e3 * ms, hus);
+            fprintf(stderr, "upd-trace %-26s at %8.1f us  (+%7.1f device, +%7.1f host)\n", tag[i], 1e3 * at, 1e3 * ms,
+                    hus);
         }
         for (int i = 0; i < n; i++) cudaEventDestroy(ev[i]);
         n = 0;
@@ -1424,7 +1426,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         a.t0 = (uint32_t)t0;
         a.nt = (uint32_t)std::min<uint64_t>(maxt, ntouch - t0);
         const uint32_t nt = a.nt;
-        UCK(cudaMemsetAsync(a.nhubs, 0, 8, s));
+        UCK(cudaMemsetAsync(a.nhubs, 0, 16, s));   // hubs, bigs, rebuild fills
         k_bsp_plan<<<warp_grid(nt, WG), MT, 0, s>>>(a, scr_need, dc, !multi, true);
         bingo_count_launch();
         UCK(cudaGetLastError());
@@ -1495,21 +1497,26 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         if (sel) {
             BSP_LAUNCH(k_bsp_select, warp_grid(sel, IG), sh, a, sel);
             BSP_LAUNCH(k_bsp_finalize, warp_grid(ht->hubs, WG), sh, a, true);
+            g_trace.mark("hub: select+finalize", sh);
             BSP_LAUNCH(k_bsp_hole_count, warp_grid(sel, IG), sh, a, sel);
             UCK(exclusive_scan_u64(a.icnt, const_cast<uint64_t *>(a.ipref), sel, itmp, sh));
             BSP_LAUNCH(k_bsp_hole_write, warp_grid(sel, IG), sh, a, sel);
             BSP_LAUNCH(k_bsp_tail, warp_grid(ht->hubs, WG), sh, a);
+            g_trace.mark("hub: holes+tail", sh);
             if (grp) {
                 BSP_LAUNCH(k_bsp_grp_count, warp_grid(grp, IG), sh, a, grp);
                 UCK(exclusive_scan_u64(a.gcnt, const_cast<uint64_t *>(a.gpref), grp, itmp, sh));
                 BSP_LAUNCH(k_bsp_grp_write, warp_grid(grp, IG), sh, a, grp);
                 BSP_LAUNCH(k_bsp_grp_tail, warp_grid(ht->hubs, WG), sh, a);
+                g_trace.mark("hub: group fronts+tails", sh);
             }
         }
         if (ht->bigs) {
-            k_bsp_rebuild_big<<<(unsigned)std::min<uint64_t>(ht->bigs, 148 * 2), LT, 0, sh>>>(a);
+            BSP_LAUNCH(k_bsp_rebuild_big, warp_grid(ht->bigs, WG), sh, a);
+            k_bsp_rebuild_fill<<<(unsigned)std::min<uint64_t>(ht->bigs, 148 * 2), LT, 0, sh>>>(a);
             bingo_count_launch();
             UCK(cudaGetLastError());
+            g_trace.mark("hub: rebuild_big", sh);
         }
         // -- small vertices
         if (ht->scr) BSP_LAUNCH(k_bsp_finalize, warp_grid(nt, WG), s, a, false);

@@ -905,56 +905,84 @@ __global__ void __launch_bounds__(MT) k_bsp_rebuild(const BspArgs a) {
     }
 }
 
-// large vertices (L > CH): one 1024-thread block each; the fill/find scan is split
+// large vertices (L > CH): one warp each for the reclassification, the alias and the
+// writes (a block per vertex left 31 warps idle behind barriers: 0.9 ms per c4 batch);
+// the few that need an adjacency scan (a group turning into a list, or a ONE group
+// whose member must be found) save their stage-A state in the gk slots and are
+// finished by k_bsp_rebuild_fill, one block each
+__global__ void __launch_bounds__(MT) k_bsp_rebuild_big(const BspArgs a) {
+    const uint32_t lane = lane_id();
+    BSP_WARP_LOOP(h, *a.nbigs) {
+        const uint32_t i = a.bigs[h];
+        RbLane r;
+        uint32_t fm, fd;
+        rebuild_classify(a, i, r, fm, fd);
+        if (!(fm | fd)) {
+            rebuild_write(a, i, r);
+            continue;
+        }
+        gkp(a, GK_KIND0, i)[lane] = r.kind1;
+        gkp(a, GK_C, i)[lane] = r.cn;
+        gkp(a, GK_MOFF, i)[lane] = r.moff;
+        gkp(a, GK_CAP, i)[lane] = r.cap;
+        gkp(a, GK_ONE, i)[lane] = r.one;
+        gkp(a, GK_INSK, i)[lane] = lane == 0 ? fm : fd;
+        if (lane == 0) a.hubs[atomicAdd(a.nhubs + 2, 1u)] = i;   // hubs[] is free again by now
+    }
+}
+
+// large vertices with a fill/find scan: one 1024-thread block each; the scan is split
 // over the 32 warps (count pass, per-group scan over warps, write pass)
-__global__ void __launch_bounds__(LT) k_bsp_rebuild_big(const BspArgs a) {
+__global__ void __launch_bounds__(LT) k_bsp_rebuild_fill(const BspArgs a) {
     __shared__ RbLane s_r[32];
     __shared__ uint32_t s_fm, s_fd;
     __shared__ uint32_t s_cnt[32][33];     // [warp][group], then exclusive prefixes
     __shared__ uint32_t s_first[32][33];
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
-    for (uint32_t h = blockIdx.x; h < *a.nbigs; h += gridDim.x) {
-        const uint32_t i = a.bigs[h];
+    for (uint32_t h = blockIdx.x; h < a.nhubs[2]; h += gridDim.x) {
+        const uint32_t i = a.hubs[h];
         if (w == 0) {
             RbLane r;
-            uint32_t fm, fd;
-            rebuild_classify(a, i, r, fm, fd);
+            r.kind1 = gkp(a, GK_KIND0, i)[lane];
+            r.cn = gkp(a, GK_C, i)[lane];
+            r.moff = gkp(a, GK_MOFF, i)[lane];
+            r.cap = gkp(a, GK_CAP, i)[lane];
+            r.one = gkp(a, GK_ONE, i)[lane];
             s_r[lane] = r;
-            if (lane == 0) { s_fm = fm; s_fd = fd; }
+            if (lane == 0) s_fm = gkp(a, GK_INSK, i)[0];
+            if (lane == 1) s_fd = gkp(a, GK_INSK, i)[1];
         }
         __syncthreads();
         const uint32_t fm = s_fm, fd = s_fd;
-        if (fm | fd) {
-            const uint32_t dn = a.vL[i] - a.vN[i];
-            const uint64_t aoff = a.vaoff[i];
-            const uint32_t seg = ((dn + 32 * 32 - 1) / (32 * 32)) * 32;   // positions per warp, multiple of 32
-            const uint32_t pb = min(dn, w * seg), pe = min(dn, pb + seg);
-            const uint32_t moff_l = s_r[lane].moff;
-            uint32_t cnt = 0, first = 0xFFFFFFFFu;
-            fill_scan(a.g, aoff, pb, pe, fm, 0u, moff_l, true, cnt, first);
-            s_cnt[w][lane] = cnt;
-            __syncthreads();
-            if (w == 0) {
-                uint32_t acc = 0;
-                for (uint32_t j = 0; j < 32; j++) {
-                    const uint32_t c = s_cnt[j][lane];
-                    s_cnt[j][lane] = acc;
-                    acc += c;
-                }
+        const uint32_t dn = a.vL[i] - a.vN[i];
+        const uint64_t aoff = a.vaoff[i];
+        const uint32_t seg = ((dn + 32 * 32 - 1) / (32 * 32)) * 32;   // positions per warp, multiple of 32
+        const uint32_t pb = min(dn, w * seg), pe = min(dn, pb + seg);
+        const uint32_t moff_l = s_r[lane].moff;
+        uint32_t cnt = 0, first = 0xFFFFFFFFu;
+        fill_scan(a.g, aoff, pb, pe, fm, 0u, moff_l, true, cnt, first);
+        s_cnt[w][lane] = cnt;
+        __syncthreads();
+        if (w == 0) {
+            uint32_t acc = 0;
+            for (uint32_t j = 0; j < 32; j++) {
+                const uint32_t c = s_cnt[j][lane];
+                s_cnt[j][lane] = acc;
+                acc += c;
             }
-            __syncthreads();
-            cnt = s_cnt[w][lane];
-            first = 0xFFFFFFFFu;
-            fill_scan(a.g, aoff, pb, pe, fm, fd, moff_l, false, cnt, first);
-            s_first[w][lane] = first;
-            __syncthreads();
-            if (w == 0 && ((fd >> lane) & 1u)) {
-                uint32_t f = 0xFFFFFFFFu;
-                for (uint32_t j = 0; j < 32; j++) f = min(f, s_first[j][lane]);
-                s_r[lane].one = f;
-            }
-            __syncthreads();
         }
+        __syncthreads();
+        cnt = s_cnt[w][lane];
+        first = 0xFFFFFFFFu;
+        fill_scan(a.g, aoff, pb, pe, fm, fd, moff_l, false, cnt, first);
+        s_first[w][lane] = first;
+        __syncthreads();
+        if (w == 0 && ((fd >> lane) & 1u)) {
+            uint32_t f = 0xFFFFFFFFu;
+            for (uint32_t j = 0; j < 32; j++) f = min(f, s_first[j][lane]);
+            s_r[lane].one = f;
+        }
+        __syncthreads();
         if (w == 0) rebuild_write(a, i, s_r[lane]);
         __syncthreads();
     }
