@@ -47,6 +47,8 @@ def parse():
                     help="torch.distributed backend for N > 1 (gloo: test the multi-rank path without NVLink)")
     ap.add_argument("--share-device", action="store_true",
                     help="test only: every rank on cuda:0 (exercise the N > 1 code path on a 1-GPU box)")
+    ap.add_argument("--e2e-layout", default="step", choices=["walker", "step"],
+                    help="path layout of the e2e pass (walker-major: one contiguous D2H per chunk)")
     ap.add_argument("--layout", default="step", choices=["walker", "step"],
                     help="path layout written by the walk (walker-major: one contiguous walk per walker)")
     return ap.parse_args()
@@ -311,7 +313,8 @@ def main():
     # ---- e2e through the C-ABI with HOST buffers (pinned): H2D batch + D2H paths each step
     e2e = None
     if e2e_steps:
-        hp = torch.empty((L + 1, V), dtype=torch.int32).pin_memory()
+        ewm = args.e2e_layout == "walker"
+        hp = torch.empty((V, L + 1) if ewm else (L + 1, V), dtype=torch.int32).pin_memory()
         hl = torch.empty(V, dtype=torch.int32).pin_memory()
         hb = [b.pin_memory() for b in batches[W + K:W + K + e2e_steps]]
         torch.cuda.synchronize()
@@ -323,7 +326,7 @@ def main():
         for k in range(e2e_steps):
             g.apply_updates(hb[k].numpy())
             g.walk_host(app=pb.DEEPWALK, length=L, seed=5000 + k, first_walker=first, num_walkers=V,
-                        paths=hp, lengths=hl)
+                        paths=hp, lengths=hl, walker_major=ewm)
             tot += int(hl.numpy().astype(np.int64).sum())
         e1.record(stream)
         torch.cuda.synchronize()
@@ -337,6 +340,7 @@ def main():
             tot = int(s)
         e2e = {"value": tot / (e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": int(nrec * 16),
                "d2h_bytes_per_step": int(4 * V * (L + 2)), "steps": e2e_steps,
+               "path_layout": "walker-major" if ewm else "step-major",
                "note": "bingo_apply_updates(HOST batch) + bingo_walk(HOST_OUTPUT paths+lengths), pinned"}
 
     # ---- a11: streaming single-record updates (synchronous C-ABI calls, host batch)
