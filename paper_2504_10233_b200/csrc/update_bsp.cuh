@@ -30,6 +30,12 @@
 
 namespace bingo {
 
+// minimum resident blocks for the latency-bound warp-per-vertex / chunk-item kernels
+// (more warps in flight hide the dependent round trips of each vertex)
+#ifndef BINGO_BSP_MINB
+#define BINGO_BSP_MINB 8
+#endif
+
 static constexpr uint32_t CH = 1024;   // adjacency positions / member slots per chunk item (32 per lane)
 static constexpr uint32_t BSP_MAXT = 1u << 21;   // touched vertices per sub-batch (state ~1.1 KB each)
 enum : uint32_t { GK_KIND0 = 0, GK_C, GK_INSK, GK_DELK, GK_MOFF, GK_CAP, GK_ONE, GK_GHO, GK_N };
@@ -115,7 +121,7 @@ __device__ __forceinline__ uint32_t hash_find(const uint32_t *hkey, uint32_t hma
 
 // ------------------------------------------------------------------ plan
 // count: add the batch's pool demand to cnt; state: write the per-vertex state
-__global__ void __launch_bounds__(MT) k_bsp_plan(const BspArgs a, uint64_t *__restrict__ scr_need, UpdCounters *cnt,
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a, uint64_t *__restrict__ scr_need, UpdCounters *cnt,
                                                  bool count, bool state) {
     __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res;
     __shared__ int b_flag;
@@ -193,7 +199,7 @@ __global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint
 }
 
 // ------------------------------------------------------------------ relocations, inserts, scratch init
-__global__ void __launch_bounds__(MT) k_bsp_alloc_insert(const BspArgs a) {
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_alloc_insert(const BspArgs a) {
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_WARP_LOOP(i, a.nt) {
@@ -343,7 +349,7 @@ __global__ void __launch_bounds__(MT) k_bsp_copy(const BspArgs a, uint64_t total
 // ------------------------------------------------------------------ delete selection, round 0 (R-8)
 // every live instance of a deleted destination: count it, and atomicMin its
 // packed (epoch << 32 | position) key
-__global__ void __launch_bounds__(MT) k_bsp_select(const BspArgs a, uint64_t total) {
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_select(const BspArgs a, uint64_t total) {
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_ITEM_LOOP(it, total) {
@@ -439,7 +445,7 @@ __device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s,
 // ------------------------------------------------------------------ picks, further rounds, per-group counts
 // hubs = false: small vertices (all of their delete path here); hubs = true: the
 // large vertices with deletes (picks only; the rest by the chunk-item kernels)
-__global__ void __launch_bounds__(MT) k_bsp_finalize(const BspArgs a, bool hubs) {
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_finalize(const BspArgs a, bool hubs) {
     __shared__ uint32_t s_delk[MT / 32][32];
     // small vertices: bitmap, holes, rename table and group holes in shared memory
     __shared__ uint32_t s_bm[MT / 32][32], s_hol[MT / 32][32], s_R[MT / 32][32], s_gh[MT / 32][64];
@@ -681,7 +687,7 @@ __device__ __forceinline__ GrpItem grp_item(const BspArgs &a, uint64_t it) {
     return gi;
 }
 
-__global__ void __launch_bounds__(MT) k_bsp_grp_count(const BspArgs a, uint64_t total) {
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_count(const BspArgs a, uint64_t total) {
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_ITEM_LOOP(it, total) {
@@ -702,7 +708,7 @@ __global__ void __launch_bounds__(MT) k_bsp_grp_count(const BspArgs a, uint64_t 
 
 // pass 1 over the front [0, L_k'): deleted slots become holes ranked in slot
 // order; survivors pointing into the adjacency tail are renamed in place
-__global__ void __launch_bounds__(MT) k_bsp_grp_write(const BspArgs a, uint64_t total) {
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_write(const BspArgs a, uint64_t total) {
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_ITEM_LOOP(it, total) {
@@ -888,7 +894,7 @@ __device__ __forceinline__ void rebuild_write(const BspArgs &a, uint32_t i, cons
 }
 
 // small vertices (L <= CH): one warp each
-__global__ void __launch_bounds__(MT) k_bsp_rebuild(const BspArgs a) {
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild(const BspArgs a) {
     BSP_WARP_LOOP(i, a.nt) {
         if (a.vL[i] > CH) continue;
         RbLane r;
@@ -910,7 +916,7 @@ __global__ void __launch_bounds__(MT) k_bsp_rebuild(const BspArgs a) {
 // the few that need an adjacency scan (a group turning into a list, or a ONE group
 // whose member must be found) save their stage-A state in the gk slots and are
 // finished by k_bsp_rebuild_fill, one block each
-__global__ void __launch_bounds__(MT) k_bsp_rebuild_big(const BspArgs a) {
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild_big(const BspArgs a) {
     const uint32_t lane = lane_id();
     BSP_WARP_LOOP(h, *a.nbigs) {
         const uint32_t i = a.bigs[h];
