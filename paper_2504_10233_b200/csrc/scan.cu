@@ -72,9 +72,19 @@ __global__ void k_tile_scan(const uint64_t *__restrict__ in, uint64_t *__restric
 // (every scanned quantity here is < 2^62).  tmp: [tiles] status words + counter.
 static constexpr uint64_t ST_A = 1ull << 62, ST_P = 2ull << 62, ST_V = (1ull << 62) - 1;
 
-__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const uint64_t *__restrict__ in,
-                                                                uint64_t *__restrict__ out, uint64_t n,
-                                                                unsigned long long *status, unsigned *counter) {
+struct ScanMulti {
+    const uint64_t *in[SCAN_MULTI_MAX];
+    uint64_t *out[SCAN_MULTI_MAX];
+};
+
+__global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const ScanMulti m, uint64_t n,
+                                                                unsigned long long *status_all, unsigned *counter_all,
+                                                                uint64_t tiles) {
+    // blockIdx.y selects the array; each array has its own tile counter and status words
+    const uint64_t *__restrict__ in = m.in[blockIdx.y];
+    uint64_t *__restrict__ out = m.out[blockIdx.y];
+    unsigned long long *status = status_all + blockIdx.y * tiles;
+    unsigned *counter = counter_all + 2 * blockIdx.y;
     __shared__ unsigned s_tile;
     __shared__ uint64_t s_excl, tot;
     if (threadIdx.x == 0) s_tile = atomicAdd(counter, 1u);
@@ -127,23 +137,41 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const uint64_t *
     if (base + SCAN_TILE >= n && threadIdx.x == SCAN_THREADS - 1) out[n] = pre;   // the last tile: the total
 }
 
-cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp, cudaStream_t s) {
+cudaError_t exclusive_scan_u64_multi(const uint64_t *const *in, uint64_t *const *out, int count, uint64_t n,
+                                     uint64_t *tmp, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
     if (n == 0) {
-        return cudaMemsetAsync(out, 0, sizeof(uint64_t), s);
+        for (int a = 0; a < count; a++) {
+            cudaError_t e = cudaMemsetAsync(out[a], 0, sizeof(uint64_t), s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
     }
     const uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
     if (tiles == 1) {
-        k_tile_scan<<<1, SCAN_THREADS, 0, s>>>(in, out, n, nullptr);
-        bingo_count_launch();
+        for (int a = 0; a < count; a++) {
+            k_tile_scan<<<1, SCAN_THREADS, 0, s>>>(in[a], out[a], n, nullptr);
+            bingo_count_launch();
+        }
         return cudaGetLastError();
     }
+    ScanMulti m;
+    for (int a = 0; a < count; a++) {
+        m.in[a] = in[a];
+        m.out[a] = out[a];
+    }
+    // tmp: [count][tiles] status words, then [count][2] u32 counters (one u64 each)
     unsigned long long *status = reinterpret_cast<unsigned long long *>(tmp);
-    unsigned *counter = reinterpret_cast<unsigned *>(tmp + tiles);
-    cudaError_t e = cudaMemsetAsync(tmp, 0, sizeof(uint64_t) * (tiles + 1), s);
+    unsigned *counter = reinterpret_cast<unsigned *>(tmp + (uint64_t)count * tiles);
+    cudaError_t e = cudaMemsetAsync(tmp, 0, sizeof(uint64_t) * ((uint64_t)count * tiles + count), s);
     if (e != cudaSuccess) return e;
-    k_scan_lookback<<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, out, n, status, counter);
+    k_scan_lookback<<<dim3((unsigned)tiles, (unsigned)count), SCAN_THREADS, 0, s>>>(m, n, status, counter, tiles);
     bingo_count_launch();
     return cudaGetLastError();
+}
+
+cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp, cudaStream_t s) {
+    return exclusive_scan_u64_multi(&in, &out, 1, n, tmp, s);
 }
 
 }  // namespace bingo

@@ -9,5 +9,10 @@ namespace bingo {
 // `tmp` must hold scan_tmp_words(n) u64.  Asynchronous on `s`.
 size_t scan_tmp_words(uint64_t n);
 cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp, cudaStream_t s);
+// `count` (<= SCAN_MULTI_MAX) independent scans of length n in one launch; tmp must hold
+// count * scan_tmp_words(n) u64
+#define SCAN_MULTI_MAX 8
+cudaError_t exclusive_scan_u64_multi(const uint64_t *const *in, uint64_t *const *out, int count, uint64_t n,
+                                     uint64_t *tmp, cudaStream_t s);
 
 }  // namespace bingo

@@ -1345,7 +1345,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         add(8 * (ntmax + 1));
         add(8 * (ntmax + 2));
         add(4ull * VST * ntmax);
-        add(8 * scan_tmp_words(ntmax + 1));
+        add(8 * 5 * scan_tmp_words(ntmax + 1));   // up to five scans in one launch
         add(sizeof(BspTotals));
         add(4 * ntmax);
         add(4 * ntmax);
@@ -1388,7 +1388,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     a.p_all = p_all;
     uint64_t *scr_need = cv.take<uint64_t>(ntmax + 1), *scr_off = cv.take<uint64_t>(ntmax + 2);
     uint32_t *vstats = cv.take<uint32_t>((size_t)VST * ntmax);
-    uint64_t *stmp = cv.take<uint64_t>(scan_tmp_words(ntmax + 1));
+    uint64_t *stmp = cv.take<uint64_t>(5 * scan_tmp_words(ntmax + 1));
     BspTotals *dt = cv.take<BspTotals>(1);
     a.hubs = cv.take<uint32_t>(ntmax);
     a.bigs = cv.take<uint32_t>(ntmax);
@@ -1430,12 +1430,12 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         k_bsp_plan<<<warp_grid(nt, WG), MT, 0, s>>>(a, scr_need, dc, !multi, true);
         bingo_count_launch();
         UCK(cudaGetLastError());
-        UCK(exclusive_scan_u64(scr_need, scr_off, nt, stmp, s));
-        UCK(exclusive_scan_u64(a.cc_copy, p_copy, nt, stmp, s));
-        UCK(exclusive_scan_u64(a.cc_sel, p_sel, nt, stmp, s));
-        UCK(exclusive_scan_u64(a.cc_grp, p_grp, nt, stmp, s));
-        if (g->nbt) UCK(exclusive_scan_u64(a.cc_all, p_all, nt, stmp, s));
-        else UCK(cudaMemsetAsync(p_all + nt, 0, 8, s));
+        {   // the five per-vertex prefix sums of the plan in one launch
+            const uint64_t *ins[5] = {scr_need, a.cc_copy, a.cc_sel, a.cc_grp, a.cc_all};
+            uint64_t *outs[5] = {scr_off, p_copy, p_sel, p_grp, p_all};
+            UCK(exclusive_scan_u64_multi(ins, outs, g->nbt ? 5 : 4, nt, stmp, s));
+            if (!g->nbt) UCK(cudaMemsetAsync(p_all + nt, 0, 8, s));
+        }
         k_bsp_totals<<<1, 32, 0, s>>>(a, dc, scr_off, dt);
         bingo_count_launch();
         UCK(cudaGetLastError());
