@@ -360,14 +360,24 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_select(const BspArgs
         const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
         const uint32_t hmask = s.Hq - 1;
         const uint32_t e = min(L, (c + 1) * CH);
-#pragma unroll 4
-        for (uint32_t p = c * CH + lane; p < e; p += 32) {
-            const uint32_t x = __ldg(&g.arc[aoff + p].x);
-            const uint32_t hit = hash_find(s.hkey, hmask, x);
-            if (hit == EMPTY_KEY) continue;
-            const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
-            atomicAdd(&s.hfound[hit], 1u);
-            atomicMin(&s.hbest[hit], key);
+        // 8 independent destination loads in flight per lane, then the (L1-resident) probes
+        for (uint32_t p0 = c * CH + lane; p0 < e; p0 += 32 * 8) {
+            uint32_t x[8];
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const uint32_t p = p0 + 32 * j;
+                x[j] = p < e ? __ldg(&g.arc[aoff + p].x) : EMPTY_KEY;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; j++) {
+                const uint32_t p = p0 + 32 * j;
+                if (p >= e) continue;
+                const uint32_t hit = hash_find(s.hkey, hmask, x[j]);
+                if (hit == EMPTY_KEY) continue;
+                const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
+                atomicAdd(&s.hfound[hit], 1u);
+                atomicMin(&s.hbest[hit], key);
+            }
         }
     }
 }
@@ -409,17 +419,26 @@ __device__ __forceinline__ void group_front(const MutateArgs &g, const DelScr &s
                                             uint32_t sb, uint32_t se, uint32_t r0, uint32_t Lp) {
     const uint32_t lane = lane_id();
     uint32_t r = r0;
-    for (uint32_t s0 = sb; s0 < se; s0 += 32) {
-        const uint32_t sl = s0 + lane;
-        bool del = false;
-        if (sl < se) {
-            const uint32_t x = Mi[sl];
-            del = bit_test(s.bm, x);
-            if (!del && x >= Lp) Mi[sl] = s.R[x - Lp];
+    for (uint32_t b0 = sb; b0 < se; b0 += 32 * 8) {
+        uint32_t xs[8];   // 8 independent member loads in flight per lane
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t sl = b0 + 32 * j + lane;
+            xs[j] = sl < se ? Mi[sl] : 0u;
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, del);
-        if (del) gh[r + __popc(bal & lanemask_lt())] = sl;
-        r += __popc(bal);
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t sl = b0 + 32 * j + lane;
+            bool del = false;
+            if (sl < se) {
+                const uint32_t x = xs[j];
+                del = bit_test(s.bm, x);
+                if (!del && x >= Lp) Mi[sl] = s.R[x - Lp];
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, del);
+            if (del) gh[r + __popc(bal & lanemask_lt())] = sl;
+            r += __popc(bal);
+        }
     }
 }
 
@@ -698,8 +717,13 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_count(const BspA
             const DelScr s = del_scr(g.scr + g.scr_off[gi.i], L, q);
             const uint32_t *Mi = g.midx + (uint64_t)gi.moff * 4;
             const uint32_t e = min(gi.cp - gi.Nk, (gi.j + 1) * CH);
-#pragma unroll 4
-            for (uint32_t sl = gi.j * CH + lane; sl < e; sl += 32) n += bit_test(s.bm, Mi[sl]) ? 1u : 0u;
+            for (uint32_t s0 = gi.j * CH + lane; s0 < e; s0 += 32 * 8) {
+                uint32_t m[8];
+#pragma unroll
+                for (int j = 0; j < 8; j++) m[j] = s0 + 32 * j < e ? __ldg(Mi + s0 + 32 * j) : 0xFFFFFFFFu;
+#pragma unroll
+                for (int j = 0; j < 8; j++) n += (m[j] != 0xFFFFFFFFu && bit_test(s.bm, m[j])) ? 1u : 0u;
+            }
             n = warp_sum(n);
         }
         if (lane == 0) a.gcnt[it] = n;
