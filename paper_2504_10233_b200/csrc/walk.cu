@@ -96,11 +96,22 @@ __global__ void __launch_bounds__(256, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO
                     if (APP == BINGO_NODE2VEC && t >= 1) {
                         // KnightKing rejection: propose first-order, accept with f/f_max;
                         // a rejected proposal re-draws everything under outer attempt o + 1 (R-14)
-                        const uint32_t cls =
-                            (next == prev) ? 0u : (probe_arc<PROF>(a, prev, prev_nbo, next, prof) ? 1u : 2u);
-                        if (!a.n2v_always[cls]) {
+                        // The accept draw (tag 2) does not depend on the class, so it is taken
+                        // first and the distance-1 probe runs only when the two candidate
+                        // classes (next != prev: distance 1 or 2) would decide differently --
+                        // the same decisions as classifying first, with most probes skipped
+                        // (p = 2, q = 0.5: half of them; p = 0.5, q = 2: three quarters).
+                        if (next == prev) {
+                            if (!a.n2v_always[0]) {
+                                const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
+                                accept = join64(r.x, r.y) < a.n2v_thr[0];
+                            }
+                        } else if (!(a.n2v_always[1] && a.n2v_always[2])) {
                             const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
-                            accept = join64(r.x, r.y) < a.n2v_thr[cls];
+                            const uint64_t x = join64(r.x, r.y);
+                            const bool a1 = a.n2v_always[1] || x < a.n2v_thr[1];
+                            const bool a2 = a.n2v_always[2] || x < a.n2v_thr[2];
+                            accept = (a1 == a2) ? a1 : (probe_arc<PROF>(a, prev, prev_nbo, next, prof) ? a1 : a2);
                         }
                     }
                     if (!accept) {
