@@ -1026,7 +1026,9 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
         a.scr_off = reinterpret_cast<const uint64_t *>(scr_off);
         a.scr = fa.scr;
         a.vstats = fa.vstats;
-        for (uint32_t t = w; t < nt; t += nw) mutate_vertex<32>(a, t, sm[w]);
+        // each warp's delete scratch in dynamic shared memory when it fits (else global)
+        extern __shared__ __align__(16) uint32_t fast_wscr[];
+        for (uint32_t t = w; t < nt; t += nw) mutate_vertex<32>(a, t, sm[w], fast_wscr + w * WARP_SCR_WORDS, WARP_SCR_WORDS);
     }
     __syncthreads();
     if (tid == 0) {
@@ -1266,7 +1268,13 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
     ho->status = 0xFFFFFFFFu;
     // one warp per touched vertex at most (a vertex's records go to one warp): small
     // blocks keep the block-wide barriers of the single-record case cheap
-    k_upd_fast<<<1, 32 * (unsigned)std::min<uint64_t>(32, std::max<uint64_t>(2, n)), 0, s>>>(fa);
+    static bool smem_set = false;
+    if (!smem_set) {   // up to 32 warps x WARP_SCR_WORDS of dynamic shared memory
+        cudaFuncSetAttribute(k_upd_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 4 * WARP_SCR_WORDS);
+        smem_set = true;
+    }
+    const unsigned fw = (unsigned)std::min<uint64_t>(32, std::max<uint64_t>(2, n));
+    k_upd_fast<<<1, 32 * fw, 4 * WARP_SCR_WORDS * fw, s>>>(fa);
     bingo_count_launch();
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);

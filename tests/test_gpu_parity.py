@@ -142,7 +142,8 @@ def test_walk_edge_cases():
         assert np.array_equal(u32(out["lengths"]), ref["lengths"])
 
 
-@pytest.mark.parametrize("p,q,index", [(2.0, 0.5, True), (0.5, 2.0, True), (1.0, 1.0, True), (2.0, 0.5, False)])
+@pytest.mark.parametrize("p,q,index", [(2.0, 0.5, True), (0.5, 2.0, True), (1.0, 1.0, True), (2.0, 0.5, False),
+                                        (1.0, 2.0, True), (0.25, 4.0, False), (3.0, 0.7, True)])
 def test_node2vec_parity(p, q, index):
     pb = _pb()
     w = synth.make_workload("c1")
