@@ -194,6 +194,12 @@ struct bingo_graph {
     uint32_t *nbt = nullptr;           // [4 * arc_cap] neighbour hash sets (node2vec), optional
     uint64_t *nbo = nullptr;           // [V] hash-set base | log2 size << 48
     uint32_t *nbtomb = nullptr;        // [V] tombstones in each hash set (incremental updates)
+    // hub delete index (update-side, derived; hub_index.cuh): per large vertex a
+    // destination -> position multimap, so deletes locate their arcs without a scan
+    uint64_t *hixo = nullptr;          // [V] table word offset | log2 entries << 48; 0 = none
+    uint32_t *hixt = nullptr;          // [V] tombstones per table
+    uint32_t *hix = nullptr;           // pool of tables, 2 words per entry {dst + 1 (0 empty), position}
+    uint64_t hix_cap = 0;              // words; bump pointer counters[5]
     uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
     unsigned long long *visit = nullptr;     // [V] PPR visit counts

@@ -48,6 +48,7 @@ static constexpr int VST = 28;
 struct UpdCounters {        // device, zeroed per batch
     unsigned long long need_arc, need_bkt, need_mem, reserve_mem;
     unsigned long long scratch_words;
+    unsigned long long need_hix;   // hub delete index: upper bound of new table words (BSP plan)
     int flag;
     unsigned n_small, n_large;
     int pad;
@@ -331,6 +332,8 @@ struct MutateArgs {
     uint32_t *nbt;
     uint64_t *nbo;
     uint32_t *nbtomb;
+    uint64_t *hixo;             // hub delete index offsets: routes that do not maintain it invalidate
+    uint32_t *hixt, *hix;       // its tombstone counts and table pool (BSP route)
     unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units
     uint32_t *vstats;           // [ntouch][VST]
     uint32_t epoch, alpha, beta, hot_b, hot_m;
@@ -844,6 +847,7 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
             a.nbtomb[u] = 0;
         }
     }
+    if (tid == 0 && a.hixo && a.hixo[u]) a.hixo[u] = 0;   // this route does not maintain the hub index
 }
 
 // small touched vertices: one warp each, 8 per block (grid-stride over all touched
@@ -1051,6 +1055,7 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
 
 #include "update_bsp.cuh"
 #include "float_update.cuh"
+#include "hub_index.cuh"
 
 // ------------------------------------------------------------------ host side
 namespace {
@@ -1216,6 +1221,9 @@ static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
     ma.nbt = g->nbt;
     ma.nbo = g->nbo;
     ma.nbtomb = g->nbtomb;
+    ma.hixo = g->hixo;
+    ma.hixt = g->hixt;
+    ma.hix = g->hix;
     ma.bump = g->counters;
     ma.epoch = e;
     ma.alpha = g->alpha;
@@ -1327,6 +1335,42 @@ static bingo_status check_capacity(bingo_graph *g, const UpdCounters &hc, const 
     return BINGO_OK;
 }
 
+// The hub delete index is opt-in (BINGO_HUB_INDEX=1).  Maintained tables make the c4
+// selection 542 -> 14 us, but on R-MAT update streams each batch's deletes reach mostly
+// hubs that had none before, so the lazy table builds (O(d) scattered atomics, ~4.6 ms per
+// c4 batch) cost more than the scans they replace.
+static bool hix_disabled() {
+    const char *ev = getenv("BINGO_HUB_INDEX");
+    return !(ev && ev[0] == '1');
+}
+
+// hub delete index storage (hub_index.cuh): per-vertex offsets / tombstone counts on first
+// use, and a table pool with room for every table this batch may build (tables are taken
+// zeroed from the pool and never reused, so new words are zeroed)
+static bingo_status ensure_hix(bingo_graph *g, unsigned long long used, unsigned long long need, cudaStream_t s) {
+    if (!need) return BINGO_OK;
+    if (!g->hixo) {
+        g->hixo = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * std::max<uint64_t>(g->V, 1));
+        g->hixt = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * std::max<uint64_t>(g->V, 1));
+        if (!g->hixo || !g->hixt) return BINGO_E_NOMEM;
+        if (cudaMemsetAsync(g->hixo, 0, sizeof(uint64_t) * std::max<uint64_t>(g->V, 1), s) != cudaSuccess ||
+            cudaMemsetAsync(g->hixt, 0, sizeof(uint32_t) * std::max<uint64_t>(g->V, 1), s) != cudaSuccess)
+            return BINGO_E_CUDA;
+    }
+    if (used + need <= g->hix_cap) return BINGO_OK;
+    const uint64_t cap = std::max<uint64_t>((used + need) + (used + need) / 4, g->hix_cap + g->hix_cap / 2);
+    uint32_t *nh = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * cap);
+    if (!nh) return BINGO_E_NOMEM;
+    if ((g->hix_cap && cudaMemcpyAsync(nh, g->hix, sizeof(uint32_t) * g->hix_cap, cudaMemcpyDeviceToDevice, s) != cudaSuccess) ||
+        cudaMemsetAsync(nh + g->hix_cap, 0, sizeof(uint32_t) * (cap - g->hix_cap), s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return BINGO_E_CUDA;
+    bingo_dev_free(g, g->hix);
+    g->hix = nh;
+    g->hix_cap = cap;
+    return BINGO_OK;
+}
+
 static inline unsigned warp_grid(uint64_t units, unsigned cap) {
     const uint64_t b = (units + MT / 32 - 1) / (MT / 32);
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, cap));
@@ -1358,6 +1402,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         add(4 * ntmax);
         add(4 * ntmax);
         add(8 * ntmax);
+        add(4 * ntmax);
         add(4 * ntmax);
         add(64);
         vb += 4096;
@@ -1402,6 +1447,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     a.bigs = cv.take<uint32_t>(ntmax);
     a.vnbo = cv.take<uint64_t>(ntmax);
     a.vnbfull = cv.take<uint32_t>(ntmax);
+    a.vhix = cv.take<uint32_t>(ntmax);
     a.nhubs = cv.take<uint32_t>(16);
     a.nbigs = a.nhubs + 1;
     auto refresh = [&]() {
@@ -1425,9 +1471,11 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         UCK(cudaGetLastError());
         UCK(cudaMemcpyAsync(&ht->c, dc, sizeof(UpdCounters), cudaMemcpyDeviceToHost, s));
         UCK(cudaMemcpyAsync(ht->bump, g->counters, sizeof(ht->bump), cudaMemcpyDeviceToHost, s));
+        UCK(cudaMemcpyAsync(&ht->hix_used, g->counters + 5, 8, cudaMemcpyDeviceToHost, s));
         UCK(cudaStreamSynchronize(s));
-        const bingo_status st = check_capacity(g, ht->c, ht->bump, s);
-        if (st != BINGO_OK) return st;
+        bingo_status st = check_capacity(g, ht->c, ht->bump, s);
+        if (st == BINGO_OK && !hix_disabled()) st = ensure_hix(g, ht->hix_used, ht->c.need_hix, s);
+        if (st != BINGO_OK) return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
         refresh();
     }
     for (uint64_t t0 = 0; t0 < ntouch; t0 += maxt) {
@@ -1435,6 +1483,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         a.nt = (uint32_t)std::min<uint64_t>(maxt, ntouch - t0);
         const uint32_t nt = a.nt;
         UCK(cudaMemsetAsync(a.nhubs, 0, 16, s));   // hubs, bigs, rebuild fills
+        UCK(cudaMemsetAsync(a.vhix, 0, 4 * (size_t)nt, s));
         k_bsp_plan<<<warp_grid(nt, WG), MT, 0, s>>>(a, scr_need, dc, !multi, true);
         bingo_count_launch();
         UCK(cudaGetLastError());
@@ -1452,8 +1501,9 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         UCK(cudaStreamSynchronize(s));
         g_trace.mark("sync plan totals", s);
         if (!multi) {
-            const bingo_status st = check_capacity(g, ht->c, ht->bump, s);
-            if (st != BINGO_OK) return st;
+            bingo_status st = check_capacity(g, ht->c, ht->bump, s);
+            if (st == BINGO_OK && !hix_disabled()) st = ensure_hix(g, ht->hix_used, ht->c.need_hix, s);
+            if (st != BINGO_OK) return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
             refresh();
         }
         // ---- from here on the (sub-)batch is applied
@@ -1502,15 +1552,23 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         }
         // -- large vertices
         if (copy) BSP_LAUNCH(k_bsp_copy, warp_grid(copy, IG), sh, a, copy);
+        const bool hix = g->hixo != nullptr && ht->bigs && !hix_disabled();
+        if (hix) {
+            BSP_LAUNCH(k_hix_prep, warp_grid(ht->bigs, WG), sh, a);
+            if (sel) BSP_LAUNCH(k_hix_build, warp_grid(sel, IG), sh, a, sel);
+        }
         if (sel) {
             BSP_LAUNCH(k_bsp_select, warp_grid(sel, IG), sh, a, sel);
+            if (hix) BSP_LAUNCH(k_hix_select, warp_grid(ht->hubs, WG), sh, a);
             BSP_LAUNCH(k_bsp_finalize, warp_grid(ht->hubs, WG), sh, a, true);
+            if (hix) BSP_LAUNCH(k_hix_del, warp_grid(ht->hubs, WG), sh, a);
             g_trace.mark("hub: select+finalize", sh);
             BSP_LAUNCH(k_bsp_hole_count, warp_grid(sel, IG), sh, a, sel);
             UCK(exclusive_scan_u64(a.icnt, const_cast<uint64_t *>(a.ipref), sel, itmp, sh));
             BSP_LAUNCH(k_bsp_hole_write, warp_grid(sel, IG), sh, a, sel);
             BSP_LAUNCH(k_bsp_tail, warp_grid(ht->hubs, WG), sh, a);
             g_trace.mark("hub: holes+tail", sh);
+            if (hix) BSP_LAUNCH(k_hix_ins, warp_grid(ht->bigs, WG), sh, a);
             if (grp) {
                 BSP_LAUNCH(k_bsp_grp_count, warp_grid(grp, IG), sh, a, grp);
                 UCK(exclusive_scan_u64(a.gcnt, const_cast<uint64_t *>(a.gpref), grp, itmp, sh));
@@ -1519,6 +1577,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
                 g_trace.mark("hub: group fronts+tails", sh);
             }
         }
+        if (hix && !sel) BSP_LAUNCH(k_hix_ins, warp_grid(ht->bigs, WG), sh, a);   // inserts only
         if (ht->bigs) {
             BSP_LAUNCH(k_bsp_rebuild_big, warp_grid(ht->bigs, WG), sh, a);
             k_bsp_rebuild_fill<<<(unsigned)std::min<uint64_t>(ht->bigs, 148 * 2), LT, 0, sh>>>(a);
@@ -1769,6 +1828,9 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     ma.nbt = g->nbt;
     ma.nbo = g->nbo;
     ma.nbtomb = g->nbtomb;
+    ma.hixo = g->hixo;
+    ma.hixt = g->hixt;
+    ma.hix = g->hix;
     ma.bump = g->counters;
     ma.vstats = vstats;
     ma.epoch = e;

@@ -54,6 +54,7 @@ struct BspArgs {
     const uint64_t *gpref;
     uint32_t *hubs, *nhubs;        // large vertices (L > CH) with deletes, any order
     uint32_t *bigs, *nbigs;        // all large vertices, any order
+    uint32_t *vhix;                // hub delete index: 0 not maintained (invalidated), 1 used, 2 built + used
     uint64_t *vnbo;                // pre-batch nbo[u] (node2vec neighbour sets)
     uint32_t *vnbfull;             // 1: the vertex's neighbour set is rebuilt from its adjacency
 };
@@ -123,9 +124,9 @@ __device__ __forceinline__ uint32_t hash_find(const uint32_t *hkey, uint32_t hma
 // count: add the batch's pool demand to cnt; state: write the per-vertex state
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a, uint64_t *__restrict__ scr_need, UpdCounters *cnt,
                                                  bool count, bool state) {
-    __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res;
+    __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res, b_hix;
     __shared__ int b_flag;
-    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = 0; b_flag = 0; }
+    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = b_hix = 0; b_flag = 0; }
     __syncthreads();
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
@@ -141,6 +142,8 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
             if (o.bkt) atomicAdd(&b_bkt, o.bkt);
             if (o.mem) atomicAdd(&b_mem, o.mem);
             if (o.res) atomicAdd(&b_res, o.res);
+            // hub delete index: words of a (re)built table, an upper bound
+            if (o.L > CH && o.q) atomicAdd(&b_hix, 2ull << nb_log2size(o.L));
         }
         if (!state) continue;
         const bool lst = is_list(pl.kind);
@@ -175,6 +178,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
         if (b_bkt) atomicAdd(&cnt->need_bkt, b_bkt);
         if (b_mem) atomicAdd(&cnt->need_mem, b_mem);
         if (b_res) atomicAdd(&cnt->reserve_mem, b_res);
+        if (b_hix) atomicAdd(&cnt->need_hix, b_hix);
         if (b_flag) atomicOr(&cnt->flag, b_flag);
     }
 }
@@ -183,7 +187,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
 struct BspTotals {
     UpdCounters c;
     unsigned long long bump[3];
-    unsigned long long scr, copy, sel, grp, all, hubs, bigs;
+    unsigned long long scr, copy, sel, grp, all, hubs, bigs, hix_used;
 };
 __global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint64_t *scr_off, BspTotals *out) {
     if (threadIdx.x != 0) return;
@@ -196,6 +200,7 @@ __global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint
     out->all = a.p_all[a.nt];
     out->hubs = *a.nhubs;
     out->bigs = *a.nbigs;
+    out->hix_used = a.g.bump[5];
 }
 
 // ------------------------------------------------------------------ relocations, inserts, scratch init
@@ -354,6 +359,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_select(const BspArgs
     const MutateArgs &g = a.g;
     BSP_ITEM_LOOP(it, total) {
         const uint32_t i = owner_of(a.p_sel, a.nt, it);
+        if (a.vhix[i]) continue;   // located through the hub delete index (k_hix_select)
         const uint32_t c = (uint32_t)(it - a.p_sel[i]);
         const uint32_t L = a.vL[i], q = a.vq[i];
         const uint64_t aoff = a.vaoff[i];
@@ -914,6 +920,7 @@ __device__ __forceinline__ void rebuild_write(const BspArgs &a, uint32_t i, cons
         th.pad1 = 0;
         g.thdr[u] = th;
         if (g.nbt) g.nbo[u] = nb_pack(4 * aoff, nb_log2size(dn));
+        if (!a.vhix[i] && g.hixo && g.hixo[u]) g.hixo[u] = 0;   // index not maintained by this batch
     }
 }
 

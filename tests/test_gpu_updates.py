@@ -71,6 +71,7 @@ def _bias_of(u, v, e, hi):
 ROUTES = {
     "bsp": {},                                                  # bulk-synchronous pipeline (default)
     "bsp-sub": {"BINGO_BSP_MAXT": "7"},                         # ... in sub-batches of 7 touched vertices
+    "bsp-hix": {"BINGO_HUB_INDEX": "1"},                        # ... with the hub delete index (opt-in)
     "legacy": {"BINGO_UPD_LEGACY": "1"},                        # per-vertex mutate kernels (warp / block)
     "legacy-block": {"BINGO_UPD_LEGACY": "1", "BINGO_UPD_SMALL_L": "0"},   # ... every vertex on a block
 }
@@ -81,6 +82,7 @@ ROUTES = {
     (3, False, 7, "bsp", 700), (4, False, 255, "bsp", 700), (5, True, 1 << 31, "bsp", 700),
     (7, False, 200, "bsp", 3500), (8, False, 7, "bsp", 5000), (9, True, 255, "bsp", 3000),
     (0, False, 200, "bsp-sub", 700), (8, False, 7, "bsp-sub", 5000),
+    (7, False, 200, "bsp-hix", 3500), (8, False, 7, "bsp-hix", 5000), (9, True, 255, "bsp-hix", 3000),
     (0, False, 200, "legacy", 700), (3, False, 7, "legacy", 700), (7, False, 200, "legacy", 3500),
     (0, False, 200, "legacy-block", 700), (3, False, 7, "legacy-block", 700),
     (6, False, 1 << 20, "legacy-block", 700)])
@@ -262,3 +264,52 @@ def test_node2vec_neighbour_index_across_batches(route, monkeypatch):
             out = g.walk(app=_pb().NODE2VEC, length=20, p=p, q=q, seed=e)
             ref = o.walk(app=oracle.APP_NODE2VEC, length=20, p=p, q=q, seed=e)
             assert np.array_equal(u32(out["paths"]), ref["paths"]), f"{route} batch {e} p={p} q={q}"
+
+
+@pytest.mark.parametrize("hix", ["1", "0"])
+def test_hub_delete_index_maintained_across_batches(hix, monkeypatch):
+    """Hub delete index (hub_index.cuh): large vertices locate their deleted arcs through a
+    destination -> position multimap kept exact across batches (deletes, tail moves, inserts),
+    dropped on repeated deletes of one pair, on other routes (single-record fast path) and on
+    load, and rebuilt (opt-in: BINGO_HUB_INDEX=1).  Dumps must equal the oracle's after every
+    batch, index on and off."""
+    monkeypatch.setenv("BINGO_HUB_INDEX", hix)
+    rng = np.random.default_rng(2024)
+    V = 3000
+    deg = rng.integers(0, 6, size=V)
+    deg[0], deg[1] = 5000, 2500                 # two hubs (> 1024 arcs: the large-vertex route)
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, V, size=A).astype(np.uint32)
+    bias = rng.integers(1, 1 << 12, size=A).astype(np.uint32)
+    g, o = _pair(ro, dst, bias)
+    live = {u: list(dst[int(ro[u]):int(ro[u + 1])]) for u in range(V)}
+    for e in range(1, 15):
+        recs = []
+        for hub in (0, 1):
+            if hub == 1 and e % 3 == 0:          # hub 1: insert-only batches now and then
+                recs += [(0, 1, int(rng.integers(0, V)), int(rng.integers(1, 4096))) for _ in range(40)]
+                continue
+            k = int(rng.integers(10, 80))
+            for v in rng.choice(np.unique(np.array(live[hub])), size=min(k, len(set(live[hub]))), replace=False):
+                recs.append((1, hub, int(v), 0))   # distinct destinations: the index route
+            recs += [(0, hub, int(rng.integers(0, V)), int(rng.integers(1, 4096))) for _ in range(k)]
+            if e % 5 == 0:                         # a repeated delete of one pair: the scan route
+                recs += [(1, hub, int(live[hub][0]), 0)] * 2
+        for _ in range(100):
+            u = int(rng.integers(2, V))
+            recs.append((0, u, int(rng.integers(0, V)), int(rng.integers(1, 4096))))
+        recs = np.array(recs, dtype=np.uint32)
+        recs = recs[rng.permutation(len(recs))]
+        if e % 4 == 2:                             # single-record calls touch hub 0 (fast path drops its index)
+            one = np.array([[1, 0, int(live[0][3]), 0], [0, 0, 7, 9]], dtype=np.uint32)
+            for r in one:
+                _same_stats(g.apply_updates(r[None, :]), o.apply_updates(r[None, :]))
+        _same_stats(g.apply_updates(recs), o.apply_updates(recs))
+        _same(g, o, V, f"batch {e}")
+        d = oracle.parse_dump(o.dump(), V)
+        live = {u: [a[0] for a in d[u]["adj"]] for u in range(V)}
+    out = g.walk(length=40, seed=11)
+    ref = o.walk(length=40, seed=11)
+    assert np.array_equal(u32(out["paths"]), ref["paths"])
