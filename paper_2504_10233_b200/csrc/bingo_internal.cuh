@@ -200,6 +200,7 @@ struct bingo_graph {
     uint32_t *hixt = nullptr;          // [V] tombstones per table
     uint32_t *hix = nullptr;           // pool of tables, 2 words per entry {dst + 1 (0 empty), position}
     uint64_t hix_cap = 0;              // words; bump pointer counters[5]
+    uint32_t hix_min = 0xFFFFFFFFu;    // vertices with more arcs than this have tables
     uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
     unsigned long long *visit = nullptr;     // [V] PPR visit counts

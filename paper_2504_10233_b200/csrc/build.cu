@@ -310,6 +310,7 @@ static bingo_status fail_cuda(bingo_graph *g, cudaError_t e, const char *where) 
 bingo_status float_prepare(bingo_graph *g, const bingo_build_desc *desc, uint32_t *ibias, uint64_t *dcnt,
                            uint64_t *dscan, uint64_t *tmp, cudaStream_t s, uint64_t *total_dec);
 bingo_status float_fill(bingo_graph *g, const bingo_build_desc *desc, const uint64_t *dscan, cudaStream_t s);
+bingo_status hix_build_all(bingo_graph *g, cudaStream_t s);
 
 extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, bingo_graph **out) {
     if (!desc || !out) return BINGO_E_INVAL;
@@ -501,6 +502,8 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
         }
     }
     CK(cudaStreamSynchronize(s));
+    st = hix_build_all(g, s);   // hub delete index (update-side, derived)
+    if (st == BINGO_E_CUDA) g->poisoned = 1;
 done:
     bingo_dev_free(g, sz);
     bingo_dev_free(g, off);

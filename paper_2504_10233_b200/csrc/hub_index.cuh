@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(MT) k_hix_prep(const BspArgs a) {
             for (uint32_t sl = lane; sl < s.Hq; sl += 32) dup |= s.hkey[sl] != EMPTY_KEY && s.hk[sl] > 1u;
             if (__any_sync(0xffffffffu, dup)) {
                 mode = 0;   // repeated deletes of one pair: the scan path (rounds) handles them
-            } else if (!valid) {
+            } else if (!valid && L > g.hix_min) {
                 mode = 2;   // build a fresh table (zeroed pool words) for the pre-batch arcs
                 if (lane == 0) {
                     const uint32_t lg = nb_log2size(L);
@@ -193,6 +193,40 @@ __global__ void __launch_bounds__(MT) k_hix_ins(const BspArgs a) {
             const uint64_t o = g.hixo[u];
             if (4ull * (Lp + g.hixt[u]) > (3ull << (o >> 48))) g.hixo[u] = 0;
         }
+    }
+}
+
+// ---- tables built with the graph (bingo_build): every vertex with d > min_d
+__global__ void k_hix_sizes(uint32_t V, const VHdr *__restrict__ hdr, uint32_t min_d, uint64_t *__restrict__ items,
+                            uint64_t *__restrict__ words) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
+        const uint32_t d = hdr[u].d;
+        const bool on = d > min_d;
+        items[u] = on ? (d + CH - 1) / CH : 0;
+        words[u] = on ? (2ull << nb_log2size(d)) : 0;
+    }
+}
+__global__ void k_hix_offsets(uint32_t V, const VHdr *__restrict__ hdr, uint32_t min_d,
+                              const uint64_t *__restrict__ woff, uint64_t *__restrict__ hixo) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
+        const uint32_t d = hdr[u].d;
+        hixo[u] = d > min_d ? (woff[u] | ((uint64_t)nb_log2size(d) << 48)) : 0ull;
+    }
+}
+__global__ void __launch_bounds__(MT) k_hix_fill(uint32_t V, const uint64_t *__restrict__ pref, uint64_t total,
+                                                 const VHdr *__restrict__ hdr, const uint2 *__restrict__ arc,
+                                                 const uint64_t *__restrict__ hixo, uint32_t *__restrict__ hix) {
+    const uint32_t lane = lane_id();
+    for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < total;
+         it += ((uint64_t)gridDim.x * blockDim.x) >> 5) {
+        const uint32_t u = owner_of(pref, V, it);
+        const uint32_t c = (uint32_t)(it - pref[u]);
+        const VHdr h = hdr[u];
+        HixT t;
+        t.t = hix + (hixo[u] & ((1ull << 48) - 1));
+        t.mask = (uint32_t)((1ull << (hixo[u] >> 48)) - 1);
+        const uint32_t e = min(h.d, (c + 1) * CH);
+        for (uint32_t p = c * CH + lane; p < e; p += 32) hix_insert(t, __ldg(&arc[h.adj_off + p].x), p);
     }
 }
 

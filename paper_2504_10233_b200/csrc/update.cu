@@ -334,6 +334,7 @@ struct MutateArgs {
     uint32_t *nbtomb;
     uint64_t *hixo;             // hub delete index offsets: routes that do not maintain it invalidate
     uint32_t *hixt, *hix;       // its tombstone counts and table pool (BSP route)
+    uint32_t hix_min;           // vertices with more arcs get (and may lazily rebuild) a table
     unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units
     uint32_t *vstats;           // [ntouch][VST]
     uint32_t epoch, alpha, beta, hot_b, hot_m;
@@ -1224,6 +1225,7 @@ static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
     ma.hixo = g->hixo;
     ma.hixt = g->hixt;
     ma.hix = g->hix;
+    ma.hix_min = g->hix_min;
     ma.bump = g->counters;
     ma.epoch = e;
     ma.alpha = g->alpha;
@@ -1335,10 +1337,12 @@ static bingo_status check_capacity(bingo_graph *g, const UpdCounters &hc, const 
     return BINGO_OK;
 }
 
-// The hub delete index is opt-in (BINGO_HUB_INDEX=1).  Maintained tables make the c4
-// selection 542 -> 14 us, but on R-MAT update streams each batch's deletes reach mostly
-// hubs that had none before, so the lazy table builds (O(d) scattered atomics, ~4.6 ms per
-// c4 batch) cost more than the scans they replace.
+// The hub delete index (opt-in, BINGO_HUB_INDEX=1): tables are built with the graph for its
+// largest vertices (hix_build_all) and maintained by the bulk-synchronous route; lazy
+// (re)builds only above the build threshold (a build costs ~9x a scan).  Measured (DESIGN.md
+// 10): the c4 selection phase drops 542 -> ~160 us serialised, but whole batches do not get
+// faster (c4 1.67 ms either way, the group fronts and hole passes dominate; c2 0.87 vs 0.82 ms),
+// so the scans stay the default.
 static bool hix_disabled() {
     const char *ev = getenv("BINGO_HUB_INDEX");
     return !(ev && ev[0] == '1');
@@ -1831,6 +1835,7 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     ma.hixo = g->hixo;
     ma.hixt = g->hixt;
     ma.hix = g->hix;
+    ma.hix_min = g->hix_min;
     ma.bump = g->counters;
     ma.vstats = vstats;
     ma.epoch = e;
@@ -1906,4 +1911,69 @@ static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, ui
         stats->epoch = e;
     }
     return BINGO_OK;
+}
+
+
+// ---------------------------------------------------------------- hub delete index at build time
+// Tables for every vertex with d > min_d, min_d the smallest of 1024 / 4096 / 16384 / 65536
+// whose tables fit 15% of the free device memory (c2: 2,411 vertices, 13.5% of the arcs,
+// 212 MB).  Called by bingo_build; a graph without room keeps no tables (scans only).
+bingo_status hix_build_all(bingo_graph *g, cudaStream_t s) {
+    if (hix_disabled() || g->V == 0 || g->float_mode) return BINGO_OK;
+    const uint64_t V = g->V;
+    uint64_t *items = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 1));
+    uint64_t *words = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 1));
+    uint64_t *pref = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 2));
+    uint64_t *woff = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 2));
+    uint64_t *tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * scan_tmp_words(V + 1));
+    bingo_status st = BINGO_OK;
+    auto fin = [&](bingo_status r) {
+        bingo_dev_free(g, items); bingo_dev_free(g, words); bingo_dev_free(g, pref); bingo_dev_free(g, woff);
+        bingo_dev_free(g, tmp);
+        return r;
+    };
+    if (!items || !words || !pref || !woff || !tmp) return fin(BINGO_OK);   // no room: no tables
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const unsigned eg = (unsigned)std::min<uint64_t>((V + 255) / 256, 148ull * 16);
+    const uint32_t mins[4] = {CH, 4 * CH, 16 * CH, 64 * CH};
+    for (uint32_t min_d : mins) {
+        k_hix_sizes<<<eg, 256, 0, s>>>(g->V, g->hdr, min_d, items, words);
+        bingo_count_launch();
+        const uint64_t *ins[2] = {items, words};
+        uint64_t *outs[2] = {pref, woff};
+        if (cudaGetLastError() != cudaSuccess || exclusive_scan_u64_multi(ins, outs, 2, V, tmp, s) != cudaSuccess)
+            return fin(BINGO_E_CUDA);
+        uint64_t tot[2] = {0, 0};
+        if (cudaMemcpyAsync(&tot[0], pref + V, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(&tot[1], woff + V, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return fin(BINGO_E_CUDA);
+        if (!tot[0]) break;                                   // no vertex that large
+        if (4.0 * (double)tot[1] > 0.15 * (double)free_b) continue;   // does not fit: a higher threshold
+        const uint64_t cap = tot[1] + tot[1] / 4 + 1024;
+        g->hixo = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * V);
+        g->hixt = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * V);
+        g->hix = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * cap);
+        if (!g->hixo || !g->hixt || !g->hix) {
+            bingo_dev_free(g, g->hixo); bingo_dev_free(g, g->hixt); bingo_dev_free(g, g->hix);
+            g->hixo = nullptr; g->hixt = nullptr; g->hix = nullptr;
+            return fin(BINGO_OK);
+        }
+        g->hix_cap = cap;
+        g->hix_min = min_d;
+        const unsigned long long used = tot[1];
+        if (cudaMemsetAsync(g->hix, 0, sizeof(uint32_t) * cap, s) != cudaSuccess ||
+            cudaMemsetAsync(g->hixt, 0, sizeof(uint32_t) * V, s) != cudaSuccess ||
+            cudaMemcpyAsync(g->counters + 5, &used, 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return fin(BINGO_E_CUDA);
+        k_hix_offsets<<<eg, 256, 0, s>>>(g->V, g->hdr, min_d, woff, g->hixo);
+        bingo_count_launch();
+        k_hix_fill<<<(unsigned)std::min<uint64_t>((tot[0] + 7) / 8, 148ull * 32), MT, 0, s>>>(
+            g->V, pref, tot[0], g->hdr, g->arc, g->hixo, g->hix);
+        bingo_count_launch();
+        if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return fin(BINGO_E_CUDA);
+        break;
+    }
+    return fin(st);
 }

@@ -143,7 +143,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
             if (o.mem) atomicAdd(&b_mem, o.mem);
             if (o.res) atomicAdd(&b_res, o.res);
             // hub delete index: words of a (re)built table, an upper bound
-            if (o.L > CH && o.q) atomicAdd(&b_hix, 2ull << nb_log2size(o.L));
+            if (o.L > CH && o.L > g.hix_min && o.q) atomicAdd(&b_hix, 2ull << nb_log2size(o.L));
         }
         if (!state) continue;
         const bool lst = is_list(pl.kind);
