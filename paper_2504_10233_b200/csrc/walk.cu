@@ -334,7 +334,7 @@ extern "C" bingo_status bingo_walk(bingo_graph *g, const bingo_walk_desc *desc, 
     const bool wmajor = (desc->flags & BINGO_WALK_WALKER_MAJOR) != 0;
     uint64_t Wc = W;
     if (paths_or_null) {
-        Wc = std::max<uint64_t>(1 << 18, (W + 7) / 8);
+        Wc = std::max<uint64_t>(1 << 17, (W + 15) / 16);   // small chunks: the first copy starts early
         Wc = std::min<uint64_t>(Wc, W);
     }
     const uint64_t nchunks = (W + Wc - 1) / Wc;
