@@ -49,7 +49,10 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
 // consecutive ids and the step-major path stores stay coalesced.  Results depend
 // only on the walker id (R-1), never on which lane ran it.
 template <int APP, bool PROF, bool WMAJOR>
-__global__ void __launch_bounds__(256, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO_N2V_MINB : BINGO_WALK_MINB))
+#ifndef BINGO_WALK_TPB
+#define BINGO_WALK_TPB 256
+#endif
+__global__ void __launch_bounds__(BINGO_WALK_TPB, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO_N2V_MINB : BINGO_WALK_MINB))
     k_walk(const WalkArgs a, unsigned long long *__restrict__ claim) {
     WalkProf prof;
     // L2 eviction priorities: the thin headers are re-read by every step of every
@@ -223,10 +226,10 @@ static unsigned walk_grid(K kernel, uint32_t W) {
     int dev = 0, sms = 148, per_sm = 1;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, BINGO_WALK_TPB, 0);
     if (const char *e = getenv("BINGO_WALK_BLOCKS_PER_SM")) per_sm = std::max(1, std::min(per_sm, atoi(e)));
     cudaGetLastError();
-    const size_t need = ((size_t)W + 255) / 256;
+    const size_t need = ((size_t)W + BINGO_WALK_TPB - 1) / BINGO_WALK_TPB;
     const size_t cap = (size_t)sms * (size_t)std::max(per_sm, 1);
     return (unsigned)std::max<size_t>(1, std::min(need, cap));
 }
@@ -267,7 +270,7 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(1);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(BINGO_WALK_TPB);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cfg.attrs = nullptr;
