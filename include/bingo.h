@@ -21,6 +21,9 @@
  *  - No exception crosses the ABI; every call returns a bingo_status.
  *  - After a CUDA error the graph is poisoned: every later call on it
  *    returns BINGO_E_STATE (bingo_destroy still frees it).
+ *  - Vertex ids crossing the ABI (CSR, starts, update records, paths, visit
+ *    counts, exports) are always the caller's; an internal relabelling
+ *    (large graphs) is invisible.
  *  - Concurrency: one writer or many readers per graph; the caller orders
  *    bingo_apply_updates against bingo_walk on one stream (P:523 (ii)).
  */
