@@ -55,6 +55,11 @@ struct WalkArgs {
 #else
 #define BINGO_L2F ".L2::64B"
 #endif
+#ifdef BINGO_L1_NOALLOC           // A/B experiment switch: one-shot random reads bypass L1 allocation
+#define BINGO_L1Q ".L1::no_allocate"
+#else
+#define BINGO_L1Q ""
+#endif
 
 struct Policies {
     uint64_t keep, stream;   // L2 cache-hint policies (createpolicy)
@@ -75,7 +80,7 @@ __device__ __forceinline__ ThinHdr load_thdr(const ThinHdr *p, const Policies &p
 // fetch, with the vertex's L2 policy (hot: evict_last, cold: evict_first)
 __device__ __forceinline__ Bucket ldg_bucket(const Bucket *p, uint64_t pol) {
     uint4 lo, hi;
-    asm volatile("ld.global.nc.L2::cache_hint" BINGO_L2F ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+    asm volatile("ld.global.nc" BINGO_L1Q ".L2::cache_hint" BINGO_L2F ".v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
                  : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z), "=r"(hi.w)
                  : "l"(p), "l"(pol));
     return unpack_bucket(lo, hi);
@@ -84,14 +89,14 @@ __device__ __forceinline__ Bucket ldg_bucket(const Bucket *p, uint64_t pol) {
 // 4 B random read with an explicit L2 policy, 64 B fetch
 __device__ __forceinline__ uint32_t ldg4(const uint32_t *p, uint64_t pol) {
     uint32_t v;
-    asm volatile("ld.global.nc.L2::cache_hint" BINGO_L2F ".u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc" BINGO_L1Q ".L2::cache_hint" BINGO_L2F ".u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
 }
 
 // 8 B random read with an explicit L2 policy, 64 B fetch
 __device__ __forceinline__ uint2 ldg8(const uint2 *p, uint64_t pol) {
     uint2 v;
-    asm volatile("ld.global.nc.L2::cache_hint" BINGO_L2F ".v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    asm volatile("ld.global.nc" BINGO_L1Q ".L2::cache_hint" BINGO_L2F ".v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
     return v;
 }
 
