@@ -901,7 +901,8 @@ __global__ void k_upd_stats(const uint32_t *__restrict__ vstats, uint32_t ntouch
 // trips before the mutation.  Status and statistics land in mapped pinned host
 // memory.  If a vertex is too large for the preallocated scratch or a pool would
 // have to grow, nothing is mutated and the host runs the general pipeline.
-static constexpr uint32_t FAST_N = 64;
+static constexpr uint32_t FAST_N = 256;       // records per single-block batch
+static constexpr uint32_t FAST_INLINE = 64;   // host records passed inline as kernel parameters
 static constexpr uint32_t FAST_MAXL = 1u << 16;
 // a touched vertex above this many (post-insert) arcs hands the batch to the bulk-synchronous
 // pipeline, whose chunk items spread the vertex's scans over the GPU (one block here walks
@@ -917,7 +918,7 @@ struct FastOut {
 
 struct FastArgs {
     MutateArgs m;                     // graph, allocator and policy fields (pointers set in-kernel)
-    uint4 recs[FAST_N];               // the batch, inline (host batches need no copy)
+    uint4 recs[FAST_INLINE];          // small host batches, inline (no copy)
     const uint4 *drecs;               // or a device batch
     const uint32_t *inv;              // external -> internal vertex ids
     uint32_t n, V;
@@ -1242,7 +1243,7 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
                           bingo_update_stats *stats, cudaStream_t s, bingo_status *out) {
     if (!g->fast_scr) {
         const size_t words = (size_t)(FAST_N * fast_words_per_vertex());
-        g->fast_scr = (uint32_t *)bingo_dev_alloc(g, 4 * words + 4 * FAST_N * VST + 64);
+        g->fast_scr = (uint32_t *)bingo_dev_alloc(g, 4 * words + 4 * FAST_N * VST + 16 * FAST_N + 64);
         if (!g->fast_scr) return false;
         void *h = nullptr;
         if (cudaHostAlloc(&h, sizeof(FastOut), cudaHostAllocMapped) != cudaSuccess) {
@@ -1258,7 +1259,14 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
     FastArgs fa;
     memset(&fa, 0, sizeof(fa));
     fill_mutate_common(g, fa.m, g->epoch + 1);
-    if (flags & BINGO_UPD_HOST_BATCH) {
+    if ((flags & BINGO_UPD_HOST_BATCH) && n > FAST_INLINE) {   // larger host batches: one H2D copy
+        uint4 *stage = reinterpret_cast<uint4 *>(g->fast_scr + FAST_N * fast_words_per_vertex() + FAST_N * VST);
+        if (cudaMemcpyAsync(stage, batch, 16 * n, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+            *out = upd_cuda_fail(g, cudaGetLastError(), "fast-path batch copy");
+            return true;
+        }
+        fa.drecs = stage;
+    } else if (flags & BINGO_UPD_HOST_BATCH) {
         memcpy(fa.recs, batch, 16 * n);
         fa.drecs = nullptr;
     } else {

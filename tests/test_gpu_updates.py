@@ -196,7 +196,8 @@ def test_larger_graph_batches_digests():
 
 
 def test_small_batches_fast_path():
-    """a11: batches of 1..64 records take the single-launch path; the state after each equals
+    """a11: batches of 1..256 records take the single-launch path (up to 64 inline, larger ones
+    through one H2D copy); the state after each equals
     the oracle's, including when a batch needs pool growth (the fast path hands over to the
     general pipeline without mutating)."""
     rng = np.random.default_rng(17)
@@ -205,10 +206,15 @@ def test_small_batches_fast_path():
     stream = np.concatenate(w.batches)
     pos = 0
     while pos < len(stream):
-        k = int(rng.integers(1, 65))
+        k = int(rng.integers(1, 65)) if rng.random() < 0.6 else int(rng.integers(65, 257))
         b = stream[pos:pos + k]
         pos += k
-        _same_stats(g.apply_updates(b), o.apply_updates(b))
+        if k > 64 and rng.random() < 0.5:   # a device batch (no staging copy)
+            import torch
+            _same_stats(g.apply_updates(torch.from_numpy(np.ascontiguousarray(b).view(np.int32)).cuda()),
+                        o.apply_updates(b))
+        else:
+            _same_stats(g.apply_updates(b), o.apply_updates(b))
     _same(g, o, w.V, "after the small-batch stream")
     # a hub gaining many arcs in small batches forces relocations (SLOW -> general path)
     for i in range(20):
