@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--length", type=int, default=80)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-walkers", type=int, default=1 << 18)
+    ap.add_argument("--cpu-walkers", type=int, default=1 << 21,
+                    help="oracle walker sample (cpu_baseline; --impl reference uses a quarter per step)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (gloo: test the multi-rank path without NVLink)")
     ap.add_argument("--share-device", action="store_true",
