@@ -48,7 +48,7 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
 // idle at the tail).  DeepWalk lanes finish together, so a warp claims 32
 // consecutive ids and the step-major path stores stay coalesced.  Results depend
 // only on the walker id (R-1), never on which lane ran it.
-template <int APP, bool PROF, bool WMAJOR>
+template <int APP, bool PROF, bool WMAJOR, bool FLT>   // FLT: float-bias graph (decimal groups, R-15)
 #ifndef BINGO_WALK_TPB
 #define BINGO_WALK_TPB 256
 #endif
@@ -87,13 +87,13 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, PROF ? 4 : (APP == BINGO_NODE2
                     h = load_thdr(a.thdr + u, pol);
                     if (APP == BINGO_NODE2VEC && a.nbo)
                         cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
-                    if (a.dec) dr = load_dec(a.dec + u);
+                    if (FLT) dr = load_dec(a.dec + u);
                     if (PROF) prof.hdr++;
                 }
                 if (h.n == 0 && dr.dcnt == 0) {
                     fin = true;                               // dead end (d = 0): truncate (R-13)
                 } else {
-                    const uint32_t next = a.dec ? sample_dst_f<PROF>(a, h, dr, w, t, o, prof, pol)
+                    const uint32_t next = FLT ? sample_dst_f<PROF>(a, h, dr, w, t, o, prof, pol)
                                                 : sample_dst<PROF>(a, h, w, t, o, prof, pol);
                     bool accept = true;
                     if (APP == BINGO_NODE2VEC && t >= 1) {
@@ -277,11 +277,12 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     cfg.numAttrs = 0;
     cudaError_t le = cudaSuccess;
     const bool wmajor = (desc->flags & BINGO_WALK_WALKER_MAJOR) != 0;
-#define BINGO_K(APP_, PROF_)                                                                      \
-    (wmajor ? (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, true>, W)),                       \
-               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, true>, a, claim))                            \
-            : (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, false>, W)),                      \
-               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, false>, a, claim)))
+#define BINGO_K3(APP_, PROF_, FLT_)                                                               \
+    (wmajor ? (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, true, FLT_>, W)),                 \
+               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, true, FLT_>, a, claim))                      \
+            : (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, false, FLT_>, W)),                \
+               cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, false, FLT_>, a, claim)))
+#define BINGO_K(APP_, PROF_) (a.dec ? BINGO_K3(APP_, PROF_, true) : BINGO_K3(APP_, PROF_, false))
     if (prof) {
         switch (desc->app) {
             case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, true); break;
@@ -298,6 +299,7 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
         }
     }
 #undef BINGO_K
+#undef BINGO_K3
     if (le != cudaSuccess) {
         fprintf(stderr, "libbingo: walk launch failed: %s\n", cudaGetErrorString(le));
         g->poisoned = 1;
