@@ -53,13 +53,56 @@ def run(seed, route):
     return None
 
 
+def run_float(seed, route):
+    for k in ("BINGO_UPD_LEGACY", "BINGO_HUB_INDEX", "BINGO_BSP_MAXT"):
+        os.environ.pop(k, None)
+    os.environ.update(route)
+    rng = np.random.default_rng(seed)
+    V = int(rng.integers(5, 300))
+    deg = rng.integers(0, 30, size=V)
+    deg[0] = int(rng.integers(300, 3000))
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    dst = rng.integers(0, V, size=int(ro[-1])).astype(np.uint32)
+    scale = float(rng.choice([1e-3, 1.0, 1e3]))
+    wf = rng.random(len(dst)) * scale + 1e-6
+    g = pb.Graph(ro, dst, wf, float_bias=True, arc_slack=float(rng.choice([0.0, 0.25])), member_slack=0.0,
+                 pool_reserve=0.0)
+    o = oracle.OracleGraph(ro, dst, wf, float_bias=True)
+    live = {u: list(dst[int(ro[u]):int(ro[u + 1])]) for u in range(V)}
+    for e in range(6):
+        n = int(rng.integers(1, 400))
+        recs = np.zeros((n, 4), dtype=np.uint32)
+        ws = np.zeros(n)
+        for i in range(n):
+            u = 0 if rng.random() < 0.3 else int(rng.integers(0, V))
+            if rng.random() < 0.5 and live[u]:
+                recs[i] = (1, u, int(live[u][int(rng.integers(0, len(live[u])))]), 0)
+            else:
+                recs[i] = (0, u, int(rng.integers(0, V)), 0)
+                ws[i] = rng.random() * scale + 1e-6
+        rg, ro_ = g.try_apply_updates(recs, bias_f64=ws), o.try_apply_updates(recs, bias_f64=ws)
+        if rg != ro_:
+            return f"float seed {seed} route {route} batch {e}: status {rg} vs {ro_}"
+        if g.export() != o.dump():
+            return f"float seed {seed} route {route} batch {e}: dump mismatch"
+        d = oracle.parse_dump(o.dump(), V, True)
+        live = {u: [a[0] for a in d[u]["adj"]] for u in range(V)}
+    out = g.walk(length=20, seed=seed)
+    ref = o.walk(length=20, seed=seed)
+    if not np.array_equal(out["paths"].cpu().numpy().view(np.uint32), ref["paths"]):
+        return f"float seed {seed} route {route}: walk mismatch"
+    return None
+
+
 if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 50
+    fl = "--float" in sys.argv
     bad = 0
     for s in range(n):
         for r in ROUTES:
-            err = run(10_000 + s, r)
+            err = (run_float if fl else run)(10_000 + s, r)
             if err:
                 bad += 1
                 print(err, flush=True)
-    print(f"{n} seeds x {len(ROUTES)} routes: {bad} failures", flush=True)
+    print(f"{'float ' if fl else ''}{n} seeds x {len(ROUTES)} routes: {bad} failures", flush=True)
