@@ -438,7 +438,9 @@ def main():
                                           "+ 4 B x path entries + 4 B x lengths, exact counts from bingo_walk_profile",
                          "load_counts": {k: prof[k] for k in ("steps", "hdr", "bkt", "mem", "arc")},
                          "gather_roofline": gather},
-            "l2_plan": {k: g.info()[k] for k in ("l2_persist_bytes", "hot_degree")},
+            "l2_plan": {"l2_persist_bytes": g.info()["l2_persist_bytes"],
+                        "hot_bucket_degree": g.info()["hot_degree"] & 0xFFFFFFFF,
+                        "hot_member_degree": g.info()["hot_degree"] >> 32},
             "streaming_update": streaming,
             "clocks": clk, "gpu_launches": int(launches),
             "e2e": e2e, "cpu_baseline": cpu,
