@@ -200,8 +200,10 @@ bingo_status bingo_apply_updates_f64(bingo_graph *g, const bingo_update *batch, 
  * Walker i (0 <= i < num_walkers) has global id first_walker_id + i and
  *   starts at starts[i], or at (first_walker_id + i) mod V if starts is NULL
  *   (one walker per vertex).  Its randomness is Philox4x32-10 keyed by
- *   seed with counter (walker id, step, (outer << 16) + inner, tag) (R-1), so a
- *   sharded run (first_walker_id) reproduces the unsharded one bit for bit.
+ *   seed with counter (walker id, step, (outer << 16) + inner,
+ *   tag + ((outer >> 16) << 8)) (R-1), so a sharded run (first_walker_id)
+ *   reproduces the unsharded one bit for bit, and node2vec's rejection
+ *   attempts never repeat a counter (expected proposals per step <= f_max/f_min).
  * A walker at a vertex of out-degree 0 stops (truncation).
  * paths_or_null: step-major u32 [(length+1) x num_walkers], entry
  *   [t * num_walkers + i] = vertex after t steps; 0xFFFFFFFF after truncation.
@@ -212,7 +214,8 @@ bingo_status bingo_apply_updates_f64(bingo_graph *g, const bingo_update *batch, 
  *   BINGO_WALK_HOST_OUTPUT (the library stages through device scratch and
  *   copies D2H on `stream`; `starts` is then HOST too).
  * Errors: EINVAL (bad app / p, q <= 0 / stop_den == 0 / NULL paths with
- *   no cap).  Asynchronous unless HOST_OUTPUT (then synchronises `stream`).
+ *   no cap / node2vec with a ratio f/f_max < 2^-64, whose class could never
+ *   be accepted).  Asynchronous unless HOST_OUTPUT (then synchronises `stream`).
  * ------------------------------------------------------------------------- */
 enum { BINGO_DEEPWALK = 0, BINGO_NODE2VEC = 1, BINGO_PPR = 2 };
 #define BINGO_WALK_HOST_OUTPUT 1u

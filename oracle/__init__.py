@@ -128,6 +128,8 @@ def n2v_thresholds(p: float, q: float):
             always[i] = 1
         else:
             thr[i] = int(Fraction(r) * (1 << 64))   # floor(ratio * 2^64), exact
+            if thr[i] == 0:   # never accepted: a walker could reject forever (bingo.h: EINVAL)
+                raise ValueError(f"node2vec ratio {r} < 2^-64 can never be accepted")
     return thr, always
 
 

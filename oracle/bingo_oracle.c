@@ -145,32 +145,31 @@ static int g_dump_float = 0;
 typedef struct o_out_s o_out;
 static void dump_vertex(const o_vertex *x, o_out *o);
 
-/* vertex accessor: materialises lazily-built vertices on first use */
+/* vertex accessor: materialises lazily-built vertices on first use.
+ * built[u]: 0 = not built, 1 = being built by one thread, 2 = built.  The thread that
+ * moves it 0 -> 1 builds the vertex and publishes it with a release store of 2; every
+ * reader acquires 2 before touching the vertex (other builders of the same vertex wait),
+ * so distinct vertices build in parallel and no read races a write. */
 static o_vertex *vx(const ora_graph *Gc, uint32_t u)
 {
     ora_graph *G = (ora_graph *)Gc;
     o_vertex *x = &G->v[u];
-    if (G->lazy && !G->built[u]) {
-#ifdef _OPENMP
-#pragma omp critical(ora_lazy)
-#endif
-        {
-            if (!G->built[u]) {
-                x->d = (uint32_t)(G->lro[u + 1] - G->lro[u]);
-                x->cap = x->d;
-                x->adj = (o_arc *)malloc(sizeof(o_arc) * (x->cap ? x->cap : 1));
-                for (uint32_t i = 0; i < x->d; i++) {
-                    x->adj[i].dst = G->ldst[G->lro[u] + i];
-                    x->adj[i].bias = G->lbias[G->lro[u] + i];
-                    x->adj[i].epoch = 0;
-                    x->adj[i].dval = 0;
-                }
-                build_vertex(G, x);
-#ifdef _OPENMP
-#pragma omp flush
-#endif
-                G->built[u] = 1;
-            }
+    if (!G->lazy || __atomic_load_n(&G->built[u], __ATOMIC_ACQUIRE) == 2) return x;
+    uint8_t expect = 0;
+    if (__atomic_compare_exchange_n(&G->built[u], &expect, 1, 0, __ATOMIC_ACQ_REL, __ATOMIC_ACQUIRE)) {
+        x->d = (uint32_t)(G->lro[u + 1] - G->lro[u]);
+        x->cap = x->d;
+        x->adj = (o_arc *)malloc(sizeof(o_arc) * (x->cap ? x->cap : 1));
+        for (uint32_t i = 0; i < x->d; i++) {
+            x->adj[i].dst = G->ldst[G->lro[u] + i];
+            x->adj[i].bias = G->lbias[G->lro[u] + i];
+            x->adj[i].epoch = 0;
+            x->adj[i].dval = 0;
+        }
+        build_vertex(G, x);
+        __atomic_store_n(&G->built[u], 2, __ATOMIC_RELEASE);
+    } else {
+        while (__atomic_load_n(&G->built[u], __ATOMIC_ACQUIRE) != 2) {
         }
     }
     return x;
@@ -795,13 +794,22 @@ static int apply_updates_int(ora_graph *G, const uint32_t *recs, const uint64_t 
 
 /* ------------------------------------------------------------------ */
 /* Sampling.                             */
-/* counter = (walker, step, (outer << 16) + inner, tag), key = seed.   */
+/* counter = (walker, step, (outer << 16) + inner, tag + (outer >> 16 << 8)), key = seed. */
 /* ------------------------------------------------------------------ */
 static void draw(uint64_t seed, uint32_t w, uint32_t t, uint32_t c2, uint32_t tag, uint32_t r[4])
 {
     uint32_t ctr[4] = {w, t, c2, tag};
     uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
     ora_philox4x32_10(ctr, key, r);
+}
+
+/* The draw of (outer attempt, inner attempt, tag): counter word 2 = (outer << 16) + inner,
+ * word 3 = tag + ((outer >> 16) << 8) -- outer attempts past 65535 carry their high bits
+ * into the tag word, so node2vec's rejection draws never repeat (R-1). */
+static void draw_oi(uint64_t seed, uint32_t w, uint32_t t, uint32_t outer, uint32_t inner, uint32_t tag,
+                    uint32_t r[4])
+{
+    draw(seed, w, t, (outer << 16) + inner, tag + ((outer >> 16) << 8), r);
 }
 
 /* One first-order sample at vertex u (d > 0): inter-group alias (Eq.5),
@@ -816,18 +824,18 @@ static uint32_t sample_arc(const o_vertex *x, uint64_t seed, uint32_t w, uint32_
         /* float mode (R-15): the decimal group with probability thrD / 2^64 */
         int dec = 1;
         if (!(x->fflags & 2u)) {
-            draw(seed, w, t, outer << 16, 5, r);
+            draw_oi(seed, w, t, outer, 0, 5, r);
             dec = (((uint64_t)r[0] << 32) | r[1]) < x->thrD;
         }
         if (dec) {
             for (uint32_t a = 0;; a++) {
-                draw(seed, w, t, (outer << 16) + a, 4, r);
+                draw_oi(seed, w, t, outer, a, 4, r);
                 uint64_t j = mulhi64(((uint64_t)r[0] << 32) | r[1], x->dcnt);
                 if (mulhi64(((uint64_t)r[2] << 32) | r[3], x->dmax) < x->dval[j]) return x->didx[j];
             }
         }
     }
-    draw(seed, w, t, outer << 16, 0, r);
+    draw_oi(seed, w, t, outer, 0, 0, r);
     /* stage (i): inter-group alias */
     uint32_t b = (uint32_t)(((uint64_t)r[0] * x->n) >> 32);
     uint64_t coin = mulhi64(((uint64_t)r[1] << 32) | r[2], x->T);
@@ -836,13 +844,13 @@ static uint32_t sample_arc(const o_vertex *x, uint64_t seed, uint32_t w, uint32_
     /* stage (ii): intra-group */
     if (g->kind == O_ONE) return g->one;
     if (g->kind == O_REGULAR || g->kind == O_SPARSE) {
-        draw(seed, w, t, outer << 16, 1, r);
+        draw_oi(seed, w, t, outer, 0, 1, r);
         uint64_t j = mulhi64(((uint64_t)r[0] << 32) | r[1], g->c);
         return g->mem[j];
     }
     /* DENSE: rejection over the whole adjacency, accept iff bias AND 2^k != 0 */
     for (uint32_t a = 0;; a++) {
-        draw(seed, w, t, (outer << 16) + a, 1, r);
+        draw_oi(seed, w, t, outer, a, 1, r);
         uint64_t j = mulhi64(((uint64_t)r[0] << 32) | r[1], x->d);
         *attempts = a + 1;
         if ((x->adj[j].bias >> g->k) & 1u) return (uint32_t)j;
@@ -906,7 +914,7 @@ void ora_walk(const ora_graph *G, uint32_t app, uint32_t L, uint64_t seed, uint3
                     int cls = n2v_class(G, prev, next);
                     if (n2v_always[cls]) break;
                     uint32_t r[4];
-                    draw(seed, w, t, o << 16, 2, r);
+                    draw_oi(seed, w, t, o, 0, 2, r);
                     if ((((uint64_t)r[0] << 32) | r[1]) < n2v_thr[cls]) break;
                 }
             } else {

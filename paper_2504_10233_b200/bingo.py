@@ -140,6 +140,22 @@ def _stream_ptr(stream) -> Optional[int]:
     return stream.cuda_stream
 
 
+def _order_on(stream, device, *tensors):
+    """A call on a caller-given stream: that stream first waits for the current stream (where
+    the temporaries / outputs below were allocated and filled), and every device tensor is
+    marked as used by it, so the caching allocator does not hand its memory out again
+    before the launch completes."""
+    if stream is None:
+        return
+    torch = _torch()
+    cur = torch.cuda.current_stream(device)
+    if stream != cur:
+        stream.wait_stream(cur)
+    for t in tensors:
+        if t is not None and isinstance(t, torch.Tensor) and t.is_cuda:
+            t.record_stream(stream)
+
+
 def _dev_u32(x, torch, device):
     if isinstance(x, torch.Tensor):
         t = x.to(device=device)
@@ -219,6 +235,7 @@ class Graph:
                       alloc=self._alloc.alloc if self._alloc else ALLOC_FN(), free=self._alloc.free if self._alloc else FREE_FN(),
                       alloc_ctx=None, bias_f64=bf.data_ptr() if bf is not None else None)
         h = ctypes.c_void_p()
+        _order_on(stream, self.device, ro, ds, bs, bf)
         with torch.cuda.device(self.device):
             _check(L.bingo_build(ctypes.byref(d), _stream_ptr(stream), ctypes.byref(h)), "bingo_build")
         self._h = h
@@ -263,6 +280,8 @@ class Graph:
             b = arr
             if bias_f64 is not None:
                 wf = np.ascontiguousarray(bias_f64, dtype=np.float64)
+        if isinstance(b, torch.Tensor):
+            _order_on(stream, self.device, b, wf)
         same = self.device.index is None or torch.cuda.current_device() == self.device.index
         with contextlib.nullcontext() if same else torch.cuda.device(self.device):
             if wf is None:
@@ -307,6 +326,7 @@ class Graph:
             ln = lengths
         d = WalkDesc(app=app, length=length, p=p, q=q, stop_num=stop[0], stop_den=stop[1], seed=seed,
                      first_walker_id=first_walker, flags=WALK_WALKER_MAJOR if walker_major else 0)
+        _order_on(stream, self.device, st, pa, ln)
         with torch.cuda.device(self.device):
             _check(_lib().bingo_walk(self._h, ctypes.byref(d), st.data_ptr() if st is not None else None, W,
                                      pa.data_ptr() if pa is not None else None,
@@ -346,6 +366,7 @@ class Graph:
         d = WalkDesc(app=app, length=length, p=p, q=q, stop_num=stop[0], stop_den=stop[1], seed=seed,
                      first_walker_id=first_walker, flags=0)
         c = np.zeros(8, dtype=np.uint64)
+        _order_on(stream, self.device, st, pa, ln)
         with torch.cuda.device(self.device):
             _check(_lib().bingo_walk_profile(self._h, ctypes.byref(d), st.data_ptr() if st is not None else None, W,
                                              pa.data_ptr() if pa is not None else None, ln.data_ptr(), c.ctypes.data,
@@ -359,6 +380,7 @@ class Graph:
     def visit_counts(self, reset: bool = False, stream=None):
         torch = _torch()
         out = torch.empty(self.V, dtype=torch.int64, device=self.device)
+        _order_on(stream, self.device, out)
         with torch.cuda.device(self.device):
             _check(_lib().bingo_visit_counts(self._h, out.data_ptr(), int(reset), 0, _stream_ptr(stream)),
                    "bingo_visit_counts")
@@ -392,6 +414,7 @@ class Graph:
     def digests(self, stream=None):
         torch = _torch()
         out = torch.empty(self.V, dtype=torch.int64, device=self.device)
+        _order_on(stream, self.device, out)
         with torch.cuda.device(self.device):
             _check(_lib().bingo_digests(self._h, out.data_ptr(), _stream_ptr(stream)), "bingo_digests")
         return out

@@ -119,6 +119,13 @@ __device__ __forceinline__ P4 philox10(uint32_t c0, uint32_t c1, uint32_t c2, ui
 
 __device__ __forceinline__ uint64_t join64(uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; }
 
+// The draw of (outer attempt, inner attempt, tag) (R-1): counter word 2 = (outer << 16) + inner,
+// word 3 = tag + ((outer >> 16) << 8), so node2vec outer attempts past 65535 never repeat a counter.
+__device__ __forceinline__ P4 draw_oi(uint32_t w, uint32_t t, uint32_t outer, uint32_t inner, uint32_t tag,
+                                      uint32_t k0, uint32_t k1) {
+    return philox10(w, t, (outer << 16) + inner, tag + ((outer >> 16) << 8), k0, k1);
+}
+
 // ---------------------------------------------------------------- warp helpers
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ uint32_t lanemask_lt() { return (1u << lane_id()) - 1u; }

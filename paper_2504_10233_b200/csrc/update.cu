@@ -21,6 +21,7 @@
 //   k_upd_stats      reduce per-vertex statistics
 // Untouched vertices are never read or written.
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -957,6 +958,16 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
         }
     }
     __syncthreads();
+    // an invalid batch is rejected whole before anything is read through its ids (a src >= V
+    // must never index hdr[]): uniform exit, nothing mutated (bingo.h: EINVAL)
+    if (flag & FAST_INVAL) {
+        if (tid == 0) {
+            fa.out->status = FAST_INVAL;
+            fa.out->ntouch = 0;
+            fa.out->inserted = 0;
+        }
+        return;
+    }
     // stable grouping by src: rank = #{j : src_j < src_i, or src_j == src_i and j < i}
     if (tid < n) {
         const uint32_t si = recs[tid].y;
@@ -1286,10 +1297,19 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
     ho->status = 0xFFFFFFFFu;
     // one warp per touched vertex at most (a vertex's records go to one warp): small
     // blocks keep the block-wide barriers of the single-record case cheap
-    static bool smem_set = false;
-    if (!smem_set) {   // up to 32 warps x WARP_SCR_WORDS of dynamic shared memory
-        cudaFuncSetAttribute(k_upd_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 4 * WARP_SCR_WORDS);
-        smem_set = true;
+    // up to 32 warps x WARP_SCR_WORDS of dynamic shared memory: the attribute is per device,
+    // so it is raised once for every device this process launches the fast path on
+    static std::atomic<uint64_t> smem_set{0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(smem_set.load(std::memory_order_acquire) & bit)) {
+        if (cudaFuncSetAttribute(k_upd_fast, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * 4 * WARP_SCR_WORDS) !=
+            cudaSuccess) {
+            *out = upd_cuda_fail(g, cudaGetLastError(), "k_upd_fast smem attribute");
+            return true;
+        }
+        smem_set.fetch_or(bit, std::memory_order_acq_rel);
     }
     const unsigned fw = (unsigned)std::min<uint64_t>(32, std::max<uint64_t>(2, n));
     k_upd_fast<<<1, 32 * fw, 4 * WARP_SCR_WORDS * fw, s>>>(fa);

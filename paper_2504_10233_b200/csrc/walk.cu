@@ -6,7 +6,7 @@
 //   VHdr[u] -> Bucket[bkt_off + b] -> (member | arc per dense attempt)
 // and one coalesced, streaming (evict-first) store of the path column.
 // Randomness: Philox4x32-10 keyed by the seed, counter (walker, step,
-// (outer << 16) + inner, tag) (R-1) -- no RNG state in memory.
+// (outer << 16) + inner, tag + ((outer >> 16) << 8)) (R-1, draw_oi) -- no RNG state in memory.
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -106,11 +106,11 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, PROF ? 4 : (APP == BINGO_NODE2
                         // (p = 2, q = 0.5: half of them; p = 0.5, q = 2: three quarters).
                         if (next == prev) {
                             if (!a.n2v_always[0]) {
-                                const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
+                                const P4 r = draw_oi(w, t, o, 0u, 2u, a.k0, a.k1);
                                 accept = join64(r.x, r.y) < a.n2v_thr[0];
                             }
                         } else if (!(a.n2v_always[1] && a.n2v_always[2])) {
-                            const P4 r = philox10(w, t, o << 16, 2u, a.k0, a.k1);
+                            const P4 r = draw_oi(w, t, o, 0u, 2u, a.k0, a.k1);
                             const uint64_t x = join64(r.x, r.y);
                             const bool a1 = a.n2v_always[1] || x < a.n2v_thr[1];
                             const bool a2 = a.n2v_always[2] || x < a.n2v_thr[2];
@@ -260,6 +260,12 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     a.k1 = (uint32_t)(desc->seed >> 32);
     n2v_thresholds(desc->app == BINGO_NODE2VEC ? desc->p : 1.0, desc->app == BINGO_NODE2VEC ? desc->q : 1.0,
                    a.n2v_thr, a.n2v_always);
+    // a class whose accept ratio f/f_max is below 2^-64 could never be accepted (its threshold
+    // floors to 0): a walker whose proposals all fall in it would never finish -> EINVAL.
+    // Otherwise the expected proposals per step are at most f_max / f_min (draw_oi never
+    // repeats a counter, so the attempts are independent).
+    for (int c = 0; c < 3; c++)
+        if (desc->app == BINGO_NODE2VEC && !a.n2v_always[c] && a.n2v_thr[c] == 0) return BINGO_E_INVAL;
     stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
     a.prof = prof;
     if (!g->walk_ctr) return BINGO_E_STATE;

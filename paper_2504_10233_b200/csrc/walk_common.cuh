@@ -118,7 +118,7 @@ __device__ __forceinline__ uint2 ldg8(const uint2 *p, uint64_t pol) {
 template <bool PROF>
 __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr &h, uint32_t w, uint32_t t,
                                                uint32_t outer, WalkProf &prof, const Policies &pol) {
-    const P4 r = philox10(w, t, outer << 16, 0u, a.k0, a.k1);
+    const P4 r = draw_oi(w, t, outer, 0u, 0u, a.k0, a.k1);
     const uint32_t b = __umulhi(r.x, (uint32_t)h.n);
     const Bucket B = ldg_bucket(a.bkt + h.bkt_off + b, (h.flags & 1u) ? pol.keep : pol.stream);
     if (PROF) prof.bkt++;
@@ -139,15 +139,15 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
     // kinds does not run it twice
 #ifdef BINGO_NO_HOIST            // A/B experiment switch: the draw inside each branch
     if (kind != K_DENSE) {
-        const P4 q0 = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
+        const P4 q0 = draw_oi(w, t, outer, 0u, 1u, a.k0, a.k1);
         const uint64_t j0 = __umul64hi(join64(q0.x, q0.y), (uint64_t)x);
         if (PROF) prof.mem++;
         return ldg4(a.mdst + (uint64_t)y * 4 + j0, (h.flags & 2u) ? pol.keep : pol.stream);
     }
-    const P4 q0 = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
+    const P4 q0 = draw_oi(w, t, outer, 0u, 1u, a.k0, a.k1);
     const uint64_t j0 = __umul64hi(join64(q0.x, q0.y), (uint64_t)x);
 #else
-    const P4 q0 = philox10(w, t, outer << 16, 1u, a.k0, a.k1);
+    const P4 q0 = draw_oi(w, t, outer, 0u, 1u, a.k0, a.k1);
     const uint64_t j0 = __umul64hi(join64(q0.x, q0.y), (uint64_t)x);
     if (kind != K_DENSE) {
         if (PROF) prof.mem++;
@@ -162,7 +162,7 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
         for (int s = 0; s < BINGO_DENSE_SPEC; s++) {
             uint64_t j = j0;
             if (base + s) {
-                const P4 q = philox10(w, t, (outer << 16) + base + s, 1u, a.k0, a.k1);
+                const P4 q = draw_oi(w, t, outer, base + s, 1u, a.k0, a.k1);
                 j = __umul64hi(join64(q.x, q.y), (uint64_t)x);
             }
             #ifdef BINGO_ARC_STREAM          // A/B experiment switch: dense arc reads always evict_first
@@ -210,12 +210,12 @@ __device__ __forceinline__ uint32_t sample_dst_f(const WalkArgs &a, const ThinHd
     if (dr.thrD) {
         bool decimal = true;
         if (!(dr.flags & 2u)) {
-            const P4 r = philox10(w, t, outer << 16, 5u, a.k0, a.k1);
+            const P4 r = draw_oi(w, t, outer, 0u, 5u, a.k0, a.k1);
             decimal = join64(r.x, r.y) < dr.thrD;
         }
         if (decimal) {
             for (uint32_t att = 0;; att++) {
-                const P4 q = philox10(w, t, (outer << 16) + att, 4u, a.k0, a.k1);
+                const P4 q = draw_oi(w, t, outer, att, 4u, a.k0, a.k1);
                 const uint64_t j = __umul64hi(join64(q.x, q.y), (uint64_t)dr.dcnt);
                 const uint4 e = __ldg(a.dmem + dr.doff + j);
                 if (PROF) prof.arc++;

@@ -42,32 +42,56 @@ class ReplicatedBingo:
         self.device = device if device is not None else getattr(engine, "device", torch.device("cpu"))
 
     # ------------------------------------------------------------ updates
-    def broadcast_batch(self, batch: Optional[torch.Tensor]) -> torch.Tensor:
-        """Rank 0's (n, 4) int32 batch reaches every rank (size first, then payload)."""
-        n = torch.zeros(1, dtype=torch.int64, device=self.device)
-        if self.rank == 0:
-            n[0] = batch.shape[0]
-        if self.world > 1:
-            dist.broadcast(n, 0, group=self.group)
-        nn = int(n.item())
+    def broadcast_batch(self, batch: Optional[torch.Tensor], n: Optional[int] = None) -> torch.Tensor:
+        """Rank 0's (n, 4) int32 batch reaches every rank.  When every rank already knows
+        the record count (`n`, e.g. a fixed batch size) only the payload is broadcast and
+        nothing waits on the host; otherwise the size goes first (one host read).  At world
+        size 1 the batch is returned as is (moved to the device if needed)."""
+        if self.world == 1:
+            return batch.to(self.device, dtype=torch.int32).contiguous()
+        if n is None:
+            nt = torch.zeros(1, dtype=torch.int64, device=self.device)
+            if self.rank == 0:
+                nt[0] = batch.shape[0]
+            dist.broadcast(nt, 0, group=self.group)
+            n = int(nt.item())
         if self.rank == 0:
             buf = batch.to(self.device, dtype=torch.int32).contiguous()
+            assert buf.shape[0] == n, (buf.shape, n)
         else:
-            buf = torch.empty((nn, 4), dtype=torch.int32, device=self.device)
-        if self.world > 1 and nn:
+            buf = torch.empty((n, 4), dtype=torch.int32, device=self.device)
+        if n:
             dist.broadcast(buf, 0, group=self.group)
         return buf
 
-    def apply_updates(self, batch: Optional[torch.Tensor]) -> dict:
-        buf = self.broadcast_batch(batch)
+    def apply_updates(self, batch: Optional[torch.Tensor], n: Optional[int] = None) -> dict:
+        buf = self.broadcast_batch(batch, n)
         return self.g.apply_updates(buf)
 
     # ------------------------------------------------------------ walks
     def walk(self, num_walkers: int, first_walker: int = 0, **kw) -> dict:
         """Walk this rank's shard of walker ids [first_walker, first_walker + num_walkers).
-        One walker per vertex by default (starts = id mod V).  Returns the engine's
-        outputs plus this rank's (first, count)."""
+        One walker per vertex by default (starts = id mod V).  Per-walker inputs and
+        outputs given for ALL walkers are sliced to this rank's shard: `starts` and
+        `lengths` ([num_walkers]) and walker-major `paths` ([num_walkers, L + 1]);
+        step-major paths must already be this shard's ([L + 1, count]).  Returns the
+        engine's outputs plus this rank's (first, count)."""
         first, count = shard_range(num_walkers, self.rank, self.world)
+        if kw.get("starts") is not None:
+            st = kw["starts"]
+            if len(st) != num_walkers:
+                raise ValueError(f"starts has {len(st)} entries for {num_walkers} walkers")
+            kw["starts"] = st[first:first + count]
+        ln = kw.get("lengths")
+        if isinstance(ln, torch.Tensor) and ln.shape[0] == num_walkers and count != num_walkers:
+            kw["lengths"] = ln[first:first + count]
+        pa = kw.get("paths")
+        if isinstance(pa, torch.Tensor):
+            if kw.get("walker_major"):
+                if pa.shape[0] == num_walkers and count != num_walkers:
+                    kw["paths"] = pa[first:first + count]
+            elif pa.dim() == 2 and pa.shape[1] != count:
+                raise ValueError("step-major paths must hold this rank's shard: shape (L + 1, count)")
         out = self.g.walk(first_walker=first_walker + first, num_walkers=count, **kw)
         out["shard"] = (first_walker + first, count)
         return out

@@ -70,8 +70,9 @@ def rmat_edges(scale: int, n_edges: int, seed: int, abcd=RMAT_ABCD, chunk: int =
     return src, dst
 
 
-def simple_undirected(scale: int, n_edges: int, seed: int, compact: bool, device="cpu"):
-    """Undirected simple edge list (lo < hi pairs, unique) with a random relabelling."""
+def simple_undirected(scale: int, n_edges: int, seed: int, compact: bool, device="cpu", resident=False):
+    """Undirected simple edge list (lo < hi pairs, unique) with a random relabelling.
+    resident=True returns int32 tensors on `device` instead of numpy u32 arrays."""
     import torch
     s, t = rmat_edges(scale, n_edges, seed, device=device)
     keep = s != t
@@ -96,6 +97,8 @@ def simple_undirected(scale: int, n_edges: int, seed: int, compact: bool, device
     a = torch.minimum(lo, hi).to(torch.int32)
     b = torch.maximum(lo, hi).to(torch.int32)
     del lo, hi, perm
+    if resident:
+        return V, a, b
     return V, a.cpu().numpy().view(np.uint32), b.cpu().numpy().view(np.uint32)
 
 
@@ -144,34 +147,38 @@ def degree_bias_of(deg: np.ndarray, dst: np.ndarray, clamp=None) -> np.ndarray:
     return w.astype(np.uint32)
 
 
-def make_workload(name: str, rounds: int = 1, device="cpu", **over) -> "Workload":
+def make_workload(name: str, rounds: int = 1, device="cpu", hold_rounds=None, resident=False,
+                  **over):
+    """resident=True (device must be CUDA): the graph stays in HBM as tensors
+    (DeviceWorkload); otherwise numpy arrays (Workload)."""
     cfg = dict(CONFIGS[name])
     cfg.update(over)
-    return Workload(cfg["scale"], cfg["edges"], compact=cfg["compact"], bias=cfg["bias"],
-                    clamp=cfg["clamp"], batch=cfg["batch"], rounds=rounds, device=device)
+    cls = DeviceWorkload if resident else Workload
+    return cls(cfg["scale"], cfg["edges"], compact=cfg["compact"], bias=cfg["bias"],
+               clamp=cfg["clamp"], batch=cfg["batch"], rounds=rounds, device=device, hold_rounds=hold_rounds)
 
 
 class Workload:
-    """A seeded graph + update stream following the recipe above."""
+    """A seeded graph + update stream following the recipe above.
+
+    hold_rounds: the held-out set B is hold_rounds x batch edges (default: `rounds`), so the
+    initial graph does not depend on how many batches are drawn (P:658 holds out the edges of
+    its 10 rounds); batch i is the same whatever `rounds` is.  Once B is used up, edges deleted
+    earlier become insertable again (the stream never runs dry)."""
 
     def __init__(self, scale, edges, seed=1, compact=True, bias="degree", clamp=None, batch=1000,
-                 rounds=1, update_seed=2, undirected=True, device="cpu"):
+                 rounds=1, update_seed=2, undirected=True, device="cpu", hold_rounds=None):
         V, a, b = simple_undirected(scale, edges, seed, compact, device=device)
         self.V = V
         E = len(a)
         # full-graph degrees fix every bias, including those of later inserts
         deg_full = np.bincount(a, minlength=V) + np.bincount(b, minlength=V)
         rng = np.random.default_rng(update_seed)
-        n_hold = min(E // 2, rounds * batch)
+        n_hold = min(E // 2, (hold_rounds if hold_rounds is not None else rounds) * batch)
         perm = rng.permutation(E)
         held = perm[:n_hold]
         live = perm[n_hold:]
-        self.batch = batch
-        self.rounds = rounds
-        self.deg_full = deg_full
-        self.bias_kind = bias
-        self.clamp = clamp
-        self._bias_seed = seed + 7
+        self._setup(V, batch, rounds, deg_full, bias, clamp, seed)
         # initial graph A
         src = np.concatenate([a[live], b[live]])
         dst = np.concatenate([b[live], a[live]])
@@ -179,46 +186,33 @@ class Workload:
         self.row_offsets, self.dst, self.bias = csr_from_arcs(V, src, dst, extra=w, device=device)
         del src, dst, w
         self.num_arcs = int(self.row_offsets[-1])
-        # update stream: coin flip, delete uniform live edge of A,
-        # insert uniform unused edge of B into A
         self.batches = []
-        live_list = live.copy()
-        n_live = len(live_list)
-        pool = held.copy()
-        rng.shuffle(pool)
-        pool_pos = 0
-        for _ in range(rounds):
-            ops = rng.integers(0, 2, size=batch)
-            uni = rng.random(batch)
-            src_r = np.zeros(batch, dtype=np.int64)
-            dst_r = np.zeros(batch, dtype=np.int64)
-            for i in range(batch):
-                if (ops[i] == 1 and n_live > 0) or pool_pos >= len(pool):
-                    j = int(uni[i] * n_live)
-                    e = live_list[j]
-                    live_list[j] = live_list[n_live - 1]
-                    n_live -= 1
-                else:
-                    ops[i] = 0
-                    e = pool[pool_pos]
-                    pool_pos += 1
-                    if n_live == len(live_list):
-                        live_list = np.concatenate([live_list, np.zeros(max(1024, batch), live_list.dtype)])
-                    live_list[n_live] = e
-                    n_live += 1
-                src_r[i] = a[e]
-                dst_r[i] = b[e]
-            recs = np.zeros((2 * batch, 4), dtype=np.uint32)
-            recs[0::2, 0] = ops
-            recs[1::2, 0] = ops
-            recs[0::2, 1] = src_r
-            recs[0::2, 2] = dst_r
-            recs[1::2, 1] = dst_r
-            recs[1::2, 2] = src_r
-            ins = ops == INSERT
-            recs[0::2, 3] = np.where(ins, self._bias(src_r, dst_r), 0)
-            recs[1::2, 3] = np.where(ins, self._bias(dst_r, src_r), 0)
-            self.batches.append(recs)
+        for ev_src, ev_dst, ops in _update_events(rng, live, held, batch, rounds, lambda e: (a[e], b[e])):
+            self.batches.append(self._records(ev_src, ev_dst, ops))
+
+    def _setup(self, V, batch, rounds, deg_full, bias, clamp, seed):
+        self.V = V
+        self.batch = batch
+        self.rounds = rounds
+        self.deg_full = deg_full
+        self.bias_kind = bias
+        self.clamp = clamp
+        self._bias_seed = seed + 7
+
+    def _records(self, src_r, dst_r, ops):
+        """Each undirected event -> two arc records {op, src, dst, bias} (S5.2)."""
+        n = len(ops)
+        recs = np.zeros((2 * n, 4), dtype=np.uint32)
+        recs[0::2, 0] = ops
+        recs[1::2, 0] = ops
+        recs[0::2, 1] = src_r
+        recs[0::2, 2] = dst_r
+        recs[1::2, 1] = dst_r
+        recs[1::2, 2] = src_r
+        ins = ops == INSERT
+        recs[0::2, 3] = np.where(ins, self._bias(src_r, dst_r), 0)
+        recs[1::2, 3] = np.where(ins, self._bias(dst_r, src_r), 0)
+        return recs
 
     def _bias(self, src, dst):
         if self.bias_kind == "degree":
@@ -236,6 +230,118 @@ class Workload:
         if self.bias_kind == "loguniform":
             return np.floor(np.exp(np.log(lo) + x * (np.log(hi + 1) - np.log(lo)))).clip(lo, hi).astype(np.uint32)
         raise ValueError(self.bias_kind)
+
+
+def _update_events(rng, live, held, batch, rounds, endpoints):
+    """The P:658 stream over edge ids: per event a fair coin (Mixed) -- delete a
+    uniform live edge (swap-remove from the live list) or insert the next unused edge of the
+    shuffled held-out pool; a deleted edge joins the end of the pool, so inserts continue
+    once the held-out edges are used up.  Yields (src, dst, ops) per round; `endpoints(e)`
+    maps an int array of edge ids to their (lo, hi) endpoint arrays."""
+    live_list = np.array(live, dtype=np.int64)       # a private copy: swap-removal mutates it
+    n_live = len(live_list)
+    pool = list(np.array(held, dtype=np.int64)[rng.permutation(len(held))])
+    pool_pos = 0
+    for _ in range(rounds):
+        ops = rng.integers(0, 2, size=batch)
+        uni = rng.random(batch)
+        ev = np.zeros(batch, dtype=np.int64)
+        for i in range(batch):
+            if (ops[i] == 1 and n_live > 0) or pool_pos >= len(pool):
+                ops[i] = 1
+                j = int(uni[i] * n_live)
+                e = int(live_list[j])
+                live_list[j] = live_list[n_live - 1]
+                n_live -= 1
+                pool.append(e)
+            else:
+                ops[i] = 0
+                e = int(pool[pool_pos])
+                pool_pos += 1
+                if n_live == len(live_list):
+                    live_list = np.concatenate([live_list, np.zeros(max(1024, batch), live_list.dtype)])
+                live_list[n_live] = e
+                n_live += 1
+            ev[i] = e
+        src_r, dst_r = endpoints(ev)
+        yield np.asarray(src_r, dtype=np.int64), np.asarray(dst_r, dtype=np.int64), ops
+
+
+class DeviceWorkload(Workload):
+    """The same recipe with the graph generated and kept in HBM (torch CUDA ops): R-MAT,
+    simple + relabelled + symmetrised, the held-out split, the (src, dst)-sorted CSR and the
+    degree biases never leave the device.  row_offsets (int64), dst and bias (int32 holding
+    u32) are CUDA tensors; the update batches are numpy (the host stream of P:658; edge ids
+    are drawn on the host, their endpoints gathered on the device).  `host_csr()` copies the
+    CSR out for the CPU oracle.  Minutes -> seconds at Twitter/Friendster scale."""
+
+    def __init__(self, scale, edges, seed=1, compact=True, bias="degree", clamp=None, batch=1000,
+                 rounds=1, update_seed=2, undirected=True, device="cuda", hold_rounds=None):
+        import torch
+        dev = torch.device(device)
+        assert dev.type == "cuda", "DeviceWorkload keeps the graph in HBM"
+        if bias != "degree":
+            raise ValueError("DeviceWorkload: degree biases only (P:664)")
+        V, a, b = simple_undirected(scale, edges, seed, compact, device=dev, resident=True)
+        E = a.numel()
+        deg_full = torch.bincount(a, minlength=V) + torch.bincount(b, minlength=V)
+        self._setup(V, batch, rounds, deg_full.cpu().numpy(), bias, clamp, seed)
+        n_hold = min(E // 2, (hold_rounds if hold_rounds is not None else rounds) * batch)
+        g = torch.Generator(device=dev).manual_seed(update_seed)
+        perm = torch.randperm(E, generator=g, device=dev)
+        held, live = perm[:n_hold], perm[n_hold:]
+        # initial graph A: both arcs of every live edge, CSR sorted by (src, dst)
+        la, lb = a[live], b[live]
+        src = torch.cat([la, lb])
+        dst = torch.cat([lb, la])
+        del la, lb
+        cnt = torch.bincount(src, minlength=V)
+        ro = torch.zeros(V + 1, dtype=torch.int64, device=dev)
+        ro[1:] = torch.cumsum(cnt, 0)
+        del cnt
+        key = (src.to(torch.int64) << 32) | dst.to(torch.int64)
+        del dst
+        out = torch.empty_like(key)
+        ro_h = ro.cpu().numpy()
+        v0 = 0
+        LIM = 1 << 30                   # sort in source-vertex ranges of <= 2^30 arcs
+        while v0 < V:
+            v1 = max(int(np.searchsorted(ro_h, ro_h[v0] + LIM, side="right")) - 1, v0 + 1)
+            if v0 == 0 and v1 >= V:
+                out = torch.sort(key).values
+            else:
+                m = (src >= v0) & (src < v1)
+                out[int(ro_h[v0]):int(ro_h[v1])] = torch.sort(key[m]).values
+                del m
+            v0 = v1
+        del key, src
+        dsorted = (out & 0xFFFFFFFF).to(torch.int32)
+        del out
+        w = torch.clamp(deg_full[dsorted.to(torch.int64)], min=1)
+        if clamp is not None:
+            w = torch.clamp(w, clamp[0], clamp[1])
+        self.row_offsets = ro
+        self.dst = dsorted
+        self.bias = w.to(torch.int64).to(torch.int32)
+        del w
+        self.num_arcs = int(ro_h[-1])
+        rng = np.random.default_rng(update_seed)
+        live_h = live.to(torch.int32).cpu().numpy()
+        held_h = held.cpu().numpy()
+        del perm, held, live
+
+        def endpoints(ev):
+            idx = torch.from_numpy(ev).to(dev)
+            return a[idx].cpu().numpy().view(np.uint32), b[idx].cpu().numpy().view(np.uint32)
+        self.batches = [self._records(s_, d_, o_)
+                        for s_, d_, o_ in _update_events(rng, live_h, held_h, batch, rounds, endpoints)]
+        del a, b
+        torch.cuda.empty_cache()
+
+    def host_csr(self):
+        """(row_offsets u64, dst u32, bias u32) numpy copies for the CPU oracle."""
+        return (self.row_offsets.cpu().numpy().view(np.uint64), self.dst.cpu().numpy().view(np.uint32),
+                self.bias.cpu().numpy().view(np.uint32))
 
 
 def random_small_graph(rng: np.random.Generator, V: int, max_deg: int, max_bias: int, directed=True):

@@ -30,11 +30,14 @@ class OracleEngine:
     def apply_updates(self, batch):
         return self.o.apply_updates(batch.numpy().view(np.uint32))
 
-    def walk(self, app=0, length=80, seed=0, first_walker=0, num_walkers=None, stop=(1, 80), **kw):
+    def walk(self, app=0, length=80, seed=0, first_walker=0, num_walkers=None, stop=(1, 80), starts=None, **kw):
         import oracle
         counts = app == oracle.APP_PPR
+        if starts is not None:
+            assert len(starts) == num_walkers
+            starts = np.asarray(starts, dtype=np.uint32)
         r = self.o.walk(app=app, length=length, seed=seed, first_walker=first_walker, num_walkers=num_walkers,
-                        stop=stop, paths=length != oracle.NONE, counts=counts, threads=1)
+                        starts=starts, stop=stop, paths=length != oracle.NONE, counts=counts, threads=1)
         if counts:
             self._counts += r["counts"]
         out = {"lengths": torch.from_numpy(r["lengths"].view(np.int32).copy())}
@@ -79,6 +82,10 @@ def _worker(rank, world, port, outdir):
     assert (first, count) == shard_range(w.V, rank, world)
     rb.walk(num_walkers=3 * w.V, length=oracle.NONE, app=oracle.APP_PPR, seed=4)
     counts = rb.visit_counts()
+    # explicit per-walker starts given for ALL walkers: each rank must walk its own slice
+    starts = np.random.default_rng(17).integers(0, w.V, size=2 * w.V + 3).astype(np.uint32)
+    sout = rb.walk(num_walkers=len(starts), length=12, seed=9, starts=starts)
+    np.save(os.path.join(outdir, f"spaths{rank}.npy"), sout["paths"].numpy())
     np.save(os.path.join(outdir, f"paths{rank}.npy"), out["paths"].numpy())
     np.save(os.path.join(outdir, f"counts{rank}.npy"), counts.numpy())
     dist.barrier()
@@ -109,6 +116,10 @@ def test_two_rank_gloo_driver(tmp_path):
     full = o.walk(length=20, seed=3, num_walkers=w.V)["paths"]
     parts = [np.load(tmp_path / f"paths{r}.npy").view(np.uint32) for r in range(world)]
     assert np.array_equal(np.concatenate(parts, axis=1), full)
+    starts = np.random.default_rng(17).integers(0, w.V, size=2 * w.V + 3).astype(np.uint32)
+    sfull = o.walk(length=12, seed=9, starts=starts, num_walkers=len(starts))["paths"]
+    sparts = [np.load(tmp_path / f"spaths{r}.npy").view(np.uint32) for r in range(world)]
+    assert np.array_equal(np.concatenate(sparts, axis=1), sfull), "explicit starts must be sliced per rank"
     ref = o.walk(app=oracle.APP_PPR, length=oracle.NONE, seed=4, num_walkers=3 * w.V, paths=False, counts=True)
     for r in range(world):
         assert np.array_equal(np.load(tmp_path / f"counts{r}.npy").view(np.uint64), ref["counts"])

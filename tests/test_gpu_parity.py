@@ -210,3 +210,25 @@ def test_walker_major_layout_and_profile():
     ppr = g.walk(app=pb.PPR, length=40, stop=(1, 7), seed=4, walker_major=True)
     rp = o.walk(app=oracle.APP_PPR, length=40, stop=(1, 7), seed=4)
     assert np.array_equal(u32(ppr["paths"]).T, rp["paths"])
+
+
+def test_walk_on_a_side_stream():
+    """temporaries (starts copied from host, auto-allocated paths/lengths) are made on
+    the current stream; a launch on another stream must be ordered after them and must keep
+    them alive until it completes."""
+    import torch
+    pb = _pb()
+    w = synth.make_workload("c1")
+    g, o = _graphs(w.row_offsets, w.dst, w.bias)
+    s = torch.cuda.Stream()
+    starts = (np.arange(50_000, dtype=np.uint64) * 7919 % w.V).astype(np.uint32)
+    outs = [g.walk(length=40, seed=100 + i, starts=starts, stream=s) for i in range(4)]
+    torch.cuda.synchronize()
+    for i, out in enumerate(outs):
+        ref = o.walk(length=40, seed=100 + i, starts=starts)
+        assert np.array_equal(u32(out["paths"]), ref["paths"])
+    g.walk(app=pb.PPR, length=pb.NO_CAP, seed=5, starts=starts, paths=None, stream=s)
+    c = g.visit_counts(reset=True, stream=s)
+    s.synchronize()
+    ref = o.walk(app=oracle.APP_PPR, length=oracle.NONE, seed=5, starts=starts, paths=False, counts=True)
+    assert np.array_equal(c.cpu().numpy().view(np.uint64), ref["counts"])

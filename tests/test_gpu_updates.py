@@ -319,3 +319,62 @@ def test_hub_delete_index_maintained_across_batches(hix, monkeypatch):
     out = g.walk(length=40, seed=11)
     ref = o.walk(length=40, seed=11)
     assert np.array_equal(u32(out["paths"]), ref["paths"])
+
+
+def test_fast_path_rejects_out_of_range_ids_without_reading_them():
+    """a single-launch (<= 256 records) batch with src = V must come back EINVAL
+    with nothing touched, also when the graph's memory does not come from the caching
+    allocator (an out-of-bounds header read would then fault instead of landing in a
+    neighbouring allocation)."""
+    pb = _pb()
+    w = synth.make_workload("c1")
+    for torch_alloc in (False, True):
+        g = pb.Graph(w.row_offsets, w.dst, w.bias, torch_alloc=torch_alloc)
+        before = g.export()
+        for bad in ([[0, w.V, 0, 1]], [[1, w.V, 3, 0]], [[0, 1, 2, 3], [1, w.V + 7, 1, 0]],
+                    [[0, 0xFFFFFFFF, 1, 1]]):
+            assert g.try_apply_updates(np.array(bad, dtype=np.uint32)) == pb.bingo.E_INVAL
+            assert g.export() == before
+        o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
+        b = w.batches[0][:100]
+        _same_stats(g.apply_updates(b), o.apply_updates(b))
+        _same(g, o, w.V)
+        g.close()
+
+
+def test_single_records_on_a_vertex_above_the_fast_path_handoff():
+    """Single-record updates touching a vertex with more than 8192 arcs (FAST_HANDOFF_L in
+    csrc/update.cu): the single-launch path hands the call to the bulk-synchronous pipeline;
+    inserts, deletes (duplicates, the newest and oldest instance) and misses stay exact."""
+    rng = np.random.default_rng(12)
+    V = 64
+    deg = rng.integers(0, 30, size=V)
+    deg[5] = 9000
+    deg[9] = 8190
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, V, size=A).astype(np.uint32)
+    bias = rng.integers(1, 5000, size=A).astype(np.uint32)
+    g, o = _pair(ro, dst, bias)
+    hub = [int(x) for x in dst[int(ro[5]):int(ro[6])]]
+    recs = []
+    for i in range(60):
+        r = rng.random()
+        if r < 0.35:
+            recs.append((0, 5, int(rng.integers(0, V)), int(rng.integers(1, 1 << 20))))
+        elif r < 0.75:
+            recs.append((1, 5, hub[int(rng.integers(0, len(hub)))], 0))
+        elif r < 0.85:
+            recs.append((1, 5, int(rng.integers(0, V)), 0))
+        elif r < 0.95:
+            recs.append((0, 9, int(rng.integers(0, V)), int(rng.integers(1, 300))))
+        else:
+            recs.append((1, 9, int(rng.integers(0, V)), 0))
+    for r in recs:
+        one = np.array([r], dtype=np.uint32)
+        _same_stats(g.apply_updates(one), o.apply_updates(one))
+    _same(g, o, V)
+    out = g.walk(length=30, seed=3, num_walkers=2000)
+    ref = o.walk(length=30, seed=3, num_walkers=2000)
+    assert np.array_equal(u32(out["paths"]), ref["paths"])

@@ -512,3 +512,67 @@ def test_lazy_oracle_equals_eager():
     d = a.digests()
     for u in range(0, w.V, 37):
         assert b.vertex_digest(u) == int(d[u])
+
+
+def test_alias_exact_tables_worked_by_hand(golden):
+    """R-4's canonical order pinned on exact tables (worked by hand from
+    the rule): a lowest->highest index slip made on both sides would change thr/alias here
+    although every distribution identity still holds."""
+    cases = {c["stage"]: c for c in golden["alias_worked"]["cases"]}
+    for c in cases.values():
+        thr, al = oracle.alias_build(c["W"])
+        assert [int(x) for x in thr] == c["thr"] and [int(x) for x in al] == c["alias"], c["stage"]
+
+    def tables(g, V):
+        v = oracle.parse_dump(g.dump(), V)[2]
+        return v, [grp["thr"] for grp in v["groups"]], [grp["alias"] for grp in v["groups"]]
+
+    g, V = running_example_graph(golden, flags=oracle.FLAG_BS_MODE)
+    v, thr, al = tables(g, V)
+    assert v["T"] == cases["running_example"]["T"]
+    assert thr == cases["running_example"]["thr"] and al == cases["running_example"]["alias"]
+    e = golden["insertion"]["edge"]
+    g.apply_updates([[0, e[0], e[1], e[2]]])
+    v, thr, al = tables(g, V)
+    assert v["T"] == cases["after_insertion"]["T"]
+    assert thr == cases["after_insertion"]["thr"] and al == cases["after_insertion"]["alias"]
+    dl = golden["deletion"]["edge"]
+    g.apply_updates([[1, dl[0], dl[1], 0]])
+    v, thr, al = tables(g, V)
+    c = cases["after_deletion"]
+    assert v["T"] == c["T"] and thr == c["thr"] and al == c["alias"]
+    assert {str(grp["k"]): grp["mem"] for grp in v["groups"]} == c["groups_by_index"]
+    # the same state built adaptively (alpha = 40, beta = 10, P:453)
+    ga, _ = running_example_graph(golden)
+    ga.apply_updates([[0, e[0], e[1], e[2]]])
+    ga.apply_updates([[1, dl[0], dl[1], 0]])
+    va = oracle.parse_dump(ga.dump(), V)[2]
+    assert [oracle.KIND_NAMES[grp["kind"]] for grp in va["groups"]] == c["kinds_adaptive"]
+    assert [grp["thr"] for grp in va["groups"]] == c["thr"] and [grp["alias"] for grp in va["groups"]] == c["alias"]
+
+
+def test_node2vec_outer_attempts_never_repeat_counters():
+    """R-1 (draw_oi): node2vec outer attempts >= 65536 carry their high bits into the tag
+    word, so attempt 65536 + x does not replay attempt x (the old 16-bit field cycled and a
+    walker that kept rejecting would loop forever).  Attempts < 65536 are unchanged: their
+    draw is the plain counter (w, t, (outer << 16) + inner, tag)."""
+    rng = np.random.default_rng(5)
+    ro, dst, bias = synth.random_small_graph(rng, 8, 40, 1000)
+    o = oracle.OracleGraph(ro, dst, bias)
+    u = int(np.argmax(np.diff(ro.astype(np.int64))))
+    same = sum(o.sample(u, 99, w, 3, x) == o.sample(u, 99, w, 3, x + 65536) for w in range(200) for x in (0, 7))
+    assert same < 200, "attempt 65536 + x must not replay attempt x"
+    # attempt < 65536: the bucket draw is Philox(w, t, outer << 16, 0) -- the first step of Eq.5
+    r = oracle.philox([3, 1, 5 << 16, 0], [99, 0])
+    v = oracle.parse_dump(o.dump(), 8)[u]
+    b = (int(r[0]) * len(v["groups"])) >> 32
+    coin = (((int(r[1]) << 32) | int(r[2])) * v["T"]) >> 64
+    g = v["groups"][b] if coin < v["groups"][b]["thr"] else v["groups"][v["groups"][b]["alias"]]
+    s = o.sample(u, 99, 3, 1, 5)
+    assert any(v["adj"][i][0] == s and (v["adj"][i][1] >> g["k"]) & 1 for i in range(v["d"])), \
+        "the sampled arc must belong to the group the (outer << 16) counter selects"
+
+
+def test_node2vec_unacceptable_ratio_rejected():
+    with pytest.raises(ValueError):
+        oracle.n2v_thresholds(1e-30, 1.0)
