@@ -1,21 +1,27 @@
 #!/usr/bin/env python
-"""bench.py -- Bingo hot path on B200: batched updates + biased DeepWalk, the paper's
-protocol (S6.1: rounds of (BATCHSIZE updates -> application)).
+"""bench.py -- Bingo hot path on B200, the paper's protocol (S6.1: rounds of
+(BATCHSIZE updates -> application)).
 
-A step = one round on BASELINE.json configs[1] (LiveJournal-shaped R-MAT, 4.7M V /
-69M arcs, degree biases): apply one update batch (50K undirected edge events = 100K
-arc records, Mixed insert/delete) then one biased DeepWalk of one walker
-per vertex x 80 steps, paths written to HBM.
+Headline (BASELINE.json configs[3], the config its "1/2/4/8 B200" metric is quoted on):
+Twitter-shaped R-MAT (46.2M V / 1.47B arcs, degree biases), a step = one round =
+  broadcast of rank 0's 100K-arc-record update batch (Mixed)
+  -> bingo_apply_updates on every replica
+  -> personalized PageRank walks (stop w.p. 1/80 after each step) of one walker per
+     vertex, the walker ids split evenly over the ranks (strong scaling: fixed total work)
+  -> the visit counts combined with ONE all-reduce (ReplicatedBingo.visit_counts).
+Secondary (configs[1], same line, key "secondary"): LiveJournal-shaped R-MAT, one update
+batch + biased DeepWalk of one walker per vertex x 80 steps, paths written to HBM.
 
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
 
-Multi-GPU (torchrun): every rank holds a replica, rank 0's update batch is broadcast
-(NCCL) inside the step, each rank walks its own walker-id range (weak scaling, one
-walker per vertex per rank); time = max over ranks of the device-timed region.
+The graph is generated in HBM (synth.DeviceWorkload, seeded), with a held-out set of 10
+batches that does not depend on --steps, so both arms run the same graph and the
+same batches.  Inputs (graph pools, 1.5-3 GB of outputs per step) exceed the 126 MB L2.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -30,6 +36,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 HBM_FALLBACK_GBS = 6650.0   # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+HOLD_ROUNDS = 10            # the held-out edges of 10 rounds of updates
+CFG_INDEX = {"c1": 0, "c2": 1, "c3": 2, "c4": 3, "c5": 4}
+METRIC = "walk steps/s (round = update batch + walk of one walker per vertex [+ PPR count all-reduce])"
 
 
 def parse():
@@ -38,29 +47,32 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c4", help="headline config (BASELINE configs[3] = c4)")
+    ap.add_argument("--secondary", default="c2", help="second workload in the same line ('' = none)")
     ap.add_argument("--length", type=int, default=80)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-walkers", type=int, default=1 << 21,
-                    help="oracle walker sample (cpu_baseline; --impl reference uses a quarter per step)")
+    ap.add_argument("--no-ceiling", action="store_true", help="skip the trace/replay gather ceiling")
+    ap.add_argument("--no-meter", action="store_true", help="skip the in-run CUPTI DRAM counters")
+    ap.add_argument("--trace-records", type=float, default=1.2e9, help="max traced steps for the ceiling")
+    ap.add_argument("--cpu-walkers", type=int, default=1 << 15, help="oracle walker sample per step")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (gloo: test the multi-rank path without NVLink)")
     ap.add_argument("--share-device", action="store_true",
                     help="test only: every rank on cuda:0 (exercise the N > 1 code path on a 1-GPU box)")
-    ap.add_argument("--e2e-layout", default="step", choices=["walker", "step"],
-                    help="path layout of the e2e pass (walker-major: one contiguous D2H per chunk)")
-    ap.add_argument("--layout", default="step", choices=["walker", "step"],
-                    help="path layout written by the walk (walker-major: one contiguous walk per walker)")
     return ap.parse_args()
+
+
+def app_of(config):
+    import synth
+    return synth.CONFIGS[config]["app"]
 
 
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         with open(p) as f:
-            d = json.load(f)
-        return d, "measured"
+            return json.load(f), "measured"
     return {"hbm_gbs": HBM_FALLBACK_GBS}, "fallback"
 
 
@@ -116,9 +128,8 @@ class ClockSampler:
 
 
 def bind_to_gpu_numa(local: int):
-    """Run this process on the CPUs local to the GPU, so pinned host buffers (first touch) sit on
-    the GPU's NUMA node: a remote node cost the e2e pass ~40% of its PCIe bandwidth (7.5 vs 12.4
-    G steps/s between runs).  Best effort: silently skipped where sysfs does not say."""
+    """Run on the CPUs local to the GPU, so pinned host buffers (first touch) sit on the GPU's
+    NUMA node.  Best effort: silently skipped where sysfs does not say."""
     try:
         import torch
         pr = torch.cuda.get_device_properties(local)
@@ -141,148 +152,160 @@ def bind_to_gpu_numa(local: int):
     return None
 
 
-def dist_setup(args):
+def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if ws > 1:
-        import torch.distributed as dist
-        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        return ws, rank, local, dist
-    return 1, 0, 0, None
+    return ws, rank, local
 
 
-def workload(args, rounds):
+def config_block(config, V, arcs, nrec, ws, extra=None):
     import synth
-    return synth.make_workload(args.config, rounds=rounds)
-
-
-def config_block(args, w, extra=None):
-    import synth
-    cfg = synth.CONFIGS[args.config]
-    c = {"workload": f"BASELINE configs[1]: {cfg['desc']}", "config": args.config, "V": int(w.V),
-         "arcs": int(w.num_arcs), "walk": f"biased DeepWalk, {w.V} walkers (1/vertex) x {args.length} steps",
-         "update_batch_arc_records": int(2 * w.batch), "update_batch_edges": int(w.batch),
-         "bias": "w(u,v)=max(1,deg(v)) (P:664)", "alpha_beta": [40, 10],
-         "l2": "inputs larger than L2: graph pools + 1.5 GB paths per step (> 126 MB L2), no flush needed"}
+    cfg = synth.CONFIGS[config]
+    app = cfg["app"]
+    walk = {"ppr": "personalized PageRank, stop 1/80 after each step (P:536), visit counts, no paths",
+            "deepwalk": "biased DeepWalk x 80 steps, step-major paths in HBM",
+            "node2vec": "node2vec p=2 q=0.5 x 80 steps"}[app]
+    c = {"workload": f"BASELINE configs[{CFG_INDEX[config]}]: {cfg['desc']}", "config": config, "V": int(V),
+         "arcs": int(arcs), "walk": f"{walk}; one walker per vertex ({V}), walker ids split over {ws} rank(s)",
+         "update_batch_arc_records": int(nrec), "update_batch_edges": int(nrec // 2),
+         "held_out_rounds": HOLD_ROUNDS, "bias": "w(u,v)=max(1,deg(v)) (P:664)", "alpha_beta": [40, 10],
+         "generator": "synth.DeviceWorkload (R-MAT 0.57/0.19/0.19/0.05, seeds 1/2), generated in HBM",
+         "l2": "inputs larger than L2 (graph pools of 3-75 GB, outputs of 0.4-1.5 GB per step): no flush needed"}
     if extra:
         c.update(extra)
     return c
 
 
-def run_reference(args):
-    """The oracle as it stands, on host cores, on the same workload: a bounded sample per step
-    (one full update batch + a walker sample), scaled to the full step."""
-    ws, rank, _, dist = dist_setup(args)
-    if rank != 0:
-        return
-    import oracle
-    w = workload(args, args.warmup + args.steps)
-    o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
-    Ws = min(w.V, args.cpu_walkers // 4)
-    ncores = os.cpu_count()
-    times, steps_full = [], []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        o.apply_updates(w.batches[i])
-        t1 = time.perf_counter()
-        r = o.walk(length=args.length, seed=1000 + i, first_walker=(i * 7919) % w.V, num_walkers=Ws, paths=True)
-        t2 = time.perf_counter()
-        sample_steps = int(r["lengths"].astype(np.int64).sum())
-        full_steps = sample_steps * (w.V / Ws)
-        t_step = (t1 - t0) + (t2 - t1) * (w.V / Ws)
-        if i >= args.warmup:
-            times.append(t_step)
-            steps_full.append(full_steps)
-    T = sum(times)
-    val = sum(steps_full) / T
-    sample = (f"per step: 1 full update batch ({2 * w.batch} arc records, single-threaded) + DeepWalk of {Ws} "
-              f"walkers x {args.length} steps (OpenMP, all cores), walk time scaled x{w.V / Ws:.1f} to {w.V} walkers")
-    print(json.dumps({"impl": "reference", "metric": "walk steps/s (round = update batch + DeepWalk)",
-                      "value": val, "unit": "steps/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-                      "ms_per_step": 1e3 * T / len(times), "higher_is_better": True, "scaling": "weak",
-                      "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-                      "config": config_block(args, w),
-                      "cpu_baseline": {"value": val, "unit": "steps/s", "cores": ncores, "kind": "oracle",
-                                       "sample": sample},
-                      "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
-          flush=True)
+# ---------------------------------------------------------------- in-run hardware counters
+class Meter:
+    """CUPTI range profiler around one launch (tools/dram_meter.cpp): DRAM bytes read + written
+    and the L2 sector hit rate of the region, measured in this process (None if unavailable,
+    e.g. under ncu)."""
+    METRICS = ("dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct")
+
+    def __init__(self):
+        from paper_2504_10233_b200 import _build
+        self.L = None
+        if os.path.exists(_build.METER_LIB):
+            try:
+                self.L = ctypes.CDLL(_build.METER_LIB)
+                self.L.dm_begin.argtypes = [ctypes.c_char_p]
+                self.L.dm_end.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+            except OSError:
+                self.L = None
+
+    def measure(self, fn, max_passes=4):
+        import torch
+        if self.L is None:
+            return None, "meter library unavailable"
+        torch.cuda.synchronize()
+        rc = self.L.dm_begin(",".join(self.METRICS).encode())
+        if rc != 0:
+            return None, f"CUPTI range profiler unavailable (step {rc})"
+        done = 0
+        for _ in range(max_passes):
+            if self.L.dm_pass_begin() != 0:
+                self.L.dm_abort()
+                return None, "pass begin failed"
+            fn()
+            torch.cuda.synchronize()
+            done = self.L.dm_pass_end()
+            if done != 0:
+                break
+        if done != 1:
+            self.L.dm_abort()
+            return None, "passes not completed"
+        vals = (ctypes.c_double * len(self.METRICS))()
+        if self.L.dm_end(vals, len(self.METRICS)) != 0:
+            return None, "evaluation failed"
+        return dict(zip(self.METRICS, list(vals))), "ok"
 
 
-def cpu_baseline(args, w, batch):
-    import oracle
-    t0 = time.perf_counter()
-    o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
-    t_build = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    o.apply_updates(batch)
-    t_upd = time.perf_counter() - t0
-    Ws = min(w.V, args.cpu_walkers)
-    t0 = time.perf_counter()
-    r = o.walk(length=args.length, seed=99, num_walkers=Ws, paths=True)
-    t_walk = time.perf_counter() - t0
-    steps = int(r["lengths"].astype(np.int64).sum())
-    scale = w.V / Ws
-    t_step = t_upd + t_walk * scale
-    return {"value": steps * scale / t_step, "unit": "steps/s", "cores": os.cpu_count(), "kind": "oracle",
-            "sample": (f"oracle built once (untimed, {t_build:.1f} s); 1 update batch of {len(batch)} arc records "
-                       f"({t_upd:.2f} s, single-threaded) + DeepWalk of {Ws} walkers x {args.length} steps "
-                       f"({t_walk:.2f} s, OpenMP); walk scaled x{scale:.1f} to the full step"),
-            "walk_steps_per_s": steps / t_walk, "update_arcs_per_s": len(batch) / t_upd}
-
-
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
+# ---------------------------------------------------------------- graph setup
+def make_graph(args, config, rounds, dev, ws, rank, dist):
+    """Rank 0 generates the workload in HBM; with NCCL the CSR and the batches are broadcast
+    to the other ranks over NVLink (every replica is built from the same arrays)."""
     import torch
-    ws, rank, local, dist = dist_setup(args)
-    if args.share_device:
-        local = 0
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    numa_cpus = bind_to_gpu_numa(local)
-    if dist is not None:
-        if args.backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group("gloo")
+    import synth
     import paper_2504_10233_b200 as pb
-    from paper_2504_10233_b200 import bingo
+    t0 = time.time()
+    share = dist is not None and args.backend == "nccl" and not args.share_device
+    if rank == 0 or not share:
+        w = synth.make_workload(config, rounds=rounds, hold_rounds=HOLD_ROUNDS, device=dev, resident=True)
+        ro, dst, bias, batches, V, A = w.row_offsets, w.dst, w.bias, w.batches, w.V, w.num_arcs
+    if share:
+        meta = torch.zeros(3, dtype=torch.int64, device=dev)
+        if rank == 0:
+            meta[0], meta[1], meta[2] = V, A, batches[0].shape[0]
+        dist.broadcast(meta, 0)
+        V, A, nrec = (int(x) for x in meta.tolist())
+        if rank != 0:
+            ro = torch.empty(V + 1, dtype=torch.int64, device=dev)
+            dst = torch.empty(A, dtype=torch.int32, device=dev)
+            bias = torch.empty(A, dtype=torch.int32, device=dev)
+        for t in (ro, dst, bias):
+            dist.broadcast(t, 0)
+        bt = (torch.from_numpy(np.stack(batches).view(np.int32)).to(dev) if rank == 0
+              else torch.empty((rounds, nrec, 4), dtype=torch.int32, device=dev))
+        dist.broadcast(bt, 0)
+        batches = [b for b in bt.cpu().numpy().view(np.uint32)]
+    t_gen = time.time() - t0
+    host_csr = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and config == args.config:
+        host_csr = (ro.cpu().numpy().view(np.uint64), dst.cpu().numpy().view(np.uint32),
+                    bias.cpu().numpy().view(np.uint32))
+    t0 = time.time()
+    g = pb.Graph(ro, dst, bias, device=dev)
+    torch.cuda.synchronize()
+    t_build = time.time() - t0
+    del ro, dst, bias
+    if rank == 0 or not share:
+        del w
+    torch.cuda.empty_cache()
+    return g, batches, V, A, host_csr, {"gen_s": round(t_gen, 2), "build_s": round(t_build, 2)}
 
+
+# ---------------------------------------------------------------- one workload
+def run_workload(args, config, dev, ws, rank, local, dist, primary):
+    import torch
+    import paper_2504_10233_b200 as pb
+    from paper_2504_10233_b200.distributed import ReplicatedBingo, shard_range
+    app = app_of(config)
     K, W = args.steps, args.warmup
-    e2e_steps = 0 if args.no_e2e else K
-    rounds = W + K + e2e_steps + 1
-    w = workload(args, rounds)
-    V, L = w.V, args.length
-    g = pb.Graph(w.row_offsets, w.dst, w.bias, device=dev)
-    batches = [torch.from_numpy(b.view(np.int32)) for b in w.batches]
+    e2e_steps = 0 if args.no_e2e or not primary else K
+    rounds = W + K + e2e_steps + (1 if primary else 2)
+    g, batches, V, A, host_csr, times = make_graph(args, config, rounds, dev, ws, rank, dist)
     nrec = batches[0].shape[0]
-    # inputs resident in HBM before the timed region (rank 0 holds the stream; others receive it)
-    dev_batches = [b.to(dev) for b in batches[:W + K]] if rank == 0 else [None] * (W + K)
-    first = rank * V            # this rank's first walker id (weak scaling: V walkers per rank)
-    wmajor = args.layout == "walker"
-    paths = torch.empty((V, L + 1) if wmajor else (L + 1, V), dtype=torch.int32, device=dev)
-    lens = [torch.empty(V, dtype=torch.int32, device=dev) for _ in range(K)]
-    scratch_len = torch.empty(V, dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream()
-
-    from paper_2504_10233_b200.distributed import ReplicatedBingo
+    dev_batches = [torch.from_numpy(b.view(np.int32)).to(dev) for b in batches[:W + K]] if rank == 0 \
+        else [None] * (W + K)
     rb = ReplicatedBingo(g, device=dev)
+    first, count = shard_range(V, rank, ws)
+    L = args.length
+    stream = torch.cuda.current_stream()
+    lens = [torch.empty(count, dtype=torch.int32, device=dev) for _ in range(K)]
+    scratch_len = torch.empty(count, dtype=torch.int32, device=dev)
+    if app == "ppr":
+        wkw = dict(app=pb.PPR, length=pb.NO_CAP, stop=(1, 80), paths=None)
+        paths = None
+    else:
+        paths = torch.empty((L + 1, count), dtype=torch.int32, device=dev)
+        wkw = dict(app=pb.DEEPWALK, length=L, paths=paths)
+    g.reset_visit_counts()
 
     def step(i, out_len, ev=None):
         if ev is not None:
             ev[0].record(stream)
-        # rank 0's batch is broadcast to every replica inside the step (NCCL over NVLink)
-        rb.apply_updates(dev_batches[i] if rank == 0 else None)
+        rb.apply_updates(dev_batches[i] if rank == 0 else None, n=nrec)   # broadcast + apply
         if ev is not None:
             ev[1].record(stream)
-        # walker ids [rank*V, (rank+1)*V): one walker per vertex per rank (weak scaling)
-        rb.walk(num_walkers=V * ws, app=pb.DEEPWALK, length=L, seed=1000 + i, paths=paths, lengths=out_len,
-                walker_major=wmajor)
+        rb.walk(num_walkers=V, seed=1000 + i, lengths=out_len, **wkw)      # this rank's walker share
         if ev is not None:
             ev[2].record(stream)
+        if app == "ppr":
+            rb.visit_counts(reset=True)                                     # the one all-reduce
+        if ev is not None:
+            ev[3].record(stream)
 
     for i in range(W):
         step(i, scratch_len)
@@ -291,7 +314,7 @@ def main():
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(K)]
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(K)]
     launches0 = g.info()["kernel_launches"]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -307,7 +330,9 @@ def main():
     t_ms = start.elapsed_time(end)
     upd_ms = [e[0].elapsed_time(e[1]) for e in evs]
     walk_ms = [e[1].elapsed_time(e[2]) for e in evs]
+    red_ms = [e[2].elapsed_time(e[3]) for e in evs]
     steps_local = sum(int(x.to(torch.int64).sum()) for x in lens)
+    t_local = t_ms
     if dist is not None:
         t = torch.tensor([t_ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -318,180 +343,364 @@ def main():
     else:
         steps_total = steps_local
     value = steps_total / (t_ms / 1e3)
-
-    # ---- roofline of the dominant kernel (the walk): algorithmic bytes from an exact
-    # per-record load count of one launch of the same configuration
-    prof = g.walk_profile(app=pb.DEEPWALK, length=L, seed=1000 + W, first_walker=first, num_walkers=V)
-    sectors = prof["hdr"] + prof["bkt"] + prof["mem"] + prof["arc"]
-    alg_bytes = 32 * sectors + 4 * V * (L + 1) + 4 * V          # dependent 32 B sectors + path + lengths
     walk_avg_s = statistics.mean(walk_ms) / 1e3
+
+    # ---- roofline of the dominant kernel (k_walk): algorithmic bytes of one launch of the
+    # same configuration from exact per-record load counts (bingo_walk_profile)
+    pkw = dict(app=wkw["app"], length=wkw["length"], stop=(1, 80), seed=1000 + W, first_walker=first,
+               num_walkers=count, paths=(app != "ppr"))
+    prof = g.walk_profile(**pkw)
+    gather_sectors = prof["hdr"] + prof["bkt"] + prof["mem"] + prof["arc"]
+    gather_bytes = 32 * gather_sectors
+    alg_bytes = gather_bytes + 4 * count                                   # + lengths
+    if app == "ppr":
+        alg_bytes += 64 * (prof["visit"] + prof["walkers"])                # counter RMW: 2 sectors per visit
+    else:
+        alg_bytes += 4 * count * (L + 1)                                   # path columns
     pk, pk_src = peaks()
     peak = float(pk["hbm_gbs"])
     achieved = alg_bytes / walk_avg_s / 1e9
-    traffic = None
-    tp = os.path.join(ROOT, "profiles", "walk_dram_traffic.json")
-    if os.path.exists(tp):
-        try:
-            with open(tp) as f:
-                traffic = json.load(f).get("bytes_per_launch")
-        except Exception:
-            traffic = None
-    gather = measure_gather(dev) if rank == 0 else None
+    g.reset_visit_counts()
 
-    # ---- e2e through the C-ABI with HOST buffers (pinned): H2D batch + D2H paths each step
-    e2e = None
+    # in-run DRAM counters of one walk launch (CUPTI), same configuration
+    traffic, meter_note, l2_hit = None, "skipped", None
+    if not args.no_meter:
+        mk = dict(pkw)
+        mk.pop("paths")
+        mk["paths"] = paths if app != "ppr" else None
+        mk["lengths"] = scratch_len
+
+        def one_walk():
+            g.walk(**mk)
+        vals, meter_note = Meter().measure(one_walk)
+        if vals:
+            traffic = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+            l2_hit = vals["lts__t_sector_hit_rate.pct"]
+        g.reset_visit_counts()
+
+    # gather ceiling for the walk's own footprint and skew: trace + dependency-free replay
+    ceiling = None
+    if not args.no_ceiling:
+        ceiling = gather_ceiling(args, g, app, pkw, prof, count, first, dev, stream)
+        g.reset_visit_counts()
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_source": f"{pk_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth)",
+            "kernel": f"k_walk<{app.upper()}> (bingo_walk)", "alg_bytes_per_launch": alg_bytes,
+            "alg_bytes_def": ("32 B x (vertex headers + alias buckets + members + dense arc attempts) "
+                              + ("+ 64 B x visit-counter RMWs " if app == "ppr" else "+ 4 B x path entries ")
+                              + "+ 4 B x lengths; exact counts from bingo_walk_profile of the same launch"),
+            "load_counts": {k: prof[k] for k in ("steps", "hdr", "bkt", "mem", "arc", "visit", "walkers")},
+            "traffic_source": f"CUPTI range profiler in this run (dram__bytes_read.sum + dram__bytes_write.sum): "
+                              f"{meter_note}",
+            "dram_gbs": (traffic / walk_avg_s / 1e9) if traffic else None,
+            "dram_frac_of_peak": (traffic / walk_avg_s / 1e9 / peak) if traffic else None,
+            "l2_sector_hit_pct": l2_hit}
+    if ceiling:
+        walk_gather_gbs = gather_bytes / walk_avg_s / 1e9
+        ceiling["walk_gather_gbs"] = walk_gather_gbs
+        ceiling["frac"] = walk_gather_gbs / ceiling["ceiling_gbs"]
+        ceiling["north_star_target"] = ">= 0.5 of the achievable random-gather bandwidth (BASELINE north_star)"
+        ceiling["north_star_met"] = ceiling["frac"] >= 0.5
+        roof["gather_ceiling"] = ceiling
+    out = {"value": value, "t_ms": t_ms, "t_local_ms": t_local, "K": K, "steps_total": steps_total,
+           "launches": int(launches), "clocks": clk, "roofline": roof, "V": V, "A": A, "nrec": nrec,
+           "update_ms": statistics.mean(upd_ms), "walk_ms": walk_avg_s * 1e3,
+           "allreduce_ms": statistics.mean(red_ms), "setup": times, "first": first, "count": count}
+
+    # ---- e2e through the public API with HOST buffers: batch H2D in, result D2H out
     if e2e_steps:
-        ewm = args.e2e_layout == "walker"
-        hp = torch.empty((V, L + 1) if ewm else (L + 1, V), dtype=torch.int32).pin_memory()
-        # one pinned lengths buffer per step: the step counts are summed after the timed region
-        hls = [torch.empty(V, dtype=torch.int32).pin_memory() for _ in range(e2e_steps)]
-        hb = [b.pin_memory() for b in batches[W + K:W + K + e2e_steps]]
-        # one untimed pass through the host buffers (first DMA into freshly pinned pages)
-        g.walk_host(app=pb.DEEPWALK, length=L, seed=4999, first_walker=first, num_walkers=V, paths=hp,
-                    lengths=hls[0], walker_major=ewm)
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
+        out["e2e"] = run_e2e(args, g, rb, batches[W + K:W + K + e2e_steps], app, V, count, first, L, dev, dist, rank,
+                             ws)
+    # ---- a11: streaming single-record updates (synchronous C-ABI calls, host batch)
+    if not primary and rank == 0:
+        out["streaming"] = streaming(g, batches, stream)
+    out["host_csr"] = host_csr
+    out["batches"] = batches
+    g.close()
+    del g, rb, dev_batches, paths, lens
+    torch.cuda.empty_cache()
+    return out
+
+
+def gather_ceiling(args, g, app, pkw, prof, count, first, dev, stream):
+    """Record the walk's own loads (bingo_walk_trace) for a prefix of this rank's walkers and
+    replay them with no dependency between loads (bingo_walk_replay): the bandwidth the memory
+    system delivers for exactly this footprint, skew and cache-policy mix when latency is
+    hidden -- the denominator of the north_star's 'achievable random-gather bandwidth'."""
+    import torch
+    lens = (prof["lengths"].to(torch.int64) if prof.get("lengths") is not None else None)
+    if lens is None:
+        return None
+    cum = torch.cumsum(lens, 0)
+    budget = int(min(args.trace_records, (torch.cuda.mem_get_info()[0] * 0.6) / 20))
+    Wt = int(torch.searchsorted(cum, torch.tensor([budget], device=cum.device), right=True)[0])
+    Wt = max(1, min(Wt, count))
+    n = int(cum[Wt - 1])
+    rec_off = torch.zeros(Wt + 1, dtype=torch.int64, device=dev)
+    rec_off[1:] = cum[:Wt]
+    trace = torch.empty(5 * n, dtype=torch.int32, device=dev)
+    kw = dict(app=pkw["app"], length=pkw["length"], stop=pkw["stop"], seed=pkw["seed"], first_walker=first,
+              num_walkers=Wt)
+    tp = g.walk_trace(rec_off, trace, **kw)
+    assert tp["steps"] == n, (tp["steps"], n)
+    ms = []
+    cnt = None
+    for _ in range(3):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        tot = 0
         e0.record(stream)
-        for k in range(e2e_steps):
-            g.apply_updates(hb[k].numpy())
-            g.walk_host(app=pb.DEEPWALK, length=L, seed=5000 + k, first_walker=first, num_walkers=V,
-                        paths=hp, lengths=hls[k], walker_major=ewm)
+        cnt = g.walk_replay(trace)
         e1.record(stream)
         torch.cuda.synchronize()
-        tot = sum(int(h.numpy().astype(np.int64).sum()) for h in hls)
-        e_ms = e0.elapsed_time(e1)
-        if dist is not None:
-            t = torch.tensor([e_ms], device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            e_ms = float(t)
-            s = torch.tensor([tot], device=dev, dtype=torch.int64)
+        ms.append(e0.elapsed_time(e1))
+    rep_ms = statistics.median(ms)
+    sectors = cnt["hdr"] + cnt["bkt"] + cnt["mem"] + cnt["arc"]
+    del trace, rec_off
+    torch.cuda.empty_cache()
+    return {"method": "bingo_walk_trace + bingo_walk_replay: the traced walks' own loads (header, bucket, "
+                      "member / first two dense attempts) re-issued with the walk's widths, L2 policies and "
+                      "64 B fetch hints but no dependency (16 loads in flight per thread, 148 x 8 x 256 "
+                      "threads); ceiling = 32 B x loads / replay time.  The trace itself is read too "
+                      "(16-20 B per step, sequential), so the ceiling is, if anything, low by that share",
+            "walkers_traced": Wt, "steps_traced": n, "replay_ms": rep_ms, "replay_loads": cnt,
+            "ceiling_gbs": 32 * sectors / (rep_ms / 1e3) / 1e9,
+            "visit_rmw_in_ceiling": False}
+
+
+def run_e2e(args, g, rb, host_batches, app, V, count, first, L, dev, dist, rank, ws):
+    import torch
+    import paper_2504_10233_b200 as pb
+    stream = torch.cuda.current_stream()
+    hb = [torch.from_numpy(b.view(np.int32)).pin_memory() for b in host_batches]
+    nrec = host_batches[0].shape[0]
+    if app == "ppr":
+        hc = torch.empty(V, dtype=torch.int64).pin_memory()
+        tot = torch.zeros(1, dtype=torch.int64, device=dev)
+    else:
+        hp = torch.empty((L + 1, count), dtype=torch.int32).pin_memory()
+        hls = [torch.empty(count, dtype=torch.int32).pin_memory() for _ in host_batches]
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k, b in enumerate(hb):
+        if ws == 1:
+            g.apply_updates(b.numpy().view(np.uint32))                       # HOST batch through the C-ABI
+        else:
+            rb.apply_updates(b.to(dev, non_blocking=True) if rank == 0 else None, n=nrec)
+        if app == "ppr":
+            rb.walk(num_walkers=V, app=pb.PPR, length=pb.NO_CAP, stop=(1, 80), seed=5000 + k, paths=None,
+                    lengths=None)
+            c = rb.visit_counts(reset=True)
+            tot += c.sum()
+            hc.copy_(c, non_blocking=True)                                   # the result, D2H
+        else:
+            g.walk_host(app=pb.DEEPWALK, length=L, seed=5000 + k, first_walker=first, num_walkers=count, paths=hp,
+                        lengths=hls[k])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    if app == "ppr":
+        steps = int(tot) - V * len(hb)            # sum(counts) = sum(lengths + 1) over all walkers
+        if dist is not None and ws > 1:
+            steps = steps                         # counts are already all-reduced: global steps
+    else:
+        steps = sum(int(h.numpy().astype(np.int64).sum()) for h in hls)
+    if dist is not None:
+        t = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t)
+        if app != "ppr":
+            s = torch.tensor([steps], device=dev, dtype=torch.int64)
             dist.all_reduce(s)
-            tot = int(s)
-        e2e = {"value": tot / (e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": int(nrec * 16),
-               "host_cpus": f"{len(numa_cpus)} CPUs local to the GPU" if numa_cpus else "unbound",
-               "d2h_bytes_per_step": int(4 * V * (L + 2)), "steps": e2e_steps,
-               "path_layout": "walker-major" if ewm else "step-major",
-               "note": "bingo_apply_updates(HOST batch) + bingo_walk(HOST_OUTPUT paths+lengths), pinned"}
+            steps = int(s)
+    d2h = 8 * V if app == "ppr" else 4 * count * (L + 2)
+    return {"value": steps / (e_ms / 1e3), "unit": "steps/s", "h2d_bytes_per_step": int(nrec * 16),
+            "d2h_bytes_per_step": int(d2h), "steps": len(hb),
+            "note": ("bingo_apply_updates(HOST batch) + bingo_walk(PPR) + all-reduced visit counts copied to "
+                     "pinned host memory each step" if app == "ppr" else
+                     "bingo_apply_updates(HOST batch) + bingo_walk(HOST_OUTPUT paths+lengths), pinned")}
 
-    # ---- a11: streaming single-record updates (synchronous C-ABI calls, host batch)
-    streaming = None
-    if rank == 0:
-        recs = w.batches[-1][:300]
-        lat_host, lat_dev = [], []
-        for r in recs:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            t0 = time.perf_counter()
-            e0.record(stream)
-            g.apply_updates(r[None, :])
-            e1.record(stream)
-            t1 = time.perf_counter()
-            torch.cuda.synchronize()
-            lat_host.append(1e6 * (t1 - t0))
-            lat_dev.append(1e3 * e0.elapsed_time(e1))
-        # the same C-ABI call without the Python wrapper (ctypes directly on pre-packed records):
-        # the library's own per-record latency, host call to completion
-        from paper_2504_10233_b200 import bingo as bb
-        packed = np.ascontiguousarray(w.batches[-2][:300], dtype=np.uint32)
-        lib, h, sp = bb._lib(), g.handle, stream.cuda_stream
-        base = packed.ctypes.data
-        lat_c = []
-        for i in range(len(packed)):
-            t0 = time.perf_counter()
-            rc = lib.bingo_apply_updates(h, base + 16 * i, 1, bb.UPD_HOST_BATCH, None, sp)
-            lat_c.append(1e6 * (time.perf_counter() - t0))
-            assert rc == 0, rc
-        streaming = {"records": len(recs), "call_us_p50": float(np.percentile(lat_host, 50)),
-                     "call_us_p99": float(np.percentile(lat_host, 99)),
-                     "device_us_p50": float(np.percentile(lat_dev, 50)),
-                     "device_us_p99": float(np.percentile(lat_dev, 99)),
-                     "abi_call_us_p50": float(np.percentile(lat_c, 50)),
-                     "abi_call_us_p99": float(np.percentile(lat_c, 99)),
-                     "abi_updates_per_s": float(len(lat_c) / (1e-6 * sum(lat_c))),
-                     "note": "one bingo_apply_updates call per arc record (epoch per record), c2 graph; call_us: "
-                             "through the Python binding; abi_call_us: the C-ABI call via ctypes, host to "
-                             "completion (the library synchronises)"}
 
+def streaming(g, batches, stream):
+    """One bingo_apply_updates call per arc record, through the Python binding and raw ctypes."""
+    import torch
+    from paper_2504_10233_b200 import bingo as bb
+    recs = batches[-1][:300]
+    lat_host, lat_dev = [], []
+    for r in recs:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        e0.record(stream)
+        g.apply_updates(r[None, :])
+        e1.record(stream)
+        t1 = time.perf_counter()
+        torch.cuda.synchronize()
+        lat_host.append(1e6 * (t1 - t0))
+        lat_dev.append(1e3 * e0.elapsed_time(e1))
+    packed = np.ascontiguousarray(batches[-2][:300], dtype=np.uint32)
+    lib, h, sp = bb._lib(), g.handle, stream.cuda_stream
+    base = packed.ctypes.data
+    lat_c = []
+    for i in range(len(packed)):
+        t0 = time.perf_counter()
+        rc = lib.bingo_apply_updates(h, base + 16 * i, 1, bb.UPD_HOST_BATCH, None, sp)
+        lat_c.append(1e6 * (time.perf_counter() - t0))
+        assert rc == 0, rc
+    return {"records": len(recs), "call_us_p50": float(np.percentile(lat_host, 50)),
+            "call_us_p99": float(np.percentile(lat_host, 99)),
+            "device_us_p50": float(np.percentile(lat_dev, 50)), "device_us_p99": float(np.percentile(lat_dev, 99)),
+            "abi_call_us_p50": float(np.percentile(lat_c, 50)), "abi_call_us_p99": float(np.percentile(lat_c, 99)),
+            "abi_updates_per_s": float(len(lat_c) / (1e-6 * sum(lat_c))),
+            "note": "one bingo_apply_updates call per arc record (epoch per record); call_us: through the Python "
+                    "binding; abi_call_us: the C-ABI call via ctypes, host to completion"}
+
+
+# ---------------------------------------------------------------- the oracle (CPU) legs
+def oracle_sample(host_csr, batches, config, steps_idx, walkers, V, seed_base, warm=True):
+    """The oracle as it stands (lazy build: vertices are materialised on first access), per
+    step: one full update batch (single-threaded) + a sample of the step's walkers (OpenMP,
+    all host cores); the walk is timed on a second pass over the same walkers so lazy
+    materialisation is not billed as walking."""
+    import oracle
+    app = app_of(config)
+    oapp = {"ppr": oracle.APP_PPR, "deepwalk": oracle.APP_DEEPWALK}[app]
+    length = oracle.NONE if app == "ppr" else 80
+    o = oracle.OracleGraph(*host_csr, lazy=True)
+    out = []
+    for i in steps_idx:
+        t0 = time.perf_counter()
+        o.apply_updates(batches[i])
+        t_upd = time.perf_counter() - t0
+        first = (i * 7919 * 4099) % max(1, V - walkers)
+        kw = dict(app=oapp, length=length, seed=seed_base + i, first_walker=first, num_walkers=walkers,
+                  paths=False, counts=(app == "ppr"), threads=os.cpu_count())
+        if warm:
+            o.walk(**kw)
+        t0 = time.perf_counter()
+        r = o.walk(**kw)
+        t_walk = time.perf_counter() - t0
+        out.append((t_upd, t_walk, int(r["lengths"].astype(np.int64).sum())))
+    return out
+
+
+def cpu_line_from(samples, V, walkers, nrec):
+    t_upd = sum(s[0] for s in samples)
+    t_walk = sum(s[1] for s in samples)
+    steps = sum(s[2] for s in samples)
+    scale = V / walkers
+    t_full = t_upd + t_walk * scale
+    return steps * scale / t_full, {"update_s_per_batch": t_upd / len(samples), "walk_s_per_sample": t_walk / len(samples),
+                                   "walk_steps_per_s": steps / t_walk, "update_arcs_per_s": nrec * len(samples) / t_upd,
+                                   "scale": scale}
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores, on the same workload as the
+    CUDA arm (same graph, same batches); each step = one full update batch + a walker sample
+    of the step, scaled to one walker per vertex.  Only rank 0 runs."""
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    import torch
+    import synth
+    config = args.config
+    dev = torch.device("cuda", local) if torch.cuda.is_available() else torch.device("cpu")
+    rounds = args.warmup + args.steps
+    t0 = time.time()
+    w = synth.make_workload(config, rounds=rounds, hold_rounds=HOLD_ROUNDS, device=dev,
+                            resident=dev.type == "cuda")
+    host = w.host_csr() if hasattr(w, "host_csr") else (w.row_offsets, w.dst, w.bias)
+    V, A, nrec = w.V, w.num_arcs, w.batches[0].shape[0]
+    batches = w.batches
+    del w
+    if dev.type == "cuda":
+        torch.cuda.empty_cache()
+    gen_s = time.time() - t0
+    walkers = min(V, max(1, args.cpu_walkers // 4))
+    samples = oracle_sample(host, batches, config, range(rounds), walkers, V, 1000, warm=True)
+    timed = samples[args.warmup:]
+    val, det = cpu_line_from(timed, V, walkers, nrec)
+    ms_step = 1e3 * (sum(s[0] for s in timed) + det["scale"] * sum(s[1] for s in timed)) / len(timed)
+    sample = (f"per step: 1 full update batch ({nrec} arc records, single-threaded, lazy oracle) + "
+              f"{app_of(config)} walk of {walkers} walkers (OpenMP, {os.cpu_count()} threads; second pass over the "
+              f"same walkers, the first materialises their vertices), walk time scaled x{det['scale']:.1f} to "
+              f"{V} walkers; generation {gen_s:.0f} s (torch on the GPU, not timed)")
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": val, "unit": "steps/s", "n_gpus": ws,
+                      "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+                      "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+                      "config": config_block(config, V, A, nrec, 1, {"parallelism": "oracle on host cores"}),
+                      "cpu_baseline": {"value": val, "unit": "steps/s", "cores": os.cpu_count(), "kind": "oracle",
+                                       "sample": sample, **det},
+                      "e2e": {"value": val, "unit": "steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    ws, rank, local = dist_env()
+    if args.share_device:
+        local = 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    numa_cpus = bind_to_gpu_numa(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    head = run_workload(args, args.config, dev, ws, rank, local, dist, primary=True)
+    sec = None
+    if args.secondary:
+        sec = run_workload(args, args.secondary, dev, ws, rank, local, dist, primary=False)
     cpu = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, w, w.batches[0])
-
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and head["host_csr"] is not None:
+        walkers = min(head["V"], args.cpu_walkers)
+        samples = oracle_sample(head["host_csr"], head["batches"], args.config, [0], walkers, head["V"], 99)
+        val, det = cpu_line_from(samples, head["V"], walkers, head["nrec"])
+        cpu = {"value": val, "unit": "steps/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": (f"lazy oracle on the same graph: 1 update batch of {head['nrec']} arc records "
+                          f"(single-threaded) + {app_of(args.config)} walk of {walkers} walkers (OpenMP; timed on a "
+                          f"second pass, the first materialises their vertices), walk scaled x{det['scale']:.0f} to "
+                          f"the full step"), **det}
     if rank == 0:
-        upd_avg = statistics.mean(upd_ms) / 1e3
+        K = args.steps
         line = {
-            "metric": "walk steps/s (round = update batch + DeepWalk)",
-            "value": value, "unit": "steps/s", "n_gpus": ws, "steps": K, "warmup": W,
-            "ms_per_step": t_ms / K, "higher_is_better": True, "scaling": "weak",
+            "metric": METRIC, "value": head["value"], "unit": "steps/s", "n_gpus": ws, "steps": K,
+            "warmup": args.warmup, "ms_per_step": head["t_ms"] / K, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": config_block(args, w, {"parallelism": f"replicated graph x{ws}, walkers sharded by id",
-                                             "path_layout": "walker-major" if wmajor else "step-major"}),
-            "walk_steps_per_s": steps_total / ws / K / walk_avg_s * ws,
-            "update_edges_per_s": nrec / upd_avg,
-            "update_ms": upd_avg * 1e3, "walk_ms": walk_avg_s * 1e3,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": f"{pk_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth)",
-                         "kernel": "k_walk<DEEPWALK> (bingo_walk)",
-                         "alg_bytes_per_launch": alg_bytes,
-                         "alg_bytes_def": "32 B x (vertex headers + alias buckets + members + dense arc attempts) "
-                                          "+ 4 B x path entries + 4 B x lengths, exact counts from bingo_walk_profile",
-                         "load_counts": {k: prof[k] for k in ("steps", "hdr", "bkt", "mem", "arc")},
-                         "gather_roofline": gather},
-            "l2_plan": {"l2_persist_bytes": g.info()["l2_persist_bytes"],
-                        "hot_bucket_degree": g.info()["hot_degree"] & 0xFFFFFFFF,
-                        "hot_member_degree": g.info()["hot_degree"] >> 32},
-            "streaming_update": streaming,
-            "clocks": clk, "gpu_launches": int(launches),
-            "e2e": e2e, "cpu_baseline": cpu,
+            "config": config_block(args.config, head["V"], head["A"], head["nrec"], ws,
+                                   {"parallelism": f"replicated graph x{ws}, walker ids split {ws} ways, batch "
+                                                   f"broadcast + visit-count all-reduce (NCCL)",
+                                    "setup": head["setup"]}),
+            "walk_steps_per_s": head["steps_total"] / K / (head["walk_ms"] / 1e3),
+            "update_edges_per_s": head["nrec"] / (head["update_ms"] / 1e3),
+            "update_ms": head["update_ms"], "walk_ms": head["walk_ms"], "allreduce_ms": head["allreduce_ms"],
+            "roofline": head["roofline"], "clocks": head["clocks"], "gpu_launches": head["launches"],
+            "e2e": head.get("e2e"), "cpu_baseline": cpu,
         }
-        if gather and gather.get("chase1_gbs"):
-            line["roofline"]["frac_of_gather_chase"] = achieved / gather["chase1_gbs"]
-            line["roofline"]["frac_of_gather_independent"] = achieved / gather["independent_gbs"]
+        if sec is not None:
+            line["secondary"] = {
+                "config": config_block(args.secondary, sec["V"], sec["A"], sec["nrec"], ws,
+                                       {"setup": sec["setup"]}),
+                "value": sec["value"], "unit": "steps/s", "ms_per_step": sec["t_ms"] / K,
+                "walk_steps_per_s": sec["steps_total"] / K / (sec["walk_ms"] / 1e3),
+                "update_edges_per_s": sec["nrec"] / (sec["update_ms"] / 1e3), "update_ms": sec["update_ms"],
+                "walk_ms": sec["walk_ms"], "roofline": sec["roofline"], "clocks": sec["clocks"],
+                "gpu_launches": sec["launches"], "streaming_update": sec.get("streaming")}
+        if numa_cpus:
+            line["host_cpus"] = f"{len(numa_cpus)} CPUs local to the GPU"
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
-
-
-def measure_gather(dev):
-    """Random 32 B-sector gather bandwidth over 8 GiB (>> L2): independent loads (8 in flight
-    per thread) and dependent pointer chases (1/2/4 chains per thread, the walker pattern)."""
-    import ctypes
-    import torch
-    from paper_2504_10233_b200 import _build
-    lib_path = _build.TOOLS_LIB
-    if not os.path.exists(lib_path):
-        return None
-    L = ctypes.CDLL(lib_path)
-    L.gather_fill.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_uint64, ctypes.c_void_p]
-    L.gather_run.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint32,
-                             ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p, ctypes.POINTER(ctypes.c_float),
-                             ctypes.POINTER(ctypes.c_double), ctypes.c_void_p]
-    nbytes = 8 << 30
-    try:
-        buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
-    except RuntimeError:
-        return None
-    scratch = torch.zeros(16, dtype=torch.int32, device=dev)
-    nslots = nbytes // 32
-    s = torch.cuda.current_stream().cuda_stream
-    L.gather_fill(buf.data_ptr(), nslots, 12345, s)
-    torch.cuda.synchronize()
-    out = {"buffer_gib": 8}
-    for mode, name, blocks, threads, iters in ((0, "independent", 148 * 8, 256, 64), (1, "chase1", 148 * 8, 256, 64),
-                                               (2, "chase2", 148 * 8, 256, 32), (3, "chase4", 148 * 8, 256, 16)):
-        best = 0.0
-        for rep in range(3):
-            ms = ctypes.c_float()
-            loads = ctypes.c_double()
-            L.gather_run(buf.data_ptr(), nslots, mode, blocks, threads, iters, 777 + rep, scratch.data_ptr(),
-                         ctypes.byref(ms), ctypes.byref(loads), s)
-            best = max(best, 32 * loads.value / (ms.value / 1e3) / 1e9)
-        out[name + "_gbs"] = best
-    del buf
-    torch.cuda.empty_cache()
-    return out
 
 
 if __name__ == "__main__":

@@ -12,6 +12,9 @@ INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libbingo.so")
 TOOLS_SRC = [os.path.join(ROOT, "tools", "gather_bench.cu"), os.path.join(ROOT, "tools", "unit_kernels.cu")]
 TOOLS_LIB = os.path.join(HERE, "libbingo_tools.so")
+# in-process hardware counters for bench.py's roofline (CUPTI range profiler; measurement only)
+METER_SRC = os.path.join(ROOT, "tools", "dram_meter.cpp")
+METER_LIB = os.path.join(HERE, "libbingo_meter.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -53,6 +56,14 @@ def build(force: bool = False, verbose: bool = False, jobs: int = 8) -> str:
         subprocess.check_call([NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
                                "-I", INCLUDE, "-I", CSRC, "-o", tmp, *TOOLS_SRC, "-lcudart"])
         os.replace(tmp, TOOLS_LIB)
+    if force or not os.path.exists(METER_LIB) or os.path.getmtime(METER_LIB) < os.path.getmtime(METER_SRC):
+        tmp = METER_LIB + f".{os.getpid()}.tmp"
+        cuda = os.path.dirname(os.path.dirname(NVCC))
+        subprocess.check_call([NVCC, "-O2", "-std=c++17", "-Wno-deprecated-gpu-targets", "-Xcompiler", "-fPIC", "-shared",
+                               "-I", os.path.join(cuda, "include"), "-o", tmp, METER_SRC,
+                               "-L", os.path.join(cuda, "lib64"), "-lcupti", "-lnvperf_host", "-lcuda",
+                               "-Xlinker", "-rpath=" + os.path.join(cuda, "lib64")])
+        os.replace(tmp, METER_LIB)
     return LIB
 
 

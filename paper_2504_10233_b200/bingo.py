@@ -33,7 +33,8 @@ NO_CAP = 0xFFFFFFFF
 # every symbol include/bingo.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ("bingo_build", "bingo_destroy", "bingo_apply_updates", "bingo_apply_updates_f64", "bingo_walk",
                "bingo_visit_counts",
-               "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str", "bingo_walk_profile")
+               "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str", "bingo_walk_profile",
+               "bingo_walk_trace", "bingo_walk_replay")
 
 
 class BingoError(RuntimeError):
@@ -109,6 +110,10 @@ def _lib():
         L.bingo_get_info.restype = ctypes.c_int
         L.bingo_walk_profile.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, P, P]
         L.bingo_walk_profile.restype = ctypes.c_int
+        L.bingo_walk_trace.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, u64, P, P]
+        L.bingo_walk_trace.restype = ctypes.c_int
+        L.bingo_walk_replay.argtypes = [P, P, u64, u32, P, P]
+        L.bingo_walk_replay.restype = ctypes.c_int
         L.bingo_status_str.argtypes = [ctypes.c_int]
         L.bingo_status_str.restype = ctypes.c_char_p
         _LIB = L
@@ -376,6 +381,36 @@ class Graph:
         out["paths"] = pa
         out["lengths"] = ln
         return out
+
+    def walk_trace(self, rec_off, trace, app: int = DEEPWALK, length: int = 80, seed: int = 0,
+                   first_walker: int = 0, num_walkers: Optional[int] = None, stop=(1, 80), stream=None) -> dict:
+        """bingo_walk_trace: the same walks, with every step's loads recorded into `trace`
+        (int32 CUDA tensor [5 * n_records], slot-major) at rec_off[i] + t (int64 CUDA tensor
+        [num_walkers + 1], exclusive prefix sum of the walkers' lengths).  Returns the load counters."""
+        torch = _torch()
+        W = num_walkers if num_walkers is not None else self.V
+        n = trace.numel() // 5
+        d = WalkDesc(app=app, length=length, p=1.0, q=1.0, stop_num=stop[0], stop_den=stop[1], seed=seed,
+                     first_walker_id=first_walker, flags=0)
+        c = np.zeros(8, dtype=np.uint64)
+        _order_on(stream, self.device, rec_off, trace)
+        with torch.cuda.device(self.device):
+            _check(_lib().bingo_walk_trace(self._h, ctypes.byref(d), None, W, rec_off.data_ptr(), trace.data_ptr(), n,
+                                           c.ctypes.data, _stream_ptr(stream)), "bingo_walk_trace")
+        names = ("steps", "hdr", "bkt", "mem", "arc", "probe", "visit", "walkers")
+        return {k: int(v) for k, v in zip(names, c)}
+
+    def walk_replay(self, trace, visits: bool = False, stream=None) -> dict:
+        """bingo_walk_replay: issue the traced loads with no dependency between them.
+        Returns the loads issued per pool."""
+        torch = _torch()
+        n = trace.numel() // 5
+        c = np.zeros(6, dtype=np.uint64)
+        _order_on(stream, self.device, trace)
+        with torch.cuda.device(self.device):
+            _check(_lib().bingo_walk_replay(self._h, trace.data_ptr(), n, 1 if visits else 0, c.ctypes.data,
+                                            _stream_ptr(stream)), "bingo_walk_replay")
+        return {"hdr": int(c[1]), "bkt": int(c[2]), "mem": int(c[3]), "arc": int(c[4]), "visit": int(c[5])}
 
     def visit_counts(self, reset: bool = False, stream=None):
         torch = _torch()

@@ -48,12 +48,16 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
 // idle at the tail).  DeepWalk lanes finish together, so a warp claims 32
 // consecutive ids and the step-major path stores stay coalesced.  Results depend
 // only on the walker id (R-1), never on which lane ran it.
-template <int APP, bool PROF, bool WMAJOR, bool FLT>   // FLT: float-bias graph (decimal groups, R-15)
+// MODE: 0 plain, 1 load counters (bingo_walk_profile), 2 counters + access trace
+// (bingo_walk_trace; DeepWalk / PPR, integer biases).
+template <int APP, int MODE, bool WMAJOR, bool FLT>   // FLT: float-bias graph (decimal groups, R-15)
 #ifndef BINGO_WALK_TPB
 #define BINGO_WALK_TPB 256
 #endif
-__global__ void __launch_bounds__(BINGO_WALK_TPB, PROF ? 4 : (APP == BINGO_NODE2VEC ? BINGO_N2V_MINB : BINGO_WALK_MINB))
+__global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2VEC ? BINGO_N2V_MINB : BINGO_WALK_MINB))
     k_walk(const WalkArgs a, unsigned long long *__restrict__ claim) {
+    constexpr bool PROF = MODE >= 1;
+    constexpr bool TRACE = MODE == 2;
     WalkProf prof;
     // L2 eviction priorities: the thin headers are re-read by every step of every
     // walker (keep), member/arc sectors are one-shot random reads (stream).
@@ -89,12 +93,13 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, PROF ? 4 : (APP == BINGO_NODE2
                         cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
                     if (FLT) dr = load_dec(a.dec + u);
                     if (PROF) prof.hdr++;
+                    if (TRACE) prof.rec[0] = trace_code(TP_THDR, true, a.thdr, a.thdr + u);
                 }
                 if (h.n == 0 && dr.dcnt == 0) {
                     fin = true;                               // dead end (d = 0): truncate (R-13)
                 } else {
                     const uint32_t next = FLT ? sample_dst_f<PROF>(a, h, dr, w, t, o, prof, pol)
-                                                : sample_dst<PROF>(a, h, w, t, o, prof, pol);
+                                                : sample_dst<PROF, TRACE>(a, h, w, t, o, prof, pol);
                     bool accept = true;
                     if (APP == BINGO_NODE2VEC && t >= 1) {
                         // KnightKing rejection: propose first-order, accept with f/f_max;
@@ -144,12 +149,23 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, PROF ? 4 : (APP == BINGO_NODE2
 #endif
 #endif
                             if (PROF) prof.visit++;
+                            if (TRACE && a.visit)
+                                prof.rec[4] = trace_code(TP_VISIT, true, a.visit, a.visit + visit_slot(u));
                             if (a.stop_always) {
                                 fin = true;
                             } else {
                                 const P4 r = philox10(w, t, 0u, 3u, a.k0, a.k1);
                                 fin = join64(r.x, r.y) < a.stop_thr;
                             }
+                        }
+                        if (TRACE) {
+                            const unsigned long long r = a.trace_off[i] + t;
+                            if (r < a.trace_off[i + 1]) {
+#pragma unroll
+                                for (int sl = 0; sl < TRACE_SLOTS; sl++) a.trace[sl * a.trace_n + r] = prof.rec[sl];
+                            }
+#pragma unroll
+                            for (int sl = 0; sl < TRACE_SLOTS; sl++) prof.rec[sl] = 0;
                         }
                         t++;
                         if (a.L != BINGO_NO_CAP && t >= a.L) fin = true;
@@ -234,8 +250,15 @@ static unsigned walk_grid(K kernel, uint32_t W) {
     return (unsigned)std::max<size_t>(1, std::min(need, cap));
 }
 
+struct TraceOut {
+    uint32_t *trace;
+    const unsigned long long *off;
+    unsigned long long n;
+};
+
 bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts, uint32_t W,
-                         uint32_t *paths, uint32_t *lengths, cudaStream_t s, unsigned long long *prof = nullptr) {
+                         uint32_t *paths, uint32_t *lengths, cudaStream_t s, unsigned long long *prof = nullptr,
+                         const TraceOut *tr = nullptr) {
     WalkArgs a;
     a.thdr = g->thdr;
     a.hdr = g->hdr;
@@ -268,6 +291,11 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
         if (desc->app == BINGO_NODE2VEC && !a.n2v_always[c] && a.n2v_thr[c] == 0) return BINGO_E_INVAL;
     stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
     a.prof = prof;
+    a.trace = tr ? tr->trace : nullptr;
+    a.trace_off = tr ? tr->off : nullptr;
+    a.trace_n = tr ? tr->n : 0;
+    if (tr && (desc->app == BINGO_NODE2VEC || g->float_mode || (desc->flags & BINGO_WALK_WALKER_MAJOR) || !prof))
+        return BINGO_E_INVAL;
     if (!g->walk_ctr) return BINGO_E_STATE;
     unsigned long long *claim = g->walk_ctr + (__atomic_fetch_add(&g->walk_slot, 1u, __ATOMIC_RELAXED) % BINGO_WALK_SLOTS);
     if (cudaMemsetAsync(claim, 0, sizeof(unsigned long long), s) != cudaSuccess) {
@@ -289,18 +317,26 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
             : (cfg.gridDim = dim3(walk_grid(k_walk<APP_, PROF_, false, FLT_>, W)),                \
                cudaLaunchKernelEx(&cfg, k_walk<APP_, PROF_, false, FLT_>, a, claim)))
 #define BINGO_K(APP_, PROF_) (a.dec ? BINGO_K3(APP_, PROF_, true) : BINGO_K3(APP_, PROF_, false))
-    if (prof) {
+    if (tr) {
+        if (desc->app == BINGO_DEEPWALK) {
+            cfg.gridDim = dim3(walk_grid(k_walk<BINGO_DEEPWALK, 2, false, false>, W));
+            le = cudaLaunchKernelEx(&cfg, k_walk<BINGO_DEEPWALK, 2, false, false>, a, claim);
+        } else {
+            cfg.gridDim = dim3(walk_grid(k_walk<BINGO_PPR, 2, false, false>, W));
+            le = cudaLaunchKernelEx(&cfg, k_walk<BINGO_PPR, 2, false, false>, a, claim);
+        }
+    } else if (prof) {
         switch (desc->app) {
-            case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, true); break;
-            case BINGO_NODE2VEC: le = BINGO_K(BINGO_NODE2VEC, true); break;
-            case BINGO_PPR: le = BINGO_K(BINGO_PPR, true); break;
+            case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, 1); break;
+            case BINGO_NODE2VEC: le = BINGO_K(BINGO_NODE2VEC, 1); break;
+            case BINGO_PPR: le = BINGO_K(BINGO_PPR, 1); break;
             default: return BINGO_E_INVAL;
         }
     } else {
         switch (desc->app) {
-            case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, false); break;
-            case BINGO_NODE2VEC: le = BINGO_K(BINGO_NODE2VEC, false); break;
-            case BINGO_PPR: le = BINGO_K(BINGO_PPR, false); break;
+            case BINGO_DEEPWALK: le = BINGO_K(BINGO_DEEPWALK, 0); break;
+            case BINGO_NODE2VEC: le = BINGO_K(BINGO_NODE2VEC, 0); break;
+            case BINGO_PPR: le = BINGO_K(BINGO_PPR, 0); break;
             default: return BINGO_E_INVAL;
         }
     }
@@ -428,6 +464,149 @@ extern "C" bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc
     bingo_dev_free(g, dprof);
     if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
     return st;
+}
+
+// ---------------------------------------------------------------- access trace + replay
+// (measurement only: the roofline's "achievable gather bandwidth" for the walk's OWN
+// footprint and skew).  bingo_walk_trace re-runs a walk (same walks as bingo_walk) and
+// records, per step, the codes of the loads the step made (trace_code in walk_common.cuh);
+// k_replay then issues exactly those loads -- same addresses, same widths, same L2 policies
+// and 64 B fetch hints -- with no dependency between them (4 records x up to 4 loads in
+// flight per thread over a full grid).  Its rate is what the memory system delivers for this
+// access mix when latency is fully hidden: the ceiling the dependent walk is measured against.
+static bool trace_pools_fit(const bingo_graph *g) {
+    const uint64_t lim = (1ull << TRACE_GRANULE_BITS) << 6;
+    return (uint64_t)g->V * sizeof(ThinHdr) <= lim && g->bkt_cap * sizeof(Bucket) <= lim && g->mem_cap * 4ull <= lim &&
+           g->arc_cap * 8ull <= lim && visit_words(g->V) * 8ull <= lim;
+}
+
+extern "C" bingo_status bingo_walk_trace(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts_or_null,
+                                         uint32_t num_walkers, const uint64_t *rec_off, uint32_t *trace,
+                                         uint64_t n_records, uint64_t *counters_host, void *stream) {
+    if (!g || !desc || !counters_host || !rec_off || !trace) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    if (!(desc->app == BINGO_DEEPWALK || desc->app == BINGO_PPR) || desc->flags || g->float_mode) return BINGO_E_INVAL;
+    if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
+    if (desc->length == BINGO_NO_CAP && desc->app != BINGO_PPR) return BINGO_E_INVAL;
+    if (g->V == 0 || !trace_pools_fit(g)) return BINGO_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *dprof = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * BINGO_PROF_N);
+    if (!dprof) return BINGO_E_NOMEM;
+    cudaError_t e = cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * BINGO_PROF_N, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(trace, 0, sizeof(uint32_t) * TRACE_SLOTS * n_records, s);
+    const TraceOut tr{trace, reinterpret_cast<const unsigned long long *>(rec_off), (unsigned long long)n_records};
+    bingo_status st = BINGO_OK;
+    if (e == cudaSuccess) st = launch_walk(g, desc, starts_or_null, num_walkers, nullptr, nullptr, s, dprof, &tr);
+    if (st == BINGO_OK && e == cudaSuccess)
+        e = cudaMemcpyAsync(counters_host, dprof, sizeof(unsigned long long) * BINGO_PROF_N, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    bingo_dev_free(g, dprof);
+    if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
+    return st;
+}
+
+struct ReplayArgs {
+    const uint32_t *trace;
+    unsigned long long n;
+    const char *base[6];
+    unsigned long long *visit;
+    unsigned long long *counts;   // [6] loads issued per pool
+    uint32_t *sink;
+    uint32_t visits;              // 1: replay the PPR visit RMWs too
+};
+
+#define REPLAY_UNROLL 4
+__global__ void __launch_bounds__(256) k_replay(const ReplayArgs a) {
+    uint64_t pol_keep, pol_stream;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    uint32_t cnt[6] = {0, 0, 0, 0, 0, 0};
+    for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r0 < a.n;
+         r0 += REPLAY_UNROLL * stride) {
+        uint32_t c[REPLAY_UNROLL][TRACE_SLOTS];
+#pragma unroll
+        for (int u = 0; u < REPLAY_UNROLL; u++) {
+            const unsigned long long r = r0 + u * stride;
+#pragma unroll
+            for (int sl = 0; sl < TRACE_SLOTS; sl++) c[u][sl] = r < a.n ? __ldcs(a.trace + sl * a.n + r) : 0u;
+        }
+        uint32_t v[REPLAY_UNROLL][TRACE_SLOTS];
+#pragma unroll
+        for (int u = 0; u < REPLAY_UNROLL; u++) {
+#pragma unroll
+            for (int sl = 0; sl < TRACE_SLOTS; sl++) {
+                const uint32_t code = c[u][sl];
+                const uint32_t pool = code >> 29;
+                const uint64_t pol = (code >> 28) & 1u ? pol_keep : pol_stream;
+                const char *p = a.base[pool < 6 ? pool : 0] + ((uint64_t)(code & ((1u << TRACE_GRANULE_BITS) - 1u)) << 6);
+                v[u][sl] = 0;
+                if (pool == TP_BKT) {
+                    const Bucket B = ldg_bucket(reinterpret_cast<const Bucket *>(p), pol);
+                    v[u][sl] = B.px ^ B.ay;
+                    cnt[pool]++;
+                } else if (pool == TP_THDR || pool == TP_ARC) {
+                    v[u][sl] = ldg8(reinterpret_cast<const uint2 *>(p), pol).x;
+                    cnt[pool]++;
+                } else if (pool == TP_MDST) {
+                    v[u][sl] = ldg4(reinterpret_cast<const uint32_t *>(p), pol);
+                    cnt[pool]++;
+                } else if (pool == TP_VISIT && a.visits) {
+                    atomicAdd(reinterpret_cast<unsigned long long *>(const_cast<char *>(p)), 1ull);
+                    cnt[pool]++;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < REPLAY_UNROLL; u++)
+#pragma unroll
+            for (int sl = 0; sl < TRACE_SLOTS; sl++) acc ^= v[u][sl];
+    }
+#pragma unroll
+    for (int k = 1; k < 6; k++) {
+        const unsigned long long x = warp_sum((unsigned long long)cnt[k]);
+        if ((threadIdx.x & 31u) == 0 && x) atomicAdd(&a.counts[k], x);
+    }
+    if (acc == 0x9E3779B9u) a.sink[0] = acc;   // keeps the loads alive
+}
+
+extern "C" bingo_status bingo_walk_replay(bingo_graph *g, const uint32_t *trace, uint64_t n_records, uint32_t flags,
+                                          uint64_t *counts_host, void *stream) {
+    if (!g || !trace || !counts_host) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned long long *dc = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * 8);
+    if (!dc) return BINGO_E_NOMEM;
+    ReplayArgs a;
+    a.trace = trace;
+    a.n = n_records;
+    a.base[0] = reinterpret_cast<const char *>(g->thdr);
+    a.base[TP_THDR] = reinterpret_cast<const char *>(g->thdr);
+    a.base[TP_BKT] = reinterpret_cast<const char *>(g->bkt);
+    a.base[TP_MDST] = reinterpret_cast<const char *>(g->mdst);
+    a.base[TP_ARC] = reinterpret_cast<const char *>(g->arc);
+    a.base[TP_VISIT] = reinterpret_cast<const char *>(g->visit);
+    a.visit = g->visit;
+    a.counts = dc;
+    a.sink = reinterpret_cast<uint32_t *>(dc + 7);
+    a.visits = flags & 1u;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaMemsetAsync(dc, 0, sizeof(unsigned long long) * 8, s);
+    if (e == cudaSuccess) {
+        k_replay<<<(unsigned)sms * 8, 256, 0, s>>>(a);
+        bingo_count_launch();
+        e = cudaGetLastError();
+    }
+    uint64_t h[8] = {0};
+    if (e == cudaSuccess) e = cudaMemcpyAsync(h, dc, sizeof(h), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    bingo_dev_free(g, dc);
+    if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
+    for (int k = 0; k < 6; k++) counts_host[k] = h[k];
+    return BINGO_OK;
 }
 
 // counts in external vertex order: out[u] = visit[inv[u]]

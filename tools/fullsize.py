@@ -39,13 +39,15 @@ def main():
     ap.add_argument("--vertices", type=int, default=3000, help="random vertices whose digests are compared")
     ap.add_argument("--walkers", type=int, default=0, help="walkers in the launch (default: one per vertex)")
     ap.add_argument("--ppr-cap", type=int, default=400)
+    ap.add_argument("--count-walkers", type=int, default=1 << 20,
+                    help="PPR: walker-id range whose visit counts are compared on EVERY vertex")
     ap.add_argument("--slack", type=float, default=0.25)
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     cfg = synth.CONFIGS[a.config]
     app = cfg["app"]
     t0 = time.time()
-    w = synth.make_workload(a.config, rounds=a.rounds, device="cuda")
+    w = synth.make_workload(a.config, rounds=a.rounds, hold_rounds=10, device="cuda", resident=True)
     torch.cuda.empty_cache()
     t_gen = time.time() - t0
     rec = {"config": a.config, "V": int(w.V), "arcs": int(w.num_arcs), "app": app, "gen_s": round(t_gen, 1)}
@@ -54,7 +56,7 @@ def main():
                  member_slack=a.slack)
     torch.cuda.synchronize()
     rec["gpu_build_s"] = round(time.time() - t0, 2)
-    o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias, lazy=True)
+    o = oracle.OracleGraph(*w.host_csr(), lazy=True)
     # ---- updates, timed on the device, replayed by the oracle
     upd_ms = []
     touched = set()
@@ -126,6 +128,30 @@ def main():
         assert np.array_equal(lens[s0:s0 + a.range_len], ref["lengths"])
     rec["walkers_compared"] = int(a.ranges * a.range_len)
     rec["oracle_walk_s"] = round(time.time() - t0, 2)
+    if app == "ppr":
+        # the visit counts of a contiguous walker-id range, compared on every vertex, and
+        # capped PPR paths (cap --ppr-cap) on sampled ranges
+        g.reset_visit_counts()
+        Wc = min(a.count_walkers, W)
+        c0 = int(rng.integers(0, max(1, W - Wc)))
+        g.walk(app=pb.PPR, length=pb.NO_CAP, stop=(1, 80), seed=5151, first_walker=c0, num_walkers=Wc, paths=None)
+        got = g.visit_counts_host(reset=True)
+        t0 = time.time()
+        ref = o.walk(app=oracle.APP_PPR, length=oracle.NONE, stop=(1, 80), seed=5151, first_walker=c0,
+                     num_walkers=Wc, paths=False, counts=True, threads=os.cpu_count())
+        rec["oracle_count_walk_s"] = round(time.time() - t0, 2)
+        bad = np.nonzero(got != ref["counts"])[0]
+        assert bad.size == 0, f"{bad.size} visit-count mismatches, first at {bad[:8].tolist()}"
+        rec["count_vector"] = {"walkers": Wc, "first_walker": c0, "vertices_compared": int(w.V),
+                               "nonzero": int(np.count_nonzero(ref["counts"])), "sum": int(ref["counts"].sum())}
+        for s0 in rng.integers(0, max(1, W - a.range_len), size=a.ranges).tolist():
+            outc = g.walk(app=pb.PPR, length=a.ppr_cap, stop=(1, 80), seed=5152, first_walker=s0,
+                          num_walkers=a.range_len)
+            refc = o.walk(app=oracle.APP_PPR, length=a.ppr_cap, stop=(1, 80), seed=5152, first_walker=s0,
+                          num_walkers=a.range_len, threads=os.cpu_count())
+            assert np.array_equal(outc["paths"].cpu().numpy().view(np.uint32), refc["paths"]), s0
+        g.reset_visit_counts()
+        rec["capped_paths_compared"] = int(a.ranges * a.range_len)
     rec["parity"] = "bit-exact"
     print(json.dumps(rec), flush=True)
     if a.out:
