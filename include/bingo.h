@@ -290,23 +290,23 @@ bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc *desc, con
  * DESIGN.md 6.1): the "achievable random-gather bandwidth" for the walk's own footprint and
  * skew.  bingo_walk_trace runs the same walks as bingo_walk (DeepWalk or PPR, integer
  * biases, step-major, no paths; counters_host as bingo_walk_profile) and records for every
- * step t < lengths[i] of walker i the loads it made, as u32 codes (pool 3 bits | L2 keep
- * policy 1 bit | 64 B granule in the pool 28 bits; 0 = none) in 5 slots (header, bucket,
- * member or dense attempt 0, dense attempt 1, PPR visit counter), slot-major:
- * trace[s * n_records + rec_off[i] + t].  rec_off: DEVICE u64 [num_walkers + 1], the
- * exclusive prefix sum of the walkers' lengths (from an earlier launch with the same
- * desc); trace: DEVICE u32 [5 * n_records].  EINVAL for node2vec, float graphs, flags,
- * or pools beyond 16 GB.  Synchronises `stream`.
+ * step t < lengths[i] of walker i one 16 B record of the loads it made at
+ * trace[rec_off[i] + t]: {vertex whose header was read, bucket index | keep << 31, member
+ * or dense attempt 0, dense attempt 1} (intra-group codes: 0xFFFFFFFF none, else
+ * arc << 31 | keep << 30 | 16 B member granule or 32 B arc sector).
+ * rec_off: DEVICE u64 [num_walkers + 1], the exclusive prefix sum of the walkers' lengths (from an earlier launch with the same desc);
+ * trace: DEVICE, 16 B x n_records.  EINVAL for node2vec, float graphs, flags, arc or
+ * member pools of 2^32 entries or bucket pools of 2^31.  Synchronises `stream`.
  * bingo_walk_replay issues exactly the recorded loads (same addresses, widths, cache
- * policies and fetch hints) with no dependency between them; flags bit 0 also replays the
- * visit-counter increments (they then change the graph's visit counts).  counts_host[6]
- * (HOST u64): loads issued per pool code 1..5.  Time it with events on `stream`;
- * synchronises `stream`. */
+ * policies and fetch hints), one walker per thread like the walk but with 2^(flags & 3)
+ * steps' loads in flight and no dependency between them, on (flags >> 8 & 255 or 8) x SMs
+ * blocks of 256 threads.  counts_host[4] (HOST u64): headers, buckets, members, arcs
+ * loaded.  Time it with events on `stream`; synchronises `stream`. */
 bingo_status bingo_walk_trace(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts_or_null,
-                              uint32_t num_walkers, const uint64_t *rec_off, uint32_t *trace, uint64_t n_records,
+                              uint32_t num_walkers, const uint64_t *rec_off, void *trace, uint64_t n_records,
                               uint64_t *counters_host, void *stream);
-bingo_status bingo_walk_replay(bingo_graph *g, const uint32_t *trace, uint64_t n_records, uint32_t flags,
-                               uint64_t *counts_host, void *stream);
+bingo_status bingo_walk_replay(bingo_graph *g, const void *trace, const uint64_t *rec_off, uint32_t num_walkers,
+                               uint32_t flags, uint64_t *counts_host, void *stream);
 
 const char *bingo_status_str(bingo_status s);
 

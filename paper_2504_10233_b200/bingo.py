@@ -112,7 +112,7 @@ def _lib():
         L.bingo_walk_profile.restype = ctypes.c_int
         L.bingo_walk_trace.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, u64, P, P]
         L.bingo_walk_trace.restype = ctypes.c_int
-        L.bingo_walk_replay.argtypes = [P, P, u64, u32, P, P]
+        L.bingo_walk_replay.argtypes = [P, P, P, u32, u32, P, P]
         L.bingo_walk_replay.restype = ctypes.c_int
         L.bingo_status_str.argtypes = [ctypes.c_int]
         L.bingo_status_str.restype = ctypes.c_char_p
@@ -385,11 +385,12 @@ class Graph:
     def walk_trace(self, rec_off, trace, app: int = DEEPWALK, length: int = 80, seed: int = 0,
                    first_walker: int = 0, num_walkers: Optional[int] = None, stop=(1, 80), stream=None) -> dict:
         """bingo_walk_trace: the same walks, with every step's loads recorded into `trace`
-        (int32 CUDA tensor [5 * n_records], slot-major) at rec_off[i] + t (int64 CUDA tensor
-        [num_walkers + 1], exclusive prefix sum of the walkers' lengths).  Returns the load counters."""
+        (CUDA tensor of 16 B x n_records, e.g. int32 [n_records, 4]) at rec_off[i] + t (int64
+        CUDA tensor [num_walkers + 1], exclusive prefix sum of the lengths).  Returns the
+        load counters."""
         torch = _torch()
         W = num_walkers if num_walkers is not None else self.V
-        n = trace.numel() // 5
+        n = trace.numel() * trace.element_size() // 16
         d = WalkDesc(app=app, length=length, p=1.0, q=1.0, stop_num=stop[0], stop_den=stop[1], seed=seed,
                      first_walker_id=first_walker, flags=0)
         c = np.zeros(8, dtype=np.uint64)
@@ -400,17 +401,17 @@ class Graph:
         names = ("steps", "hdr", "bkt", "mem", "arc", "probe", "visit", "walkers")
         return {k: int(v) for k, v in zip(names, c)}
 
-    def walk_replay(self, trace, visits: bool = False, stream=None) -> dict:
-        """bingo_walk_replay: issue the traced loads with no dependency between them.
-        Returns the loads issued per pool."""
+    def walk_replay(self, trace, rec_off, ahead: int = 4, blocks_per_sm: int = 8, stream=None) -> dict:
+        """bingo_walk_replay: the traced loads, walker by walker, `ahead` steps in flight per
+        thread and no dependency between steps.  Returns the loads issued per record type."""
         torch = _torch()
-        n = trace.numel() // 5
-        c = np.zeros(6, dtype=np.uint64)
-        _order_on(stream, self.device, trace)
+        c = np.zeros(4, dtype=np.uint64)
+        _order_on(stream, self.device, trace, rec_off)
         with torch.cuda.device(self.device):
-            _check(_lib().bingo_walk_replay(self._h, trace.data_ptr(), n, 1 if visits else 0, c.ctypes.data,
-                                            _stream_ptr(stream)), "bingo_walk_replay")
-        return {"hdr": int(c[1]), "bkt": int(c[2]), "mem": int(c[3]), "arc": int(c[4]), "visit": int(c[5])}
+            flags = {1: 0, 2: 1, 4: 2, 8: 3}[ahead] | (blocks_per_sm << 8)
+            _check(_lib().bingo_walk_replay(self._h, trace.data_ptr(), rec_off.data_ptr(), rec_off.numel() - 1,
+                                            flags, c.ctypes.data, _stream_ptr(stream)), "bingo_walk_replay")
+        return {"hdr": int(c[0]), "bkt": int(c[1]), "mem": int(c[2]), "arc": int(c[3])}
 
     def visit_counts(self, reset: bool = False, stream=None):
         torch = _torch()

@@ -93,7 +93,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                         cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
                     if (FLT) dr = load_dec(a.dec + u);
                     if (PROF) prof.hdr++;
-                    if (TRACE) prof.rec[0] = trace_code(TP_THDR, true, a.thdr, a.thdr + u);
+                    if (TRACE) prof.rec.x = u;
                 }
                 if (h.n == 0 && dr.dcnt == 0) {
                     fin = true;                               // dead end (d = 0): truncate (R-13)
@@ -149,8 +149,6 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
 #endif
 #endif
                             if (PROF) prof.visit++;
-                            if (TRACE && a.visit)
-                                prof.rec[4] = trace_code(TP_VISIT, true, a.visit, a.visit + visit_slot(u));
                             if (a.stop_always) {
                                 fin = true;
                             } else {
@@ -160,12 +158,8 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                         }
                         if (TRACE) {
                             const unsigned long long r = a.trace_off[i] + t;
-                            if (r < a.trace_off[i + 1]) {
-#pragma unroll
-                                for (int sl = 0; sl < TRACE_SLOTS; sl++) a.trace[sl * a.trace_n + r] = prof.rec[sl];
-                            }
-#pragma unroll
-                            for (int sl = 0; sl < TRACE_SLOTS; sl++) prof.rec[sl] = 0;
+                            if (r < a.trace_off[i + 1]) a.trace[r] = prof.rec;
+                            prof.rec = make_uint4(0u, 0u, TR_EMPTY, TR_EMPTY);
                         }
                         t++;
                         if (a.L != BINGO_NO_CAP && t >= a.L) fin = true;
@@ -251,9 +245,8 @@ static unsigned walk_grid(K kernel, uint32_t W) {
 }
 
 struct TraceOut {
-    uint32_t *trace;
+    uint4 *trace;
     const unsigned long long *off;
-    unsigned long long n;
 };
 
 bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts, uint32_t W,
@@ -293,7 +286,6 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     a.prof = prof;
     a.trace = tr ? tr->trace : nullptr;
     a.trace_off = tr ? tr->off : nullptr;
-    a.trace_n = tr ? tr->n : 0;
     if (tr && (desc->app == BINGO_NODE2VEC || g->float_mode || (desc->flags & BINGO_WALK_WALKER_MAJOR) || !prof))
         return BINGO_E_INVAL;
     if (!g->walk_ctr) return BINGO_E_STATE;
@@ -469,32 +461,29 @@ extern "C" bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc
 // ---------------------------------------------------------------- access trace + replay
 // (measurement only: the roofline's "achievable gather bandwidth" for the walk's OWN
 // footprint and skew).  bingo_walk_trace re-runs a walk (same walks as bingo_walk) and
-// records, per step, the codes of the loads the step made (trace_code in walk_common.cuh);
-// k_replay then issues exactly those loads -- same addresses, same widths, same L2 policies
-// and 64 B fetch hints -- with no dependency between them (4 records x up to 4 loads in
-// flight per thread over a full grid).  Its rate is what the memory system delivers for this
-// access mix when latency is fully hidden: the ceiling the dependent walk is measured against.
-static bool trace_pools_fit(const bingo_graph *g) {
-    const uint64_t lim = (1ull << TRACE_GRANULE_BITS) << 6;
-    return (uint64_t)g->V * sizeof(ThinHdr) <= lim && g->bkt_cap * sizeof(Bucket) <= lim && g->mem_cap * 4ull <= lim &&
-           g->arc_cap * 8ull <= lim && visit_words(g->V) * 8ull <= lim;
-}
-
+// records, per step, the loads the step made (16 B records, walk_common.cuh);
+// k_replay then issues exactly those loads -- same addresses, widths, L2 policies and 64 B
+// fetch hints -- walker by walker like the walk (a thread takes a walker and runs through
+// its steps), but with no dependency between steps: REPLAY_AHEAD steps (up to 16 loads)
+// in flight per thread.  That is the walk with perfect prefetching: what the memory system
+// delivers for this access stream when latency is hidden -- the ceiling the dependent walk
+// is measured against.
 extern "C" bingo_status bingo_walk_trace(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts_or_null,
-                                         uint32_t num_walkers, const uint64_t *rec_off, uint32_t *trace,
+                                         uint32_t num_walkers, const uint64_t *rec_off, void *trace,
                                          uint64_t n_records, uint64_t *counters_host, void *stream) {
     if (!g || !desc || !counters_host || !rec_off || !trace) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     if (!(desc->app == BINGO_DEEPWALK || desc->app == BINGO_PPR) || desc->flags || g->float_mode) return BINGO_E_INVAL;
     if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
     if (desc->length == BINGO_NO_CAP && desc->app != BINGO_PPR) return BINGO_E_INVAL;
-    if (g->V == 0 || !trace_pools_fit(g)) return BINGO_E_INVAL;
+    if (g->V == 0 || g->arc_cap >= (1ull << 32) || g->mem_cap >= (1ull << 32) || g->bkt_cap >= (1ull << 31))
+        return BINGO_E_INVAL;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long *dprof = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * BINGO_PROF_N);
     if (!dprof) return BINGO_E_NOMEM;
     cudaError_t e = cudaMemsetAsync(dprof, 0, sizeof(unsigned long long) * BINGO_PROF_N, s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(trace, 0, sizeof(uint32_t) * TRACE_SLOTS * n_records, s);
-    const TraceOut tr{trace, reinterpret_cast<const unsigned long long *>(rec_off), (unsigned long long)n_records};
+    if (e == cudaSuccess) e = cudaMemsetAsync(trace, 0xFF, sizeof(uint4) * n_records, s);
+    const TraceOut tr{reinterpret_cast<uint4 *>(trace), reinterpret_cast<const unsigned long long *>(rec_off)};
     bingo_status st = BINGO_OK;
     if (e == cudaSuccess) st = launch_walk(g, desc, starts_or_null, num_walkers, nullptr, nullptr, s, dprof, &tr);
     if (st == BINGO_OK && e == cudaSuccess)
@@ -506,97 +495,102 @@ extern "C" bingo_status bingo_walk_trace(bingo_graph *g, const bingo_walk_desc *
 }
 
 struct ReplayArgs {
-    const uint32_t *trace;
-    unsigned long long n;
-    const char *base[6];
-    unsigned long long *visit;
-    unsigned long long *counts;   // [6] loads issued per pool
+    const uint4 *trace;
+    const unsigned long long *off;
+    uint32_t walkers;
+    const ThinHdr *thdr;
+    const Bucket *bkt;
+    const uint32_t *mdst;
+    const uint2 *arc;
+    unsigned long long *counts;   // [4] loads issued: headers, buckets, members, arcs
     uint32_t *sink;
-    uint32_t visits;              // 1: replay the PPR visit RMWs too
 };
 
-#define REPLAY_UNROLL 4
+__device__ __forceinline__ uint32_t replay_intra(const ReplayArgs &a, uint32_t c, uint64_t keep, uint64_t strm,
+                                                 uint32_t &nm, uint32_t &na) {
+    if (c == TR_EMPTY) return 0;
+    const uint64_t pol = (c >> 30) & 1u ? keep : strm;
+    const uint64_t gr = c & 0x3FFFFFFFu;
+    if (c >> 31) {
+        na++;
+        return ldg8(a.arc + (gr << 2), pol).x;
+    }
+    nm++;
+    return ldg4(a.mdst + (gr << 2), pol);
+}
+
+template <int REPLAY_AHEAD>
 __global__ void __launch_bounds__(256) k_replay(const ReplayArgs a) {
     uint64_t pol_keep, pol_stream;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
-    const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
-    uint32_t acc = 0;
-    uint32_t cnt[6] = {0, 0, 0, 0, 0, 0};
-    for (unsigned long long r0 = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; r0 < a.n;
-         r0 += REPLAY_UNROLL * stride) {
-        uint32_t c[REPLAY_UNROLL][TRACE_SLOTS];
+    const Policies pol{pol_keep, pol_stream};
+    uint32_t acc = 0, nh = 0, nm = 0, na = 0;
+    for (uint32_t j = blockIdx.x * blockDim.x + threadIdx.x; j < a.walkers; j += gridDim.x * blockDim.x) {
+        const unsigned long long r1 = a.off[j + 1];
+        for (unsigned long long r = a.off[j]; r < r1; r += REPLAY_AHEAD) {
+            uint4 c[REPLAY_AHEAD];
 #pragma unroll
-        for (int u = 0; u < REPLAY_UNROLL; u++) {
-            const unsigned long long r = r0 + u * stride;
+            for (int u = 0; u < REPLAY_AHEAD; u++)
+                c[u] = r + u < r1 ? __ldcs(a.trace + r + u) : make_uint4(TR_EMPTY, TR_EMPTY, TR_EMPTY, TR_EMPTY);
+            uint32_t v[REPLAY_AHEAD][4];
 #pragma unroll
-            for (int sl = 0; sl < TRACE_SLOTS; sl++) c[u][sl] = r < a.n ? __ldcs(a.trace + sl * a.n + r) : 0u;
-        }
-        uint32_t v[REPLAY_UNROLL][TRACE_SLOTS];
-#pragma unroll
-        for (int u = 0; u < REPLAY_UNROLL; u++) {
-#pragma unroll
-            for (int sl = 0; sl < TRACE_SLOTS; sl++) {
-                const uint32_t code = c[u][sl];
-                const uint32_t pool = code >> 29;
-                const uint64_t pol = (code >> 28) & 1u ? pol_keep : pol_stream;
-                const char *p = a.base[pool < 6 ? pool : 0] + ((uint64_t)(code & ((1u << TRACE_GRANULE_BITS) - 1u)) << 6);
-                v[u][sl] = 0;
-                if (pool == TP_BKT) {
-                    const Bucket B = ldg_bucket(reinterpret_cast<const Bucket *>(p), pol);
-                    v[u][sl] = B.px ^ B.ay;
-                    cnt[pool]++;
-                } else if (pool == TP_THDR || pool == TP_ARC) {
-                    v[u][sl] = ldg8(reinterpret_cast<const uint2 *>(p), pol).x;
-                    cnt[pool]++;
-                } else if (pool == TP_MDST) {
-                    v[u][sl] = ldg4(reinterpret_cast<const uint32_t *>(p), pol);
-                    cnt[pool]++;
-                } else if (pool == TP_VISIT && a.visits) {
-                    atomicAdd(reinterpret_cast<unsigned long long *>(const_cast<char *>(p)), 1ull);
-                    cnt[pool]++;
+            for (int u = 0; u < REPLAY_AHEAD; u++) {
+                v[u][0] = v[u][1] = 0;
+                if (c[u].x != TR_EMPTY) {
+                    v[u][0] = load_thdr(a.thdr + c[u].x, pol).bkt_off;
+                    const Bucket B = ldg_bucket(a.bkt + (c[u].y & 0x7FFFFFFFu), c[u].y >> 31 ? pol_keep : pol_stream);
+                    v[u][1] = B.px ^ B.ay;
+                    nh++;
                 }
+                v[u][2] = replay_intra(a, c[u].z, pol_keep, pol_stream, nm, na);
+                v[u][3] = replay_intra(a, c[u].w, pol_keep, pol_stream, nm, na);
             }
+#pragma unroll
+            for (int u = 0; u < REPLAY_AHEAD; u++) acc ^= v[u][0] ^ v[u][1] ^ v[u][2] ^ v[u][3];
         }
-#pragma unroll
-        for (int u = 0; u < REPLAY_UNROLL; u++)
-#pragma unroll
-            for (int sl = 0; sl < TRACE_SLOTS; sl++) acc ^= v[u][sl];
     }
-#pragma unroll
-    for (int k = 1; k < 6; k++) {
-        const unsigned long long x = warp_sum((unsigned long long)cnt[k]);
-        if ((threadIdx.x & 31u) == 0 && x) atomicAdd(&a.counts[k], x);
+    const unsigned long long x[3] = {warp_sum((unsigned long long)nh), warp_sum((unsigned long long)nm),
+                                     warp_sum((unsigned long long)na)};
+    if ((threadIdx.x & 31u) == 0) {
+        if (x[0]) { atomicAdd(&a.counts[0], x[0]); atomicAdd(&a.counts[1], x[0]); }
+        if (x[1]) atomicAdd(&a.counts[2], x[1]);
+        if (x[2]) atomicAdd(&a.counts[3], x[2]);
     }
     if (acc == 0x9E3779B9u) a.sink[0] = acc;   // keeps the loads alive
 }
 
-extern "C" bingo_status bingo_walk_replay(bingo_graph *g, const uint32_t *trace, uint64_t n_records, uint32_t flags,
-                                          uint64_t *counts_host, void *stream) {
-    if (!g || !trace || !counts_host) return BINGO_E_INVAL;
+extern "C" bingo_status bingo_walk_replay(bingo_graph *g, const void *trace, const uint64_t *rec_off,
+                                          uint32_t num_walkers, uint32_t flags, uint64_t *counts_host, void *stream) {
+    if (!g || !trace || !rec_off || !counts_host) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long *dc = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * 8);
     if (!dc) return BINGO_E_NOMEM;
     ReplayArgs a;
-    a.trace = trace;
-    a.n = n_records;
-    a.base[0] = reinterpret_cast<const char *>(g->thdr);
-    a.base[TP_THDR] = reinterpret_cast<const char *>(g->thdr);
-    a.base[TP_BKT] = reinterpret_cast<const char *>(g->bkt);
-    a.base[TP_MDST] = reinterpret_cast<const char *>(g->mdst);
-    a.base[TP_ARC] = reinterpret_cast<const char *>(g->arc);
-    a.base[TP_VISIT] = reinterpret_cast<const char *>(g->visit);
-    a.visit = g->visit;
+    a.trace = reinterpret_cast<const uint4 *>(trace);
+    a.off = reinterpret_cast<const unsigned long long *>(rec_off);
+    a.walkers = num_walkers;
+    a.thdr = g->thdr;
+    a.bkt = g->bkt;
+    a.mdst = g->mdst;
+    a.arc = g->arc;
     a.counts = dc;
     a.sink = reinterpret_cast<uint32_t *>(dc + 7);
-    a.visits = flags & 1u;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e = cudaMemsetAsync(dc, 0, sizeof(unsigned long long) * 8, s);
+    // flags: bits 0-1 log2(steps in flight per thread: 1, 2, 4, 8), bits 8-15 blocks per SM (0: 8)
+    const unsigned bps = ((flags >> 8) & 0xFFu) ? ((flags >> 8) & 0xFFu) : 8u;
+    const dim3 grid((unsigned)sms * bps);
     if (e == cudaSuccess) {
-        k_replay<<<(unsigned)sms * 8, 256, 0, s>>>(a);
+        switch (flags & 3u) {
+            case 0: k_replay<1><<<grid, 256, 0, s>>>(a); break;
+            case 1: k_replay<2><<<grid, 256, 0, s>>>(a); break;
+            case 2: k_replay<4><<<grid, 256, 0, s>>>(a); break;
+            default: k_replay<8><<<grid, 256, 0, s>>>(a); break;
+        }
         bingo_count_launch();
         e = cudaGetLastError();
     }
@@ -605,7 +599,7 @@ extern "C" bingo_status bingo_walk_replay(bingo_graph *g, const uint32_t *trace,
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     bingo_dev_free(g, dc);
     if (e != cudaSuccess) { g->poisoned = 1; return BINGO_E_CUDA; }
-    for (int k = 0; k < 6; k++) counts_host[k] = h[k];
+    for (int k = 0; k < 4; k++) counts_host[k] = h[k];
     return BINGO_OK;
 }
 

@@ -12,21 +12,21 @@ namespace bingo {
 enum { PR_STEPS = 0, PR_HDR, PR_BKT, PR_MEM, PR_ARC, PR_PROBE, PR_VISIT, PR_WALKERS, BINGO_PROF_N_ };
 #define BINGO_PROF_N 8
 
-// access trace (bingo_walk_trace, measurement only): per accepted step up to TRACE_SLOTS
-// loads, each a u32 code = pool (3 bits) | L2 keep policy (1 bit) | 64 B granule within the
-// pool (28 bits); 0 = empty slot.  Slots: header, bucket, member or dense attempt 0, dense
-// attempt 1, PPR visit counter.
-enum : uint32_t { TP_THDR = 1, TP_BKT = 2, TP_MDST = 3, TP_ARC = 4, TP_VISIT = 5 };
-#define TRACE_SLOTS 5
-#define TRACE_GRANULE_BITS 28
-__device__ __forceinline__ uint32_t trace_code(uint32_t pool, bool keep, const void *base, const void *p) {
-    const uint64_t gr = (uint64_t)((const char *)p - (const char *)base) >> 6;
-    return (pool << 29) | ((uint32_t)keep << 28) | ((uint32_t)gr & ((1u << TRACE_GRANULE_BITS) - 1u));
+// access trace (bingo_walk_trace, measurement only): one 16 B record per accepted step,
+// the loads the step made:
+//   x: vertex (internal id) whose thin header was read
+//   y: bucket pool index | L2 keep policy << 31
+//   z: member or dense attempt 0, w: dense attempt 1 -- TR_EMPTY, or
+//      kind << 31 (0 member dst, 1 arc) | keep << 30 | granule (30 bits): 16 B of the member
+//      pool or the 32 B sector of the arc pool (4 arcs) -- inside the sector the walk read
+#define TR_EMPTY 0xFFFFFFFFu
+__device__ __forceinline__ uint32_t tr_intra(bool arc, bool keep, uint64_t elem) {
+    return ((uint32_t)arc << 31) | ((uint32_t)keep << 30) | (uint32_t)((elem >> 2) & 0x3FFFFFFFu);
 }
 
 struct WalkProf {
     unsigned long long steps = 0, hdr = 0, bkt = 0, mem = 0, arc = 0, probe = 0, visit = 0, walkers = 0;
-    uint32_t rec[TRACE_SLOTS] = {0, 0, 0, 0, 0};   // trace mode: this step's load codes
+    uint4 rec = make_uint4(0u, 0u, TR_EMPTY, TR_EMPTY);   // trace mode: this step's loads
     __device__ void flush(unsigned long long *out) {
         unsigned long long v[8] = {steps, hdr, bkt, mem, arc, probe, visit, walkers};
 #pragma unroll
@@ -61,10 +61,9 @@ struct WalkArgs {
     unsigned long long stop_thr;
     uint32_t stop_always;
     unsigned long long *prof;
-    // trace mode: slot-major codes trace[s * trace_n + trace_off[i] + t] for t < lengths[i]
-    uint32_t *trace;
+    // trace mode: record of step t of walker i at trace[trace_off[i] + t]
+    uint4 *trace;
     const unsigned long long *trace_off;
-    unsigned long long trace_n;
 };
 
 #ifdef BINGO_NO_L2_64B            // A/B experiment switch: no 64 B L2 fetch hint
@@ -139,7 +138,7 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
     const uint32_t b = __umulhi(r.x, (uint32_t)h.n);
     const Bucket B = ldg_bucket(a.bkt + h.bkt_off + b, (h.flags & 1u) ? pol.keep : pol.stream);
     if (PROF) prof.bkt++;
-    if (TRACE) prof.rec[1] = trace_code(TP_BKT, h.flags & 1u, a.bkt, a.bkt + h.bkt_off + b);
+    if (TRACE) prof.rec.y = (h.bkt_off + b) | ((uint32_t)(h.flags & 1u) << 31);
     const bool alt = join64(r.y, r.z) >= B.lim;
     const uint32_t x = alt ? B.ax : B.px;
     const uint32_t y = alt ? B.ay : B.py;
@@ -169,7 +168,7 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
     const uint64_t j0 = __umul64hi(join64(q0.x, q0.y), (uint64_t)x);
     if (kind != K_DENSE) {
         if (PROF) prof.mem++;
-        if (TRACE) prof.rec[2] = trace_code(TP_MDST, h.flags & 2u, a.mdst, a.mdst + (uint64_t)y * 4 + j0);
+        if (TRACE) prof.rec.z = tr_intra(false, h.flags & 2u, (uint64_t)y * 4 + j0);
         return ldg4(a.mdst + (uint64_t)y * 4 + j0, (h.flags & 2u) ? pol.keep : pol.stream);
     }
 #endif
@@ -202,7 +201,9 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
                     const P4 q = draw_oi(w, t, outer, base + s, 1u, a.k0, a.k1);
                     j = __umul64hi(join64(q.x, q.y), (uint64_t)x);
                 }
-                prof.rec[2 + base + s] = trace_code(TP_ARC, h.flags & 2u, a.arc, adj + j);
+                const uint32_t code = tr_intra(true, h.flags & 2u, ((uint64_t)y << 2) + j);
+                if (base + s == 0) prof.rec.z = code;
+                else prof.rec.w = code;
             }
             res = acc ? e[s].x : res;
             done = done || acc;

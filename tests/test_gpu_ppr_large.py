@@ -129,3 +129,35 @@ def test_node2vec_profile_dense_attempts(big, monkeypatch):
     ref = o.walk(app=oracle.APP_NODE2VEC, length=20, p=2.0, q=0.5, seed=44, num_walkers=50_000)
     assert np.array_equal(u32(pr["paths"]), ref["paths"])
     assert pr["arc"] == ref["dense_attempts"]
+
+
+@pytest.mark.parametrize("app", ["deepwalk", "ppr"])
+def test_trace_replay_counts(big, app, monkeypatch):
+    """Measurement path (bench.py's gather ceiling): bingo_walk_trace runs the same walks as
+    bingo_walk and records one entry per step; bingo_walk_replay re-issues exactly the loads the
+    profile counted (headers = buckets = steps, members = profile members, dense attempts =
+    the first two of every dense step)."""
+    import torch
+    import paper_2504_10233_b200 as pb
+    w, o = big
+    g = _gpu_graph(w, "relabel", monkeypatch)
+    kw = dict(app=pb.PPR, length=pb.NO_CAP, stop=(1, 80)) if app == "ppr" else dict(app=pb.DEEPWALK, length=80)
+    W = 200_000
+    pr = g.walk_profile(seed=55, first_walker=FIRST, num_walkers=W, paths=False, **kw)
+    lens = pr["lengths"].to(torch.int64)
+    off = torch.zeros(W + 1, dtype=torch.int64, device=lens.device)
+    off[1:] = torch.cumsum(lens, 0)
+    n = int(off[-1])
+    trace = torch.empty((n, 4), dtype=torch.int32, device=lens.device)
+    tp = g.walk_trace(off, trace, seed=55, first_walker=FIRST, num_walkers=W, **kw)
+    for k in ("steps", "hdr", "bkt", "mem", "arc"):
+        assert tp[k] == pr[k], (k, tp[k], pr[k])
+    assert n == pr["steps"]
+    rep = g.walk_replay(trace, off)
+    assert rep["hdr"] == rep["bkt"] == n
+    assert rep["mem"] == pr["mem"]
+    assert 0 < rep["arc"] <= pr["arc"]
+    ref = o.walk(app=oracle.APP_PPR if app == "ppr" else oracle.APP_DEEPWALK,
+                 length=oracle.NONE if app == "ppr" else 80, stop=(1, 80), seed=55, first_walker=FIRST,
+                 num_walkers=W, paths=False)
+    assert np.array_equal(lens.cpu().numpy().astype(np.uint32), ref["lengths"])
