@@ -557,13 +557,30 @@ def streaming(g, batches, stream):
         rc = lib.bingo_apply_updates(h, base + 16 * i, 1, bb.UPD_HOST_BATCH, None, sp)
         lat_c.append(1e6 * (time.perf_counter() - t0))
         assert rc == 0, rc
-    return {"records": len(recs), "call_us_p50": float(np.percentile(lat_host, 50)),
+    # f2: the same kind of records through the persistent streaming queue (bingo_stream_update):
+    # raw C-ABI call, host post -> device apply -> host sees the result
+    qrec = np.ascontiguousarray(batches[-3][:2000], dtype=np.uint32)
+    st = bb.UpdateStats()
+    qbase = qrec.ctypes.data
+    lat_q = []
+    for i in range(len(qrec)):
+        t0 = time.perf_counter()
+        rc = lib.bingo_stream_update(h, qbase + 16 * i, ctypes.byref(st), sp)
+        lat_q.append(1e6 * (time.perf_counter() - t0))
+        assert rc == 0, rc
+    torch.cuda.synchronize()
+    return {"records": len(recs), "queue_records": len(lat_q),
+            "queue_us_p50": float(np.percentile(lat_q, 50)), "queue_us_p90": float(np.percentile(lat_q, 90)),
+            "queue_us_p99": float(np.percentile(lat_q, 99)),
+            "queue_updates_per_s": float(len(lat_q) / (1e-6 * sum(lat_q))),
+            "call_us_p50": float(np.percentile(lat_host, 50)),
             "call_us_p99": float(np.percentile(lat_host, 99)),
             "device_us_p50": float(np.percentile(lat_dev, 50)), "device_us_p99": float(np.percentile(lat_dev, 99)),
             "abi_call_us_p50": float(np.percentile(lat_c, 50)), "abi_call_us_p99": float(np.percentile(lat_c, 99)),
             "abi_updates_per_s": float(len(lat_c) / (1e-6 * sum(lat_c))),
-            "note": "one bingo_apply_updates call per arc record (epoch per record); call_us: through the Python "
-                    "binding; abi_call_us: the C-ABI call via ctypes, host to completion"}
+            "note": "one call per arc record (epoch per record); queue_us: bingo_stream_update (persistent "
+                    "device-side queue, no launch per record), host to completion via ctypes; call_us: "
+                    "bingo_apply_updates through the Python binding; abi_call_us: bingo_apply_updates via ctypes"}
 
 
 # ---------------------------------------------------------------- the oracle (CPU) legs

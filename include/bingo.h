@@ -184,6 +184,19 @@ bingo_status bingo_apply_updates(bingo_graph *g, const bingo_update *batch, uint
 bingo_status bingo_apply_updates_f64(bingo_graph *g, const bingo_update *batch, const double *bias_f64, uint64_t n,
                                      uint32_t flags, bingo_update_stats *stats_or_null, void *stream);
 
+/* bingo_stream_update -- one arc record applied through the persistent streaming queue
+ * (streaming updates, P:126 / P:316-336).  Same semantics, statistics, epoch and
+ * errors as bingo_apply_updates(g, rec, 1, BINGO_UPD_HOST_BATCH, ...) -- rec is HOST memory,
+ * the call returns when the record is applied -- but without a kernel launch per record: a
+ * one-warp kernel stays resident on `stream` and polls a ring in mapped pinned host memory;
+ * its results come back the same way.  It exits when any other call on the graph needs the
+ * graph (that call is ordered after it: the epoch fence), after 2 ms without a record (a
+ * caller synchronising `stream` waits at most that long), or on a record that needs pool
+ * growth or touches a vertex above 8192 arcs (that record then takes the batched pipeline).
+ * Integer-bias graphs only (EINVAL for float graphs). */
+bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *rec, bingo_update_stats *stats_or_null,
+                                 void *stream);
+
 /* ---------------------------------------------------------------------------
  * bingo_walk -- the batched walker step (S3 "random walk query", P:215;
  * Eq.5/Eq.6 two-stage sample; dense rejection P:465; applications S6.1

@@ -34,7 +34,7 @@ NO_CAP = 0xFFFFFFFF
 ABI_SYMBOLS = ("bingo_build", "bingo_destroy", "bingo_apply_updates", "bingo_apply_updates_f64", "bingo_walk",
                "bingo_visit_counts",
                "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str", "bingo_walk_profile",
-               "bingo_walk_trace", "bingo_walk_replay")
+               "bingo_walk_trace", "bingo_walk_replay", "bingo_stream_update")
 
 
 class BingoError(RuntimeError):
@@ -110,6 +110,8 @@ def _lib():
         L.bingo_get_info.restype = ctypes.c_int
         L.bingo_walk_profile.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, P, P]
         L.bingo_walk_profile.restype = ctypes.c_int
+        L.bingo_stream_update.argtypes = [P, P, ctypes.POINTER(UpdateStats), P]
+        L.bingo_stream_update.restype = ctypes.c_int
         L.bingo_walk_trace.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, u64, P, P]
         L.bingo_walk_trace.restype = ctypes.c_int
         L.bingo_walk_replay.argtypes = [P, P, P, u32, u32, P, P]
@@ -296,6 +298,23 @@ class Graph:
                 rc = _lib().bingo_apply_updates_f64(self._h, ptr, wptr, n, flags, ctypes.byref(st),
                                                     _stream_ptr(stream))
             _check(rc, "bingo_apply_updates")
+        return {"inserted": st.inserted, "deleted": st.deleted, "missing_deletes": st.missing_deletes,
+                "touched_vertices": st.touched_vertices,
+                "kind_transitions": np.array(st.kind_transitions, dtype=np.uint64).reshape(5, 5),
+                "epoch": st.epoch}
+
+    def stream_update(self, record, stream=None, stats: bool = True):
+        """bingo_stream_update: one {op, src, dst, bias} record through the persistent
+        streaming queue (no launch per record); returns the statistics like apply_updates."""
+        torch = _torch()
+        rec = np.ascontiguousarray(record, dtype=np.uint32).reshape(4)
+        st = UpdateStats()
+        with contextlib.nullcontext() if torch.cuda.current_device() == self.device.index else \
+                torch.cuda.device(self.device):
+            _check(_lib().bingo_stream_update(self._h, rec.ctypes.data, ctypes.byref(st) if stats else None,
+                                              _stream_ptr(stream)), "bingo_stream_update")
+        if not stats:
+            return None
         return {"inserted": st.inserted, "deleted": st.deleted, "missing_deletes": st.missing_deletes,
                 "touched_vertices": st.touched_vertices,
                 "kind_transitions": np.array(st.kind_transitions, dtype=np.uint64).reshape(5, 5),

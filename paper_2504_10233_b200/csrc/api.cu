@@ -32,6 +32,7 @@ void bingo_dev_free(bingo_graph *g, void *p) {
 
 extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
+    bingo_sq_release(g);
     void *bufs[] = {g->perm, g->inv, g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->arc_dval, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->nbtomb, g->hixo, g->hixt, g->hix, g->dec, g->dmem, g->counters, g->visit, g->dev_flag,
                     g->scratch, g->wscratch, g->vscratch, g->bscratch, g->iscratch, g->fast_scr};
     for (void *p : bufs) bingo_dev_free(g, p);
@@ -61,6 +62,7 @@ extern "C" const char *bingo_status_str(bingo_status s) {
 }
 
 extern "C" bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *stream) {
+    if (g) bingo_sq_quiesce(g, (cudaStream_t)stream);
     if (!g || !info) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     unsigned long long c[4];
@@ -106,6 +108,7 @@ struct Out {
 }  // namespace
 
 extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t cap, size_t *size_out, void *stream) {
+    if (g) bingo_sq_quiesce(g, (cudaStream_t)stream);
     if (!g || !size_out) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     cudaStream_t s = (cudaStream_t)stream;
@@ -251,6 +254,7 @@ __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 
 }  // namespace bingo
 
 extern "C" bingo_status bingo_digests(bingo_graph *g, uint64_t *digests, void *stream) {
+    if (g) bingo_sq_quiesce(g, (cudaStream_t)stream);
     if (!g || !digests) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     if (!g->V) return BINGO_OK;

@@ -235,7 +235,19 @@ struct bingo_graph {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     void *fast_out_host = nullptr;           // mapped pinned status/stats of the fast path
     void *fast_out_dev = nullptr;
+    // streaming queue (bingo_stream_update): mapped pinned ring + persistent kernel
+    void *sq_host = nullptr;                 // StreamQ (update.cu), host view
+    void *sq_dev = nullptr;                  // its device view
+    bool sq_running = false;                 // a k_stream_upd generation may be live on sq_stream
+    uint32_t sq_gen = 0, sq_seq = 0;         // last generation launched, next record number
+    cudaStream_t sq_stream = nullptr;        // the stream it was launched on
+    cudaEvent_t sq_ev = nullptr;             // recorded after the launch: completes when it exits
 };
+
+// stops a running streaming-queue kernel and orders `s` after its exit (update.cu); every
+// entry point that touches the graph calls it first (the epoch fence of the streaming queue)
+void bingo_sq_quiesce(bingo_graph *g, cudaStream_t s);
+void bingo_sq_release(bingo_graph *g);
 
 // process-wide count of kernel launches issued by libbingo (api.cu)
 void bingo_count_launch(unsigned n = 1);

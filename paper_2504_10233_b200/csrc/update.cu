@@ -934,7 +934,14 @@ __host__ __device__ inline unsigned long long fast_words_per_vertex() {
     return (FAST_MAXL + 31) / 32 + 8ull * (2 * FAST_N) + 3ull * FAST_N + 16;
 }
 
-__global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
+// the whole small-batch update in one block (k_upd_fast; the streaming queue's persistent
+// kernel k_stream_upd runs it with one warp per record).  Records come from `src` (device or
+// shared memory, fa.n of them); status / statistics go to fa.out.
+__device__ __forceinline__ uint32_t fast_status(uint32_t f) {
+    return (f & FAST_INVAL) ? FAST_INVAL : (f & FAST_OVERFLOW) ? FAST_OVERFLOW : (f & FAST_SLOW) ? FAST_SLOW : FAST_OK;
+}
+
+__device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint4 *src) {
     __shared__ uint4 recs[FAST_N];
     __shared__ uint32_t sval[FAST_N], seg[FAST_N + 1], tv[FAST_N];
     __shared__ unsigned long long scr_off[FAST_N + 1];
@@ -944,7 +951,7 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
     const uint32_t tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
     const uint32_t n = fa.n;
     if (tid == 0) { need_arc = need_bkt = need_mem = 0; flag = 0; }
-    if (tid < n) recs[tid] = fa.drecs ? fa.drecs[tid] : fa.recs[tid];
+    if (tid < n) recs[tid] = src[tid];
     __syncthreads();
     // validation (whole batch, before anything else)
     if (tid < n) {
@@ -966,7 +973,7 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
             fa.out->ntouch = 0;
             fa.out->inserted = 0;
         }
-        return;
+        return FAST_INVAL;
     }
     // stable grouping by src: rank = #{j : src_j < src_i, or src_j == src_i and j < i}
     if (tid < n) {
@@ -1048,10 +1055,10 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
         for (uint32_t t = w; t < nt; t += nw) mutate_vertex<32>(a, t, sm[w], fast_wscr + w * WARP_SCR_WORDS, WARP_SCR_WORDS);
     }
     __syncthreads();
+    const uint32_t fin = flag;   // final since the barrier before the mutation
     if (tid == 0) {
         FastOut *o = fa.out;
-        const uint32_t f = flag;
-        o->status = (f & FAST_INVAL) ? FAST_INVAL : (f & FAST_OVERFLOW) ? FAST_OVERFLOW : (f & FAST_SLOW) ? FAST_SLOW : FAST_OK;
+        o->status = fast_status(fin);
         o->ntouch = nt;
         unsigned long long ins = 0;
         for (uint32_t i = 0; i < n; i++) ins += recs[i].x == 0u ? 1ull : 0ull;
@@ -1061,6 +1068,105 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
         unsigned long long acc = 0;
         for (uint32_t t = 0; t < nt; t++) acc += fa.vstats[(uint64_t)t * VST + tid];
         fa.out->stats[tid] = acc;
+    }
+    return fast_status(fin);
+}
+
+__global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
+    upd_fast_body(fa, fa.drecs ? fa.drecs : fa.recs);
+}
+
+// ------------------------------------------------------------------ streaming queue
+// A persistent single-warp kernel that applies single-record updates as the host posts them,
+// without a launch per record.  Host -> device: slots of a ring in mapped pinned host memory
+// (seq + record); device -> host: the FastOut of the record, then done_seq, in mapped memory.
+// The kernel runs on the caller's stream, so every later operation on that stream is ordered
+// after it (the epoch fence: the library stops the kernel before any other operation on the
+// graph).  It exits on stop, after SQ_IDLE_NS without a record (a caller that synchronises
+// its stream does not wait forever), or after a record the single-warp path cannot take
+// (FAST_SLOW: pool growth, a vertex above FAST_HANDOFF_L arcs) -- the host applies that one
+// through the batched pipeline and relaunches on the next record.
+static constexpr uint32_t SQ_N = 64;
+static constexpr unsigned long long SQ_IDLE_NS = 2000000ull;
+struct StreamSlot {
+    unsigned int seq;         // record k is valid when seq == k + 1 ...
+    unsigned int gen;         // ... for the kernel generation gen only
+    unsigned int pad[2];
+    uint4 rec;
+};
+struct StreamQ {
+    unsigned int run_gen;     // host -> device: the generation that may run
+    unsigned int done_seq;    // device -> host: records completed
+    unsigned int exit_gen;    // device -> host: the generation that exited ...
+    unsigned int exit_seq;    // ... without taking record exit_seq (or after a FAST_SLOW record)
+    unsigned int pad[28];
+    FastOut out;              // device -> host: the last record's status / statistics
+    StreamSlot slot[SQ_N];
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ unsigned int ld_volatile_u32(const unsigned int *p) {
+    return *reinterpret_cast<const volatile unsigned int *>(p);
+}
+
+__device__ __forceinline__ uint4 ld_volatile_u4(const uint4 *p) {
+    uint4 v;
+    asm volatile("ld.volatile.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+
+__global__ void __launch_bounds__(32) k_stream_upd(const FastArgs fa0, StreamQ *q, unsigned int seq0, unsigned int gen) {
+    __shared__ uint4 rec;
+    __shared__ unsigned int cmd;   // 0 process, 1 exit
+    FastArgs fa = fa0;
+    fa.n = 1;
+    fa.out = &q->out;
+    unsigned int k = seq0;
+    for (;;) {
+        if (threadIdx.x == 0) {
+            unsigned int c = 1;
+            const unsigned long long t0 = globaltimer_ns();
+            for (;;) {
+                const StreamSlot *sl = &q->slot[k % SQ_N];
+                if (ld_volatile_u32(&sl->seq) == k + 1 && ld_volatile_u32(&sl->gen) == gen) {
+                    __threadfence_system();
+                    rec = ld_volatile_u4(&sl->rec);
+                    c = 0;
+                    break;
+                }
+                // stopped, or idle: exit without taking record k (the host relaunches)
+                if (ld_volatile_u32(&q->run_gen) != gen || globaltimer_ns() - t0 > SQ_IDLE_NS) break;
+                __nanosleep(32);
+            }
+            cmd = c;
+        }
+        __syncthreads();
+        if (cmd) break;
+        const unsigned int st = upd_fast_body(fa, &rec);
+        __syncthreads();
+        k++;
+        if (threadIdx.x == 0) {
+            if (st == FAST_SLOW) {   // the host applies this record through the batched pipeline
+                *reinterpret_cast<volatile unsigned int *>(&q->exit_seq) = k;
+                *reinterpret_cast<volatile unsigned int *>(&q->exit_gen) = gen;
+            }
+            __threadfence_system();
+            *reinterpret_cast<volatile unsigned int *>(&q->done_seq) = k;
+        }
+        if (st == FAST_SLOW) return;
+        if (st == FAST_OK) fa.m.epoch++;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        *reinterpret_cast<volatile unsigned int *>(&q->exit_seq) = k;
+        __threadfence_system();
+        *reinterpret_cast<volatile unsigned int *>(&q->exit_gen) = gen;
+        __threadfence_system();
     }
 }
 
@@ -1250,8 +1356,7 @@ static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
 }
 
 // returns true when the fast path decided the call (OK / EINVAL / EOVERFLOW / CUDA)
-static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
-                          bingo_update_stats *stats, cudaStream_t s, bingo_status *out) {
+static bool ensure_fast_scratch(bingo_graph *g) {
     if (!g->fast_scr) {
         const size_t words = (size_t)(FAST_N * fast_words_per_vertex());
         g->fast_scr = (uint32_t *)bingo_dev_alloc(g, 4 * words + 4 * FAST_N * VST + 16 * FAST_N + 64);
@@ -1267,9 +1372,29 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
             return false;
         }
     }
-    FastArgs fa;
+    return true;
+}
+
+static void fill_fast_common(bingo_graph *g, FastArgs &fa) {
     memset(&fa, 0, sizeof(fa));
     fill_mutate_common(g, fa.m, g->epoch + 1);
+    fa.V = g->V;
+    fa.inv = g->inv;
+    fa.arc_cap = g->arc_cap;
+    fa.bkt_cap = g->bkt_cap;
+    fa.mem_units_cap = g->mem_cap / 4;
+    fa.scr = g->fast_scr;
+    fa.scr_cap = FAST_N * fast_words_per_vertex();
+    fa.vstats = g->fast_scr + fa.scr_cap;
+    fa.out = (FastOut *)g->fast_out_dev;
+}
+
+// returns true when the fast path decided the call (OK / EINVAL / EOVERFLOW / CUDA)
+static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
+                          bingo_update_stats *stats, cudaStream_t s, bingo_status *out) {
+    if (!ensure_fast_scratch(g)) return false;
+    FastArgs fa;
+    fill_fast_common(g, fa);
     if ((flags & BINGO_UPD_HOST_BATCH) && n > FAST_INLINE) {   // larger host batches: one H2D copy
         uint4 *stage = reinterpret_cast<uint4 *>(g->fast_scr + FAST_N * fast_words_per_vertex() + FAST_N * VST);
         if (cudaMemcpyAsync(stage, batch, 16 * n, cudaMemcpyHostToDevice, s) != cudaSuccess) {
@@ -1284,15 +1409,6 @@ static bool try_fast_path(bingo_graph *g, const bingo_update *batch, uint64_t n,
         fa.drecs = reinterpret_cast<const uint4 *>(batch);
     }
     fa.n = (uint32_t)n;
-    fa.V = g->V;
-    fa.inv = g->inv;
-    fa.arc_cap = g->arc_cap;
-    fa.bkt_cap = g->bkt_cap;
-    fa.mem_units_cap = g->mem_cap / 4;
-    fa.scr = g->fast_scr;
-    fa.scr_cap = FAST_N * fast_words_per_vertex();
-    fa.vstats = g->fast_scr + fa.scr_cap;
-    fa.out = (FastOut *)g->fast_out_dev;
     FastOut *ho = (FastOut *)g->fast_out_host;
     ho->status = 0xFFFFFFFFu;
     // one warp per touched vertex at most (a vertex's records go to one warp): small
@@ -1684,6 +1800,7 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     // float-bias graphs take real biases (bingo_apply_updates_f64, R-16); integer graphs do not
     if (n && g->float_mode != (wf != nullptr)) return BINGO_E_INVAL;
     if (n >= 0xFFFFFFFFull) return BINGO_E_INVAL;
+    bingo_sq_quiesce(g, (cudaStream_t)stream);
     const bool fm = g->float_mode;
     g_trace.on = getenv("BINGO_UPD_TRACE") != nullptr;
     g_trace.mark("start", (cudaStream_t)stream);
@@ -2004,4 +2121,137 @@ bingo_status hix_build_all(bingo_graph *g, cudaStream_t s) {
         break;
     }
     return fin(st);
+}
+
+
+// ---------------------------------------------------------------- streaming queue (host side)
+void bingo_sq_quiesce(bingo_graph *g, cudaStream_t s) {
+    if (!g || !g->sq_running) return;
+    StreamQ *q = (StreamQ *)g->sq_host;
+    __atomic_store_n(&q->run_gen, 0u, __ATOMIC_SEQ_CST);   // generations start at 1: the kernel exits
+    if (s != g->sq_stream) cudaStreamWaitEvent(s, g->sq_ev, 0);
+    g->sq_running = false;
+}
+
+void bingo_sq_release(bingo_graph *g) {
+    if (!g || !g->sq_host) return;
+    bingo_sq_quiesce(g, g->sq_stream);
+    if (g->sq_ev) {
+        cudaEventSynchronize(g->sq_ev);
+        cudaEventDestroy(g->sq_ev);
+    }
+    cudaFreeHost(g->sq_host);
+    g->sq_host = g->sq_dev = nullptr;
+    g->sq_ev = nullptr;
+}
+
+static bingo_status sq_launch(bingo_graph *g, cudaStream_t s) {
+    if (!g->sq_host) {
+        void *h = nullptr;
+        if (cudaHostAlloc(&h, sizeof(StreamQ), cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            return BINGO_E_NOMEM;
+        }
+        memset(h, 0, sizeof(StreamQ));
+        if (cudaHostGetDevicePointer(&g->sq_dev, h, 0) != cudaSuccess ||
+            cudaEventCreateWithFlags(&g->sq_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            cudaFreeHost(h);
+            return BINGO_E_CUDA;
+        }
+        g->sq_host = h;
+    }
+    if (!ensure_fast_scratch(g)) return BINGO_E_NOMEM;
+    {   // the static shared memory of upd_fast_body plus one warp's delete scratch exceed 48 KB:
+        // raise the dynamic limit once per device (the attribute is per device)
+        static std::atomic<uint64_t> sq_smem_set{0};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        const uint64_t bit = 1ull << (dev & 63);
+        if (!(sq_smem_set.load(std::memory_order_acquire) & bit)) {
+            if (cudaFuncSetAttribute(k_stream_upd, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * WARP_SCR_WORDS) !=
+                cudaSuccess)
+                return upd_cuda_fail(g, cudaGetLastError(), "k_stream_upd smem attribute");
+            sq_smem_set.fetch_or(bit, std::memory_order_acq_rel);
+        }
+    }
+    StreamQ *q = (StreamQ *)g->sq_host;
+    FastArgs fa;
+    fill_fast_common(g, fa);
+    fa.n = 1;
+    const unsigned gen = ++g->sq_gen ? g->sq_gen : ++g->sq_gen;   // never 0 (0 = stopped)
+    __atomic_store_n(&q->run_gen, gen, __ATOMIC_SEQ_CST);
+    k_stream_upd<<<1, 32, 4 * WARP_SCR_WORDS, s>>>(fa, (StreamQ *)g->sq_dev, g->sq_seq, gen);
+    bingo_count_launch();
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaEventRecord(g->sq_ev, s);
+    if (e != cudaSuccess) return upd_cuda_fail(g, e, "k_stream_upd");
+    g->sq_stream = s;
+    g->sq_running = true;
+    return BINGO_OK;
+}
+
+extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *rec, bingo_update_stats *stats,
+                                            void *stream) {
+    if (!g || !rec) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    if (g->float_mode) return BINGO_E_INVAL;   // float graphs take real biases (bingo_apply_updates_f64)
+    cudaStream_t s = (cudaStream_t)stream;
+    if (stats) memset(stats, 0, sizeof(*stats));
+    if (g->sq_running && g->sq_stream != s) bingo_sq_quiesce(g, s);
+    StreamQ *q = (StreamQ *)g->sq_host;
+    const unsigned k = g->sq_seq;
+    for (int attempt = 0;; attempt++) {
+        if (!g->sq_running) {
+            const bingo_status st = sq_launch(g, s);
+            if (st != BINGO_OK) return st;
+            q = (StreamQ *)g->sq_host;
+        }
+        const unsigned gen = g->sq_gen;
+        StreamSlot *sl = &q->slot[k % SQ_N];
+        memcpy((void *)&sl->rec, rec, 16);
+        __atomic_store_n(&sl->gen, gen, __ATOMIC_SEQ_CST);
+        __atomic_store_n(&sl->seq, k + 1, __ATOMIC_SEQ_CST);
+        bool taken = false;
+        for (uint64_t spin = 0;; spin++) {
+            if (__atomic_load_n(&q->done_seq, __ATOMIC_ACQUIRE) == k + 1) {
+                taken = true;
+                break;
+            }
+            if (__atomic_load_n(&q->exit_gen, __ATOMIC_ACQUIRE) == gen &&
+                __atomic_load_n(&q->exit_seq, __ATOMIC_ACQUIRE) == k &&
+                __atomic_load_n(&q->done_seq, __ATOMIC_ACQUIRE) != k + 1) {
+                g->sq_running = false;   // idle exit raced with the post: relaunch and repost
+                break;
+            }
+            if ((spin & 0xFFFFF) == 0xFFFFF) {   // a dead context must not spin forever
+                const cudaError_t e = cudaStreamQuery(s);
+                if (e != cudaSuccess && e != cudaErrorNotReady) return upd_cuda_fail(g, e, "k_stream_upd");
+            }
+        }
+        if (taken) break;
+        if (attempt > 1000) return upd_cuda_fail(g, cudaErrorUnknown, "streaming queue");
+    }
+    g->sq_seq = k + 1;
+    const FastOut &o = q->out;
+    const uint32_t st = __atomic_load_n(&o.status, __ATOMIC_ACQUIRE);
+    if (st == FAST_INVAL) return BINGO_E_INVAL;
+    if (st == FAST_OVERFLOW) return BINGO_E_OVERFLOW;
+    if (st == FAST_SLOW) {   // the kernel has exited; this record goes through the batched pipeline
+        g->sq_running = false;
+        return apply_impl(g, rec, nullptr, 1, BINGO_UPD_HOST_BATCH, stats, stream);
+    }
+    if (st != FAST_OK) return upd_cuda_fail(g, cudaErrorUnknown, "k_stream_upd status");
+    g->epoch++;
+    const uint64_t deleted = o.stats[0];
+    g->num_arcs = g->num_arcs + o.inserted - deleted;
+    if (stats) {
+        stats->inserted = o.inserted;
+        stats->deleted = deleted;
+        stats->missing_deletes = o.stats[1];
+        stats->touched_vertices = o.ntouch;
+        for (int i = 0; i < 25; i++) stats->kind_transitions[i / 5][i % 5] = o.stats[2 + i];
+        stats->epoch = g->epoch;
+    }
+    return BINGO_OK;
 }

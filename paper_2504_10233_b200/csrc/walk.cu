@@ -354,6 +354,7 @@ extern "C" bingo_status bingo_walk(bingo_graph *g, const bingo_walk_desc *desc, 
                                    void *stream) {
     if (!g || !desc) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
+    bingo_sq_quiesce(g, (cudaStream_t)stream);
     if (desc->app > BINGO_PPR) return BINGO_E_INVAL;
     if (desc->app == BINGO_NODE2VEC && !(desc->p > 0 && desc->q > 0)) return BINGO_E_INVAL;
     if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
@@ -438,6 +439,7 @@ extern "C" bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc
                                            uint64_t *counters_host, void *stream) {
     if (!g || !desc || !counters_host) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
+    bingo_sq_quiesce(g, (cudaStream_t)stream);
     if (desc->app > BINGO_PPR || (desc->flags & BINGO_WALK_HOST_OUTPUT)) return BINGO_E_INVAL;
     if (desc->app == BINGO_NODE2VEC && !(desc->p > 0 && desc->q > 0)) return BINGO_E_INVAL;
     if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
@@ -473,6 +475,7 @@ extern "C" bingo_status bingo_walk_trace(bingo_graph *g, const bingo_walk_desc *
                                          uint64_t n_records, uint64_t *counters_host, void *stream) {
     if (!g || !desc || !counters_host || !rec_off || !trace) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
+    bingo_sq_quiesce(g, (cudaStream_t)stream);
     if (!(desc->app == BINGO_DEEPWALK || desc->app == BINGO_PPR) || desc->flags || g->float_mode) return BINGO_E_INVAL;
     if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
     if (desc->length == BINGO_NO_CAP && desc->app != BINGO_PPR) return BINGO_E_INVAL;
@@ -564,6 +567,7 @@ extern "C" bingo_status bingo_walk_replay(bingo_graph *g, const void *trace, con
                                           uint32_t num_walkers, uint32_t flags, uint64_t *counts_host, void *stream) {
     if (!g || !trace || !rec_off || !counts_host) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
+    bingo_sq_quiesce(g, (cudaStream_t)stream);
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long *dc = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * 8);
     if (!dc) return BINGO_E_NOMEM;
@@ -612,6 +616,7 @@ __global__ void k_visit_gather(uint32_t V, const uint32_t *__restrict__ inv, con
 extern "C" bingo_status bingo_visit_counts(bingo_graph *g, uint64_t *counts, int reset, uint32_t flags, void *stream) {
     if (!g) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
+    bingo_sq_quiesce(g, (cudaStream_t)stream);
     cudaStream_t s = (cudaStream_t)stream;
     cudaError_t e = cudaSuccess;
     const size_t bytes = sizeof(uint64_t) * g->V;

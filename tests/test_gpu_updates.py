@@ -378,3 +378,64 @@ def test_single_records_on_a_vertex_above_the_fast_path_handoff():
     out = g.walk(length=30, seed=3, num_walkers=2000)
     ref = o.walk(length=30, seed=3, num_walkers=2000)
     assert np.array_equal(u32(out["paths"]), ref["paths"])
+
+
+def test_streaming_queue_single_records():
+    """f2: records applied one at a time through the persistent device-side queue
+    (bingo_stream_update) equal the oracle after every record -- statistics each time, full
+    dumps at checkpoints -- with walks, batched updates, stream synchronisation (idle exit),
+    invalid records and records that need the batched pipeline interleaved."""
+    import time
+    import torch
+    pb = _pb()
+    w = synth.make_workload("c1", rounds=3)
+    g, o = _pair(w.row_offsets, w.dst, w.bias)
+    recs = np.concatenate([w.batches[0][:300], w.batches[1][:100]])
+    for i, r in enumerate(recs):
+        sg = g.stream_update(r)
+        so = o.apply_updates(r[None, :])
+        _same_stats(sg, so)
+        if i in (50, 149, 250):
+            _same(g, o, w.V, f"after streaming record {i}")
+            out = g.walk(length=20, seed=i, num_walkers=500)          # quiesces the queue
+            ref = o.walk(length=20, seed=i, num_walkers=500)
+            assert np.array_equal(u32(out["paths"]), ref["paths"])
+        if i == 100:
+            torch.cuda.synchronize()                                  # waits for the idle exit
+            time.sleep(0.005)
+        if i == 200:
+            b = w.batches[2][:400]                                    # a batched update in between
+            _same_stats(g.apply_updates(b), o.apply_updates(b))
+        if i == 300:
+            with pytest.raises(pb.bingo.BingoError):
+                g.stream_update(np.array([0, w.V, 1, 1], dtype=np.uint32))
+            with pytest.raises(pb.bingo.BingoError):
+                g.stream_update(np.array([0, 1, 2, 0], dtype=np.uint32))
+    _same(g, o, w.V, "end")
+    assert g.info()["epoch"] == o.epoch
+
+
+def test_streaming_queue_hub_handoff_and_pool_growth():
+    """Records the single-warp path cannot take (a vertex above 8192 arcs, pool growth) leave
+    the queue for the batched pipeline and come back."""
+    rng = np.random.default_rng(21)
+    V = 64
+    deg = rng.integers(0, 20, size=V)
+    deg[7] = 9000
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    dst = rng.integers(0, V, size=int(ro[-1])).astype(np.uint32)
+    bias = rng.integers(1, 3000, size=int(ro[-1])).astype(np.uint32)
+    pb = _pb()
+    g = pb.Graph(ro, dst, bias, arc_slack=0.0, member_slack=0.0, pool_reserve=0.0)
+    o = oracle.OracleGraph(ro, dst, bias)
+    hub = [int(x) for x in dst[int(ro[7]):int(ro[8])]]
+    for i in range(200):
+        u = 7 if i % 5 == 0 else int(rng.integers(0, V))
+        if rng.random() < 0.6:
+            r = np.array([0, u, int(rng.integers(0, V)), int(rng.integers(1, 1 << 16))], dtype=np.uint32)
+        else:
+            v = hub[int(rng.integers(0, len(hub)))] if u == 7 else int(rng.integers(0, V))
+            r = np.array([1, u, v, 0], dtype=np.uint32)
+        _same_stats(g.stream_update(r), o.apply_updates(r[None, :]))
+    _same(g, o, V)

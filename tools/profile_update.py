@@ -17,9 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--batches", type=int, default=5)
 ap.add_argument("--single", type=int, default=0, help="also time this many single-record updates")
-ap.add_argument("--gen", default="cpu", help="workload generator device (cuda for c3-c5)")
+ap.add_argument("--gen", default="resident", help="cpu | cuda | resident (generated and kept in HBM, as bench.py)")
 a = ap.parse_args()
-w = synth.make_workload(a.config, rounds=a.batches + 1, device=a.gen)
+if a.gen == "resident":
+    w = synth.make_workload(a.config, rounds=a.batches + 1, hold_rounds=10, device="cuda", resident=True)
+else:
+    w = synth.make_workload(a.config, rounds=a.batches + 1, device=a.gen)
 torch.cuda.empty_cache()
 g = pb.Graph(w.row_offsets, w.dst, w.bias)
 db = [torch.from_numpy(b.view(np.int32)).cuda() for b in w.batches]
