@@ -299,6 +299,27 @@ bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc *desc, con
                                 uint32_t num_walkers, uint32_t *paths_or_null, uint32_t *lengths_or_null,
                                 uint64_t *counters_host, void *stream);
 
+/* bingo_walk_partition -- one round of the 1-D partitioned walk with walker transfer
+ * (SURVEY f3).  The graph g is this rank's partition: built over the full vertex
+ * id space with only the arcs of the vertices it owns, the external ids in
+ * [bounds[me], bounds[me + 1]) (bounds: DEVICE u32 [parts + 1], ascending, bounds[0] = 0).
+ * inbox: DEVICE records {walker id, current vertex (external id), steps taken, flags bit 0 =
+ * fresh} of n_in walkers standing on owned vertices; a fresh walker writes path entry 0 and
+ * (PPR) counts its start.  Each walker takes steps exactly as bingo_walk would (same
+ * counters, same results) while its vertex is owned; one that steps onto another rank's
+ * vertex is appended to outbox[owner * out_cap + k] (DEVICE, 16 B records, out_cap >= n_in;
+ * out_count[owner] DEVICE u32, zeroed by the caller, counts them) with its steps so far.
+ * Paths / lengths (DEVICE, layouts of bingo_walk for num_walkers walkers, index = walker id -
+ * desc->first_walker_id) receive the entries of the steps taken here; the rank where a
+ * walker finishes writes its length and sentinels.  PPR visit counts accumulate on the rank
+ * that took the step (sum them over ranks).  DeepWalk and PPR, integer biases.
+ * *finished_host: walkers that finished in this round.  Synchronises `stream`. */
+bingo_status bingo_walk_partition(bingo_graph *g, const bingo_walk_desc *desc, uint32_t num_walkers,
+                                  const uint32_t *bounds, uint32_t parts, uint32_t me, const void *inbox,
+                                  uint32_t n_in, void *outbox, uint64_t out_cap, uint32_t *out_count,
+                                  uint32_t *paths_or_null, uint32_t *lengths_or_null, uint64_t *finished_host,
+                                  void *stream);
+
 /* bingo_walk_trace / bingo_walk_replay -- measurement only (the walk's roofline,
  * DESIGN.md 6.1): the "achievable random-gather bandwidth" for the walk's own footprint and
  * skew.  bingo_walk_trace runs the same walks as bingo_walk (DeepWalk or PPR, integer

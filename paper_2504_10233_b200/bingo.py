@@ -34,7 +34,7 @@ NO_CAP = 0xFFFFFFFF
 ABI_SYMBOLS = ("bingo_build", "bingo_destroy", "bingo_apply_updates", "bingo_apply_updates_f64", "bingo_walk",
                "bingo_visit_counts",
                "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str", "bingo_walk_profile",
-               "bingo_walk_trace", "bingo_walk_replay", "bingo_stream_update")
+               "bingo_walk_trace", "bingo_walk_replay", "bingo_stream_update", "bingo_walk_partition")
 
 
 class BingoError(RuntimeError):
@@ -110,6 +110,9 @@ def _lib():
         L.bingo_get_info.restype = ctypes.c_int
         L.bingo_walk_profile.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, P, P]
         L.bingo_walk_profile.restype = ctypes.c_int
+        L.bingo_walk_partition.argtypes = [P, ctypes.POINTER(WalkDesc), u32, P, u32, u32, P, u32, P, u64, P, P, P,
+                                           P, P]
+        L.bingo_walk_partition.restype = ctypes.c_int
         L.bingo_stream_update.argtypes = [P, P, ctypes.POINTER(UpdateStats), P]
         L.bingo_stream_update.restype = ctypes.c_int
         L.bingo_walk_trace.argtypes = [P, ctypes.POINTER(WalkDesc), P, u32, P, P, u64, P, P]
@@ -400,6 +403,29 @@ class Graph:
         out["paths"] = pa
         out["lengths"] = ln
         return out
+
+    def walk_partition(self, bounds, me: int, inbox, outbox, out_count, app: int = DEEPWALK, length: int = 80,
+                       seed: int = 0, first_walker: int = 0, num_walkers: Optional[int] = None, stop=(1, 80),
+                       paths=None, lengths=None, stream=None) -> int:
+        """bingo_walk_partition: one round of the 1-D partitioned walk on this partition graph.
+        bounds: int32 CUDA tensor [parts + 1]; inbox: int32 CUDA [n, 4]; outbox: int32 CUDA
+        [parts, cap, 4] (cap >= n); out_count: int32 CUDA [parts], zeroed.  Returns the number of
+        walkers that finished here."""
+        torch = _torch()
+        W = num_walkers if num_walkers is not None else self.V
+        n = inbox.shape[0]
+        parts = bounds.numel() - 1
+        d = WalkDesc(app=app, length=length, p=1.0, q=1.0, stop_num=stop[0], stop_den=stop[1], seed=seed,
+                     first_walker_id=first_walker, flags=0)
+        fin = ctypes.c_uint64(0)
+        _order_on(stream, self.device, bounds, inbox, outbox, out_count, paths, lengths)
+        with torch.cuda.device(self.device):
+            _check(_lib().bingo_walk_partition(
+                self._h, ctypes.byref(d), W, bounds.data_ptr(), parts, me, inbox.data_ptr() if n else None, n,
+                outbox.data_ptr(), outbox.shape[1], out_count.data_ptr(),
+                paths.data_ptr() if paths is not None else None, lengths.data_ptr() if lengths is not None else None,
+                ctypes.byref(fin), _stream_ptr(stream)), "bingo_walk_partition")
+        return int(fin.value)
 
     def walk_trace(self, rec_off, trace, app: int = DEEPWALK, length: int = 80, seed: int = 0,
                    first_walker: int = 0, num_walkers: Optional[int] = None, stop=(1, 80), stream=None) -> dict:

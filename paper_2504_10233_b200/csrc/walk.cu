@@ -607,6 +607,177 @@ extern "C" bingo_status bingo_walk_replay(bingo_graph *g, const void *trace, con
     return BINGO_OK;
 }
 
+// ---------------------------------------------------------------- 1-D partitioned walk
+// The paper's multi-GPU design (after KnightKing): the graph is partitioned by
+// vertex (each rank builds its graph over the full id space with only its own vertices'
+// arcs) and WALKERS move to the rank that owns their current vertex.  One launch advances
+// every walker of the inbox while it stays on owned vertices; a walker that steps onto a
+// vertex another rank owns is written to that rank's outbox region and leaves.  Because
+// every draw is keyed by (walker, step) (R-1), the partitioned walk takes exactly the
+// single-GPU walk's steps, and the exchange order does not matter.
+struct PartArgs {
+    WalkArgs a;                       // graph, RNG, thresholds; paths / lengths indexed by i = w - first
+    const uint4 *inbox;               // {walker id, current vertex (external), steps taken, fresh}
+    uint32_t n_in;
+    uint4 *outbox;                    // [parts][cap]
+    unsigned long long cap;
+    uint32_t *out_count;              // [parts] (pre-zeroed)
+    const uint32_t *bounds;           // [parts + 1] owned external-id ranges
+    uint32_t parts, me;
+    unsigned long long *done;         // walkers that finished here
+};
+
+__device__ __forceinline__ uint32_t part_owner(const PartArgs &p, uint32_t x) {
+    uint32_t r = 0;
+    while (r + 1 < p.parts && x >= __ldg(p.bounds + r + 1)) r++;
+    return r;
+}
+
+template <int APP>
+__global__ void __launch_bounds__(BINGO_WALK_TPB) k_walk_part(const PartArgs p, unsigned long long *__restrict__ claim) {
+    const WalkArgs &a = p.a;
+    uint64_t pol_keep, pol_stream;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    const Policies pol{pol_keep, pol_stream};
+    WalkProf prof;
+    const uint32_t lane = threadIdx.x & 31u;
+    unsigned long long fin_here = 0;
+    for (;;) {
+        unsigned long long j0 = 0;
+        if (lane == 0) j0 = atomicAdd(claim, 32ull);
+        j0 = __shfl_sync(0xffffffffu, j0, 0);
+        if (j0 >= p.n_in) break;
+        const unsigned long long j = j0 + lane;
+        if (j < p.n_in) {   // the warp reconverges before its next claim
+        const uint4 rec = p.inbox[j];
+        const uint32_t w = rec.x;
+        const uint64_t i = (uint64_t)(w - a.first_walker);
+        uint32_t t = rec.z;
+        uint32_t ux = rec.y;                                  // external id of the current vertex
+        uint32_t u = a.inv ? __ldg(a.inv + ux) : ux;
+        if (rec.w & 1u) {                                     // fresh walker: its start vertex is ours
+            if (a.paths) __stcs(&a.paths[i], ux);
+            if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
+        }
+        bool finished = false;
+        for (;;) {
+            if (a.L != BINGO_NO_CAP && t >= a.L) { finished = true; break; }
+            const ThinHdr h = load_thdr(a.thdr + u, pol);
+            if (h.n == 0) { finished = true; break; }      // an owned dead end (d = 0): truncate (R-13)
+            const uint32_t next = sample_dst<false>(a, h, w, t, 0u, prof, pol);
+            const uint32_t nx = a.perm ? __ldg(a.perm + next) : next;
+            if (a.paths) __stcs(&a.paths[(size_t)(t + 1) * a.W + i], nx);
+            bool stop = false;
+            if (APP == BINGO_PPR) {
+                if (a.visit) atomicAdd(&a.visit[visit_slot(next)], 1ull);
+                if (a.stop_always) {
+                    stop = true;
+                } else {
+                    const P4 r = philox10(w, t, 0u, 3u, a.k0, a.k1);
+                    stop = join64(r.x, r.y) < a.stop_thr;
+                }
+            }
+            t++;
+            if (stop) { finished = true; break; }
+            const uint32_t o = part_owner(p, nx);
+            if (o != p.me) {                                  // leaves for the owner of its new vertex
+                const unsigned long long pos = atomicAdd(&p.out_count[o], 1u);
+                if (pos < p.cap) p.outbox[(unsigned long long)o * p.cap + pos] = make_uint4(w, nx, t, 0u);
+                break;
+            }
+            u = next;
+        }
+        if (finished) {
+            fin_here++;
+            if (a.lengths) a.lengths[i] = t;
+            if (a.paths && a.L != BINGO_NO_CAP)
+                for (uint32_t s2 = t + 1; s2 <= a.L; s2++) __stcs(&a.paths[(size_t)s2 * a.W + i], 0xFFFFFFFFu);
+        }
+        }
+        __syncwarp();
+    }
+    const unsigned long long f = warp_sum(fin_here);
+    if (lane == 0 && f) atomicAdd(p.done, f);
+}
+
+extern "C" bingo_status bingo_walk_partition(bingo_graph *g, const bingo_walk_desc *desc, uint32_t num_walkers,
+                                             const uint32_t *bounds, uint32_t parts, uint32_t me, const void *inbox,
+                                             uint32_t n_in, void *outbox, uint64_t out_cap, uint32_t *out_count,
+                                             uint32_t *paths_or_null, uint32_t *lengths_or_null,
+                                             uint64_t *finished_host, void *stream) {
+    if (!g || !desc || !bounds || !out_count || (n_in && !inbox) || !outbox || parts == 0 || me >= parts ||
+        !finished_host || out_cap < n_in)
+        return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    bingo_sq_quiesce(g, (cudaStream_t)stream);
+    if (!(desc->app == BINGO_DEEPWALK || desc->app == BINGO_PPR) || g->float_mode) return BINGO_E_INVAL;
+    if (desc->flags || (desc->app == BINGO_PPR && desc->stop_den == 0)) return BINGO_E_INVAL;
+    if (desc->length == BINGO_NO_CAP && (paths_or_null || desc->app != BINGO_PPR)) return BINGO_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    PartArgs p;
+    memset(&p, 0, sizeof(p));
+    WalkArgs &a = p.a;
+    a.thdr = g->thdr;
+    a.hdr = g->hdr;
+    a.bkt = g->bkt;
+    a.arc = g->arc;
+    a.mdst = g->mdst;
+    a.visit = g->visit;
+    a.perm = g->perm;
+    a.inv = g->inv;
+    a.paths = paths_or_null;
+    a.lengths = lengths_or_null;
+    a.W = num_walkers;
+    a.V = g->V;
+    a.L = desc->length;
+    a.first_walker = desc->first_walker_id;
+    a.k0 = (uint32_t)desc->seed;
+    a.k1 = (uint32_t)(desc->seed >> 32);
+    stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
+    p.inbox = reinterpret_cast<const uint4 *>(inbox);
+    p.n_in = n_in;
+    p.outbox = reinterpret_cast<uint4 *>(outbox);
+    p.cap = out_cap;
+    p.out_count = out_count;
+    p.bounds = bounds;
+    p.parts = parts;
+    p.me = me;
+    unsigned long long *dc = (unsigned long long *)bingo_dev_alloc(g, 2 * sizeof(unsigned long long));
+    if (!dc) return BINGO_E_NOMEM;
+    p.done = dc + 1;
+    cudaError_t e = cudaMemsetAsync(dc, 0, 2 * sizeof(unsigned long long), s);
+    if (e == cudaSuccess && n_in) {
+        int dev = 0, sms = 148, per_sm = 1;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (desc->app == BINGO_PPR) {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk_part<BINGO_PPR>, BINGO_WALK_TPB, 0);
+            const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_in + BINGO_WALK_TPB - 1) / BINGO_WALK_TPB,
+                                                                                      (uint64_t)sms * std::max(per_sm, 1)));
+            k_walk_part<BINGO_PPR><<<grid, BINGO_WALK_TPB, 0, s>>>(p, dc);
+        } else {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk_part<BINGO_DEEPWALK>, BINGO_WALK_TPB, 0);
+            const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>((n_in + BINGO_WALK_TPB - 1) / BINGO_WALK_TPB,
+                                                                                      (uint64_t)sms * std::max(per_sm, 1)));
+            k_walk_part<BINGO_DEEPWALK><<<grid, BINGO_WALK_TPB, 0, s>>>(p, dc);
+        }
+        bingo_count_launch();
+        e = cudaGetLastError();
+    }
+    unsigned long long fh = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&fh, dc + 1, 8, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    *finished_host = fh;
+    bingo_dev_free(g, dc);
+    if (e != cudaSuccess) {
+        fprintf(stderr, "libbingo: partitioned walk failed: %s\n", cudaGetErrorString(e));
+        g->poisoned = 1;
+        return BINGO_E_CUDA;
+    }
+    return BINGO_OK;
+}
+
 // counts in external vertex order: out[u] = visit[inv[u]]
 __global__ void k_visit_gather(uint32_t V, const uint32_t *__restrict__ inv, const unsigned long long *__restrict__ visit,
                                unsigned long long *__restrict__ out) {

@@ -7,9 +7,12 @@ depends only on the graph and its own Philox stream keyed by its global id
 (R-1), so giving rank r the id range [first_r, first_r + count_r) reproduces the
 single-GPU run bit for bit.  Every rank applies every update batch (replicas
 stay identical because bingo_apply_updates is deterministic); replica equality
-is checkable with `replica_digest`.  The paper's own multi-GPU design (1-D
-partitioning with walker transfer) was never evaluated; it is the
-NEXT item f3 in DESIGN.md.
+is checkable with `replica_digest`.
+
+For graphs larger than one GPU, `PartitionedBingo` is the paper's own multi-GPU
+design (1-D partitioning with walker transfer): each rank
+holds only its vertex range's arcs and walkers move, over NCCL all-to-all, to the
+rank that owns their current vertex; the walks are still the single-GPU walks.
 
 Collectives go through torch.distributed (NCCL over NVLink on B200; gloo for
 the CPU tests of this module's logic).  The engine is a `bingo.Graph` (or any
@@ -116,3 +119,148 @@ class ReplicatedBingo:
         allv = [torch.zeros_like(t) for _ in range(self.world)]
         dist.all_gather(allv, t, group=self.group)
         return all(int(x.item()) == int(t.item()) for x in allv)
+
+
+# ---------------------------------------------------------------- 1-D partitioning
+def partition_bounds(row_offsets, parts: int) -> list:
+    """Contiguous external-id ranges [b_r, b_{r+1}) holding about the same number of arcs
+    (1-D partitioning; KnightKing balances by edges too)."""
+    import numpy as np
+    ro = np.asarray(row_offsets.cpu() if isinstance(row_offsets, torch.Tensor) else row_offsets).astype(np.int64)
+    V = len(ro) - 1
+    A = int(ro[-1])
+    b = [0]
+    for r in range(1, parts):
+        b.append(int(min(max(np.searchsorted(ro, A * r // parts, side="left"), b[-1]), V)))
+    b.append(V)
+    return b
+
+
+def partition_csr(row_offsets, dst, bias, v0: int, v1: int):
+    """This rank's partition graph: the full vertex-id space, arcs only for rows [v0, v1)."""
+    is_t = isinstance(row_offsets, torch.Tensor)
+    if is_t:
+        ro = row_offsets.to(torch.int64)
+        a0, a1 = int(ro[v0]), int(ro[v1])
+        lro = torch.clamp(ro - a0, min=0, max=a1 - a0)
+        return lro, dst[a0:a1], bias[a0:a1]
+    import numpy as np
+    ro = np.asarray(row_offsets, dtype=np.int64)
+    a0, a1 = int(ro[v0]), int(ro[v1])
+    lro = np.clip(ro - a0, 0, a1 - a0).astype(np.uint64)
+    return lro, np.asarray(dst)[a0:a1], np.asarray(bias)[a0:a1]
+
+
+def fresh_inbox(bounds, me: int, num_walkers: int, first_walker: int, V: int, device) -> torch.Tensor:
+    """The walkers whose start vertex ((first + i) mod V) this rank owns: {id, start, 0, fresh}."""
+    ids = torch.arange(num_walkers, dtype=torch.int64, device=device) + first_walker
+    st = ids % V
+    mine = (st >= bounds[me]) & (st < bounds[me + 1])
+    ids, st = ids[mine], st[mine]
+    out = torch.zeros((ids.numel(), 4), dtype=torch.int32, device=device)
+    out[:, 0] = ids.to(torch.int32)
+    out[:, 1] = st.to(torch.int32)
+    out[:, 3] = 1
+    return out
+
+
+class PartitionedBingo:
+    """One rank of the 1-D partitioned walk with walker transfer.
+
+    `engine` is this rank's partition graph (a bingo.Graph built from partition_csr, or any
+    object with walk_partition / visit_counts); `bounds` the P + 1 range boundaries.  A walk
+    runs in rounds: every rank advances the walkers on its vertices until they leave
+    (bingo_walk_partition), then the leaving walkers are exchanged with ONE all-to-all per
+    round; rounds repeat until no walker is left anywhere (an all-reduce of the count).
+    Every draw is keyed by (walker, step), so paths, lengths and visit counts equal the
+    single-GPU walk's: paths / lengths are assembled by a sum over ranks (each entry is
+    written by exactly one rank), PPR counts by the usual all-reduce."""
+
+    def __init__(self, engine, bounds, device=None, group=None):
+        self.g = engine
+        self.group = group
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        assert len(bounds) == self.world + 1
+        self.bounds_list = list(bounds)
+        self.device = device if device is not None else getattr(engine, "device", torch.device("cpu"))
+        self.bounds = torch.tensor(bounds, dtype=torch.int32, device=self.device)
+        self.rounds = 0
+
+    def _exchange(self, outbox: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
+        send_counts = counts.to(torch.int64)
+        recv_counts = torch.zeros_like(send_counts)
+        dist.all_to_all_single(recv_counts, send_counts, group=self.group)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        send = torch.cat([outbox[d, :sc[d]] for d in range(self.world)]) if sum(sc) else \
+            torch.zeros((0, 4), dtype=torch.int32, device=self.device)
+        recv = torch.empty((sum(rc), 4), dtype=torch.int32, device=self.device)
+        dist.all_to_all_single(recv, send, rc, sc, group=self.group)
+        return recv
+
+    def walk(self, num_walkers: int, app: int = 0, length: int = 80, seed: int = 0, first_walker: int = 0,
+             stop=(1, 80), paths: bool = True, max_rounds: int = 1 << 20) -> dict:
+        V = self.bounds_list[-1]
+        W = num_walkers
+        no_cap = length == 0xFFFFFFFF
+        pa = torch.zeros((length + 1, W), dtype=torch.int32, device=self.device) if (paths and not no_cap) else None
+        ln = torch.zeros(W, dtype=torch.int32, device=self.device)
+        inbox = fresh_inbox(self.bounds_list, self.rank, W, first_walker, V, self.device)
+        finished = 0
+        self.rounds = 0
+        for _ in range(max_rounds):
+            n = inbox.shape[0]
+            outbox = torch.empty((self.world, max(n, 1), 4), dtype=torch.int32, device=self.device)
+            cnt = torch.zeros(self.world, dtype=torch.int32, device=self.device)
+            finished += self.g.walk_partition(self.bounds, self.rank, inbox, outbox, cnt, app=app, length=length,
+                                              seed=seed, first_walker=first_walker, num_walkers=W, stop=stop,
+                                              paths=pa, lengths=ln)
+            self.rounds += 1
+            inbox = self._exchange(outbox, cnt) if self.world > 1 else outbox[0, :int(cnt[0])]
+            left = torch.tensor([inbox.shape[0]], dtype=torch.int64, device=self.device)
+            if self.world > 1:
+                dist.all_reduce(left, group=self.group)
+            if int(left) == 0:
+                break
+        if self.world > 1:
+            dist.all_reduce(ln, group=self.group)
+            if pa is not None:
+                dist.all_reduce(pa, group=self.group)
+        return {"paths": pa, "lengths": ln, "rounds": self.rounds}
+
+    def visit_counts(self, reset: bool = False) -> torch.Tensor:
+        c = self.g.visit_counts(reset=reset)
+        if self.world > 1:
+            dist.all_reduce(c, op=dist.ReduceOp.SUM, group=self.group)
+        return c
+
+
+def walk_partitions_local(engines, bounds, num_walkers: int, app: int = 0, length: int = 80, seed: int = 0,
+                          first_walker: int = 0, stop=(1, 80), paths: bool = True, device=None) -> dict:
+    """The same rounds with every partition in THIS process (e.g. several partition graphs on
+    one GPU): the all-to-all becomes a regrouping of the outboxes; paths and lengths are
+    shared buffers (each entry written by exactly one partition)."""
+    P = len(engines)
+    device = device if device is not None else engines[0].device
+    bt = torch.tensor(bounds, dtype=torch.int32, device=device)
+    V = bounds[-1]
+    W = num_walkers
+    no_cap = length == 0xFFFFFFFF
+    pa = torch.zeros((length + 1, W), dtype=torch.int32, device=device) if (paths and not no_cap) else None
+    ln = torch.zeros(W, dtype=torch.int32, device=device)
+    inbox = [fresh_inbox(bounds, r, W, first_walker, V, device) for r in range(P)]
+    rounds = 0
+    while any(x.shape[0] for x in inbox):
+        nxt = [[] for _ in range(P)]
+        for r in range(P):
+            n = inbox[r].shape[0]
+            outbox = torch.empty((P, max(n, 1), 4), dtype=torch.int32, device=device)
+            cnt = torch.zeros(P, dtype=torch.int32, device=device)
+            engines[r].walk_partition(bt, r, inbox[r], outbox, cnt, app=app, length=length, seed=seed,
+                                      first_walker=first_walker, num_walkers=W, stop=stop, paths=pa, lengths=ln)
+            for d, c in enumerate(cnt.tolist()):
+                if c:
+                    nxt[d].append(outbox[d, :c])
+        inbox = [torch.cat(x) if x else torch.zeros((0, 4), dtype=torch.int32, device=device) for x in nxt]
+        rounds += 1
+    return {"paths": pa, "lengths": ln, "rounds": rounds}
