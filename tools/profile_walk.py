@@ -17,9 +17,12 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--walks", type=int, default=2)
 ap.add_argument("--app", default="deepwalk")
-ap.add_argument("--gen", default="cpu", help="workload generator device (cuda: minutes faster for c3/c4)")
+ap.add_argument("--gen", default="resident", help="cpu | cuda | resident (generated and kept in HBM, as bench.py)")
 a = ap.parse_args()
-w = synth.make_workload(a.config, rounds=2, device=a.gen)
+if a.gen == "resident":
+    w = synth.make_workload(a.config, rounds=2, hold_rounds=10, device="cuda", resident=True)
+else:
+    w = synth.make_workload(a.config, rounds=2, device=a.gen)
 torch.cuda.empty_cache()
 g = pb.Graph(w.row_offsets, w.dst, w.bias, neighbor_index=("node2vec" in a.app))
 for b in w.batches:
