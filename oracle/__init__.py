@@ -79,6 +79,14 @@ def lib():
             L.ora_dump.argtypes = [P, P, ctypes.c_size_t]
             L.ora_dump.restype = ctypes.c_size_t
             L.ora_digests.argtypes = [P, P]
+            L.ora_build_radix.argtypes = [u32, P, P, P, u32, ctypes.POINTER(P)]
+            L.ora_build_radix.restype = ctypes.c_int
+            L.ora_radix_free.argtypes = [P]
+            L.ora_radix_sample.argtypes = [P, u32, u64, u32, u32]
+            L.ora_radix_sample.restype = u32
+            L.ora_radix_walk.argtypes = [P, u32, u32, u64, u32, P, u32, P, P, P, u64, u32, ctypes.c_int]
+            L.ora_radix_dump.argtypes = [P, P, ctypes.c_size_t]
+            L.ora_radix_dump.restype = ctypes.c_size_t
             _lib = L
     return _lib
 
@@ -278,5 +286,82 @@ def parse_dump(buf: bytes, V: int, float_mode: bool = False) -> list:
             dc = u32()
             v["dec"] = [(u32(), u64()) for _ in range(dc)]
         out.append(v)
+    assert pos == len(buf), (pos, len(buf))
+    return out
+
+
+class RadixGraph:
+    """The arbitrary-radix-base structure (base B = 2^b, reading R-17): static
+    build + sampling; DeepWalk and PPR walks."""
+
+    def __init__(self, row_offsets, dst, bias, b: int):
+        L = lib()
+        self.V = len(row_offsets) - 1
+        self.b = b
+        ro = np.ascontiguousarray(row_offsets, dtype=np.uint64)
+        ds = np.ascontiguousarray(dst, dtype=np.uint32)
+        bs = np.ascontiguousarray(bias, dtype=np.uint32)
+        h = ctypes.c_void_p()
+        rc = L.ora_build_radix(self.V, _p(ro), _p(ds), _p(bs), b, ctypes.byref(h))
+        if rc != 0:
+            raise ValueError(f"ora_build_radix failed with status {rc}")
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib().ora_radix_free(h)
+            self._h = None
+
+    def sample(self, u, seed, w, t) -> int:
+        return int(lib().ora_radix_sample(self._h, u, seed, w, t))
+
+    def walk(self, app=APP_DEEPWALK, length=80, seed=0, first_walker=0, starts=None, num_walkers=None,
+             stop=(1, 80), paths=True, counts=False, threads=0):
+        W = num_walkers if num_walkers is not None else (len(starts) if starts is not None else self.V)
+        st = np.ascontiguousarray(starts, dtype=np.uint32) if starts is not None else None
+        pa = np.zeros(((length + 1), W), dtype=np.uint32) if (paths and length != NONE) else None
+        ln = np.zeros(W, dtype=np.uint32)
+        cn = np.zeros(self.V, dtype=np.uint64) if counts else None
+        sthr, salw = stop_threshold(*stop)
+        lib().ora_radix_walk(self._h, app, length, seed, first_walker, _p(st), W, _p(pa), _p(ln), _p(cn), sthr, salw,
+                             threads)
+        return {"paths": pa, "lengths": ln, "counts": cn}
+
+    def dump(self) -> bytes:
+        n = lib().ora_radix_dump(self._h, None, 0)
+        buf = np.zeros(max(n, 1), dtype=np.uint8)
+        lib().ora_radix_dump(self._h, _p(buf), n)
+        return buf[:n].tobytes()
+
+
+def parse_radix_dump(buf: bytes, V: int) -> list:
+    """Parse the radix canonical dump (R-18) into per-vertex dicts (test helper)."""
+    mv = memoryview(buf)
+    pos = 0
+
+    def u32():
+        nonlocal pos
+        v = int.from_bytes(mv[pos:pos + 4], "little")
+        pos += 4
+        return v
+
+    def u64():
+        nonlocal pos
+        v = int.from_bytes(mv[pos:pos + 8], "little")
+        pos += 8
+        return v
+    out = []
+    for _ in range(V):
+        d, n = u32(), u32()
+        groups = []
+        for _ in range(n):
+            i, thr, al, ns = u32(), u64(), u32(), u32()
+            subs = []
+            for _ in range(ns):
+                j, c, sthr, sal = u32(), u32(), u64(), u32()
+                subs.append({"j": j, "c": c, "thr": sthr, "alias": sal, "mem": [u32() for _ in range(c)]})
+            groups.append({"i": i, "thr": thr, "alias": al, "subs": subs})
+        out.append({"d": d, "groups": groups, "T": u64()})
     assert pos == len(buf), (pos, len(buf))
     return out

@@ -1036,3 +1036,234 @@ size_t ora_dump_vertex(const ora_graph *G, uint32_t u, uint8_t *buf, size_t cap)
     dump_vertex(vx(G, u), &o);
     return o.pos;
 }
+
+/* ------------------------------------------------------------------ */
+/* Arbitrary radix base B = 2^b (S "Bingo with Arbitrary Radix Bases", */
+/* P:910-928; reading R-17).  Static structure: build + sampling.      */
+/*   w = sum_i d_i B^i, digits d_i in [0, B).  Group B^i holds the arcs */
+/*   with d_i != 0, weight W_i = B^i sum_j j c_ij; inside it subgroup j */
+/*   holds the arcs with d_i = j (c_ij of them, ascending adjacency     */
+/*   index) -- the neighbours of a group no longer share one bias       */
+/*   (P:917), so a second, inter-subgroup alias over the weights        */
+/*   j c_ij picks the subgroup, then a member uniformly.    */
+/*   P(a) = sum_i (W_i/T)(d_i(a) c_{i,d_i(a)} B^i / W_i)(1/c_{i,d_i(a)}) */
+/*        = w(a)/T (Theorem 1, base B).  Both alias tables are the      */
+/*   integer Vose of R-4 (ora_alias_build).                             */
+/* ------------------------------------------------------------------ */
+typedef struct {
+    uint32_t j, c;
+    uint64_t thr;
+    uint32_t alias;
+    uint32_t *mem;            /* adjacency indices with digit j, ascending */
+} r_sub;
+
+typedef struct {
+    uint32_t i;               /* digit position: group B^i */
+    uint64_t W, S;            /* W = B^i S, S = sum_j j c_ij */
+    uint64_t thr;
+    uint32_t alias, ns;
+    r_sub *sub;
+} r_group;
+
+typedef struct {
+    uint32_t d, n;
+    const uint32_t *dst, *bias;
+    r_group *grp;
+    uint64_t T;
+} r_vertex;
+
+typedef struct ora_radix {
+    uint32_t V, b;
+    uint32_t *dst, *bias;     /* owned copies of the CSR arrays */
+    r_vertex *v;
+} ora_radix;
+
+static uint32_t digit(uint32_t w, uint32_t i, uint32_t b)
+{
+    const uint32_t sh = i * b;
+    return sh >= 32 ? 0u : (w >> sh) & ((1u << b) - 1u);
+}
+
+void ora_radix_free(ora_radix *G)
+{
+    if (!G) return;
+    for (uint32_t u = 0; u < G->V; u++) {
+        r_vertex *x = &G->v[u];
+        for (uint32_t g = 0; g < x->n; g++) {
+            for (uint32_t s = 0; s < x->grp[g].ns; s++) free(x->grp[g].sub[s].mem);
+            free(x->grp[g].sub);
+        }
+        free(x->grp);
+    }
+    free(G->v);
+    free(G->dst);
+    free(G->bias);
+    free(G);
+}
+
+/* b in [1, 5]: B = 2^b <= 32, so a group has at most 31 subgroups. */
+int ora_build_radix(uint32_t V, const uint64_t *ro, const uint32_t *dst, const uint32_t *bias, uint32_t b,
+                    ora_radix **out)
+{
+    if (b < 1 || b > 5) return O_EINVAL;
+    const uint32_t B = 1u << b, K = (32 + b - 1) / b;
+    ora_radix *G = (ora_radix *)calloc(1, sizeof(ora_radix));
+    const uint64_t A = ro[V];
+    G->V = V;
+    G->b = b;
+    G->dst = (uint32_t *)xrealloc(NULL, sizeof(uint32_t) * (A ? A : 1));
+    G->bias = (uint32_t *)xrealloc(NULL, sizeof(uint32_t) * (A ? A : 1));
+    memcpy(G->dst, dst, sizeof(uint32_t) * A);
+    memcpy(G->bias, bias, sizeof(uint32_t) * A);
+    G->v = (r_vertex *)calloc(V ? V : 1, sizeof(r_vertex));
+    for (uint32_t u = 0; u < V; u++) {
+        r_vertex *x = &G->v[u];
+        x->d = (uint32_t)(ro[u + 1] - ro[u]);
+        x->dst = G->dst + ro[u];
+        x->bias = G->bias + ro[u];
+        x->T = 0;
+        for (uint32_t a = 0; a < x->d; a++) {
+            if (x->bias[a] == 0) { ora_radix_free(G); return O_EINVAL; }
+            x->T += x->bias[a];
+        }
+        /* groups in ascending i, subgroups in ascending j */
+        x->grp = (r_group *)calloc(K, sizeof(r_group));
+        for (uint32_t i = 0; i < K; i++) {
+            uint32_t c[32] = {0};
+            for (uint32_t a = 0; a < x->d; a++) c[digit(x->bias[a], i, b)]++;
+            uint64_t S = 0;
+            uint32_t ns = 0;
+            for (uint32_t j = 1; j < B; j++) {
+                S += (uint64_t)j * c[j];
+                ns += c[j] ? 1u : 0u;
+            }
+            if (!ns) continue;
+            r_group *g = &x->grp[x->n++];
+            g->i = i;
+            g->S = S;
+            g->W = S << (i * b);          /* B^i S < 2^32 d: no overflow for d < 2^32 */
+            g->sub = (r_sub *)calloc(ns, sizeof(r_sub));
+            uint64_t sw[32];
+            for (uint32_t j = 1; j < B; j++) {
+                if (!c[j]) continue;
+                r_sub *sb = &g->sub[g->ns];
+                sb->j = j;
+                sb->c = c[j];
+                sb->mem = (uint32_t *)xrealloc(NULL, sizeof(uint32_t) * c[j]);
+                uint32_t k = 0;
+                for (uint32_t a = 0; a < x->d; a++)
+                    if (digit(x->bias[a], i, b) == j) sb->mem[k++] = a;
+                sw[g->ns] = (uint64_t)j * c[j];
+                g->ns++;
+            }
+            uint64_t thr[32];
+            uint32_t al[32];
+            ora_alias_build(g->ns, sw, thr, al);    /* inter-subgroup alias */
+            for (uint32_t s = 0; s < g->ns; s++) { g->sub[s].thr = thr[s]; g->sub[s].alias = al[s]; }
+        }
+        if (x->n) {
+            if ((unsigned __int128)x->T * x->n >= ((unsigned __int128)1 << 64)) { ora_radix_free(G); return O_EOVERFLOW; }
+            uint64_t W[32], thr[32];
+            uint32_t al[32];
+            for (uint32_t g = 0; g < x->n; g++) W[g] = x->grp[g].W;
+            ora_alias_build(x->n, W, thr, al);      /* inter-group alias (Eq.5) */
+            for (uint32_t g = 0; g < x->n; g++) { x->grp[g].thr = thr[g]; x->grp[g].alias = al[g]; }
+        }
+    }
+    *out = G;
+    return O_OK;
+}
+
+/* three-stage sample (R-17): tag 0 group (bucket, coin vs thr over T), tag 6 subgroup
+ * (bucket, coin vs thr over S_i), tag 1 member floor(X c / 2^64).  Returns the dst. */
+uint32_t ora_radix_sample(const ora_radix *G, uint32_t u, uint64_t seed, uint32_t w, uint32_t t)
+{
+    const r_vertex *x = &G->v[u];
+    if (x->d == 0) return O_NONE;
+    uint32_t r[4];
+    draw_oi(seed, w, t, 0, 0, 0, r);
+    uint32_t bk = (uint32_t)(((uint64_t)r[0] * x->n) >> 32);
+    uint64_t coin = mulhi64(((uint64_t)r[1] << 32) | r[2], x->T);
+    const r_group *g = &x->grp[coin < x->grp[bk].thr ? bk : x->grp[bk].alias];
+    draw_oi(seed, w, t, 0, 0, 6, r);
+    bk = (uint32_t)(((uint64_t)r[0] * g->ns) >> 32);
+    coin = mulhi64(((uint64_t)r[1] << 32) | r[2], g->S);
+    const r_sub *sb = &g->sub[coin < g->sub[bk].thr ? bk : g->sub[bk].alias];
+    draw_oi(seed, w, t, 0, 0, 1, r);
+    const uint64_t j = mulhi64(((uint64_t)r[0] << 32) | r[1], sb->c);
+    return x->dst[sb->mem[j]];
+}
+
+/* DeepWalk (app 0) and PPR (app 2) over a radix structure, as ora_walk (R-13). */
+void ora_radix_walk(const ora_radix *G, uint32_t app, uint32_t L, uint64_t seed, uint32_t first_walker,
+                    const uint32_t *starts, uint32_t W, uint32_t *paths, uint32_t *lengths, uint64_t *counts,
+                    uint64_t stop_thr, uint32_t stop_always, int nthreads)
+{
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(static)
+#endif
+    for (int64_t i = 0; i < (int64_t)W; i++) {
+        const uint32_t w = first_walker + (uint32_t)i;
+        uint32_t u = starts ? starts[i] : (uint32_t)(((uint64_t)first_walker + (uint64_t)i) % G->V);
+        uint32_t steps = 0;
+        if (paths) paths[(size_t)i] = u;
+        if (counts && app == 2) {
+#ifdef _OPENMP
+#pragma omp atomic
+#endif
+            counts[u]++;
+        }
+        for (uint32_t t = 0; L == 0xFFFFFFFFu || t < L; t++) {
+            if (G->v[u].d == 0) break;
+            const uint32_t next = ora_radix_sample(G, u, seed, w, t);
+            steps++;
+            if (paths) paths[(size_t)(t + 1) * W + (size_t)i] = next;
+            u = next;
+            if (app == 2) {
+                if (counts) {
+#ifdef _OPENMP
+#pragma omp atomic
+#endif
+                    counts[u]++;
+                }
+                if (stop_always) break;
+                uint32_t r[4];
+                draw(seed, w, t, 0, 3, r);
+                if ((((uint64_t)r[0] << 32) | r[1]) < stop_thr) break;
+            }
+        }
+        if (lengths) lengths[i] = steps;
+        if (paths && L != 0xFFFFFFFFu)
+            for (uint32_t t = steps + 1; t <= L; t++) paths[(size_t)t * W + (size_t)i] = O_NONE;
+    }
+}
+
+/* canonical dump (R-18), per vertex: u32 d; u32 n; n x {u32 i, u64 thr, u32 alias, u32 ns,
+ * ns x {u32 j, u32 c, u64 thr, u32 alias, c x u32 dst}}; u64 T. */
+size_t ora_radix_dump(const ora_radix *G, uint8_t *buf, size_t cap)
+{
+    o_out o = {buf, cap, 0};
+    for (uint32_t u = 0; u < G->V; u++) {
+        const r_vertex *x = &G->v[u];
+        put32(&o, x->d);
+        put32(&o, x->n);
+        for (uint32_t g = 0; g < x->n; g++) {
+            const r_group *gr = &x->grp[g];
+            put32(&o, gr->i);
+            put64(&o, gr->thr);
+            put32(&o, gr->alias);
+            put32(&o, gr->ns);
+            for (uint32_t s = 0; s < gr->ns; s++) {
+                const r_sub *sb = &gr->sub[s];
+                put32(&o, sb->j);
+                put32(&o, sb->c);
+                put64(&o, sb->thr);
+                put32(&o, sb->alias);
+                for (uint32_t k = 0; k < sb->c; k++) put32(&o, x->dst[sb->mem[k]]);
+            }
+        }
+        put64(&o, x->T);
+    }
+    return o.pos;
+}
