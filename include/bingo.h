@@ -93,6 +93,14 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
 #define BINGO_BUILD_FLOAT_BIAS 4u     /* biases come from bias_f64 (S4.3 floating-point extension, R-15) */
 #define BINGO_BUILD_ID_LAYOUT 8u      /* pools in vertex-id order (default: hot-first) */
 #define BINGO_BUILD_RELABEL 16u       /* relabel vertices hot-first internally at any V (default: V >= 2^23) */
+/* Arbitrary radix base B = 2^b, b in [1, 5] (reading R-17): group B^i holds
+ * the arcs whose base-B digit i is nonzero, split into subgroups by digit value with an
+ * inter-subgroup alias; walks take group -> subgroup -> member.  A STATIC structure (every
+ * subgroup a member list, vertex-id layout): DeepWalk and PPR walks (step-major paths),
+ * bingo_export in the radix dump format (R-18), bingo_visit_counts; bingo_apply_updates and
+ * the other calls return EINVAL.  0 (default): the paper's base-2 Bingo with Eq.9 groups. */
+#define BINGO_BUILD_RADIX_LOG2(b) ((uint32_t)(b) << 8)
+#define BINGO_BUILD_RADIX_MASK 0xF00u
 
 typedef void *(*bingo_alloc_fn)(size_t bytes, void *ctx);
 typedef void (*bingo_free_fn)(void *ptr, void *ctx);

@@ -219,7 +219,7 @@ class Graph:
     def __init__(self, row_offsets, dst, bias, alpha: int = 40, beta: int = 10, bs_mode: bool = False,
                  arc_slack: float = 0.25, member_slack: float = 0.25, pool_reserve: float = 0.1,
                  neighbor_index: bool = False, float_bias: bool = False, device=None, stream=None,
-                 torch_alloc: bool = True):
+                 torch_alloc: bool = True, radix_log2: int = 0):
         torch = _torch()
         L = _lib()
         self.device = torch.device(device if device is not None else "cuda")
@@ -240,7 +240,7 @@ class Graph:
         d = BuildDesc(num_vertices=self.V, num_arcs=ds.numel(), row_offsets=ro.data_ptr(), dst=ds.data_ptr(),
                       bias=bs.data_ptr(), alpha_pct=alpha, beta_pct=beta,
                       flags=(BUILD_BS_MODE if bs_mode else 0) | (BUILD_NEIGHBOR_INDEX if neighbor_index else 0)
-                      | (BUILD_FLOAT_BIAS if float_bias else 0),
+                      | (BUILD_FLOAT_BIAS if float_bias else 0) | ((int(radix_log2) & 0xF) << 8),
                       arc_slack=arc_slack, member_slack=member_slack, pool_reserve=pool_reserve,
                       alloc=self._alloc.alloc if self._alloc else ALLOC_FN(), free=self._alloc.free if self._alloc else FREE_FN(),
                       alloc_ctx=None, bias_f64=bf.data_ptr() if bf is not None else None)

@@ -112,6 +112,11 @@ extern "C" bingo_status bingo_export(bingo_graph *g, uint8_t *host_buf, size_t c
     if (!g || !size_out) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     cudaStream_t s = (cudaStream_t)stream;
+    if (g->radix_log2) {   // the radix structure's own dump (R-18)
+        const bingo_status rs = export_radix(g, host_buf, cap, size_out, s);
+        if (rs == BINGO_E_CUDA) g->poisoned = 1;
+        return rs;
+    }
     unsigned long long c[4];
     std::vector<VHdr> hdr(g->V);
     std::vector<uint32_t> perm(g->V), inv(g->V);   // dumps are in external ids and order (R-11)
@@ -255,6 +260,7 @@ __global__ void k_digests(uint32_t V, const VHdr *__restrict__ hdr, const uint2 
 
 extern "C" bingo_status bingo_digests(bingo_graph *g, uint64_t *digests, void *stream) {
     if (g) bingo_sq_quiesce(g, (cudaStream_t)stream);
+    if (g && g->radix_log2) return BINGO_E_INVAL;
     if (!g || !digests) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     if (!g->V) return BINGO_OK;

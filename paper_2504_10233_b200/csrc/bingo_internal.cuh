@@ -36,6 +36,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "bingo.h"
+
 #include "float_bias.cuh"
 
 namespace bingo {
@@ -195,6 +197,7 @@ struct bingo_graph {
     uint32_t *mdst = nullptr;          // [mem_cap] member dst (walker side)
     uint32_t *midx = nullptr;          // [mem_cap] member adjacency index (canonical)
     bool float_mode = false;
+    uint32_t radix_log2 = 0;           // 0: Bingo base 2 with adaptive groups; b >= 1: static base-2^b structure (radix.cu)
     bingo::DecRec *dec = nullptr;      // [V] decimal-group records (float mode)
     uint4 *dmem = nullptr;             // decimal members {idx, dst, D lo, D hi}
     uint64_t dmem_cap = 0;
@@ -247,6 +250,11 @@ struct bingo_graph {
 // stops a running streaming-queue kernel and orders `s` after its exit (update.cu); every
 // entry point that touches the graph calls it first (the epoch fence of the streaming queue)
 void bingo_sq_quiesce(bingo_graph *g, cudaStream_t s);
+// arbitrary radix base (radix.cu)
+bingo_status build_radix(bingo_graph *g, const bingo_build_desc *desc, uint32_t b, cudaStream_t s);
+bingo_status launch_walk_radix(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts, uint32_t W,
+                               uint32_t *paths, uint32_t *lengths, cudaStream_t s);
+bingo_status export_radix(bingo_graph *g, uint8_t *buf, size_t cap, size_t *size_out, cudaStream_t s);
 void bingo_sq_release(bingo_graph *g);
 
 // process-wide count of kernel launches issued by libbingo (api.cu)

@@ -335,6 +335,20 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     g->member_slack = desc->member_slack >= 0 ? desc->member_slack : 0.25;
     g->pool_reserve = desc->pool_reserve >= 0 ? desc->pool_reserve : 0.1;
     g->num_arcs = desc->num_arcs;
+    if (desc->flags & BINGO_BUILD_RADIX_MASK) {   // arbitrary radix base (radix.cu)
+        const uint32_t b = (desc->flags & BINGO_BUILD_RADIX_MASK) >> 8;
+        if (b > 5 || (desc->flags & (BINGO_BUILD_FLOAT_BIAS | BINGO_BUILD_NEIGHBOR_INDEX | BINGO_BUILD_BS_MODE))) {
+            delete g;
+            return BINGO_E_INVAL;
+        }
+        const bingo_status rs = build_radix(g, desc, b, s);
+        if (rs != BINGO_OK) {
+            bingo_destroy(g);
+            return rs;
+        }
+        *out = g;
+        return BINGO_OK;
+    }
 
     const uint64_t nV = (uint64_t)V;
     const size_t tmpw = scan_tmp_words(nV);

@@ -1800,6 +1800,7 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     // float-bias graphs take real biases (bingo_apply_updates_f64, R-16); integer graphs do not
     if (n && g->float_mode != (wf != nullptr)) return BINGO_E_INVAL;
     if (n >= 0xFFFFFFFFull) return BINGO_E_INVAL;
+    if (g->radix_log2) return BINGO_E_INVAL;   // static radix-base structure (radix.cu)
     bingo_sq_quiesce(g, (cudaStream_t)stream);
     const bool fm = g->float_mode;
     g_trace.on = getenv("BINGO_UPD_TRACE") != nullptr;
@@ -2195,7 +2196,7 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
                                             void *stream) {
     if (!g || !rec) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
-    if (g->float_mode) return BINGO_E_INVAL;   // float graphs take real biases (bingo_apply_updates_f64)
+    if (g->float_mode || g->radix_log2) return BINGO_E_INVAL;   // float graphs take real biases; radix graphs are static
     cudaStream_t s = (cudaStream_t)stream;
     if (stats) memset(stats, 0, sizeof(*stats));
     if (g->sq_running && g->sq_stream != s) bingo_sq_quiesce(g, s);

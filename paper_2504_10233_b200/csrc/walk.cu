@@ -363,6 +363,10 @@ extern "C" bingo_status bingo_walk(bingo_graph *g, const bingo_walk_desc *desc, 
     if (num_walkers == 0) return BINGO_OK;
     if (g->V == 0) return BINGO_E_INVAL;
     cudaStream_t s = (cudaStream_t)stream;
+    if (g->radix_log2) {
+        if (desc->flags & BINGO_WALK_HOST_OUTPUT) return BINGO_E_INVAL;
+        return launch_walk_radix(g, desc, starts_or_null, num_walkers, paths_or_null, lengths_or_null, s);
+    }
     if (!(desc->flags & BINGO_WALK_HOST_OUTPUT))
         return launch_walk(g, desc, starts_or_null, num_walkers, paths_or_null, lengths_or_null, s);
     // HOST buffers: the walkers run in chunks whose paths are staged in two device
@@ -440,6 +444,7 @@ extern "C" bingo_status bingo_walk_profile(bingo_graph *g, const bingo_walk_desc
     if (!g || !desc || !counters_host) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     bingo_sq_quiesce(g, (cudaStream_t)stream);
+    if (g->radix_log2) return BINGO_E_INVAL;
     if (desc->app > BINGO_PPR || (desc->flags & BINGO_WALK_HOST_OUTPUT)) return BINGO_E_INVAL;
     if (desc->app == BINGO_NODE2VEC && !(desc->p > 0 && desc->q > 0)) return BINGO_E_INVAL;
     if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
@@ -476,6 +481,7 @@ extern "C" bingo_status bingo_walk_trace(bingo_graph *g, const bingo_walk_desc *
     if (!g || !desc || !counters_host || !rec_off || !trace) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     bingo_sq_quiesce(g, (cudaStream_t)stream);
+    if (g->radix_log2) return BINGO_E_INVAL;
     if (!(desc->app == BINGO_DEEPWALK || desc->app == BINGO_PPR) || desc->flags || g->float_mode) return BINGO_E_INVAL;
     if (desc->app == BINGO_PPR && desc->stop_den == 0) return BINGO_E_INVAL;
     if (desc->length == BINGO_NO_CAP && desc->app != BINGO_PPR) return BINGO_E_INVAL;
@@ -568,6 +574,7 @@ extern "C" bingo_status bingo_walk_replay(bingo_graph *g, const void *trace, con
     if (!g || !trace || !rec_off || !counts_host) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     bingo_sq_quiesce(g, (cudaStream_t)stream);
+    if (g->radix_log2) return BINGO_E_INVAL;
     cudaStream_t s = (cudaStream_t)stream;
     unsigned long long *dc = (unsigned long long *)bingo_dev_alloc(g, sizeof(unsigned long long) * 8);
     if (!dc) return BINGO_E_NOMEM;
@@ -711,6 +718,7 @@ extern "C" bingo_status bingo_walk_partition(bingo_graph *g, const bingo_walk_de
         return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
     bingo_sq_quiesce(g, (cudaStream_t)stream);
+    if (g->radix_log2) return BINGO_E_INVAL;
     if (!(desc->app == BINGO_DEEPWALK || desc->app == BINGO_PPR) || g->float_mode) return BINGO_E_INVAL;
     if (desc->flags || (desc->app == BINGO_PPR && desc->stop_den == 0)) return BINGO_E_INVAL;
     if (desc->length == BINGO_NO_CAP && (paths_or_null || desc->app != BINGO_PPR)) return BINGO_E_INVAL;
