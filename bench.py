@@ -230,7 +230,7 @@ def make_graph(args, config, rounds, dev, ws, rank, dist):
     import synth
     import paper_2504_10233_b200 as pb
     t0 = time.time()
-    share = dist is not None and args.backend == "nccl" and not args.share_device
+    share = dist is not None          # rank 0 generates, the others receive (NCCL over NVLink; gloo in tests)
     if rank == 0 or not share:
         w = synth.make_workload(config, rounds=rounds, hold_rounds=HOLD_ROUNDS, device=dev, resident=True)
         ro, dst, bias, batches, V, A = w.row_offsets, w.dst, w.bias, w.batches, w.V, w.num_arcs
@@ -568,8 +568,17 @@ def streaming(g, batches, stream):
         rc = lib.bingo_stream_update(h, qbase + 16 * i, ctypes.byref(st), sp)
         lat_q.append(1e6 * (time.perf_counter() - t0))
         assert rc == 0, rc
+    # the queue's own round trip: records rejected by validation (src = V) do no graph work
+    bad = np.array([[0, 0xFFFFFFFF, 0, 1]] * 300, dtype=np.uint32)
+    lat_b = []
+    for i in range(len(bad)):
+        t0 = time.perf_counter()
+        rc = lib.bingo_stream_update(h, bad.ctypes.data + 16 * i, None, sp)
+        lat_b.append(1e6 * (time.perf_counter() - t0))
+        assert rc == bb.E_INVAL, rc
     torch.cuda.synchronize()
     return {"records": len(recs), "queue_records": len(lat_q),
+            "queue_roundtrip_us_p50": float(np.percentile(lat_b, 50)),
             "queue_us_p50": float(np.percentile(lat_q, 50)), "queue_us_p90": float(np.percentile(lat_q, 90)),
             "queue_us_p99": float(np.percentile(lat_q, 99)),
             "queue_updates_per_s": float(len(lat_q) / (1e-6 * sum(lat_q))),
@@ -587,8 +596,9 @@ def streaming(g, batches, stream):
 def oracle_sample(host_csr, batches, config, steps_idx, walkers, V, seed_base, warm=True):
     """The oracle as it stands (lazy build: vertices are materialised on first access), per
     step: one full update batch (single-threaded) + a sample of the step's walkers (OpenMP,
-    all host cores); the walk is timed on a second pass over the same walkers so lazy
-    materialisation is not billed as walking."""
+    all host cores).  First-touch materialisation is never billed: the batch's vertices are
+    materialised before the update is timed, and the walk is timed on a second pass over
+    the same walkers."""
     import oracle
     app = app_of(config)
     oapp = {"ppr": oracle.APP_PPR, "deepwalk": oracle.APP_DEEPWALK}[app]
@@ -596,6 +606,8 @@ def oracle_sample(host_csr, batches, config, steps_idx, walkers, V, seed_base, w
     o = oracle.OracleGraph(*host_csr, lazy=True)
     out = []
     for i in steps_idx:
+        # first-touch materialisation of the batch's vertices is not update work: done untimed
+        o.touch(np.unique(batches[i][:, 1:3]), threads=os.cpu_count())
         t0 = time.perf_counter()
         o.apply_updates(batches[i])
         t_upd = time.perf_counter() - t0
@@ -649,7 +661,8 @@ def run_reference(args):
     timed = samples[args.warmup:]
     val, det = cpu_line_from(timed, V, walkers, nrec)
     ms_step = 1e3 * (sum(s[0] for s in timed) + det["scale"] * sum(s[1] for s in timed)) / len(timed)
-    sample = (f"per step: 1 full update batch ({nrec} arc records, single-threaded, lazy oracle) + "
+    sample = (f"per step: 1 full update batch ({nrec} arc records, single-threaded, lazy oracle, its vertices "
+              f"materialised untimed) + "
               f"{app_of(config)} walk of {walkers} walkers (OpenMP, {os.cpu_count()} threads; second pass over the "
               f"same walkers, the first materialises their vertices), walk time scaled x{det['scale']:.1f} to "
               f"{V} walkers; generation {gen_s:.0f} s (torch on the GPU, not timed)")

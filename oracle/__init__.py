@@ -79,6 +79,7 @@ def lib():
             L.ora_dump.argtypes = [P, P, ctypes.c_size_t]
             L.ora_dump.restype = ctypes.c_size_t
             L.ora_digests.argtypes = [P, P]
+            L.ora_touch.argtypes = [P, P, u64, ctypes.c_int]
             L.ora_build_radix.argtypes = [u32, P, P, P, u32, ctypes.POINTER(P)]
             L.ora_build_radix.restype = ctypes.c_int
             L.ora_radix_free.argtypes = [P]
@@ -207,6 +208,11 @@ class OracleGraph:
 
     def sample(self, u, seed, w, t, outer=0) -> int:
         return int(lib().ora_sample(self._h, u, seed, w, t, outer))
+
+    def touch(self, ids, threads=0):
+        """Materialise these vertices now (lazy graphs; measurement support)."""
+        a = np.ascontiguousarray(ids, dtype=np.uint32)
+        lib().ora_touch(self._h, _p(a) if len(a) else None, len(a), threads)
 
     def walk(self, app=APP_DEEPWALK, length=80, seed=0, first_walker=0, starts=None, num_walkers=None,
              p=1.0, q=1.0, stop=(1, 80), paths=True, counts=False, threads=0):

@@ -1267,3 +1267,15 @@ size_t ora_radix_dump(const ora_radix *G, uint8_t *buf, size_t cap)
     }
     return o.pos;
 }
+
+/* Materialise the listed vertices of a lazy graph (parallel; no effect on an eager one):
+ * measurement support, so timed operations are not billed for first-touch builds. */
+void ora_touch(const ora_graph *G, const uint32_t *ids, uint64_t n, int nthreads)
+{
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#pragma omp parallel for schedule(dynamic, 64)
+#endif
+    for (int64_t k = 0; k < (int64_t)n; k++)
+        if (ids[k] < G->V) (void)vx(G, ids[k]);
+}

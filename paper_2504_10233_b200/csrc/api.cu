@@ -85,7 +85,8 @@ extern "C" bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *s
     info->l2_persist_bytes = g->persist_bytes;
     info->hot_degree = ((uint64_t)g->hot_mem_degree << 32) | g->hot_bkt_degree;
     info->device_bytes = (sizeof(VHdr) + sizeof(ThinHdr)) * (uint64_t)g->V + (sizeof(uint2) + 4) * g->arc_cap +
-                         (sizeof(Bucket) + sizeof(GCan)) * g->bkt_cap + 8ull * g->mem_cap + 8ull * g->V +
+                         (sizeof(Bucket) + sizeof(GCan)) * g->bkt_cap + (g->radix_log2 ? 4ull : 8ull) * g->mem_cap +
+                         8ull * g->V +
                          g->scratch_bytes + g->wscratch_bytes + g->vscratch_bytes + g->bscratch_bytes +
                          g->iscratch_bytes;
     return BINGO_OK;

@@ -151,13 +151,15 @@ __global__ void __launch_bounds__(256) k_rb_fill(uint32_t V, const uint64_t *__r
             }
             sub0 = incl - v;
         }
-        // member unit offsets of every subgroup in (i ascending, j ascending) order
+        // member offsets of every subgroup in (i ascending, j ascending) order, as entry
+        // cursors relative to the vertex's first member unit (the pool index is u64)
+        const uint64_t mbase = moff[u] * 4;
         if (lane == 0) {
-            uint64_t mo = moff[u];
+            uint32_t mo = 0;
             for (uint32_t i = 0; i < K; i++)
                 for (uint32_t j = 1; j < B; j++) {
                     const uint32_t cc = c[i * B + j];
-                    cu[i * B + j] = (uint32_t)(mo * 4);   // entry cursor (units x 4)
+                    cu[i * B + j] = mo * 4;
                     mo += (cc + 3) / 4;
                 }
         }
@@ -204,7 +206,7 @@ __global__ void __launch_bounds__(256) k_rb_fill(uint32_t V, const uint64_t *__r
             uint64_t sthr;
             uint32_t salias;
             vose_warp(sact, ns, sact ? (uint64_t)j_s * c_s : 0ull, S, sthr, salias);
-            const uint32_t mo_s = sact ? cu[i * B + j_s] / 4 : 0u;
+            const uint32_t mo_s = sact ? (uint32_t)(mbase / 4) + cu[i * B + j_s] / 4 : 0u;
             Bucket Bs;
             Bs.lim = alias_lim(sthr, S);
             Bs.px = c_s;
@@ -237,7 +239,7 @@ __global__ void __launch_bounds__(256) k_rb_fill(uint32_t V, const uint64_t *__r
                 if (key != 0xFFFFFFFFu) pos = cu[i * B + j] + __popc(same & lanemask_lt());
                 __syncwarp();
                 if (key != 0xFFFFFFFFu) {
-                    mdst[pos] = v;
+                    mdst[mbase + pos] = v;
                     if ((__ffs(same) - 1) == (int)lane) cu[i * B + j] += __popc(same);
                 }
                 __syncwarp();
@@ -402,7 +404,7 @@ bingo_status build_radix(bingo_graph *g, const bingo_build_desc *desc, uint32_t 
         if (hflag & 1) return done(BINGO_E_INVAL);
         if (hflag & 4) return done(BINGO_E_OVERFLOW);
     }
-    if (tot[0] >= 0x7FFFFFF0ull || tot[1] >= 0x3FFFFFF0ull) return done(BINGO_E_OVERFLOW);
+    if (tot[0] >= 0x7FFFFFF0ull || tot[1] >= 0xFFFFFFF0ull) return done(BINGO_E_OVERFLOW);
     g->bkt_cap = rb_pool(tot[0], 0.0);
     g->mem_cap = 4 * rb_pool(tot[1], 0.0);
     g->bkt = (Bucket *)bingo_dev_alloc(g, sizeof(Bucket) * g->bkt_cap);

@@ -2231,7 +2231,12 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
             }
         }
         if (taken) break;
-        if (attempt > 1000) return upd_cuda_fail(g, cudaErrorUnknown, "streaming queue");
+        if (attempt >= 2) {
+            // the kernel keeps exiting before it sees the record: launches are being serialised
+            // (a profiler replaying kernels one at a time).  Apply this record with one launch.
+            __atomic_store_n(&sl->seq, 0u, __ATOMIC_SEQ_CST);
+            return apply_impl(g, rec, nullptr, 1, BINGO_UPD_HOST_BATCH, stats, stream);
+        }
     }
     g->sq_seq = k + 1;
     const FastOut &o = q->out;
