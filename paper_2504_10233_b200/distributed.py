@@ -23,6 +23,7 @@ from __future__ import annotations
 
 from typing import Optional, Tuple
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -187,6 +188,41 @@ class PartitionedBingo:
         self.bounds = torch.tensor(bounds, dtype=torch.int32, device=self.device)
         self.rounds = 0
 
+    # ------------------------------------------------------------ sharded updates
+    def apply_updates(self, batch: Optional[torch.Tensor], n: Optional[int] = None) -> dict:
+        """Sharded update application: rank 0's batch is broadcast, validated whole on every
+        rank (EINVAL before anything is applied, bingo.h), and each rank applies only the
+        records whose SOURCE vertex it owns -- its partition holds the only copy of that
+        vertex's sampling structure (adjacency, groups, alias), so the update work is split P
+        ways and no vertex state has to be exchanged.  Every rank applies every batch (an
+        empty share still advances the epoch, R-9), so arc epochs match the single-graph run.
+        The statistics are summed over ranks."""
+        V = self.bounds_list[-1]
+        if self.world > 1:
+            if n is None:
+                nt = torch.zeros(1, dtype=torch.int64, device=self.device)
+                if self.rank == 0:
+                    nt[0] = batch.shape[0]
+                dist.broadcast(nt, 0, group=self.group)
+                n = int(nt.item())
+            buf = batch.to(self.device, dtype=torch.int32).contiguous() if self.rank == 0 else \
+                torch.empty((n, 4), dtype=torch.int32, device=self.device)
+            if n:
+                dist.broadcast(buf, 0, group=self.group)
+        else:
+            buf = batch.to(self.device, dtype=torch.int32).contiguous()
+        mine = owned_records(buf, self.bounds_list, self.rank, V)
+        st = self.g.apply_updates(mine)
+        if self.world > 1:
+            vec = torch.tensor([st["inserted"], st["deleted"], st["missing_deletes"], st["touched_vertices"]]
+                               + [int(x) for x in np.asarray(st["kind_transitions"]).reshape(-1)],
+                               dtype=torch.int64, device=self.device)
+            dist.all_reduce(vec, group=self.group)
+            v = vec.tolist()
+            st = dict(st, inserted=v[0], deleted=v[1], missing_deletes=v[2], touched_vertices=v[3],
+                      kind_transitions=np.array(v[4:29], dtype=np.uint64).reshape(5, 5))
+        return st
+
     def _exchange(self, outbox: torch.Tensor, counts: torch.Tensor) -> torch.Tensor:
         send_counts = counts.to(torch.int64)
         recv_counts = torch.zeros_like(send_counts)
@@ -233,6 +269,27 @@ class PartitionedBingo:
         if self.world > 1:
             dist.all_reduce(c, op=dist.ReduceOp.SUM, group=self.group)
         return c
+
+
+def owned_records(batch: torch.Tensor, bounds, me: int, V: int) -> torch.Tensor:
+    """The records of a (n, 4) {op, src, dst, bias} batch whose source vertex this rank owns,
+    in batch order, after validating the WHOLE batch (the ABI's whole-batch rule: one bad
+    record anywhere rejects the batch before any rank applies anything)."""
+    b = batch.to(torch.int64) & 0xFFFFFFFF
+    op, src, dst, w = b[:, 0], b[:, 1], b[:, 2], b[:, 3]
+    bad = (op > 1) | (src >= V) | (dst >= V) | ((op == 0) & (w == 0))
+    if bool(bad.any()):
+        from . import bingo
+        raise bingo.BingoError(bingo.E_INVAL, "partitioned apply_updates")
+    mine = (src >= bounds[me]) & (src < bounds[me + 1])
+    return batch[mine].contiguous()
+
+
+def apply_updates_partitions_local(engines, bounds, batch) -> list:
+    """Sharded update application with every partition in THIS process: partition r applies
+    the records whose source it owns (PartitionedBingo.apply_updates without the broadcast)."""
+    V = bounds[-1]
+    return [e.apply_updates(owned_records(batch, bounds, r, V)) for r, e in enumerate(engines)]
 
 
 def walk_partitions_local(engines, bounds, num_walkers: int, app: int = 0, length: int = 80, seed: int = 0,

@@ -56,3 +56,35 @@ def test_partitioned_equals_replicated_gpu_walk():
     out = walk_partitions_local(engines, bounds, w.V, length=80, seed=21)
     assert np.array_equal(u32(out["paths"]), u32(full["paths"]))
     assert np.array_equal(u32(out["lengths"]), u32(full["lengths"]))
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_sharded_updates_on_partitions(P):
+    """f1 in the partitioned regime: every partition applies only the batch records whose
+    source vertex it owns (the only copy of that vertex's sampling structure).  After each
+    batch the owned vertices' canonical digests equal the oracle graph that applied every
+    record, the summed statistics equal its statistics, and the partitioned walk equals its
+    walk."""
+    import paper_2504_10233_b200 as pb
+    from paper_2504_10233_b200.distributed import (apply_updates_partitions_local, partition_bounds, partition_csr,
+                                                   walk_partitions_local)
+    w = synth.Workload(14, 150_000, compact=True, batch=4000, rounds=3)
+    o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
+    bounds = partition_bounds(w.row_offsets, P)
+    engines = [pb.Graph(*partition_csr(w.row_offsets, w.dst, w.bias, bounds[r], bounds[r + 1])) for r in range(P)]
+    import torch
+    for b in w.batches:
+        sts = apply_updates_partitions_local(engines, bounds, torch.from_numpy(b.view(np.int32)).cuda())
+        so = o.apply_updates(b)
+        for k in ("inserted", "deleted", "missing_deletes", "touched_vertices"):
+            assert sum(st[k] for st in sts) == so[k], k
+        assert all(st["epoch"] == so["epoch"] for st in sts)
+        full = o.digests()
+        for r, e in enumerate(engines):
+            dg = e.digests().cpu().numpy().view(np.uint64)
+            assert np.array_equal(dg[bounds[r]:bounds[r + 1]], full[bounds[r]:bounds[r + 1]]), r
+    out = walk_partitions_local(engines, bounds, 40_000, length=50, seed=4)
+    ref = o.walk(length=50, seed=4, num_walkers=40_000)
+    assert np.array_equal(u32(out["paths"]), ref["paths"])
+    with pytest.raises(pb.bingo.BingoError):
+        apply_updates_partitions_local(engines, bounds, torch.tensor([[0, 1, w.V, 3]], dtype=torch.int32).cuda())

@@ -1,5 +1,6 @@
 """-m "not gpu": the 1-D partitioned walk's driver (paper_2504_10233_b200.distributed.
-PartitionedBingo) on world_size 2 with gloo on CPU.  Each rank's engine
+PartitionedBingo) and its sharded update application (f1) on world_size 2
+with gloo on CPU.  Each rank's engine
 is the CPU oracle built from its partition (partition_csr: only its rows' arcs) wrapped in a
 test-only stepper with bingo_walk_partition's contract (walk while on owned vertices, leave
 for the owner otherwise).  Walker transfer by all-to-all must reproduce the unpartitioned
@@ -84,6 +85,9 @@ class OraclePartEngine:
                     paths[t + 1:, i] = -1
         return fin
 
+    def apply_updates(self, batch):
+        return self.o.apply_updates(batch.numpy().view(np.uint32))
+
     def visit_counts(self, reset=False):
         c = torch.from_numpy(self.counts.copy())
         if reset:
@@ -108,7 +112,7 @@ def _worker(rank, world, port, outdir):
     import oracle
     import synth
     from paper_2504_10233_b200.distributed import PartitionedBingo, partition_bounds, partition_csr
-    w = synth.make_workload("c1")
+    w = synth.make_workload("c1", rounds=2)
     bounds = partition_bounds(w.row_offsets, world)
     ro, dst, bias = partition_csr(w.row_offsets, w.dst, w.bias, bounds[rank], bounds[rank + 1])
     pb = PartitionedBingo(OraclePartEngine(ro, dst, bias), bounds)
@@ -119,6 +123,15 @@ def _worker(rank, world, port, outdir):
     np.save(os.path.join(outdir, f"plen{rank}.npy"), out["lengths"].numpy())
     np.save(os.path.join(outdir, f"counts{rank}.npy"), pb.visit_counts().numpy())
     np.save(os.path.join(outdir, f"rounds{rank}.npy"), np.array([out["rounds"]]))
+    # sharded update application: each rank applies the records its vertices own
+    for b in w.batches:
+        st = pb.apply_updates(torch.from_numpy(b.view(np.int32)) if rank == 0 else None, n=b.shape[0])
+        np.save(os.path.join(outdir, f"st{rank}_{st['epoch']}.npy"),
+                np.array([st["inserted"], st["deleted"], st["missing_deletes"], st["touched_vertices"]]))
+    dig = pb.g.o.digests()[bounds[rank]:bounds[rank + 1]]
+    np.save(os.path.join(outdir, f"dig{rank}.npy"), dig)
+    out = pb.walk(num_walkers=500, length=12, seed=8)
+    np.save(os.path.join(outdir, f"upaths{rank}.npy"), out["paths"].numpy())
     dist.barrier()
     dist.destroy_process_group()
 
@@ -146,7 +159,7 @@ def test_two_rank_partitioned_walk_gloo(tmp_path):
     import synth
     world = 2
     mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
-    w = synth.make_workload("c1")
+    w = synth.make_workload("c1", rounds=2)
     o = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
     ref = o.walk(length=15, seed=3, first_walker=40, num_walkers=700)
     for r in range(world):     # assembled on every rank
@@ -157,3 +170,18 @@ def test_two_rank_partitioned_walk_gloo(tmp_path):
         assert np.array_equal(np.load(tmp_path / f"plen{r}.npy").view(np.uint32), refp["lengths"])
         assert np.array_equal(np.load(tmp_path / f"counts{r}.npy").view(np.uint64), refp["counts"])
         assert int(np.load(tmp_path / f"rounds{r}.npy")[0]) > 2     # walkers really moved between ranks
+    # after sharded updates: owned vertices' canonical state, statistics and walks equal the
+    # single graph that applied every record
+    o2 = oracle.OracleGraph(w.row_offsets, w.dst, w.bias)
+    for b in w.batches:
+        so = o2.apply_updates(b)
+        for r in range(world):
+            got = np.load(tmp_path / f"st{r}_{so['epoch']}.npy")
+            assert got.tolist() == [so["inserted"], so["deleted"], so["missing_deletes"], so["touched_vertices"]]
+    from paper_2504_10233_b200.distributed import partition_bounds
+    bounds = partition_bounds(w.row_offsets, world)
+    full = o2.digests()
+    assert np.array_equal(np.concatenate([np.load(tmp_path / f"dig{r}.npy") for r in range(world)]), full)
+    ref = o2.walk(length=12, seed=8, num_walkers=500)
+    for r in range(world):
+        assert np.array_equal(np.load(tmp_path / f"upaths{r}.npy").view(np.uint32), ref["paths"])
