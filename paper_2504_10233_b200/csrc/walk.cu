@@ -21,8 +21,7 @@ using namespace bingo;
 namespace bingo {
 
 template <int APP, bool PROF, bool WMAJOR>
-__device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint32_t &w, uint32_t &u,
-                                             uint32_t *svis) {
+__device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint32_t &w, uint32_t &u) {
     w = a.first_walker + (uint32_t)i;
     const uint32_t u0 = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);   // external
     u = a.inv ? __ldg(a.inv + u0) : u0;
@@ -30,10 +29,7 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
         if (WMAJOR) a.paths[i * ((size_t)a.L + 1)] = u0;
         else __stcs(&a.paths[i], u0);
     }
-    if (APP == BINGO_PPR && a.visit) {
-        if (a.visit_smem && u < BINGO_VISIT_SMEM) atomicAdd(&svis[u], 1u);
-        else atomicAdd(&a.visit[visit_slot(u)], 1ull);
-    }
+    if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
 }
 
 #ifndef BINGO_WALK_MINB
@@ -84,13 +80,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
     ThinHdr h;
     DecRec dr;
     dr.dcnt = 0;
-    // PPR: per-block counters of the hottest ids (BINGO_VISIT_SMEM), flushed at block exit
-    __shared__ uint32_t svis[APP == BINGO_PPR ? BINGO_VISIT_SMEM : 1];
-    if (APP == BINGO_PPR && a.visit_smem) {
-        for (uint32_t x = threadIdx.x; x < BINGO_VISIT_SMEM; x += blockDim.x) svis[x] = 0;
-        __syncthreads();
-    }
-    if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u, svis);
+    if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u);
     for (;;) {
         bool fin = false;
         if (active) {
@@ -149,14 +139,10 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
 #ifndef BINGO_EXP_NO_VISIT       // measurement experiment only: skip the visit counts
 #ifndef BINGO_VISIT_PLAIN          // one atomic per distinct vertex per warp iteration (A/B: plain)
                             if (a.visit) {
-                                if (a.visit_smem && u < BINGO_VISIT_SMEM) {
-                                    atomicAdd(&svis[u], 1u);
-                                } else {
-                                    const unsigned act = __activemask();
-                                    const unsigned same = __match_any_sync(act, u);
-                                    if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u))
-                                        atomicAdd(&a.visit[visit_slot(u)], (unsigned long long)__popc(same));
-                                }
+                                const unsigned act = __activemask();
+                                const unsigned same = __match_any_sync(act, u);
+                                if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u))
+                                    atomicAdd(&a.visit[visit_slot(u)], (unsigned long long)__popc(same));
                             }
 #else
                             if (a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
@@ -205,17 +191,12 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                 o = 0;
                 prev = 0xFFFFFFFFu;
                 prev_nbo = cur_nbo = 0;
-                if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u, svis);
+                if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u);
             }
         }
         if (!__any_sync(0xffffffffu, active)) break;
     }
     if (PROF) prof.flush(a.prof);
-    if (APP == BINGO_PPR && a.visit_smem) {
-        __syncthreads();
-        for (uint32_t x = threadIdx.x; x < BINGO_VISIT_SMEM; x += blockDim.x)
-            if (svis[x]) atomicAdd(&a.visit[visit_slot(x)], (unsigned long long)svis[x]);
-    }
 }
 
 }  // namespace bingo
@@ -282,7 +263,6 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     a.dec = g->float_mode ? g->dec : nullptr;
     a.dmem = g->dmem;
     a.visit = g->visit;
-    a.visit_smem = (g->perm != nullptr && !getenv("BINGO_NO_VISIT_SMEM")) ? 1u : 0u;   // relabelled: ids < 4096 are the hottest
     a.starts = starts;
     a.perm = g->perm;
     a.inv = g->inv;

@@ -50,7 +50,6 @@ struct WalkArgs {
     const DecRec *dec;      // float mode (R-15) or null
     const uint4 *dmem;
     unsigned long long *visit;
-    uint32_t visit_smem;    // PPR on a relabelled graph: count the hottest ids in shared memory
     const uint32_t *starts;
     const uint32_t *perm, *inv;   // internal <-> external vertex ids (paths and starts are external)
     uint32_t *paths;
@@ -77,14 +76,6 @@ struct WalkArgs {
 #else
 #define BINGO_L1Q ""
 #endif
-
-// PPR visit counts of the VISIT_SMEM hottest internal ids (ids < VISIT_SMEM after the
-// hot-first relabelling) are accumulated per block in shared memory and added to the global
-// counters once at block exit; the rest go to global memory (warp-aggregated reductions).
-#ifndef BINGO_VISIT_SMEM
-#define BINGO_VISIT_SMEM 4096u
-#endif
-__device__ __forceinline__ void visit_add(const unsigned long long *, uint32_t, uint32_t);
 
 struct Policies {
     uint64_t keep, stream;   // L2 cache-hint policies (createpolicy)
