@@ -909,6 +909,9 @@ static constexpr uint32_t FAST_MAXL = 1u << 16;
 // pipeline, whose chunk items spread the vertex's scans over the GPU (one block here walks
 // them alone: c5 batches of 16 records took 0.9 ms on the fast path, profiles/r01_streaming_c5)
 static constexpr uint32_t FAST_HANDOFF_L = 8192;
+// the streaming kernel (one record, 1024 threads) mutates a vertex above this many arcs with
+// the whole block instead of one warp
+static constexpr uint32_t FAST_BLOCK_L = 512;
 enum : uint32_t { FAST_OK = 0, FAST_INVAL = 1, FAST_OVERFLOW = 4, FAST_SLOW = 8 };
 
 struct FastOut {
@@ -947,10 +950,13 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
     __shared__ unsigned long long scr_off[FAST_N + 1];
     __shared__ MutSmem sm[32];
     __shared__ unsigned long long need_arc, need_bkt, need_mem;
-    __shared__ uint32_t flag, ntouch, go;
+    __shared__ uint32_t flag, ntouch, go, blockwide;
     const uint32_t tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
+    // a whole 1024-thread block on one touched vertex (the streaming kernel): its O(d) scans
+    // are spread over 32 warps, so vertices up to FAST_MAXL arcs stay on this path
+    const bool block_mode = blockDim.x == LT;
     const uint32_t n = fa.n;
-    if (tid == 0) { need_arc = need_bkt = need_mem = 0; flag = 0; }
+    if (tid == 0) { need_arc = need_bkt = need_mem = 0; flag = 0; blockwide = 0; }
     if (tid < n) recs[tid] = src[tid];
     __syncthreads();
     // validation (whole batch, before anything else)
@@ -1014,7 +1020,9 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
                                       fa.m.arc_slack, fa.m.mem_slack);
         if (lane == 0) {
             if (o.overflow) atomicOr(&flag, FAST_OVERFLOW);
-            if (o.L > FAST_HANDOFF_L || o.q > FAST_N) atomicOr(&flag, FAST_SLOW);
+            const bool single = block_mode && nt == 1;
+            if (o.L > (single ? FAST_MAXL : FAST_HANDOFF_L) || o.q > FAST_N) atomicOr(&flag, FAST_SLOW);
+            if (single && o.L > FAST_BLOCK_L) blockwide = 1;
             atomicAdd(&need_arc, o.arc);
             atomicAdd(&need_bkt, o.bkt);
             atomicAdd(&need_mem, o.mem + o.res);
@@ -1052,7 +1060,10 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
         a.vstats = fa.vstats;
         // each warp's delete scratch in dynamic shared memory when it fits (else global)
         extern __shared__ __align__(16) uint32_t fast_wscr[];
-        for (uint32_t t = w; t < nt; t += nw) mutate_vertex<32>(a, t, sm[w], fast_wscr + w * WARP_SCR_WORDS, WARP_SCR_WORDS);
+        if (blockwide) mutate_vertex<LT>(a, 0, sm[0]);   // uniform: the single vertex, every thread
+        else
+            for (uint32_t t = w; t < nt; t += nw)
+                mutate_vertex<32>(a, t, sm[w], fast_wscr + w * WARP_SCR_WORDS, WARP_SCR_WORDS);
     }
     __syncthreads();
     const uint32_t fin = flag;   // final since the barrier before the mutation
@@ -1120,7 +1131,7 @@ __device__ __forceinline__ uint4 ld_volatile_u4(const uint4 *p) {
     return v;
 }
 
-__global__ void __launch_bounds__(32) k_stream_upd(const FastArgs fa0, StreamQ *q, unsigned int seq0, unsigned int gen) {
+__global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *q, unsigned int seq0, unsigned int gen) {
     __shared__ uint4 rec;
     __shared__ unsigned int cmd;   // 0 process, 1 exit
     FastArgs fa = fa0;
@@ -2182,7 +2193,7 @@ static bingo_status sq_launch(bingo_graph *g, cudaStream_t s) {
     fa.n = 1;
     const unsigned gen = ++g->sq_gen ? g->sq_gen : ++g->sq_gen;   // never 0 (0 = stopped)
     __atomic_store_n(&q->run_gen, gen, __ATOMIC_SEQ_CST);
-    k_stream_upd<<<1, 32, 4 * WARP_SCR_WORDS, s>>>(fa, (StreamQ *)g->sq_dev, g->sq_seq, gen);
+    k_stream_upd<<<1, LT, 4 * WARP_SCR_WORDS, s>>>(fa, (StreamQ *)g->sq_dev, g->sq_seq, gen);
     bingo_count_launch();
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaEventRecord(g->sq_ev, s);
