@@ -293,6 +293,8 @@ typedef struct {
     uint64_t kernel_launches;  /* process-wide count of libbingo kernel launches so far */
     uint64_t l2_persist_bytes; /* L2 persisting set-aside in effect (walker hot set) */
     uint64_t hot_degree;       /* low 32 bits: degree from which buckets are L2 evict_last; high 32: member arrays */
+    uint64_t update_reruns;    /* batches of the one-sync update route that found a pool or scratch short,
+                                  mutated nothing, and were re-applied on the synchronous route */
 } bingo_info;
 bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *stream);
 

@@ -75,7 +75,8 @@ class Info(ctypes.Structure):
                 ("bucket_pool_used", ctypes.c_uint64), ("bucket_pool_cap", ctypes.c_uint64),
                 ("member_pool_used", ctypes.c_uint64), ("member_pool_cap", ctypes.c_uint64),
                 ("device_bytes", ctypes.c_uint64), ("kernel_launches", ctypes.c_uint64),
-                ("l2_persist_bytes", ctypes.c_uint64), ("hot_degree", ctypes.c_uint64)]
+                ("l2_persist_bytes", ctypes.c_uint64), ("hot_degree", ctypes.c_uint64),
+                ("update_reruns", ctypes.c_uint64)]
 
 
 _LIB = None

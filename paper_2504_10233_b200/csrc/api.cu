@@ -34,9 +34,10 @@ extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
     bingo_sq_release(g);
     void *bufs[] = {g->perm, g->inv, g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->arc_dval, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->nbtomb, g->hixo, g->hixt, g->hix, g->dec, g->dmem, g->counters, g->visit, g->dev_flag,
-                    g->scratch, g->wscratch, g->vscratch, g->bscratch, g->iscratch, g->fast_scr};
+                    g->scratch, g->wscratch, g->vscratch, g->bscratch, g->iscratch, g->fast_scr, g->vslot};
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
+    if (g->uhost) cudaFreeHost(g->uhost);
     if (g->fast_out_host) cudaFreeHost(g->fast_out_host);
     if (g->aux_stream) cudaStreamDestroy(g->aux_stream);
     if (g->copy_stream) cudaStreamDestroy(g->copy_stream);
@@ -84,6 +85,7 @@ extern "C" bingo_status bingo_get_info(bingo_graph *g, bingo_info *info, void *s
     info->kernel_launches = g_launch_count.load();
     info->l2_persist_bytes = g->persist_bytes;
     info->hot_degree = ((uint64_t)g->hot_mem_degree << 32) | g->hot_bkt_degree;
+    info->update_reruns = g->n_sync_reruns;
     info->device_bytes = (sizeof(VHdr) + sizeof(ThinHdr)) * (uint64_t)g->V + (sizeof(uint2) + 4) * g->arc_cap +
                          (sizeof(Bucket) + sizeof(GCan)) * g->bkt_cap + (g->radix_log2 ? 4ull : 8ull) * g->mem_cap +
                          8ull * g->V +

@@ -231,6 +231,11 @@ struct bingo_graph {
     size_t bscratch_bytes = 0;
     void *iscratch = nullptr;                // bulk-synchronous update: per-chunk-item counts
     size_t iscratch_bytes = 0;
+    uint64_t isc_sel = 0, isc_grp = 0;       // chunk-item capacities carved from iscratch
+    void *uhost = nullptr;                   // pinned staging of the one-sync update route
+    uint32_t *vslot = nullptr;               // [V] per-vertex claim slots of the update segmentation (EMPTY between batches)
+    bool radix_front = false;                // this batch re-segments with the radix sort (a segment too long)
+    uint64_t n_sync_reruns = 0;              // one-sync batches re-run on the synchronous route
     uint32_t *fast_scr = nullptr;            // small-batch fast path scratch (device)
     cudaStream_t aux_stream = nullptr;       // side stream for hub mutations
     cudaStream_t copy_stream = nullptr;      // D2H of walk chunks (HOST_OUTPUT)

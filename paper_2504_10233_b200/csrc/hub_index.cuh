@@ -55,6 +55,7 @@ __device__ __forceinline__ bool hix_move(const HixT &h, uint32_t v, uint32_t p, 
 
 // per large touched vertex: decide whether this batch uses / builds / drops its index
 __global__ void __launch_bounds__(MT) k_hix_prep(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_WARP_LOOP(h, *a.nbigs) {
@@ -86,10 +87,12 @@ __global__ void __launch_bounds__(MT) k_hix_prep(const BspArgs a) {
 
 // table builds: the pre-batch positions [0, d) of every vertex in mode 2 (chunk items)
 __global__ void __launch_bounds__(MT) k_hix_build(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_ITEM_LOOP(it, total) {
-        const uint32_t i = owner_of(a.p_sel, a.nt, it);
+    const uint32_t NT = bsp_nt(a);
+    total = bsp_total(a, a.p_sel, total);
+    BSP_ITEM_RANGE(it, i, total, a.p_sel, NT) {
         if (a.vhix[i] != 2u) continue;
         const uint32_t c = (uint32_t)(it - a.p_sel[i]);
         const uint32_t d = a.vL[i] - a.vm[i];
@@ -103,6 +106,7 @@ __global__ void __launch_bounds__(MT) k_hix_build(const BspArgs a, uint64_t tota
 // round 0 of the selection (R-8) through the index: every live instance of each deleted
 // destination, pre-batch ones from the table, this batch's inserts by a scan of [d, L)
 __global__ void __launch_bounds__(MT) k_hix_select(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_WARP_LOOP(h, *a.nhubs) {
@@ -143,6 +147,7 @@ __global__ void __launch_bounds__(MT) k_hix_select(const BspArgs a) {
 
 // after the picks, before the arcs move: the picked pre-batch arcs leave the table
 __global__ void __launch_bounds__(MT) k_hix_del(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_WARP_LOOP(h, *a.nhubs) {
@@ -166,6 +171,7 @@ __global__ void __launch_bounds__(MT) k_hix_del(const BspArgs a) {
 // after the adjacency tail window moved (R-6): moved arcs update their entries, this batch's
 // surviving inserts add theirs; a table past 3/4 load is dropped
 __global__ void __launch_bounds__(MT) k_hix_ins(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_WARP_LOOP(h, *a.nbigs) {

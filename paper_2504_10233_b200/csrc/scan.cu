@@ -1,5 +1,7 @@
 // scan.cu -- single-pass exclusive scan over u64 (decoupled look-back).
 // Tiles of 2048 elements (256 threads x 8).
+#include <algorithm>
+
 #include "scan.cuh"
 #include "bingo_internal.cuh"
 
@@ -79,7 +81,10 @@ struct ScanMulti {
 
 __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const ScanMulti m, uint64_t n,
                                                                 unsigned long long *status_all, unsigned *counter_all,
-                                                                uint64_t tiles) {
+                                                                uint64_t tiles, const unsigned long long *pn) {
+    // pn: the length is read from device memory (clamped to n, the launch's capacity);
+    // tiles past it leave at once (nothing looks back at them)
+    if (pn) n = min((uint64_t)*pn, n);
     // blockIdx.y selects the array; each array has its own tile counter and status words
     const uint64_t *__restrict__ in = m.in[blockIdx.y];
     uint64_t *__restrict__ out = m.out[blockIdx.y];
@@ -91,6 +96,7 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const ScanMulti 
     __syncthreads();
     const uint64_t tile = s_tile;
     const uint64_t base = tile * SCAN_TILE;
+    if (tile && base >= n) return;
     uint64_t v[SCAN_ITEMS];
     uint64_t acc = 0;
 #pragma unroll
@@ -100,31 +106,42 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const ScanMulti 
         acc += v[j];
     }
     uint64_t pre = block_exclusive(acc, &tot);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
+        // warp 0 publishes the tile aggregate, then looks back over a window of 32
+        // predecessors at once (lane l reads tile - 1 - l): the nearest inclusive prefix
+        // plus the aggregates in front of it; tiles before 0 count as a prefix of 0
+        const uint32_t lane = threadIdx.x;
         volatile unsigned long long *st = status;
         uint64_t excl = 0;
         if (tile == 0) {
-            st[0] = ST_P | (tot & ST_V);
+            if (lane == 0) st[0] = ST_P | (tot & ST_V);
         } else {
-            st[tile] = ST_A | (tot & ST_V);
+            if (lane == 0) st[tile] = ST_A | (tot & ST_V);
             __threadfence();
-            uint64_t j = tile - 1;
+            int64_t j0 = (int64_t)tile - 1;
             unsigned spins = 0;
             for (;;) {
-                const unsigned long long w = st[j];
+                const int64_t j = j0 - (int64_t)lane;
+                const unsigned long long w = j >= 0 ? st[j] : ST_P;
                 const unsigned long long f = w & ~ST_V;
-                if (f == 0) {   // predecessor not published yet (it started earlier: it will)
-                    if (++spins > (1u << 28)) __trap();   // never hang the device silently
+                const unsigned notready = __ballot_sync(0xffffffffu, f == 0);
+                const unsigned isp = __ballot_sync(0xffffffffu, f == ST_P);
+                const unsigned upto = isp ? ((isp & (0u - isp)) << 1) - 1u : 0xffffffffu;   // lanes 0..first P
+                if (notready & upto) {   // a predecessor has not published yet (it started earlier: it will)
+                    if (++spins > (1u << 26)) __trap();   // never hang the device silently
                     continue;
                 }
-                excl += w & ST_V;
-                if (f == ST_P || j == 0) break;
-                j--;
+                uint64_t x = ((upto >> lane) & 1u) ? (w & ST_V) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+                excl += x;
+                if (isp) break;
+                j0 -= 32;
             }
             __threadfence();
-            st[tile] = ST_P | ((excl + tot) & ST_V);
+            if (lane == 0) st[tile] = ST_P | ((excl + tot) & ST_V);
         }
-        s_excl = excl;
+        if (lane == 0) s_excl = excl;
     }
     __syncthreads();
     pre += s_excl;
@@ -137,8 +154,8 @@ __global__ void __launch_bounds__(SCAN_THREADS) k_scan_lookback(const ScanMulti 
     if (base + SCAN_TILE >= n && threadIdx.x == SCAN_THREADS - 1) out[n] = pre;   // the last tile: the total
 }
 
-cudaError_t exclusive_scan_u64_multi(const uint64_t *const *in, uint64_t *const *out, int count, uint64_t n,
-                                     uint64_t *tmp, cudaStream_t s) {
+static cudaError_t scan_multi(const uint64_t *const *in, uint64_t *const *out, int count, uint64_t n,
+                              uint64_t *tmp, cudaStream_t s, const unsigned long long *pn) {
     if (count <= 0) return cudaSuccess;
     if (n == 0) {
         for (int a = 0; a < count; a++) {
@@ -148,7 +165,7 @@ cudaError_t exclusive_scan_u64_multi(const uint64_t *const *in, uint64_t *const 
         return cudaSuccess;
     }
     const uint64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
-    if (tiles == 1) {
+    if (tiles == 1 && !pn) {
         for (int a = 0; a < count; a++) {
             k_tile_scan<<<1, SCAN_THREADS, 0, s>>>(in[a], out[a], n, nullptr);
             bingo_count_launch();
@@ -165,9 +182,19 @@ cudaError_t exclusive_scan_u64_multi(const uint64_t *const *in, uint64_t *const 
     unsigned *counter = reinterpret_cast<unsigned *>(tmp + (uint64_t)count * tiles);
     cudaError_t e = cudaMemsetAsync(tmp, 0, sizeof(uint64_t) * ((uint64_t)count * tiles + count), s);
     if (e != cudaSuccess) return e;
-    k_scan_lookback<<<dim3((unsigned)tiles, (unsigned)count), SCAN_THREADS, 0, s>>>(m, n, status, counter, tiles);
+    k_scan_lookback<<<dim3((unsigned)tiles, (unsigned)count), SCAN_THREADS, 0, s>>>(m, n, status, counter, tiles, pn);
     bingo_count_launch();
     return cudaGetLastError();
+}
+
+cudaError_t exclusive_scan_u64_multi(const uint64_t *const *in, uint64_t *const *out, int count, uint64_t n,
+                                     uint64_t *tmp, cudaStream_t s) {
+    return scan_multi(in, out, count, n, tmp, s, nullptr);
+}
+
+cudaError_t exclusive_scan_u64_multi_dn(const uint64_t *const *in, uint64_t *const *out, int count,
+                                        const unsigned long long *pn, uint64_t nmax, uint64_t *tmp, cudaStream_t s) {
+    return scan_multi(in, out, count, std::max<uint64_t>(nmax, 1), tmp, s, pn);
 }
 
 cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, uint64_t *tmp, cudaStream_t s) {

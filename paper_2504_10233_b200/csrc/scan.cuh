@@ -14,5 +14,9 @@ cudaError_t exclusive_scan_u64(const uint64_t *in, uint64_t *out, uint64_t n, ui
 #define SCAN_MULTI_MAX 8
 cudaError_t exclusive_scan_u64_multi(const uint64_t *const *in, uint64_t *const *out, int count, uint64_t n,
                                      uint64_t *tmp, cudaStream_t s);
+// the same with the length read on the device from *pn (<= nmax; tmp sized for nmax):
+// for launches enqueued before the length is known on the host
+cudaError_t exclusive_scan_u64_multi_dn(const uint64_t *const *in, uint64_t *const *out, int count,
+                                        const unsigned long long *pn, uint64_t nmax, uint64_t *tmp, cudaStream_t s);
 
 }  // namespace bingo

@@ -117,6 +117,136 @@ __global__ void k_upd_segments(const uint64_t *__restrict__ head_ex, const uint3
     }
 }
 
+// ------------------------------------------------------------------ segmentation without a sort (default)
+// Touched vertices get dense ids by claiming a per-vertex slot (vslot, all EMPTY between
+// batches), records are counted and placed per id, and only the order INSIDE a segment is
+// then restored (batch order): short segments by one thread, long ones by a block.
+// Six small launches instead of a 3-pass radix sort + heads + scan + segments.  Touched ids
+// come in claim order (any order is valid: vertices are independent).
+static constexpr uint32_t SEG_SHORT = 32, SEG_LONG_MAX = 8192;
+
+// Touched ids are ranked by source-id bin (2^SEG_BSH consecutive ids; claim order inside a
+// bin), so consecutive touched vertices sit on the same pages of the per-vertex arrays --
+// every later phase walks them in that order (a fully unsorted order cost ~10% at c2).
+static constexpr uint32_t SEG_BSH = 11;
+
+// validate (as k_upd_validate) + claim: the first record of each source owns its vertex and
+// takes a rank inside the vertex's bin
+__global__ void k_seg_claim(const uint4 *in, uint4 *out, uint64_t n, uint32_t V, const uint32_t *__restrict__ inv,
+                            uint32_t *vslot, uint32_t *__restrict__ key, uint32_t *__restrict__ otix,
+                            unsigned long long *bcnt, uint32_t *nlong, UpdCounters *cnt, bool allow_zero) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) *nlong = 0;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        uint4 r = in[i];
+        const bool bad = r.x > 1u || r.y >= V || r.z >= V || (r.x == 0u && r.w == 0u && !allow_zero);
+        if (bad) {
+            atomicOr(&cnt->flag, 1);
+        } else if (inv) {
+            r.y = __ldg(inv + r.y);
+            r.z = __ldg(inv + r.z);
+        }
+        out[i] = r;
+        const uint32_t k = bad ? 0u : r.y;   // an invalid batch is rejected whole; its records go to vertex 0
+        key[i] = k;
+        const bool own = atomicCAS(&vslot[k], EMPTY_KEY, (uint32_t)i) == EMPTY_KEY;
+        otix[i] = own ? (uint32_t)atomicAdd(&bcnt[k >> SEG_BSH], 1ull) : EMPTY_KEY;
+    }
+}
+
+// touched id t = bin offset + rank in bin; per-id record counts
+__global__ void k_seg_count(uint64_t n, const uint32_t *__restrict__ key, uint32_t *__restrict__ otix,
+                            const uint32_t *__restrict__ vslot, const uint64_t *__restrict__ boff,
+                            uint32_t *__restrict__ kt, uint32_t *__restrict__ tv, unsigned long long *cnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t k = key[i];
+        const uint32_t o = vslot[k];
+        const uint32_t t = (uint32_t)boff[k >> SEG_BSH] + otix[o];
+        kt[i] = t;
+        if (o == (uint32_t)i) tv[t] = k;
+        atomicAdd(&cnt[t], 1ull);
+    }
+}
+
+// places every record in its segment (any order), releases the vertex slots
+__global__ void k_seg_place(uint64_t n, const uint32_t *__restrict__ key, const uint32_t *__restrict__ otix,
+                            const uint32_t *__restrict__ kt, unsigned long long *cnt, const uint64_t *__restrict__ off,
+                            uint32_t *__restrict__ sv, uint32_t *__restrict__ seg, uint32_t *vslot,
+                            const unsigned long long *pnt) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = kt[i];
+        const unsigned long long r = atomicAdd(&cnt[t], ~0ull);   // old count: ranks n_t - 1 .. 0
+        sv[off[t] + r - 1] = (uint32_t)i;
+        if (otix[i] != EMPTY_KEY) {
+            seg[t] = (uint32_t)off[t];
+            vslot[key[i]] = EMPTY_KEY;
+        }
+        if (i == 0) seg[*pnt] = (uint32_t)n;
+    }
+}
+
+// batch order inside each segment: short segments by one thread (insertion sort), longer
+// ones are listed for k_seg_order_long
+__global__ void k_seg_order(const uint32_t *__restrict__ seg, uint32_t *__restrict__ sv, const unsigned long long *pnt,
+                            uint32_t *__restrict__ longs, uint32_t *nlong) {
+    const uint32_t nt = (uint32_t)*pnt;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
+        const uint32_t b = seg[t], e = seg[t + 1];
+        if (e - b < 2) continue;
+        if (e - b > SEG_SHORT) {
+            longs[atomicAdd(nlong, 1u)] = t;
+            continue;
+        }
+        uint32_t x[SEG_SHORT];
+        for (uint32_t j = 0; j < e - b; j++) {
+            const uint32_t v = sv[b + j];
+            uint32_t p = j;
+            while (p > 0 && x[p - 1] > v) {
+                x[p] = x[p - 1];
+                p--;
+            }
+            x[p] = v;
+        }
+        for (uint32_t j = 0; j < e - b; j++) sv[b + j] = x[j];
+    }
+}
+
+// one block per long segment: bitonic sort of its record indices in shared memory; a segment
+// above SEG_LONG_MAX records sets flag 8 and the batch is re-segmented by the radix sort
+__global__ void __launch_bounds__(1024) k_seg_order_long(const uint32_t *__restrict__ seg, uint32_t *__restrict__ sv,
+                                                         const uint32_t *__restrict__ longs, const uint32_t *nlong,
+                                                         UpdCounters *cnt) {
+    __shared__ uint32_t x[SEG_LONG_MAX];
+    const uint32_t nl = *nlong;
+    for (uint32_t j = blockIdx.x; j < nl; j += gridDim.x) {
+        const uint32_t t = longs[j];
+        const uint32_t b = seg[t], len = seg[t + 1] - b;
+        if (len > SEG_LONG_MAX) {
+            if (threadIdx.x == 0) atomicOr(&cnt->flag, 8);
+            continue;
+        }
+        const uint32_t P = next_pow2(len);
+        for (uint32_t q = threadIdx.x; q < P; q += blockDim.x) x[q] = q < len ? sv[b + q] : 0xFFFFFFFFu;
+        __syncthreads();
+        for (uint32_t k = 2; k <= P; k <<= 1) {
+            for (uint32_t h = k >> 1; h > 0; h >>= 1) {
+                for (uint32_t q = threadIdx.x; q < P; q += blockDim.x) {
+                    const uint32_t r = q ^ h;
+                    if (r > q) {
+                        const uint32_t u = x[q], v = x[r];
+                        if ((u > v) == ((q & k) == 0)) {
+                            x[q] = v;
+                            x[r] = u;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        for (uint32_t q = threadIdx.x; q < len; q += blockDim.x) sv[b + q] = x[q];
+        __syncthreads();
+    }
+}
+
 // ------------------------------------------------------------------ per-vertex pre-batch view
 struct OldGroups {
     uint32_t mask;      // nonempty groups (bit k)
@@ -876,7 +1006,9 @@ __global__ void __launch_bounds__(LT) k_upd_mutate_block(const MutateArgs a, con
     }
 }
 
-__global__ void k_upd_stats(const uint32_t *__restrict__ vstats, uint32_t ntouch, unsigned long long *__restrict__ out) {
+__global__ void k_upd_stats(const uint32_t *__restrict__ vstats, uint32_t ntouch, unsigned long long *__restrict__ out,
+                            const unsigned long long *pnt = nullptr) {
+    if (pnt) ntouch = (uint32_t)*pnt;   // one-sync route: the count is on the device
     __shared__ unsigned long long acc[VST];
     if (threadIdx.x < VST) acc[threadIdx.x] = 0;
     __syncthreads();
@@ -1099,10 +1231,11 @@ __global__ void __launch_bounds__(1024) k_upd_fast(const FastArgs fa) {
 // through the batched pipeline and relaunches on the next record.
 static constexpr uint32_t SQ_N = 64;
 static constexpr unsigned long long SQ_IDLE_NS = 2000000ull;
-struct StreamSlot {
+struct alignas(32) StreamSlot {
     unsigned int seq;         // record k is valid when seq == k + 1 ...
     unsigned int gen;         // ... for the kernel generation gen only
-    unsigned int pad[2];
+    unsigned int chk;         // = seq, written first (the host writes chk, rec, gen, seq in order)
+    unsigned int pad;
     uint4 rec;
 };
 struct StreamQ {
@@ -1125,6 +1258,22 @@ __device__ __forceinline__ unsigned int ld_volatile_u32(const unsigned int *p) {
     return *reinterpret_cast<const volatile unsigned int *>(p);
 }
 
+// one 32 B system-scope load of a whole slot (LDG.E.256.STRONG.SYS): a single PCIe read of
+// one host cache line, so seq and the record it guards come from one snapshot (x86 stores
+// become visible in program order: a snapshot holding seq = k + 1 holds chk, rec and gen too)
+struct SlotView {
+    unsigned int seq, gen, chk, pad;
+    uint4 rec;
+};
+__device__ __forceinline__ SlotView ld_slot(const StreamSlot *p) {
+    SlotView v;
+    asm volatile("ld.relaxed.sys.global.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v.seq), "=r"(v.gen), "=r"(v.chk), "=r"(v.pad), "=r"(v.rec.x), "=r"(v.rec.y), "=r"(v.rec.z),
+                   "=r"(v.rec.w)
+                 : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ uint4 ld_volatile_u4(const uint4 *p) {
     uint4 v;
     asm volatile("ld.volatile.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
@@ -1142,17 +1291,18 @@ __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *
         if (threadIdx.x == 0) {
             unsigned int c = 1;
             const unsigned long long t0 = globaltimer_ns();
-            for (;;) {
-                const StreamSlot *sl = &q->slot[k % SQ_N];
-                if (ld_volatile_u32(&sl->seq) == k + 1 && ld_volatile_u32(&sl->gen) == gen) {
-                    __threadfence_system();
-                    rec = ld_volatile_u4(&sl->rec);
+            const StreamSlot *sl = &q->slot[k % SQ_N];
+            for (unsigned int poll = 0;; poll++) {
+                const SlotView v = ld_slot(sl);   // back-to-back polls: one PCIe read each
+                if (v.seq == k + 1 && v.chk == k + 1 && v.gen == gen) {
+                    rec = v.rec;
                     c = 0;
                     break;
                 }
                 // stopped, or idle: exit without taking record k (the host relaunches)
-                if (ld_volatile_u32(&q->run_gen) != gen || globaltimer_ns() - t0 > SQ_IDLE_NS) break;
-                __nanosleep(32);
+                if ((poll & 3u) == 3u &&
+                    (ld_volatile_u32(&q->run_gen) != gen || globaltimer_ns() - t0 > SQ_IDLE_NS))
+                    break;
             }
             cmd = c;
         }
@@ -1535,16 +1685,21 @@ static inline unsigned warp_grid(uint64_t units, unsigned cap) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, cap));
 }
 
-// Bulk-synchronous batch (update_bsp.cuh) over the touched vertices of a sorted,
-// segmented batch.  Touched vertices are processed in sub-batches of at most
-// BSP_MAXT (vertices are independent, all sub-batches use epoch e); the pool
-// demand of the whole batch is reserved before anything is mutated.
-static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t *sv, const uint32_t *seg,
-                              const uint32_t *tv, uint64_t ntouch, uint32_t e, UpdCounters *dc,
-                              unsigned long long *dstats, cudaStream_t s) {
-    uint64_t maxt = BSP_MAXT;   // BINGO_BSP_MAXT: smaller sub-batches (tests)
+// touched vertices per sub-batch (BINGO_BSP_MAXT: smaller sub-batches, tests)
+static uint64_t bsp_maxt() {
+    uint64_t maxt = BSP_MAXT;
     if (const char *ev = getenv("BINGO_BSP_MAXT")) maxt = std::max<uint64_t>(1, strtoull(ev, nullptr, 10));
-    const uint64_t ntmax = std::min<uint64_t>(ntouch, maxt);
+    return maxt;
+}
+
+// per-vertex state of a (sub-)batch of up to ntmax touched vertices, carved from bscratch
+struct BspBufs {
+    uint64_t *p_copy, *p_sel, *p_grp, *p_all, *scr_need, *scr_off, *stmp;
+    uint32_t *vstats;
+    BspTotals *dt;
+    int *abort;
+};
+static bingo_status bsp_scratch(bingo_graph *g, uint64_t ntmax, BspArgs &a, BspBufs &b) {
     size_t vb = 0;
     {
         auto add = [&](size_t x) { vb = ((vb + 255) & ~(size_t)255) + x; };
@@ -1563,20 +1718,14 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         add(8 * ntmax);
         add(4 * ntmax);
         add(4 * ntmax);
+        add(4 * ntmax);
+        add(8 * 33 * ntmax);
+        add(64);
         add(64);
         vb += 4096;
     }
     if (!ensure_buf(g, g->bscratch, g->bscratch_bytes, vb)) return BINGO_E_NOMEM;
-    if (g->hscratch_bytes < sizeof(BspTotals)) {
-        if (g->hscratch) cudaFreeHost(g->hscratch);
-        g->hscratch = nullptr;
-        g->hscratch_bytes = 0;
-        UCK(cudaMallocHost(&g->hscratch, sizeof(BspTotals)));
-        g->hscratch_bytes = sizeof(BspTotals);
-    }
-    BspTotals *ht = (BspTotals *)g->hscratch;
     Carve cv{(char *)g->bscratch, 0};
-    BspArgs a;
     memset(&a, 0, sizeof(a));
     a.vL = cv.take<uint32_t>(ntmax);
     a.vq = cv.take<uint32_t>(ntmax);
@@ -1592,23 +1741,99 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     a.cc_sel = cv.take<uint64_t>(ntmax + 1);
     a.cc_grp = cv.take<uint64_t>(ntmax + 1);
     a.cc_all = cv.take<uint64_t>(ntmax + 1);
-    uint64_t *p_copy = cv.take<uint64_t>(ntmax + 2), *p_sel = cv.take<uint64_t>(ntmax + 2),
-             *p_grp = cv.take<uint64_t>(ntmax + 2), *p_all = cv.take<uint64_t>(ntmax + 2);
-    a.p_copy = p_copy;
-    a.p_sel = p_sel;
-    a.p_grp = p_grp;
-    a.p_all = p_all;
-    uint64_t *scr_need = cv.take<uint64_t>(ntmax + 1), *scr_off = cv.take<uint64_t>(ntmax + 2);
-    uint32_t *vstats = cv.take<uint32_t>((size_t)VST * ntmax);
-    uint64_t *stmp = cv.take<uint64_t>(5 * scan_tmp_words(ntmax + 1));
-    BspTotals *dt = cv.take<BspTotals>(1);
+    b.p_copy = cv.take<uint64_t>(ntmax + 2);
+    b.p_sel = cv.take<uint64_t>(ntmax + 2);
+    b.p_grp = cv.take<uint64_t>(ntmax + 2);
+    b.p_all = cv.take<uint64_t>(ntmax + 2);
+    a.p_copy = b.p_copy;
+    a.p_sel = b.p_sel;
+    a.p_grp = b.p_grp;
+    a.p_all = b.p_all;
+    b.scr_need = cv.take<uint64_t>(ntmax + 1);
+    b.scr_off = cv.take<uint64_t>(ntmax + 2);
+    b.vstats = cv.take<uint32_t>((size_t)VST * ntmax);
+    b.stmp = cv.take<uint64_t>(5 * scan_tmp_words(ntmax + 1));
+    b.dt = cv.take<BspTotals>(1);
     a.hubs = cv.take<uint32_t>(ntmax);
     a.bigs = cv.take<uint32_t>(ntmax);
     a.vnbo = cv.take<uint64_t>(ntmax);
     a.vnbfull = cv.take<uint32_t>(ntmax);
     a.vhix = cv.take<uint32_t>(ntmax);
+    a.vrank = cv.take<uint32_t>(ntmax);
+    a.sorts = cv.take<uint2>(ntmax * 33);
     a.nhubs = cv.take<uint32_t>(16);
     a.nbigs = a.nhubs + 1;
+    b.abort = cv.take<int>(16);
+    return BINGO_OK;
+}
+
+// per-chunk-item counts and their prefixes (hole ranks, group-hole ranks), sized with
+// slack so later batches of the one-sync route fit without a host round trip
+static bingo_status bsp_items(bingo_graph *g, uint64_t sel, uint64_t grp, BspArgs &a, uint64_t *&itmp) {
+    if (sel > g->isc_sel || grp > g->isc_grp || !g->iscratch) {
+        const uint64_t ns = std::max<uint64_t>(g->isc_sel, sel + sel / 2 + 64);
+        const uint64_t ng = std::max<uint64_t>(g->isc_grp, grp + grp / 2 + 64);
+        size_t ib = 0;
+        auto add = [&](size_t x) { ib = ((ib + 255) & ~(size_t)255) + x; };
+        add(8 * (ns + 1)); add(8 * (ns + 2)); add(8 * (ng + 1)); add(8 * (ng + 2));
+        add(8 * scan_tmp_words(std::max(ns, ng) + 1));
+        ib += 1024;
+        if (!ensure_buf(g, g->iscratch, g->iscratch_bytes, ib)) return BINGO_E_NOMEM;
+        g->isc_sel = ns;
+        g->isc_grp = ng;
+    }
+    Carve ic{(char *)g->iscratch, 0};
+    a.icnt = ic.take<uint64_t>(g->isc_sel + 1);
+    a.ipref = ic.take<uint64_t>(g->isc_sel + 2);
+    a.gcnt = ic.take<uint64_t>(g->isc_grp + 1);
+    a.gpref = ic.take<uint64_t>(g->isc_grp + 2);
+    itmp = ic.take<uint64_t>(scan_tmp_words(std::max(g->isc_sel, g->isc_grp) + 1));
+    return BINGO_OK;
+}
+
+// delete scratch words (per-vertex bitmaps and hashes), grown with slack
+static bingo_status bsp_vscratch(bingo_graph *g, uint64_t words) {
+    const size_t need = 4 * (words + 64);
+    if (g->vscratch_bytes >= need) return BINGO_OK;
+    return ensure_buf(g, g->vscratch, g->vscratch_bytes, need + need / 2) ? BINGO_OK : BINGO_E_NOMEM;
+}
+
+static bingo_status ensure_aux_stream(bingo_graph *g) {
+    if (g->aux_stream) return BINGO_OK;
+    if (cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming) != cudaSuccess)
+        return BINGO_E_CUDA;
+    return BINGO_OK;
+}
+
+// Bulk-synchronous batch (update_bsp.cuh) over the touched vertices of a sorted,
+// segmented batch.  Touched vertices are processed in sub-batches of at most
+// BSP_MAXT (vertices are independent, all sub-batches use epoch e); the pool
+// demand of the whole batch is reserved before anything is mutated.
+static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t *sv, const uint32_t *seg,
+                              const uint32_t *tv, uint64_t ntouch, uint32_t e, UpdCounters *dc,
+                              unsigned long long *dstats, cudaStream_t s) {
+    const uint64_t maxt = bsp_maxt();
+    const uint64_t ntmax = std::min<uint64_t>(ntouch, maxt);
+    BspArgs a;
+    BspBufs b;
+    {
+        const bingo_status st = bsp_scratch(g, ntmax, a, b);
+        if (st != BINGO_OK) return st;
+    }
+    if (g->hscratch_bytes < sizeof(BspTotals)) {
+        if (g->hscratch) cudaFreeHost(g->hscratch);
+        g->hscratch = nullptr;
+        g->hscratch_bytes = 0;
+        UCK(cudaMallocHost(&g->hscratch, sizeof(BspTotals)));
+        g->hscratch_bytes = sizeof(BspTotals);
+    }
+    BspTotals *ht = (BspTotals *)g->hscratch;
+    uint64_t *scr_need = b.scr_need, *scr_off = b.scr_off, *stmp = b.stmp;
+    uint64_t *p_copy = b.p_copy, *p_sel = b.p_sel, *p_grp = b.p_grp, *p_all = b.p_all;
+    uint32_t *vstats = b.vstats;
+    BspTotals *dt = b.dt;
     auto refresh = [&]() {
         fill_mutate_common(g, a.g, e);
         a.g.recs = recs;
@@ -1620,11 +1845,14 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     };
     refresh();
     const bool multi = ntouch > maxt;
-    const unsigned WG = 148 * 16, IG = 148 * 32;
+    const unsigned WG = 148 * 16, IG = 148 * 8;
+    BspCaps nocaps;
+    memset(&nocaps, 0, sizeof(nocaps));
     if (multi) {
         // demand of the whole batch first (read-only pass)
         a.t0 = 0;
         a.nt = (uint32_t)ntouch;
+        a.gks = a.nt;
         k_bsp_plan<<<warp_grid(ntouch, WG), MT, 0, s>>>(a, scr_need, dc, true, false);
         bingo_count_launch();
         UCK(cudaGetLastError());
@@ -1640,8 +1868,9 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     for (uint64_t t0 = 0; t0 < ntouch; t0 += maxt) {
         a.t0 = (uint32_t)t0;
         a.nt = (uint32_t)std::min<uint64_t>(maxt, ntouch - t0);
+        a.gks = a.nt;
         const uint32_t nt = a.nt;
-        UCK(cudaMemsetAsync(a.nhubs, 0, 16, s));   // hubs, bigs, rebuild fills
+        UCK(cudaMemsetAsync(a.nhubs, 0, 32, s));   // hubs, bigs, rebuild fills, -, rank hubs, big sorts
         UCK(cudaMemsetAsync(a.vhix, 0, 4 * (size_t)nt, s));
         k_bsp_plan<<<warp_grid(nt, WG), MT, 0, s>>>(a, scr_need, dc, !multi, true);
         bingo_count_launch();
@@ -1652,7 +1881,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             UCK(exclusive_scan_u64_multi(ins, outs, g->nbt ? 5 : 4, nt, stmp, s));
             if (!g->nbt) UCK(cudaMemsetAsync(p_all + nt, 0, 8, s));
         }
-        k_bsp_totals<<<1, 32, 0, s>>>(a, dc, scr_off, dt);
+        k_bsp_totals<<<1, 32, 0, s>>>(a, dc, scr_off, dt, nocaps, nullptr);
         bingo_count_launch();
         UCK(cudaGetLastError());
         g_trace.mark("plan+scans", s);
@@ -1668,25 +1897,14 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         // ---- from here on the (sub-)batch is applied
         const uint64_t sel = ht->sel, grp = ht->grp, copy = ht->copy, all = ht->all;
         if (ht->scr) {
-            if (!ensure_buf(g, g->vscratch, g->vscratch_bytes, 4 * (ht->scr + 64))) return BINGO_E_NOMEM;
+            const bingo_status st = bsp_vscratch(g, ht->scr);
+            if (st != BINGO_OK) return st;
             a.g.scr = (uint32_t *)g->vscratch;
         }
         uint64_t *itmp = nullptr;
         if (sel || grp) {
-            size_t ib = 0;
-            auto add = [&](size_t x) { ib = ((ib + 255) & ~(size_t)255) + x; };
-            add(8 * (sel + 1)); add(8 * (sel + 2)); add(8 * (grp + 1)); add(8 * (grp + 2));
-            add(8 * scan_tmp_words(std::max(sel, grp) + 1));
-            ib += 1024;
-            if (!ensure_buf(g, g->iscratch, g->iscratch_bytes, ib)) return BINGO_E_NOMEM;
-            Carve ic{(char *)g->iscratch, 0};
-            a.icnt = ic.take<uint64_t>(sel + 1);
-            uint64_t *ipref = ic.take<uint64_t>(sel + 2);
-            a.gcnt = ic.take<uint64_t>(grp + 1);
-            uint64_t *gpref = ic.take<uint64_t>(grp + 2);
-            a.ipref = ipref;
-            a.gpref = gpref;
-            itmp = ic.take<uint64_t>(scan_tmp_words(std::max(sel, grp) + 1));
+            const bingo_status st = bsp_items(g, sel, grp, a, itmp);
+            if (st != BINGO_OK) return st;
         }
 #define BSP_LAUNCH(kern, grid, strm, ...)                            \
         do {                                                         \
@@ -1699,10 +1917,9 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         // two independent chains over disjoint vertex sets (shared state: bump
         // counters, atomics only): small vertices on `s`, large ones on the side stream
         const bool side = ht->bigs != 0;
-        if (side && !g->aux_stream) {
-            UCK(cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking));
-            UCK(cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming));
-            UCK(cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming));
+        if (side) {
+            const bingo_status st = ensure_aux_stream(g);
+            if (st != BINGO_OK) return upd_cuda_fail(g, cudaGetLastError(), "aux stream");
         }
         cudaStream_t sh = side ? g->aux_stream : s;
         if (side) {
@@ -1721,6 +1938,11 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             if (hix) BSP_LAUNCH(k_hix_select, warp_grid(ht->hubs, WG), sh, a);
             BSP_LAUNCH(k_bsp_finalize, warp_grid(ht->hubs, WG), sh, a, true);
             if (hix) BSP_LAUNCH(k_hix_del, warp_grid(ht->hubs, WG), sh, a);
+            BSP_LAUNCH(k_bsp_hub_sort, warp_grid(ht->hubs, WG), sh, a);
+            k_bsp_sort_big<<<148, 256, 0, sh>>>(a);
+            bingo_count_launch();
+            UCK(cudaGetLastError());
+            UCK(cudaMemsetAsync(a.nhubs + 5, 0, 4, sh));
             g_trace.mark("hub: select+finalize", sh);
             BSP_LAUNCH(k_bsp_hole_count, warp_grid(sel, IG), sh, a, sel);
             UCK(exclusive_scan_u64(a.icnt, const_cast<uint64_t *>(a.ipref), sel, itmp, sh));
@@ -1732,6 +1954,10 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
                 BSP_LAUNCH(k_bsp_grp_count, warp_grid(grp, IG), sh, a, grp);
                 UCK(exclusive_scan_u64(a.gcnt, const_cast<uint64_t *>(a.gpref), grp, itmp, sh));
                 BSP_LAUNCH(k_bsp_grp_write, warp_grid(grp, IG), sh, a, grp);
+                BSP_LAUNCH(k_bsp_grp_sort, warp_grid(ht->hubs, WG), sh, a);
+                k_bsp_sort_big<<<148, 256, 0, sh>>>(a);
+                bingo_count_launch();
+                UCK(cudaGetLastError());
                 BSP_LAUNCH(k_bsp_grp_tail, warp_grid(ht->hubs, WG), sh, a);
                 g_trace.mark("hub: group fronts+tails", sh);
             }
@@ -1766,6 +1992,142 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
     return BINGO_OK;
 }
 
+// One-sync bulk-synchronous batch: the whole pipeline of apply_bsp is enqueued at once,
+// before the host knows the touched-vertex count (*pnt, on the device) or any total of the
+// plan.  Kernels read those on the device (BspArgs::pnt; item loops take their totals from
+// the plan's prefix sums; grids are sized for the capacity, n touched vertices at most), and
+// k_bsp_totals checks the batch against the pools and scratch allocated when it was
+// enqueued.  If anything is short (or the batch is invalid) every mutating kernel returns at
+// once, and the caller, after its single sync, grows what is short and re-runs the batch on
+// the synchronous route (apply_bsp): the graph is untouched until the gate passes.
+static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uint32_t *sv, const uint32_t *seg,
+                                    const uint32_t *tv, const unsigned long long *pnt, uint64_t nmax, uint32_t e,
+                                    UpdCounters *dc, unsigned long long *dstats, cudaStream_t s,
+                                    BspTotals **dtot) {
+    const uint64_t ntmax = std::max<uint64_t>(nmax, 1);
+    BspArgs a;
+    BspBufs b;
+    {
+        const bingo_status st = bsp_scratch(g, ntmax, a, b);
+        if (st != BINGO_OK) return st;
+    }
+    uint64_t *itmp = nullptr;
+    {
+        const bingo_status st = bsp_items(g, 0, 0, a, itmp);
+        if (st != BINGO_OK) return st;
+    }
+    {
+        const bingo_status st = ensure_aux_stream(g);
+        if (st != BINGO_OK) return upd_cuda_fail(g, cudaGetLastError(), "aux stream");
+    }
+    fill_mutate_common(g, a.g, e);
+    a.g.recs = recs;
+    a.g.sval = sv;
+    a.g.seg = seg;
+    a.g.tv = tv;
+    a.g.scr_off = b.scr_off;
+    a.g.vstats = b.vstats;
+    a.g.scr = (uint32_t *)g->vscratch;
+    a.t0 = 0;
+    a.nt = 0;
+    a.pnt = pnt;
+    a.gks = (uint32_t)ntmax;
+    a.abort = b.abort;
+    BspCaps caps;
+    memset(&caps, 0, sizeof(caps));
+    caps.arc = g->arc_cap;
+    caps.bkt = g->bkt_cap;
+    caps.mem_units = g->mem_cap / 4;
+    caps.hix = g->hix_cap;
+    caps.hix_on = !hix_disabled();
+    if (caps.hix_on && !g->hixo) caps.hix = 0;   // tables need the offsets first: the sync route allocates them
+    caps.scr_words = g->vscratch_bytes >= 4 * 64 ? g->vscratch_bytes / 4 - 64 : 0;
+    caps.sel = g->isc_sel;
+    caps.grp = g->isc_grp;
+    const unsigned WG = 148 * 16, IG = 148 * 8, HG = 148 * 4;   // IG: item kernels, one wave of contiguous per-warp ranges
+    const unsigned wg = warp_grid(ntmax, WG), hg = warp_grid(ntmax, HG);
+    UCK(cudaMemsetAsync(a.nhubs, 0, 32, s));
+    UCK(cudaMemsetAsync(a.vhix, 0, 4 * (size_t)ntmax, s));
+    k_bsp_plan<<<wg, MT, 0, s>>>(a, b.scr_need, dc, true, true);
+    bingo_count_launch();
+    UCK(cudaGetLastError());
+    {
+        const uint64_t *ins[5] = {b.scr_need, a.cc_copy, a.cc_sel, a.cc_grp, a.cc_all};
+        uint64_t *outs[5] = {b.scr_off, b.p_copy, b.p_sel, b.p_grp, b.p_all};
+        UCK(exclusive_scan_u64_multi_dn(ins, outs, 5, pnt, ntmax, b.stmp, s));
+    }
+    k_bsp_totals<<<1, 32, 0, s>>>(a, dc, b.scr_off, b.dt, caps, b.abort);
+    bingo_count_launch();
+    UCK(cudaGetLastError());
+    *dtot = b.dt;
+    g_trace.mark("plan+scans+gate", s);
+#define BSP_LAUNCH(kern, grid, strm, ...)                            \
+    do {                                                             \
+        kern<<<(grid), MT, 0, (strm)>>>(__VA_ARGS__);                \
+        bingo_count_launch();                                        \
+        UCK(cudaGetLastError());                                     \
+    } while (0)
+    BSP_LAUNCH(k_bsp_alloc_insert, wg, s, a);
+    g_trace.mark("alloc_insert", s);
+    cudaStream_t sh = g->aux_stream;
+    UCK(cudaEventRecord(g->ev_fork, s));
+    UCK(cudaStreamWaitEvent(sh, g->ev_fork, 0));
+    // -- large vertices (side stream); item totals and hub counts are read on the device
+    BSP_LAUNCH(k_bsp_copy, IG, sh, a, 0ull);
+    const bool hix = g->hixo != nullptr && !hix_disabled();
+    if (hix) {
+        BSP_LAUNCH(k_hix_prep, hg, sh, a);
+        BSP_LAUNCH(k_hix_build, IG, sh, a, 0ull);
+    }
+    BSP_LAUNCH(k_bsp_select, IG, sh, a, 0ull);
+    if (hix) BSP_LAUNCH(k_hix_select, hg, sh, a);
+    BSP_LAUNCH(k_bsp_finalize, hg, sh, a, true);
+    if (hix) BSP_LAUNCH(k_hix_del, hg, sh, a);
+    BSP_LAUNCH(k_bsp_hub_sort, hg, sh, a);
+    k_bsp_sort_big<<<148, 256, 0, sh>>>(a);
+    bingo_count_launch();
+    UCK(cudaGetLastError());
+    UCK(cudaMemsetAsync(a.nhubs + 5, 0, 4, sh));
+    g_trace.mark("hub: select+finalize", sh);
+    BSP_LAUNCH(k_bsp_hole_count, IG, sh, a, 0ull);
+    UCK(exclusive_scan_u64_multi_dn(&a.icnt, const_cast<uint64_t **>(&a.ipref), 1, &b.dt->sel, g->isc_sel, itmp, sh));
+    BSP_LAUNCH(k_bsp_hole_write, IG, sh, a, 0ull);
+    BSP_LAUNCH(k_bsp_tail, hg, sh, a);
+    g_trace.mark("hub: holes+tail", sh);
+    if (hix) BSP_LAUNCH(k_hix_ins, hg, sh, a);
+    BSP_LAUNCH(k_bsp_grp_count, IG, sh, a, 0ull);
+    UCK(exclusive_scan_u64_multi_dn(&a.gcnt, const_cast<uint64_t **>(&a.gpref), 1, &b.dt->grp, g->isc_grp, itmp, sh));
+    BSP_LAUNCH(k_bsp_grp_write, IG, sh, a, 0ull);
+    BSP_LAUNCH(k_bsp_grp_sort, hg, sh, a);
+    k_bsp_sort_big<<<148, 256, 0, sh>>>(a);
+    bingo_count_launch();
+    UCK(cudaGetLastError());
+    BSP_LAUNCH(k_bsp_grp_tail, hg, sh, a);
+    g_trace.mark("hub: group fronts+tails", sh);
+    BSP_LAUNCH(k_bsp_rebuild_big, hg, sh, a);
+    k_bsp_rebuild_fill<<<148 * 2, LT, 0, sh>>>(a);
+    bingo_count_launch();
+    UCK(cudaGetLastError());
+    g_trace.mark("hub: rebuild_big", sh);
+    // -- small vertices
+    BSP_LAUNCH(k_bsp_finalize, wg, s, a, false);
+    BSP_LAUNCH(k_bsp_rebuild, wg, s, a);
+    g_trace.mark("small-vertex chain", s);
+    UCK(cudaEventRecord(g->ev_join, sh));
+    UCK(cudaStreamWaitEvent(s, g->ev_join, 0));
+    g_trace.mark("join hub chain", s);
+    if (g->nbt) {
+        BSP_LAUNCH(k_bsp_nb_incr, wg, s, a);
+        BSP_LAUNCH(k_bsp_nb_clear, IG, s, a, 0ull);
+        BSP_LAUNCH(k_bsp_nb_fill, IG, s, a, 0ull);
+    }
+#undef BSP_LAUNCH
+    k_upd_stats<<<(unsigned)std::min<uint64_t>((ntmax + 255) / 256, 148), 256, 0, s>>>(b.vstats, 0, dstats, pnt);
+    bingo_count_launch();
+    UCK(cudaGetLastError());
+    return BINGO_OK;
+}
+
 static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
                                  const unsigned long long *dstats, bingo_update_stats *stats, cudaStream_t s);
 
@@ -1782,6 +2144,39 @@ static bool use_legacy_mutate() {
     const char *ev = getenv("BINGO_UPD_LEGACY");
     return ev && ev[0] == '1';
 }
+
+// BINGO_UPD_RADIX_FRONT=1: segment every batch with the radix sort (A/B, tests)
+static bool use_radix_front() {
+    const char *ev = getenv("BINGO_UPD_RADIX_FRONT");
+    return ev && ev[0] == '1';
+}
+
+// BINGO_UPD_SYNC=1: the bulk-synchronous route with a host round trip after the front end
+// and after the plan (apply_bsp) instead of the one-sync route (tests, A/B)
+static bool use_sync_route() {
+    const char *ev = getenv("BINGO_UPD_SYNC");
+    return ev && ev[0] == '1';
+}
+
+// pinned host staging of the one-sync route: the plan totals / gate and the statistics
+struct UpdHost {
+    BspTotals t;
+    unsigned long long stats[32];
+};
+static UpdHost *upd_host(bingo_graph *g) {
+    if (!g->uhost) {
+        void *h = nullptr;
+        if (cudaMallocHost(&h, sizeof(UpdHost)) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        g->uhost = h;
+    }
+    return (UpdHost *)g->uhost;
+}
+
+static bingo_status finish_batch_host(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
+                                      const unsigned long long *hs, bingo_update_stats *stats);
 
 static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const double *wf, uint64_t n,
                                uint32_t flags, bingo_update_stats *stats, void *stream);
@@ -1802,6 +2197,16 @@ struct DinsGuard {
     bingo_graph *g;
     ~DinsGuard() { g->cur_dins = nullptr; }
 };
+
+// the batch again, segmented by the radix sort (a segment exceeded SEG_LONG_MAX records;
+// nothing was mutated)
+static bingo_status apply_radix_front(bingo_graph *g, const bingo_update *batch, const double *wf, uint64_t n,
+                                      uint32_t flags, bingo_update_stats *stats, void *stream) {
+    g->radix_front = true;
+    const bingo_status st = apply_impl(g, batch, wf, n, flags, stats, stream);
+    g->radix_front = false;
+    return st;
+}
 
 static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const double *wf, uint64_t n,
                                uint32_t flags, bingo_update_stats *stats, void *stream) {
@@ -1872,7 +2277,30 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     UCK(cudaMemsetAsync(dc, 0, sizeof(UpdCounters), s));
     UCK(cudaMemsetAsync(dstats, 0, 8 * 32, s));
     const unsigned gb = (unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 16);
-    k_upd_validate<<<gb, 256, 0, s>>>(src_recs, drec, n, g->V, g->inv, k0, v0, dc, fm);
+    // segmentation by source (a7): claim + count + place + in-segment order by default; the
+    // 3-pass radix sort when BINGO_UPD_RADIX_FRONT=1 or a segment exceeds SEG_LONG_MAX records
+    const bool radix_front = g->radix_front || use_radix_front();
+    uint32_t *nlong = reinterpret_cast<uint32_t *>(head_ex + n + 1);
+    const uint64_t nbins = ((uint64_t)std::max<uint32_t>(g->V, 1) + (1u << SEG_BSH) - 1) >> SEG_BSH;
+    uint64_t *bcnt = nullptr, *boff = nullptr, *btmp = nullptr;
+    if (!radix_front) {
+        if (!g->vslot) {
+            const size_t vs = 4 * (size_t)std::max<uint32_t>(g->V, 1);
+            const size_t words = (nbins + 1) + (nbins + 2) + scan_tmp_words(nbins + 1);
+            g->vslot = (uint32_t *)bingo_dev_alloc(g, vs + 8 * words + 256);
+            if (!g->vslot) return BINGO_E_NOMEM;
+            UCK(cudaMemsetAsync(g->vslot, 0xFF, vs, s));
+        }
+        bcnt = reinterpret_cast<uint64_t *>(((uintptr_t)(g->vslot + std::max<uint32_t>(g->V, 1)) + 255) & ~(uintptr_t)255);
+        boff = bcnt + nbins + 1;
+        btmp = boff + nbins + 2;
+        UCK(cudaMemsetAsync(bcnt, 0, 8 * nbins, s));
+        UCK(cudaMemsetAsync(head, 0, 8 * n, s));   // per-id record counts
+        k_seg_claim<<<gb, 256, 0, s>>>(src_recs, drec, n, g->V, g->inv, g->vslot, k0, v0,
+                                       reinterpret_cast<unsigned long long *>(bcnt), nlong, dc, fm);
+    } else {
+        k_upd_validate<<<gb, 256, 0, s>>>(src_recs, drec, n, g->V, g->inv, k0, v0, dc, fm);
+    }
     bingo_count_launch();
     UCK(cudaGetLastError());
     DinsGuard dguard{g};
@@ -1887,23 +2315,84 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
         UCK(cudaGetLastError());
         g->cur_dins = dins;
     }
-    bool in1 = false;
-    UCK(radix_sort_pairs(k0, v0, k1, v1, n, key_bits_for(g->V), rtmp, s, &in1));
-    const uint32_t *sk = in1 ? k1 : k0;
-    const uint32_t *sv = in1 ? v1 : v0;
-    k_upd_heads<<<gb, 256, 0, s>>>(sk, n, head);
-    bingo_count_launch();
-    UCK(cudaGetLastError());
-    UCK(exclusive_scan_u64(head, head_ex, n, stmp, s));   // head_ex[n] = #touched
-    k_upd_segments<<<gb, 256, 0, s>>>(head_ex, sk, n, seg, tv);
-    bingo_count_launch();
-    UCK(cudaGetLastError());
+    const uint32_t *sv;
+    const unsigned long long *d_ntouch;
+    if (!radix_front) {
+        UCK(exclusive_scan_u64(bcnt, boff, nbins, btmp, s));   // boff[nbins] = #touched
+        const unsigned long long *ntc = reinterpret_cast<const unsigned long long *>(boff + nbins);
+        unsigned long long *cnt = reinterpret_cast<unsigned long long *>(head);
+        k_seg_count<<<gb, 256, 0, s>>>(n, k0, v0, g->vslot, boff, k1, tv, cnt);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        {
+            const uint64_t *in = head;
+            uint64_t *out = head_ex;
+            UCK(exclusive_scan_u64_multi_dn(&in, &out, 1, ntc, n, stmp, s));
+        }
+        k_seg_place<<<gb, 256, 0, s>>>(n, k0, v0, k1, cnt, head_ex, v1, seg, g->vslot, ntc);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        k_seg_order<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 148 * 8), 256, 0, s>>>(seg, v1, ntc, large_list,
+                                                                                          nlong);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        k_seg_order_long<<<148, 1024, 0, s>>>(seg, v1, large_list, nlong, dc);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        sv = v1;
+        d_ntouch = ntc;
+    } else {
+        bool in1 = false;
+        UCK(radix_sort_pairs(k0, v0, k1, v1, n, key_bits_for(g->V), rtmp, s, &in1));
+        const uint32_t *sk = in1 ? k1 : k0;
+        sv = in1 ? v1 : v0;
+        k_upd_heads<<<gb, 256, 0, s>>>(sk, n, head);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        UCK(exclusive_scan_u64(head, head_ex, n, stmp, s));   // head_ex[n] = #touched
+        k_upd_segments<<<gb, 256, 0, s>>>(head_ex, sk, n, seg, tv);
+        bingo_count_launch();
+        UCK(cudaGetLastError());
+        d_ntouch = reinterpret_cast<const unsigned long long *>(head_ex + n);
+    }
     uint64_t ntouch = 0;
     g_trace.mark("front (validate+sort+seg)", s);
-    UCK(cudaMemcpyAsync(&ntouch, head_ex + n, 8, cudaMemcpyDeviceToHost, s));
-    UCK(cudaStreamSynchronize(s));
-    g_trace.mark("sync #touched", s);
     const uint32_t e = g->epoch + 1;
+    if (!fm && !use_legacy_mutate() && n <= bsp_maxt() && !use_sync_route()) {
+        // one host sync per batch: the plan, the gate and every phase are enqueued at once
+        BspTotals *dtot = nullptr;
+        bingo_status st = apply_bsp_async(g, recs, sv, seg, tv, d_ntouch, n, e, dc, dstats, s, &dtot);
+        if (st != BINGO_OK) return st;
+        UpdHost *hh = upd_host(g);
+        if (!hh) return BINGO_E_NOMEM;
+        UCK(cudaMemcpyAsync(&hh->t, dtot, sizeof(BspTotals), cudaMemcpyDeviceToHost, s));
+        UCK(cudaMemcpyAsync(hh->stats, dstats, sizeof(hh->stats), cudaMemcpyDeviceToHost, s));
+        g_trace.mark("tail (stats)", s);
+        UCK(cudaStreamSynchronize(s));
+        g_trace.mark("sync", s);
+        g_trace.dump();
+        const int ab = hh->t.abort;
+        ntouch = hh->t.nt;
+        if (ab & 1) return BINGO_E_INVAL;
+        if (ab & 4) return BINGO_E_OVERFLOW;
+        if (ab & 8) return apply_radix_front(g, batch, wf, n, flags, stats, stream);
+        if (!ab) return finish_batch_host(g, n, ntouch, e, hh->stats, stats);
+        // something was short: nothing was mutated; the synchronous route grows and applies
+        g->n_sync_reruns++;
+        UCK(cudaMemsetAsync(dc, 0, sizeof(UpdCounters), s));   // the batch is valid (checked above)
+        UCK(cudaMemsetAsync(dstats, 0, 8 * 32, s));
+        st = apply_bsp(g, recs, sv, seg, tv, ntouch, e, dc, dstats, s);
+        if (st != BINGO_OK) return st;
+        return finish_batch(g, n, ntouch, e, dstats, stats, s);
+    }
+    UCK(cudaMemcpyAsync(&ntouch, d_ntouch, 8, cudaMemcpyDeviceToHost, s));
+    {
+        int *hfl = reinterpret_cast<int *>(g->hscratch);
+        UCK(cudaMemcpyAsync(hfl, &dc->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+        UCK(cudaStreamSynchronize(s));
+        if (*hfl & 8) return apply_radix_front(g, batch, wf, n, flags, stats, stream);
+    }
+    g_trace.mark("sync #touched", s);
     if (fm && ntouch) {
         // decimal-member regions for the batch; validation errors and pool growth before any mutation
         k_float_plan<<<(unsigned)std::min<uint64_t>((ntouch + 255) / 256, 148 * 16), 256, 0, s>>>(
@@ -2050,6 +2539,11 @@ static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, ui
     UCK(cudaStreamSynchronize(s));
     g_trace.mark("sync stats", s);
     g_trace.dump();
+    return finish_batch_host(g, n, ntouch, e, hs, stats);
+}
+
+static bingo_status finish_batch_host(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
+                                      const unsigned long long *hs, bingo_update_stats *stats) {
     g->epoch = e;
     // inserted = number of insert records (validated batch)
     uint64_t inserted = 0;
@@ -2221,8 +2715,9 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
         }
         const unsigned gen = g->sq_gen;
         StreamSlot *sl = &q->slot[k % SQ_N];
+        __atomic_store_n(&sl->chk, k + 1, __ATOMIC_RELEASE);
         memcpy((void *)&sl->rec, rec, 16);
-        __atomic_store_n(&sl->gen, gen, __ATOMIC_SEQ_CST);
+        __atomic_store_n(&sl->gen, gen, __ATOMIC_RELEASE);
         __atomic_store_n(&sl->seq, k + 1, __ATOMIC_SEQ_CST);
         bool taken = false;
         for (uint64_t spin = 0;; spin++) {

@@ -38,7 +38,11 @@ namespace bingo {
 
 static constexpr uint32_t CH = 1024;   // adjacency positions / member slots per chunk item (32 per lane)
 static constexpr uint32_t BSP_MAXT = 1u << 21;   // touched vertices per sub-batch (state ~1.1 KB each)
-enum : uint32_t { GK_KIND0 = 0, GK_C, GK_INSK, GK_DELK, GK_MOFF, GK_CAP, GK_ONE, GK_GHO, GK_N };
+enum : uint32_t { GK_KIND0 = 0, GK_C, GK_INSK, GK_DELK, GK_MOFF, GK_CAP, GK_ONE, GK_GHO, GK_GHN, GK_N };
+// hubs whose batch deletes at most SORT_MAX arcs take their holes by sorting their picks and
+// their group holes by one pass over each group front (appends, then a sort); larger ones
+// use the counted-rank passes (k_bsp_hole_count / k_bsp_grp_count + scans)
+static constexpr uint32_t SORT_MAX = 4096;
 
 struct BspArgs {
     MutateArgs g;                  // graph, batch (global touched index), delete scratch, vstats (local)
@@ -57,11 +61,26 @@ struct BspArgs {
     uint32_t *vhix;                // hub delete index: 0 not maintained (invalidated), 1 used, 2 built + used
     uint64_t *vnbo;                // pre-batch nbo[u] (node2vec neighbour sets)
     uint32_t *vnbfull;             // 1: the vertex's neighbour set is rebuilt from its adjacency
+    uint32_t *vrank;               // hubs: 1 = counted-rank passes (N > SORT_MAX), 0 = sorted picks
+    uint2 *sorts;                  // (vertex, 32 = picks | group k) lists longer than a warp, for k_bsp_sort_big
+    // one-sync route (apply_bsp_async): the launches are enqueued before the host knows the
+    // touched-vertex count or the item totals, so kernels read them on the device
+    const unsigned long long *pnt; // non-null: nt = *pnt (t0 = 0); else the host value nt
+    uint32_t gks;                  // stride of the gk slots (>= nt)
+    const int *abort;              // non-null: k_bsp_check's verdict; nonzero = mutate nothing
 };
 
 __device__ __forceinline__ uint32_t *gkp(const BspArgs &a, uint32_t f, uint32_t i) {
-    return a.gk + ((uint64_t)f * a.nt + i) * 32;
+    return a.gk + ((uint64_t)f * a.gks + i) * 32;
 }
+__device__ __forceinline__ uint32_t bsp_nt(const BspArgs &a) {
+    return a.pnt ? (uint32_t)*a.pnt : a.nt;
+}
+// item totals: the host value, or (one-sync route) the prefix total of the plan
+__device__ __forceinline__ uint64_t bsp_total(const BspArgs &a, const uint64_t *pref, uint64_t total) {
+    return a.pnt ? pref[bsp_nt(a)] : total;
+}
+#define BSP_ABORTED(a) ((a).abort && *(volatile const int *)(a).abort)
 
 // per-vertex delete scratch (words from plan: bsp_scr_words)
 struct DelScr {
@@ -120,6 +139,22 @@ __device__ __forceinline__ uint32_t hash_find(const uint32_t *hkey, uint32_t hma
     for (uint64_t it = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; it < (total);    \
          it += ((uint64_t)gridDim.x * blockDim.x) >> 5)
 
+// the owner of item it, given the owner of an earlier item of the same warp
+__device__ __forceinline__ uint32_t owner_next(const uint64_t *pref, uint32_t i, uint64_t it) {
+    while (__ldg(pref + i + 1) <= it) i++;
+    return i;
+}
+// Chunk items [0, total) in one contiguous range per warp; i = the item's owner (largest i
+// with pref[i] <= it).  One binary search per warp, then the owner advances with the items
+// (a hub's items are consecutive), instead of a dependent binary search of ~17 steps per item.
+#define BSP_ITEM_RANGE(it, i, total, pref, n)                                                   \
+    const uint64_t nw_##it = ((uint64_t)gridDim.x * blockDim.x) >> 5;                          \
+    const uint64_t per_##it = ((uint64_t)(total) + nw_##it - 1) / nw_##it;                     \
+    const uint64_t b_##it = (((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * per_##it; \
+    const uint64_t e_##it = min((uint64_t)(total), b_##it + per_##it);                          \
+    uint32_t i = b_##it < e_##it ? owner_of(pref, n, b_##it) : 0u;                             \
+    for (uint64_t it = b_##it; it < e_##it && ((i = owner_next(pref, i, it)), true); it++)
+
 // ------------------------------------------------------------------ plan
 // count: add the batch's pool demand to cnt; state: write the per-vertex state
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a, uint64_t *__restrict__ scr_need, UpdCounters *cnt,
@@ -130,7 +165,8 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
     __syncthreads();
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_WARP_LOOP(i, a.nt) {
+    const uint32_t NT = bsp_nt(a);
+    BSP_WARP_LOOP(i, NT) {
         const uint32_t t = a.t0 + i;
         const VHdr h = g.hdr[g.tv[t]];
         PlanLane pl;
@@ -188,26 +224,60 @@ struct BspTotals {
     UpdCounters c;
     unsigned long long bump[3];
     unsigned long long scr, copy, sel, grp, all, hubs, bigs, hix_used;
+    unsigned long long nt;     // touched vertices
+    int abort;                 // one-sync route: 1 EINVAL, 4 EOVERFLOW, 2 capacity (the host grows, re-runs)
+    int pad;
 };
-__global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint64_t *scr_off, BspTotals *out) {
+// capacities the one-sync route was enqueued with
+struct BspCaps {
+    unsigned long long arc, bkt, mem_units, hix, scr_words, sel, grp;
+    int hix_on;
+};
+// Totals of the plan.  One-sync route (abort != null): also its gate -- the totals against
+// what was allocated when the batch was enqueued.  Anything that does not fit (or an invalid
+// / overflowing batch) sets *abort and every later kernel of the batch returns at once:
+// nothing is mutated, and the host grows what is short and re-runs the batch on the
+// synchronous route.
+__global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint64_t *scr_off, BspTotals *out,
+                             const BspCaps caps, int *abort) {
     if (threadIdx.x != 0) return;
-    out->c = *cnt;
-    for (int j = 0; j < 3; j++) out->bump[j] = a.g.bump[j];
-    out->scr = scr_off[a.nt];
-    out->copy = a.p_copy[a.nt];
-    out->sel = a.p_sel[a.nt];
-    out->grp = a.p_grp[a.nt];
-    out->all = a.p_all[a.nt];
-    out->hubs = *a.nhubs;
-    out->bigs = *a.nbigs;
-    out->hix_used = a.g.bump[5];
+    const uint32_t nt = bsp_nt(a);
+    BspTotals t;
+    t.c = *cnt;
+    for (int j = 0; j < 3; j++) t.bump[j] = a.g.bump[j];
+    t.scr = scr_off[nt];
+    t.copy = a.p_copy[nt];
+    t.sel = a.p_sel[nt];
+    t.grp = a.p_grp[nt];
+    t.all = a.p_all[nt];
+    t.hubs = *a.nhubs;
+    t.bigs = *a.nbigs;
+    t.hix_used = a.g.bump[5];
+    t.nt = nt;
+    t.pad = 0;
+    int ab = 0;
+    if (abort) {
+        if (t.c.flag & 1) ab |= 1;
+        if (t.c.flag & 4) ab |= 4;
+        if (t.c.flag & 8) ab |= 8;   // a segment was too long to order: re-segment (radix sort), re-run
+        if (t.bump[0] + t.c.need_arc > caps.arc || t.bump[1] + t.c.need_bkt > caps.bkt ||
+            t.bump[2] + t.c.need_mem + t.c.reserve_mem > caps.mem_units)
+            ab |= 2;
+        if (caps.hix_on && t.c.need_hix && t.hix_used + t.c.need_hix > caps.hix) ab |= 2;
+        if (t.scr > caps.scr_words || t.sel > caps.sel || t.grp > caps.grp) ab |= 2;
+        *abort = ab;
+    }
+    t.abort = ab;
+    *out = t;
 }
 
 // ------------------------------------------------------------------ relocations, inserts, scratch init
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_alloc_insert(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_WARP_LOOP(i, a.nt) {
+    const uint32_t NT = bsp_nt(a);
+    BSP_WARP_LOOP(i, NT) {
         const uint32_t t = a.t0 + i;
         const uint32_t beg = g.seg[t], end = g.seg[t + 1];
         const VHdr h = g.hdr[g.tv[t]];
@@ -252,6 +322,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_alloc_insert(const B
             gkp(a, GK_CAP, i)[lane] = cap;
         }
         gkp(a, GK_DELK, i)[lane] = 0;
+        gkp(a, GK_GHN, i)[lane] = 0;
         uint32_t gm = __ballot_sync(0xffffffffu, grow);
         while (gm) {
             const int k = __ffs(gm) - 1;
@@ -334,10 +405,12 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_alloc_insert(const B
 
 // ------------------------------------------------------------------ adjacency relocation copies
 __global__ void __launch_bounds__(MT) k_bsp_copy(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_ITEM_LOOP(it, total) {
-        const uint32_t i = owner_of(a.p_copy, a.nt, it);
+    const uint32_t NT = bsp_nt(a);
+    total = bsp_total(a, a.p_copy, total);
+    BSP_ITEM_RANGE(it, i, total, a.p_copy, NT) {
         const uint32_t c = (uint32_t)(it - a.p_copy[i]);
         const VHdr h = g.hdr[g.tv[a.t0 + i]];
         const uint64_t to = a.vaoff[i];
@@ -355,10 +428,12 @@ __global__ void __launch_bounds__(MT) k_bsp_copy(const BspArgs a, uint64_t total
 // every live instance of a deleted destination: count it, and atomicMin its
 // packed (epoch << 32 | position) key
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_select(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_ITEM_LOOP(it, total) {
-        const uint32_t i = owner_of(a.p_sel, a.nt, it);
+    const uint32_t NT = bsp_nt(a);
+    total = bsp_total(a, a.p_sel, total);
+    BSP_ITEM_RANGE(it, i, total, a.p_sel, NT) {
         if (a.vhix[i]) continue;   // located through the hub delete index (k_hix_select)
         const uint32_t c = (uint32_t)(it - a.p_sel[i]);
         const uint32_t L = a.vL[i], q = a.vq[i];
@@ -448,6 +523,159 @@ __device__ __forceinline__ void group_front(const MutateArgs &g, const DelScr &s
     }
 }
 
+// group front, slots [sb, se): as group_front, but the deleted slots are appended to gh
+// through the group's counter in any order (sorted afterwards)
+__device__ __forceinline__ void group_front_append(const MutateArgs &g, const DelScr &s, uint32_t *Mi, uint32_t *gh,
+                                                   uint32_t *ghn, uint32_t sb, uint32_t se, uint32_t Lp) {
+    const uint32_t lane = lane_id();
+    for (uint32_t b0 = sb; b0 < se; b0 += 32 * 8) {
+        uint32_t xs[8];   // 8 independent member loads in flight per lane
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t sl = b0 + 32 * j + lane;
+            xs[j] = sl < se ? Mi[sl] : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+            const uint32_t sl = b0 + 32 * j + lane;
+            bool del = false;
+            if (sl < se) {
+                const uint32_t x = xs[j];
+                del = bit_test(s.bm, x);
+                if (!del && x >= Lp) Mi[sl] = s.R[x - Lp];
+            }
+            const uint32_t bal = __ballot_sync(0xffffffffu, del);
+            if (bal) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(ghn, (uint32_t)__popc(bal));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                if (del) gh[base + __popc(bal & lanemask_lt())] = sl;
+            }
+        }
+    }
+}
+
+// ascending sort of x[0, n) in shared memory (bitonic; n <= cap, cap a power of two), the
+// whole block
+__device__ __forceinline__ void block_sort_u32(uint32_t *x, uint32_t n) {
+    const uint32_t P = next_pow2(n);
+    for (uint32_t q = n + threadIdx.x; q < P; q += blockDim.x) x[q] = 0xFFFFFFFFu;
+    __syncthreads();
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t h = k >> 1; h > 0; h >>= 1) {
+            for (uint32_t q = threadIdx.x; q < P; q += blockDim.x) {
+                const uint32_t r = q ^ h;
+                if (r > q) {
+                    const uint32_t u = x[q], v = x[r];
+                    if ((u > v) == ((q & k) == 0)) {
+                        x[q] = v;
+                        x[r] = u;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// ascending sort of one value per lane (bitonic over the warp; pad with 0xFFFFFFFF)
+__device__ __forceinline__ uint32_t warp_sort_u32(uint32_t x) {
+    const uint32_t lane = lane_id();
+#pragma unroll
+    for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+            const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+            x = (lower == up) ? min(x, y) : max(x, y);
+        }
+    }
+    return x;
+}
+
+// hubs with deletes: picks (appended by k_bsp_finalize) in ascending order; its prefix below
+// L' is exactly the hole list of R-6 (the counted-rank route writes the same list).  One warp
+// per hub: up to 32 picks in registers; up to SORT_MAX by k_bsp_sort_big; more take the
+// counted-rank route (vrank = 1).
+__global__ void __launch_bounds__(MT) k_bsp_hub_sort(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(h, *a.nhubs) {
+        const uint32_t i = a.hubs[h];
+        const uint32_t N = a.vN[i];
+        if (lane == 0) {
+            a.vrank[i] = N > SORT_MAX ? 1u : 0u;
+            if (N > SORT_MAX) atomicAdd(a.nhubs + 4, 1u);   // some hub takes the counted-rank passes
+        }
+        if (N < 2 || N > SORT_MAX) continue;
+        const DelScr s = del_scr(g.scr + g.scr_off[i], a.vL[i], a.vq[i]);
+        if (N > 32) {
+            if (lane == 0) a.sorts[atomicAdd(a.nhubs + 5, 1u)] = make_uint2(i, 32u);
+            continue;
+        }
+        const uint32_t x = warp_sort_u32(lane < N ? s.holes[lane] : 0xFFFFFFFFu);
+        if (lane < N) s.holes[lane] = x;
+    }
+}
+
+// sorted-picks hubs: each list group's appended deleted slots in ascending order (one warp
+// per hub, a group at a time; longer lists by k_bsp_sort_big)
+__global__ void __launch_bounds__(MT) k_bsp_grp_sort(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    BSP_WARP_LOOP(h, *a.nhubs) {
+        const uint32_t i = a.hubs[h];
+        if (!a.vN[i] || a.vrank[i]) continue;
+        const DelScr s = del_scr(g.scr + g.scr_off[i], a.vL[i], a.vq[i]);
+        const uint32_t n_l = ((a.vlist0[i] >> lane) & 1u) ? gkp(a, GK_GHN, i)[lane] : 0u;
+        const uint32_t gho_l = gkp(a, GK_GHO, i)[lane];
+        uint32_t m = __ballot_sync(0xffffffffu, n_l >= 2);
+        while (m) {
+            const int k = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t n = __shfl_sync(0xffffffffu, n_l, k);
+            uint32_t *gh = s.gh + __shfl_sync(0xffffffffu, gho_l, k);
+            if (n > 32) {
+                if (lane == 0) a.sorts[atomicAdd(a.nhubs + 5, 1u)] = make_uint2(i, (uint32_t)k);
+                continue;
+            }
+            const uint32_t x = warp_sort_u32(lane < n ? gh[lane] : 0xFFFFFFFFu);
+            if (lane < n) gh[lane] = x;
+        }
+    }
+}
+
+// the listed longer sorts (a hub's picks: group 32; a group's deleted slots: group k), one
+// block each, bitonic in shared memory; the list is consumed (its counter reset)
+__global__ void __launch_bounds__(256) k_bsp_sort_big(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
+    __shared__ uint32_t x[SORT_MAX];
+    const MutateArgs &g = a.g;
+    const uint32_t ns = a.nhubs[5];
+    for (uint32_t j = blockIdx.x; j < ns; j += gridDim.x) {
+        const uint2 e = a.sorts[j];
+        const uint32_t i = e.x;
+        const DelScr s = del_scr(g.scr + g.scr_off[i], a.vL[i], a.vq[i]);
+        uint32_t *v;
+        uint32_t n;
+        if (e.y == 32u) {
+            v = s.holes;
+            n = a.vN[i];
+        } else {
+            v = s.gh + gkp(a, GK_GHO, i)[e.y];
+            n = gkp(a, GK_GHN, i)[e.y];
+        }
+        for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) x[q] = v[q];
+        __syncthreads();
+        block_sort_u32(x, n);
+        for (uint32_t q = threadIdx.x; q < n; q += blockDim.x) v[q] = x[q];
+        __syncthreads();
+    }
+    __syncthreads();
+}
+
 // group tail window [L_k', c'): survivors, renamed, fill the holes in rank order (R-6)
 __device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s, uint32_t *Md, uint32_t *Mi,
                                            const uint32_t *gh, uint32_t cp, uint32_t Nk, uint32_t Lp) {
@@ -472,11 +700,14 @@ __device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s,
 // large vertices with deletes (picks only; the rest by the chunk-item kernels)
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_finalize(const BspArgs a, bool hubs) {
     __shared__ uint32_t s_delk[MT / 32][32];
+    __shared__ uint32_t s_np[MT / 32];   // hubs: picks appended to the holes array so far
     // small vertices: bitmap, holes, rename table and group holes in shared memory
     __shared__ uint32_t s_bm[MT / 32][32], s_hol[MT / 32][32], s_R[MT / 32][32], s_gh[MT / 32][64];
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
     const MutateArgs &g = a.g;
-    BSP_WARP_LOOP(j, hubs ? *a.nhubs : a.nt) {
+    const uint32_t NT = hubs ? *a.nhubs : bsp_nt(a);
+    BSP_WARP_LOOP(j, NT) {
         const uint32_t i = hubs ? a.hubs[j] : j;
         const uint32_t q = a.vq[i];
         const uint32_t L = a.vL[i];
@@ -486,6 +717,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_finalize(const BspAr
         const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
         const uint32_t hmask = s.Hq - 1;
         s_delk[w][lane] = 0;
+        if (lane == 0) s_np[w] = 0;
         if (small) {
             // round 0 of a small vertex (large ones: k_bsp_select items)
             for (uint32_t p = lane; p < L; p += 32) {
@@ -517,6 +749,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_finalize(const BspAr
                 if (b == ~0ull) continue;
                 const uint32_t p = (uint32_t)b;
                 atomicOr(&s.bm[p >> 5], 1u << (p & 31u));
+                if (hubs) s.holes[atomicAdd(&s_np[w], 1u)] = p;   // unordered; k_bsp_hub_sort orders them
                 const uint32_t hs = ++s.hsel[sl];
                 s.hprev[sl] = b;
                 s.hbest[sl] = ~0ull;
@@ -616,7 +849,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_finalize(const BspAr
 // ------------------------------------------------------------------ holes: marked positions < L', ascending
 __device__ __forceinline__ uint32_t hole_word(const BspArgs &a, uint32_t i, uint32_t c, uint32_t &wi, DelScr &s) {
     const uint32_t L = a.vL[i], q = a.vq[i], N = a.vN[i];
-    if (!N) return 0;
+    if (!N || !a.vrank[i]) return 0;   // sorted-picks hubs have their holes already
     const uint32_t Lp = L - N;
     s = del_scr(a.g.scr + a.g.scr_off[i], L, q);
     wi = c * 32 + lane_id();
@@ -628,8 +861,11 @@ __device__ __forceinline__ uint32_t hole_word(const BspArgs &a, uint32_t i, uint
 }
 
 __global__ void __launch_bounds__(MT) k_bsp_hole_count(const BspArgs a, uint64_t total) {
-    BSP_ITEM_LOOP(it, total) {
-        const uint32_t i = owner_of(a.p_sel, a.nt, it);
+    if (BSP_ABORTED(a)) return;
+    if (!a.nhubs[4]) return;   // no hub takes the counted-rank route this batch
+    const uint32_t NT = bsp_nt(a);
+    total = bsp_total(a, a.p_sel, total);
+    BSP_ITEM_RANGE(it, i, total, a.p_sel, NT) {
         const uint32_t c = (uint32_t)(it - a.p_sel[i]);
         uint32_t wi;
         DelScr s;
@@ -639,10 +875,13 @@ __global__ void __launch_bounds__(MT) k_bsp_hole_count(const BspArgs a, uint64_t
 }
 
 __global__ void __launch_bounds__(MT) k_bsp_hole_write(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
+    if (!a.nhubs[4]) return;   // no hub takes the counted-rank route this batch
     const uint32_t lane = lane_id();
-    BSP_ITEM_LOOP(it, total) {
-        const uint32_t i = owner_of(a.p_sel, a.nt, it);
-        if (!a.vN[i]) continue;
+    const uint32_t NT = bsp_nt(a);
+    total = bsp_total(a, a.p_sel, total);
+    BSP_ITEM_RANGE(it, i, total, a.p_sel, NT) {
+        if (!a.vN[i] || !a.vrank[i]) continue;
         const uint32_t c = (uint32_t)(it - a.p_sel[i]);
         uint32_t wi = 0;
         DelScr s;
@@ -665,6 +904,7 @@ __global__ void __launch_bounds__(MT) k_bsp_hole_write(const BspArgs a, uint64_t
 
 // ------------------------------------------------------------------ adjacency tail window [L', L) (R-6)
 __global__ void __launch_bounds__(MT) k_bsp_tail(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_WARP_LOOP(h, *a.nhubs) {
@@ -685,10 +925,10 @@ struct GrpItem {
     uint32_t i, k, j, first;   // first: item index of chunk 0 of (i, k)
     uint32_t cp, Nk, moff, gho;
 };
-__device__ __forceinline__ GrpItem grp_item(const BspArgs &a, uint64_t it) {
+__device__ __forceinline__ GrpItem grp_item(const BspArgs &a, uint64_t it, uint32_t owner) {
     const uint32_t lane = lane_id();
     GrpItem gi;
-    gi.i = owner_of(a.p_grp, a.nt, it);
+    gi.i = owner;
     const uint32_t c = (uint32_t)(it - a.p_grp[gi.i]);
     const uint32_t list0 = a.vlist0[gi.i];
     const bool lst = (list0 >> lane) & 1u;
@@ -713,12 +953,16 @@ __device__ __forceinline__ GrpItem grp_item(const BspArgs &a, uint64_t it) {
 }
 
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_count(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
+    if (!a.nhubs[4]) return;   // no hub takes the counted-rank route this batch
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_ITEM_LOOP(it, total) {
-        const GrpItem gi = grp_item(a, it);
+    total = bsp_total(a, a.p_grp, total);
+    const uint32_t NT = bsp_nt(a);
+    BSP_ITEM_RANGE(it, own, total, a.p_grp, NT) {
+        const GrpItem gi = grp_item(a, it, own);
         uint32_t n = 0;
-        if (gi.Nk) {
+        if (gi.Nk && a.vrank[gi.i]) {
             const uint32_t L = a.vL[gi.i], q = a.vq[gi.i];
             const DelScr s = del_scr(g.scr + g.scr_off[gi.i], L, q);
             const uint32_t *Mi = g.midx + (uint64_t)gi.moff * 4;
@@ -739,16 +983,24 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_count(const BspA
 // pass 1 over the front [0, L_k'): deleted slots become holes ranked in slot
 // order; survivors pointing into the adjacency tail are renamed in place
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_write(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_ITEM_LOOP(it, total) {
-        const GrpItem gi = grp_item(a, it);
+    total = bsp_total(a, a.p_grp, total);
+    const uint32_t NT = bsp_nt(a);
+    BSP_ITEM_RANGE(it, own, total, a.p_grp, NT) {
+        const GrpItem gi = grp_item(a, it, own);
         const uint32_t N = a.vN[gi.i];
         if (!N || (!gi.Nk && !((a.vmoved[gi.i] >> gi.k) & 1u))) continue;   // group unchanged
         const uint32_t L = a.vL[gi.i], q = a.vq[gi.i], Lp = L - N;
         const DelScr s = del_scr(g.scr + g.scr_off[gi.i], L, q);
         uint32_t *Mi = g.midx + (uint64_t)gi.moff * 4;
         const uint32_t Lk = gi.cp - gi.Nk;
+        if (!a.vrank[gi.i]) {   // deleted slots appended (any order), sorted by k_bsp_grp_sort
+            group_front_append(g, s, Mi, s.gh + gi.gho, gkp(a, GK_GHN, gi.i) + gi.k, gi.j * CH,
+                               min(Lk, (gi.j + 1) * CH), Lp);
+            continue;
+        }
         const uint32_t r0 = gi.Nk ? (uint32_t)(a.gpref[it] - a.gpref[gi.first]) : 0u;
         group_front(g, s, Mi, s.gh + gi.gho, gi.j * CH, min(Lk, (gi.j + 1) * CH), r0, Lp);
     }
@@ -757,6 +1009,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_write(const BspA
 // pass 2 over each group's tail window [L_k', c'): survivors, renamed, fill the
 // holes in rank order (R-6)
 __global__ void __launch_bounds__(MT) k_bsp_grp_tail(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
     BSP_WARP_LOOP(h, *a.nhubs) {
@@ -926,7 +1179,9 @@ __device__ __forceinline__ void rebuild_write(const BspArgs &a, uint32_t i, cons
 
 // small vertices (L <= CH): one warp each
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild(const BspArgs a) {
-    BSP_WARP_LOOP(i, a.nt) {
+    if (BSP_ABORTED(a)) return;
+    const uint32_t NT = bsp_nt(a);
+    BSP_WARP_LOOP(i, NT) {
         if (a.vL[i] > CH) continue;
         RbLane r;
         uint32_t fm, fd;
@@ -948,6 +1203,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild(const BspArg
 // whose member must be found) save their stage-A state in the gk slots and are
 // finished by k_bsp_rebuild_fill, one block each
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild_big(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     BSP_WARP_LOOP(h, *a.nbigs) {
         const uint32_t i = a.bigs[h];
@@ -971,6 +1227,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild_big(const Bs
 // large vertices with a fill/find scan: one 1024-thread block each; the scan is split
 // over the 32 warps (count pass, per-group scan over warps, write pass)
 __global__ void __launch_bounds__(LT) k_bsp_rebuild_fill(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     __shared__ RbLane s_r[32];
     __shared__ uint32_t s_fm, s_fd;
     __shared__ uint32_t s_cnt[32][33];     // [warp][group], then exclusive prefixes
@@ -1032,9 +1289,11 @@ __global__ void __launch_bounds__(LT) k_bsp_rebuild_fill(const BspArgs a) {
 // instances selected, hsel = hfound > 0) is tombstoned.  Otherwise the vertex is
 // flagged for the full rebuild by the chunk items below.
 __global__ void __launch_bounds__(MT) k_bsp_nb_incr(const BspArgs a) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_WARP_LOOP(i, a.nt) {
+    const uint32_t NT = bsp_nt(a);
+    BSP_WARP_LOOP(i, NT) {
         const uint32_t t = a.t0 + i;
         const uint32_t u = g.tv[t];
         const uint32_t L = a.vL[i], q = a.vq[i];
@@ -1077,10 +1336,12 @@ __global__ void __launch_bounds__(MT) k_bsp_nb_incr(const BspArgs a) {
 }
 
 __global__ void __launch_bounds__(MT) k_bsp_nb_clear(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_ITEM_LOOP(it, total) {
-        const uint32_t i = owner_of(a.p_all, a.nt, it);
+    const uint32_t NT = bsp_nt(a);
+    total = bsp_total(a, a.p_all, total);
+    BSP_ITEM_RANGE(it, i, total, a.p_all, NT) {
         if (!a.vnbfull[i]) continue;
         const uint32_t c = (uint32_t)(it - a.p_all[i]);
         const uint32_t dn = a.vL[i] - a.vN[i];
@@ -1092,10 +1353,12 @@ __global__ void __launch_bounds__(MT) k_bsp_nb_clear(const BspArgs a, uint64_t t
 }
 
 __global__ void __launch_bounds__(MT) k_bsp_nb_fill(const BspArgs a, uint64_t total) {
+    if (BSP_ABORTED(a)) return;
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
-    BSP_ITEM_LOOP(it, total) {
-        const uint32_t i = owner_of(a.p_all, a.nt, it);
+    const uint32_t NT = bsp_nt(a);
+    total = bsp_total(a, a.p_all, total);
+    BSP_ITEM_RANGE(it, i, total, a.p_all, NT) {
         if (!a.vnbfull[i]) continue;
         const uint32_t c = (uint32_t)(it - a.p_all[i]);
         const uint32_t dn = a.vL[i] - a.vN[i];

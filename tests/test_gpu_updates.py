@@ -72,6 +72,8 @@ ROUTES = {
     "bsp": {},                                                  # bulk-synchronous pipeline (default)
     "bsp-sub": {"BINGO_BSP_MAXT": "7"},                         # ... in sub-batches of 7 touched vertices
     "bsp-hix": {"BINGO_HUB_INDEX": "1"},                        # ... with the hub delete index (opt-in)
+    "bsp-sync": {"BINGO_UPD_SYNC": "1"},                        # ... host round trips after front end / plan
+    "bsp-radix": {"BINGO_UPD_RADIX_FRONT": "1"},                # ... segmented by the radix sort
     "legacy": {"BINGO_UPD_LEGACY": "1"},                        # per-vertex mutate kernels (warp / block)
     "legacy-block": {"BINGO_UPD_LEGACY": "1", "BINGO_UPD_SMALL_L": "0"},   # ... every vertex on a block
 }
@@ -83,6 +85,8 @@ ROUTES = {
     (7, False, 200, "bsp", 3500), (8, False, 7, "bsp", 5000), (9, True, 255, "bsp", 3000),
     (0, False, 200, "bsp-sub", 700), (8, False, 7, "bsp-sub", 5000),
     (7, False, 200, "bsp-hix", 3500), (8, False, 7, "bsp-hix", 5000), (9, True, 255, "bsp-hix", 3000),
+    (0, False, 200, "bsp-sync", 700), (8, False, 7, "bsp-sync", 5000), (9, True, 255, "bsp-sync", 3000),
+    (1, False, 1 << 20, "bsp-radix", 700), (8, False, 7, "bsp-radix", 5000),
     (0, False, 200, "legacy", 700), (3, False, 7, "legacy", 700), (7, False, 200, "legacy", 3500),
     (0, False, 200, "legacy-block", 700), (3, False, 7, "legacy-block", 700),
     (6, False, 1 << 20, "legacy-block", 700)])
@@ -223,7 +227,7 @@ def test_small_batches_fast_path():
     _same(g, o, w.V, "after hub growth")
 
 
-@pytest.mark.parametrize("route", ["bsp", "bsp-sub", "legacy"])
+@pytest.mark.parametrize("route", ["bsp", "bsp-sub", "bsp-sync", "legacy"])
 def test_node2vec_neighbour_index_across_batches(route, monkeypatch):
     """The node2vec distance test (Eq.1, A-17) reads per-vertex neighbour sets that updates
     maintain in place (inserted destinations added, a destination whose last live instance
@@ -439,3 +443,107 @@ def test_streaming_queue_hub_handoff_and_pool_growth():
             r = np.array([1, u, v, 0], dtype=np.uint32)
         _same_stats(g.stream_update(r), o.apply_updates(r[None, :]))
     _same(g, o, V)
+
+
+@pytest.mark.parametrize("hix", ["0", "1"])
+def test_one_sync_route_reruns_only_when_short(hix, monkeypatch):
+    """The one-sync route (apply_bsp_async) enqueues the whole batch before the host knows
+    the touched-vertex count; a batch that finds a pool or its scratch short mutates nothing
+    and is re-applied on the synchronous route.  Bulk batches (> 256 records, so not the
+    single-launch fast path) on a graph with hubs: every batch equals the oracle, the first
+    batch(es) re-run while scratch is sized, later ones complete in one host round trip."""
+    monkeypatch.setenv("BINGO_HUB_INDEX", hix)
+    rng = np.random.default_rng(99)
+    V = 4000
+    deg = rng.integers(0, 12, size=V)
+    deg[:3] = (6000, 3000, 1500)
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, V, size=A).astype(np.uint32)
+    bias = rng.integers(1, 1 << 10, size=A).astype(np.uint32)
+    g, o = _pair(ro, dst, bias)
+    live = {u: list(dst[int(ro[u]):int(ro[u + 1])]) for u in range(V)}
+    for e in range(1, 13):
+        recs = []
+        for _ in range(int(rng.integers(300, 1500))):
+            u = int(rng.integers(0, 3)) if rng.random() < 0.4 else int(rng.integers(0, V))
+            if live[u] and rng.random() < 0.5:
+                recs.append((1, u, int(live[u][int(rng.integers(0, len(live[u])))]), 0))
+            else:
+                recs.append((0, u, int(rng.integers(0, V)), int(rng.integers(1, 1 << 10))))
+        recs = np.array(recs, dtype=np.uint32)
+        _same_stats(g.apply_updates(recs), o.apply_updates(recs))
+        if e % 3 == 0:
+            _same(g, o, V, f"batch {e}")
+        d = oracle.parse_dump(o.dump(), V)
+        live = {u: [a[0] for a in d[u]["adj"]] for u in range(V)}
+        if e == 6:
+            mid = g.info()["update_reruns"]
+    reruns = g.info()["update_reruns"]
+    assert 1 <= mid and reruns - mid <= 2, (mid, reruns)   # scratch settles: later batches take one sync
+    out = g.walk(length=40, seed=3)
+    ref = o.walk(length=40, seed=3)
+    assert np.array_equal(u32(out["paths"]), ref["paths"])
+
+
+@pytest.mark.parametrize("hub_records", [40, 3000, 9000])
+def test_segment_order_short_long_and_radix_fallback(hub_records):
+    """Segmentation (a7) without a sort: records are placed per touched vertex in any order,
+    then put back in batch order inside each segment -- one thread for <= 32 records, a
+    block bitonic sort for <= 8192, and above that the batch is re-segmented by the radix
+    sort.  One hub receives hub_records interleaved inserts and deletes (order matters: a
+    delete takes the earliest live instance, R-8, and inserts append in batch order,
+    P:500); the rest of the batch touches other vertices.  Dumps must equal the oracle's."""
+    rng = np.random.default_rng(hub_records)
+    V = 600
+    deg = rng.integers(1, 8, size=V)
+    deg[0] = 2000
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, 50, size=A).astype(np.uint32)     # many duplicates of few destinations
+    bias = rng.integers(1, 1 << 12, size=A).astype(np.uint32)
+    g, o = _pair(ro, dst, bias)
+    for e in range(3):
+        recs = []
+        for j in range(hub_records):
+            v = int(rng.integers(0, 50))
+            recs.append((1, 0, v, 0) if rng.random() < 0.45 else (0, 0, v, int(rng.integers(1, 1 << 12))))
+        for _ in range(400):
+            u = int(rng.integers(1, V))
+            recs.append((0, u, int(rng.integers(0, V)), int(rng.integers(1, 1 << 12))))
+        recs = np.array(recs, dtype=np.uint32)
+        recs = recs[rng.permutation(len(recs))]
+        _same_stats(g.apply_updates(recs), o.apply_updates(recs))
+        _same(g, o, V, f"hub_records {hub_records} batch {e}")
+
+
+@pytest.mark.parametrize("ndel", [20, 300, 5000])
+def test_hub_delete_routes_by_pick_count(ndel):
+    """A hub's holes come from its sorted picks (one warp for <= 32, a block sort for
+    <= 4096) and its group holes from one pass over each group front plus a sort; a batch
+    deleting more than 4096 arcs of one hub takes the counted-rank passes instead.  Each
+    route must leave the oracle's structure (R-6 pairing on the adjacency and on every
+    member list)."""
+    rng = np.random.default_rng(ndel)
+    V = 2000
+    deg = rng.integers(0, 5, size=V)
+    deg[0] = 12000
+    ro = np.zeros(V + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    A = int(ro[-1])
+    dst = rng.integers(0, V, size=A).astype(np.uint32)
+    bias = rng.integers(1, 1 << 14, size=A).astype(np.uint32)
+    g, o = _pair(ro, dst, bias)
+    for e in range(3):
+        d = oracle.parse_dump(o.dump(), V)
+        hub = [a[0] for a in d[0]["adj"]]
+        pick = rng.choice(len(hub), size=min(ndel, len(hub)), replace=False)
+        recs = [(1, 0, int(hub[j]), 0) for j in pick]
+        recs += [(0, 0, int(rng.integers(0, V)), int(rng.integers(1, 1 << 14))) for _ in range(300)]
+        recs += [(0, int(rng.integers(1, V)), int(rng.integers(0, V)), int(rng.integers(1, 1 << 14)))
+                 for _ in range(300)]
+        recs = np.array(recs, dtype=np.uint32)[rng.permutation(len(recs))]
+        _same_stats(g.apply_updates(recs), o.apply_updates(recs))
+        _same(g, o, V, f"ndel {ndel} batch {e}")
