@@ -210,6 +210,12 @@ struct bingo_graph {
     uint32_t *hixt = nullptr;          // [V] tombstones per table
     uint32_t *hix = nullptr;           // pool of tables, 2 words per entry {dst + 1 (0 empty), position}
     uint64_t hix_cap = 0;              // words; bump pointer counters[5]
+    uint64_t *gixo = nullptr;          // [V] group index (group_index.cuh): table offset | log2 size << 48, 0 = none
+    uint32_t *gixt = nullptr;          // [V] its tombstones
+    uint32_t *gix = nullptr;           // table pool (zeroed words), bump pointer counters[6]
+    uint64_t gix_cap = 0;              // words
+    uint32_t gix_min = 1024;           // vertices with more arcs may get a table
+    bool gix_full = false;             // the pool could not grow: no new tables
     uint32_t hix_min = 0xFFFFFFFFu;    // vertices with more arcs than this have tables
     uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch

@@ -311,6 +311,7 @@ bingo_status float_prepare(bingo_graph *g, const bingo_build_desc *desc, uint32_
                            uint64_t *dscan, uint64_t *tmp, cudaStream_t s, uint64_t *total_dec);
 bingo_status float_fill(bingo_graph *g, const bingo_build_desc *desc, const uint64_t *dscan, cudaStream_t s);
 bingo_status hix_build_all(bingo_graph *g, cudaStream_t s);
+bingo_status gix_build_all(bingo_graph *g, cudaStream_t s);
 
 extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, bingo_graph **out) {
     if (!desc || !out) return BINGO_E_INVAL;
@@ -517,6 +518,7 @@ extern "C" bingo_status bingo_build(const bingo_build_desc *desc, void *stream, 
     }
     CK(cudaStreamSynchronize(s));
     st = hix_build_all(g, s);   // hub delete index (update-side, derived)
+    if (st == BINGO_OK) st = gix_build_all(g, s);   // group index (update-side, derived)
     if (st == BINGO_E_CUDA) g->poisoned = 1;
 done:
     bingo_dev_free(g, sz);

@@ -72,12 +72,19 @@ __global__ void __launch_bounds__(MT) k_hix_prep(const BspArgs a) {
             if (__any_sync(0xffffffffu, dup)) {
                 mode = 0;   // repeated deletes of one pair: the scan path (rounds) handles them
             } else if (!valid && L > g.hix_min) {
-                mode = 2;   // build a fresh table (zeroed pool words) for the pre-batch arcs
-                if (lane == 0) {
-                    const uint32_t lg = nb_log2size(L);
-                    const unsigned long long off = atomicAdd(&g.bump[5], 2ull << lg);
-                    g.hixo[u] = (uint64_t)off | ((uint64_t)lg << 48);
-                    g.hixt[u] = 0;
+                // build a fresh table (zeroed pool words) for the pre-batch arcs, if the pool has room
+                unsigned long long off = 0;
+                const uint32_t lg = nb_log2size(L);
+                if (lane == 0) off = atomicAdd(&g.bump[5], 2ull << lg);
+                off = __shfl_sync(0xffffffffu, off, 0);
+                if (off + (2ull << lg) <= g.hix_cap) {
+                    mode = 2;
+                    if (lane == 0) {
+                        g.hixo[u] = (uint64_t)off | ((uint64_t)lg << 48);
+                        g.hixt[u] = 0;
+                    }
+                } else {
+                    mode = 0;   // no room: this batch scans
                 }
             }
         }

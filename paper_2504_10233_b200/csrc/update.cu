@@ -50,6 +50,7 @@ struct UpdCounters {        // device, zeroed per batch
     unsigned long long need_arc, need_bkt, need_mem, reserve_mem;
     unsigned long long scratch_words;
     unsigned long long need_hix;   // hub delete index: upper bound of new table words (BSP plan)
+    unsigned long long need_gix;   // group index: upper bound of new table words (BSP plan)
     int flag;
     unsigned n_small, n_large;
     int pad;
@@ -184,29 +185,46 @@ __global__ void k_seg_place(uint64_t n, const uint32_t *__restrict__ key, const 
     }
 }
 
-// batch order inside each segment: short segments by one thread (insertion sort), longer
-// ones are listed for k_seg_order_long
+// batch order inside each segment: one segment per lane; two records by the lane itself,
+// up to 32 by the warp together (a shuffle sort per segment), longer ones are listed for
+// k_seg_order_long
 __global__ void k_seg_order(const uint32_t *__restrict__ seg, uint32_t *__restrict__ sv, const unsigned long long *pnt,
                             uint32_t *__restrict__ longs, uint32_t *nlong) {
     const uint32_t nt = (uint32_t)*pnt;
-    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < nt; t += gridDim.x * blockDim.x) {
-        const uint32_t b = seg[t], e = seg[t + 1];
-        if (e - b < 2) continue;
-        if (e - b > SEG_SHORT) {
-            longs[atomicAdd(nlong, 1u)] = t;
-            continue;
+    const uint32_t lane = threadIdx.x & 31u;
+    const uint32_t ntr = (nt + 31u) & ~31u;   // whole warps (the shuffle sorts)
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < ntr; t += gridDim.x * blockDim.x) {
+        uint32_t b = 0, len = 0;
+        if (t < nt) {
+            b = seg[t];
+            len = seg[t + 1] - b;
         }
-        uint32_t x[SEG_SHORT];
-        for (uint32_t j = 0; j < e - b; j++) {
-            const uint32_t v = sv[b + j];
-            uint32_t p = j;
-            while (p > 0 && x[p - 1] > v) {
-                x[p] = x[p - 1];
-                p--;
+        if (len == 2) {
+            const uint32_t x = sv[b], y = sv[b + 1];
+            if (x > y) {
+                sv[b] = y;
+                sv[b + 1] = x;
             }
-            x[p] = v;
+        } else if (len > SEG_SHORT) {
+            longs[atomicAdd(nlong, 1u)] = t;
         }
-        for (uint32_t j = 0; j < e - b; j++) sv[b + j] = x[j];
+        uint32_t m = __ballot_sync(0xffffffffu, len > 2 && len <= SEG_SHORT);
+        while (m) {
+            const int l = __ffs(m) - 1;
+            m &= m - 1;
+            const uint32_t bb = __shfl_sync(0xffffffffu, b, l), ll = __shfl_sync(0xffffffffu, len, l);
+            uint32_t x = lane < ll ? sv[bb + lane] : 0xFFFFFFFFu;
+#pragma unroll
+            for (uint32_t k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+                for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+                    const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+                    const bool up = (lane & k) == 0, lower = (lane & j) == 0;
+                    x = (lower == up) ? min(x, y) : max(x, y);
+                }
+            }
+            if (lane < ll) sv[bb + lane] = x;
+        }
     }
 }
 
@@ -466,7 +484,12 @@ struct MutateArgs {
     uint64_t *hixo;             // hub delete index offsets: routes that do not maintain it invalidate
     uint32_t *hixt, *hix;       // its tombstone counts and table pool (BSP route)
     uint32_t hix_min;           // vertices with more arcs get (and may lazily rebuild) a table
-    unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units
+    unsigned long long hix_cap; // hub index pool words (bump pointer bump[5])
+    uint64_t *gixo;             // group index (group_index.cuh): per-vertex table offsets, null = off
+    uint32_t *gixt, *gix;       // its tombstone counts and table pool
+    uint32_t gix_min;           // vertices with more arcs may get a table
+    unsigned long long gix_cap; // pool words (bump pointer bump[6])
+    unsigned long long *bump;   // [0] arc, [1] bkt, [2] mem units, [5] hub index, [6] group index
     uint32_t *vstats;           // [ntouch][VST]
     uint32_t epoch, alpha, beta, hot_b, hot_m;
     bool bs;
@@ -980,6 +1003,7 @@ __device__ __forceinline__ void mutate_vertex(const MutateArgs &a, const uint32_
         }
     }
     if (tid == 0 && a.hixo && a.hixo[u]) a.hixo[u] = 0;   // this route does not maintain the hub index
+    if (tid == 0 && a.gixo && a.gixo[u]) a.gixo[u] = 0;   // ... nor the group index
 }
 
 // small touched vertices: one warp each, 8 per block (grid-stride over all touched
@@ -1333,9 +1357,11 @@ __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *
 
 }  // namespace bingo
 
+#include "gix_table.cuh"
 #include "update_bsp.cuh"
 #include "float_update.cuh"
 #include "hub_index.cuh"
+#include "group_index.cuh"
 
 // ------------------------------------------------------------------ host side
 namespace {
@@ -1505,6 +1531,12 @@ static void fill_mutate_common(bingo_graph *g, MutateArgs &ma, uint32_t e) {
     ma.hixt = g->hixt;
     ma.hix = g->hix;
     ma.hix_min = g->hix_min;
+    ma.hix_cap = g->hix_cap;
+    ma.gixo = g->gixo;
+    ma.gixt = g->gixt;
+    ma.gix = g->gix;
+    ma.gix_min = g->gix_min;
+    ma.gix_cap = g->gix_cap;
     ma.bump = g->counters;
     ma.epoch = e;
     ma.alpha = g->alpha;
@@ -1650,7 +1682,25 @@ static bingo_status check_capacity(bingo_graph *g, const UpdCounters &hc, const 
 // so the scans stay the default.
 static bool hix_disabled() {
     const char *ev = getenv("BINGO_HUB_INDEX");
-    return !(ev && ev[0] == '1');
+    return ev && ev[0] == '0';
+}
+
+// Both update indices (hub delete index, group index) are kept only for vertices of more than
+// BINGO_INDEX_MIN arcs (default 16384; the build raises it 4x at a time until the tables fit
+// their memory budget).  Below that the O(d) scans of the bulk-synchronous route are cheaper
+// than keeping a table exact across batches (measured: at c2, hubs of 1K-16K
+// arcs change group layouts and get rebuilt often enough that indexing them made batches
+// slower, 0.82 -> 1.1-1.6 ms).
+static uint32_t index_min() {
+    uint32_t m = 16 * CH;
+    if (const char *ev = getenv("BINGO_INDEX_MIN")) m = std::max<uint32_t>(CH, (uint32_t)strtoul(ev, nullptr, 10));
+    return m;
+}
+// Without BINGO_INDEX_MIN the indices are built only for graphs of >= 2^28 arcs: on smaller
+// graphs the hubs are small enough that their scans beat keeping tables (c2: 0.82 ms per
+// 100K-record batch without, 1.05 ms with; c4: 1.51 ms without, 1.34 ms with).
+static bool index_wanted(const bingo_graph *g) {
+    return getenv("BINGO_INDEX_MIN") != nullptr || g->num_arcs >= (1ull << 28);
 }
 
 // hub delete index storage (hub_index.cuh): per-vertex offsets / tombstone counts on first
@@ -1680,9 +1730,61 @@ static bingo_status ensure_hix(bingo_graph *g, unsigned long long used, unsigned
     return BINGO_OK;
 }
 
+// The group index (group_index.cuh) is on unless BINGO_GROUP_INDEX=0; tables are taken from
+// a pool at batch time.  Growing the pool is best effort: without room the hubs keep the
+// member-list scans (g->gix_full), never an error.
+static bool gix_enabled() {
+    const char *ev = getenv("BINGO_GROUP_INDEX");
+    return !(ev && ev[0] == '0');
+}
+static bingo_status ensure_gix_arrays(bingo_graph *g, cudaStream_t s) {
+    if (g->gixo || g->gix_full || !gix_enabled() || g->float_mode || !g->V) return BINGO_OK;
+    uint64_t *o = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * g->V);
+    uint32_t *t = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->V);
+    if (!o || !t) {
+        bingo_dev_free(g, o);
+        bingo_dev_free(g, t);
+        g->gix_full = true;
+        return BINGO_OK;
+    }
+    if (cudaMemsetAsync(o, 0, sizeof(uint64_t) * g->V, s) != cudaSuccess ||
+        cudaMemsetAsync(t, 0, sizeof(uint32_t) * g->V, s) != cudaSuccess)
+        return BINGO_E_CUDA;
+    g->gix_min = index_min();
+    g->gixo = o;
+    g->gixt = t;
+    return BINGO_OK;
+}
+static bingo_status ensure_gix(bingo_graph *g, unsigned long long used, unsigned long long need, cudaStream_t s) {
+    if (!need || !g->gixo || g->gix_full || used + need <= g->gix_cap) return BINGO_OK;
+    const uint64_t cap = std::max<uint64_t>((used + need) + (used + need) / 2, g->gix_cap + g->gix_cap / 2);
+    uint32_t *nh = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * cap);
+    if (!nh) {
+        g->gix_full = true;
+        return BINGO_OK;
+    }
+    if ((g->gix_cap && cudaMemcpyAsync(nh, g->gix, sizeof(uint32_t) * std::min<uint64_t>(used, g->gix_cap),
+                                       cudaMemcpyDeviceToDevice, s) != cudaSuccess) ||
+        cudaMemsetAsync(nh + std::min<uint64_t>(used, g->gix_cap), 0,
+                        sizeof(uint32_t) * (cap - std::min<uint64_t>(used, g->gix_cap)), s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return BINGO_E_CUDA;
+    bingo_dev_free(g, g->gix);
+    g->gix = nh;
+    g->gix_cap = cap;
+    return BINGO_OK;
+}
+
 static inline unsigned warp_grid(uint64_t units, unsigned cap) {
     const uint64_t b = (units + MT / 32 - 1) / (MT / 32);
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, cap));
+}
+
+// grid cap of the warp-per-vertex kernels, in blocks (BINGO_BSP_WG blocks per SM, A/B)
+static unsigned bsp_wg() {
+    unsigned per_sm = 16;
+    if (const char *ev = getenv("BINGO_BSP_WG")) per_sm = std::max(1u, (unsigned)strtoul(ev, nullptr, 10));
+    return 148 * per_sm;
 }
 
 // touched vertices per sub-batch (BINGO_BSP_MAXT: smaller sub-batches, tests)
@@ -1720,6 +1822,8 @@ static bingo_status bsp_scratch(bingo_graph *g, uint64_t ntmax, BspArgs &a, BspB
         add(4 * ntmax);
         add(4 * ntmax);
         add(8 * 33 * ntmax);
+        add(4 * ntmax);
+        add(4 * ntmax);
         add(64);
         add(64);
         vb += 4096;
@@ -1761,6 +1865,8 @@ static bingo_status bsp_scratch(bingo_graph *g, uint64_t ntmax, BspArgs &a, BspB
     a.vhix = cv.take<uint32_t>(ntmax);
     a.vrank = cv.take<uint32_t>(ntmax);
     a.sorts = cv.take<uint2>(ntmax * 33);
+    a.vgix = cv.take<uint32_t>(ntmax);
+    a.vgixe = cv.take<uint32_t>(ntmax);
     a.nhubs = cv.take<uint32_t>(16);
     a.nbigs = a.nhubs + 1;
     b.abort = cv.take<int>(16);
@@ -1842,10 +1948,11 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         a.g.tv = tv;
         a.g.scr_off = scr_off;
         a.g.vstats = vstats;
+        a.err = dstats + 31;
     };
     refresh();
     const bool multi = ntouch > maxt;
-    const unsigned WG = 148 * 16, IG = 148 * 8;
+    const unsigned WG = bsp_wg(), IG = 148 * 8;
     BspCaps nocaps;
     memset(&nocaps, 0, sizeof(nocaps));
     if (multi) {
@@ -1859,9 +1966,11 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         UCK(cudaMemcpyAsync(&ht->c, dc, sizeof(UpdCounters), cudaMemcpyDeviceToHost, s));
         UCK(cudaMemcpyAsync(ht->bump, g->counters, sizeof(ht->bump), cudaMemcpyDeviceToHost, s));
         UCK(cudaMemcpyAsync(&ht->hix_used, g->counters + 5, 8, cudaMemcpyDeviceToHost, s));
+        UCK(cudaMemcpyAsync(&ht->gix_used, g->counters + 6, 8, cudaMemcpyDeviceToHost, s));
         UCK(cudaStreamSynchronize(s));
         bingo_status st = check_capacity(g, ht->c, ht->bump, s);
         if (st == BINGO_OK && !hix_disabled()) st = ensure_hix(g, ht->hix_used, ht->c.need_hix, s);
+        if (st == BINGO_OK) st = ensure_gix(g, ht->gix_used, ht->c.need_gix, s);
         if (st != BINGO_OK) return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
         refresh();
     }
@@ -1891,6 +2000,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
         if (!multi) {
             bingo_status st = check_capacity(g, ht->c, ht->bump, s);
             if (st == BINGO_OK && !hix_disabled()) st = ensure_hix(g, ht->hix_used, ht->c.need_hix, s);
+            if (st == BINGO_OK) st = ensure_gix(g, ht->gix_used, ht->c.need_gix, s);
             if (st != BINGO_OK) return st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st;
             refresh();
         }
@@ -1943,6 +2053,10 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             bingo_count_launch();
             UCK(cudaGetLastError());
             UCK(cudaMemsetAsync(a.nhubs + 5, 0, 4, sh));
+            if (g->gixo) {
+                BSP_LAUNCH(k_gix_prep, warp_grid(ht->bigs, WG), sh, a);
+                if (grp) BSP_LAUNCH(k_gix_build, warp_grid(grp, IG), sh, a, grp);
+            }
             g_trace.mark("hub: select+finalize", sh);
             BSP_LAUNCH(k_bsp_hole_count, warp_grid(sel, IG), sh, a, sel);
             UCK(exclusive_scan_u64(a.icnt, const_cast<uint64_t *>(a.ipref), sel, itmp, sh));
@@ -1950,6 +2064,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             BSP_LAUNCH(k_bsp_tail, warp_grid(ht->hubs, WG), sh, a);
             g_trace.mark("hub: holes+tail", sh);
             if (hix) BSP_LAUNCH(k_hix_ins, warp_grid(ht->bigs, WG), sh, a);
+            if (g->gixo) BSP_LAUNCH(k_gix_front, warp_grid(ht->hubs, WG), sh, a);
             if (grp) {
                 BSP_LAUNCH(k_bsp_grp_count, warp_grid(grp, IG), sh, a, grp);
                 UCK(exclusive_scan_u64(a.gcnt, const_cast<uint64_t *>(a.gpref), grp, itmp, sh));
@@ -1963,6 +2078,7 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             }
         }
         if (hix && !sel) BSP_LAUNCH(k_hix_ins, warp_grid(ht->bigs, WG), sh, a);   // inserts only
+        if (g->gixo && !sel && ht->bigs) BSP_LAUNCH(k_gix_prep, warp_grid(ht->bigs, WG), sh, a);
         if (ht->bigs) {
             BSP_LAUNCH(k_bsp_rebuild_big, warp_grid(ht->bigs, WG), sh, a);
             k_bsp_rebuild_fill<<<(unsigned)std::min<uint64_t>(ht->bigs, 148 * 2), LT, 0, sh>>>(a);
@@ -2027,6 +2143,7 @@ static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uin
     a.g.tv = tv;
     a.g.scr_off = b.scr_off;
     a.g.vstats = b.vstats;
+    a.err = dstats + 31;
     a.g.scr = (uint32_t *)g->vscratch;
     a.t0 = 0;
     a.nt = 0;
@@ -2042,9 +2159,11 @@ static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uin
     caps.hix_on = !hix_disabled();
     if (caps.hix_on && !g->hixo) caps.hix = 0;   // tables need the offsets first: the sync route allocates them
     caps.scr_words = g->vscratch_bytes >= 4 * 64 ? g->vscratch_bytes / 4 - 64 : 0;
+    caps.gix = g->gix_cap;
+    caps.gix_on = g->gixo && !g->gix_full;
     caps.sel = g->isc_sel;
     caps.grp = g->isc_grp;
-    const unsigned WG = 148 * 16, IG = 148 * 8, HG = 148 * 4;   // IG: item kernels, one wave of contiguous per-warp ranges
+    const unsigned WG = bsp_wg(), IG = 148 * 8, HG = 148 * 4;   // IG: item kernels, one wave of contiguous per-warp ranges
     const unsigned wg = warp_grid(ntmax, WG), hg = warp_grid(ntmax, HG);
     UCK(cudaMemsetAsync(a.nhubs, 0, 32, s));
     UCK(cudaMemsetAsync(a.vhix, 0, 4 * (size_t)ntmax, s));
@@ -2088,6 +2207,10 @@ static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uin
     bingo_count_launch();
     UCK(cudaGetLastError());
     UCK(cudaMemsetAsync(a.nhubs + 5, 0, 4, sh));
+    if (g->gixo) {
+        BSP_LAUNCH(k_gix_prep, hg, sh, a);
+        BSP_LAUNCH(k_gix_build, IG, sh, a, 0ull);
+    }
     g_trace.mark("hub: select+finalize", sh);
     BSP_LAUNCH(k_bsp_hole_count, IG, sh, a, 0ull);
     UCK(exclusive_scan_u64_multi_dn(&a.icnt, const_cast<uint64_t **>(&a.ipref), 1, &b.dt->sel, g->isc_sel, itmp, sh));
@@ -2095,6 +2218,7 @@ static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uin
     BSP_LAUNCH(k_bsp_tail, hg, sh, a);
     g_trace.mark("hub: holes+tail", sh);
     if (hix) BSP_LAUNCH(k_hix_ins, hg, sh, a);
+    if (g->gixo) BSP_LAUNCH(k_gix_front, hg, sh, a);
     BSP_LAUNCH(k_bsp_grp_count, IG, sh, a, 0ull);
     UCK(exclusive_scan_u64_multi_dn(&a.gcnt, const_cast<uint64_t **>(&a.gpref), 1, &b.dt->grp, g->isc_grp, itmp, sh));
     BSP_LAUNCH(k_bsp_grp_write, IG, sh, a, 0ull);
@@ -2248,6 +2372,10 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
         g->hscratch_bytes = 0;
         UCK(cudaMallocHost(&g->hscratch, hneed));
         g->hscratch_bytes = hneed;
+    }
+    if (!use_legacy_mutate() && !fm) {
+        const bingo_status st = ensure_gix_arrays(g, s);
+        if (st != BINGO_OK) return upd_cuda_fail(g, cudaGetLastError(), "group index arrays");
     }
     Carve cv{(char *)g->scratch, 0};
     uint4 *drec = cv.take<uint4>(n);
@@ -2482,6 +2610,12 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     ma.hixt = g->hixt;
     ma.hix = g->hix;
     ma.hix_min = g->hix_min;
+    ma.hix_cap = g->hix_cap;
+    ma.gixo = g->gixo;
+    ma.gixt = g->gixt;
+    ma.gix = g->gix;
+    ma.gix_min = g->gix_min;
+    ma.gix_cap = g->gix_cap;
     ma.bump = g->counters;
     ma.vstats = vstats;
     ma.epoch = e;
@@ -2544,6 +2678,11 @@ static bingo_status finish_batch(bingo_graph *g, uint64_t n, uint64_t ntouch, ui
 
 static bingo_status finish_batch_host(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
                                       const unsigned long long *hs, bingo_update_stats *stats) {
+    if (hs[31]) {   // an internal index inconsistency (never expected): fail loudly, graph unusable
+        fprintf(stderr, "libbingo: group index inconsistency in %llu vertices\n", hs[31]);
+        g->poisoned = 1;
+        return BINGO_E_CUDA;
+    }
     g->epoch = e;
     // inserted = number of insert records (validated batch)
     uint64_t inserted = 0;
@@ -2570,7 +2709,7 @@ static bingo_status finish_batch_host(bingo_graph *g, uint64_t n, uint64_t ntouc
 // whose tables fit 15% of the free device memory (c2: 2,411 vertices, 13.5% of the arcs,
 // 212 MB).  Called by bingo_build; a graph without room keeps no tables (scans only).
 bingo_status hix_build_all(bingo_graph *g, cudaStream_t s) {
-    if (hix_disabled() || g->V == 0 || g->float_mode) return BINGO_OK;
+    if (hix_disabled() || g->V == 0 || g->float_mode || !index_wanted(g)) return BINGO_OK;
     const uint64_t V = g->V;
     uint64_t *items = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 1));
     uint64_t *words = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 1));
@@ -2587,7 +2726,8 @@ bingo_status hix_build_all(bingo_graph *g, cudaStream_t s) {
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     const unsigned eg = (unsigned)std::min<uint64_t>((V + 255) / 256, 148ull * 16);
-    const uint32_t mins[4] = {CH, 4 * CH, 16 * CH, 64 * CH};
+    const uint32_t m0 = index_min();
+    const uint32_t mins[4] = {m0, 4 * m0, 16 * m0, 64 * m0};
     for (uint32_t min_d : mins) {
         k_hix_sizes<<<eg, 256, 0, s>>>(g->V, g->hdr, min_d, items, words);
         bingo_count_launch();
@@ -2627,6 +2767,83 @@ bingo_status hix_build_all(bingo_graph *g, cudaStream_t s) {
         break;
     }
     return fin(st);
+}
+
+
+// ---------------------------------------------------------------- group index at build time
+// Tables for every vertex with d > min_d, min_d the smallest of 1024 / 4096 / 16384 / 65536
+// whose tables fit 15% of the free device memory; the pool gets 25% more for the tables that
+// later batches rebuild (a dropped index, a vertex growing past min_d).  Called by bingo_build
+// after the hub delete index; a graph without room keeps no tables (member-list scans only).
+bingo_status gix_build_all(bingo_graph *g, cudaStream_t s) {
+    if (!gix_enabled() || g->V == 0 || g->float_mode) return BINGO_OK;
+    if (!index_wanted(g)) {
+        g->gix_full = true;   // no group index for this graph (no lazy arrays either)
+        return BINGO_OK;
+    }
+    const uint64_t V = g->V;
+    uint64_t *words = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 1));
+    uint64_t *woff = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (V + 2));
+    uint64_t *tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * scan_tmp_words(V + 1));
+    uint32_t *list = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * (V + 1));
+    auto fin = [&](bingo_status r) {
+        bingo_dev_free(g, words); bingo_dev_free(g, woff); bingo_dev_free(g, tmp); bingo_dev_free(g, list);
+        return r;
+    };
+    if (!words || !woff || !tmp || !list) return fin(BINGO_OK);   // no room: no tables
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const unsigned eg = (unsigned)std::min<uint64_t>((V + 255) / 256, 148ull * 16);
+    const unsigned wg = (unsigned)std::min<uint64_t>((V + 7) / 8, 148ull * 32);
+    const uint32_t m0 = index_min();
+    const uint32_t mins[4] = {m0, 4 * m0, 16 * m0, 64 * m0};
+    uint32_t *nlist = list + V;
+    for (uint32_t min_d : mins) {
+        k_gix_sizes<<<wg, MT, 0, s>>>(g->V, g->hdr, g->bkt, g->gcan, min_d, words, nullptr, nullptr);
+        bingo_count_launch();
+        if (cudaGetLastError() != cudaSuccess || exclusive_scan_u64(words, woff, V, tmp, s) != cudaSuccess)
+            return fin(BINGO_E_CUDA);
+        uint64_t tot = 0;
+        if (cudaMemcpyAsync(&tot, woff + V, 8, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return fin(BINGO_E_CUDA);
+        if (!tot) break;                                                   // no vertex that large
+        if (4.0 * 1.25 * (double)tot > 0.15 * (double)free_b) continue;   // does not fit: a higher threshold
+        const uint64_t cap = std::max<uint64_t>(tot + tot / 4, 1u << 20);
+        g->gixo = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * V);
+        g->gixt = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * V);
+        g->gix = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * cap);
+        if (!g->gixo || !g->gixt || !g->gix) {
+            bingo_dev_free(g, g->gixo); bingo_dev_free(g, g->gixt); bingo_dev_free(g, g->gix);
+            g->gixo = nullptr; g->gixt = nullptr; g->gix = nullptr;
+            return fin(BINGO_OK);
+        }
+        g->gix_cap = cap;
+        g->gix_min = min_d;
+        const unsigned long long used = tot;
+        if (cudaMemsetAsync(g->gix, 0, sizeof(uint32_t) * cap, s) != cudaSuccess ||
+            cudaMemsetAsync(g->gixt, 0, sizeof(uint32_t) * V, s) != cudaSuccess ||
+            cudaMemsetAsync(nlist, 0, 4, s) != cudaSuccess ||
+            cudaMemcpyAsync(g->counters + 6, &used, 8, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return fin(BINGO_E_CUDA);
+        k_gix_sizes<<<wg, MT, 0, s>>>(g->V, g->hdr, g->bkt, g->gcan, min_d, words, list, nlist);
+        bingo_count_launch();
+        k_gix_offsets<<<eg, 256, 0, s>>>(g->V, words, woff, g->gixo);
+        bingo_count_launch();
+        uint32_t nl = 0;
+        if (cudaGetLastError() != cudaSuccess || cudaMemcpyAsync(&nl, nlist, 4, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return fin(BINGO_E_CUDA);
+        if (nl) {
+            k_gix_fill<<<(unsigned)std::min<uint32_t>(nl, 148u * 8), 256, 0, s>>>(list, nl, g->hdr, g->bkt, g->gcan,
+                                                                                   g->midx, g->gixo, g->gix);
+            bingo_count_launch();
+        }
+        if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess) return fin(BINGO_E_CUDA);
+        return fin(BINGO_OK);
+    }
+    g->gix_full = true;   // no threshold fits the budget: no group index for this graph
+    return fin(BINGO_OK);
 }
 
 

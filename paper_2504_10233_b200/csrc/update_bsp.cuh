@@ -63,6 +63,9 @@ struct BspArgs {
     uint32_t *vnbfull;             // 1: the vertex's neighbour set is rebuilt from its adjacency
     uint32_t *vrank;               // hubs: 1 = counted-rank passes (N > SORT_MAX), 0 = sorted picks
     uint2 *sorts;                  // (vertex, 32 = picks | group k) lists longer than a warp, for k_bsp_sort_big
+    uint32_t *vgix;                // group index this batch: 0 none, 1 used, 2 built + used, 3 build failed (scan)
+    uint32_t *vgixe;               // plan: list-group members after the inserts (group index entries)
+    unsigned long long *err;       // internal inconsistencies found (group index); the host fails the call
     // one-sync route (apply_bsp_async): the launches are enqueued before the host knows the
     // touched-vertex count or the item totals, so kernels read them on the device
     const unsigned long long *pnt; // non-null: nt = *pnt (t0 = 0); else the host value nt
@@ -85,6 +88,7 @@ __device__ __forceinline__ uint64_t bsp_total(const BspArgs &a, const uint64_t *
 // per-vertex delete scratch (words from plan: bsp_scr_words)
 struct DelScr {
     uint32_t *bm, *hkey, *hk, *hfound, *hsel, *holes, *R, *gh;
+    uint2 *pk;                      // hubs: the picks (position, bias) in pick order (group index)
     unsigned long long *hbest, *hprev;
     uint32_t Hq;
 };
@@ -92,7 +96,7 @@ __host__ __device__ inline uint64_t bsp_scr_words(uint32_t L, uint32_t q, uint32
     if (!q) return 0;
     uint64_t Hq = 1;
     while (Hq < 2ull * q) Hq <<= 1;
-    uint64_t w = (uint64_t)(L + 31) / 32 + 8 * Hq + (2ull + nlist) * q + 8;
+    uint64_t w = (uint64_t)(L + 31) / 32 + 8 * Hq + (4ull + nlist) * q + 8;
     return (w + 7) & ~7ull;
 }
 __device__ __forceinline__ DelScr del_scr(uint32_t *base, uint32_t L, uint32_t q) {
@@ -107,7 +111,8 @@ __device__ __forceinline__ DelScr del_scr(uint32_t *base, uint32_t L, uint32_t q
     s.hprev = s.hbest + s.Hq;
     s.holes = reinterpret_cast<uint32_t *>(s.hprev + s.Hq);
     s.R = s.holes + q;
-    s.gh = s.R + q;
+    s.pk = reinterpret_cast<uint2 *>(s.R + q);
+    s.gh = s.R + 3 * q;
     return s;
 }
 
@@ -159,9 +164,9 @@ __device__ __forceinline__ uint32_t owner_next(const uint64_t *pref, uint32_t i,
 // count: add the batch's pool demand to cnt; state: write the per-vertex state
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a, uint64_t *__restrict__ scr_need, UpdCounters *cnt,
                                                  bool count, bool state) {
-    __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res, b_hix;
+    __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res, b_hix, b_gix;
     __shared__ int b_flag;
-    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = b_hix = 0; b_flag = 0; }
+    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = b_hix = b_gix = 0; b_flag = 0; }
     __syncthreads();
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
@@ -179,10 +184,18 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
             if (o.mem) atomicAdd(&b_mem, o.mem);
             if (o.res) atomicAdd(&b_res, o.res);
             // hub delete index: words of a (re)built table, an upper bound
-            if (o.L > CH && o.L > g.hix_min && o.q) atomicAdd(&b_hix, 2ull << nb_log2size(o.L));
+            // (only vertices without a table: a table dropped at k_hix_prep is re-taken from the
+            // pool's slack, or the vertex scans this batch)
+            if (g.hixo && o.L > CH && o.L > g.hix_min && o.q && !g.hixo[g.tv[t]])
+                atomicAdd(&b_hix, 2ull << nb_log2size(o.L));
         }
-        if (!state) continue;
         const bool lst = is_list(pl.kind);
+        // group index: entries of a table built this batch (list members after the inserts)
+        const uint32_t gixe = g.gixo ? warp_sum(lst ? pl.c + pl.insk : 0u) : 0u;
+        if (count && lane == 0 && g.gixo && o.L > CH && o.L > g.gix_min && o.L <= GIX_MAXL && o.q &&
+            !g.gixo[g.tv[t]])
+            atomicAdd(&b_gix, 2ull << nb_log2size(max(gixe, 1u)));
+        if (!state) continue;
         gkp(a, GK_KIND0, i)[lane] = pl.kind;
         gkp(a, GK_C, i)[lane] = pl.c;
         gkp(a, GK_INSK, i)[lane] = pl.insk;
@@ -195,6 +208,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
             a.vq[i] = o.q;
             a.vm[i] = o.L - h.d;
             a.vlist0[i] = pl.list0;
+            a.vgixe[i] = gixe;
             scr_need[i] = bsp_scr_words(o.L, o.q, __popc(pl.list0));
             // chunk items only for LARGE vertices (L > CH); a small vertex's scans are
             // done by its own warp inside alloc_insert / finalize
@@ -215,6 +229,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
         if (b_mem) atomicAdd(&cnt->need_mem, b_mem);
         if (b_res) atomicAdd(&cnt->reserve_mem, b_res);
         if (b_hix) atomicAdd(&cnt->need_hix, b_hix);
+        if (b_gix) atomicAdd(&cnt->need_gix, b_gix);
         if (b_flag) atomicOr(&cnt->flag, b_flag);
     }
 }
@@ -223,15 +238,15 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
 struct BspTotals {
     UpdCounters c;
     unsigned long long bump[3];
-    unsigned long long scr, copy, sel, grp, all, hubs, bigs, hix_used;
+    unsigned long long scr, copy, sel, grp, all, hubs, bigs, hix_used, gix_used;
     unsigned long long nt;     // touched vertices
     int abort;                 // one-sync route: 1 EINVAL, 4 EOVERFLOW, 2 capacity (the host grows, re-runs)
     int pad;
 };
 // capacities the one-sync route was enqueued with
 struct BspCaps {
-    unsigned long long arc, bkt, mem_units, hix, scr_words, sel, grp;
-    int hix_on;
+    unsigned long long arc, bkt, mem_units, hix, scr_words, sel, grp, gix;
+    int hix_on, gix_on;
 };
 // Totals of the plan.  One-sync route (abort != null): also its gate -- the totals against
 // what was allocated when the batch was enqueued.  Anything that does not fit (or an invalid
@@ -253,6 +268,7 @@ __global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint
     t.hubs = *a.nhubs;
     t.bigs = *a.nbigs;
     t.hix_used = a.g.bump[5];
+    t.gix_used = a.g.bump[6];
     t.nt = nt;
     t.pad = 0;
     int ab = 0;
@@ -264,6 +280,7 @@ __global__ void k_bsp_totals(const BspArgs a, const UpdCounters *cnt, const uint
             t.bump[2] + t.c.need_mem + t.c.reserve_mem > caps.mem_units)
             ab |= 2;
         if (caps.hix_on && t.c.need_hix && t.hix_used + t.c.need_hix > caps.hix) ab |= 2;
+        if (caps.gix_on && t.c.need_gix && t.gix_used + t.c.need_gix > caps.gix) ab |= 2;
         if (t.scr > caps.scr_words || t.sel > caps.sel || t.grp > caps.grp) ab |= 2;
         *abort = ab;
     }
@@ -337,7 +354,10 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_alloc_insert(const B
             }
         }
         // inserts in batch order: adjacency appends at d + rank,
-        // member appends to groups that are REGULAR/SPARSE before the batch
+        // member appends to groups that are REGULAR/SPARSE before the batch (and their
+        // group-index entries, when the vertex has a table)
+        const uint64_t go = (g.gixo && m && L > CH) ? g.gixo[g.tv[t]] : 0ull;
+        bool gok = true;
         if (m) {
             uint32_t run = 0, insk = 0;
             for (uint32_t base = beg; base < end; base += 32) {
@@ -362,15 +382,18 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_alloc_insert(const B
                     const uint32_t start = __shfl_sync(0xffffffffu, c + insk, k);
                     const uint32_t mo = __shfl_sync(0xffffffffu, moff, k);
                     if (is_list(kind_kk) && ((w >> k) & 1u)) {
-                        const uint64_t e = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
+                        const uint32_t sl = start + __popc(bal & lanemask_lt());
+                        const uint64_t e = (uint64_t)mo * 4 + sl;
                         g.mdst[e] = r.z;
                         g.midx[e] = idx;
+                        if (go) gok &= gix_insert(gix_table(g.gix, go), gix_key(idx, (uint32_t)k), sl);
                     }
                     if (lane == (uint32_t)k) insk += __popc(bal);
                 }
                 run += __popc(bal_i);
             }
         }
+        if (go && !__all_sync(0xffffffffu, gok) && lane == 0) g.gixo[g.tv[t]] = 0;   // full: rebuilt when needed
         // delete scratch: bitmap, hash of the distinct deleted destinations
         if (q) {
             const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
@@ -678,7 +701,8 @@ __global__ void __launch_bounds__(256) k_bsp_sort_big(const BspArgs a) {
 
 // group tail window [L_k', c'): survivors, renamed, fill the holes in rank order (R-6)
 __device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s, uint32_t *Md, uint32_t *Mi,
-                                           const uint32_t *gh, uint32_t cp, uint32_t Nk, uint32_t Lp) {
+                                           const uint32_t *gh, uint32_t cp, uint32_t Nk, uint32_t Lp,
+                                           uint64_t gixo = 0, uint32_t k = 0) {
     const uint32_t lane = lane_id();
     uint32_t carry = 0;
     for (uint32_t s0 = cp - Nk; s0 < cp; s0 += 32) {
@@ -688,8 +712,10 @@ __device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s,
         const uint32_t bal = __ballot_sync(0xffffffffu, surv);
         if (surv) {
             const uint32_t hslot = gh[carry + __popc(bal & lanemask_lt())];
+            const uint32_t xn = x >= Lp ? s.R[x - Lp] : x;
             Md[hslot] = Md[sl];
-            Mi[hslot] = x >= Lp ? s.R[x - Lp] : x;
+            Mi[hslot] = xn;
+            if (gixo) gix_reslot(g, gixo, xn, k, hslot);   // its group-index entry follows
         }
         carry += __popc(bal);
     }
@@ -749,12 +775,16 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_finalize(const BspAr
                 if (b == ~0ull) continue;
                 const uint32_t p = (uint32_t)b;
                 atomicOr(&s.bm[p >> 5], 1u << (p & 31u));
-                if (hubs) s.holes[atomicAdd(&s_np[w], 1u)] = p;   // unordered; k_bsp_hub_sort orders them
                 const uint32_t hs = ++s.hsel[sl];
                 s.hprev[sl] = b;
                 s.hbest[sl] = ~0ull;
                 N++;
                 uint32_t bits = g.arc[aoff + p].y;
+                if (hubs) {   // unordered; k_bsp_hub_sort orders the positions, the group index reads the pairs
+                    const uint32_t j = atomicAdd(&s_np[w], 1u);
+                    s.holes[j] = p;
+                    s.pk[j] = make_uint2(p, bits);
+                }
                 while (bits) {
                     const int k = __ffs(bits) - 1;
                     bits &= bits - 1;
@@ -996,6 +1026,7 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_grp_write(const BspA
         const DelScr s = del_scr(g.scr + g.scr_off[gi.i], L, q);
         uint32_t *Mi = g.midx + (uint64_t)gi.moff * 4;
         const uint32_t Lk = gi.cp - gi.Nk;
+        if (g.gixo && (a.vgix[gi.i] == 1u || a.vgix[gi.i] == 2u || a.vgix[gi.i] == 4u)) continue;   // k_gix_front did it
         if (!a.vrank[gi.i]) {   // deleted slots appended (any order), sorted by k_bsp_grp_sort
             group_front_append(g, s, Mi, s.gh + gi.gho, gkp(a, GK_GHN, gi.i) + gi.k, gi.j * CH,
                                min(Lk, (gi.j + 1) * CH), Lp);
@@ -1023,6 +1054,7 @@ __global__ void __launch_bounds__(MT) k_bsp_grp_tail(const BspArgs a) {
         const uint32_t cp_l = gkp(a, GK_C, i)[lane] + gkp(a, GK_INSK, i)[lane];
         const uint32_t mo_l = gkp(a, GK_MOFF, i)[lane];
         const uint32_t gho_l = gkp(a, GK_GHO, i)[lane];
+        const uint64_t go = (g.gixo && (a.vgix[i] == 1u || a.vgix[i] == 2u)) ? g.gixo[g.tv[a.t0 + i]] : 0ull;
         while (gm) {
             const int k = __ffs(gm) - 1;
             gm &= gm - 1;
@@ -1030,7 +1062,8 @@ __global__ void __launch_bounds__(MT) k_bsp_grp_tail(const BspArgs a) {
             const uint32_t Nk = __shfl_sync(0xffffffffu, Nk_l, k);
             const uint32_t mo = __shfl_sync(0xffffffffu, mo_l, k);
             const uint32_t gho = __shfl_sync(0xffffffffu, gho_l, k);
-            group_tail(g, s, g.mdst + (uint64_t)mo * 4, g.midx + (uint64_t)mo * 4, s.gh + gho, cp, Nk, Lp);
+            group_tail(g, s, g.mdst + (uint64_t)mo * 4, g.midx + (uint64_t)mo * 4, s.gh + gho, cp, Nk, Lp, go,
+                       (uint32_t)k);
         }
     }
 }
@@ -1092,7 +1125,7 @@ __device__ __forceinline__ void rebuild_classify(const BspArgs &a, uint32_t i, R
 // records the first position of each find group in first_k
 __device__ __forceinline__ void fill_scan(const MutateArgs &g, uint64_t aoff, uint32_t pb, uint32_t pe, uint32_t fm,
                                           uint32_t fd, uint32_t moff_l, bool count_only, uint32_t &cnt_l,
-                                          uint32_t &first_l) {
+                                          uint32_t &first_l, uint64_t go = 0, uint32_t *vg = nullptr) {
     const uint32_t lane = lane_id();
     for (uint32_t base = pb; base < pe; base += 32) {
         const uint32_t p = base + lane;
@@ -1111,9 +1144,12 @@ __device__ __forceinline__ void fill_scan(const MutateArgs &g, uint64_t aoff, ui
                 const uint32_t start = __shfl_sync(0xffffffffu, cnt_l, kb);
                 const uint32_t mo = __shfl_sync(0xffffffffu, moff_l, kb);
                 if ((e.y >> kb) & 1u) {
-                    const uint64_t qq = (uint64_t)mo * 4 + start + __popc(bal & lanemask_lt());
+                    const uint32_t sl = start + __popc(bal & lanemask_lt());
+                    const uint64_t qq = (uint64_t)mo * 4 + sl;
                     g.mdst[qq] = e.x;
                     g.midx[qq] = p;
+                    // a group that became a list: its members enter the vertex's group index
+                    if (go && !gix_insert(gix_table(g.gix, go), gix_key(p, (uint32_t)kb), sl)) *vg = 4u;
                 }
             }
             if (lane == (uint32_t)kb) cnt_l += __popc(bal);
@@ -1175,6 +1211,17 @@ __device__ __forceinline__ void rebuild_write(const BspArgs &a, uint32_t i, cons
         if (g.nbt) g.nbo[u] = nb_pack(4 * aoff, nb_log2size(dn));
         if (!a.vhix[i] && g.hixo && g.hixo[u]) g.hixo[u] = 0;   // index not maintained by this batch
     }
+    if (g.gixo) {   // group index: kept only if this batch maintained it and the list groups stay lists
+        const uint32_t ent = warp_sum(is_list(r.kind1) ? r.cn : 0u);
+        if (lane == 0) {
+            const uint64_t o = g.gixo[u];
+            if (o) {
+                const uint32_t mode = a.vL[i] > CH ? a.vgix[i] : 0u;
+                const bool keep = (mode == 1u || mode == 2u) && 4ull * ((uint64_t)ent + g.gixt[u]) <= (3ull << (o >> 48));
+                if (!keep) g.gixo[u] = 0;
+            }
+        }
+    }
 }
 
 // small vertices (L <= CH): one warp each
@@ -1207,9 +1254,34 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild_big(const Bs
     const uint32_t lane = lane_id();
     BSP_WARP_LOOP(h, *a.nbigs) {
         const uint32_t i = a.bigs[h];
+        const uint32_t kind0 = gkp(a, GK_KIND0, i)[lane];
         RbLane r;
         uint32_t fm, fd;
         rebuild_classify(a, i, r, fm, fd);
+        const uint32_t gm = a.vgix[i];
+        if (a.g.gixo && (gm == 1u || gm == 2u)) {
+            // a group leaving the list layouts (-> one-element, dense or empty): its members
+            // leave the group index (the list itself, compacted, is still in place)
+            const uint32_t u = a.g.tv[a.t0 + i];
+            const GixT t = gix_table(a.g.gix, a.g.gixo[u]);
+            uint32_t lm = __ballot_sync(0xffffffffu, is_list(kind0) && !is_list(r.kind1) && r.cn);
+            uint32_t rem = 0;
+            while (lm) {
+                const int k = __ffs(lm) - 1;
+                lm &= lm - 1;
+                const uint32_t cn = __shfl_sync(0xffffffffu, r.cn, k);
+                const uint32_t *Mi = a.g.midx + (uint64_t)__shfl_sync(0xffffffffu, r.moff, k) * 4;
+                for (uint32_t sl = lane; sl < cn; sl += 32) {
+                    const uint32_t e = gix_find(t, gix_key(Mi[sl], (uint32_t)k));
+                    if (e != 0xFFFFFFFFu) {
+                        t.t[2 * e] = GIX_TOMB;
+                        rem++;
+                    }
+                }
+            }
+            rem = warp_sum(rem);
+            if (lane == 0 && rem) a.g.gixt[u] += rem;
+        }
         if (!(fm | fd)) {
             rebuild_write(a, i, r);
             continue;
@@ -1268,7 +1340,9 @@ __global__ void __launch_bounds__(LT) k_bsp_rebuild_fill(const BspArgs a) {
         __syncthreads();
         cnt = s_cnt[w][lane];
         first = 0xFFFFFFFFu;
-        fill_scan(a.g, aoff, pb, pe, fm, fd, moff_l, false, cnt, first);
+        const uint32_t gm = a.vgix[i];
+        const uint64_t go = (a.g.gixo && (gm == 1u || gm == 2u)) ? a.g.gixo[a.g.tv[a.t0 + i]] : 0ull;
+        fill_scan(a.g, aoff, pb, pe, fm, fd, moff_l, false, cnt, first, go, a.vgix + i);
         s_first[w][lane] = first;
         __syncthreads();
         if (w == 0 && ((fd >> lane) & 1u)) {

@@ -71,9 +71,11 @@ def _bias_of(u, v, e, hi):
 ROUTES = {
     "bsp": {},                                                  # bulk-synchronous pipeline (default)
     "bsp-sub": {"BINGO_BSP_MAXT": "7"},                         # ... in sub-batches of 7 touched vertices
-    "bsp-hix": {"BINGO_HUB_INDEX": "1"},                        # ... with the hub delete index (opt-in)
+    "bsp-hix": {"BINGO_HUB_INDEX": "1", "BINGO_INDEX_MIN": "1024"},   # ... with both update indices from 1K arcs
+    "bsp-noidx": {"BINGO_HUB_INDEX": "0", "BINGO_GROUP_INDEX": "0"},  # ... without any update index
     "bsp-sync": {"BINGO_UPD_SYNC": "1"},                        # ... host round trips after front end / plan
     "bsp-radix": {"BINGO_UPD_RADIX_FRONT": "1"},                # ... segmented by the radix sort
+    "bsp-nogix": {"BINGO_GROUP_INDEX": "0", "BINGO_INDEX_MIN": "1024"},  # ... hub delete index, group scans
     "legacy": {"BINGO_UPD_LEGACY": "1"},                        # per-vertex mutate kernels (warp / block)
     "legacy-block": {"BINGO_UPD_LEGACY": "1", "BINGO_UPD_SMALL_L": "0"},   # ... every vertex on a block
 }
@@ -87,6 +89,8 @@ ROUTES = {
     (7, False, 200, "bsp-hix", 3500), (8, False, 7, "bsp-hix", 5000), (9, True, 255, "bsp-hix", 3000),
     (0, False, 200, "bsp-sync", 700), (8, False, 7, "bsp-sync", 5000), (9, True, 255, "bsp-sync", 3000),
     (1, False, 1 << 20, "bsp-radix", 700), (8, False, 7, "bsp-radix", 5000),
+    (7, False, 200, "bsp-nogix", 3500), (9, True, 255, "bsp-nogix", 3000),
+    (7, False, 200, "bsp-noidx", 3500), (8, False, 7, "bsp-noidx", 5000),
     (0, False, 200, "legacy", 700), (3, False, 7, "legacy", 700), (7, False, 200, "legacy", 3500),
     (0, False, 200, "legacy-block", 700), (3, False, 7, "legacy-block", 700),
     (6, False, 1 << 20, "legacy-block", 700)])
@@ -284,6 +288,7 @@ def test_hub_delete_index_maintained_across_batches(hix, monkeypatch):
     load, and rebuilt (opt-in: BINGO_HUB_INDEX=1).  Dumps must equal the oracle's after every
     batch, index on and off."""
     monkeypatch.setenv("BINGO_HUB_INDEX", hix)
+    monkeypatch.setenv("BINGO_INDEX_MIN", "1024")
     rng = np.random.default_rng(2024)
     V = 3000
     deg = rng.integers(0, 6, size=V)
@@ -445,14 +450,16 @@ def test_streaming_queue_hub_handoff_and_pool_growth():
     _same(g, o, V)
 
 
-@pytest.mark.parametrize("hix", ["0", "1"])
-def test_one_sync_route_reruns_only_when_short(hix, monkeypatch):
+@pytest.mark.parametrize("hix,gix", [("0", "1"), ("1", "1"), ("1", "0")])
+def test_one_sync_route_reruns_only_when_short(hix, gix, monkeypatch):
     """The one-sync route (apply_bsp_async) enqueues the whole batch before the host knows
     the touched-vertex count; a batch that finds a pool or its scratch short mutates nothing
     and is re-applied on the synchronous route.  Bulk batches (> 256 records, so not the
     single-launch fast path) on a graph with hubs: every batch equals the oracle, the first
     batch(es) re-run while scratch is sized, later ones complete in one host round trip."""
     monkeypatch.setenv("BINGO_HUB_INDEX", hix)
+    monkeypatch.setenv("BINGO_GROUP_INDEX", gix)
+    monkeypatch.setenv("BINGO_INDEX_MIN", "1024")
     rng = np.random.default_rng(99)
     V = 4000
     deg = rng.integers(0, 12, size=V)
@@ -519,13 +526,16 @@ def test_segment_order_short_long_and_radix_fallback(hub_records):
         _same(g, o, V, f"hub_records {hub_records} batch {e}")
 
 
-@pytest.mark.parametrize("ndel", [20, 300, 5000])
-def test_hub_delete_routes_by_pick_count(ndel):
+@pytest.mark.parametrize("ndel,gix", [(20, "1"), (300, "1"), (5000, "1"), (300, "0")])
+def test_hub_delete_routes_by_pick_count(ndel, gix, monkeypatch):
     """A hub's holes come from its sorted picks (one warp for <= 32, a block sort for
     <= 4096) and its group holes from one pass over each group front plus a sort; a batch
     deleting more than 4096 arcs of one hub takes the counted-rank passes instead.  Each
     route must leave the oracle's structure (R-6 pairing on the adjacency and on every
-    member list)."""
+    member list).  With the group index (default) the group holes and renames of the sorted
+    routes come from its lookups, and the index persists across the batches."""
+    monkeypatch.setenv("BINGO_GROUP_INDEX", gix)
+    monkeypatch.setenv("BINGO_INDEX_MIN", "1024")
     rng = np.random.default_rng(ndel)
     V = 2000
     deg = rng.integers(0, 5, size=V)
@@ -536,7 +546,7 @@ def test_hub_delete_routes_by_pick_count(ndel):
     dst = rng.integers(0, V, size=A).astype(np.uint32)
     bias = rng.integers(1, 1 << 14, size=A).astype(np.uint32)
     g, o = _pair(ro, dst, bias)
-    for e in range(3):
+    for e in range(5):
         d = oracle.parse_dump(o.dump(), V)
         hub = [a[0] for a in d[0]["adj"]]
         pick = rng.choice(len(hub), size=min(ndel, len(hub)), replace=False)

@@ -38,6 +38,7 @@ for i in range(1, a.batches + 1):
     t1 = time.perf_counter()
     print(f"batch {i}: {e0.elapsed_time(e1):.3f} ms device, {1e3 * (t1 - t0):.3f} ms host, "
           f"touched {st['touched_vertices']}, deleted {st['deleted']}, missing {st['missing_deletes']}")
+print(f"update_reruns {g.info()['update_reruns']}")
 if a.single:
     recs = w.batches[0][: a.single]
     lat = []
