@@ -1107,7 +1107,15 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
     __shared__ MutSmem sm[32];
     __shared__ unsigned long long need_arc, need_bkt, need_mem;
     __shared__ uint32_t flag, ntouch, go, blockwide;
+    __shared__ uint32_t s_vst[VST];   // one touched vertex: its statistics stay in shared memory
     const uint32_t tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
+    // the pool bump pointers, read now so their latency hides behind the validation and plan
+    unsigned long long bump0 = 0, bump1 = 0, bump2 = 0;
+    if (tid == 0) {
+        bump0 = fa.m.bump[0];
+        bump1 = fa.m.bump[1];
+        bump2 = fa.m.bump[2];
+    }
     // a whole 1024-thread block on one touched vertex (the streaming kernel): its O(d) scans
     // are spread over 32 warps, so vertices up to FAST_MAXL arcs stay on this path
     const bool block_mode = blockDim.x == LT;
@@ -1196,8 +1204,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
         scr_off[nt] = acc;
         uint32_t f = flag;
         if (!(f & (FAST_INVAL | FAST_OVERFLOW))) {
-            const unsigned long long *c = fa.m.bump;
-            if (c[0] + need_arc > fa.arc_cap || c[1] + need_bkt > fa.bkt_cap || c[2] + need_mem > fa.mem_units_cap ||
+            if (bump0 + need_arc > fa.arc_cap || bump1 + need_bkt > fa.bkt_cap || bump2 + need_mem > fa.mem_units_cap ||
                 acc > fa.scr_cap)
                 f |= FAST_SLOW;
         }
@@ -1213,7 +1220,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
         a.tv = tv;
         a.scr_off = reinterpret_cast<const uint64_t *>(scr_off);
         a.scr = fa.scr;
-        a.vstats = fa.vstats;
+        a.vstats = nt == 1 ? s_vst : fa.vstats;
         // each warp's delete scratch in dynamic shared memory when it fits (else global)
         extern __shared__ __align__(16) uint32_t fast_wscr[];
         if (blockwide) mutate_vertex<LT>(a, 0, sm[0]);   // uniform: the single vertex, every thread
@@ -1232,8 +1239,9 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
         o->inserted = ins;
     }
     if (go && tid < 27) {
+        const uint32_t *vst = nt == 1 ? s_vst : fa.vstats;
         unsigned long long acc = 0;
-        for (uint32_t t = 0; t < nt; t++) acc += fa.vstats[(uint64_t)t * VST + tid];
+        for (uint32_t t = 0; t < nt; t++) acc += vst[(uint64_t)t * VST + tid];
         fa.out->stats[tid] = acc;
     }
     return fast_status(fin);
