@@ -166,7 +166,8 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
                                                  bool count, bool state) {
     __shared__ unsigned long long b_arc, b_bkt, b_mem, b_res, b_hix, b_gix;
     __shared__ int b_flag;
-    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = b_hix = b_gix = 0; b_flag = 0; }
+    __shared__ uint32_t b_done;
+    if (threadIdx.x == 0) { b_arc = b_bkt = b_mem = b_res = b_hix = b_gix = 0; b_flag = 0; b_done = 0; }
     __syncthreads();
     const uint32_t lane = lane_id();
     const MutateArgs &g = a.g;
@@ -222,15 +223,24 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_plan(const BspArgs a
         }
     }
     if (!count) return;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (b_arc) atomicAdd(&cnt->need_arc, b_arc);
-        if (b_bkt) atomicAdd(&cnt->need_bkt, b_bkt);
-        if (b_mem) atomicAdd(&cnt->need_mem, b_mem);
-        if (b_res) atomicAdd(&cnt->reserve_mem, b_res);
-        if (b_hix) atomicAdd(&cnt->need_hix, b_hix);
-        if (b_gix) atomicAdd(&cnt->need_gix, b_gix);
-        if (b_flag) atomicOr(&cnt->flag, b_flag);
+    // the block's last warp to finish publishes its totals (no block barrier: a warp that is
+    // done does not wait for the block's slowest vertex)
+    if (lane != 0) return;
+    __threadfence_block();
+    if (atomicAdd(&b_done, 1u) != (blockDim.x >> 5) - 1) return;
+    __threadfence_block();
+    {
+        const unsigned long long x_arc = *(volatile unsigned long long *)&b_arc, x_bkt = *(volatile unsigned long long *)&b_bkt,
+                                 x_mem = *(volatile unsigned long long *)&b_mem, x_res = *(volatile unsigned long long *)&b_res,
+                                 x_hix = *(volatile unsigned long long *)&b_hix, x_gix = *(volatile unsigned long long *)&b_gix;
+        const int x_flag = *(volatile int *)&b_flag;
+        if (x_arc) atomicAdd(&cnt->need_arc, x_arc);
+        if (x_bkt) atomicAdd(&cnt->need_bkt, x_bkt);
+        if (x_mem) atomicAdd(&cnt->need_mem, x_mem);
+        if (x_res) atomicAdd(&cnt->reserve_mem, x_res);
+        if (x_hix) atomicAdd(&cnt->need_hix, x_hix);
+        if (x_gix) atomicAdd(&cnt->need_gix, x_gix);
+        if (x_flag) atomicOr(&cnt->flag, x_flag);
     }
 }
 

@@ -70,6 +70,17 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
 #endif
     const Policies pol{pol_keep, pol_stream};
+#if BINGO_SMEM_HDR
+    for (uint32_t j = threadIdx.x; j < a.sm_hdr; j += blockDim.x)
+        s_thdr[j] = __ldg(reinterpret_cast<const unsigned long long *>(a.thdr) + j);
+#endif
+#if BINGO_SMEM_BKT
+    for (uint32_t j = threadIdx.x; j < 2 * a.sm_bkt; j += blockDim.x)
+        s_bkt[j] = __ldg(reinterpret_cast<const uint4 *>(a.bkt) + j);
+#endif
+#if BINGO_SMEM_HDR || BINGO_SMEM_BKT
+    __syncthreads();
+#endif
     const size_t row = (size_t)a.L + 1;
     const uint32_t lane = threadIdx.x & 31u;
     const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
@@ -88,6 +99,15 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                 fin = true;                                   // L = 0
             } else {
                 if (APP != BINGO_NODE2VEC || o == 0) {        // node2vec keeps u's header across proposals
+#if BINGO_SMEM_HDR
+                    if (u < a.sm_hdr) {
+                        const unsigned long long v = s_thdr[u];
+                        h.bkt_off = (uint32_t)v;
+                        h.n = (uint8_t)(v >> 32);
+                        h.flags = (uint8_t)(v >> 40);
+                        h.pad1 = 0;
+                    } else
+#endif
                     h = load_thdr(a.thdr + u, pol);
                     if (APP == BINGO_NODE2VEC && a.nbo)
                         cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
@@ -284,6 +304,10 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
         if (desc->app == BINGO_NODE2VEC && !a.n2v_always[c] && a.n2v_thr[c] == 0) return BINGO_E_INVAL;
     stop_threshold(desc->stop_num, desc->stop_den, &a.stop_thr, &a.stop_always);
     a.prof = prof;
+    // shared-memory staging: headers only where ids are hot-first (relabelled), not in the
+    // trace / float kernels
+    a.sm_hdr = (g->inv && !tr && !g->float_mode) ? (uint32_t)std::min<uint64_t>(BINGO_SMEM_HDR, g->V) : 0u;
+    a.sm_bkt = (!tr && !g->float_mode) ? (uint32_t)std::min<uint64_t>(BINGO_SMEM_BKT, g->bkt_cap) : 0u;
     a.trace = tr ? tr->trace : nullptr;
     a.trace_off = tr ? tr->off : nullptr;
     if (tr && (desc->app == BINGO_NODE2VEC || g->float_mode || (desc->flags & BINGO_WALK_WALKER_MAJOR) || !prof))

@@ -64,7 +64,24 @@ struct WalkArgs {
     // trace mode: record of step t of walker i at trace[trace_off[i] + t]
     uint4 *trace;
     const unsigned long long *trace_off;
+    // shared-memory staging (k_walk): the first sm_hdr thin headers (relabelled graphs: the
+    // hottest vertices) and the first sm_bkt buckets (hot-first pool) are copied into every
+    // block's shared memory at launch; 0 = off
+    uint32_t sm_hdr, sm_bkt;
 };
+
+#ifndef BINGO_SMEM_HDR
+#define BINGO_SMEM_HDR 0
+#endif
+#ifndef BINGO_SMEM_BKT
+#define BINGO_SMEM_BKT 0
+#endif
+#if BINGO_SMEM_HDR
+__shared__ unsigned long long s_thdr[BINGO_SMEM_HDR];
+#endif
+#if BINGO_SMEM_BKT
+__shared__ uint4 s_bkt[2 * BINGO_SMEM_BKT];
+#endif
 
 #ifdef BINGO_NO_L2_64B            // A/B experiment switch: no 64 B L2 fetch hint
 #define BINGO_L2F ""
@@ -136,7 +153,13 @@ __device__ __forceinline__ uint32_t sample_dst(const WalkArgs &a, const ThinHdr 
                                                uint32_t outer, WalkProf &prof, const Policies &pol) {
     const P4 r = draw_oi(w, t, outer, 0u, 0u, a.k0, a.k1);
     const uint32_t b = __umulhi(r.x, (uint32_t)h.n);
+#if BINGO_SMEM_BKT
+    const uint32_t bi = h.bkt_off + b;
+    const Bucket B = bi < a.sm_bkt ? unpack_bucket(s_bkt[2 * bi], s_bkt[2 * bi + 1])
+                                   : ldg_bucket(a.bkt + bi, (h.flags & 1u) ? pol.keep : pol.stream);
+#else
     const Bucket B = ldg_bucket(a.bkt + h.bkt_off + b, (h.flags & 1u) ? pol.keep : pol.stream);
+#endif
     if (PROF) prof.bkt++;
     if (TRACE) prof.rec.y = (h.bkt_off + b) | ((uint32_t)(h.flags & 1u) << 31);
     const bool alt = join64(r.y, r.z) >= B.lim;
