@@ -1694,19 +1694,17 @@ static bool hix_disabled() {
 }
 
 // Both update indices (hub delete index, group index) are kept only for vertices of more than
-// BINGO_INDEX_MIN arcs (default 16384; the build raises it 4x at a time until the tables fit
+// BINGO_INDEX_MIN arcs (default 4096; the build raises it 4x at a time until the tables fit
 // their memory budget).  Below that the O(d) scans of the bulk-synchronous route are cheaper
-// than keeping a table exact across batches (measured: at c2, hubs of 1K-16K
-// arcs change group layouts and get rebuilt often enough that indexing them made batches
-// slower, 0.82 -> 1.1-1.6 ms).
+// than keeping a table exact across batches (measured).
 static uint32_t index_min() {
-    uint32_t m = 16 * CH;
+    uint32_t m = 4 * CH;
     if (const char *ev = getenv("BINGO_INDEX_MIN")) m = std::max<uint32_t>(CH, (uint32_t)strtoul(ev, nullptr, 10));
     return m;
 }
 // Without BINGO_INDEX_MIN the indices are built only for graphs of >= 2^28 arcs: on smaller
 // graphs the hubs are small enough that their scans beat keeping tables (c2: 0.82 ms per
-// 100K-record batch without, 1.05 ms with; c4: 1.51 ms without, 1.34 ms with).
+// 100K-record batch without, 1.05-1.5 ms with; c4: 1.51 ms without, ~1.2 ms with).
 static bool index_wanted(const bingo_graph *g) {
     return getenv("BINGO_INDEX_MIN") != nullptr || g->num_arcs >= (1ull << 28);
 }
@@ -1793,6 +1791,13 @@ static unsigned bsp_wg() {
     unsigned per_sm = 16;
     if (const char *ev = getenv("BINGO_BSP_WG")) per_sm = std::max(1u, (unsigned)strtoul(ev, nullptr, 10));
     return 148 * per_sm;
+}
+
+// BINGO_BSP_FUSED=1: small vertices by the fused k_bsp_small instead of k_bsp_finalize +
+// k_bsp_rebuild (A/B: the fused kernel spills more and was 2-3% slower at c2 and c4)
+static bool bsp_unfused() {
+    const char *ev = getenv("BINGO_BSP_FUSED");
+    return !(ev && ev[0] == '1');
 }
 
 // touched vertices per sub-batch (BINGO_BSP_MAXT: smaller sub-batches, tests)
@@ -1912,9 +1917,16 @@ static bingo_status bsp_vscratch(bingo_graph *g, uint64_t words) {
     return ensure_buf(g, g->vscratch, g->vscratch_bytes, need + need / 2) ? BINGO_OK : BINGO_E_NOMEM;
 }
 
+// The hub chain (a long sequence of dependent, mostly small kernels) is the critical path of a
+// batch; the small-vertex chain beside it is bulk work over all SMs.  The side stream gets the
+// highest priority, so the block scheduler starts the hub kernels' blocks first whenever SMs
+// free up (BINGO_AUX_PRIO=0: default priority, A/B).
 static bingo_status ensure_aux_stream(bingo_graph *g) {
     if (g->aux_stream) return BINGO_OK;
-    if (cudaStreamCreateWithFlags(&g->aux_stream, cudaStreamNonBlocking) != cudaSuccess ||
+    int least = 0, greatest = 0;
+    const char *ev = getenv("BINGO_AUX_PRIO");
+    if ((ev && ev[0] == '0') || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) greatest = 0;
+    if (cudaStreamCreateWithPriority(&g->aux_stream, cudaStreamNonBlocking, greatest) != cudaSuccess ||
         cudaEventCreateWithFlags(&g->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&g->ev_join, cudaEventDisableTiming) != cudaSuccess)
         return BINGO_E_CUDA;
@@ -2095,8 +2107,12 @@ static bingo_status apply_bsp(bingo_graph *g, const uint4 *recs, const uint32_t 
             g_trace.mark("hub: rebuild_big", sh);
         }
         // -- small vertices
-        if (ht->scr) BSP_LAUNCH(k_bsp_finalize, warp_grid(nt, WG), s, a, false);
-        BSP_LAUNCH(k_bsp_rebuild, warp_grid(nt, WG), s, a);
+        if (bsp_unfused()) {
+            if (ht->scr) BSP_LAUNCH(k_bsp_finalize, warp_grid(nt, WG), s, a, false);
+            BSP_LAUNCH(k_bsp_rebuild, warp_grid(nt, WG), s, a);
+        } else {
+            BSP_LAUNCH(k_bsp_small, warp_grid(nt, WG), s, a);
+        }
         g_trace.mark("small-vertex chain", s);
         if (side) {
             UCK(cudaEventRecord(g->ev_join, sh));
@@ -2242,8 +2258,12 @@ static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uin
     UCK(cudaGetLastError());
     g_trace.mark("hub: rebuild_big", sh);
     // -- small vertices
-    BSP_LAUNCH(k_bsp_finalize, wg, s, a, false);
-    BSP_LAUNCH(k_bsp_rebuild, wg, s, a);
+    if (bsp_unfused()) {
+        BSP_LAUNCH(k_bsp_finalize, wg, s, a, false);
+        BSP_LAUNCH(k_bsp_rebuild, wg, s, a);
+    } else {
+        BSP_LAUNCH(k_bsp_small, wg, s, a);
+    }
     g_trace.mark("small-vertex chain", s);
     UCK(cudaEventRecord(g->ev_join, sh));
     UCK(cudaStreamWaitEvent(s, g->ev_join, 0));

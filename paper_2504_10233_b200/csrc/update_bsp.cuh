@@ -734,155 +734,164 @@ __device__ __forceinline__ void group_tail(const MutateArgs &g, const DelScr &s,
 // ------------------------------------------------------------------ picks, further rounds, per-group counts
 // hubs = false: small vertices (all of their delete path here); hubs = true: the
 // large vertices with deletes (picks only; the rest by the chunk-item kernels)
+// one vertex of k_bsp_finalize (hubs: picks only; small vertices: the whole delete-and-swap);
+// the warp's shared-memory slices are passed in
+__device__ __forceinline__ void finalize_vertex(const BspArgs &a, const uint32_t i, const bool hubs, uint32_t *s_delk_w,
+                                                uint32_t *s_np_w, uint32_t *s_bm_w, uint32_t *s_hol_w,
+                                                uint32_t *s_R_w, uint32_t *s_gh_w) {
+    const uint32_t lane = lane_id();
+    const MutateArgs &g = a.g;
+    const uint32_t q = a.vq[i];
+    const uint32_t L = a.vL[i];
+    const bool small = L <= CH;
+    if (!q || small == hubs) return;
+    const uint64_t aoff = a.vaoff[i];
+    const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
+    const uint32_t hmask = s.Hq - 1;
+    s_delk_w[lane] = 0;
+    if (lane == 0) *s_np_w = 0;
+    if (small) {
+        // round 0 of a small vertex (large ones: k_bsp_select items)
+        for (uint32_t p = lane; p < L; p += 32) {
+            const uint32_t hit = hash_find(s.hkey, hmask, g.arc[aoff + p].x);
+            if (hit == EMPTY_KEY) continue;
+            const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
+            atomicAdd(&s.hfound[hit], 1u);
+            atomicMin(&s.hbest[hit], key);
+        }
+    }
+    __syncwarp();
+    uint32_t N = 0;
+    for (uint32_t round = 0;; round++) {
+        if (round) {
+            // round r > 0: per destination still owed a delete, the smallest key
+            // above the previous pick (repeated deletes of one (u, v), R-8)
+            for (uint32_t p = lane; p < L; p += 32) {
+                const uint32_t hit = hash_find(s.hkey, hmask, g.arc[aoff + p].x);
+                if (hit == EMPTY_KEY) continue;
+                const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
+                if (s.hsel[hit] < s.hk[hit] && key > s.hprev[hit]) atomicMin(&s.hbest[hit], key);
+            }
+            __syncwarp();
+        }
+        bool more = false;
+        for (uint32_t sl = lane; sl < s.Hq; sl += 32) {
+            if (s.hkey[sl] == EMPTY_KEY || s.hsel[sl] >= s.hk[sl]) continue;
+            const unsigned long long b = s.hbest[sl];
+            if (b == ~0ull) continue;
+            const uint32_t p = (uint32_t)b;
+            atomicOr(&s.bm[p >> 5], 1u << (p & 31u));
+            const uint32_t hs = ++s.hsel[sl];
+            s.hprev[sl] = b;
+            s.hbest[sl] = ~0ull;
+            N++;
+            uint32_t bits = g.arc[aoff + p].y;
+            if (hubs) {   // unordered; k_bsp_hub_sort orders the positions, the group index reads the pairs
+                const uint32_t j = atomicAdd(s_np_w, 1u);
+                s.holes[j] = p;
+                s.pk[j] = make_uint2(p, bits);
+            }
+            while (bits) {
+                const int k = __ffs(bits) - 1;
+                bits &= bits - 1;
+                atomicAdd(&s_delk_w[k], 1u);
+            }
+            if (hs < s.hk[sl] && hs < s.hfound[sl]) more = true;
+        }
+        __syncwarp();
+        if (!__any_sync(0xffffffffu, more)) break;
+    }
+    uint32_t miss = 0;
+    for (uint32_t sl = lane; sl < s.Hq; sl += 32)
+        if (s.hkey[sl] != EMPTY_KEY) miss += s.hk[sl] - s.hsel[sl];
+    N = warp_sum(N);
+    miss = warp_sum(miss);
+    __syncwarp();
+    const uint32_t delk = s_delk_w[lane];
+    const uint32_t list0 = a.vlist0[i];
+    // gh offsets: the deleted-slot lists of the list groups, packed in k order
+    const uint32_t v = ((list0 >> lane) & 1u) ? delk : 0u;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= (uint32_t)o) x += y;
+    }
+    gkp(a, GK_DELK, i)[lane] = delk;
+    gkp(a, GK_GHO, i)[lane] = x - v;
+    if (lane == 0) {
+        a.vN[i] = N;
+        a.vmiss[i] = miss;
+    }
+    __syncwarp();
+    if (!small || !N) return;
+    // ---- small vertex: the whole delete-and-swap here (L <= CH: one bitmap word per lane)
+    const uint32_t Lp = L - N;
+    DelScr ls = s;
+    ls.bm = s_bm_w;
+    s_bm_w[lane] = lane < (L + 31) / 32 ? s.bm[lane] : 0u;
+    if (N <= 32) {
+        ls.holes = s_hol_w;
+        ls.R = s_R_w;
+    }
+    if (__shfl_sync(0xffffffffu, x, 31) <= 64) ls.gh = s_gh_w;
+    __syncwarp();
+    {
+        uint32_t word = 0;
+        if (lane * 32 < Lp) {
+            word = ls.bm[lane];
+            const uint32_t lim = Lp - lane * 32;
+            if (lim < 32) word &= (1u << lim) - 1u;
+        }
+        const uint32_t pc = __popc(word);
+        uint32_t y = pc;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= (uint32_t)o) y += z;
+        }
+        uint32_t r = y - pc;
+        while (word) {
+            const int b = __ffs(word) - 1;
+            word &= word - 1;
+            ls.holes[r++] = lane * 32 + b;
+        }
+    }
+    __syncwarp();
+    const uint32_t moved = tail_window(g, ls, aoff, L, Lp);
+    __syncwarp();
+    if (N <= 32 && lane < N) s.R[lane] = ls.R[lane];   // rebuild reads R (ONE groups)
+    const uint32_t cp_l = gkp(a, GK_C, i)[lane] + gkp(a, GK_INSK, i)[lane];
+    const uint32_t mo_l = gkp(a, GK_MOFF, i)[lane];
+    // only groups that lost a member or hold an arc that moved change
+    uint32_t lm = list0 & (__ballot_sync(0xffffffffu, delk != 0) | moved);
+    while (lm) {
+        const int k = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t cp = __shfl_sync(0xffffffffu, cp_l, k);
+        const uint32_t Nk = __shfl_sync(0xffffffffu, delk, k);
+        const uint32_t mo = __shfl_sync(0xffffffffu, mo_l, k);
+        const uint32_t gho = __shfl_sync(0xffffffffu, x - v, k);
+        uint32_t *Md = g.mdst + (uint64_t)mo * 4;
+        uint32_t *Mi = g.midx + (uint64_t)mo * 4;
+        group_front(g, ls, Mi, ls.gh + gho, 0, cp - Nk, 0, Lp);
+        __syncwarp();
+        if (Nk) group_tail(g, ls, Md, Mi, ls.gh + gho, cp, Nk, Lp);
+        __syncwarp();
+    }
+}
+
 __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_finalize(const BspArgs a, bool hubs) {
     __shared__ uint32_t s_delk[MT / 32][32];
     __shared__ uint32_t s_np[MT / 32];   // hubs: picks appended to the holes array so far
     // small vertices: bitmap, holes, rename table and group holes in shared memory
     __shared__ uint32_t s_bm[MT / 32][32], s_hol[MT / 32][32], s_R[MT / 32][32], s_gh[MT / 32][64];
     if (BSP_ABORTED(a)) return;
-    const uint32_t lane = lane_id(), w = threadIdx.x >> 5;
-    const MutateArgs &g = a.g;
+    const uint32_t w = threadIdx.x >> 5;
     const uint32_t NT = hubs ? *a.nhubs : bsp_nt(a);
     BSP_WARP_LOOP(j, NT) {
         const uint32_t i = hubs ? a.hubs[j] : j;
-        const uint32_t q = a.vq[i];
-        const uint32_t L = a.vL[i];
-        const bool small = L <= CH;
-        if (!q || small == hubs) continue;
-        const uint64_t aoff = a.vaoff[i];
-        const DelScr s = del_scr(g.scr + g.scr_off[i], L, q);
-        const uint32_t hmask = s.Hq - 1;
-        s_delk[w][lane] = 0;
-        if (lane == 0) s_np[w] = 0;
-        if (small) {
-            // round 0 of a small vertex (large ones: k_bsp_select items)
-            for (uint32_t p = lane; p < L; p += 32) {
-                const uint32_t hit = hash_find(s.hkey, hmask, g.arc[aoff + p].x);
-                if (hit == EMPTY_KEY) continue;
-                const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
-                atomicAdd(&s.hfound[hit], 1u);
-                atomicMin(&s.hbest[hit], key);
-            }
-        }
-        __syncwarp();
-        uint32_t N = 0;
-        for (uint32_t round = 0;; round++) {
-            if (round) {
-                // round r > 0: per destination still owed a delete, the smallest key
-                // above the previous pick (repeated deletes of one (u, v), R-8)
-                for (uint32_t p = lane; p < L; p += 32) {
-                    const uint32_t hit = hash_find(s.hkey, hmask, g.arc[aoff + p].x);
-                    if (hit == EMPTY_KEY) continue;
-                    const unsigned long long key = ((unsigned long long)g.arc_epoch[aoff + p] << 32) | p;
-                    if (s.hsel[hit] < s.hk[hit] && key > s.hprev[hit]) atomicMin(&s.hbest[hit], key);
-                }
-                __syncwarp();
-            }
-            bool more = false;
-            for (uint32_t sl = lane; sl < s.Hq; sl += 32) {
-                if (s.hkey[sl] == EMPTY_KEY || s.hsel[sl] >= s.hk[sl]) continue;
-                const unsigned long long b = s.hbest[sl];
-                if (b == ~0ull) continue;
-                const uint32_t p = (uint32_t)b;
-                atomicOr(&s.bm[p >> 5], 1u << (p & 31u));
-                const uint32_t hs = ++s.hsel[sl];
-                s.hprev[sl] = b;
-                s.hbest[sl] = ~0ull;
-                N++;
-                uint32_t bits = g.arc[aoff + p].y;
-                if (hubs) {   // unordered; k_bsp_hub_sort orders the positions, the group index reads the pairs
-                    const uint32_t j = atomicAdd(&s_np[w], 1u);
-                    s.holes[j] = p;
-                    s.pk[j] = make_uint2(p, bits);
-                }
-                while (bits) {
-                    const int k = __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    atomicAdd(&s_delk[w][k], 1u);
-                }
-                if (hs < s.hk[sl] && hs < s.hfound[sl]) more = true;
-            }
-            __syncwarp();
-            if (!__any_sync(0xffffffffu, more)) break;
-        }
-        uint32_t miss = 0;
-        for (uint32_t sl = lane; sl < s.Hq; sl += 32)
-            if (s.hkey[sl] != EMPTY_KEY) miss += s.hk[sl] - s.hsel[sl];
-        N = warp_sum(N);
-        miss = warp_sum(miss);
-        __syncwarp();
-        const uint32_t delk = s_delk[w][lane];
-        const uint32_t list0 = a.vlist0[i];
-        // gh offsets: the deleted-slot lists of the list groups, packed in k order
-        const uint32_t v = ((list0 >> lane) & 1u) ? delk : 0u;
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= (uint32_t)o) x += y;
-        }
-        gkp(a, GK_DELK, i)[lane] = delk;
-        gkp(a, GK_GHO, i)[lane] = x - v;
-        if (lane == 0) {
-            a.vN[i] = N;
-            a.vmiss[i] = miss;
-        }
-        __syncwarp();
-        if (!small || !N) continue;
-        // ---- small vertex: the whole delete-and-swap here (L <= CH: one bitmap word per lane)
-        const uint32_t Lp = L - N;
-        DelScr ls = s;
-        ls.bm = s_bm[w];
-        s_bm[w][lane] = lane < (L + 31) / 32 ? s.bm[lane] : 0u;
-        if (N <= 32) {
-            ls.holes = s_hol[w];
-            ls.R = s_R[w];
-        }
-        if (__shfl_sync(0xffffffffu, x, 31) <= 64) ls.gh = s_gh[w];
-        __syncwarp();
-        {
-            uint32_t word = 0;
-            if (lane * 32 < Lp) {
-                word = ls.bm[lane];
-                const uint32_t lim = Lp - lane * 32;
-                if (lim < 32) word &= (1u << lim) - 1u;
-            }
-            const uint32_t pc = __popc(word);
-            uint32_t y = pc;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
-                if (lane >= (uint32_t)o) y += z;
-            }
-            uint32_t r = y - pc;
-            while (word) {
-                const int b = __ffs(word) - 1;
-                word &= word - 1;
-                ls.holes[r++] = lane * 32 + b;
-            }
-        }
-        __syncwarp();
-        const uint32_t moved = tail_window(g, ls, aoff, L, Lp);
-        __syncwarp();
-        if (N <= 32 && lane < N) s.R[lane] = ls.R[lane];   // rebuild reads R (ONE groups)
-        const uint32_t cp_l = gkp(a, GK_C, i)[lane] + gkp(a, GK_INSK, i)[lane];
-        const uint32_t mo_l = gkp(a, GK_MOFF, i)[lane];
-        // only groups that lost a member or hold an arc that moved change
-        uint32_t lm = list0 & (__ballot_sync(0xffffffffu, delk != 0) | moved);
-        while (lm) {
-            const int k = __ffs(lm) - 1;
-            lm &= lm - 1;
-            const uint32_t cp = __shfl_sync(0xffffffffu, cp_l, k);
-            const uint32_t Nk = __shfl_sync(0xffffffffu, delk, k);
-            const uint32_t mo = __shfl_sync(0xffffffffu, mo_l, k);
-            const uint32_t gho = __shfl_sync(0xffffffffu, x - v, k);
-            uint32_t *Md = g.mdst + (uint64_t)mo * 4;
-            uint32_t *Mi = g.midx + (uint64_t)mo * 4;
-            group_front(g, ls, Mi, ls.gh + gho, 0, cp - Nk, 0, Lp);
-            __syncwarp();
-            if (Nk) group_tail(g, ls, Md, Mi, ls.gh + gho, cp, Nk, Lp);
-            __syncwarp();
-        }
+        finalize_vertex(a, i, hubs, s_delk[w], s_np + w, s_bm[w], s_hol[w], s_R[w], s_gh[w]);
     }
 }
 
@@ -1246,6 +1255,32 @@ __global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_rebuild(const BspArg
         if (fm | fd) {
             // one ascending pass over the post-batch adjacency materialises new lists
             // and finds the member of ONE groups
+            uint32_t cnt = 0, first = 0xFFFFFFFFu;
+            fill_scan(a.g, a.vaoff[i], 0, a.vL[i] - a.vN[i], fm, fd, r.moff, false, cnt, first);
+            if ((fd >> lane_id()) & 1u) r.one = first;
+        }
+        rebuild_write(a, i, r);
+    }
+}
+
+// small vertices (L <= CH): k_bsp_finalize(small) and k_bsp_rebuild fused -- the whole
+// delete-and-swap, then the rebuild, by one warp per vertex in one launch (its state is read
+// once, and no warp waits for the second kernel's launch and ramp)
+__global__ void __launch_bounds__(MT, BINGO_BSP_MINB) k_bsp_small(const BspArgs a) {
+    __shared__ uint32_t s_delk[MT / 32][32];
+    __shared__ uint32_t s_np[MT / 32];
+    __shared__ uint32_t s_bm[MT / 32][32], s_hol[MT / 32][32], s_R[MT / 32][32], s_gh[MT / 32][64];
+    if (BSP_ABORTED(a)) return;
+    const uint32_t w = threadIdx.x >> 5;
+    const uint32_t NT = bsp_nt(a);
+    BSP_WARP_LOOP(i, NT) {
+        if (a.vL[i] > CH) continue;
+        finalize_vertex(a, i, false, s_delk[w], s_np + w, s_bm[w], s_hol[w], s_R[w], s_gh[w]);
+        __syncwarp();
+        RbLane r;
+        uint32_t fm, fd;
+        rebuild_classify(a, i, r, fm, fd);
+        if (fm | fd) {
             uint32_t cnt = 0, first = 0xFFFFFFFFu;
             fill_scan(a.g, a.vaoff[i], 0, a.vL[i] - a.vN[i], fm, fd, r.moff, false, cnt, first);
             if ((fd >> lane_id()) & 1u) r.one = first;

@@ -73,6 +73,7 @@ ROUTES = {
     "bsp-sub": {"BINGO_BSP_MAXT": "7"},                         # ... in sub-batches of 7 touched vertices
     "bsp-hix": {"BINGO_HUB_INDEX": "1", "BINGO_INDEX_MIN": "1024"},   # ... with both update indices from 1K arcs
     "bsp-noidx": {"BINGO_HUB_INDEX": "0", "BINGO_GROUP_INDEX": "0"},  # ... without any update index
+    "bsp-fused": {"BINGO_BSP_FUSED": "1"},                      # ... small vertices by one fused kernel
     "bsp-sync": {"BINGO_UPD_SYNC": "1"},                        # ... host round trips after front end / plan
     "bsp-radix": {"BINGO_UPD_RADIX_FRONT": "1"},                # ... segmented by the radix sort
     "bsp-nogix": {"BINGO_GROUP_INDEX": "0", "BINGO_INDEX_MIN": "1024"},  # ... hub delete index, group scans
@@ -91,6 +92,7 @@ ROUTES = {
     (1, False, 1 << 20, "bsp-radix", 700), (8, False, 7, "bsp-radix", 5000),
     (7, False, 200, "bsp-nogix", 3500), (9, True, 255, "bsp-nogix", 3000),
     (7, False, 200, "bsp-noidx", 3500), (8, False, 7, "bsp-noidx", 5000),
+    (0, False, 200, "bsp-fused", 700), (5, True, 1 << 31, "bsp-fused", 700),
     (0, False, 200, "legacy", 700), (3, False, 7, "legacy", 700), (7, False, 200, "legacy", 3500),
     (0, False, 200, "legacy-block", 700), (3, False, 7, "legacy-block", 700),
     (6, False, 1 << 20, "legacy-block", 700)])
@@ -231,7 +233,7 @@ def test_small_batches_fast_path():
     _same(g, o, w.V, "after hub growth")
 
 
-@pytest.mark.parametrize("route", ["bsp", "bsp-sub", "bsp-sync", "legacy"])
+@pytest.mark.parametrize("route", ["bsp", "bsp-sub", "bsp-sync", "bsp-fused", "legacy"])
 def test_node2vec_neighbour_index_across_batches(route, monkeypatch):
     """The node2vec distance test (Eq.1, A-17) reads per-vertex neighbour sets that updates
     maintain in place (inserted destinations added, a destination whose last live instance
