@@ -155,11 +155,23 @@ __device__ __forceinline__ T warp_sum(T v) {
 #define BINGO_VISIT_PAD 4096u
 #endif
 #define BINGO_VISIT_STRIDE 32u
+#ifdef BINGO_VISIT_REC
+// A/B layout: every counter sits beside a copy of its vertex's thin header in one 16 B record
+// {header, count}, so a PPR step's header read and its visit increment share a sector (and a
+// page); the copies are refreshed from thdr at every PPR launch (k_visit_hdr)
+__host__ __device__ inline uint64_t visit_rec(uint32_t j) {
+    return j < BINGO_VISIT_PAD ? (uint64_t)j * BINGO_VISIT_STRIDE
+                               : (uint64_t)BINGO_VISIT_PAD * BINGO_VISIT_STRIDE + 2ull * (j - BINGO_VISIT_PAD);
+}
+__host__ __device__ inline uint64_t visit_slot(uint32_t j) { return visit_rec(j) + 1; }
+__host__ __device__ inline uint64_t visit_words(uint32_t V) { return visit_rec(V); }
+#else
 __host__ __device__ inline uint64_t visit_slot(uint32_t j) {
     return j < BINGO_VISIT_PAD ? (uint64_t)j * BINGO_VISIT_STRIDE
                                : (uint64_t)BINGO_VISIT_PAD * BINGO_VISIT_STRIDE + (j - BINGO_VISIT_PAD);
 }
 __host__ __device__ inline uint64_t visit_words(uint32_t V) { return visit_slot(V); }
+#endif
 
 // walker-claim counters: each walk launch takes the next of these slots (zeroed on its
 // stream), so up to BINGO_WALK_SLOTS launches may run concurrently on one graph.

@@ -108,6 +108,11 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                         h.pad1 = 0;
                     } else
 #endif
+#ifdef BINGO_VISIT_REC
+                    if (APP == BINGO_PPR && a.visit)
+                        h = load_thdr(reinterpret_cast<const ThinHdr *>(a.visit + visit_rec(u)), pol);
+                    else
+#endif
                     h = load_thdr(a.thdr + u, pol);
                     if (APP == BINGO_NODE2VEC && a.nbo)
                         cur_nbo = __ldg(reinterpret_cast<const unsigned long long *>(a.nbo + u));
@@ -269,6 +274,13 @@ struct TraceOut {
     const unsigned long long *off;
 };
 
+#ifdef BINGO_VISIT_REC
+__global__ void k_visit_hdr(uint32_t V, const ThinHdr *__restrict__ thdr, unsigned long long *visit) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x)
+        visit[visit_rec(u)] = *reinterpret_cast<const unsigned long long *>(thdr + u);
+}
+#endif
+
 bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint32_t *starts, uint32_t W,
                          uint32_t *paths, uint32_t *lengths, cudaStream_t s, unsigned long long *prof = nullptr,
                          const TraceOut *tr = nullptr) {
@@ -313,6 +325,12 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     if (tr && (desc->app == BINGO_NODE2VEC || g->float_mode || (desc->flags & BINGO_WALK_WALKER_MAJOR) || !prof))
         return BINGO_E_INVAL;
     if (!g->walk_ctr) return BINGO_E_STATE;
+#ifdef BINGO_VISIT_REC
+    if (desc->app == BINGO_PPR && a.visit && g->V) {
+        k_visit_hdr<<<(unsigned)std::min<uint64_t>((g->V + 255) / 256, 148ull * 16), 256, 0, s>>>(g->V, g->thdr, g->visit);
+        bingo_count_launch();
+    }
+#endif
     unsigned long long *claim = g->walk_ctr + (__atomic_fetch_add(&g->walk_slot, 1u, __ATOMIC_RELAXED) % BINGO_WALK_SLOTS);
     if (cudaMemsetAsync(claim, 0, sizeof(unsigned long long), s) != cudaSuccess) {
         g->poisoned = 1;
