@@ -166,11 +166,23 @@ __host__ __device__ inline uint64_t visit_rec(uint32_t j) {
 __host__ __device__ inline uint64_t visit_slot(uint32_t j) { return visit_rec(j) + 1; }
 __host__ __device__ inline uint64_t visit_words(uint32_t V) { return visit_rec(V); }
 #else
-__host__ __device__ inline uint64_t visit_slot(uint32_t j) {
-    return j < BINGO_VISIT_PAD ? (uint64_t)j * BINGO_VISIT_STRIDE
-                               : (uint64_t)BINGO_VISIT_PAD * BINGO_VISIT_STRIDE + (j - BINGO_VISIT_PAD);
+// A/B switch: the hottest vertices' counters split into BINGO_VISIT_COPIES sub-counters, each
+// in its own 256 B slot of a different copy of the padded region (copy r of vertex j at
+// (r * PAD + j) * STRIDE), a warp adding to copy (warp id mod COPIES) and the export summing
+// them.  Measured slower (more counter lines in L2 beats less same-line serialisation), so 1.
+// visit_slot(j) is copy 0, which every other writer uses.
+#ifndef BINGO_VISIT_COPIES
+#define BINGO_VISIT_COPIES 1u   // A/B (profiles/r02_visit_copies_ab.txt): 4 copies +5%, 8 +10%, 32 +51% walk time
+#endif
+__host__ __device__ inline uint64_t visit_slot_r(uint32_t j, uint32_t r) {
+    return j < BINGO_VISIT_PAD ? ((uint64_t)r * BINGO_VISIT_PAD + j) * BINGO_VISIT_STRIDE
+                               : (uint64_t)BINGO_VISIT_COPIES * BINGO_VISIT_PAD * BINGO_VISIT_STRIDE + (j - BINGO_VISIT_PAD);
 }
-__host__ __device__ inline uint64_t visit_words(uint32_t V) { return visit_slot(V); }
+__host__ __device__ inline uint64_t visit_slot(uint32_t j) { return visit_slot_r(j, 0); }
+__host__ __device__ inline uint64_t visit_words(uint32_t V) {
+    return V <= BINGO_VISIT_PAD ? (uint64_t)BINGO_VISIT_COPIES * BINGO_VISIT_PAD * BINGO_VISIT_STRIDE
+                                : visit_slot(V);
+}
 #endif
 
 // walker-claim counters: each walk launch takes the next of these slots (zeroed on its

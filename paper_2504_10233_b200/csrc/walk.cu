@@ -166,8 +166,14 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                             if (a.visit) {
                                 const unsigned act = __activemask();
                                 const unsigned same = __match_any_sync(act, u);
-                                if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u))
+                                if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u)) {
+#ifdef BINGO_VISIT_REC
                                     atomicAdd(&a.visit[visit_slot(u)], (unsigned long long)__popc(same));
+#else
+                                    const uint32_t r = ((threadIdx.x >> 5) + blockIdx.x) % BINGO_VISIT_COPIES;
+                                    atomicAdd(&a.visit[visit_slot_r(u, r)], (unsigned long long)__popc(same));
+#endif
+                                }
                             }
 #else
                             if (a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
@@ -831,7 +837,17 @@ extern "C" bingo_status bingo_walk_partition(bingo_graph *g, const bingo_walk_de
 // counts in external vertex order: out[u] = visit[inv[u]]
 __global__ void k_visit_gather(uint32_t V, const uint32_t *__restrict__ inv, const unsigned long long *__restrict__ visit,
                                unsigned long long *__restrict__ out) {
-    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) out[u] = visit[visit_slot(inv ? inv[u] : u)];
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
+        const uint32_t j = inv ? inv[u] : u;
+#ifdef BINGO_VISIT_REC
+        out[u] = visit[visit_slot(j)];
+#else
+        unsigned long long c = visit[visit_slot(j)];
+        if (j < BINGO_VISIT_PAD)
+            for (uint32_t r = 1; r < BINGO_VISIT_COPIES; r++) c += visit[visit_slot_r(j, r)];
+        out[u] = c;
+#endif
+    }
 }
 
 extern "C" bingo_status bingo_visit_counts(bingo_graph *g, uint64_t *counts, int reset, uint32_t flags, void *stream) {
