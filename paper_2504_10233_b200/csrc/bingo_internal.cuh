@@ -244,6 +244,7 @@ struct bingo_graph {
     uint64_t mem_cap = 0;              // entries
     unsigned long long *counters = nullptr;  // device bump pointers: [0] arc, [1] bkt, [2] mem units, [3..] scratch
     unsigned long long *visit = nullptr;     // [V] PPR visit counts
+    unsigned int *visit32 = nullptr;         // BINGO_VISIT32 A/B: per-launch u32 counts, folded into visit
     unsigned long long *walk_ctr = nullptr;  // [BINGO_WALK_SLOTS] walker-claim counters (counters + 16)
     uint32_t walk_slot = 0;                  // next claim-counter slot (host, atomic increment)
     int *dev_flag = nullptr;                 // device error flag

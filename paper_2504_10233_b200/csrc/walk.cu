@@ -20,8 +20,23 @@ using namespace bingo;
 
 namespace bingo {
 
+// PPR visit-count increment: a reduction in L2 with the evict_last hint, so the counter lines
+// stay resident between increments.  Without it each counter's line is evicted between its
+// (random, repeated) increments and every increment pays a DRAM read-modify-write: c4 PPR
+// 156.5 -> 134.7 ms (tools/ab_variants.sh, profiles/r02_visit_hint_ab.txt); evict_first for
+// the non-padded counters instead: 172 ms.  BINGO_VISIT_NOHINT: plain atomicAdd (A/B).
+__device__ __forceinline__ void visit_add(unsigned long long *p, unsigned long long v, const Policies &pol) {
+#ifdef BINGO_VISIT_NOHINT
+    atomicAdd(p, v);
+#else
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol.keep)
+                 : "memory");
+#endif
+}
+
 template <int APP, bool PROF, bool WMAJOR>
-__device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint32_t &w, uint32_t &u) {
+__device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint32_t &w, uint32_t &u,
+                                             const Policies &pol) {
     w = a.first_walker + (uint32_t)i;
     const uint32_t u0 = a.starts ? a.starts[i] : (uint32_t)(((uint64_t)a.first_walker + i) % a.V);   // external
     u = a.inv ? __ldg(a.inv + u0) : u0;
@@ -29,7 +44,11 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
         if (WMAJOR) a.paths[i * ((size_t)a.L + 1)] = u0;
         else __stcs(&a.paths[i], u0);
     }
-    if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
+#ifdef BINGO_VISIT32
+    if (APP == BINGO_PPR && a.visit32) atomicAdd(&a.visit32[visit_slot(u)], 1u);
+    else
+#endif
+    if (APP == BINGO_PPR && a.visit) visit_add(a.visit + visit_slot(u), 1ull, pol);
 }
 
 #ifndef BINGO_WALK_MINB
@@ -91,7 +110,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
     ThinHdr h;
     DecRec dr;
     dr.dcnt = 0;
-    if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u);
+    if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u, pol);
     for (;;) {
         bool fin = false;
         if (active) {
@@ -167,16 +186,29 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                                 const unsigned act = __activemask();
                                 const unsigned same = __match_any_sync(act, u);
                                 if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u)) {
-#ifdef BINGO_VISIT_REC
-                                    atomicAdd(&a.visit[visit_slot(u)], (unsigned long long)__popc(same));
-#else
-                                    const uint32_t r = ((threadIdx.x >> 5) + blockIdx.x) % BINGO_VISIT_COPIES;
-                                    atomicAdd(&a.visit[visit_slot_r(u, r)], (unsigned long long)__popc(same));
+#ifdef BINGO_VISIT32
+                                    if (a.visit32) atomicAdd(&a.visit32[visit_slot(u)], (unsigned)__popc(same));
+                                    else
 #endif
+                                    {
+#ifdef BINGO_VISIT_REC
+                                        atomicAdd(&a.visit[visit_slot(u)], (unsigned long long)__popc(same));
+#else
+                                        const uint32_t r = ((threadIdx.x >> 5) + blockIdx.x) % BINGO_VISIT_COPIES;
+#ifdef BINGO_VISIT_REDPOL        // A/B: counters of the non-padded (colder) vertices with an L2 evict_first hint
+                                        if (u >= BINGO_VISIT_PAD)
+                                            asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u64 [%0], %1, %2;"
+                                                         :: "l"(a.visit + visit_slot_r(u, r)), "l"((unsigned long long)__popc(same)),
+                                                            "l"(pol.stream) : "memory");
+                                        else
+#endif
+                                        visit_add(a.visit + visit_slot_r(u, r), (unsigned long long)__popc(same), pol);
+#endif
+                                    }
                                 }
                             }
 #else
-                            if (a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
+                            if (a.visit) visit_add(a.visit + visit_slot(u), 1ull, pol);
 #endif
 #endif
                             if (PROF) prof.visit++;
@@ -222,7 +254,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                 o = 0;
                 prev = 0xFFFFFFFFu;
                 prev_nbo = cur_nbo = 0;
-                if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u);
+                if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u, pol);
             }
         }
         if (!__any_sync(0xffffffffu, active)) break;
@@ -280,6 +312,20 @@ struct TraceOut {
     const unsigned long long *off;
 };
 
+#ifdef BINGO_VISIT32
+// fold one launch's u32 counts into the u64 totals (and clear them)
+__global__ void k_visit_fold(uint32_t V, unsigned int *v32, unsigned long long *visit) {
+    for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x) {
+        const uint64_t sl = visit_slot(u);
+        const unsigned int c = v32[sl];
+        if (c) {
+            visit[sl] += c;
+            v32[sl] = 0;
+        }
+    }
+}
+#endif
+
 #ifdef BINGO_VISIT_REC
 __global__ void k_visit_hdr(uint32_t V, const ThinHdr *__restrict__ thdr, unsigned long long *visit) {
     for (uint32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < V; u += gridDim.x * blockDim.x)
@@ -328,6 +374,23 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
     a.sm_bkt = (!tr && !g->float_mode) ? (uint32_t)std::min<uint64_t>(BINGO_SMEM_BKT, g->bkt_cap) : 0u;
     a.trace = tr ? tr->trace : nullptr;
     a.trace_off = tr ? tr->off : nullptr;
+    a.visit32 = nullptr;
+#ifdef BINGO_VISIT32
+    if (desc->app == BINGO_PPR && !tr && g->V) {
+        // a launch's visits (W x (1 + mean length)) must stay far below 2^32 per counter
+        const double mean = desc->stop_num ? std::min<double>((double)desc->stop_den / desc->stop_num,
+                                                              desc->length == BINGO_NO_CAP ? 1e30 : desc->length)
+                                           : 1.0;
+        if ((double)W * (1.0 + mean) < 2.0e9) {
+            if (!g->visit32) {
+                g->visit32 = (unsigned int *)bingo_dev_alloc(g, 4 * std::max<uint64_t>(visit_words(g->V), 1));
+                if (g->visit32 && cudaMemsetAsync(g->visit32, 0, 4 * std::max<uint64_t>(visit_words(g->V), 1), s) != cudaSuccess)
+                    return BINGO_E_CUDA;
+            }
+            a.visit32 = g->visit32;
+        }
+    }
+#endif
     if (tr && (desc->app == BINGO_NODE2VEC || g->float_mode || (desc->flags & BINGO_WALK_WALKER_MAJOR) || !prof))
         return BINGO_E_INVAL;
     if (!g->walk_ctr) return BINGO_E_STATE;
@@ -388,6 +451,12 @@ bingo_status launch_walk(bingo_graph *g, const bingo_walk_desc *desc, const uint
         return BINGO_E_CUDA;
     }
     bingo_count_launch();
+#ifdef BINGO_VISIT32
+    if (a.visit32) {
+        k_visit_fold<<<(unsigned)std::min<uint64_t>((g->V + 255) / 256, 148ull * 16), 256, 0, s>>>(g->V, a.visit32, g->visit);
+        bingo_count_launch();
+    }
+#endif
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         fprintf(stderr, "libbingo: walk launch failed: %s\n", cudaGetErrorString(e));
@@ -713,7 +782,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB) k_walk_part(const PartArgs p, 
         uint32_t u = a.inv ? __ldg(a.inv + ux) : ux;
         if (rec.w & 1u) {                                     // fresh walker: its start vertex is ours
             if (a.paths) __stcs(&a.paths[i], ux);
-            if (APP == BINGO_PPR && a.visit) atomicAdd(&a.visit[visit_slot(u)], 1ull);
+            if (APP == BINGO_PPR && a.visit) visit_add(a.visit + visit_slot(u), 1ull, pol);
         }
         bool finished = false;
         for (;;) {
@@ -725,7 +794,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB) k_walk_part(const PartArgs p, 
             if (a.paths) __stcs(&a.paths[(size_t)(t + 1) * a.W + i], nx);
             bool stop = false;
             if (APP == BINGO_PPR) {
-                if (a.visit) atomicAdd(&a.visit[visit_slot(next)], 1ull);
+                if (a.visit) visit_add(a.visit + visit_slot(next), 1ull, pol);
                 if (a.stop_always) {
                     stop = true;
                 } else {

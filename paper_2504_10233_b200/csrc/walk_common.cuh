@@ -68,6 +68,7 @@ struct WalkArgs {
     // hottest vertices) and the first sm_bkt buckets (hot-first pool) are copied into every
     // block's shared memory at launch; 0 = off
     uint32_t sm_hdr, sm_bkt;
+    unsigned int *visit32;  // BINGO_VISIT32 A/B: per-launch u32 counters (null: the u64 counters)
 };
 
 #ifndef BINGO_SMEM_HDR
