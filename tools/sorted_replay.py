@@ -25,6 +25,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c4")
 ap.add_argument("--records", type=float, default=6e8)
 ap.add_argument("--chunk", type=int, default=8)
+ap.add_argument("--variants", default="")
+ap.add_argument("--window", type=float, default=0, help="sort within windows of this many records")
 a = ap.parse_args()
 
 w = synth.make_workload(a.config, rounds=1, hold_rounds=10, device="cuda", resident=True)
@@ -57,8 +59,9 @@ out.update(walkers_traced=Wt, records=n)
 
 def replay(tr, off, tag):
     best = None
+    sw = {}
     for ahead in (1, 2, 4, 8):
-        for bps in (2, 4, 8):
+        for bps in (2, 4, 6, 8):
             ts = []
             for _ in range(2):
                 e0.record()
@@ -67,9 +70,10 @@ def replay(tr, off, tag):
                 torch.cuda.synchronize()
                 ts.append(e0.elapsed_time(e1))
             t = min(ts)
+            sw[f"a{ahead}b{bps}"] = round(t, 3)
             if best is None or t < best[0]:
                 best = (t, ahead, bps)
-    out[tag] = {"ms": best[0], "ahead": best[1], "bps": best[2], "g_records_s": n / best[0] / 1e6}
+    out[tag] = {"ms": best[0], "ahead": best[1], "bps": best[2], "g_records_s": n / best[0] / 1e6, "sweep": sw}
     print(tag, out[tag], flush=True)
 
 
@@ -79,12 +83,30 @@ coff = torch.arange(0, n + C, C, dtype=torch.int64, device="cuda").clamp_(max=n)
 coff = torch.unique_consecutive(coff)
 replay(trace, coff, "chunk")
 key = trace[:, 0].to(torch.int64)
-for k in (None, 14, 10, 6):
-    kk = key if k is None else (key >> k)
+win = int(a.window) if a.window else 0
+
+
+def hybrid(k, hot_bits, cold_shift):
+    # hubs (internal id = hot rank < 2^hot_bits) keep their own bin, the rest are binned by id >> cold_shift
+    h = 1 << hot_bits
+    return torch.where(k < h, k, h + (k >> cold_shift))
+
+
+variants = [("sorted", lambda k: k), ("bins10", lambda k: k >> 10), ("bins6", lambda k: k >> 6),
+            ("hyb15_s11", lambda k: hybrid(k, 15, 11)), ("hyb15_s8", lambda k: hybrid(k, 15, 8)),
+            ("hyb12_s11", lambda k: hybrid(k, 12, 11)), ("hyb17_s6", lambda k: hybrid(k, 17, 6))]
+if a.variants:
+    variants = [v for v in variants if v[0] in a.variants.split(",")]
+for tag, f in variants:
+    kk = f(key)
+    if win:   # sort within windows of `win` records (one super-step's worth of walkers)
+        kk = kk + (torch.arange(n, device="cuda", dtype=torch.int64) // win) * (1 << 40)
+        tag = tag + "_win"
     idx = torch.sort(kk, stable=True).indices
+    del kk
     st = trace.index_select(0, idx)
     del idx
-    replay(st, coff, "sorted" if k is None else f"bins{k}")
+    replay(st, coff, tag)
     del st
     torch.cuda.empty_cache()
 print(json.dumps(out))
