@@ -69,6 +69,9 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
 // only on the walker id (R-1), never on which lane ran it.
 // MODE: 0 plain, 1 load counters (bingo_walk_profile), 2 counters + access trace
 // (bingo_walk_trace; DeepWalk / PPR, integer biases).
+#ifndef WALK_CLAIM_CHUNK
+#define WALK_CLAIM_CHUNK 32u
+#endif
 template <int APP, int MODE, bool WMAJOR, bool FLT>   // FLT: float-bias graph (decimal groups, R-15)
 #ifndef BINGO_WALK_TPB
 #define BINGO_WALK_TPB 256
@@ -111,6 +114,22 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
     DecRec dr;
     dr.dcnt = 0;
     if (active) walker_start<APP, PROF, WMAJOR>(a, i, w, u, pol);
+    // PPR lanes finish one at a time (stop w.p. 1/80 per step): their walker ids beyond the
+    // static first one come from a warp-private reserve refilled WALK_CLAIM_CHUNK ids at a
+    // time, one chunk claimed ahead, so the launch counter's atomic (7.6% of the c4 PPR stall
+    // samples when every refill waited for it, ncu s3) leaves the dependent path: c4 PPR
+    // 134.0 -> 130.4 ms.  DeepWalk warps finish together (one refill per walk length) and
+    // keep the direct claim (the reserve: c2 11% slower); node2vec too (8 more registers, one
+    // block less per SM: c3 19.7 -> 25.8 ms).  A/B: profiles/r02_walk_claim_ab.txt.  Which
+    // lane runs which walker never changes a result (R-1).
+#ifdef BINGO_CLAIM_SINGLE
+    constexpr bool CHUNKED = false;
+#else
+    constexpr bool CHUNKED = APP == BINGO_PPR;
+#endif
+    unsigned long long res_base = 0, res_next = 0;
+    uint32_t res_left = 0;
+    if (CHUNKED && lane == 0) res_next = atomicAdd(claim, (unsigned long long)WALK_CLAIM_CHUNK);
     for (;;) {
         bool fin = false;
         if (active) {
@@ -240,15 +259,34 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                 }
             }
         }
-        // refill: the lanes that finished claim consecutive walker ids in lane order
+        // refill: the lanes that finished take consecutive walker ids in lane order
         const unsigned fmask = __ballot_sync(0xffffffffu, fin);
         if (fmask) {
-            const uint32_t leader = __ffs(fmask) - 1;
-            unsigned long long base = 0;
-            if (lane == leader) base = atomicAdd(claim, (unsigned long long)__popc(fmask));
-            base = __shfl_sync(0xffffffffu, base, leader);
+            unsigned long long id;
+            if (!CHUNKED) {   // one atomic on the launch counter per refill (the warp waits for it)
+                const uint32_t leader = __ffs(fmask) - 1;
+                unsigned long long base = 0;
+                if (lane == leader) base = atomicAdd(claim, (unsigned long long)__popc(fmask));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                id = base + __popc(fmask & ((1u << lane) - 1u));
+            } else {
+                // from the warp's reserve; when it runs out, switch to the chunk claimed ahead and
+                // claim the next one (lane 0's atomic result is read only at the following switch)
+                const uint32_t nf = __popc(fmask), rank = __popc(fmask & ((1u << lane) - 1u));
+                if (nf <= res_left) {
+                    id = res_base + rank;
+                    res_base += nf;
+                    res_left -= nf;
+                } else {
+                    const unsigned long long nb = __shfl_sync(0xffffffffu, res_next, 0);
+                    id = rank < res_left ? res_base + rank : nb + (rank - res_left);
+                    res_base = nb + (nf - res_left);
+                    res_left = WALK_CLAIM_CHUNK - (nf - res_left);
+                    if (lane == 0) res_next = atomicAdd(claim, (unsigned long long)WALK_CLAIM_CHUNK);
+                }
+            }
             if (fin) {
-                i = nthreads + base + __popc(fmask & ((1u << lane) - 1u));
+                i = nthreads + id;
                 active = i < a.W;
                 t = 0;
                 o = 0;
