@@ -1100,6 +1100,21 @@ __device__ __forceinline__ uint32_t fast_status(uint32_t f) {
     return (f & FAST_INVAL) ? FAST_INVAL : (f & FAST_OVERFLOW) ? FAST_OVERFLOW : (f & FAST_SLOW) ? FAST_SLOW : FAST_OK;
 }
 
+#ifdef BINGO_SQ_TRACE
+// measurement build only (tools/sq_trace.py): globaltimer marks of the streaming kernel's phases
+static constexpr uint32_t SQT_N = 8192;
+__device__ unsigned long long g_sqt[SQT_N][8];
+__shared__ unsigned long long s_sqt[8];
+#define SQ_MARK(j)                                                                               \
+    do {                                                                                         \
+        if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(s_sqt[j]));      \
+    } while (0)
+#else
+#define SQ_MARK(j) \
+    do {       \
+    } while (0)
+#endif
+
 __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint4 *src) {
     __shared__ uint4 recs[FAST_N];
     __shared__ uint32_t sval[FAST_N], seg[FAST_N + 1], tv[FAST_N];
@@ -1135,6 +1150,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
         }
     }
     __syncthreads();
+    SQ_MARK(1);
     // an invalid batch is rejected whole before anything is read through its ids (a src >= V
     // must never index hdr[]): uniform exit, nothing mutated (bingo.h: EINVAL)
     if (flag & FAST_INVAL) {
@@ -1212,6 +1228,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
         go = f == 0 ? 1u : 0u;
     }
     __syncthreads();
+    SQ_MARK(2);
     if (go) {
         MutateArgs a = fa.m;
         a.recs = recs;
@@ -1229,6 +1246,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
                 mutate_vertex<32>(a, t, sm[w], fast_wscr + w * WARP_SCR_WORDS, WARP_SCR_WORDS);
     }
     __syncthreads();
+    SQ_MARK(3);
     const uint32_t fin = flag;   // final since the barrier before the mutation
     if (tid == 0) {
         FastOut *o = fa.out;
@@ -1270,13 +1288,25 @@ struct alignas(32) StreamSlot {
     unsigned int pad;
     uint4 rec;
 };
+// The completion of a streamed record: ONE 32 B system-scope store (st.v8, a single PCIe
+// write), so no __threadfence_system is needed between the result and the sequence number that
+// publishes it (the fence cost 1.7 us per record, tools/sq_trace.py).  w0 = records completed;
+// w1 = status | ntouch << 4 | inserted << 8 | missing << 16 (bit 31: the statistics did not fit
+// and are in StreamQ::out, written and fenced before this store); w2 = deleted; w3..w7 = the 25
+// kind-transition counts, 6 bits each (a single touched vertex has <= 32 groups), and w7's top
+// 10 bits repeat w0's low 10 bits so the host can tell a torn read.
+struct alignas(32) SqDone {
+    unsigned int w[8];
+};
 struct StreamQ {
     unsigned int run_gen;     // host -> device: the generation that may run
-    unsigned int done_seq;    // device -> host: records completed
+    unsigned int done_seq;    // (unused since the packed completion)
     unsigned int exit_gen;    // device -> host: the generation that exited ...
     unsigned int exit_seq;    // ... without taking record exit_seq (or after a FAST_SLOW record)
-    unsigned int pad[28];
-    FastOut out;              // device -> host: the last record's status / statistics
+    unsigned int pad[12];
+    SqDone done;              // device -> host: the last record's completion (packed)
+    unsigned int pad2[8];
+    FastOut out;              // device -> host: statistics that do not fit the packed completion
     StreamSlot slot[SQ_N];
 };
 
@@ -1312,12 +1342,44 @@ __device__ __forceinline__ uint4 ld_volatile_u4(const uint4 *p) {
     return v;
 }
 
+__device__ __forceinline__ void st_done(SqDone *p, const unsigned int (&d)[8]) {
+    asm volatile("st.relaxed.sys.global.v8.u32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(d[0]), "r"(d[1]),
+                 "r"(d[2]), "r"(d[3]), "r"(d[4]), "r"(d[5]), "r"(d[6]), "r"(d[7])
+                 : "memory");
+}
+
+// pack a record's result (SqDone); false if a field does not fit
+__device__ __forceinline__ bool sq_pack(const FastOut &o, unsigned int st, unsigned int seq, unsigned int (&d)[8]) {
+    const bool ok = st == FAST_OK;   // other statuses carry no statistics (the body leaves them unset)
+    bool fits = !ok || (o.ntouch < 16 && o.inserted < 256 && o.stats[1] < 256 && o.stats[0] <= 0xFFFFFFFFull);
+    unsigned long long f[3] = {0, 0, 0};   // 150-bit transition field, then w7's check bits
+    for (int i = 0; i < 25; i++) {
+        const unsigned long long c = ok ? o.stats[2 + i] : 0ull;
+        fits = fits && c < 64;
+        const int b = 6 * i;
+        f[b >> 6] |= (c & 63ull) << (b & 63);
+        if ((b & 63) > 58) f[(b >> 6) + 1] |= (c & 63ull) >> (64 - (b & 63));
+    }
+    d[0] = seq;
+    d[1] = ok ? ((st & 15u) | (o.ntouch & 15u) << 4 | ((unsigned int)o.inserted & 255u) << 8 |
+                 ((unsigned int)o.stats[1] & 255u) << 16 | (fits ? 0u : 1u << 31))
+              : (st & 15u);
+    d[2] = ok ? (unsigned int)o.stats[0] : 0u;
+    d[3] = (unsigned int)f[0];
+    d[4] = (unsigned int)(f[0] >> 32);
+    d[5] = (unsigned int)f[1];
+    d[6] = (unsigned int)(f[1] >> 32);
+    d[7] = ((unsigned int)f[2] & 0x3FFFFFu) | (seq & 0x3FFu) << 22;
+    return fits;
+}
+
 __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *q, unsigned int seq0, unsigned int gen) {
     __shared__ uint4 rec;
     __shared__ unsigned int cmd;   // 0 process, 1 exit
+    __shared__ FastOut s_out;      // the body's result, packed into ONE store below
     FastArgs fa = fa0;
     fa.n = 1;
-    fa.out = &q->out;
+    fa.out = &s_out;
     unsigned int k = seq0;
     for (;;) {
         if (threadIdx.x == 0) {
@@ -1329,6 +1391,7 @@ __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *
                 if (v.seq == k + 1 && v.chk == k + 1 && v.gen == gen) {
                     rec = v.rec;
                     c = 0;
+                    SQ_MARK(0);
                     break;
                 }
                 // stopped, or idle: exit without taking record k (the host relaunches)
@@ -1342,14 +1405,24 @@ __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *
         if (cmd) break;
         const unsigned int st = upd_fast_body(fa, &rec);
         __syncthreads();
+        SQ_MARK(4);
         k++;
         if (threadIdx.x == 0) {
             if (st == FAST_SLOW) {   // the host applies this record through the batched pipeline
                 *reinterpret_cast<volatile unsigned int *>(&q->exit_seq) = k;
                 *reinterpret_cast<volatile unsigned int *>(&q->exit_gen) = gen;
             }
-            __threadfence_system();
-            *reinterpret_cast<volatile unsigned int *>(&q->done_seq) = k;
+            unsigned int d[8];
+            if (!sq_pack(s_out, st, k, d)) {   // statistics too wide: the full FastOut, fenced first
+                q->out = s_out;
+                __threadfence_system();
+            }
+            SQ_MARK(5);
+            st_done(&q->done, d);
+#ifdef BINGO_SQ_TRACE
+            for (int j = 0; j < 6; j++) g_sqt[(k - 1) % SQT_N][j] = s_sqt[j];
+            g_sqt[(k - 1) % SQT_N][6] = st;
+#endif
         }
         if (st == FAST_SLOW) return;
         if (st == FAST_OK) fa.m.epoch++;
@@ -2952,6 +3025,7 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
     if (g->sq_running && g->sq_stream != s) bingo_sq_quiesce(g, s);
     StreamQ *q = (StreamQ *)g->sq_host;
     const unsigned k = g->sq_seq;
+    unsigned int dw[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     for (int attempt = 0;; attempt++) {
         if (!g->sq_running) {
             const bingo_status st = sq_launch(g, s);
@@ -2966,13 +3040,18 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
         __atomic_store_n(&sl->seq, k + 1, __ATOMIC_SEQ_CST);
         bool taken = false;
         for (uint64_t spin = 0;; spin++) {
-            if (__atomic_load_n(&q->done_seq, __ATOMIC_ACQUIRE) == k + 1) {
+            if (__atomic_load_n(&q->done.w[0], __ATOMIC_ACQUIRE) == k + 1) {
+                // one 32 B device store: re-read until w0 and w7's check bits agree (a torn read)
+                for (;;) {
+                    for (int j = 7; j >= 0; j--) dw[j] = __atomic_load_n(&q->done.w[j], __ATOMIC_ACQUIRE);
+                    if (dw[0] == k + 1 && (dw[7] >> 22) == ((k + 1) & 0x3FFu)) break;
+                }
                 taken = true;
                 break;
             }
             if (__atomic_load_n(&q->exit_gen, __ATOMIC_ACQUIRE) == gen &&
                 __atomic_load_n(&q->exit_seq, __ATOMIC_ACQUIRE) == k &&
-                __atomic_load_n(&q->done_seq, __ATOMIC_ACQUIRE) != k + 1) {
+                __atomic_load_n(&q->done.w[0], __ATOMIC_ACQUIRE) != k + 1) {
                 g->sq_running = false;   // idle exit raced with the post: relaunch and repost
                 break;
             }
@@ -2990,8 +3069,7 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
         }
     }
     g->sq_seq = k + 1;
-    const FastOut &o = q->out;
-    const uint32_t st = __atomic_load_n(&o.status, __ATOMIC_ACQUIRE);
+    const uint32_t st = dw[1] & 15u;
     if (st == FAST_INVAL) return BINGO_E_INVAL;
     if (st == FAST_OVERFLOW) return BINGO_E_OVERFLOW;
     if (st == FAST_SLOW) {   // the kernel has exited; this record goes through the batched pipeline
@@ -3000,15 +3078,44 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
     }
     if (st != FAST_OK) return upd_cuda_fail(g, cudaErrorUnknown, "k_stream_upd status");
     g->epoch++;
-    const uint64_t deleted = o.stats[0];
-    g->num_arcs = g->num_arcs + o.inserted - deleted;
+    uint64_t inserted, deleted, missing, ntouch, tr[25];
+    if (dw[1] >> 31) {   // the statistics did not fit the packed completion
+        const FastOut &o = q->out;
+        inserted = o.inserted;
+        deleted = o.stats[0];
+        missing = o.stats[1];
+        ntouch = o.ntouch;
+        for (int i = 0; i < 25; i++) tr[i] = o.stats[2 + i];
+    } else {
+        inserted = (dw[1] >> 8) & 255u;
+        missing = (dw[1] >> 16) & 255u;
+        ntouch = (dw[1] >> 4) & 15u;
+        deleted = dw[2];
+        const uint64_t f0 = (uint64_t)dw[3] | (uint64_t)dw[4] << 32, f1 = (uint64_t)dw[5] | (uint64_t)dw[6] << 32,
+                       f2 = dw[7] & 0x3FFFFFu;
+        const uint64_t f[3] = {f0, f1, f2};
+        for (int i = 0; i < 25; i++) {
+            const int b = 6 * i;
+            uint64_t c = f[b >> 6] >> (b & 63);
+            if ((b & 63) > 58) c |= f[(b >> 6) + 1] << (64 - (b & 63));
+            tr[i] = c & 63u;
+        }
+    }
+    g->num_arcs = g->num_arcs + inserted - deleted;
     if (stats) {
-        stats->inserted = o.inserted;
+        stats->inserted = inserted;
         stats->deleted = deleted;
-        stats->missing_deletes = o.stats[1];
-        stats->touched_vertices = o.ntouch;
-        for (int i = 0; i < 25; i++) stats->kind_transitions[i / 5][i % 5] = o.stats[2 + i];
+        stats->missing_deletes = missing;
+        stats->touched_vertices = ntouch;
+        for (int i = 0; i < 25; i++) stats->kind_transitions[i / 5][i % 5] = tr[i];
         stats->epoch = g->epoch;
     }
     return BINGO_OK;
 }
+
+#ifdef BINGO_SQ_TRACE
+extern "C" int bingo_sq_trace_read(unsigned long long *host, int n) {
+    if (n > (int)SQT_N) n = SQT_N;
+    return (int)cudaMemcpyFromSymbol(host, g_sqt, sizeof(unsigned long long) * 8 * n);
+}
+#endif
