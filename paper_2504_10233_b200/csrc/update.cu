@@ -1395,7 +1395,7 @@ __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *
                     break;
                 }
                 // stopped, or idle: exit without taking record k (the host relaunches)
-                if ((poll & 3u) == 3u &&
+                if ((poll & 15u) == 15u &&
                     (ld_volatile_u32(&q->run_gen) != gen || globaltimer_ns() - t0 > SQ_IDLE_NS))
                     break;
             }

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
 #endif
                                     {
 #ifdef BINGO_VISIT_REC
-                                        atomicAdd(&a.visit[visit_slot(u)], (unsigned long long)__popc(same));
+                                        visit_add(a.visit + visit_slot(u), (unsigned long long)__popc(same), pol);
 #else
                                         const uint32_t r = ((threadIdx.x >> 5) + blockIdx.x) % BINGO_VISIT_COPIES;
 #ifdef BINGO_VISIT_REDPOL        // A/B: counters of the non-padded (colder) vertices with an L2 evict_first hint
