@@ -1373,6 +1373,9 @@ __device__ __forceinline__ bool sq_pack(const FastOut &o, unsigned int st, unsig
     return fits;
 }
 
+#ifndef BINGO_SQ_CHECK_EVERY   // polls per stop / idle check (a check is one more PCIe read)
+#define BINGO_SQ_CHECK_EVERY 16u
+#endif
 __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *q, unsigned int seq0, unsigned int gen) {
     __shared__ uint4 rec;
     __shared__ unsigned int cmd;   // 0 process, 1 exit
@@ -1395,7 +1398,7 @@ __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *
                     break;
                 }
                 // stopped, or idle: exit without taking record k (the host relaunches)
-                if ((poll & 15u) == 15u &&
+                if ((poll % BINGO_SQ_CHECK_EVERY) == BINGO_SQ_CHECK_EVERY - 1 &&
                     (ld_volatile_u32(&q->run_gen) != gen || globaltimer_ns() - t0 > SQ_IDLE_NS))
                     break;
             }
