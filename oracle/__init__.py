@@ -88,6 +88,10 @@ def lib():
             L.ora_radix_walk.argtypes = [P, u32, u32, u64, u32, P, u32, P, P, P, u64, u32, ctypes.c_int]
             L.ora_radix_dump.argtypes = [P, P, ctypes.c_size_t]
             L.ora_radix_dump.restype = ctypes.c_size_t
+            L.ora_radix_apply_updates.argtypes = [P, P, u64, P]
+            L.ora_radix_apply_updates.restype = ctypes.c_int
+            L.ora_radix_adj.argtypes = [P, u32, P]
+            L.ora_radix_adj.restype = u32
             _lib = L
     return _lib
 
@@ -321,6 +325,28 @@ class RadixGraph:
 
     def sample(self, u, seed, w, t) -> int:
         return int(lib().ora_radix_sample(self._h, u, seed, w, t))
+
+    def apply_updates(self, recs) -> dict:
+        """One batch (reading R-19): the base-2 adjacency readings R-6..R-9, then the touched
+        vertices' nested structure rebuilt from their adjacency."""
+        r = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 4)
+        st = np.zeros(30, dtype=np.uint64)
+        rc = int(lib().ora_radix_apply_updates(self._h, _p(r) if len(r) else None, len(r), _p(st)))
+        if rc != 0:
+            raise ValueError(f"ora_radix_apply_updates failed with status {rc}")
+        return {"inserted": int(st[0]), "deleted": int(st[1]), "missing_deletes": int(st[2]),
+                "touched_vertices": int(st[3]), "epoch": int(st[29])}
+
+    def try_apply_updates(self, recs) -> int:
+        r = np.ascontiguousarray(recs, dtype=np.uint32).reshape(-1, 4)
+        return int(lib().ora_radix_apply_updates(self._h, _p(r) if len(r) else None, len(r), None))
+
+    def adjacency(self, u):
+        """[d, 3] uint32 array of (dst, bias, epoch) in adjacency order."""
+        d = int(lib().ora_radix_adj(self._h, u, None))
+        out = np.zeros((max(d, 1), 3), dtype=np.uint32)
+        lib().ora_radix_adj(self._h, u, _p(out))
+        return out[:d]
 
     def walk(self, app=APP_DEEPWALK, length=80, seed=0, first_walker=0, starts=None, num_walkers=None,
              stop=(1, 80), paths=True, counts=False, threads=0):

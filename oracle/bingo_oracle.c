@@ -1067,7 +1067,9 @@ typedef struct {
 
 typedef struct {
     uint32_t d, n;
-    const uint32_t *dst, *bias;
+    uint32_t *dst, *bias;     /* into the CSR copies, or the vertex's own arrays once updated */
+    uint32_t *epoch;          /* NULL: every arc from the build (epoch 0) */
+    uint32_t cap;             /* capacity of the own arrays (0: CSR-backed) */
     r_group *grp;
     uint64_t T;
 } r_vertex;
@@ -1076,6 +1078,7 @@ typedef struct ora_radix {
     uint32_t V, b;
     uint32_t *dst, *bias;     /* owned copies of the CSR arrays */
     r_vertex *v;
+    uint32_t epoch;           /* successful ora_radix_apply_updates calls (R-9) */
 } ora_radix;
 
 static uint32_t digit(uint32_t w, uint32_t i, uint32_t b)
@@ -1084,16 +1087,24 @@ static uint32_t digit(uint32_t w, uint32_t i, uint32_t b)
     return sh >= 32 ? 0u : (w >> sh) & ((1u << b) - 1u);
 }
 
+static void radix_free_groups(r_vertex *x)
+{
+    for (uint32_t g = 0; g < x->n; g++) {
+        for (uint32_t s = 0; s < x->grp[g].ns; s++) free(x->grp[g].sub[s].mem);
+        free(x->grp[g].sub);
+    }
+    free(x->grp);
+    x->grp = NULL;
+    x->n = 0;
+}
+
 void ora_radix_free(ora_radix *G)
 {
     if (!G) return;
     for (uint32_t u = 0; u < G->V; u++) {
         r_vertex *x = &G->v[u];
-        for (uint32_t g = 0; g < x->n; g++) {
-            for (uint32_t s = 0; s < x->grp[g].ns; s++) free(x->grp[g].sub[s].mem);
-            free(x->grp[g].sub);
-        }
-        free(x->grp);
+        radix_free_groups(x);
+        if (x->cap) { free(x->dst); free(x->bias); free(x->epoch); }
     }
     free(G->v);
     free(G->dst);
@@ -1101,12 +1112,14 @@ void ora_radix_free(ora_radix *G)
     free(G);
 }
 
+static int radix_build_vertex(r_vertex *x, uint32_t b);
+
 /* b in [1, 5]: B = 2^b <= 32, so a group has at most 31 subgroups. */
 int ora_build_radix(uint32_t V, const uint64_t *ro, const uint32_t *dst, const uint32_t *bias, uint32_t b,
                     ora_radix **out)
 {
     if (b < 1 || b > 5) return O_EINVAL;
-    const uint32_t B = 1u << b, K = (32 + b - 1) / b;
+    /* B = 2^b <= 32, K = ceil(32 / b) digit positions: see radix_build_vertex */
     ora_radix *G = (ora_radix *)calloc(1, sizeof(ora_radix));
     const uint64_t A = ro[V];
     G->V = V;
@@ -1121,11 +1134,23 @@ int ora_build_radix(uint32_t V, const uint64_t *ro, const uint32_t *dst, const u
         x->d = (uint32_t)(ro[u + 1] - ro[u]);
         x->dst = G->dst + ro[u];
         x->bias = G->bias + ro[u];
-        x->T = 0;
-        for (uint32_t a = 0; a < x->d; a++) {
+        for (uint32_t a = 0; a < x->d; a++)
             if (x->bias[a] == 0) { ora_radix_free(G); return O_EINVAL; }
-            x->T += x->bias[a];
-        }
+        if (radix_build_vertex(x, b) != O_OK) { ora_radix_free(G); return O_EOVERFLOW; }
+    }
+    *out = G;
+    return O_OK;
+}
+
+/* The nested structure of one vertex from its adjacency (x->dst, x->bias, x->d), replacing
+ * any previous one: groups in ascending i, subgroups in ascending j, members ascending. */
+static int radix_build_vertex(r_vertex *x, uint32_t b)
+{
+    const uint32_t B = 1u << b, K = (32 + b - 1) / b;
+    radix_free_groups(x);
+    {
+        x->T = 0;
+        for (uint32_t a = 0; a < x->d; a++) x->T += x->bias[a];
         /* groups in ascending i, subgroups in ascending j */
         x->grp = (r_group *)calloc(K, sizeof(r_group));
         for (uint32_t i = 0; i < K; i++) {
@@ -1162,7 +1187,7 @@ int ora_build_radix(uint32_t V, const uint64_t *ro, const uint32_t *dst, const u
             for (uint32_t s = 0; s < g->ns; s++) { g->sub[s].thr = thr[s]; g->sub[s].alias = al[s]; }
         }
         if (x->n) {
-            if ((unsigned __int128)x->T * x->n >= ((unsigned __int128)1 << 64)) { ora_radix_free(G); return O_EOVERFLOW; }
+            if ((unsigned __int128)x->T * x->n >= ((unsigned __int128)1 << 64)) return O_EOVERFLOW;
             uint64_t W[32], thr[32];
             uint32_t al[32];
             for (uint32_t g = 0; g < x->n; g++) W[g] = x->grp[g].W;
@@ -1170,8 +1195,140 @@ int ora_build_radix(uint32_t V, const uint64_t *ro, const uint32_t *dst, const u
             for (uint32_t g = 0; g < x->n; g++) { x->grp[g].thr = thr[g]; x->grp[g].alias = al[g]; }
         }
     }
-    *out = G;
     return O_OK;
+}
+
+/* Updates of a radix graph (reading R-19; the paper leaves nested dynamic structures to
+ * future work).  The adjacency follows exactly the base-2 readings: whole-batch
+ * validation (op 0/1, ids < V, insert bias > 0: a radix arc needs a nonzero digit), epoch =
+ * the number of the successful call (R-9), records grouped by source in batch order,
+ * inserts appended in batch order (R-7), each delete takes the live instance with the smallest
+ * (epoch, position) (R-8), the adjacency compacted by the two-phase delete-and-swap (R-6).
+ * Then every touched vertex's nested structure is rebuilt from its adjacency exactly as the
+ * build does (groups, subgroups, members ascending, both integer-Vose tables), so the structure
+ * stays a function of the adjacency.  Overflow (whole batch, nothing mutated): d + inserts >=
+ * 2^32 - 1, or (T + inserted biases) x ceil(32 / b) >= 2^64.  stats as ora_apply_updates
+ * ([0] inserted [1] deleted [2] missing [3] touched, [29] epoch; no kind transitions). */
+static void radix_own(r_vertex *x, uint32_t need)
+{
+    if (x->cap >= need && x->cap) return;
+    uint32_t cap = x->cap ? x->cap : 4;
+    while (cap < need) cap *= 2;
+    uint32_t *nd = (uint32_t *)malloc(sizeof(uint32_t) * cap), *nb = (uint32_t *)malloc(sizeof(uint32_t) * cap),
+             *ne = (uint32_t *)calloc(cap, sizeof(uint32_t));
+    memcpy(nd, x->dst, sizeof(uint32_t) * x->d);
+    memcpy(nb, x->bias, sizeof(uint32_t) * x->d);
+    if (x->epoch) memcpy(ne, x->epoch, sizeof(uint32_t) * x->d);
+    if (x->cap) { free(x->dst); free(x->bias); free(x->epoch); }
+    x->dst = nd;
+    x->bias = nb;
+    x->epoch = ne;
+    x->cap = cap;
+}
+
+int ora_radix_apply_updates(ora_radix *G, const uint32_t *recs, uint64_t n, uint64_t *stats)
+{
+    uint64_t st[30];
+    memset(st, 0, sizeof(st));
+    const uint32_t K = (32 + G->b - 1) / G->b;
+    for (uint64_t r = 0; r < n; r++) {
+        const uint32_t *rec = recs + 4 * r;
+        if (rec[0] > 1 || rec[1] >= G->V || rec[2] >= G->V) return O_EINVAL;
+        if (rec[0] == 0 && rec[3] == 0) return O_EINVAL;
+    }
+    /* stable grouping by source (counting sort keeps batch order) */
+    uint64_t *cnt = (uint64_t *)calloc((size_t)G->V + 1, sizeof(uint64_t));
+    for (uint64_t r = 0; r < n; r++) cnt[recs[4 * r + 1] + 1]++;
+    for (uint32_t u = 0; u < G->V; u++) cnt[u + 1] += cnt[u];
+    uint64_t *idx = (uint64_t *)malloc(sizeof(uint64_t) * (n ? n : 1));
+    uint64_t *pos = (uint64_t *)malloc(sizeof(uint64_t) * ((size_t)G->V + 1));
+    memcpy(pos, cnt, sizeof(uint64_t) * ((size_t)G->V + 1));
+    for (uint64_t r = 0; r < n; r++) idx[pos[recs[4 * r + 1]]++] = r;
+    free(pos);
+    /* overflow checks for every touched vertex before anything changes */
+    for (uint32_t u = 0; u < G->V; u++) {
+        if (cnt[u + 1] == cnt[u]) continue;
+        const r_vertex *x = &G->v[u];
+        uint64_t ins = 0, m = 0;
+        for (uint64_t k = cnt[u]; k < cnt[u + 1]; k++) {
+            const uint32_t *rec = recs + 4 * idx[k];
+            if (rec[0] == 0) { ins += rec[3]; m++; }
+        }
+        if ((uint64_t)x->d + m >= 0xFFFFFFFFull ||
+            (unsigned __int128)(x->T + ins) * K >= ((unsigned __int128)1 << 64)) {
+            free(cnt); free(idx);
+            return O_EOVERFLOW;
+        }
+    }
+    const uint32_t e = ++G->epoch;
+    for (uint32_t u = 0; u < G->V; u++) {
+        if (cnt[u + 1] == cnt[u]) continue;
+        r_vertex *x = &G->v[u];
+        uint32_t m = 0;
+        for (uint64_t k = cnt[u]; k < cnt[u + 1]; k++) m += recs[4 * idx[k]] == 0 ? 1u : 0u;
+        radix_own(x, x->d + m);
+        /* (1) inserts, batch order (R-7) */
+        for (uint64_t k = cnt[u]; k < cnt[u + 1]; k++) {
+            const uint32_t *rec = recs + 4 * idx[k];
+            if (rec[0] != 0) continue;
+            x->dst[x->d] = rec[2];
+            x->bias[x->d] = rec[3];
+            x->epoch[x->d] = e;
+            x->d++;
+            st[ST_INS]++;
+        }
+        /* (2) deletes, batch order: smallest (epoch, position) live instance (R-8) */
+        const uint32_t L = x->d;
+        uint8_t *taken = (uint8_t *)calloc(L ? L : 1, 1);
+        uint32_t N = 0;
+        for (uint64_t k = cnt[u]; k < cnt[u + 1]; k++) {
+            const uint32_t *rec = recs + 4 * idx[k];
+            if (rec[0] != 1) continue;
+            uint32_t best = O_NONE;
+            for (uint32_t p = 0; p < L; p++) {
+                if (taken[p] || x->dst[p] != rec[2]) continue;
+                if (best == O_NONE || x->epoch[p] < x->epoch[best]) best = p;
+            }
+            if (best == O_NONE) { st[ST_MISS]++; continue; }
+            taken[best] = 1;
+            N++;
+            st[ST_DEL]++;
+        }
+        /* (3) two-phase delete-and-swap of the adjacency (R-6): dst, bias and epoch move together */
+        if (N) {
+            uint32_t *P = (uint32_t *)malloc(sizeof(uint32_t) * N);
+            uint32_t np = 0;
+            for (uint32_t p = 0; p < L; p++) if (taken[p]) P[np++] = p;
+            two_phase_delete(x->dst, sizeof(uint32_t), L, P, N, NULL, NULL, NULL);
+            two_phase_delete(x->bias, sizeof(uint32_t), L, P, N, NULL, NULL, NULL);
+            two_phase_delete(x->epoch, sizeof(uint32_t), L, P, N, NULL, NULL, NULL);
+            x->d = L - N;
+            free(P);
+        }
+        free(taken);
+        /* (4) the nested structure from the new adjacency (cannot overflow: checked above) */
+        radix_build_vertex(x, G->b);
+        st[ST_TOUCH]++;
+    }
+    free(cnt);
+    free(idx);
+    st[ST_EPOCH] = e;
+    if (stats) memcpy(stats, st, sizeof(st));
+    return O_OK;
+}
+
+/* The adjacency of vertex u: d, then (dst, bias, epoch) of each arc into out[3 * d]
+ * (out may be NULL to query d). */
+uint32_t ora_radix_adj(const ora_radix *G, uint32_t u, uint32_t *out)
+{
+    const r_vertex *x = &G->v[u];
+    if (out)
+        for (uint32_t a = 0; a < x->d; a++) {
+            out[3 * a] = x->dst[a];
+            out[3 * a + 1] = x->bias[a];
+            out[3 * a + 2] = x->epoch ? x->epoch[a] : 0u;
+        }
+    return x->d;
 }
 
 /* three-stage sample (R-17): tag 0 group (bucket, coin vs thr over T), tag 6 subgroup

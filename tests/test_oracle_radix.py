@@ -138,3 +138,77 @@ def test_radix_walk_laws():
     rp = gc.walk(app=oracle.APP_PPR, length=oracle.NONE, seed=2, num_walkers=200_000, paths=False, counts=True)
     assert abs(rp["lengths"].mean() - 80) < 0.5
     assert int(rp["counts"].sum()) == int(rp["lengths"].astype(np.int64).sum()) + 200_000
+
+
+# ---------------------------------------------------------------- radix updates (reading R-19)
+def _csr_of(adj_lists):
+    """CSR (row offsets, dst, bias) of per-vertex [(dst, bias, epoch)] lists."""
+    deg = [len(a) for a in adj_lists]
+    ro = np.zeros(len(adj_lists) + 1, dtype=np.uint64)
+    ro[1:] = np.cumsum(deg)
+    dst = np.array([e[0] for a in adj_lists for e in a], dtype=np.uint32)
+    bias = np.array([e[1] for a in adj_lists for e in a], dtype=np.uint32)
+    return ro, dst, bias
+
+
+@pytest.mark.parametrize("b", [1, 2, 3, 4, 5])
+def test_radix_updates_follow_the_base2_adjacency_readings(b):
+    """R-19: the adjacency of an updated radix graph is, arc for arc and epoch for epoch, the
+    adjacency the base-2 oracle's independently written update path (R-6..R-9, pinned by the
+    paper's insertion / deletion examples) produces for the same batches; statistics agree;
+    and the nested structure equals a fresh build of that adjacency (whose tables are pinned
+    by Theorem 1 above)."""
+    rng = np.random.default_rng(100 + b)
+    V = 30
+    ro, dst, bias = synth.random_small_graph(rng, V, 40, 1 << 12)
+    base = oracle.OracleGraph(ro, dst, bias)
+    rad = oracle.RadixGraph(ro, dst, bias, b)
+    existing = [(u, int(dst[a])) for u in range(V) for a in range(int(ro[u]), int(ro[u + 1]))]
+    for r in range(6):
+        # hubs: some vertices get many records (duplicates, deletes of arcs inserted earlier
+        # in the same batch, missing deletes, delete-all-then-regrow on vertex 0)
+        recs = synth.random_batch(rng, V, 120, 1 << 12, existing=existing, p_delete=0.45)
+        if r == 3:
+            dels = [(synth.DELETE, 0, e[0], 0) for e in rad.adjacency(0)]
+            recs = np.concatenate([recs, np.array(dels, dtype=np.uint32).reshape(-1, 4),
+                                   np.array([(synth.INSERT, 0, 5, 7), (synth.INSERT, 0, 5, 9)], dtype=np.uint32)])
+        sb = base.apply_updates(recs)
+        sr = rad.apply_updates(recs)
+        for k in ("inserted", "deleted", "missing_deletes", "touched_vertices", "epoch"):
+            assert sr[k] == sb[k], (k, sr[k], sb[k])
+        pb = oracle.parse_dump(base.dump(), V)
+        adj = []
+        for u in range(V):
+            a = [tuple(int(x) for x in e) for e in rad.adjacency(u)]
+            assert a == [tuple(e) for e in pb[u]["adj"]], (r, u)
+            adj.append(a)
+        existing = [(u, e[0]) for u in range(V) for e in adj[u]]
+        fresh = oracle.RadixGraph(*_csr_of(adj), b)
+        assert rad.dump() == fresh.dump(), r
+        rv = oracle.parse_radix_dump(rad.dump(), V)
+        for u in range(V):
+            if not adj[u]:
+                continue
+            T = sum(e[1] for e in adj[u])
+            want = Counter()
+            for e in adj[u]:
+                want[e[0]] += Fraction(e[1], T)
+            assert radix_distribution(rv[u]) == want, (r, u)
+
+
+def test_radix_update_validation_and_overflow_leave_the_graph_untouched():
+    rng = np.random.default_rng(7)
+    ro, dst, bias = synth.random_small_graph(rng, 12, 10, 100)
+    rad = oracle.RadixGraph(ro, dst, bias, 3)
+    before = rad.dump()
+    bad = [np.array([[0, 3, 4, 0]], dtype=np.uint32),            # insert with bias 0
+           np.array([[2, 3, 4, 5]], dtype=np.uint32),            # unknown op
+           np.array([[0, 3, 12, 5]], dtype=np.uint32),           # dst >= V
+           np.array([[1, 2, 4, 0], [0, 12, 4, 5]], dtype=np.uint32)]   # src >= V after a valid record
+    for recs in bad:
+        assert rad.try_apply_updates(recs) == 1
+        assert rad.dump() == before
+    st = rad.apply_updates(np.zeros((0, 4), dtype=np.uint32))      # an empty batch is a successful call
+    assert st["epoch"] == 1 and rad.dump() == before
+    st = rad.apply_updates(np.array([[0, 1, 2, 3]], dtype=np.uint32))
+    assert st["epoch"] == 2 and rad.adjacency(1)[-1].tolist() == [2, 3, 2]
