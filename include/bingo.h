@@ -95,10 +95,13 @@ enum { BINGO_KIND_EMPTY = 0, BINGO_KIND_ONE = 1, BINGO_KIND_DENSE = 2, BINGO_KIN
 #define BINGO_BUILD_RELABEL 16u       /* relabel vertices hot-first internally at any V (default: V >= 2^23) */
 /* Arbitrary radix base B = 2^b, b in [1, 5] (reading R-17): group B^i holds
  * the arcs whose base-B digit i is nonzero, split into subgroups by digit value with an
- * inter-subgroup alias; walks take group -> subgroup -> member.  A STATIC structure (every
- * subgroup a member list, vertex-id layout): DeepWalk and PPR walks (step-major paths),
- * bingo_export in the radix dump format (R-18), bingo_visit_counts; bingo_apply_updates and
- * the other calls return EINVAL.  0 (default): the paper's base-2 Bingo with Eq.9 groups. */
+ * inter-subgroup alias; walks take group -> subgroup -> member.  Every subgroup a member list,
+ * vertex-id layout: DeepWalk and PPR walks (step-major paths), bingo_export in the radix dump
+ * format (R-18), bingo_visit_counts, and bingo_apply_updates (reading R-19: the adjacency as
+ * below, then each touched vertex's nested structure rebuilt from it; statistics without kind
+ * transitions; EOVERFLOW when (T + inserted bias) * ceil(32 / b) >= 2^64 or d + inserts >=
+ * 2^32 - 1); the other calls (node2vec, float biases, streaming queue, traces, partitions)
+ * return EINVAL.  0 (default): the paper's base-2 Bingo with Eq.9 groups. */
 #define BINGO_BUILD_RADIX_LOG2(b) ((uint32_t)(b) << 8)
 #define BINGO_BUILD_RADIX_MASK 0xF00u
 

@@ -7,10 +7,12 @@
 // drawn uniformly.  Fewer groups (K = 32 / b instead of 32: the complexity and memory term
 // of Table timecmp) against one more dependent stage per step.
 //
-// HBM layout (vertex-id order; static: the paper leaves nested dynamic structures to future
-// work, so bingo_apply_updates returns EINVAL on these graphs):
+// HBM layout (vertex-id order).  The paper leaves nested dynamic structures to future work
+// (P:927); here bingo_apply_updates rebuilds a touched vertex's structure from its updated
+// adjacency (reading R-19, apply_radix below), which lives in the arc pool:
 //   thdr[u]   {first bucket, n groups}
-//   hdr[u]    T, d (exports)
+//   hdr[u]    T, d, adjacency offset / capacity (exports, updates)
+//   arc, arc_epoch  the adjacency {dst, bias} and insert epochs (R-19), CSR order at build
 //   bkt/gcan  per vertex: its n group buckets, then every group's subgroup buckets
 //             (contiguous per group, ascending j).  A group bucket's view (px, py) is
 //             (number of subgroups, pool index of its first subgroup bucket); a subgroup
@@ -28,6 +30,7 @@
 #include "bingo_internal.cuh"
 #include "build_common.cuh"
 #include "scan.cuh"
+#include "sort.cuh"
 #include "walk_common.cuh"
 
 using namespace bingo;
@@ -44,12 +47,21 @@ __device__ __forceinline__ uint32_t rb_digit(uint32_t w, uint32_t i, uint32_t b)
 
 // per-warp histogram c[i * B + j] of the vertex's digits (shared atomics), then the
 // per-vertex sizes: buckets n + nsub, member units sum ceil(c / 4), T; overflow flag.
-__device__ __forceinline__ void rb_hist(const uint32_t *bias, uint64_t a0, uint32_t d, uint32_t b, uint32_t *c) {
+// A vertex's arcs as seen by the build: dst[a * st], bias[a * st] (st = 1: CSR arrays; st = 2:
+// the {dst, bias} uint2 arc pool of an updatable radix graph).
+struct RbArcs {
+    const uint32_t *dst, *bias;
+    uint32_t st;
+    __device__ __forceinline__ uint32_t w(uint32_t a) const { return bias[(uint64_t)a * st]; }
+    __device__ __forceinline__ uint32_t v(uint32_t a) const { return dst[(uint64_t)a * st]; }
+};
+
+__device__ __forceinline__ void rb_hist(const RbArcs &arcs, uint32_t d, uint32_t b, uint32_t *c) {
     const uint32_t lane = lane_id(), B = 1u << b, K = (32 + b - 1) / b;
     for (uint32_t x = lane; x < K * B; x += 32) c[x] = 0;
     __syncwarp();
     for (uint32_t a = lane; a < d; a += 32) {
-        const uint32_t w = bias[a0 + a];
+        const uint32_t w = arcs.w(a);
         for (uint32_t i = 0; i < K; i++) {
             const uint32_t j = rb_digit(w, i, b);
             if (j) atomicAdd(&c[i * B + j], 1u);
@@ -58,12 +70,47 @@ __device__ __forceinline__ void rb_hist(const uint32_t *bias, uint64_t a0, uint3
     __syncwarp();
 }
 
+// one warp: the vertex's bucket count (groups + subgroups) and member units; T (overflow flags)
+__device__ __forceinline__ void rb_sizes_vertex(const RbArcs &arcs, uint32_t d, uint32_t b, uint32_t *c,
+                                                uint64_t &nb_out, uint64_t &units_out, uint64_t &T_out,
+                                                int *__restrict__ flag) {
+    const uint32_t lane = lane_id(), B = 1u << b, K = (32 + b - 1) / b;
+    uint64_t T = 0;
+    for (uint32_t a = lane; a < d; a += 32) {
+        const uint32_t w = arcs.w(a);
+        if (w == 0) atomicOr(flag, 1);
+        T += w;
+    }
+    T = warp_sum(T);
+    rb_hist(arcs, d, b, c);
+    uint32_t ng = 0, nsub = 0;
+    uint64_t units = 0;
+    for (uint32_t i = lane; i < K; i += 32) {
+        uint32_t ns = 0;
+        for (uint32_t j = 1; j < B; j++) {
+            const uint32_t cc = c[i * B + j];
+            ns += cc ? 1u : 0u;
+            units += (cc + 3) / 4;
+        }
+        nsub += ns;
+        ng += ns ? 1u : 0u;
+    }
+    ng = warp_sum(ng);
+    nsub = warp_sum(nsub);
+    units = warp_sum(units);
+    if (lane == 0 && (unsigned __int128)T * ng >= ((unsigned __int128)1 << 64)) atomicOr(flag, 4);
+    nb_out = ng + nsub;
+    units_out = units;
+    T_out = T;
+    __syncwarp();
+}
+
 __global__ void __launch_bounds__(256) k_rb_sizes(uint32_t V, const uint64_t *__restrict__ ro,
                                                   const uint32_t *__restrict__ bias, uint32_t b,
                                                   uint64_t *__restrict__ nbkt, uint64_t *__restrict__ nmem,
                                                   int *__restrict__ flag) {
     __shared__ uint32_t cs[RB_WARPS][RB_CELLS];
-    const uint32_t wib = threadIdx.x >> 5, lane = lane_id(), B = 1u << b, K = (32 + b - 1) / b;
+    const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
     uint32_t *c = cs[wib];
     for (uint32_t u = blockIdx.x * RB_WARPS + wib; u < V; u += gridDim.x * RB_WARPS) {
         const uint64_t a0 = ro[u];
@@ -72,37 +119,170 @@ __global__ void __launch_bounds__(256) k_rb_sizes(uint32_t V, const uint64_t *__
             if (lane == 0) atomicOr(flag, 4);
             continue;
         }
-        const uint32_t d = (uint32_t)dd;
-        uint64_t T = 0;
-        for (uint32_t a = lane; a < d; a += 32) {
-            const uint32_t w = bias[a0 + a];
-            if (w == 0) atomicOr(flag, 1);
-            T += w;
-        }
-        T = warp_sum(T);
-        rb_hist(bias, a0, d, b, c);
-        uint32_t ng = 0, nsub = 0;
-        uint64_t units = 0;
-        for (uint32_t i = lane; i < K; i += 32) {
-            uint32_t ns = 0;
-            for (uint32_t j = 1; j < B; j++) {
-                const uint32_t cc = c[i * B + j];
-                ns += cc ? 1u : 0u;
-                units += (cc + 3) / 4;
-            }
-            nsub += ns;
-            ng += ns ? 1u : 0u;
-        }
-        ng = warp_sum(ng);
-        nsub = warp_sum(nsub);
-        units = warp_sum(units);
+        const RbArcs arcs{nullptr, bias + a0, 1u};
+        uint64_t nb, units, T;
+        rb_sizes_vertex(arcs, (uint32_t)dd, b, c, nb, units, T, flag);
         if (lane == 0) {
-            if ((unsigned __int128)T * ng >= ((unsigned __int128)1 << 64)) atomicOr(flag, 4);
-            nbkt[u] = ng + nsub;
+            nbkt[u] = nb;
             nmem[u] = units;
         }
-        __syncwarp();
     }
+}
+
+// One warp builds vertex u's nested structure from its arcs into buckets [bo_, bo_ + n + nsub)
+// and member units from munits (groups ascending i, subgroups ascending j, members in
+// adjacency order, both integer-Vose tables), and writes its headers (adj_off / adj_cap:
+// where its arcs live, updatable graphs).  c, cu: the warp's shared digit histogram / cursors.
+__device__ __forceinline__ void rb_fill_vertex(uint32_t u, const RbArcs &arcs, uint32_t d, uint32_t b, uint64_t bo_,
+                                               uint64_t munits, uint64_t adj_off, uint32_t adj_cap, uint32_t *c,
+                                               uint32_t *cu, VHdr *__restrict__ hdr, ThinHdr *__restrict__ thdr,
+                                               Bucket *__restrict__ bkt, GCan *__restrict__ gcan,
+                                               uint32_t *__restrict__ mdst) {
+    const uint32_t lane = lane_id(), B = 1u << b, K = (32 + b - 1) / b;
+    uint64_t T = 0;
+    for (uint32_t a = lane; a < d; a += 32) T += arcs.w(a);
+    T = warp_sum(T);
+    rb_hist(arcs, d, b, c);
+    // lane g < n owns nonempty group g (ascending i): its digit i, subgroup count ns and
+    // S = sum_j j c_ij; lane-serial prefix of ns for the subgroup bucket bases
+    uint32_t gi = 0, gns = 0;
+    uint64_t gS = 0;
+    uint32_t n = 0;
+    for (uint32_t i = 0; i < K; i++) {
+        uint32_t ns = 0;
+        uint64_t S = 0;
+        for (uint32_t j = 1; j < B; j++) {
+            const uint32_t cc = c[i * B + j];
+            ns += cc ? 1u : 0u;
+            S += (uint64_t)j * cc;
+        }
+        if (!ns) continue;
+        if (lane == n) { gi = i; gns = ns; gS = S; }
+        n++;
+    }
+    const uint64_t bo = bo_;
+    uint32_t sub0 = 0;   // exclusive prefix of ns over the groups before lane's group
+    {
+        uint32_t v = lane < n ? gns : 0u;
+        uint32_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        sub0 = incl - v;
+    }
+    // member offsets of every subgroup in (i ascending, j ascending) order, as entry
+    // cursors relative to the vertex's first member unit (the pool index is u64)
+    const uint64_t mbase = munits * 4;
+    if (lane == 0) {
+        uint32_t mo = 0;
+        for (uint32_t i = 0; i < K; i++)
+            for (uint32_t j = 1; j < B; j++) {
+                const uint32_t cc = c[i * B + j];
+                cu[i * B + j] = mo * 4;
+                mo += (cc + 3) / 4;
+            }
+    }
+    __syncwarp();
+    // group alias (R-4) over W_g = B^i S_g, one lane per group
+    const bool act = lane < n;
+    const uint64_t W = act ? (gS << (gi * b)) : 0ull;
+    uint64_t thr;
+    uint32_t alias;
+    vose_warp(act, n, W, T, thr, alias);
+    const uint32_t sub_base = (uint32_t)(bo + n + sub0);
+    {
+        Bucket Bk;
+        Bk.lim = alias_lim(thr, T);
+        Bk.px = gns;
+        Bk.py = sub_base;
+        Bk.kk = make_kk(gi, K_REGULAR);
+        Bk.alias = (uint8_t)alias;
+        Bk.pad = 0;
+        Bk.spare = 0;
+        Bk.ax = __shfl_sync(0xffffffffu, gns, alias);
+        Bk.ay = __shfl_sync(0xffffffffu, sub_base, alias);
+        Bk.a_kk = (uint8_t)__shfl_sync(0xffffffffu, (uint32_t)Bk.kk, alias);
+        if (act) {
+            store_bucket(&bkt[bo + lane], Bk);
+            store_gcan(&gcan[bo + lane], thr, gns, gi);
+        }
+    }
+    // subgroup aliases (R-4), group by group, one lane per subgroup
+    for (uint32_t g = 0; g < n; g++) {
+        const uint32_t i = __shfl_sync(0xffffffffu, gi, g);
+        const uint32_t ns = __shfl_sync(0xffffffffu, gns, g);
+        const uint64_t S = __shfl_sync(0xffffffffu, gS, g);
+        const uint32_t sb = __shfl_sync(0xffffffffu, sub_base, g);
+        // lane s < ns owns the s-th nonempty subgroup (ascending j)
+        uint32_t j_s = 0, c_s = 0, k = 0;
+        for (uint32_t j = 1; j < B; j++) {
+            const uint32_t cc = c[i * B + j];
+            if (!cc) continue;
+            if (lane == k) { j_s = j; c_s = cc; }
+            k++;
+        }
+        const bool sact = lane < ns;
+        uint64_t sthr;
+        uint32_t salias;
+        vose_warp(sact, ns, sact ? (uint64_t)j_s * c_s : 0ull, S, sthr, salias);
+        const uint32_t mo_s = sact ? (uint32_t)(mbase / 4) + cu[i * B + j_s] / 4 : 0u;
+        Bucket Bs;
+        Bs.lim = alias_lim(sthr, S);
+        Bs.px = c_s;
+        Bs.py = mo_s;
+        Bs.kk = make_kk(j_s, K_REGULAR);
+        Bs.alias = (uint8_t)salias;
+        Bs.pad = 0;
+        Bs.spare = 0;
+        Bs.ax = __shfl_sync(0xffffffffu, c_s, salias);
+        Bs.ay = __shfl_sync(0xffffffffu, mo_s, salias);
+        Bs.a_kk = (uint8_t)__shfl_sync(0xffffffffu, (uint32_t)Bs.kk, salias);
+        if (sact) {
+            store_bucket(&bkt[(uint64_t)sb + lane], Bs);
+            store_gcan(&gcan[(uint64_t)sb + lane], sthr, c_s, j_s);
+        }
+    }
+    __syncwarp();
+    // members: arcs in ascending index, 32 at a time; for each digit position the lanes
+    // with the same digit value are ranked by lane (= adjacency order) and appended
+    for (uint32_t base = 0; base < d; base += 32) {
+        const uint32_t a = base + lane;
+        const bool in = a < d;
+        const uint32_t w = in ? arcs.w(a) : 0u;
+        const uint32_t v = in ? arcs.v(a) : 0u;
+        for (uint32_t i = 0; i < K; i++) {
+            const uint32_t j = rb_digit(w, i, b);
+            const uint32_t key = in && j ? j : 0xFFFFFFFFu;
+            const uint32_t same = __match_any_sync(0xffffffffu, key);
+            uint32_t pos = 0;
+            if (key != 0xFFFFFFFFu) pos = cu[i * B + j] + __popc(same & lanemask_lt());
+            __syncwarp();
+            if (key != 0xFFFFFFFFu) {
+                mdst[mbase + pos] = v;
+                if ((__ffs(same) - 1) == (int)lane) cu[i * B + j] += __popc(same);
+            }
+            __syncwarp();
+        }
+    }
+    if (lane == 0) {
+        ThinHdr th;
+        th.bkt_off = (uint32_t)bo;
+        th.n = (uint8_t)n;
+        th.flags = 0;
+        th.pad1 = 0;
+        thdr[u] = th;
+        VHdr h;
+        memset(&h, 0, sizeof(h));
+        h.T = T;
+        h.d = d;
+        h.bkt_off = (uint32_t)bo;
+        h.n = (uint8_t)n;
+        h.adj_off = adj_off;
+        h.adj_cap = adj_cap;
+        hdr[u] = h;
+    }
+    __syncwarp();
 }
 
 __global__ void __launch_bounds__(256) k_rb_fill(uint32_t V, const uint64_t *__restrict__ ro,
@@ -113,155 +293,22 @@ __global__ void __launch_bounds__(256) k_rb_fill(uint32_t V, const uint64_t *__r
                                                  GCan *__restrict__ gcan, uint32_t *__restrict__ mdst) {
     __shared__ uint32_t cs[RB_WARPS][RB_CELLS];
     __shared__ uint32_t cur[RB_WARPS][RB_CELLS];   // member write cursor of subgroup (i, j), 4-entry units x 4
-    const uint32_t wib = threadIdx.x >> 5, lane = lane_id(), B = 1u << b, K = (32 + b - 1) / b;
-    uint32_t *c = cs[wib];
-    uint32_t *cu = cur[wib];
+    const uint32_t wib = threadIdx.x >> 5;
     for (uint32_t u = blockIdx.x * RB_WARPS + wib; u < V; u += gridDim.x * RB_WARPS) {
         const uint64_t a0 = ro[u];
         const uint32_t d = (uint32_t)(ro[u + 1] - a0);
-        uint64_t T = 0;
-        for (uint32_t a = lane; a < d; a += 32) T += bias[a0 + a];
-        T = warp_sum(T);
-        rb_hist(bias, a0, d, b, c);
-        // lane g < n owns nonempty group g (ascending i): its digit i, subgroup count ns and
-        // S = sum_j j c_ij; lane-serial prefix of ns for the subgroup bucket bases
-        uint32_t gi = 0, gns = 0;
-        uint64_t gS = 0;
-        uint32_t n = 0;
-        for (uint32_t i = 0; i < K; i++) {
-            uint32_t ns = 0;
-            uint64_t S = 0;
-            for (uint32_t j = 1; j < B; j++) {
-                const uint32_t cc = c[i * B + j];
-                ns += cc ? 1u : 0u;
-                S += (uint64_t)j * cc;
-            }
-            if (!ns) continue;
-            if (lane == n) { gi = i; gns = ns; gS = S; }
-            n++;
-        }
-        const uint64_t bo = boff[u];
-        uint32_t sub0 = 0;   // exclusive prefix of ns over the groups before lane's group
-        {
-            uint32_t v = lane < n ? gns : 0u;
-            uint32_t incl = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= (uint32_t)o) incl += y;
-            }
-            sub0 = incl - v;
-        }
-        // member offsets of every subgroup in (i ascending, j ascending) order, as entry
-        // cursors relative to the vertex's first member unit (the pool index is u64)
-        const uint64_t mbase = moff[u] * 4;
-        if (lane == 0) {
-            uint32_t mo = 0;
-            for (uint32_t i = 0; i < K; i++)
-                for (uint32_t j = 1; j < B; j++) {
-                    const uint32_t cc = c[i * B + j];
-                    cu[i * B + j] = mo * 4;
-                    mo += (cc + 3) / 4;
-                }
-        }
-        __syncwarp();
-        // group alias (R-4) over W_g = B^i S_g, one lane per group
-        const bool act = lane < n;
-        const uint64_t W = act ? (gS << (gi * b)) : 0ull;
-        uint64_t thr;
-        uint32_t alias;
-        vose_warp(act, n, W, T, thr, alias);
-        const uint32_t sub_base = (uint32_t)(bo + n + sub0);
-        {
-            Bucket Bk;
-            Bk.lim = alias_lim(thr, T);
-            Bk.px = gns;
-            Bk.py = sub_base;
-            Bk.kk = make_kk(gi, K_REGULAR);
-            Bk.alias = (uint8_t)alias;
-            Bk.pad = 0;
-            Bk.spare = 0;
-            Bk.ax = __shfl_sync(0xffffffffu, gns, alias);
-            Bk.ay = __shfl_sync(0xffffffffu, sub_base, alias);
-            Bk.a_kk = (uint8_t)__shfl_sync(0xffffffffu, (uint32_t)Bk.kk, alias);
-            if (act) {
-                store_bucket(&bkt[bo + lane], Bk);
-                store_gcan(&gcan[bo + lane], thr, gns, gi);
-            }
-        }
-        // subgroup aliases (R-4), group by group, one lane per subgroup
-        for (uint32_t g = 0; g < n; g++) {
-            const uint32_t i = __shfl_sync(0xffffffffu, gi, g);
-            const uint32_t ns = __shfl_sync(0xffffffffu, gns, g);
-            const uint64_t S = __shfl_sync(0xffffffffu, gS, g);
-            const uint32_t sb = __shfl_sync(0xffffffffu, sub_base, g);
-            // lane s < ns owns the s-th nonempty subgroup (ascending j)
-            uint32_t j_s = 0, c_s = 0, k = 0;
-            for (uint32_t j = 1; j < B; j++) {
-                const uint32_t cc = c[i * B + j];
-                if (!cc) continue;
-                if (lane == k) { j_s = j; c_s = cc; }
-                k++;
-            }
-            const bool sact = lane < ns;
-            uint64_t sthr;
-            uint32_t salias;
-            vose_warp(sact, ns, sact ? (uint64_t)j_s * c_s : 0ull, S, sthr, salias);
-            const uint32_t mo_s = sact ? (uint32_t)(mbase / 4) + cu[i * B + j_s] / 4 : 0u;
-            Bucket Bs;
-            Bs.lim = alias_lim(sthr, S);
-            Bs.px = c_s;
-            Bs.py = mo_s;
-            Bs.kk = make_kk(j_s, K_REGULAR);
-            Bs.alias = (uint8_t)salias;
-            Bs.pad = 0;
-            Bs.spare = 0;
-            Bs.ax = __shfl_sync(0xffffffffu, c_s, salias);
-            Bs.ay = __shfl_sync(0xffffffffu, mo_s, salias);
-            Bs.a_kk = (uint8_t)__shfl_sync(0xffffffffu, (uint32_t)Bs.kk, salias);
-            if (sact) {
-                store_bucket(&bkt[(uint64_t)sb + lane], Bs);
-                store_gcan(&gcan[(uint64_t)sb + lane], sthr, c_s, j_s);
-            }
-        }
-        __syncwarp();
-        // members: arcs in ascending index, 32 at a time; for each digit position the lanes
-        // with the same digit value are ranked by lane (= adjacency order) and appended
-        for (uint32_t base = 0; base < d; base += 32) {
-            const uint32_t a = base + lane;
-            const bool in = a < d;
-            const uint32_t w = in ? bias[a0 + a] : 0u;
-            const uint32_t v = in ? dst[a0 + a] : 0u;
-            for (uint32_t i = 0; i < K; i++) {
-                const uint32_t j = rb_digit(w, i, b);
-                const uint32_t key = in && j ? j : 0xFFFFFFFFu;
-                const uint32_t same = __match_any_sync(0xffffffffu, key);
-                uint32_t pos = 0;
-                if (key != 0xFFFFFFFFu) pos = cu[i * B + j] + __popc(same & lanemask_lt());
-                __syncwarp();
-                if (key != 0xFFFFFFFFu) {
-                    mdst[mbase + pos] = v;
-                    if ((__ffs(same) - 1) == (int)lane) cu[i * B + j] += __popc(same);
-                }
-                __syncwarp();
-            }
-        }
-        if (lane == 0) {
-            ThinHdr th;
-            th.bkt_off = (uint32_t)bo;
-            th.n = (uint8_t)n;
-            th.flags = 0;
-            th.pad1 = 0;
-            thdr[u] = th;
-            VHdr h;
-            memset(&h, 0, sizeof(h));
-            h.T = T;
-            h.d = d;
-            h.bkt_off = (uint32_t)bo;
-            h.n = (uint8_t)n;
-            hdr[u] = h;
-        }
-        __syncwarp();
+        const RbArcs arcs{dst + a0, bias + a0, 1u};
+        // the arcs live in the graph's arc pool at the same offsets (a copy of the CSR)
+        rb_fill_vertex(u, arcs, d, b, boff[u], moff[u], a0, d, cs[wib], cur[wib], hdr, thdr, bkt, gcan, mdst);
     }
+}
+
+// the CSR copied into the arc pool at the same offsets (updatable radix graphs keep their
+// adjacency: reading R-19)
+__global__ void k_rb_arcs(uint64_t A, const uint32_t *__restrict__ dst, const uint32_t *__restrict__ bias,
+                          uint2 *__restrict__ arc) {
+    for (uint64_t a = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; a < A; a += (uint64_t)gridDim.x * blockDim.x)
+        arc[a] = make_uint2(dst[a], bias[a]);
 }
 
 // three-stage sample (R-17): group (tag 0), subgroup (tag 6), member (tag 1)
@@ -410,7 +457,19 @@ bingo_status build_radix(bingo_graph *g, const bingo_build_desc *desc, uint32_t 
     g->bkt = (Bucket *)bingo_dev_alloc(g, sizeof(Bucket) * g->bkt_cap);
     g->gcan = (GCan *)bingo_dev_alloc(g, sizeof(GCan) * g->bkt_cap);
     g->mdst = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->mem_cap);
-    if (!g->bkt || !g->gcan || !g->mdst) return done(BINGO_E_NOMEM);
+    // the adjacency (dst, bias) and arc epochs, for updates (R-19); slack for relocations
+    const uint64_t A = desc->num_arcs;
+    g->arc_cap = rb_pool(A, g->arc_slack);
+    g->arc = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * g->arc_cap);
+    g->arc_epoch = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->arc_cap);
+    if (!g->bkt || !g->gcan || !g->mdst || !g->arc || !g->arc_epoch) return done(BINGO_E_NOMEM);
+    RCK(cudaMemsetAsync(g->arc_epoch, 0, sizeof(uint32_t) * std::max<uint64_t>(A, 1), s));
+    if (A) {
+        k_rb_arcs<<<(unsigned)std::min<uint64_t>((A + 255) / 256, 148ull * 32), 256, 0, s>>>(A, desc->dst, desc->bias,
+                                                                                             g->arc);
+        bingo_count_launch();
+        RCK(cudaGetLastError());
+    }
     if (V) {
         k_rb_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, b, off, off + (nV + 1), g->hdr,
                                          g->thdr, g->bkt, g->gcan, g->mdst);
@@ -419,7 +478,7 @@ bingo_status build_radix(bingo_graph *g, const bingo_build_desc *desc, uint32_t 
         RCK(cudaStreamSynchronize(s));
     }
 #undef RCK
-    unsigned long long hc[3] = {0, tot[0], tot[1]};
+    unsigned long long hc[3] = {A, tot[0], tot[1]};
     if (cudaMemcpy(g->counters, hc, sizeof(hc), cudaMemcpyHostToDevice) != cudaSuccess) {
         g->poisoned = 1;
         return done(BINGO_E_CUDA);
@@ -536,4 +595,418 @@ bingo_status export_radix(bingo_graph *g, uint8_t *buf, size_t cap, size_t *size
     }
     *size_out = pos;
     return BINGO_OK;
+}
+
+// ---------------------------------------------------------------- updates (reading R-19)
+// The paper leaves the nested dynamic structure unbuilt.  A batch: whole-batch
+// validation -> stable sort by source (batch order inside a vertex) -> per touched
+// vertex (one warp): the adjacency copied to fresh space in the arc pool with the inserts
+// appended (R-7), the deletes' picks (R-8) marked in a bitmap, the two-phase delete-and-swap
+// (R-6) -> the nested structure rebuilt from the new adjacency into fresh bucket / member
+// space (rb_fill_vertex, as the build) -> headers.  The headers change only in the last
+// kernel, after every pool is known to be large enough, so EINVAL / EOVERFLOW / NOMEM leave
+// the graph as it was.
+namespace bingo {
+
+struct RbuArgs {
+    const uint4 *recs;                 // the batch, device copy
+    const uint32_t *sval;              // record indices sorted by source (stable)
+    const uint32_t *seg;               // [nt + 1] segment starts in sval order
+    const uint32_t *tv;                // [nt] touched vertices
+    uint32_t nt, b, epoch;             // epoch of this batch (R-9)
+    VHdr *hdr;
+    ThinHdr *thdr;
+    uint2 *arc;
+    uint32_t *arc_epoch;
+    Bucket *bkt;
+    GCan *gcan;
+    uint32_t *mdst;
+    uint64_t *need_arc, *need_scr;     // plan: L = d + inserts, scratch words
+    const uint64_t *arc_pref, *scr_pref;
+    uint64_t arc_base, bkt_base, mem_base;   // pool bump pointers at this batch
+    uint32_t *scr;
+    uint32_t *newL;                    // post-batch degree
+    uint64_t *nbk, *nun;               // post-batch bucket / member-unit demand
+    const uint64_t *bk_pref, *un_pref;
+    unsigned long long *st;            // [3] inserted, deleted, missing
+    int *flag;                         // 1 invalid, 4 overflow
+};
+
+__global__ void k_rbu_validate(const uint4 *__restrict__ recs, uint64_t n, uint32_t V, int *flag,
+                               uint32_t *__restrict__ keys, uint32_t *__restrict__ vals) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint4 r = recs[i];
+        if (r.x > 1u || r.y >= V || r.z >= V || (r.x == 0u && r.w == 0u)) atomicOr(flag, 1);
+        keys[i] = r.y < V ? r.y : 0u;
+        vals[i] = (uint32_t)i;
+    }
+}
+
+__global__ void k_rbu_heads(const uint32_t *__restrict__ skeys, uint64_t n, uint64_t *__restrict__ head) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        head[i] = (i == 0 || skeys[i] != skeys[i - 1]) ? 1ull : 0ull;
+}
+
+__global__ void k_rbu_seg(const uint32_t *__restrict__ skeys, const uint64_t *__restrict__ head,
+                          const uint64_t *__restrict__ hpref, uint64_t n, uint32_t *__restrict__ seg,
+                          uint32_t *__restrict__ tv, unsigned long long *ntouch) {
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+        if (head[i]) {
+            seg[hpref[i]] = (uint32_t)i;
+            tv[hpref[i]] = skeys[i];
+        }
+        if (i == n - 1) {
+            const uint64_t nt = hpref[i] + head[i];
+            seg[nt] = (uint32_t)n;
+            *ntouch = nt;
+        }
+    }
+}
+
+#define RBU_WARP_LOOP(t, n) \
+    for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < (n); t += (gridDim.x * blockDim.x) >> 5)
+
+// per touched vertex: arc demand L = d + inserts, scratch (bitmap + holes + survivors), overflow
+__global__ void __launch_bounds__(256) k_rbu_plan(const RbuArgs a) {
+    const uint32_t lane = lane_id(), K = (32 + a.b - 1) / a.b;
+    RBU_WARP_LOOP(t, a.nt) {
+        const uint32_t beg = a.seg[t], end = a.seg[t + 1];
+        uint32_t m = 0, q = 0;
+        uint64_t ins = 0;
+        for (uint32_t p = beg + lane; p < end; p += 32) {
+            const uint4 r = a.recs[a.sval[p]];
+            if (r.x == 0u) { m++; ins += r.w; }
+            else q++;
+        }
+        m = warp_sum(m);
+        q = warp_sum(q);
+        ins = warp_sum(ins);
+        if (lane == 0) {
+            const VHdr h = a.hdr[a.tv[t]];
+            const uint64_t L = (uint64_t)h.d + m;
+            if (L >= 0xFFFFFFFFull || (unsigned __int128)(h.T + ins) * K >= ((unsigned __int128)1 << 64))
+                atomicOr(a.flag, 4);
+            a.need_arc[t] = L;
+            a.need_scr[t] = (L + 31) / 32 + 2ull * q;
+        }
+    }
+}
+
+__device__ __forceinline__ unsigned long long warp_min_u64(unsigned long long v) {
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(0xffffffffu, v, o);
+        v = y < v ? y : v;
+    }
+    return v;
+}
+
+// enumerate, ascending, the positions p in [lo, hi) whose bitmap bit equals `want`, into out[]
+__device__ __forceinline__ uint32_t rbu_enumerate(const uint32_t *bm, uint32_t lo, uint32_t hi, bool want,
+                                                  uint32_t *out) {
+    const uint32_t lane = lane_id();
+    uint32_t total = 0;
+    if (lo >= hi) return 0;
+    for (uint32_t w0 = lo / 32; w0 * 32 < hi; w0 += 32) {
+        const uint32_t w = w0 + lane;
+        uint32_t bits = 0;
+        if (w * 32 < hi) {
+            bits = want ? bm[w] : ~bm[w];
+            const uint32_t s = w * 32;
+            if (s < lo) bits &= ~0u << (lo - s);
+            if (hi - s < 32) bits &= (1u << (hi - s)) - 1u;
+        }
+        const uint32_t c = __popc(bits);
+        uint32_t incl = c;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= (uint32_t)o) incl += y;
+        }
+        uint32_t k = total + incl - c;
+        while (bits) {
+            const uint32_t bit = __ffs(bits) - 1;
+            bits &= bits - 1;
+            out[k++] = w * 32 + bit;
+        }
+        total += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    __syncwarp();
+    return total;
+}
+
+// per touched vertex: the new adjacency in fresh arc space (R-7, R-8, R-6)
+__global__ void __launch_bounds__(256) k_rbu_mutate(const RbuArgs a) {
+    const uint32_t lane = lane_id();
+    RBU_WARP_LOOP(t, a.nt) {
+        const uint32_t u = a.tv[t], beg = a.seg[t], end = a.seg[t + 1];
+        const VHdr h = a.hdr[u];
+        const uint32_t d = h.d;
+        const uint64_t off = a.arc_base + a.arc_pref[t], old = h.adj_off;
+        const uint32_t L = (uint32_t)a.need_arc[t];
+        for (uint32_t p = lane; p < d; p += 32) {
+            a.arc[off + p] = a.arc[old + p];
+            a.arc_epoch[off + p] = a.arc_epoch[old + p];
+        }
+        // (1) inserts appended in batch order (R-7)
+        uint32_t m = 0;
+        for (uint32_t p0 = beg; p0 < end; p0 += 32) {
+            const uint32_t p = p0 + lane;
+            uint4 r = make_uint4(1u, 0u, 0u, 0u);
+            if (p < end) r = a.recs[a.sval[p]];
+            const bool ins = p < end && r.x == 0u;
+            const uint32_t bal = __ballot_sync(0xffffffffu, ins);
+            if (ins) {
+                const uint32_t pos = d + m + __popc(bal & lanemask_lt());
+                a.arc[off + pos] = make_uint2(r.z, r.w);
+                a.arc_epoch[off + pos] = a.epoch;
+            }
+            m += __popc(bal);
+        }
+        uint32_t *bm = a.scr + a.scr_pref[t];
+        const uint32_t words = (L + 31) / 32;
+        for (uint32_t w = lane; w < words; w += 32) bm[w] = 0;
+        __syncwarp();
+        // (2) deletes in batch order: the live instance with the smallest (epoch, position) (R-8)
+        uint32_t N = 0, miss = 0;
+        for (uint32_t p = beg; p < end; p++) {
+            const uint4 r = a.recs[a.sval[p]];
+            if (r.x != 1u) continue;
+            unsigned long long best = ~0ull;
+            for (uint32_t x = lane; x < L; x += 32) {
+                if (a.arc[off + x].x != r.z || ((bm[x >> 5] >> (x & 31)) & 1u)) continue;
+                const unsigned long long key = ((unsigned long long)a.arc_epoch[off + x] << 32) | x;
+                best = key < best ? key : best;
+            }
+            best = warp_min_u64(best);
+            if (best == ~0ull) {
+                miss++;
+            } else {
+                const uint32_t x = (uint32_t)best;
+                if (lane == 0) bm[x >> 5] |= 1u << (x & 31);
+                N++;
+            }
+            __syncwarp();
+        }
+        // (3) two-phase delete-and-swap (R-6): survivor j of the tail window fills hole j
+        const uint32_t Lp = L - N;
+        if (N) {
+            uint32_t *hl = bm + words, *sv = hl + N;
+            const uint32_t nh = rbu_enumerate(bm, 0, Lp, true, hl);
+            rbu_enumerate(bm, Lp, L, false, sv);
+            for (uint32_t j = lane; j < nh; j += 32) {
+                a.arc[off + hl[j]] = a.arc[off + sv[j]];
+                a.arc_epoch[off + hl[j]] = a.arc_epoch[off + sv[j]];
+            }
+        }
+        if (lane == 0) {
+            a.newL[t] = Lp;
+            if (m) atomicAdd(&a.st[0], (unsigned long long)m);
+            if (N) atomicAdd(&a.st[1], (unsigned long long)N);
+            if (miss) atomicAdd(&a.st[2], (unsigned long long)miss);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rbu_sizes(const RbuArgs a) {
+    __shared__ uint32_t cs[RB_WARPS][RB_CELLS];
+    const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
+    RBU_WARP_LOOP(t, a.nt) {
+        const uint64_t off = a.arc_base + a.arc_pref[t];
+        const RbArcs arcs{&a.arc[off].x, &a.arc[off].y, 2u};
+        uint64_t nb, units, T;
+        rb_sizes_vertex(arcs, a.newL[t], a.b, cs[wib], nb, units, T, a.flag);
+        if (lane == 0) {
+            a.nbk[t] = nb;
+            a.nun[t] = units;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rbu_fill(const RbuArgs a) {
+    __shared__ uint32_t cs[RB_WARPS][RB_CELLS];
+    __shared__ uint32_t cur[RB_WARPS][RB_CELLS];
+    const uint32_t wib = threadIdx.x >> 5;
+    RBU_WARP_LOOP(t, a.nt) {
+        const uint64_t off = a.arc_base + a.arc_pref[t];
+        const RbArcs arcs{&a.arc[off].x, &a.arc[off].y, 2u};
+        rb_fill_vertex(a.tv[t], arcs, a.newL[t], a.b, a.bkt_base + a.bk_pref[t], a.mem_base + a.un_pref[t], off,
+                       (uint32_t)a.need_arc[t], cs[wib], cur[wib], a.hdr, a.thdr, a.bkt, a.gcan, a.mdst);
+    }
+}
+
+}  // namespace bingo
+
+// grow a device array (realloc + copy): the pools are offset-addressed, so nothing else changes
+template <typename T>
+static bool rb_grow(bingo_graph *g, T *&p, uint64_t old_n, uint64_t new_n, cudaStream_t s) {
+    T *q = (T *)bingo_dev_alloc(g, sizeof(T) * new_n);
+    if (!q) return false;
+    if (old_n && (cudaMemcpyAsync(q, p, sizeof(T) * old_n, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+                  cudaStreamSynchronize(s) != cudaSuccess)) {
+        bingo_dev_free(g, q);
+        return false;
+    }
+    bingo_dev_free(g, p);
+    p = q;
+    return true;
+}
+
+// bingo_apply_updates on a radix graph (called by apply_impl after the common checks)
+bingo_status apply_radix(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
+                         bingo_update_stats *stats, cudaStream_t s) {
+    const uint32_t V = g->V;
+    std::vector<void *> tmp;
+    auto take = [&](size_t bytes) {
+        void *p = bingo_dev_alloc(g, std::max<size_t>(bytes, 16));
+        if (p) tmp.push_back(p);
+        return p;
+    };
+    auto fin = [&](bingo_status r) {
+        for (void *p : tmp) bingo_dev_free(g, p);
+        return r;
+    };
+    auto fail = [&](const char *w) {
+        fprintf(stderr, "libbingo: CUDA error in %s: %s\n", w, cudaGetErrorString(cudaGetLastError()));
+        g->poisoned = 1;
+        return fin(BINGO_E_CUDA);
+    };
+#define RBU(call, w)                              \
+    do {                                          \
+        if ((call) != cudaSuccess) return fail(w); \
+    } while (0)
+    uint4 *recs = (uint4 *)take(16 * n);
+    uint32_t *k0 = (uint32_t *)take(4 * n), *v0 = (uint32_t *)take(4 * n), *k1 = (uint32_t *)take(4 * n),
+             *v1 = (uint32_t *)take(4 * n);
+    uint64_t *rtmp = (uint64_t *)take(8 * radix_tmp_words(n));
+    uint64_t *head = (uint64_t *)take(8 * (n + 1)), *hpref = (uint64_t *)take(8 * (n + 1));
+    uint64_t *stmp = (uint64_t *)take(8 * scan_tmp_words(n + 1));
+    uint32_t *seg = (uint32_t *)take(4 * (n + 1)), *tv = (uint32_t *)take(4 * n);
+    // small device block: [0..2] stats, [3] ntouch, [4..6] bump pointers copy; flag after
+    unsigned long long *dsm = (unsigned long long *)take(8 * 8 + 16);
+    int *dflag = reinterpret_cast<int *>(dsm + 8);
+    if (!recs || !k0 || !v0 || !k1 || !v1 || !rtmp || !head || !hpref || !stmp || !seg || !tv || !dsm)
+        return fin(BINGO_E_NOMEM);
+    RBU(cudaMemcpyAsync(recs, batch, 16 * n, (flags & BINGO_UPD_HOST_BATCH) ? cudaMemcpyHostToDevice
+                                                                           : cudaMemcpyDeviceToDevice, s), "radix batch copy");
+    RBU(cudaMemsetAsync(dsm, 0, 8 * 8 + 16, s), "radix memset");
+    const unsigned G1 = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k_rbu_validate<<<G1, 256, 0, s>>>(recs, n, V, dflag, k0, v0);
+    bingo_count_launch();
+    int kb = 1;
+    while (kb < 32 && ((uint64_t)(V ? V - 1 : 0) >> kb)) kb++;
+    bool in1 = false;
+    RBU(radix_sort_pairs(k0, v0, k1, v1, n, kb, rtmp, s, &in1), "radix sort");
+    const uint32_t *skeys = in1 ? k1 : k0, *sval = in1 ? v1 : v0;
+    k_rbu_heads<<<G1, 256, 0, s>>>(skeys, n, head);
+    bingo_count_launch();
+    RBU(exclusive_scan_u64(head, hpref, n, stmp, s), "radix scan");
+    k_rbu_seg<<<G1, 256, 0, s>>>(skeys, head, hpref, n, seg, tv, dsm + 3);
+    bingo_count_launch();
+    RBU(cudaMemcpyAsync(dsm + 4, g->counters, 3 * 8, cudaMemcpyDeviceToDevice, s), "radix bumps");
+    unsigned long long h1[8];
+    int hflag = 0;
+    RBU(cudaMemcpyAsync(h1, dsm, sizeof(h1), cudaMemcpyDeviceToHost, s), "radix sync 1");
+    RBU(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "radix sync 1");
+    RBU(cudaStreamSynchronize(s), "radix sync 1");
+    if (hflag & 1) return fin(BINGO_E_INVAL);
+    const uint32_t nt = (uint32_t)h1[3];
+    RbuArgs a;
+    memset(&a, 0, sizeof(a));
+    a.recs = recs;
+    a.sval = sval;
+    a.seg = seg;
+    a.tv = tv;
+    a.nt = nt;
+    a.b = g->radix_log2;
+    a.epoch = g->epoch + 1;
+    a.st = dsm;
+    a.flag = dflag;
+    uint64_t *need = (uint64_t *)take(8 * 2 * (nt + 1)), *pref = (uint64_t *)take(8 * 2 * (nt + 1));
+    uint64_t *stmp2 = (uint64_t *)take(8 * 2 * scan_tmp_words(nt + 1));   // two scans at once
+    a.newL = (uint32_t *)take(4 * (nt + 1));
+    if (!need || !pref || !stmp2 || !a.newL) return fin(BINGO_E_NOMEM);
+    a.need_arc = need;
+    a.need_scr = need + (nt + 1);
+    a.arc_pref = pref;
+    a.scr_pref = pref + (nt + 1);
+    a.hdr = g->hdr;
+    const unsigned GW = (unsigned)std::min<uint64_t>((nt + 7) / 8, 148ull * 16);
+    k_rbu_plan<<<GW, 256, 0, s>>>(a);
+    bingo_count_launch();
+    {
+        const uint64_t *in[2] = {a.need_arc, a.need_scr};
+        uint64_t *out[2] = {pref, pref + (nt + 1)};
+        RBU(exclusive_scan_u64_multi(in, out, 2, nt, stmp2, s), "radix plan scan");
+    }
+    uint64_t tot[2] = {0, 0};
+    RBU(cudaMemcpyAsync(&tot[0], pref + nt, 8, cudaMemcpyDeviceToHost, s), "radix sync 2");
+    RBU(cudaMemcpyAsync(&tot[1], pref + (nt + 1) + nt, 8, cudaMemcpyDeviceToHost, s), "radix sync 2");
+    RBU(cudaMemcpyAsync(&hflag, dflag, sizeof(int), cudaMemcpyDeviceToHost, s), "radix sync 2");
+    RBU(cudaStreamSynchronize(s), "radix sync 2");
+    if (hflag & 4) return fin(BINGO_E_OVERFLOW);
+    const uint64_t bump0 = h1[4], bump1 = h1[5], bump2 = h1[6];
+    if (bump0 + tot[0] > g->arc_cap) {   // the arc pool: room for the fresh copies of the touched vertices
+        const uint64_t cap = std::max<uint64_t>(bump0 + tot[0] + (bump0 + tot[0]) / 4, g->arc_cap + g->arc_cap / 4);
+        if (!rb_grow(g, g->arc, g->arc_cap, cap, s) || !rb_grow(g, g->arc_epoch, g->arc_cap, cap, s))
+            return fin(BINGO_E_NOMEM);
+        g->arc_cap = cap;
+    }
+    a.scr = (uint32_t *)take(4 * (tot[1] + 1));
+    a.nbk = (uint64_t *)take(8 * 2 * (nt + 1));
+    uint64_t *bpref = (uint64_t *)take(8 * 2 * (nt + 1));
+    if (!a.scr || !a.nbk || !bpref) return fin(BINGO_E_NOMEM);
+    a.nun = a.nbk + (nt + 1);
+    a.bk_pref = bpref;
+    a.un_pref = bpref + (nt + 1);
+    a.arc = g->arc;
+    a.arc_epoch = g->arc_epoch;
+    a.arc_base = bump0;
+    k_rbu_mutate<<<GW, 256, 0, s>>>(a);
+    bingo_count_launch();
+    k_rbu_sizes<<<GW, 256, 0, s>>>(a);
+    bingo_count_launch();
+    {
+        const uint64_t *in[2] = {a.nbk, a.nun};
+        uint64_t *out[2] = {bpref, bpref + (nt + 1)};
+        RBU(exclusive_scan_u64_multi(in, out, 2, nt, stmp2, s), "radix sizes scan");
+    }
+    uint64_t tb[2] = {0, 0};
+    RBU(cudaMemcpyAsync(&tb[0], bpref + nt, 8, cudaMemcpyDeviceToHost, s), "radix sync 3");
+    RBU(cudaMemcpyAsync(&tb[1], bpref + (nt + 1) + nt, 8, cudaMemcpyDeviceToHost, s), "radix sync 3");
+    RBU(cudaStreamSynchronize(s), "radix sync 3");
+    if (bump1 + tb[0] > g->bkt_cap) {
+        const uint64_t cap = std::max<uint64_t>(bump1 + tb[0] + (bump1 + tb[0]) / 4, g->bkt_cap + g->bkt_cap / 4);
+        if (cap >= 0x7FFFFFF0ull) return fin(BINGO_E_NOMEM);
+        if (!rb_grow(g, g->bkt, g->bkt_cap, cap, s) || !rb_grow(g, g->gcan, g->bkt_cap, cap, s)) return fin(BINGO_E_NOMEM);
+        g->bkt_cap = cap;
+    }
+    if (4 * (bump2 + tb[1]) > g->mem_cap) {
+        const uint64_t units = std::max<uint64_t>(bump2 + tb[1] + (bump2 + tb[1]) / 4, g->mem_cap / 4 + g->mem_cap / 16);
+        if (units >= 0xFFFFFFF0ull) return fin(BINGO_E_NOMEM);
+        if (!rb_grow(g, g->mdst, g->mem_cap, 4 * units, s)) return fin(BINGO_E_NOMEM);
+        g->mem_cap = 4 * units;
+    }
+    a.bkt = g->bkt;
+    a.gcan = g->gcan;
+    a.mdst = g->mdst;
+    a.thdr = g->thdr;
+    a.bkt_base = bump1;
+    a.mem_base = bump2;
+    k_rbu_fill<<<GW, 256, 0, s>>>(a);
+    bingo_count_launch();
+    RBU(cudaGetLastError(), "radix update kernels");
+    unsigned long long nb[3] = {bump0 + tot[0], bump1 + tb[0], bump2 + tb[1]};
+    RBU(cudaMemcpyAsync(g->counters, nb, sizeof(nb), cudaMemcpyHostToDevice, s), "radix bumps");
+    RBU(cudaMemcpyAsync(h1, dsm, 3 * 8, cudaMemcpyDeviceToHost, s), "radix stats");
+    RBU(cudaStreamSynchronize(s), "radix stats");
+#undef RBU
+    g->epoch++;
+    g->num_arcs = g->num_arcs + h1[0] - h1[1];
+    if (stats) {
+        stats->inserted = h1[0];
+        stats->deleted = h1[1];
+        stats->missing_deletes = h1[2];
+        stats->touched_vertices = nt;
+        stats->epoch = g->epoch;
+    }
+    return fin(BINGO_OK);
 }

@@ -2406,6 +2406,9 @@ static UpdHost *upd_host(bingo_graph *g) {
 static bingo_status finish_batch_host(bingo_graph *g, uint64_t n, uint64_t ntouch, uint32_t e,
                                       const unsigned long long *hs, bingo_update_stats *stats);
 
+bingo_status apply_radix(bingo_graph *g, const bingo_update *batch, uint64_t n, uint32_t flags,
+                         bingo_update_stats *stats, cudaStream_t s);
+
 static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const double *wf, uint64_t n,
                                uint32_t flags, bingo_update_stats *stats, void *stream);
 
@@ -2444,7 +2447,6 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
     // float-bias graphs take real biases (bingo_apply_updates_f64, R-16); integer graphs do not
     if (n && g->float_mode != (wf != nullptr)) return BINGO_E_INVAL;
     if (n >= 0xFFFFFFFFull) return BINGO_E_INVAL;
-    if (g->radix_log2) return BINGO_E_INVAL;   // static radix-base structure (radix.cu)
     bingo_sq_quiesce(g, (cudaStream_t)stream);
     const bool fm = g->float_mode;
     g_trace.on = getenv("BINGO_UPD_TRACE") != nullptr;
@@ -2456,6 +2458,7 @@ static bingo_status apply_impl(bingo_graph *g, const bingo_update *batch, const 
         if (stats) stats->epoch = g->epoch;
         return BINGO_OK;
     }
+    if (g->radix_log2) return apply_radix(g, batch, n, flags, stats, s);   // radix-base graphs (radix.cu, R-19)
     // ---- small batches: single-launch fast path (falls through when it reports SLOW)
     if (n <= FAST_N && !fm) {
         bingo_status fst;
