@@ -1,6 +1,7 @@
-"""f4 at a BASELINE config: the base-2^b static structure (b = 1..4) against the paper's base-2
-Bingo with adaptive groups -- memory (buckets, member entries, bytes), groups per vertex, and the
-DeepWalk / PPR walk time of one launch over every vertex."""
+"""f4 at a BASELINE config: the base-2^b structure (b = 1..4) against the paper's base-2 Bingo
+with adaptive groups -- memory (buckets, member entries, bytes), the DeepWalk / PPR walk time of
+one launch over every vertex, and (session 3, reading R-19) the time of the config's update
+batches (the radix graphs rebuild every touched vertex from its adjacency)."""
 import argparse
 import json
 import os
@@ -17,7 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--bases", default="0,1,2,3,4")
 a = ap.parse_args()
-w = synth.make_workload(a.config, rounds=1, hold_rounds=10, device="cuda", resident=True)
+w = synth.make_workload(a.config, rounds=6, hold_rounds=10, device="cuda", resident=True)
 rec = {"config": a.config, "V": w.V, "arcs": w.num_arcs, "structures": {}}
 for b in [int(x) for x in a.bases.split(",")]:
     g = pb.Graph(w.row_offsets, w.dst, w.bias, radix_log2=b) if b else pb.Graph(w.row_offsets, w.dst, w.bias)
@@ -26,9 +27,22 @@ for b in [int(x) for x in a.bases.split(",")]:
     r = {"device_gb": info["device_bytes"] / 1e9, "buckets": info["bucket_pool_used"],
          "member_entries": info["member_pool_used"], "arcs_stored": info["arc_pool_used"],
          "sampling_bytes": 32 * info["bucket_pool_used"] + 4 * info["member_pool_used"]
-                           + 8 * info["arc_pool_used"] + 8 * w.V,
-         "sampling_bytes_def": "32 B buckets + 4 B member dsts + 8 B {dst, bias} arcs (base 2 dense groups "
-                               "sample them) + 8 B thin header per vertex: what a walk reads"}
+                           + (0 if b else 8 * info["arc_pool_used"]) + 8 * w.V,
+         "sampling_bytes_def": "32 B buckets + 4 B member dsts + 8 B {dst, bias} arcs (base 2 only: its dense "
+                               "groups sample them) + 8 B thin header per vertex: what a walk reads"}
+    ums = []
+    for k, bt in enumerate(w.batches):
+        db = torch.from_numpy(bt.view("int32")).cuda()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.apply_updates(db)
+        e1.record()
+        torch.cuda.synchronize()
+        if k >= 2:
+            ums.append(e0.elapsed_time(e1))
+    ums.sort()
+    r["update_ms_median"] = ums[len(ums) // 2]
+    r["update_records"] = int(w.batches[0].shape[0])
     for app, name in ((pb.DEEPWALK, "deepwalk"), (pb.PPR, "ppr")):
         kw = dict(app=app, seed=5)
         if app == pb.PPR:
