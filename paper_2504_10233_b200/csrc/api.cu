@@ -34,7 +34,7 @@ extern "C" void bingo_destroy(bingo_graph *g) {
     if (!g) return;
     bingo_sq_release(g);
     void *bufs[] = {g->perm, g->inv, g->hdr, g->thdr, g->gcan, g->arc, g->arc_epoch, g->arc_dval, g->bkt, g->mdst, g->midx, g->nbt, g->nbo, g->nbtomb, g->hixo, g->hixt, g->hix, g->dec, g->dmem, g->counters, g->visit, g->dev_flag,
-                    g->scratch, g->wscratch, g->vscratch, g->bscratch, g->iscratch, g->fast_scr, g->vslot, g->gixo, g->gixt, g->gix, g->visit32};
+                    g->scratch, g->wscratch, g->vscratch, g->bscratch, g->iscratch, g->fast_scr, g->vslot, g->gixo, g->gixt, g->gix, g->visit32, g->rb_meta};
     for (void *p : bufs) bingo_dev_free(g, p);
     if (g->hscratch) cudaFreeHost(g->hscratch);
     if (g->uhost) cudaFreeHost(g->uhost);

@@ -221,7 +221,8 @@ struct bingo_graph {
     uint32_t *mdst = nullptr;          // [mem_cap] member dst (walker side)
     uint32_t *midx = nullptr;          // [mem_cap] member adjacency index (canonical)
     bool float_mode = false;
-    uint32_t radix_log2 = 0;           // 0: Bingo base 2 with adaptive groups; b >= 1: static base-2^b structure (radix.cu)
+    uint32_t radix_log2 = 0;           // 0: Bingo base 2 with adaptive groups; b >= 1: base-2^b structure (radix.cu)
+    uint64_t *rb_meta = nullptr;       // radix graphs: [V] first member unit, [V] (bucket cap << 32 | unit cap)
     bingo::DecRec *dec = nullptr;      // [V] decimal-group records (float mode)
     uint4 *dmem = nullptr;             // decimal members {idx, dst, D lo, D hi}
     uint64_t dmem_cap = 0;

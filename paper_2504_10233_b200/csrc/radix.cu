@@ -129,20 +129,12 @@ __global__ void __launch_bounds__(256) k_rb_sizes(uint32_t V, const uint64_t *__
     }
 }
 
-// One warp builds vertex u's nested structure from its arcs into buckets [bo_, bo_ + n + nsub)
-// and member units from munits (groups ascending i, subgroups ascending j, members in
-// adjacency order, both integer-Vose tables), and writes its headers (adj_off / adj_cap:
-// where its arcs live, updatable graphs).  c, cu: the warp's shared digit histogram / cursors.
-__device__ __forceinline__ void rb_fill_vertex(uint32_t u, const RbArcs &arcs, uint32_t d, uint32_t b, uint64_t bo_,
-                                               uint64_t munits, uint64_t adj_off, uint32_t adj_cap, uint32_t *c,
-                                               uint32_t *cu, VHdr *__restrict__ hdr, ThinHdr *__restrict__ thdr,
-                                               Bucket *__restrict__ bkt, GCan *__restrict__ gcan,
-                                               uint32_t *__restrict__ mdst) {
+// One warp: from the digit histogram c (cells i * B + j) and T, the vertex's group and subgroup
+// buckets at bo (both integer-Vose tables), and in cu the first member entry of every subgroup
+// relative to munits * 4 (groups ascending i, subgroups ascending j).  Returns n (groups).
+__device__ __forceinline__ uint32_t rb_tables(const uint32_t *c, uint32_t *cu, uint64_t T, uint32_t b, uint64_t bo,
+                                              uint64_t munits, Bucket *__restrict__ bkt, GCan *__restrict__ gcan) {
     const uint32_t lane = lane_id(), B = 1u << b, K = (32 + b - 1) / b;
-    uint64_t T = 0;
-    for (uint32_t a = lane; a < d; a += 32) T += arcs.w(a);
-    T = warp_sum(T);
-    rb_hist(arcs, d, b, c);
     // lane g < n owns nonempty group g (ascending i): its digit i, subgroup count ns and
     // S = sum_j j c_ij; lane-serial prefix of ns for the subgroup bucket bases
     uint32_t gi = 0, gns = 0;
@@ -160,7 +152,6 @@ __device__ __forceinline__ void rb_fill_vertex(uint32_t u, const RbArcs &arcs, u
         if (lane == n) { gi = i; gns = ns; gS = S; }
         n++;
     }
-    const uint64_t bo = bo_;
     uint32_t sub0 = 0;   // exclusive prefix of ns over the groups before lane's group
     {
         uint32_t v = lane < n ? gns : 0u;
@@ -244,11 +235,19 @@ __device__ __forceinline__ void rb_fill_vertex(uint32_t u, const RbArcs &arcs, u
         }
     }
     __syncwarp();
+    return n;
+}
+
+// One warp: the members of arcs [lo, hi) in ascending index appended to their subgroups at the
+// cursors cu (entries relative to mbase; advanced).
+__device__ __forceinline__ void rb_members(const RbArcs &arcs, uint32_t lo, uint32_t hi, uint32_t b, uint32_t *cu,
+                                           uint64_t mbase, uint32_t *__restrict__ mdst) {
+    const uint32_t lane = lane_id(), B = 1u << b, K = (32 + b - 1) / b;
     // members: arcs in ascending index, 32 at a time; for each digit position the lanes
     // with the same digit value are ranked by lane (= adjacency order) and appended
-    for (uint32_t base = 0; base < d; base += 32) {
+    for (uint32_t base = lo; base < hi; base += 32) {
         const uint32_t a = base + lane;
-        const bool in = a < d;
+        const bool in = a < hi;
         const uint32_t w = in ? arcs.w(a) : 0u;
         const uint32_t v = in ? arcs.v(a) : 0u;
         for (uint32_t i = 0; i < K; i++) {
@@ -265,23 +264,45 @@ __device__ __forceinline__ void rb_fill_vertex(uint32_t u, const RbArcs &arcs, u
             __syncwarp();
         }
     }
-    if (lane == 0) {
-        ThinHdr th;
-        th.bkt_off = (uint32_t)bo;
-        th.n = (uint8_t)n;
-        th.flags = 0;
-        th.pad1 = 0;
-        thdr[u] = th;
-        VHdr h;
-        memset(&h, 0, sizeof(h));
-        h.T = T;
-        h.d = d;
-        h.bkt_off = (uint32_t)bo;
-        h.n = (uint8_t)n;
-        h.adj_off = adj_off;
-        h.adj_cap = adj_cap;
-        hdr[u] = h;
-    }
+    __syncwarp();
+}
+
+__device__ __forceinline__ void rb_headers(uint32_t u, uint64_t T, uint32_t d, uint64_t bo, uint32_t n,
+                                           uint64_t adj_off, uint32_t adj_cap, VHdr *__restrict__ hdr,
+                                           ThinHdr *__restrict__ thdr) {
+    ThinHdr th;
+    th.bkt_off = (uint32_t)bo;
+    th.n = (uint8_t)n;
+    th.flags = 0;
+    th.pad1 = 0;
+    thdr[u] = th;
+    VHdr h;
+    memset(&h, 0, sizeof(h));
+    h.T = T;
+    h.d = d;
+    h.bkt_off = (uint32_t)bo;
+    h.n = (uint8_t)n;
+    h.adj_off = adj_off;
+    h.adj_cap = adj_cap;
+    hdr[u] = h;
+}
+
+// One warp builds vertex u's nested structure from its arcs into buckets [bo, bo + n + nsub)
+// and member units from munits, and writes its headers (adj_off / adj_cap: where its arcs
+// live, updatable graphs).  c, cu: the warp's shared digit histogram / cursors.
+__device__ __forceinline__ void rb_fill_vertex(uint32_t u, const RbArcs &arcs, uint32_t d, uint32_t b, uint64_t bo,
+                                               uint64_t munits, uint64_t adj_off, uint32_t adj_cap, uint32_t *c,
+                                               uint32_t *cu, VHdr *__restrict__ hdr, ThinHdr *__restrict__ thdr,
+                                               Bucket *__restrict__ bkt, GCan *__restrict__ gcan,
+                                               uint32_t *__restrict__ mdst) {
+    const uint32_t lane = lane_id();
+    uint64_t T = 0;
+    for (uint32_t a = lane; a < d; a += 32) T += arcs.w(a);
+    T = warp_sum(T);
+    rb_hist(arcs, d, b, c);
+    const uint32_t n = rb_tables(c, cu, T, b, bo, munits, bkt, gcan);
+    rb_members(arcs, 0, d, b, cu, munits * 4, mdst);
+    if (lane == 0) rb_headers(u, T, d, bo, n, adj_off, adj_cap, hdr, thdr);
     __syncwarp();
 }
 
@@ -290,7 +311,8 @@ __global__ void __launch_bounds__(256) k_rb_fill(uint32_t V, const uint64_t *__r
                                                  uint32_t b, const uint64_t *__restrict__ boff,
                                                  const uint64_t *__restrict__ moff, VHdr *__restrict__ hdr,
                                                  ThinHdr *__restrict__ thdr, Bucket *__restrict__ bkt,
-                                                 GCan *__restrict__ gcan, uint32_t *__restrict__ mdst) {
+                                                 GCan *__restrict__ gcan, uint32_t *__restrict__ mdst,
+                                                 uint64_t *__restrict__ meta) {
     __shared__ uint32_t cs[RB_WARPS][RB_CELLS];
     __shared__ uint32_t cur[RB_WARPS][RB_CELLS];   // member write cursor of subgroup (i, j), 4-entry units x 4
     const uint32_t wib = threadIdx.x >> 5;
@@ -300,6 +322,10 @@ __global__ void __launch_bounds__(256) k_rb_fill(uint32_t V, const uint64_t *__r
         const RbArcs arcs{dst + a0, bias + a0, 1u};
         // the arcs live in the graph's arc pool at the same offsets (a copy of the CSR)
         rb_fill_vertex(u, arcs, d, b, boff[u], moff[u], a0, d, cs[wib], cur[wib], hdr, thdr, bkt, gcan, mdst);
+        if (lane_id() == 0) {   // the vertex's structure space, for in-place rebuilds (R-19)
+            meta[u] = moff[u];
+            meta[V + u] = ((boff[u + 1] - boff[u]) << 32) | (moff[u + 1] - moff[u]);
+        }
     }
 }
 
@@ -462,7 +488,8 @@ bingo_status build_radix(bingo_graph *g, const bingo_build_desc *desc, uint32_t 
     g->arc_cap = rb_pool(A, g->arc_slack);
     g->arc = (uint2 *)bingo_dev_alloc(g, sizeof(uint2) * g->arc_cap);
     g->arc_epoch = (uint32_t *)bingo_dev_alloc(g, sizeof(uint32_t) * g->arc_cap);
-    if (!g->bkt || !g->gcan || !g->mdst || !g->arc || !g->arc_epoch) return done(BINGO_E_NOMEM);
+    g->rb_meta = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 2 * std::max<uint64_t>(nV, 1));
+    if (!g->bkt || !g->gcan || !g->mdst || !g->arc || !g->arc_epoch || !g->rb_meta) return done(BINGO_E_NOMEM);
     RCK(cudaMemsetAsync(g->arc_epoch, 0, sizeof(uint32_t) * std::max<uint64_t>(A, 1), s));
     if (A) {
         k_rb_arcs<<<(unsigned)std::min<uint64_t>((A + 255) / 256, 148ull * 32), 256, 0, s>>>(A, desc->dst, desc->bias,
@@ -472,7 +499,7 @@ bingo_status build_radix(bingo_graph *g, const bingo_build_desc *desc, uint32_t 
     }
     if (V) {
         k_rb_fill<<<blocks, 256, 0, s>>>(V, desc->row_offsets, desc->dst, desc->bias, b, off, off + (nV + 1), g->hdr,
-                                         g->thdr, g->bkt, g->gcan, g->mdst);
+                                         g->thdr, g->bkt, g->gcan, g->mdst, g->rb_meta);
         bingo_count_launch();
         RCK(cudaGetLastError());
         RCK(cudaStreamSynchronize(s));
@@ -621,15 +648,23 @@ struct RbuArgs {
     Bucket *bkt;
     GCan *gcan;
     uint32_t *mdst;
+    uint64_t *meta;                    // g->rb_meta: [V] first member unit, [V] (bucket cap << 32 | unit cap)
+    uint32_t V;
+    uint2 *wa;                         // working adjacency (scratch): the new arcs of every touched vertex
+    uint32_t *we;                      // ... and their epochs
     uint64_t *need_arc, *need_scr;     // plan: L = d + inserts, scratch words
     const uint64_t *arc_pref, *scr_pref;
     uint64_t arc_base, bkt_base, mem_base;   // pool bump pointers at this batch
     uint32_t *scr;
     uint32_t *newL;                    // post-batch degree
-    uint64_t *nbk, *nun;               // post-batch bucket / member-unit demand
-    const uint64_t *bk_pref, *un_pref;
+    // sizes: fresh pool space a vertex needs (0: its new adjacency / structure fits where it is;
+    // else the size with 25% slack, which becomes its capacity)
+    uint64_t *nfa, *nbk, *nun;
+    const uint64_t *fa_pref, *bk_pref, *un_pref;
     unsigned long long *st;            // [3] inserted, deleted, missing
     int *flag;                         // 1 invalid, 4 overflow
+    uint32_t *big;                     // touched indices t with newL > RBU_BIG (a block each)
+    unsigned long long *nbig;
 };
 
 __global__ void k_rbu_validate(const uint4 *__restrict__ recs, uint64_t n, uint32_t V, int *flag,
@@ -663,6 +698,17 @@ __global__ void k_rbu_seg(const uint32_t *__restrict__ skeys, const uint64_t *__
     }
 }
 
+// a vertex with more deletes than this finds its R-8 picks among candidates (one pass over
+// the adjacency with a hash of the deleted dsts) instead of one adjacency scan per delete
+static constexpr uint32_t RBU_SCAN_Q = 4;
+// vertices with more arcs after the batch are sized and rebuilt by a whole block
+static constexpr uint32_t RBU_BIG = 4096;
+__host__ __device__ __forceinline__ uint64_t rbu_hash_size(uint32_t q) {
+    uint64_t h = 16;
+    while (h < 2ull * q) h <<= 1;
+    return h;
+}
+
 #define RBU_WARP_LOOP(t, n) \
     for (uint32_t t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < (n); t += (gridDim.x * blockDim.x) >> 5)
 
@@ -687,7 +733,9 @@ __global__ void __launch_bounds__(256) k_rbu_plan(const RbuArgs a) {
             if (L >= 0xFFFFFFFFull || (unsigned __int128)(h.T + ins) * K >= ((unsigned __int128)1 << 64))
                 atomicOr(a.flag, 4);
             a.need_arc[t] = L;
-            a.need_scr[t] = (L + 31) / 32 + 2ull * q;
+            // bitmap, holes + survivors, and (q > RBU_SCAN_Q) a hash of the deleted dsts plus
+            // the candidate positions (arcs whose dst is deleted)
+            a.need_scr[t] = (L + 31) / 32 + 2ull * q + (q > RBU_SCAN_Q ? rbu_hash_size(q) + L : 0ull);
         }
     }
 }
@@ -740,11 +788,13 @@ __global__ void __launch_bounds__(256) k_rbu_mutate(const RbuArgs a) {
         const uint32_t u = a.tv[t], beg = a.seg[t], end = a.seg[t + 1];
         const VHdr h = a.hdr[u];
         const uint32_t d = h.d;
-        const uint64_t off = a.arc_base + a.arc_pref[t], old = h.adj_off;
+        const uint64_t off = a.arc_pref[t], old = h.adj_off;   // working copy in scratch
         const uint32_t L = (uint32_t)a.need_arc[t];
+        uint2 *const wa = a.wa;
+        uint32_t *const we = a.we;
         for (uint32_t p = lane; p < d; p += 32) {
-            a.arc[off + p] = a.arc[old + p];
-            a.arc_epoch[off + p] = a.arc_epoch[old + p];
+            wa[off + p] = a.arc[old + p];
+            we[off + p] = a.arc_epoch[old + p];
         }
         // (1) inserts appended in batch order (R-7)
         uint32_t m = 0;
@@ -756,8 +806,8 @@ __global__ void __launch_bounds__(256) k_rbu_mutate(const RbuArgs a) {
             const uint32_t bal = __ballot_sync(0xffffffffu, ins);
             if (ins) {
                 const uint32_t pos = d + m + __popc(bal & lanemask_lt());
-                a.arc[off + pos] = make_uint2(r.z, r.w);
-                a.arc_epoch[off + pos] = a.epoch;
+                wa[off + pos] = make_uint2(r.z, r.w);
+                we[off + pos] = a.epoch;
             }
             m += __popc(bal);
         }
@@ -765,15 +815,61 @@ __global__ void __launch_bounds__(256) k_rbu_mutate(const RbuArgs a) {
         const uint32_t words = (L + 31) / 32;
         for (uint32_t w = lane; w < words; w += 32) bm[w] = 0;
         __syncwarp();
-        // (2) deletes in batch order: the live instance with the smallest (epoch, position) (R-8)
+        // (2) deletes in batch order: the live instance with the smallest (epoch, position) (R-8).
+        // Few deletes: scan the adjacency per delete.  Many: one pass collects the candidate
+        // positions (arcs whose dst some delete names, via a hash of the deleted dsts) and each
+        // delete scans only those -- the same picks, O(L + q x candidates) instead of O(q L).
+        const uint32_t q = (uint32_t)(end - beg) - m;
+        const uint32_t *cand = nullptr;
+        uint32_t nc = L;
+        if (q > RBU_SCAN_Q) {
+            const uint32_t H = (uint32_t)rbu_hash_size(q);
+            uint32_t *ht = bm + words + 2 * q, *cw = ht + H;
+            for (uint32_t j = lane; j < H; j += 32) ht[j] = 0xFFFFFFFFu;
+            __syncwarp();
+            for (uint32_t p0 = beg; p0 < end; p0 += 32) {
+                const uint32_t p = p0 + lane;
+                if (p < end) {
+                    const uint4 r = a.recs[a.sval[p]];
+                    if (r.x == 1u) {
+                        uint32_t sl = (r.z * 0x9E3779B1u) & (H - 1);
+                        for (;;) {
+                            const uint32_t o = atomicCAS(&ht[sl], 0xFFFFFFFFu, r.z);
+                            if (o == 0xFFFFFFFFu || o == r.z) break;
+                            sl = (sl + 1) & (H - 1);
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+            nc = 0;
+            for (uint32_t x0 = 0; x0 < L; x0 += 32) {
+                const uint32_t x = x0 + lane;
+                bool hit = false;
+                if (x < L) {
+                    const uint32_t v = wa[off + x].x;
+                    for (uint32_t sl = (v * 0x9E3779B1u) & (H - 1);; sl = (sl + 1) & (H - 1)) {
+                        const uint32_t k = ht[sl];
+                        if (k == v) { hit = true; break; }
+                        if (k == 0xFFFFFFFFu) break;
+                    }
+                }
+                const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+                if (hit) cw[nc + __popc(bal & lanemask_lt())] = x;
+                nc += __popc(bal);
+            }
+            __syncwarp();
+            cand = cw;
+        }
         uint32_t N = 0, miss = 0;
         for (uint32_t p = beg; p < end; p++) {
             const uint4 r = a.recs[a.sval[p]];
             if (r.x != 1u) continue;
             unsigned long long best = ~0ull;
-            for (uint32_t x = lane; x < L; x += 32) {
-                if (a.arc[off + x].x != r.z || ((bm[x >> 5] >> (x & 31)) & 1u)) continue;
-                const unsigned long long key = ((unsigned long long)a.arc_epoch[off + x] << 32) | x;
+            for (uint32_t c = lane; c < nc; c += 32) {
+                const uint32_t x = cand ? cand[c] : c;
+                if (wa[off + x].x != r.z || ((bm[x >> 5] >> (x & 31)) & 1u)) continue;
+                const unsigned long long key = ((unsigned long long)we[off + x] << 32) | x;
                 best = key < best ? key : best;
             }
             best = warp_min_u64(best);
@@ -793,12 +889,13 @@ __global__ void __launch_bounds__(256) k_rbu_mutate(const RbuArgs a) {
             const uint32_t nh = rbu_enumerate(bm, 0, Lp, true, hl);
             rbu_enumerate(bm, Lp, L, false, sv);
             for (uint32_t j = lane; j < nh; j += 32) {
-                a.arc[off + hl[j]] = a.arc[off + sv[j]];
-                a.arc_epoch[off + hl[j]] = a.arc_epoch[off + sv[j]];
+                wa[off + hl[j]] = wa[off + sv[j]];
+                we[off + hl[j]] = we[off + sv[j]];
             }
         }
         if (lane == 0) {
             a.newL[t] = Lp;
+            if (Lp > RBU_BIG) a.big[atomicAdd(a.nbig, 1ull)] = t;
             if (m) atomicAdd(&a.st[0], (unsigned long long)m);
             if (N) atomicAdd(&a.st[1], (unsigned long long)N);
             if (miss) atomicAdd(&a.st[2], (unsigned long long)miss);
@@ -806,19 +903,56 @@ __global__ void __launch_bounds__(256) k_rbu_mutate(const RbuArgs a) {
     }
 }
 
+// fresh pool space for vertex t: none where the new adjacency / structure fits the vertex's
+// current space (rebuilt in place), else the size plus 25% slack
+__device__ __forceinline__ void rbu_demand(const RbuArgs &a, uint32_t t, uint64_t nb, uint64_t units) {
+    const uint32_t u = a.tv[t], L = a.newL[t];
+    const VHdr h = a.hdr[u];
+    const uint64_t caps = a.meta[a.V + u];
+    a.nfa[t] = L <= h.adj_cap ? 0ull : (uint64_t)L + L / 4;
+    a.nbk[t] = nb <= (caps >> 32) ? 0ull : nb + nb / 4;
+    a.nun[t] = units <= (caps & 0xFFFFFFFFull) ? 0ull : units + units / 4;
+}
+
 __global__ void __launch_bounds__(256) k_rbu_sizes(const RbuArgs a) {
     __shared__ uint32_t cs[RB_WARPS][RB_CELLS];
     const uint32_t wib = threadIdx.x >> 5, lane = lane_id();
     RBU_WARP_LOOP(t, a.nt) {
-        const uint64_t off = a.arc_base + a.arc_pref[t];
-        const RbArcs arcs{&a.arc[off].x, &a.arc[off].y, 2u};
+        if (a.newL[t] > RBU_BIG) continue;   // k_rbu_sizes_big
+        const uint64_t off = a.arc_pref[t];
+        const RbArcs arcs{&a.wa[off].x, &a.wa[off].y, 2u};
         uint64_t nb, units, T;
         rb_sizes_vertex(arcs, a.newL[t], a.b, cs[wib], nb, units, T, a.flag);
-        if (lane == 0) {
-            a.nbk[t] = nb;
-            a.nun[t] = units;
-        }
+        if (lane == 0) rbu_demand(a, t, nb, units);
     }
+}
+
+// where vertex t's new adjacency and structure go (in place, or the fresh space of its demand);
+// copies the working adjacency there (threads `id` of `nthr`) and records the structure space
+struct RbuPlace {
+    uint64_t aoff, bo, mu;
+    uint32_t acap;
+};
+__device__ __forceinline__ RbuPlace rbu_place(const RbuArgs &a, uint32_t t, uint32_t id, uint32_t nthr) {
+    const uint32_t u = a.tv[t], L = a.newL[t];
+    const VHdr h = a.hdr[u];
+    const uint64_t caps = a.meta[a.V + u];
+    RbuPlace p;
+    const bool fa = a.nfa[t] != 0, fb = a.nbk[t] != 0, fu = a.nun[t] != 0;
+    p.aoff = fa ? a.arc_base + a.fa_pref[t] : h.adj_off;
+    p.acap = fa ? (uint32_t)a.nfa[t] : h.adj_cap;
+    p.bo = fb ? a.bkt_base + a.bk_pref[t] : h.bkt_off;
+    p.mu = fu ? a.mem_base + a.un_pref[t] : a.meta[u];
+    const uint64_t w = a.arc_pref[t];
+    for (uint32_t x = id; x < L; x += nthr) {
+        a.arc[p.aoff + x] = a.wa[w + x];
+        a.arc_epoch[p.aoff + x] = a.we[w + x];
+    }
+    if (id == 0) {
+        a.meta[u] = p.mu;
+        a.meta[a.V + u] = ((fb ? a.nbk[t] : caps >> 32) << 32) | (fu ? a.nun[t] : caps & 0xFFFFFFFFull);
+    }
+    return p;
 }
 
 __global__ void __launch_bounds__(256) k_rbu_fill(const RbuArgs a) {
@@ -826,10 +960,114 @@ __global__ void __launch_bounds__(256) k_rbu_fill(const RbuArgs a) {
     __shared__ uint32_t cur[RB_WARPS][RB_CELLS];
     const uint32_t wib = threadIdx.x >> 5;
     RBU_WARP_LOOP(t, a.nt) {
-        const uint64_t off = a.arc_base + a.arc_pref[t];
-        const RbArcs arcs{&a.arc[off].x, &a.arc[off].y, 2u};
-        rb_fill_vertex(a.tv[t], arcs, a.newL[t], a.b, a.bkt_base + a.bk_pref[t], a.mem_base + a.un_pref[t], off,
-                       (uint32_t)a.need_arc[t], cs[wib], cur[wib], a.hdr, a.thdr, a.bkt, a.gcan, a.mdst);
+        if (a.newL[t] > RBU_BIG) continue;   // k_rbu_fill_big
+        const RbuPlace pl = rbu_place(a, t, lane_id(), 32);
+        const uint64_t off = a.arc_pref[t];
+        const RbArcs arcs{&a.wa[off].x, &a.wa[off].y, 2u};
+        rb_fill_vertex(a.tv[t], arcs, a.newL[t], a.b, pl.bo, pl.mu, pl.aoff, pl.acap, cs[wib], cur[wib], a.hdr,
+                       a.thdr, a.bkt, a.gcan, a.mdst);
+    }
+}
+
+// Large vertices, one 256-thread block each: per-warp digit counts over 8 contiguous chunks
+// of the adjacency (their sum is the histogram), the tables by warp 0, then every warp appends
+// its chunk's members at cursors offset by the earlier chunks' counts -- the same ascending
+// member order as one warp over the whole adjacency.
+__device__ __forceinline__ void rbu_block_counts(const RbArcs &arcs, uint32_t L, uint32_t b,
+                                                 uint32_t (*cnt)[RB_CELLS], uint32_t *c, unsigned long long *sT) {
+    const uint32_t B = 1u << b, K = (32 + b - 1) / b, wib = threadIdx.x >> 5, lane = lane_id();
+    for (uint32_t x = threadIdx.x; x < RB_WARPS * RB_CELLS; x += blockDim.x) cnt[x / RB_CELLS][x % RB_CELLS] = 0;
+    if (threadIdx.x == 0) *sT = 0;
+    __syncthreads();
+    const uint32_t chunk = (L + RB_WARPS - 1) / RB_WARPS, lo = min(L, wib * chunk), hi = min(L, lo + chunk);
+    uint64_t T = 0;
+    for (uint32_t a = lo + lane; a < hi; a += 32) {
+        const uint32_t w = arcs.w(a);
+        T += w;
+        for (uint32_t i = 0; i < K; i++) {
+            const uint32_t j = rb_digit(w, i, b);
+            if (j) atomicAdd(&cnt[wib][i * B + j], 1u);
+        }
+    }
+    T = warp_sum(T);
+    if (lane == 0) atomicAdd(sT, (unsigned long long)T);
+    __syncthreads();
+    for (uint32_t x = threadIdx.x; x < RB_CELLS; x += blockDim.x) {
+        uint32_t sum = 0;
+        for (uint32_t w = 0; w < RB_WARPS; w++) sum += cnt[w][x];
+        c[x] = sum;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) k_rbu_sizes_big(const RbuArgs a) {
+    __shared__ uint32_t cnt[RB_WARPS][RB_CELLS];
+    __shared__ uint32_t c[RB_CELLS];
+    __shared__ unsigned long long sT;
+    const uint32_t B = 1u << a.b, K = (32 + a.b - 1) / a.b, lane = lane_id();
+    for (uint32_t bi = blockIdx.x; bi < *a.nbig; bi += gridDim.x) {
+        const uint32_t t = a.big[bi];
+        const uint64_t off = a.arc_pref[t];
+        const RbArcs arcs{&a.wa[off].x, &a.wa[off].y, 2u};
+        rbu_block_counts(arcs, a.newL[t], a.b, cnt, c, &sT);
+        if (threadIdx.x < 32) {
+            uint32_t ng = 0, nsub = 0;
+            uint64_t units = 0;
+            for (uint32_t i = lane; i < K; i += 32) {
+                uint32_t ns = 0;
+                for (uint32_t j = 1; j < B; j++) {
+                    const uint32_t cc = c[i * B + j];
+                    ns += cc ? 1u : 0u;
+                    units += (cc + 3) / 4;
+                }
+                nsub += ns;
+                ng += ns ? 1u : 0u;
+            }
+            ng = warp_sum(ng);
+            nsub = warp_sum(nsub);
+            units = warp_sum(units);
+            if (lane == 0) {
+                if ((unsigned __int128)sT * ng >= ((unsigned __int128)1 << 64)) atomicOr(a.flag, 4);
+                rbu_demand(a, t, ng + nsub, units);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_rbu_fill_big(const RbuArgs a) {
+    __shared__ uint32_t cnt[RB_WARPS][RB_CELLS];
+    __shared__ uint32_t c[RB_CELLS], cu[RB_CELLS];
+    __shared__ unsigned long long sT;
+    __shared__ uint32_t sn;
+    const uint32_t wib = threadIdx.x >> 5;
+    for (uint32_t bi = blockIdx.x; bi < *a.nbig; bi += gridDim.x) {
+        const uint32_t t = a.big[bi], L = a.newL[t];
+        const RbuPlace pl = rbu_place(a, t, threadIdx.x, blockDim.x);
+        const uint64_t off = a.arc_pref[t];
+        const RbArcs arcs{&a.wa[off].x, &a.wa[off].y, 2u};
+        rbu_block_counts(arcs, L, a.b, cnt, c, &sT);
+        const uint64_t bo = pl.bo, munits = pl.mu;
+        if (wib == 0) {
+            const uint32_t n = rb_tables(c, cu, sT, a.b, bo, munits, a.bkt, a.gcan);
+            if (lane_id() == 0) sn = n;
+        }
+        __syncthreads();
+        for (uint32_t x = threadIdx.x; x < RB_CELLS; x += blockDim.x) {   // chunk w's cursor per cell
+            uint32_t run = cu[x];
+            for (uint32_t w = 0; w < RB_WARPS; w++) {
+                const uint32_t k = cnt[w][x];
+                cnt[w][x] = run;
+                run += k;
+            }
+        }
+        __syncthreads();
+        const uint32_t chunk = (L + RB_WARPS - 1) / RB_WARPS, lo = min(L, wib * chunk), hi = min(L, lo + chunk);
+        rb_members(arcs, lo, hi, a.b, cnt[wib], munits * 4, a.mdst);
+        __syncthreads();
+        if (threadIdx.x == 0)
+            rb_headers(a.tv[t], sT, L, bo, sn, pl.aoff, pl.acap, a.hdr, a.thdr);
+        __syncthreads();
     }
 }
 
@@ -880,7 +1118,7 @@ bingo_status apply_radix(bingo_graph *g, const bingo_update *batch, uint64_t n, 
     uint64_t *head = (uint64_t *)take(8 * (n + 1)), *hpref = (uint64_t *)take(8 * (n + 1));
     uint64_t *stmp = (uint64_t *)take(8 * scan_tmp_words(n + 1));
     uint32_t *seg = (uint32_t *)take(4 * (n + 1)), *tv = (uint32_t *)take(4 * n);
-    // small device block: [0..2] stats, [3] ntouch, [4..6] bump pointers copy; flag after
+    // small device block: [0..2] stats, [3] ntouch, [4..6] bump pointers copy, [7] big vertices; flag after
     unsigned long long *dsm = (unsigned long long *)take(8 * 8 + 16);
     int *dflag = reinterpret_cast<int *>(dsm + 8);
     if (!recs || !k0 || !v0 || !k1 || !v1 || !rtmp || !head || !hpref || !stmp || !seg || !tv || !dsm)
@@ -944,47 +1182,62 @@ bingo_status apply_radix(bingo_graph *g, const bingo_update *batch, uint64_t n, 
     RBU(cudaStreamSynchronize(s), "radix sync 2");
     if (hflag & 4) return fin(BINGO_E_OVERFLOW);
     const uint64_t bump0 = h1[4], bump1 = h1[5], bump2 = h1[6];
-    if (bump0 + tot[0] > g->arc_cap) {   // the arc pool: room for the fresh copies of the touched vertices
-        const uint64_t cap = std::max<uint64_t>(bump0 + tot[0] + (bump0 + tot[0]) / 4, g->arc_cap + g->arc_cap / 4);
-        if (!rb_grow(g, g->arc, g->arc_cap, cap, s) || !rb_grow(g, g->arc_epoch, g->arc_cap, cap, s))
-            return fin(BINGO_E_NOMEM);
-        g->arc_cap = cap;
-    }
+    // the working adjacency (scratch): every touched vertex's new arcs, then sizes and the
+    // fresh pool space of the vertices that no longer fit where they are
+    a.wa = (uint2 *)take(8 * (tot[0] + 1));
+    a.we = (uint32_t *)take(4 * (tot[0] + 1));
     a.scr = (uint32_t *)take(4 * (tot[1] + 1));
-    a.nbk = (uint64_t *)take(8 * 2 * (nt + 1));
-    uint64_t *bpref = (uint64_t *)take(8 * 2 * (nt + 1));
-    if (!a.scr || !a.nbk || !bpref) return fin(BINGO_E_NOMEM);
-    a.nun = a.nbk + (nt + 1);
-    a.bk_pref = bpref;
-    a.un_pref = bpref + (nt + 1);
+    a.big = (uint32_t *)take(4 * (nt + 1));
+    a.nbig = dsm + 7;
+    a.nfa = (uint64_t *)take(8 * 3 * (nt + 1));
+    uint64_t *bpref = (uint64_t *)take(8 * 3 * (nt + 1));
+    uint64_t *stmp3 = (uint64_t *)take(8 * 3 * scan_tmp_words(nt + 1));
+    if (!a.wa || !a.we || !a.scr || !a.big || !a.nfa || !bpref || !stmp3) return fin(BINGO_E_NOMEM);
+    a.nbk = a.nfa + (nt + 1);
+    a.nun = a.nfa + 2 * (nt + 1);
+    a.fa_pref = bpref;
+    a.bk_pref = bpref + (nt + 1);
+    a.un_pref = bpref + 2 * (nt + 1);
     a.arc = g->arc;
     a.arc_epoch = g->arc_epoch;
-    a.arc_base = bump0;
+    a.meta = g->rb_meta;
+    a.V = V;
     k_rbu_mutate<<<GW, 256, 0, s>>>(a);
     bingo_count_launch();
     k_rbu_sizes<<<GW, 256, 0, s>>>(a);
     bingo_count_launch();
+    k_rbu_sizes_big<<<148 * 2, 256, 0, s>>>(a);
+    bingo_count_launch();
     {
-        const uint64_t *in[2] = {a.nbk, a.nun};
-        uint64_t *out[2] = {bpref, bpref + (nt + 1)};
-        RBU(exclusive_scan_u64_multi(in, out, 2, nt, stmp2, s), "radix sizes scan");
+        const uint64_t *in[3] = {a.nfa, a.nbk, a.nun};
+        uint64_t *out[3] = {bpref, bpref + (nt + 1), bpref + 2 * (nt + 1)};
+        RBU(exclusive_scan_u64_multi(in, out, 3, nt, stmp3, s), "radix sizes scan");
     }
-    uint64_t tb[2] = {0, 0};
-    RBU(cudaMemcpyAsync(&tb[0], bpref + nt, 8, cudaMemcpyDeviceToHost, s), "radix sync 3");
-    RBU(cudaMemcpyAsync(&tb[1], bpref + (nt + 1) + nt, 8, cudaMemcpyDeviceToHost, s), "radix sync 3");
+    uint64_t tb[3] = {0, 0, 0};
+    for (int k = 0; k < 3; k++)
+        RBU(cudaMemcpyAsync(&tb[k], bpref + k * (nt + 1) + nt, 8, cudaMemcpyDeviceToHost, s), "radix sync 3");
     RBU(cudaStreamSynchronize(s), "radix sync 3");
-    if (bump1 + tb[0] > g->bkt_cap) {
-        const uint64_t cap = std::max<uint64_t>(bump1 + tb[0] + (bump1 + tb[0]) / 4, g->bkt_cap + g->bkt_cap / 4);
+    if (bump0 + tb[0] > g->arc_cap) {   // relocated adjacencies
+        const uint64_t cap = std::max<uint64_t>(bump0 + tb[0] + (bump0 + tb[0]) / 4, g->arc_cap + g->arc_cap / 4);
+        if (!rb_grow(g, g->arc, g->arc_cap, cap, s) || !rb_grow(g, g->arc_epoch, g->arc_cap, cap, s))
+            return fin(BINGO_E_NOMEM);
+        g->arc_cap = cap;
+    }
+    if (bump1 + tb[1] > g->bkt_cap) {
+        const uint64_t cap = std::max<uint64_t>(bump1 + tb[1] + (bump1 + tb[1]) / 4, g->bkt_cap + g->bkt_cap / 4);
         if (cap >= 0x7FFFFFF0ull) return fin(BINGO_E_NOMEM);
         if (!rb_grow(g, g->bkt, g->bkt_cap, cap, s) || !rb_grow(g, g->gcan, g->bkt_cap, cap, s)) return fin(BINGO_E_NOMEM);
         g->bkt_cap = cap;
     }
-    if (4 * (bump2 + tb[1]) > g->mem_cap) {
-        const uint64_t units = std::max<uint64_t>(bump2 + tb[1] + (bump2 + tb[1]) / 4, g->mem_cap / 4 + g->mem_cap / 16);
+    if (4 * (bump2 + tb[2]) > g->mem_cap) {
+        const uint64_t units = std::max<uint64_t>(bump2 + tb[2] + (bump2 + tb[2]) / 4, g->mem_cap / 4 + g->mem_cap / 16);
         if (units >= 0xFFFFFFF0ull) return fin(BINGO_E_NOMEM);
         if (!rb_grow(g, g->mdst, g->mem_cap, 4 * units, s)) return fin(BINGO_E_NOMEM);
         g->mem_cap = 4 * units;
     }
+    a.arc = g->arc;
+    a.arc_epoch = g->arc_epoch;
+    a.arc_base = bump0;
     a.bkt = g->bkt;
     a.gcan = g->gcan;
     a.mdst = g->mdst;
@@ -993,8 +1246,10 @@ bingo_status apply_radix(bingo_graph *g, const bingo_update *batch, uint64_t n, 
     a.mem_base = bump2;
     k_rbu_fill<<<GW, 256, 0, s>>>(a);
     bingo_count_launch();
+    k_rbu_fill_big<<<148 * 2, 256, 0, s>>>(a);
+    bingo_count_launch();
     RBU(cudaGetLastError(), "radix update kernels");
-    unsigned long long nb[3] = {bump0 + tot[0], bump1 + tb[0], bump2 + tb[1]};
+    unsigned long long nb[3] = {bump0 + tb[0], bump1 + tb[1], bump2 + tb[2]};
     RBU(cudaMemcpyAsync(g->counters, nb, sizeof(nb), cudaMemcpyHostToDevice, s), "radix bumps");
     RBU(cudaMemcpyAsync(h1, dsm, 3 * 8, cudaMemcpyDeviceToHost, s), "radix stats");
     RBU(cudaStreamSynchronize(s), "radix stats");

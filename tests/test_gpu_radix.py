@@ -79,9 +79,11 @@ def test_radix_updates_match_the_oracle(b):
     rng = np.random.default_rng(40 + b)
     V = 300
     ro, dst, bias = synth.random_small_graph(rng, V, 60, int(rng.choice([255, 1 << 20, (1 << 32) - 1])))
-    # one hub with a few thousand arcs
+    # hubs: vertex 7 crosses the block-per-vertex threshold (4096 arcs) downwards when it loses
+    # 2500 arcs, vertex 11 stays above it
     deg = np.diff(ro.astype(np.int64))
-    deg[7] = 3000
+    deg[7] = 6000
+    deg[11] = 9000
     ro = np.zeros(V + 1, dtype=np.uint64)
     ro[1:] = np.cumsum(deg)
     dst = rng.integers(0, V, size=int(ro[-1])).astype(np.uint32)
