@@ -1862,9 +1862,11 @@ static inline unsigned warp_grid(uint64_t units, unsigned cap) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, cap));
 }
 
-// grid cap of the warp-per-vertex kernels, in blocks (BINGO_BSP_WG blocks per SM, A/B)
+// grid cap of the warp-per-vertex kernels, in blocks (BINGO_BSP_WG blocks per SM, A/B): 64
+// (about one touched vertex per warp at 100K-record batches; the block scheduler balances the
+// waves) over 16: c2 0.778 -> 0.748 ms, c4 1.276 -> 1.226 ms (profiles/r02_update_wg_ab.txt)
 static unsigned bsp_wg() {
-    unsigned per_sm = 16;
+    unsigned per_sm = 64;
     if (const char *ev = getenv("BINGO_BSP_WG")) per_sm = std::max(1u, (unsigned)strtoul(ev, nullptr, 10));
     return 148 * per_sm;
 }
