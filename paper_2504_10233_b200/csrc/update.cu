@@ -1862,6 +1862,12 @@ static inline unsigned warp_grid(uint64_t units, unsigned cap) {
     return (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(b, cap));
 }
 
+// blocks per SM (148 SMs) from an environment override (A/B), else the default
+static unsigned bsp_env_grid(const char *name, unsigned per_sm) {
+    if (const char *ev = getenv(name)) per_sm = std::max(1u, (unsigned)strtoul(ev, nullptr, 10));
+    return 148 * per_sm;
+}
+
 // grid cap of the warp-per-vertex kernels, in blocks (BINGO_BSP_WG blocks per SM, A/B): 64
 // (about one touched vertex per warp at 100K-record batches; the block scheduler balances the
 // waves) over 16: c2 0.778 -> 0.748 ms, c4 1.276 -> 1.226 ms (profiles/r02_update_wg_ab.txt)
@@ -2265,7 +2271,11 @@ static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uin
     caps.gix_on = g->gixo && !g->gix_full;
     caps.sel = g->isc_sel;
     caps.grp = g->isc_grp;
-    const unsigned WG = bsp_wg(), IG = 148 * 8, HG = 148 * 4;   // IG: item kernels, one wave of contiguous per-warp ranges
+    // IG: item kernels, one wave of contiguous per-warp ranges; HG: the hub chain's per-hub kernels
+    // (IG 16 per SM on graphs >= 2^28 arcs, whose hub scans fill more items: c4 1.222 -> 1.177 ms;
+    // c2 is 2% faster at 8; profiles/r02_update_wg_ab.txt)
+    const unsigned WG = bsp_wg(), HG = bsp_env_grid("BINGO_BSP_HG", 4),
+                   IG = bsp_env_grid("BINGO_BSP_IG", g->num_arcs >= (1ull << 28) ? 16u : 8u);
     const unsigned wg = warp_grid(ntmax, WG), hg = warp_grid(ntmax, HG);
     UCK(cudaMemsetAsync(a.nhubs, 0, 32, s));
     UCK(cudaMemsetAsync(a.vhix, 0, 4 * (size_t)ntmax, s));
