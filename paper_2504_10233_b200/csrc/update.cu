@@ -1770,11 +1770,12 @@ static bool hix_disabled() {
 }
 
 // Both update indices (hub delete index, group index) are kept only for vertices of more than
-// BINGO_INDEX_MIN arcs (default 4096; the build raises it 4x at a time until the tables fit
+// BINGO_INDEX_MIN arcs (default 2048; the build raises it 4x at a time until the tables fit
 // their memory budget).  Below that the O(d) scans of the bulk-synchronous route are cheaper
-// than keeping a table exact across batches (measured).
+// than keeping a table exact across batches (measured; c4 after session 3's
+// grid changes: 4096 1.19 ms, 2048 1.14 ms, 1024 1.14 ms per 100K-record batch).
 static uint32_t index_min() {
-    uint32_t m = 4 * CH;
+    uint32_t m = 2 * CH;
     if (const char *ev = getenv("BINGO_INDEX_MIN")) m = std::max<uint32_t>(CH, (uint32_t)strtoul(ev, nullptr, 10));
     return m;
 }
