@@ -154,7 +154,9 @@ __device__ __forceinline__ T warp_sum(T v) {
 #ifndef BINGO_VISIT_PAD
 #define BINGO_VISIT_PAD 4096u
 #endif
-#define BINGO_VISIT_STRIDE 32u
+#ifndef BINGO_VISIT_STRIDE
+#define BINGO_VISIT_STRIDE 32u   // u64 words per padded counter slot (256 B)
+#endif
 #ifdef BINGO_VISIT_REC
 // A/B layout: every counter sits beside a copy of its vertex's thin header in one 16 B record
 // {header, count}, so a PPR step's header read and its visit increment share a sector (and a
