@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-ceiling", action="store_true", help="skip the trace/replay gather ceiling")
     ap.add_argument("--no-meter", action="store_true", help="skip the in-run CUPTI DRAM counters")
     ap.add_argument("--trace-records", type=float, default=1.2e9, help="max traced steps for the ceiling")
+    ap.add_argument("--sort-records", type=float, default=6e8, help="traced steps replayed in window-sorted order")
     ap.add_argument("--cpu-walkers", type=int, default=1 << 15, help="oracle walker sample per step")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for N > 1 (gloo: test the multi-rank path without NVLink)")
@@ -461,8 +462,44 @@ def gather_ceiling(args, g, app, pkw, prof, count, first, dev, stream):
     best = min(sweep, key=sweep.get)
     rep_ms = sweep[best]
     sectors = cnt["hdr"] + cnt["bkt"] + cnt["mem"] + cnt["arc"]
-    del trace, rec_off
+    walker_gbs = 32 * sectors / (rep_ms / 1e3) / 1e9
+    # second order: the same records sorted by vertex inside windows of one walker per vertex
+    # (what one step of a level-synchronous walk over every walker could issue; DESIGN 6.1,
+    # tools/sorted_replay.py), replayed in chunks of 8 records per thread
+    del rec_off
     torch.cuda.empty_cache()
+    srt = None
+    try:
+        V = g.V
+        n2 = int(min(n, args.sort_records, torch.cuda.mem_get_info()[0] * 0.8 / 40))
+        key = trace[:n2, 0].to(torch.int64) + (torch.arange(n2, device=dev, dtype=torch.int64) // V << 40)
+        idx = torch.sort(key).indices
+        del key
+        st = trace[:n2].index_select(0, idx)
+        del idx
+        coff = torch.unique_consecutive(torch.arange(0, n2 + 8, 8, dtype=torch.int64, device=dev).clamp_(max=n2))
+        ssweep, scnt = {}, None
+        for ahead in (1, 8):
+            for bps in (2, 4):
+                ms = []
+                for _ in range(2):
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    scnt = g.walk_replay(st, coff, ahead=ahead, blocks_per_sm=bps)
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    ms.append(e0.elapsed_time(e1))
+                ssweep[f"ahead{ahead}_bps{bps}"] = min(ms)
+        sbest = min(ssweep, key=ssweep.get)
+        ssect = scnt["hdr"] + scnt["bkt"] + scnt["mem"] + scnt["arc"]
+        srt = {"records": n2, "window_records": V, "replay_ms": ssweep[sbest], "replay_best": sbest,
+               "replay_sweep_ms": ssweep, "ceiling_gbs": 32 * ssect / (ssweep[sbest] / 1e3) / 1e9}
+        del st, coff
+    except torch.cuda.OutOfMemoryError:
+        srt = {"skipped": "not enough free memory for the sort"}
+    del trace
+    torch.cuda.empty_cache()
+    ceil_gbs = max(walker_gbs, srt.get("ceiling_gbs", 0.0))
     return {"method": "bingo_walk_trace + bingo_walk_replay: the traced walks' own loads (header, bucket, "
                       "member / first two dense attempts) re-issued walker by walker with the walk's widths, L2 "
                       "policies and 64 B fetch hints, but 1-8 steps (up to 32 loads) in flight per thread and no "
@@ -472,8 +509,11 @@ def gather_ceiling(args, g, app, pkw, prof, count, first, dev, stream):
                       "ceiling is, if anything, low by that share.  PPR visit-counter RMWs are not replayed "
                       "(they cost the walk time, so the fraction understates)",
             "walkers_traced": Wt, "steps_traced": n, "replay_ms": rep_ms, "replay_best": best,
-            "replay_sweep_ms": sweep, "replay_loads": cnt,
-            "ceiling_gbs": 32 * sectors / (rep_ms / 1e3) / 1e9}
+            "replay_sweep_ms": sweep, "replay_loads": cnt, "walker_order_gbs": walker_gbs,
+            "window_sorted": srt,
+            "ceiling_def": "the better of the two orders: walker by walker (the walk's own order), and sorted "
+                           "by vertex inside windows of one walker per vertex (a level-synchronous order)",
+            "ceiling_gbs": ceil_gbs}
 
 
 def run_e2e(args, g, rb, host_batches, app, V, count, first, L, dev, dist, rank, ws):
