@@ -47,7 +47,11 @@ def main():
     cfg = synth.CONFIGS[a.config]
     app = cfg["app"]
     t0 = time.time()
-    w = synth.make_workload(a.config, rounds=a.rounds, hold_rounds=10, device="cuda", resident=True)
+    if a.config == "c5":   # too big for the in-HBM generator's temporaries: generated on the GPU, kept on the host
+        w = synth.make_workload(a.config, rounds=a.rounds, device="cuda")
+        w.host_csr = lambda: (w.row_offsets, w.dst, w.bias)
+    else:
+        w = synth.make_workload(a.config, rounds=a.rounds, hold_rounds=10, device="cuda", resident=True)
     torch.cuda.empty_cache()
     t_gen = time.time() - t0
     rec = {"config": a.config, "V": int(w.V), "arcs": int(w.num_arcs), "app": app, "gen_s": round(t_gen, 1)}
