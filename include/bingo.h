@@ -355,6 +355,34 @@ bingo_status bingo_walk_trace(bingo_graph *g, const bingo_walk_desc *desc, const
 bingo_status bingo_walk_replay(bingo_graph *g, const void *trace, const uint64_t *rec_off, uint32_t num_walkers,
                                uint32_t flags, uint64_t *counts_host, void *stream);
 
+/* ---------------------------------------------------------------------------
+ * bingo_export_vertices / bingo_import_vertices -- per-vertex state exchange between
+ * replicas (replicated regime): sharded update application.  Updates are
+ * independent per source vertex, so with P replicas rank r applies (with
+ * bingo_apply_updates) only the records whose source it owns, exports the post-batch state
+ * of those touched vertices, and imports every other rank's exports; every replica then
+ * holds the canonical state of the single-graph run (R-11: adjacency with epochs, groups,
+ * kinds, integer-Vose tables, member order, T).
+ *
+ * export: ids = DEVICE array of n vertex ids (the caller's ids, < V, each at most once).
+ *   offsets (DEVICE, n + 1 u64) receives the record offsets in u32 words, offsets[n] the
+ *   total, also written to *words_out (HOST).  buf == NULL: sizes only.  Else buf (DEVICE,
+ *   cap_words u32) receives the records: u, d, n, T (2 words), d x (dst, bias, epoch), then
+ *   per nonempty group k, kind, c, thr (2 words), alias and its payload (list groups: the c
+ *   member adjacency indices in list order; one-element groups: the arc index), all ids
+ *   internal (replicas share the build's relabelling).  Errors: EINVAL (an id >= V, a
+ *   float-bias, radix-base or neighbour-index graph), EOVERFLOW (cap_words too small).
+ * import: buf / offsets (DEVICE) as an export of a replica of the same graph produced them
+ *   (n records).  Each record's vertex is rewritten in place where its adjacency, buckets or
+ *   a same-k member list fit, else in fresh pool space; its hub / group indices are dropped
+ *   (rebuilt lazily).  The epoch does not change.  Errors: EINVAL as above, NOMEM if a pool
+ *   cannot grow (nothing written).  Both synchronise `stream`.
+ * ------------------------------------------------------------------------- */
+bingo_status bingo_export_vertices(bingo_graph *g, const uint32_t *ids, uint32_t n, uint32_t *buf,
+                                   uint64_t cap_words, uint64_t *offsets, uint64_t *words_out, void *stream);
+bingo_status bingo_import_vertices(bingo_graph *g, const uint32_t *buf, const uint64_t *offsets, uint32_t n,
+                                   void *stream);
+
 const char *bingo_status_str(bingo_status s);
 
 #ifdef __cplusplus

@@ -34,7 +34,8 @@ NO_CAP = 0xFFFFFFFF
 ABI_SYMBOLS = ("bingo_build", "bingo_destroy", "bingo_apply_updates", "bingo_apply_updates_f64", "bingo_walk",
                "bingo_visit_counts",
                "bingo_export", "bingo_digests", "bingo_get_info", "bingo_status_str", "bingo_walk_profile",
-               "bingo_walk_trace", "bingo_walk_replay", "bingo_stream_update", "bingo_walk_partition")
+               "bingo_walk_trace", "bingo_walk_replay", "bingo_stream_update", "bingo_walk_partition",
+               "bingo_export_vertices", "bingo_import_vertices")
 
 
 class BingoError(RuntimeError):
@@ -120,6 +121,10 @@ def _lib():
         L.bingo_walk_trace.restype = ctypes.c_int
         L.bingo_walk_replay.argtypes = [P, P, P, u32, u32, P, P]
         L.bingo_walk_replay.restype = ctypes.c_int
+        L.bingo_export_vertices.argtypes = [P, P, u32, P, u64, P, ctypes.POINTER(u64), P]
+        L.bingo_export_vertices.restype = ctypes.c_int
+        L.bingo_import_vertices.argtypes = [P, P, P, u32, P]
+        L.bingo_import_vertices.restype = ctypes.c_int
         L.bingo_status_str.argtypes = [ctypes.c_int]
         L.bingo_status_str.restype = ctypes.c_char_p
         _LIB = L
@@ -458,6 +463,38 @@ class Graph:
             _check(_lib().bingo_walk_replay(self._h, trace.data_ptr(), rec_off.data_ptr(), rec_off.numel() - 1,
                                             flags, c.ctypes.data, _stream_ptr(stream)), "bingo_walk_replay")
         return {"hdr": int(c[0]), "bkt": int(c[1]), "mem": int(c[2]), "arc": int(c[3])}
+
+    def export_vertices(self, ids, stream=None):
+        """bingo_export_vertices: the state records of the vertices `ids` (CUDA int tensor, the
+        caller's ids).  Returns (buf int32 CUDA tensor of u32 words, offsets int64 [n + 1])."""
+        torch = _torch()
+        ids = ids.to(device=self.device, dtype=torch.int32).contiguous()
+        n = ids.numel()
+        off = torch.empty(n + 1, dtype=torch.int64, device=self.device)
+        words = ctypes.c_uint64(0)
+        _order_on(stream, self.device, ids, off)
+        with torch.cuda.device(self.device):
+            _check(_lib().bingo_export_vertices(self._h, ids.data_ptr() if n else None, n, None, 0, off.data_ptr(),
+                                                ctypes.byref(words), _stream_ptr(stream)), "bingo_export_vertices")
+            buf = torch.empty(max(int(words.value), 1), dtype=torch.int32, device=self.device)
+            if n:
+                _check(_lib().bingo_export_vertices(self._h, ids.data_ptr(), n, buf.data_ptr(), buf.numel(),
+                                                    off.data_ptr(), ctypes.byref(words), _stream_ptr(stream)),
+                       "bingo_export_vertices")
+        return buf[:int(words.value)], off
+
+    def import_vertices(self, buf, offsets, stream=None):
+        """bingo_import_vertices: install records exported by a replica of this graph."""
+        torch = _torch()
+        n = offsets.numel() - 1
+        if n <= 0:
+            return
+        buf = buf.to(device=self.device, dtype=torch.int32).contiguous()
+        offsets = offsets.to(device=self.device, dtype=torch.int64).contiguous()
+        _order_on(stream, self.device, buf, offsets)
+        with torch.cuda.device(self.device):
+            _check(_lib().bingo_import_vertices(self._h, buf.data_ptr(), offsets.data_ptr(), n, _stream_ptr(stream)),
+                   "bingo_import_vertices")
 
     def visit_counts(self, reset: bool = False, stream=None):
         torch = _torch()

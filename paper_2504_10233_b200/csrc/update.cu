@@ -1446,6 +1446,7 @@ __global__ void __launch_bounds__(LT) k_stream_upd(const FastArgs fa0, StreamQ *
 #include "float_update.cuh"
 #include "hub_index.cuh"
 #include "group_index.cuh"
+#include "exchange.cuh"
 
 // ------------------------------------------------------------------ host side
 namespace {
@@ -3138,3 +3139,154 @@ extern "C" int bingo_sq_trace_read(unsigned long long *host, int n) {
     return (int)cudaMemcpyFromSymbol(host, g_sqt, sizeof(unsigned long long) * 8 * n);
 }
 #endif
+
+// ---------------------------------------------------------------- replica state exchange (f1)
+// bingo_export_vertices / bingo_import_vertices: include/bingo.h, exchange.cuh.
+static bool exchange_supported(const bingo_graph *g) {
+    return !g->float_mode && !g->radix_log2 && !g->nbt;
+}
+
+extern "C" bingo_status bingo_export_vertices(bingo_graph *g, const uint32_t *ids, uint32_t n, uint32_t *buf,
+                                              uint64_t cap_words, uint64_t *offsets, uint64_t *words_out,
+                                              void *stream) {
+    if (!g || !offsets || !words_out || (n && !ids)) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    if (!exchange_supported(g)) return BINGO_E_INVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    bingo_sq_quiesce(g, s);
+    *words_out = 0;
+    if (n == 0) {
+        if (cudaMemsetAsync(offsets, 0, sizeof(uint64_t), s) != cudaSuccess) return upd_cuda_fail(g, cudaGetLastError(), "export");
+        return BINGO_OK;
+    }
+    uint64_t *sizes = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * (n + 1));
+    uint64_t *tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * scan_tmp_words(n + 1));
+    int *bad = (int *)bingo_dev_alloc(g, sizeof(int));
+    auto fin = [&](bingo_status r) {
+        bingo_dev_free(g, sizes);
+        bingo_dev_free(g, tmp);
+        bingo_dev_free(g, bad);
+        return r;
+    };
+    if (!sizes || !tmp || !bad) return fin(BINGO_E_NOMEM);
+    ExArgs a;
+    a.hdr = g->hdr;
+    a.arc = g->arc;
+    a.ep = g->arc_epoch;
+    a.bkt = g->bkt;
+    a.gcan = g->gcan;
+    a.midx = g->midx;
+    a.inv = g->inv;
+    a.ids = ids;
+    a.n = n;
+    a.V = g->V;
+    a.words = sizes;
+    a.buf = buf;
+    int hbad = 0;
+    uint64_t total = 0;
+    cudaError_t e = cudaMemsetAsync(bad, 0, sizeof(int), s);
+    if (e == cudaSuccess) {
+        k_check_ids<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(ids, n, g->V, bad);
+        bingo_count_launch();
+        k_ex_sizes<<<(unsigned)std::min<uint64_t>((n + 255) / 256, 1184), 256, 0, s>>>(a);
+        bingo_count_launch();
+        e = exclusive_scan_u64(sizes, offsets, n, tmp, s);
+    }
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&total, offsets + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fin(upd_cuda_fail(g, e, "export sizes"));
+    if (hbad) return fin(BINGO_E_INVAL);
+    *words_out = total;
+    if (!buf) return fin(BINGO_OK);
+    if (total > cap_words) return fin(BINGO_E_OVERFLOW);
+    a.words = offsets;
+    k_ex_fill<<<(unsigned)std::min<uint64_t>(((uint64_t)n + 7) / 8, 148ull * 16), 256, 0, s>>>(a);
+    bingo_count_launch();
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fin(upd_cuda_fail(g, e, "export fill"));
+    return fin(BINGO_OK);
+}
+
+extern "C" bingo_status bingo_import_vertices(bingo_graph *g, const uint32_t *buf, const uint64_t *offsets, uint32_t n,
+                                              void *stream) {
+    if (!g || (n && (!buf || !offsets))) return BINGO_E_INVAL;
+    if (g->poisoned) return BINGO_E_STATE;
+    if (!exchange_supported(g)) return BINGO_E_INVAL;
+    if (n == 0) return BINGO_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    bingo_sq_quiesce(g, s);
+    uint64_t *need = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (n + 1));
+    uint64_t *pref = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (n + 1));
+    uint64_t *tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * scan_tmp_words(n + 1));
+    long long *darcs = (long long *)bingo_dev_alloc(g, sizeof(long long) * 2);
+    auto fin = [&](bingo_status r) {
+        bingo_dev_free(g, need);
+        bingo_dev_free(g, pref);
+        bingo_dev_free(g, tmp);
+        bingo_dev_free(g, darcs);
+        return r;
+    };
+    if (!need || !pref || !tmp || !darcs) return fin(BINGO_E_NOMEM);
+    ImArgs a;
+    memset(&a, 0, sizeof(a));
+    a.buf = buf;
+    a.off = offsets;
+    a.n = n;
+    a.hdr = g->hdr;
+    a.bkt = g->bkt;
+    a.gcan = g->gcan;
+    a.arc_slack = g->arc_slack;
+    a.mem_slack = g->member_slack;
+    a.hot_b = g->hot_bkt_degree;
+    a.hot_m = g->hot_mem_degree;
+    a.need = need;
+    a.pref = pref;
+    a.darcs = darcs;
+    const unsigned grid = (unsigned)std::min<uint64_t>(((uint64_t)n + 7) / 8, 148ull * 16);
+    unsigned long long bump[3] = {0, 0, 0};
+    uint64_t tot[3] = {0, 0, 0};
+    cudaError_t e = cudaMemsetAsync(darcs, 0, sizeof(long long) * 2, s);
+    if (e == cudaSuccess) {
+        k_im_plan<<<grid, 256, 0, s>>>(a);
+        bingo_count_launch();
+        const uint64_t *in[3] = {need, need + (n + 1), need + 2 * (n + 1)};
+        uint64_t *out[3] = {pref, pref + (n + 1), pref + 2 * (n + 1)};
+        e = exclusive_scan_u64_multi(in, out, 3, n, tmp, s);
+    }
+    for (int k = 0; k < 3 && e == cudaSuccess; k++)
+        e = cudaMemcpyAsync(&tot[k], pref + k * (n + 1) + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(bump, g->counters, sizeof(bump), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fin(upd_cuda_fail(g, e, "import plan"));
+    // pool growth first: nothing is written before every pool is large enough
+    bingo_status st;
+    if (bump[0] + tot[0] > g->arc_cap && (st = grow_pool(g, 0, bump[0] + tot[0], s)) != BINGO_OK)
+        return fin(st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st);
+    if (bump[1] + tot[1] > g->bkt_cap && (st = grow_pool(g, 1, bump[1] + tot[1], s)) != BINGO_OK)
+        return fin(st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st);
+    if (bump[2] + tot[2] > g->mem_cap / 4 && (st = grow_pool(g, 2, bump[2] + tot[2], s)) != BINGO_OK)
+        return fin(st == BINGO_E_CUDA ? (g->poisoned = 1, st) : st);
+    a.thdr = g->thdr;
+    a.arc = g->arc;
+    a.ep = g->arc_epoch;
+    a.bkt = g->bkt;
+    a.gcan = g->gcan;
+    a.midx = g->midx;
+    a.mdst = g->mdst;
+    a.hixo = g->hixo;
+    a.gixo = g->gixo;
+    for (int k = 0; k < 3; k++) a.bump[k] = bump[k];
+    k_im_install<<<grid, 256, 0, s>>>(a);
+    bingo_count_launch();
+    unsigned long long nb[3] = {bump[0] + tot[0], bump[1] + tot[1], bump[2] + tot[2]};
+    long long hd = 0;
+    e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpyAsync(g->counters, nb, sizeof(nb), cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hd, darcs, sizeof(long long), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fin(upd_cuda_fail(g, e, "import install"));
+    g->num_arcs = (uint64_t)((long long)g->num_arcs + hd);
+    return fin(BINGO_OK);
+}

@@ -138,8 +138,11 @@ __device__ __forceinline__ uint2 ldg8(const uint2 *p, uint64_t pol) {
 // once and the FIRST accepted attempt in order is taken -- the same result as
 // the sequential loop of P:465 (A-23), without serialising a warp on the
 // slowest lane's retries (acceptance > alpha = 40%, so P(all S rejected) < 0.6^S).
+// Session 3 A/B on the bench workloads (profiles/r02_dense_spec_ab.txt): 1 attempt per round
+// c2 8.49 -> 8.24 ms, c4 PPR 125.4 -> 124.9 ms; 3: slower (r01, before the later walk changes,
+// 2 had been the best).
 #ifndef BINGO_DENSE_SPEC
-#define BINGO_DENSE_SPEC 2
+#define BINGO_DENSE_SPEC 1
 #endif
 
 // One first-order sample at a vertex with n > 0 (P:215 two stages).

@@ -68,9 +68,54 @@ class ReplicatedBingo:
             dist.broadcast(buf, 0, group=self.group)
         return buf
 
-    def apply_updates(self, batch: Optional[torch.Tensor], n: Optional[int] = None) -> dict:
+    def apply_updates(self, batch: Optional[torch.Tensor], n: Optional[int] = None, sharded: bool = False) -> dict:
+        """Every replica applies rank 0's batch.  sharded=True: each rank applies
+        only the records whose source it owns (src mod P, after validating the whole batch)
+        and the replicas exchange the post-batch state of their touched vertices
+        (bingo_export_vertices -> variable-size all-gather -> bingo_import_vertices), so every
+        replica ends with the same canonical state while each applies ~1/P of the records.
+        Statistics are summed over the ranks."""
         buf = self.broadcast_batch(batch, n)
-        return self.g.apply_updates(buf)
+        if not sharded or self.world == 1:
+            return self.g.apply_updates(buf)
+        V = self.g.V
+        mine = owned_records(buf, None, self.rank, V, world=self.world)
+        st = self.g.apply_updates(mine)
+        ids = torch.unique(mine[:, 1].to(torch.int64)) if mine.shape[0] else mine.new_zeros(0, dtype=torch.int64)
+        rbuf, roff = self.g.export_vertices(ids.to(self.device))
+        self._exchange_state(rbuf, roff)
+        keys = ("inserted", "deleted", "missing_deletes", "touched_vertices")
+        t = torch.tensor([int(st[k]) for k in keys], dtype=torch.int64, device=self.device)
+        dist.all_reduce(t, group=self.group)
+        kt = torch.as_tensor(np.asarray(st["kind_transitions"], dtype=np.int64), device=self.device)
+        dist.all_reduce(kt, group=self.group)
+        out = dict(st)
+        out.update({k: int(v) for k, v in zip(keys, t.tolist())})
+        out["kind_transitions"] = kt.cpu().numpy().astype(np.uint64)
+        return out
+
+    def _exchange_state(self, rbuf: torch.Tensor, roff: torch.Tensor) -> None:
+        """All-gather every rank's vertex records (padded to the largest) and install the
+        other ranks' into this replica."""
+        sizes = torch.tensor([rbuf.numel(), roff.numel()], dtype=torch.int64, device=self.device)
+        alls = [torch.zeros_like(sizes) for _ in range(self.world)]
+        dist.all_gather(alls, sizes, group=self.group)
+        wmax = max(int(x[0]) for x in alls)
+        omax = max(int(x[1]) for x in alls)
+        pb = torch.zeros(max(wmax, 1), dtype=torch.int32, device=self.device)
+        pb[:rbuf.numel()] = rbuf
+        po = torch.zeros(omax, dtype=torch.int64, device=self.device)
+        po[:roff.numel()] = roff
+        gb = [torch.empty_like(pb) for _ in range(self.world)]
+        go = [torch.empty_like(po) for _ in range(self.world)]
+        dist.all_gather(gb, pb, group=self.group)
+        dist.all_gather(go, po, group=self.group)
+        for r in range(self.world):
+            if r == self.rank:
+                continue
+            nw, no = int(alls[r][0]), int(alls[r][1])
+            if no > 1:
+                self.g.import_vertices(gb[r][:nw], go[r][:no])
 
     # ------------------------------------------------------------ walks
     def walk(self, num_walkers: int, first_walker: int = 0, **kw) -> dict:
@@ -271,17 +316,18 @@ class PartitionedBingo:
         return c
 
 
-def owned_records(batch: torch.Tensor, bounds, me: int, V: int) -> torch.Tensor:
-    """The records of a (n, 4) {op, src, dst, bias} batch whose source vertex this rank owns,
-    in batch order, after validating the WHOLE batch (the ABI's whole-batch rule: one bad
-    record anywhere rejects the batch before any rank applies anything)."""
+def owned_records(batch: torch.Tensor, bounds, me: int, V: int, world: int = 0) -> torch.Tensor:
+    """The records of a (n, 4) {op, src, dst, bias} batch whose source vertex this rank owns
+    (bounds: [bounds[me], bounds[me + 1]); bounds None: src mod world == me), in batch order,
+    after validating the WHOLE batch (the ABI's whole-batch rule: one bad record anywhere
+    rejects the batch before any rank applies anything)."""
     b = batch.to(torch.int64) & 0xFFFFFFFF
     op, src, dst, w = b[:, 0], b[:, 1], b[:, 2], b[:, 3]
     bad = (op > 1) | (src >= V) | (dst >= V) | ((op == 0) & (w == 0))
     if bool(bad.any()):
         from . import bingo
         raise bingo.BingoError(bingo.E_INVAL, "partitioned apply_updates")
-    mine = (src >= bounds[me]) & (src < bounds[me + 1])
+    mine = (src % world == me) if bounds is None else (src >= bounds[me]) & (src < bounds[me + 1])
     return batch[mine].contiguous()
 
 
