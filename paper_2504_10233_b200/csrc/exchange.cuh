@@ -103,6 +103,7 @@ struct ImArgs {
     GCan *gcan;
     uint32_t *midx, *mdst;
     uint64_t *hixo, *gixo;
+    uint32_t V;
     double arc_slack, mem_slack;
     uint32_t hot_b, hot_m;
     uint64_t *need;           // [3][n + 1]: fresh arcs, buckets, member units (then scanned)
@@ -154,6 +155,28 @@ __global__ void __launch_bounds__(256) k_im_plan(const ImArgs a) {
     const uint32_t lane = lane_id();
     for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < a.n; i += (gridDim.x * blockDim.x) >> 5) {
         const uint32_t *r = a.buf + a.off[i];
+        const uint64_t len = a.off[i + 1] - a.off[i];
+        // a record must parse: vertex < V, at most 32 groups, every group inside the record,
+        // kinds / digits / member indices in range (EINVAL before anything is written)
+        bool ok = len >= 5 && r[0] < a.V && r[2] <= 32 && 5 + 3ull * r[1] <= len;
+        if (ok) {
+            uint64_t pos = 5 + 3ull * r[1];
+            for (uint32_t b = 0; ok && b < r[2]; b++) {
+                ok = pos + 6 <= len && r[pos] < 32 && r[pos + 1] <= K_REGULAR;
+                if (!ok) break;
+                const uint32_t kb = r[pos + 1], cb = r[pos + 2];
+                const uint64_t pl = is_list(kb) ? cb : (kb == K_ONE ? 1u : 0u);
+                ok = pos + 6 + pl <= len;
+                for (uint64_t j = lane; ok && j < pl; j += 32)
+                    if (r[pos + 6 + j] >= r[1]) atomicOr(a.bad, 1);
+                pos += 6 + pl;
+            }
+            ok = ok && pos == len;
+        }
+        if (!ok) {
+            if (lane == 0) atomicOr(a.bad, 1);
+            continue;
+        }
         const uint32_t u = r[0], d = r[1], n = r[2];
         const VHdr h = a.hdr[u];
         uint32_t k, kind, c, alias;

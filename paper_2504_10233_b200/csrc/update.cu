@@ -3220,7 +3220,7 @@ extern "C" bingo_status bingo_import_vertices(bingo_graph *g, const uint32_t *bu
     uint64_t *need = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (n + 1));
     uint64_t *pref = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * (n + 1));
     uint64_t *tmp = (uint64_t *)bingo_dev_alloc(g, sizeof(uint64_t) * 3 * scan_tmp_words(n + 1));
-    long long *darcs = (long long *)bingo_dev_alloc(g, sizeof(long long) * 2);
+    long long *darcs = (long long *)bingo_dev_alloc(g, sizeof(long long) * 2);   // [0] arcs delta, [1] bad flag
     auto fin = [&](bingo_status r) {
         bingo_dev_free(g, need);
         bingo_dev_free(g, pref);
@@ -3244,6 +3244,8 @@ extern "C" bingo_status bingo_import_vertices(bingo_graph *g, const uint32_t *bu
     a.need = need;
     a.pref = pref;
     a.darcs = darcs;
+    a.bad = reinterpret_cast<int *>(darcs + 1);
+    a.V = g->V;
     const unsigned grid = (unsigned)std::min<uint64_t>(((uint64_t)n + 7) / 8, 148ull * 16);
     unsigned long long bump[3] = {0, 0, 0};
     uint64_t tot[3] = {0, 0, 0};
@@ -3258,8 +3260,11 @@ extern "C" bingo_status bingo_import_vertices(bingo_graph *g, const uint32_t *bu
     for (int k = 0; k < 3 && e == cudaSuccess; k++)
         e = cudaMemcpyAsync(&tot[k], pref + k * (n + 1) + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaMemcpyAsync(bump, g->counters, sizeof(bump), cudaMemcpyDeviceToHost, s);
+    int hbad = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, a.bad, sizeof(int), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return fin(upd_cuda_fail(g, e, "import plan"));
+    if (hbad) return fin(BINGO_E_INVAL);
     // pool growth first: nothing is written before every pool is large enough
     bingo_status st;
     if (bump[0] + tot[0] > g->arc_cap && (st = grow_pool(g, 0, bump[0] + tot[0], s)) != BINGO_OK)

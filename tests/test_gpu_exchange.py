@@ -92,6 +92,19 @@ def test_export_import_errors():
     before = g.export()
     g.import_vertices(*g.export_vertices(torch.arange(w.V, dtype=torch.int32).cuda()))   # a no-op round trip
     assert g.export() == before
+    # records that do not parse are rejected before anything is written
+    buf, off = g.export_vertices(torch.arange(4, dtype=torch.int32).cuda())
+    for bad in ("vertex", "length", "member"):
+        b2 = buf.clone()
+        if bad == "vertex":
+            b2[0] = w.V
+        elif bad == "length":
+            b2[1] += 1
+        else:   # a list member index beyond the adjacency, or (no list groups) the group count
+            b2[2] = 33
+        with pytest.raises(pb.bingo.BingoError):
+            g.import_vertices(b2, off)
+        assert g.export() == before
     gn = pb.Graph(w.row_offsets, w.dst, w.bias, neighbor_index=True)
     with pytest.raises(pb.bingo.BingoError):
         gn.export_vertices(torch.tensor([0], dtype=torch.int32).cuda())
