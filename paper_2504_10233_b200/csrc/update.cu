@@ -3039,7 +3039,7 @@ extern "C" bingo_status bingo_stream_update(bingo_graph *g, const bingo_update *
                                             void *stream) {
     if (!g || !rec) return BINGO_E_INVAL;
     if (g->poisoned) return BINGO_E_STATE;
-    if (g->float_mode || g->radix_log2) return BINGO_E_INVAL;   // float graphs take real biases; radix graphs are static
+    if (g->float_mode || g->radix_log2) return BINGO_E_INVAL;   // float graphs take real biases; radix graphs update through bingo_apply_updates (R-19)
     cudaStream_t s = (cudaStream_t)stream;
     if (stats) memset(stats, 0, sizeof(*stats));
     if (g->sq_running && g->sq_stream != s) bingo_sq_quiesce(g, s);
