@@ -767,7 +767,9 @@ def main():
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": config_block(args.config, head["V"], head["A"], head["nrec"], ws,
                                    {"parallelism": f"replicated graph x{ws}, walker ids split {ws} ways, batch "
-                                                   f"broadcast + visit-count all-reduce (NCCL)",
+                                                   f"broadcast + visit-count all-reduce"
+                                                   f" ({'NCCL' if args.backend == 'nccl' else args.backend})"
+                                                   + (", every rank on one device (test)" if args.share_device else ""),
                                     "setup": head["setup"]}),
             "walk_steps_per_s": head["steps_total"] / K / (head["walk_ms"] / 1e3),
             "update_edges_per_s": head["nrec"] / (head["update_ms"] / 1e3),
