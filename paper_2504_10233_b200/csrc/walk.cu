@@ -34,6 +34,13 @@ __device__ __forceinline__ void visit_add(unsigned long long *p, unsigned long l
 #endif
 }
 
+#ifdef BINGO_VISIT32
+__device__ __forceinline__ void visit_add32(unsigned int *p, unsigned int v, const Policies &pol) {
+    asm volatile("red.relaxed.gpu.global.add.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol.keep)
+                 : "memory");
+}
+#endif
+
 template <int APP, bool PROF, bool WMAJOR>
 __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint32_t &w, uint32_t &u,
                                              const Policies &pol) {
@@ -45,7 +52,7 @@ __device__ __forceinline__ void walker_start(const WalkArgs &a, uint64_t i, uint
         else __stcs(&a.paths[i], u0);
     }
 #ifdef BINGO_VISIT32
-    if (APP == BINGO_PPR && a.visit32) atomicAdd(&a.visit32[visit_slot(u)], 1u);
+    if (APP == BINGO_PPR && a.visit32) visit_add32(&a.visit32[visit_slot(u)], 1u, pol);
     else
 #endif
     if (APP == BINGO_PPR && a.visit) visit_add(a.visit + visit_slot(u), 1ull, pol);
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(BINGO_WALK_TPB, MODE ? 4 : (APP == BINGO_NODE2
                                 const unsigned same = __match_any_sync(act, u);
                                 if ((__ffs(same) - 1) == (int)(threadIdx.x & 31u)) {
 #ifdef BINGO_VISIT32
-                                    if (a.visit32) atomicAdd(&a.visit32[visit_slot(u)], (unsigned)__popc(same));
+                                    if (a.visit32) visit_add32(&a.visit32[visit_slot(u)], (unsigned)__popc(same), pol);
                                     else
 #endif
                                     {
