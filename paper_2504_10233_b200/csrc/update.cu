@@ -1121,7 +1121,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
     __shared__ unsigned long long scr_off[FAST_N + 1];
     __shared__ MutSmem sm[32];
     __shared__ unsigned long long need_arc, need_bkt, need_mem;
-    __shared__ uint32_t flag, ntouch, go, blockwide;
+    __shared__ uint32_t flag, ntouch, go, blockwide, lite;
     __shared__ uint32_t s_vst[VST];   // one touched vertex: its statistics stay in shared memory
     const uint32_t tid = threadIdx.x, lane = tid & 31u, w = tid >> 5;
     // the pool bump pointers, read now so their latency hides behind the validation and plan
@@ -1192,8 +1192,56 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
     }
     __syncthreads();
     const uint32_t nt = ntouch;
-    // plan, one warp per touched vertex
     const uint32_t nw = blockDim.x >> 5;   // launched with 32 * clamp(n, 2, 32) threads
+#ifndef BINGO_SQ_NO_LITE
+    // Streamed single record (the persistent queue's 1024-thread block): a conservative plan
+    // from the header alone.  Every demand is bounded from above -- groups after the record
+    // <= n + popc(w), each list <= L members -- so if the bounded demand fits the pools the
+    // exact one does, and if the bounded overflow test passes the exact one (R-10) does; the
+    // vertex's buckets are prefetched into L1 for the mutation.  Anything the bounds cannot
+    // decide takes the exact plan below.  Saves the plan's group loads and reductions and a
+    // block barrier on the dependent path (BINGO_SQ_NO_LITE: A/B).
+    bool use_lite = false;   // block-uniform: decided from n, nt and (after a barrier) `lite`
+    if (block_mode && n == 1 && nt == 1) {
+        if (w == 0) {
+            const VHdr h = fa.m.hdr[tv[0]];
+            if (lane < h.n) {
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(fa.m.bkt + h.bkt_off + lane));
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(fa.m.gcan + h.bkt_off + lane));
+            }
+            if (lane == 0) {
+                const uint4 r = recs[0];
+                const uint32_t m = r.x == 0u ? 1u : 0u, q = r.x == 1u ? 1u : 0u, wb = m ? r.w : 0u;
+                const uint32_t L = h.d + m, nbmax = h.n + __popc(wb);
+                const uint64_t Tn = h.T + wb;
+                bool ok = Tn >= h.T && __umul64hi(Tn, (uint64_t)nbmax) == 0 && (uint64_t)h.d + m < 0xFFFFFFFFull;
+                uint32_t f = flag;
+                if (L > FAST_MAXL) f |= FAST_SLOW;
+                const uint64_t need_a = L > h.adj_cap ? arc_capacity(L, fa.m.arc_slack) : 0ull;
+                const uint64_t need_b = nbmax > h.ncap ? bucket_capacity(nbmax) : 0ull;
+                const uint64_t need_m = (uint64_t)nbmax * member_units(L, fa.m.mem_slack);
+                uint64_t words = 0;
+                if (q) words = ((uint64_t)(L + 31) / 32 + 8ull * next_pow2(2) + 3ull + 8ull + 7ull) & ~7ull;
+                ok = ok && bump0 + need_a <= fa.arc_cap && bump1 + need_b <= fa.bkt_cap &&
+                     bump2 + need_m <= fa.mem_units_cap && words <= fa.scr_cap;
+                if (ok || (f & FAST_SLOW)) {
+                    scr_off[0] = 0;
+                    scr_off[1] = words;
+                    blockwide = L > FAST_BLOCK_L ? 1u : 0u;
+                    flag = f;
+                    go = f == 0 ? 1u : 0u;
+                    lite = 1;
+                } else {
+                    lite = 0;
+                }
+            }
+        }
+        __syncthreads();
+        use_lite = lite != 0;
+    }
+    if (!use_lite) {
+#endif
+    // plan, one warp per touched vertex
     for (uint32_t t = w; t < nt; t += nw) {
         const VHdr h = fa.m.hdr[tv[t]];
         const PlanOut o = plan_vertex(recs, sval, seg[t], seg[t + 1], h, fa.m.bkt, fa.m.gcan, fa.m.alpha, fa.m.bs,
@@ -1228,6 +1276,9 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
         go = f == 0 ? 1u : 0u;
     }
     __syncthreads();
+#ifndef BINGO_SQ_NO_LITE
+    }
+#endif
     SQ_MARK(2);
     if (go) {
         MutateArgs a = fa.m;
