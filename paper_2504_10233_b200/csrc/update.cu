@@ -1194,15 +1194,15 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
     const uint32_t nt = ntouch;
     const uint32_t nw = blockDim.x >> 5;   // launched with 32 * clamp(n, 2, 32) threads
 #ifndef BINGO_SQ_NO_LITE
-    // Streamed single record (the persistent queue's 1024-thread block): a conservative plan
-    // from the header alone.  Every demand is bounded from above -- groups after the record
+    // A single record (the persistent queue's 1024-thread block, or a one-record launch): a
+    // conservative plan from the header alone.  Every demand is bounded from above -- groups after the record
     // <= n + popc(w), each list <= L members -- so if the bounded demand fits the pools the
     // exact one does, and if the bounded overflow test passes the exact one (R-10) does; the
     // vertex's buckets are prefetched into L1 for the mutation.  Anything the bounds cannot
     // decide takes the exact plan below.  Saves the plan's group loads and reductions and a
     // block barrier on the dependent path (BINGO_SQ_NO_LITE: A/B).
     bool use_lite = false;   // block-uniform: decided from n, nt and (after a barrier) `lite`
-    if (block_mode && n == 1 && nt == 1) {
+    if (n == 1 && nt == 1) {
         if (w == 0) {
             const VHdr h = fa.m.hdr[tv[0]];
             if (lane < h.n) {
@@ -1216,7 +1216,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
                 const uint64_t Tn = h.T + wb;
                 bool ok = Tn >= h.T && __umul64hi(Tn, (uint64_t)nbmax) == 0 && (uint64_t)h.d + m < 0xFFFFFFFFull;
                 uint32_t f = flag;
-                if (L > FAST_MAXL) f |= FAST_SLOW;
+                if (L > (block_mode ? FAST_MAXL : FAST_HANDOFF_L)) f |= FAST_SLOW;
                 const uint64_t need_a = L > h.adj_cap ? arc_capacity(L, fa.m.arc_slack) : 0ull;
                 const uint64_t need_b = nbmax > h.ncap ? bucket_capacity(nbmax) : 0ull;
                 const uint64_t need_m = (uint64_t)nbmax * member_units(L, fa.m.mem_slack);
@@ -1227,7 +1227,7 @@ __device__ __forceinline__ uint32_t upd_fast_body(const FastArgs &fa, const uint
                 if (ok || (f & FAST_SLOW)) {
                     scr_off[0] = 0;
                     scr_off[1] = words;
-                    blockwide = L > FAST_BLOCK_L ? 1u : 0u;
+                    blockwide = block_mode && L > FAST_BLOCK_L ? 1u : 0u;
                     flag = f;
                     go = f == 0 ? 1u : 0u;
                     lite = 1;
