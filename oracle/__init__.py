@@ -180,7 +180,7 @@ class OracleGraph:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and lib is not None:   # module globals are gone at interpreter exit
             lib().ora_free(h)
             self._h = None
 
@@ -319,7 +319,7 @@ class RadixGraph:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value:
+        if h is not None and h.value and lib is not None:
             lib().ora_radix_free(h)
             self._h = None
 
