@@ -2325,10 +2325,12 @@ static bingo_status apply_bsp_async(bingo_graph *g, const uint4 *recs, const uin
     caps.sel = g->isc_sel;
     caps.grp = g->isc_grp;
     // IG: item kernels, one wave of contiguous per-warp ranges; HG: the hub chain's per-hub kernels
-    // (IG 16 per SM on graphs >= 2^28 arcs, whose hub scans fill more items: c4 1.222 -> 1.177 ms;
-    // c2 is 2% faster at 8; profiles/r02_update_wg_ab.txt)
-    const unsigned WG = bsp_wg(), HG = bsp_env_grid("BINGO_BSP_HG", 4),
-                   IG = bsp_env_grid("BINGO_BSP_IG", g->num_arcs >= (1ull << 28) ? 16u : 8u);
+    // (IG 16 and HG 16 per SM on graphs >= 2^28 arcs, whose hub scans fill more items and whose
+    // hub chain is the critical path: c4 1.222 -> 1.177 ms (IG), 1.122 -> 1.09 ms (HG); c2 is 1-2%
+    // faster at 8 / 4; profiles/r02_update_wg_ab.txt)
+    const bool big_graph = g->num_arcs >= (1ull << 28);
+    const unsigned WG = bsp_wg(), HG = bsp_env_grid("BINGO_BSP_HG", big_graph ? 16u : 4u),
+                   IG = bsp_env_grid("BINGO_BSP_IG", big_graph ? 16u : 8u);
     const unsigned wg = warp_grid(ntmax, WG), hg = warp_grid(ntmax, HG);
     UCK(cudaMemsetAsync(a.nhubs, 0, 32, s));
     UCK(cudaMemsetAsync(a.vhix, 0, 4 * (size_t)ntmax, s));
